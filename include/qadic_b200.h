@@ -1,0 +1,159 @@
+/* qadic_b200.h -- C ABI of the B200-native qadic hot path (libqadic_b200.so).
+ *
+ * Drop-in boundary for the reference package `qadic` (arXiv 0809.0063).
+ * Every pointer argument is a DEVICE pointer (cudaMalloc / torch CUDA
+ * storage) unless stated otherwise; `stream` is a cudaStream_t passed as
+ * void* (NULL = legacy default stream).  Calls are asynchronous on `stream`
+ * and return a qadic_status; a non-zero status leaves a message retrievable
+ * with qadic_last_error().  No torch types cross this boundary.
+ *
+ * Citations are into /root/reference/pkg/src/qadic/ (file:line of the
+ * reference interface each entry point replaces).
+ */
+#ifndef QADIC_B200_H
+#define QADIC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QADIC_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define QADIC_API __attribute__((visibility("default")))
+#else
+#define QADIC_API
+#endif
+
+typedef enum qadic_status {
+    QADIC_OK = 0,
+    QADIC_ERR_SHAPE = 1,       /* ValueError("incompatible shapes") _speed.pyx:61-62 / DimensionMismatch errors.py */
+    QADIC_ERR_PARAMS = 2,      /* ParamsViolation: a digit or word bound would overflow (params.py:99-141) */
+    QADIC_ERR_VALUE = 3,       /* ValueError: argument outside its domain (e.g. d*t >= 64, _speed.pyx:135-136) */
+    QADIC_ERR_CUDA = 4,        /* CUDA runtime / launch failure */
+    QADIC_ERR_UNSUPPORTED = 5  /* shape or field outside what this build supports */
+} qadic_status;
+
+typedef enum qadic_engine {
+    QADIC_ENGINE_AUTO = 0,     /* the measured-faster exact engine (tcgen05 INT8 planes) */
+    QADIC_ENGINE_I8_TC = 1,    /* tcgen05.mma kind::i8 on coefficient planes, int32 TMEM accumulators */
+    QADIC_ENGINE_F64_DMMA = 2  /* the paper's formulation: DQT-packed FP64 words on DMMA tensor cores */
+} qadic_engine;
+
+QADIC_API int qadic_abi_version(void);
+QADIC_API const char *qadic_last_error(void);
+/* number of kernels this library launched since load (instrumentation) */
+QADIC_API int64_t qadic_launch_count(void);
+
+/* ---------------------------------------------------------------------------
+ * Layer K: the operator/plugin kernels (_kernels/__init__.py:52-69).
+ * Semantics identical to _kernels/_speed.pyx (uint64 wraps mod 2^64).
+ * ------------------------------------------------------------------------- */
+
+/* C[m,n] = A[m,k] @ B[k,n] over uint64 mod 2^64.  _speed.pyx:15-30, 58-66 */
+QADIC_API int qadic_matmul_exact_u64(const uint64_t *a, const uint64_t *b, uint64_t *c,
+                           int64_t m, int64_t k, int64_t n, void *stream);
+
+/* C = A @ B mod p, reducing every `chunk` inner steps (floor-mod, int64).
+ * _speed.pyx:33-55, 69-82 ; pure.py:20-28 */
+QADIC_API int qadic_matmul_mod_i64(const int64_t *a, const int64_t *b, int64_t *c,
+                         int64_t m, int64_t k, int64_t n, int64_t p, int64_t chunk,
+                         void *stream);
+
+/* out[na+nb-1] = full convolution.  _speed.pyx:85-92,105-110 / 95-102,113-118 */
+QADIC_API int qadic_conv_exact_u64(const uint64_t *a, int64_t na, const uint64_t *b, int64_t nb,
+                         uint64_t *out, void *stream);
+QADIC_API int qadic_conv_exact_i64(const int64_t *a, int64_t na, const int64_t *b, int64_t nb,
+                         int64_t *out, void *stream);
+
+/* out[n, d+1]: u_i = (r >> it) - p*((r//p) >> it).  _speed.pyx:121-140.
+ * The division is an FP64 reciprocal multiply (fdiv.py:338-363) for r < 2^53,
+ * integer division above. */
+QADIC_API int qadic_redq_compress_u64(const uint64_t *r, int64_t n, int64_t p, int32_t t, int32_t d,
+                            uint64_t *out, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * REDQ bulk reduction (redq.py:318-343): compress + correct, then either
+ * repack (packed_out[n]) or emit digits (digits_out[n, d+1], uint64).
+ * Either output may be NULL.
+ * ------------------------------------------------------------------------- */
+QADIC_API int qadic_reduce_words(const uint64_t *words, int64_t n, int64_t p, int32_t t, int32_t d,
+                       uint64_t *packed_out, uint64_t *digits_out, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * DQT pack / unpack (dqt.py:39-92, cmm.py:72-85,130-145, polymul.py:126-151).
+ * ------------------------------------------------------------------------- */
+
+/* words[rows, ceil(cols/k)] = row-packed (FORWARD, reverse=0) or digit-reversed
+ * (REVERSED, reverse=1) groups of k consecutive uint8 entries, zero-padded. */
+QADIC_API int qadic_pack_rows_u8(const uint8_t *m, int64_t rows, int64_t cols, int32_t k, int32_t t,
+                       int32_t reverse, uint64_t *words, void *stream);
+/* inverse of qadic_pack_rows_u8 for reduced digits: out[rows, cols] uint8 */
+QADIC_API int qadic_unpack_rows_u8(const uint64_t *words, int64_t rows, int64_t cols, int32_t k,
+                         int32_t t, int32_t reverse, uint8_t *out, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * GF(p^k) field description shared by the GF entry points.
+ * Built on the host from GFqField (gfext.py:103-213): L/H correction tables
+ * (gfext.py:176-213) are re-expressed with coefficient bytes instead of
+ * discrete-log handles (entry = sum coeff_l << 8l), and the fold rows
+ * xpow[i] = X^i mod f (gfext.py:200-205) drive the INT8 plane expansion.
+ * ------------------------------------------------------------------------- */
+typedef struct qadic_field_desc {
+    int32_t p;                /* prime, 2 <= p <= 127 on the GPU path */
+    int32_t k;                /* extension degree, 1 <= k <= 4 */
+    int32_t t;                /* radix exponent, q = 2^t */
+    int32_t u_bits;           /* ceil(log2 p): L/H index bits per digit (gfext.py:178) */
+    uint8_t xpow[7][4];       /* X^i mod f coefficients, i = 0..2k-2 */
+    const uint32_t *l_table;  /* device, 2^(u_bits*k) entries */
+    const uint32_t *h_table;  /* device, 2^(u_bits*k) entries */
+} qadic_field_desc;
+
+/* cfg2 -- out[batch, k] = sum_j v1[b,j]*v2[b,j] over GF(p^k), coefficient I/O
+ * (uint8 [batch, len, k]).  GFqField.fgdp, gfext.py:268-297, batched. */
+QADIC_API int qadic_gf_dot_batch_u8(const qadic_field_desc *f, const uint8_t *v1, const uint8_t *v2,
+                          int64_t batch, int64_t len, uint8_t *out, void *stream);
+
+/* cfg3 / cfg5 -- C[m,n,k] = A[m,kdim,k] @ B[kdim,n,k] over GF(p^k), coefficient
+ * I/O.  GFqField.matmul, gfext.py:311-345.  fold_period (F64 engine only) is the
+ * number of inner terms accumulated between in-register REDQ folds (0 = none,
+ * requires kdim <= the field's dot bound); the INT8 engine needs no folds while
+ * kdim*k*(p-1)^2 < 2^31.  `workspace` must hold qadic_gf_matmul_workspace()
+ * bytes (device). */
+QADIC_API size_t qadic_gf_matmul_workspace(const qadic_field_desc *f, int64_t m, int64_t kdim, int64_t n,
+                                 int32_t engine);
+QADIC_API int qadic_gf_matmul_u8(const qadic_field_desc *f, const uint8_t *a, const uint8_t *b,
+                       int64_t m, int64_t kdim, int64_t n, int32_t engine, int32_t fold_period,
+                       void *workspace, size_t workspace_bytes, uint8_t *c, void *stream);
+
+/* cfg4 -- C[m,n] = A[m,kdim] @ B[kdim,n] mod p with B row-compressed d+1
+ * entries per word at radix 2^t (cmm.right_cmm(a, compress_rows(b)),
+ * cmm.py:244-276, 97-110).  uint8 I/O. */
+QADIC_API size_t qadic_right_cmm_workspace(int64_t m, int64_t kdim, int64_t n, int32_t d, int32_t engine);
+QADIC_API int qadic_right_cmm_u8(const uint8_t *a, const uint8_t *b, int64_t m, int64_t kdim, int64_t n,
+                       int64_t p, int32_t t, int32_t d, int32_t engine, void *workspace,
+                       size_t workspace_bytes, uint8_t *c, void *stream);
+
+/* cfg1 -- out[n, 2k-1] = a[n,k] * b[n,k] over F_p for n independent pairs:
+ * one packed FP64 product + REDQ per pair.  polymul.polymul_fqt,
+ * polymul.py:274-313 (one word per operand), batched. */
+QADIC_API int qadic_polymul_batch_u8(const uint8_t *a, const uint8_t *b, int64_t n, int32_t k, int64_t p,
+                           int32_t t, uint8_t *out, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Handle conversion for the discrete-log API (gfext.py:43-46, 136-146):
+ *   out[i*width + j] = table[idx[i]*width + j]        (index -> coefficients)
+ *   out[i] = index_of_code[sum_l c[i,l] p^l]           (coefficients -> index)
+ * ------------------------------------------------------------------------- */
+QADIC_API int qadic_gather_u8(const int64_t *idx, int64_t n, const uint8_t *table, int64_t table_rows,
+                    int32_t width, uint8_t *out, void *stream);
+QADIC_API int qadic_index_of_coeffs(const uint8_t *c, int64_t n, int32_t k, int32_t p,
+                          const int64_t *index_of_code, int64_t *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QADIC_B200_H */

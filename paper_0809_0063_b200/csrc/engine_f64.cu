@@ -1,0 +1,342 @@
+// Engine F64: the paper's own formulation on B200 FP64 tensor cores.
+//
+// DQT-packed words (GFqField._build_pack_table,
+// src/gfext.py:158-174; cmm._pack_axis, src/cmm.py:72-85) are exact
+// integers below 2^53, so FP64 matrix products of them are exact
+// (PAPER.md:216-223).  tcgen05 has no f64 kind, so the product runs on
+// warp-level DMMA (mma.sync.m8n8k4.f64 -> SASS DMMA.8x8x4) with a 3-stage
+// cp.async pipeline, and the whole inverse DQT is fused into the epilogue:
+//
+//   REDQ compression with the FP64 reciprocal (qadic_common.cuh), then
+//   * GF(p^k):  L/H correction+fold tables staged in shared memory
+//               (src/gfext.py:176-213, 336-344) -> k coefficient bytes
+//   * right_cmm: corrected digits (src/redq.py:308-315) -> d+1 entries
+//
+// When the inner dimension exceeds the a-priori bound (cfg5: fold budget 9,
+// src/polymul.py:159-167), every `fold` inner terms the accumulators are
+// digit-reduced in registers (compress + correct + repack,
+// src/redq.py:318-332) -- the delayed-reduction fold of
+// src/polymul.py:198-208 without leaving the register file.
+#include "qadic_common.cuh"
+#include "qadic_internal.h"
+
+namespace qadic {
+
+int make_field_const(const qadic_field_desc* d, FieldConst* f);
+
+namespace f64 {
+
+constexpr int BM = 128, BN = 128, BK = 16;
+constexpr int SA = BK + 4;   // A smem row pitch (doubles): conflict-free fragment loads
+constexpr int SB = BN + 4;   // B smem row pitch (doubles)
+constexpr int STAGES = 3;
+constexpr int THREADS = 512;  // 16 warps, 4 (M) x 4 (N), 32x32 per warp
+constexpr int TABLE_MAX = 4096;
+constexpr size_t PIPE_BYTES = (size_t)STAGES * (BM * SA + BK * SB) * sizeof(double);
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+                 "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N));
+}
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+enum Epi { EPI_GF = 0, EPI_CMM = 1 };
+
+struct Params {
+    const double* a;  // [Mp, Kp] packed words
+    const double* b;  // [Kp, Np]
+    int64_t M, Nw, Kp, Np;   // logical rows, logical word columns, padded dims
+    int64_t n_out;           // output entries per row (GF: N; CMM: N)
+    int fold;                // 0 = none; else multiple of 4
+    int d;                   // CMM: digits per word - 1
+    uint8_t* c;
+};
+
+// digit-reduce one accumulator in registers and repack (reduce_words_array)
+template <int ND>
+__device__ __forceinline__ double fold_word(double r, const FieldConst& f) {
+    uint32_t u[ND + 1];
+    redq_compress_f64<ND>(r, f.invp_up, (double)f.p, f.bound, f.p, (int)f.t, u);
+    uint64_t w = u[ND];
+#pragma unroll
+    for (int i = ND - 1; i >= 0; --i) w = (w << f.t) | mod_small(u[i] + f.corr * u[i + 1], f.p, f.magic);
+    return (double)w;
+}
+
+template <int K, Epi EPI, bool SMEM_TABLES>
+__global__ void __launch_bounds__(THREADS, 1) dmma_gemm_kernel(Params prm, FieldConst f) {
+    constexpr int ND = EPI == EPI_GF ? 2 * K - 2 : 0;
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    double* sA = reinterpret_cast<double*>(smem_raw);
+    double* sB = sA + STAGES * BM * SA;
+    uint32_t* s_l = reinterpret_cast<uint32_t*>(sB + STAGES * BK * SB);
+    uint32_t* s_h = s_l + TABLE_MAX;
+
+    const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+    const int wm = warp / 4, wn = warp % 4;
+    const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+
+    if (EPI == EPI_GF && SMEM_TABLES) {
+        const int size = 1 << (f.bb * K);
+        for (int i = tid; i < size; i += THREADS) {
+            s_l[i] = f.l_table[i];
+            s_h[i] = f.h_table[i];
+        }
+    }
+
+    auto load_stage = [&](int slot, int64_t k0) {
+        double* a_s = sA + slot * BM * SA;
+        double* b_s = sB + slot * BK * SB;
+        // A: 128 rows x 16 doubles = 1024 16-byte chunks; B: 16 rows x 128 doubles
+#pragma unroll
+        for (int it = 0; it < 2; ++it) {
+            const int c = tid + it * THREADS;
+            const int r = c / (BK / 2), q = c % (BK / 2);
+            cp_async16(a_s + r * SA + 2 * q, prm.a + (m0 + r) * prm.Kp + k0 + 2 * q);
+            const int rb = c / (BN / 2), qb = c % (BN / 2);
+            cp_async16(b_s + rb * SB + 2 * qb, prm.b + (k0 + rb) * prm.Np + n0 + 2 * qb);
+        }
+    };
+
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    const int nk = (int)(prm.Kp / BK);
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < nk) load_stage(s, (int64_t)s * BK);
+        cp_async_commit();
+    }
+    const int ar = lane >> 2, ac = lane & 3;
+    for (int kt = 0; kt < nk; ++kt) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        if (kt + STAGES - 1 < nk) load_stage((kt + STAGES - 1) % STAGES, (int64_t)(kt + STAGES - 1) * BK);
+        cp_async_commit();
+        const double* a_s = sA + (kt % STAGES) * BM * SA + (wm * 32 + ar) * SA + ac;
+        const double* b_s = sB + (kt % STAGES) * BK * SB + ac * SB + wn * 32 + ar;
+#pragma unroll
+        for (int k4 = 0; k4 < BK / 4; ++k4) {
+            double af[4], bf[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) af[i] = a_s[i * 8 * SA + k4 * 4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bf[j] = b_s[k4 * 4 * SB + j * 8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+            if (EPI == EPI_GF && prm.fold) {
+                const int64_t kdone = (int64_t)kt * BK + (k4 + 1) * 4;
+                if (kdone % prm.fold == 0 && kdone < prm.Kp) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            acc[i][j][0] = fold_word<ND>(acc[i][j][0], f);
+                            acc[i][j][1] = fold_word<ND>(acc[i][j][1], f);
+                        }
+                }
+            }
+        }
+    }
+    cp_async_wait<0>();
+    __syncthreads();  // tables visible (loaded before the main loop)
+
+    // ---- fused inverse DQT epilogue ----
+    const uint32_t* ltab = SMEM_TABLES ? s_l : f.l_table;
+    const uint32_t* htab = SMEM_TABLES ? s_h : f.h_table;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int64_t row = m0 + wm * 32 + i * 8 + ar;
+        if (row >= prm.M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t col = n0 + wn * 32 + j * 8 + ac * 2 + h;  // word column
+                if (col >= prm.Nw) continue;
+                const double r = acc[i][j][h];
+                if (EPI == EPI_GF) {
+                    uint32_t u[ND + 1];
+                    redq_compress_f64<ND>(r, f.invp_up, (double)f.p, f.bound, f.p, (int)f.t, u);
+                    uint32_t li = 0, hi = 0;
+#pragma unroll
+                    for (int q = 0; q < K; ++q) {
+                        li |= u[q] << (f.bb * q);
+                        hi |= u[K - 1 + q] << (f.bb * q);
+                    }
+                    const uint32_t res = add_coeff_bytes(ltab[li], htab[hi], f.p, K);
+                    uint8_t* dst = prm.c + (row * prm.n_out + col) * K;
+#pragma unroll
+                    for (int l = 0; l < K; ++l) dst[l] = (uint8_t)(res >> (8 * l));
+                } else {
+                    // right_cmm: d+1 corrected digits of one word = d+1 output entries
+                    const int dd = prm.d;
+                    const uint64_t ri = (uint64_t)r;
+                    const uint64_t si = (uint64_t)fdiv_floor(r, f.invp_up, (double)f.p, f.bound);
+                    uint32_t prev = (uint32_t)ri - f.p * (uint32_t)si;
+                    uint8_t* dst = prm.c + row * prm.n_out;
+                    for (int q = 0; q <= dd; ++q) {
+                        uint32_t next = 0;
+                        if (q < dd) next = (uint32_t)(ri >> ((q + 1) * f.t)) - f.p * (uint32_t)(si >> ((q + 1) * f.t));
+                        const uint32_t mu = q < dd ? mod_small(prev + f.corr * next, f.p, f.magic) : prev;
+                        const int64_t oc = col * (dd + 1) + q;
+                        if (oc < prm.n_out) dst[oc] = (uint8_t)mu;
+                        prev = next;
+                    }
+                }
+            }
+        }
+    }
+}
+
+// ---- DQT pack kernels (uint8 coefficients -> FP64 words, zero-padded) ----------
+// GF: src[R, C, k] -> dst[Rp, Cp], word = sum_l c_l << l t   (gfext.py:158-174)
+__global__ void pack_gf_kernel(const uint8_t* __restrict__ src, int64_t R, int64_t C, int k, int t,
+                               double* __restrict__ dst, int64_t Rp, int64_t Cp) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= Rp * Cp) return;
+    const int64_t r = i / Cp, c = i % Cp;
+    uint64_t w = 0;
+    if (r < R && c < C) {
+        const uint8_t* e = src + (r * C + c) * k;
+        for (int l = 0; l < k; ++l) w |= (uint64_t)e[l] << (l * t);
+    }
+    dst[i] = (double)w;
+}
+// CMM rows: src[R, C] uint8, groups of g entries -> word = sum_j e_j << j t (cmm.py:72-85)
+__global__ void pack_rows_f64_kernel(const uint8_t* __restrict__ src, int64_t R, int64_t C, int g, int t,
+                                     double* __restrict__ dst, int64_t Rp, int64_t Wp) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= Rp * Wp) return;
+    const int64_t r = i / Wp, w = i % Wp;
+    uint64_t v = 0;
+    if (r < R) {
+        for (int j = 0; j < g; ++j) {
+            const int64_t c = w * g + j;
+            if (c < C) v |= (uint64_t)src[r * C + c] << (j * t);
+        }
+    }
+    dst[i] = (double)v;
+}
+
+static inline int64_t rup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+template <int K, Epi EPI>
+static int launch(const Params& prm, const FieldConst& f, cudaStream_t s) {
+    const bool smem_tables = EPI == EPI_GF && (1 << (f.bb * K)) <= TABLE_MAX;
+    const size_t smem = PIPE_BYTES + (smem_tables ? 2 * TABLE_MAX * sizeof(uint32_t) : 0);
+    dim3 grid((unsigned)(prm.Np / BN), (unsigned)((prm.M + BM - 1) / BM));
+    QADIC_REQUIRE(grid.y <= 65535, QADIC_ERR_UNSUPPORTED, "m too large");
+    if (smem_tables) {
+        auto kern = dmma_gemm_kernel<K, EPI, true>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, THREADS, smem, s>>>(prm, f);
+    } else {
+        auto kern = dmma_gemm_kernel<K, EPI, false>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, THREADS, smem, s>>>(prm, f);
+    }
+    return check_launch("f64 dmma gemm");
+}
+
+}  // namespace f64
+
+size_t f64_gf_workspace(int64_t m, int64_t kdim, int64_t n) {
+    using namespace f64;
+    const int64_t Mp = rup(m, BM), Kp = rup(kdim, BK), Np = rup(n, BN);
+    return (size_t)(Mp * Kp + Kp * Np) * sizeof(double);
+}
+
+size_t f64_cmm_workspace(int64_t m, int64_t kdim, int64_t n, int d) {
+    using namespace f64;
+    const int64_t W = (n + d) / (d + 1);
+    const int64_t Mp = rup(m, BM), Kp = rup(kdim, BK), Np = rup(W, BN);
+    return (size_t)(Mp * Kp + Kp * Np) * sizeof(double);
+}
+
+int f64_gf_matmul(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
+                  int fold, void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s) {
+    using namespace f64;
+    const int64_t Mp = rup(m, BM), Kp = rup(kdim, BK), Np = rup(n, BN);
+    QADIC_REQUIRE(ws && ws_bytes >= f64_gf_workspace(m, kdim, n), QADIC_ERR_VALUE, "workspace too small");
+    double* aw = static_cast<double*>(ws);
+    double* bw = aw + Mp * Kp;
+    pack_gf_kernel<<<(unsigned)((Mp * Kp + 255) / 256), 256, 0, s>>>(a, m, kdim, (int)f.k, (int)f.t, aw, Mp, Kp);
+    int rc = check_launch("f64 pack A");
+    if (rc) return rc;
+    pack_gf_kernel<<<(unsigned)((Kp * Np + 255) / 256), 256, 0, s>>>(b, kdim, n, (int)f.k, (int)f.t, bw, Kp, Np);
+    rc = check_launch("f64 pack B");
+    if (rc) return rc;
+    Params prm;
+    prm.a = aw;
+    prm.b = bw;
+    prm.M = m;
+    prm.Nw = n;
+    prm.Kp = Kp;
+    prm.Np = Np;
+    prm.n_out = n;
+    prm.fold = fold;
+    prm.d = 0;
+    prm.c = c;
+    switch (f.k) {
+        case 1: return launch<1, EPI_GF>(prm, f, s);
+        case 2: return launch<2, EPI_GF>(prm, f, s);
+        case 3: return launch<3, EPI_GF>(prm, f, s);
+        default: return launch<4, EPI_GF>(prm, f, s);
+    }
+}
+
+int f64_right_cmm(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n, uint32_t p, int t, int d,
+                  void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s) {
+    using namespace f64;
+    const int g = d + 1;
+    const int64_t W = (n + d) / g;
+    const int64_t Mp = rup(m, BM), Kp = rup(kdim, BK), Np = rup(W, BN);
+    QADIC_REQUIRE(ws && ws_bytes >= f64_cmm_workspace(m, kdim, n, d), QADIC_ERR_VALUE, "workspace too small");
+    double* aw = static_cast<double*>(ws);
+    double* bw = aw + Mp * Kp;
+    pack_rows_f64_kernel<<<(unsigned)((Mp * Kp + 255) / 256), 256, 0, s>>>(a, m, kdim, 1, t, aw, Mp, Kp);
+    int rc = check_launch("f64 pack A");
+    if (rc) return rc;
+    pack_rows_f64_kernel<<<(unsigned)((Kp * Np + 255) / 256), 256, 0, s>>>(b, kdim, n, g, t, bw, Kp, Np);
+    rc = check_launch("f64 pack B");
+    if (rc) return rc;
+    FieldConst f = {};
+    f.p = p;
+    f.k = 1;
+    f.t = (uint32_t)t;
+    const uint64_t q = 1ull << t;
+    f.corr = (q % p == 0) ? 0u : (uint32_t)((p - q % p) % p);
+    f.magic = small_magic(p);
+    f.invp_up = host_reciprocal_up(p);
+    f.bound = host_case2_bound();
+    Params prm;
+    prm.a = aw;
+    prm.b = bw;
+    prm.M = m;
+    prm.Nw = W;
+    prm.Kp = Kp;
+    prm.Np = Np;
+    prm.n_out = n;
+    prm.fold = 0;
+    prm.d = d;
+    prm.c = c;
+    return launch<1, EPI_CMM>(prm, f, s);
+}
+
+}  // namespace qadic

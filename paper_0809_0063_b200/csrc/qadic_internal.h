@@ -1,0 +1,21 @@
+// Host-side internals shared by the translation units of libqadic_b200.so.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/qadic_b200.h"
+
+namespace qadic {
+
+// RU(1/p): the smallest double >= 1/p (fdiv.py:166-180, mode UP).
+double host_reciprocal_up(int64_t p);
+// First r at which floor(RN(r*RU(1/p))) may exceed floor(r/p) -- the fdiv
+// case-2 bound for beta = 53 (fdiv.py:250-260, 317-335): 3002399751580331.
+double host_case2_bound();
+
+void set_error(int code, const char* fmt, ...);
+int check_launch(const char* what);
+void count_launch(int n = 1);
+
+}  // namespace qadic

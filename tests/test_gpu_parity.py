@@ -1,0 +1,302 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's
+golden vectors and the pinned CPU oracle.  Bit-exact (integer work)."""
+
+import numpy as np
+import pytest
+
+import paper_0809_0063_b200 as Q
+from oracle import qadic_oracle as O
+from paper_0809_0063_b200 import _kernels, cmm, gfext, polymul, redq, workloads as W
+from paper_0809_0063_b200.params import PackingParams, cmm_params, dqt_params, fqt_params
+
+pytestmark = pytest.mark.gpu
+
+
+def _field(golden_scalars, name):
+    s = golden_scalars[f"field_{name}"]
+    return gfext.build_field(s["p"], s["k"], irreducible=s["irreducible"], max_dot_length=s["n_max"])
+
+
+# ---------------------------------------------------------------------------
+# Layer K (reference tests/test_kernels.py semantics)
+# ---------------------------------------------------------------------------
+class TestLayerK:
+    def test_backend_registry(self):
+        assert _kernels.available_backends() == ("cuda",)
+        assert _kernels.get_backend() == "cuda"
+        with pytest.raises(ValueError):
+            _kernels.set_backend("pure")
+
+    def test_matmul_u64_wraps(self, golden):
+        c = _kernels.matmul_exact_u64(golden["k_mm_u64_a"], golden["k_mm_u64_b"])
+        assert c.dtype == np.uint64
+        assert np.array_equal(c, golden["k_mm_u64_c"])
+
+    def test_matmul_u64_random_shapes(self):
+        rng = np.random.default_rng(5)
+        for m, k, n in ((1, 1, 1), (65, 129, 3), (200, 17, 130), (3, 300, 64)):
+            a = rng.integers(0, 1 << 63, (m, k), dtype=np.uint64)
+            b = rng.integers(0, 1 << 63, (k, n), dtype=np.uint64)
+            assert np.array_equal(_kernels.matmul_exact_u64(a, b), O.matmul_exact_u64(a, b))
+
+    def test_matmul_mod(self, golden):
+        for chunk in (7, 64, 10**6):
+            c = _kernels.matmul_mod_i64(golden["k_mm_mod_a"], golden["k_mm_mod_b"], 7, chunk)
+            assert np.array_equal(c, golden[f"k_mm_mod_c_{chunk}"])
+
+    def test_conv(self, golden):
+        a, b = golden["k_conv_a"], golden["k_conv_b"]
+        assert np.array_equal(_kernels.conv_exact_i64(a, b), golden["k_conv_i64"])
+        au = a.astype(np.uint64) << np.uint64(30)
+        assert np.array_equal(_kernels.conv_exact_u64(au, b.astype(np.uint64)), golden["k_conv_u64"])
+
+    @pytest.mark.parametrize("name", ["a", "cfg1", "cfg2", "cfg3", "cfg5", "wide"])
+    def test_redq(self, golden, golden_scalars, name):
+        p, t, d = golden_scalars[f"k_redq_{name}"]
+        r = golden[f"k_redq_{name}_r"]
+        assert np.array_equal(_kernels.redq_compress_u64(r, p, t, d), golden[f"k_redq_{name}_u"])
+        assert np.array_equal(redq.reduce_words_digits(r, p, t, d), golden[f"k_redq_{name}_digits"])
+        assert np.array_equal(redq.reduce_words_array(r, p, t, d), golden[f"k_redq_{name}_words"])
+
+    def test_redq_fdiv_boundary(self):
+        """Accumulators around the fdiv case-2 bound and 2^53 (the cold
+        multiply-back branch and the integer-division branch)."""
+        B = Q.fdiv.case2_bound()
+        r = np.array([B - 2, B - 1, B, B + 1, (1 << 53) - 1, 1 << 53, (1 << 53) + 1, (1 << 64) - 1,
+                      0, 1, 2, 3], dtype=np.uint64)
+        rng = np.random.default_rng(9)
+        r = np.concatenate([r, rng.integers(B, 1 << 53, 20000, dtype=np.uint64)])
+        for p, t, d in ((3, 17, 2), (7, 10, 4), (5, 13, 3), (127, 20, 2)):
+            assert np.array_equal(_kernels.redq_compress_u64(r, p, t, d), O.redq_compress_u64(r, p, t, d))
+
+    def test_redq_rejects_wide_span(self):
+        with pytest.raises(ValueError):
+            _kernels.redq_compress_u64(np.zeros(3, np.uint64), 3, 16, 4)
+
+    def test_empty(self):
+        a = np.zeros((0, 4), dtype=np.uint64)
+        b = np.zeros((4, 3), dtype=np.uint64)
+        assert _kernels.matmul_exact_u64(a, b).shape == (0, 3)
+        z = _kernels.matmul_exact_u64(np.zeros((2, 0), np.uint64), np.zeros((0, 5), np.uint64))
+        assert z.shape == (2, 5) and not z.any()
+        assert _kernels.redq_compress_u64(np.zeros(0, np.uint64), 3, 5, 2).shape == (0, 3)
+
+    def test_shape_errors(self):
+        with pytest.raises(ValueError):
+            _kernels.matmul_exact_u64(np.zeros((2, 3), np.uint64), np.zeros((4, 2), np.uint64))
+
+
+# ---------------------------------------------------------------------------
+# cfg1: batched polynomial products
+# ---------------------------------------------------------------------------
+class TestPolymul:
+    def test_cfg1_golden(self, golden):
+        prm = dqt_params(3, n=1, k=4)
+        c = polymul.polymul_fqt_batch(golden["cfg1_a"], golden["cfg1_b"], prm)
+        assert np.array_equal(c, golden["cfg1_c"])
+
+    @pytest.mark.parametrize("n", [1, 3, 1023, 1024, 1025, 5000])
+    def test_cfg1_ragged(self, n):
+        g = W.rng(n)
+        a = g.integers(0, 3, (n, 4), dtype=np.uint8)
+        b = g.integers(0, 3, (n, 4), dtype=np.uint8)
+        c = polymul.polymul_fqt_batch(a, b, dqt_params(3, n=1, k=4))
+        assert np.array_equal(c, O.polymul_batch(a, b, 3, 5))
+
+    @pytest.mark.parametrize("p,k", [(2, 6), (5, 3), (7, 2), (3, 1), (11, 2)])
+    def test_generic_widths(self, p, k):
+        prm = dqt_params(p, n=1, k=k)
+        g = W.rng(p * 10 + k)
+        a = g.integers(0, p, (777, k), dtype=np.uint8)
+        b = g.integers(0, p, (777, k), dtype=np.uint8)
+        c = polymul.polymul_fqt_batch(a, b, prm)
+        assert np.array_equal(c, O.polymul_batch(a, b, p, prm.t))
+
+    def test_all_maximal(self):
+        prm = dqt_params(3, n=1, k=4)
+        a = np.full((4096, 4), 2, np.uint8)
+        c = polymul.polymul_fqt_batch(a, a, prm)
+        assert np.array_equal(c, O.polymul_batch(a, a, 3, 5))
+
+    @pytest.mark.parametrize("name", ["l3", "l7", "l2"])
+    def test_long_fqt(self, golden, golden_scalars, name):
+        p, t, d = golden_scalars[f"poly_{name}"]
+        prm = fqt_params(p, d)
+        a = polymul.ModPoly(golden[f"poly_{name}_a"], p)
+        b = polymul.ModPoly(golden[f"poly_{name}_b"], p)
+        assert np.array_equal(polymul.polymul_fqt(a, b, prm).coeffs, golden[f"poly_{name}_c"])
+        kara = polymul.polymul_fqt(a, b, prm, "karatsuba", threshold=8)
+        assert np.array_equal(kara.coeffs, golden[f"poly_{name}_c"])
+        assert polymul.polymul_delayed(a, b).same_poly(kara)
+
+    def test_worked_example(self, golden_scalars):
+        a = polymul.ModPoly.from_list([1, 1], 3)
+        b = polymul.ModPoly.from_list([2, 1], 3)
+        assert polymul.polymul_fqt(a, b, fqt_params(3, 1)).coeffs.tolist() == golden_scalars["we_polymul"]
+
+
+# ---------------------------------------------------------------------------
+# cfg2: batched GF dot products
+# ---------------------------------------------------------------------------
+class TestGFDot:
+    def test_cfg2_golden_handles(self, golden, golden_scalars):
+        f = _field(golden_scalars, "gf9_64")
+        for a, b, o in (("cfg2_v1_idx", "cfg2_v2_idx", "cfg2_out_idx"), ("cfg2_n1_v1", "cfg2_n1_v2", "cfg2_n1_out"),
+                        ("cfg2_n7_v1", "cfg2_n7_v2", "cfg2_n7_out"), ("cfg2_n33_v1", "cfg2_n33_v2", "cfg2_n33_out")):
+            assert np.array_equal(f.fgdp_batch(golden[a], golden[b]), golden[o])
+
+    def test_scalar_fgdp(self, golden, golden_scalars):
+        f = _field(golden_scalars, "gf9_64")
+        v1, v2, out = golden["cfg2_v1_idx"], golden["cfg2_v2_idx"], golden["cfg2_out_idx"]
+        for i in range(3):
+            got = f.fgdp([f.elem(int(x)) for x in v1[i]], [f.elem(int(y)) for y in v2[i]])
+            assert got.index == out[i]
+
+    def test_gf25(self, golden, golden_scalars):
+        f = _field(golden_scalars, "gf25_20")
+        assert np.array_equal(f.fgdp_batch(golden["gf25_v1"], golden["gf25_v2"]), golden["gf25_out"])
+
+    @pytest.mark.parametrize("p,k,n", [(3, 2, 64), (7, 3, 9), (2, 4, 20), (5, 1, 100), (3, 2, 5), (3, 3, 17)])
+    def test_vs_oracle(self, p, k, n):
+        f = gfext.build_field(p, k, max_dot_length=n)
+        of = O.build_field(p, k, max_dot_length=n)
+        g = W.rng(p + k + n)
+        v1 = g.integers(0, p, (3001, n, k), dtype=np.uint8)
+        v2 = g.integers(0, p, (3001, n, k), dtype=np.uint8)
+        assert np.array_equal(f.fgdp_batch_coeffs(v1, v2), O.gf_dot_batch(of, v1, v2))
+
+    def test_length_guard(self, golden_scalars):
+        f = _field(golden_scalars, "gf9_64")
+        with pytest.raises(Q.ParamsViolation):
+            f.fgdp_batch_coeffs(np.zeros((2, 65, 2), np.uint8), np.zeros((2, 65, 2), np.uint8))
+
+
+# ---------------------------------------------------------------------------
+# cfg3 / cfg5: GF(p^k) matmul, both engines
+# ---------------------------------------------------------------------------
+ENGINES = ["i8", "f64"]
+
+
+class TestGFMatmul:
+    @pytest.mark.parametrize("engine", ENGINES)
+    @pytest.mark.parametrize("fname,pre", [("gf9_8192", "cfg3"), ("gf9_8192", "cfg3s"), ("gf11_64", "gf11"),
+                                           ("gf27_20", "gf27")])
+    def test_golden(self, golden, golden_scalars, engine, fname, pre):
+        f = _field(golden_scalars, fname)
+        sfx = "_idx" if pre.startswith("cfg") else ""
+        c = f.matmul(golden[f"{pre}_a{sfx}"], golden[f"{pre}_b{sfx}"], engine=engine)
+        assert np.array_equal(c, golden[f"{pre}_c{sfx}"])
+
+    @pytest.mark.parametrize("engine", ENGINES)
+    def test_cfg5_golden_folded(self, golden, golden_scalars, engine):
+        f = _field(golden_scalars, "gf343_9")
+        a = f.to_coeffs(golden["cfg5_a_idx"])
+        b = f.to_coeffs(golden["cfg5_b_idx"])
+        c = f.matmul_coeffs(a, b, engine=engine)
+        assert np.array_equal(f.to_indices(c), golden["cfg5_c_idx"])
+
+    @pytest.mark.parametrize("engine", ENGINES)
+    @pytest.mark.parametrize("m,kd,n", [(1, 1, 1), (128, 64, 128), (130, 200, 257), (257, 1000, 129),
+                                        (64, 4096, 96), (300, 33, 7)])
+    def test_cfg3_shapes(self, engine, m, kd, n):
+        f = W.field_for(W.CONFIGS[3])
+        of = O.build_field(3, 2, irreducible=[1, 0, 1], max_dot_length=8192)
+        g = W.rng(m + kd + n)
+        a = g.integers(0, 3, (m, kd, 2), dtype=np.uint8)
+        b = g.integers(0, 3, (kd, n, 2), dtype=np.uint8)
+        assert np.array_equal(f.matmul_coeffs(a, b, engine=engine), O.gf_matmul(of, a, b))
+
+    @pytest.mark.parametrize("engine", ENGINES)
+    @pytest.mark.parametrize("m,kd,n", [(64, 900, 80), (129, 2051, 33), (256, 8192, 256)])
+    def test_cfg5_shapes(self, engine, m, kd, n):
+        c5 = W.CONFIGS[5]
+        f = W.field_for(c5)
+        of = O.build_field(7, 3, irreducible=[5, 0, 0, 1], max_dot_length=9)
+        g = W.rng(m * kd + n)
+        a = g.integers(0, 7, (m, kd, 3), dtype=np.uint8)
+        b = g.integers(0, 7, (kd, n, 3), dtype=np.uint8)
+        ref = O.gf_matmul_planes(of, a, b)
+        assert np.array_equal(f.matmul_coeffs(a, b, engine=engine), ref)
+        if kd <= 900:
+            assert np.array_equal(ref, O.gf_matmul_folded(of, a, b, 9))
+
+    def test_all_maximal_cfg3(self):
+        """every product digit at its maximum (the strict bound's corner)."""
+        f = W.field_for(W.CONFIGS[3])
+        of = O.build_field(3, 2, irreducible=[1, 0, 1], max_dot_length=8192)
+        a = np.full((128, 8192, 2), 2, np.uint8)
+        b = np.full((8192, 256, 2), 2, np.uint8)
+        ref = O.gf_matmul_planes(of, a, b)
+        for e in ENGINES:
+            assert np.array_equal(f.matmul_coeffs(a, b, engine=e), ref)
+
+    def test_guards(self, golden_scalars):
+        f = _field(golden_scalars, "gf9_64")
+        with pytest.raises(Q.ParamsViolation):
+            f.matmul(np.zeros((2, 65), np.int64), np.zeros((65, 2), np.int64))
+        with pytest.raises(Q.DimensionMismatch):
+            f.matmul(np.zeros((2, 3), np.int64), np.zeros((4, 2), np.int64))
+        with pytest.raises(ValueError):
+            f.matmul(np.full((2, 3), 9, np.int64), np.zeros((3, 2), np.int64))
+
+
+# ---------------------------------------------------------------------------
+# cfg4: right-compressed matmul
+# ---------------------------------------------------------------------------
+class TestRightCMM:
+    @pytest.mark.parametrize("engine", ENGINES)
+    @pytest.mark.parametrize("n", [250, 97])
+    @pytest.mark.parametrize("tag", ["strict", "cfg4"])
+    def test_golden(self, golden, golden_scalars, engine, n, tag):
+        p, t, d, nmax = golden_scalars[f"cfg4_{n}_{tag}"]
+        prm = PackingParams(p=p, q=1 << t, d=d, n_max=nmax)
+        a = golden[f"cfg4_{n}_a"]
+        cb = cmm.compress_rows(a, prm)
+        assert np.array_equal(cb.words, golden[f"cfg4_{n}_{tag}_words"])
+        assert np.array_equal(cmm.right_cmm(a, cb, engine=engine), golden[f"cfg4_{n}_{tag}_c"])
+
+    @pytest.mark.parametrize("engine", ENGINES)
+    def test_cmm5_golden(self, golden, golden_scalars, engine):
+        p, t, d, nmax = golden_scalars["cmm5"]
+        prm = PackingParams(p=p, q=1 << t, d=d, n_max=nmax)
+        c = cmm.right_cmm(golden["cmm5_a"], cmm.compress_rows(golden["cmm5_b"], prm), engine=engine)
+        assert np.array_equal(c, golden["cmm5_c"])
+
+    @pytest.mark.parametrize("engine", ENGINES)
+    @pytest.mark.parametrize("n", [1, 2, 129, 1000, 2048])
+    def test_symmetric(self, engine, n):
+        c4 = W.CONFIGS[4]
+        a = W.make_inputs(c4, (n,), seed=n)["a"]
+        prm = cmm_params(3, n, strict=True)
+        got = cmm.right_cmm(a, cmm.compress_rows(a, prm), engine=engine)
+        assert np.array_equal(got, O.modmatmul_planes(a, a, 3))
+
+    def test_keep_packed_and_modmatmul(self):
+        g = W.rng(44)
+        a = g.integers(0, 5, (70, 90), dtype=np.int64)
+        b = g.integers(0, 5, (90, 50), dtype=np.int64)
+        prm = cmm_params(5, 90, strict=True)
+        kp = cmm.right_cmm(a, cmm.compress_rows(b, prm), keep_packed=True)
+        assert np.array_equal(cmm.uncompress(kp), O.modmatmul_planes(a, b, 5))
+        assert np.array_equal(cmm.modmatmul(a, b, 5), O.modmatmul_planes(a, b, 5))
+
+    def test_other_variants(self):
+        g = W.rng(45)
+        for p in (2, 3, 5, 7):
+            a = g.integers(0, p, (37, 61), dtype=np.int64)
+            b = g.integers(0, p, (61, 29), dtype=np.int64)
+            ref = O.modmatmul_planes(a, b, p)
+            prm = cmm_params(p, 61, strict=True)
+            assert np.array_equal(cmm.left_cmm(cmm.compress_cols(a, prm), b), ref)
+            ca = cmm.compress_rows(a, prm, cmm.REVERSED)
+            cb = cmm.compress_cols(b, prm, cmm.FORWARD)
+            assert np.array_equal(cmm.cmm_multiply(ca, cb), ref)
+            assert np.array_equal(cmm.full_cmm(a, b, Q.full_cmm_params(p, 61, strict=True)), ref)
+            for build, order in ((cmm.compress_rows, cmm.FORWARD), (cmm.compress_cols, cmm.REVERSED)):
+                assert np.array_equal(cmm.uncompress(build(a, prm, order)), a)
+
+    def test_bound_guard(self):
+        prm = cmm_params(3, 16, strict=False)  # inclusive radix: refused by right_cmm
+        a = np.ones((4, 16), np.int64)
+        with pytest.raises(Q.ParamsViolation):
+            cmm.right_cmm(a, cmm.compress_rows(np.ones((16, 4), np.int64), prm))
