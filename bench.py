@@ -1,0 +1,525 @@
+"""Benchmark of the qadic hot path on B200 (contract: see DESIGN.md section 6).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5|all]
+                    [--engine auto|i8|f64] [--impl ours|reference]
+
+One "step" is one pass of the hot path over one batch of the config's
+synthetic seeded input (BASELINE.json configs).  Default workload: cfg5 --
+the GF(7^3) matmul 8192^3 that BASELINE.json runs at 1/2/4/8 GPUs.
+Multi-GPU (torchrun, one rank per GPU): matmul configs shard A by row
+blocks and broadcast B once per step over NCCL (no reduction); batched
+configs shard the batch with no collective.  Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            pk = json.load(fh)
+        return pk, "measured"
+    except OSError:
+        return dict(PEAKS_FALLBACK), "fallback"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            with open(self.path) as fh:
+                for line in fh:
+                    parts = [x.strip() for x in line.split(",")]
+                    if len(parts) >= 9:
+                        rows.append(parts)
+        except OSError:
+            pass
+        finally:
+            if self.path:
+                os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+
+        sm = [num(r[1]) for r in rows if num(r[1]) is not None]
+        mx = [num(r[2]) for r in rows if num(r[2]) is not None]
+        busy = [s for s in sm if s and mx and s > 0.3 * max(mx)] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max((num(r[3]) or 0.0) for r in rows)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def build_step(cfg, engine, rank, ws, torch, dist, Q, W):
+    """Returns (step(i), e2e_step(i) or None, units/step/rank, meta)."""
+    c = W.CONFIGS[cfg]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    meta = {"config": {"workload": c.label}}
+    if cfg in (3, 5):
+        f = W.field_for(c)
+        m, kd, n = c.shape
+        rows = m // ws
+        host = W.make_inputs(c)
+        a_h = np.ascontiguousarray(host["a"][rank * rows:(rank + 1) * rows])
+        b_h = host["b"]
+        a = torch.from_numpy(a_h).to(dev)
+        b = torch.from_numpy(b_h).to(dev) if rank == 0 else torch.empty(b_h.shape, dtype=torch.uint8, device=dev)
+        out = torch.empty((rows, n, c.k), dtype=torch.uint8, device=dev)
+
+        def step(i):
+            if ws > 1:
+                dist.broadcast(b, src=0)
+            f.matmul_coeffs(a, b, engine=engine, out=out)
+
+        a_pin = torch.from_numpy(a_h).pin_memory()
+        b_pin = torch.from_numpy(b_h).pin_memory()
+        o_pin = torch.empty((rows, n, c.k), dtype=torch.uint8).pin_memory()
+
+        def e2e(i):
+            bb = b_pin if rank == 0 else b
+            if ws > 1:
+                b_dev = b_pin.to(dev, non_blocking=True) if rank == 0 else b
+                dist.broadcast(b_dev, src=0)
+                bb = b_dev
+            f.matmul_coeffs(a_pin, bb, engine=engine, out=o_pin)
+            torch.cuda.current_stream().synchronize()
+
+        e2e_bytes = (a_h.nbytes + (b_h.nbytes if rank == 0 else 0), rows * n * c.k)
+        units = rows * kd * n
+        meta["config"].update({"M": m, "N": n, "K": kd, "k": c.k, "p": c.p, "fold_every": c.dot_bound,
+                               "engine": engine, "l2": "inputs 2x%d MiB > 126 MB L2" % (b_h.nbytes >> 20),
+                               "parallelism": f"rowblock{ws}+bcastB" if ws > 1 else "single"})
+        meta["work"] = W.work_units(c, (rows, kd, n))
+        return step, e2e, units, e2e_bytes, meta
+    if cfg == 4:
+        (n,) = c.shape
+        rows = n // ws
+        prm = W.params_for(c)
+        host = W.make_inputs(c)["a"]
+        full = torch.from_numpy(host).to(dev) if rank == 0 else torch.empty((n, n), dtype=torch.uint8, device=dev)
+        out = torch.empty((rows, n), dtype=torch.uint8, device=dev)
+
+        def step(i):
+            if ws > 1:
+                dist.broadcast(full, src=0)
+            cb = Q.cmm.compress_rows(full, prm)
+            Q.cmm.right_cmm(full[rank * rows:(rank + 1) * rows], cb, engine=engine, out=out)
+
+        pin = torch.from_numpy(host).pin_memory()
+        o_pin = torch.empty((rows, n), dtype=torch.uint8).pin_memory()
+
+        def e2e(i):
+            d = pin.to(dev, non_blocking=True) if rank == 0 else full
+            if ws > 1:
+                dist.broadcast(d, src=0)
+            cb = Q.cmm.compress_rows(d, prm)
+            Q.cmm.right_cmm(d[rank * rows:(rank + 1) * rows], cb, engine=engine, out=o_pin)
+            torch.cuda.current_stream().synchronize()
+
+        units = rows * n * n
+        meta["config"].update({"n": n, "p": 3, "t": prm.t, "entries_per_word": prm.k, "engine": engine,
+                               "density": 0.5, "l2": "A 256 MiB > 126 MB L2",
+                               "parallelism": f"rowblock{ws}+bcastA" if ws > 1 else "single"})
+        w = W.work_units(c)
+        meta["work"] = {k: v // ws for k, v in w.items() if isinstance(v, int)}
+        meta["work"]["i8_macs"] = rows * n * n
+        return step, e2e, units, (host.nbytes if rank == 0 else 0, rows * n), meta
+    # batched configs: rotate buffer sets totalling > L2 so every step reads HBM
+    if cfg == 1:
+        (nn,) = c.shape
+        shard = (nn // ws, )
+        prm = W.params_for(c)
+    else:
+        bsz, ln = c.shape
+        shard = (bsz // ws, ln)
+        f = W.field_for(c)
+    sets = 16
+    bufs = []
+    for s in range(sets):
+        x = W.make_inputs(c, shard, seed=1000 * cfg + 100 * rank + s)
+        bufs.append({k: torch.from_numpy(v).to(dev) for k, v in x.items()})
+    if cfg == 1:
+        outs = [torch.empty((shard[0], 2 * c.k - 1), dtype=torch.uint8, device=dev) for _ in range(sets)]
+
+        def step(i):
+            x = bufs[i % sets]
+            Q.polymul.polymul_fqt_batch(x["a"], x["b"], prm, out=outs[i % sets])
+
+        host = W.make_inputs(c, shard, seed=1000 * cfg + 100 * rank)
+        pins = {k: torch.from_numpy(v).pin_memory() for k, v in host.items()}
+        o_pin = torch.empty((shard[0], 2 * c.k - 1), dtype=torch.uint8).pin_memory()
+
+        def e2e(i):
+            Q.polymul.polymul_fqt_batch(pins["a"], pins["b"], prm, out=o_pin)
+            torch.cuda.current_stream().synchronize()
+
+        units = shard[0]
+        io = (host["a"].nbytes * 2, o_pin.numel())
+    else:
+        outs = [torch.empty((shard[0], c.k), dtype=torch.uint8, device=dev) for _ in range(sets)]
+
+        def step(i):
+            x = bufs[i % sets]
+            f.fgdp_batch_coeffs(x["v1"], x["v2"], out=outs[i % sets])
+
+        host = W.make_inputs(c, shard, seed=1000 * cfg + 100 * rank)
+        pins = {k: torch.from_numpy(v).pin_memory() for k, v in host.items()}
+        o_pin = torch.empty((shard[0], c.k), dtype=torch.uint8).pin_memory()
+
+        def e2e(i):
+            f.fgdp_batch_coeffs(pins["v1"], pins["v2"], out=o_pin)
+            torch.cuda.current_stream().synchronize()
+
+        units = shard[0] * shard[1]
+        io = (host["v1"].nbytes * 2, o_pin.numel())
+    per_set = sum(v.numel() for v in bufs[0].values())
+    meta["config"].update({"shape": list(c.shape), "p": c.p, "k": c.k, "engine": "fused",
+                           "l2": f"rotating {sets} input sets x {per_set >> 20} MiB > 126 MB L2",
+                           "parallelism": f"batch{ws}" if ws > 1 else "single"})
+    meta["work"] = W.work_units(c, shard)
+    return step, e2e, units, io, meta
+
+
+def dominant_kernel(cfg, engine, prof):
+    """Name of the kernel the roofline is quoted on: the longest total."""
+    if not prof:
+        return None
+    return max(prof, key=lambda k: prof[k][1])
+
+
+def roofline(cfg, engine, kname, kstats, work, peaks, peak_src):
+    if kname is None:
+        return None
+    count, total_ms = kstats
+    avg_s = total_ms / count / 1e3
+    if kname == "i8 gemm":
+        ops = 2 * work["i8_macs"]
+        achieved = ops / avg_s / 1e12
+        peak = 2 * peaks["bf16_tflops"]
+        src = f"2 x {peak_src} bf16 burst (sm_100 dense int8 rate = 2x bf16; nominal 4500)"
+        return {"bound": "tensor", "kernel": kname, "achieved": round(achieved, 1), "peak": round(peak, 1),
+                "unit": "TOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+                "avg_launch_ms": round(avg_s * 1e3, 4), "algorithmic_ops_per_launch": ops, "peak_source": src}
+    if kname == "f64 dmma gemm":
+        ops = 2 * work["f64_fmas"]
+        achieved = ops / avg_s / 1e12
+        peak = 40.0
+        return {"bound": "tensor", "kernel": kname, "achieved": round(achieved, 2), "peak": peak,
+                "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+                "avg_launch_ms": round(avg_s * 1e3, 3), "algorithmic_ops_per_launch": ops,
+                "peak_source": "nominal B200 FP64 tensor 40 TFLOP/s (no measured FP64 peak on this pool)"}
+    # HBM-bound kernels: uint8 I/O bytes of one launch
+    byts = work["io_bytes"]
+    achieved = byts / avg_s / 1e9
+    peak = peaks["hbm_gbs"]
+    return {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": None, "avg_launch_ms": round(avg_s * 1e3, 5),
+            "algorithmic_bytes_per_launch": byts, "peak_source": f"{peak_src} hbm_gbs (copy)"}
+
+
+def parse_prof(text):
+    out = {}
+    for line in text.strip().splitlines():
+        name, cnt, ms = line.rsplit(",", 2)
+        out[name] = (int(cnt), float(ms))
+    return out
+
+
+def traffic_from_profiles(cfg, engine, kname):
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            t = json.load(fh)
+        return t.get(f"cfg{cfg}:{engine}:{kname}")
+    except (OSError, ValueError):
+        return None
+
+
+def cpu_baseline_leg(cfg, args):
+    """Reference CPU path on rank 0, single core, bounded sample (~10-30 s)."""
+    from oracle import cpu_ref
+    from paper_0809_0063_b200 import workloads as W
+
+    c = W.CONFIGS[cfg]
+    # ~10-30 s of single-core work: whole batch repeated (cfg1/2) or a row block at full K, N
+    rows, reps = {1: (1 << 20, 20), 2: (65536, 100), 3: (64, 1), 4: (64, 1), 5: (12, 1)}[cfg]
+    full = W.make_inputs(c) if cfg not in (3, 5) else _matmul_sample_inputs(c, rows)
+    units, secs = 0, 0.0
+    kind = "port"
+    for _ in range(reps):
+        u, s, kind = cpu_ref.time_reference(cfg, full, rows, workers=1)
+        units += u
+        secs += s
+    unit = "pairs/s" if cfg == 1 else ("F_p mult-adds/s" if cfg == 4 else "GF mult-adds/s")
+    what = {1: f"{reps} x {rows} pairs", 2: f"{reps} x {rows} dots of length 64", 3: f"{rows} rows x 8192 x 8192",
+            4: f"{rows} rows x 16384 x 16384", 5: f"{rows} rows x 8192 x 8192, fold every 9"}[cfg]
+    return {"value": units / secs, "unit": unit, "cores": 1, "kind": kind,
+            "sample": f"{what} ({secs:.1f} s); reference _speed kernels + numpy driver composition"}
+
+
+def _matmul_sample_inputs(c, rows):
+    from paper_0809_0063_b200 import workloads as W
+
+    x = W.make_inputs(c)
+    return {"a": x["a"][:max(rows, 64)], "b": x["b"]}
+
+
+def run_ours(args):
+    import torch
+
+    ws, rank, local = dist_env()
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    import paper_0809_0063_b200 as Q
+    from paper_0809_0063_b200 import _native as N, workloads as W
+
+    N.load_library()
+    cfg = args.config
+    engine = args.engine
+    step, e2e, units, io, meta = build_step(cfg, engine, rank, ws, torch, dist, Q, W)
+    peaks, peak_src = load_peaks()
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for i in range(args.warmup):
+        step(i)
+    barrier()
+    # launch-bound batched configs: the K steps are captured once into a CUDA
+    # graph and replayed (the kernels are identical; host launch cost leaves)
+    graph = None
+    launches0 = N.launch_count()
+    if cfg in (1, 2) and not args.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for i in range(args.steps):
+                step(i)
+        graph.replay()  # warm replay
+        barrier()
+    # ---- timed pass: K steps, CUDA events on the launching stream ----
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        if graph is not None:
+            graph.replay()
+        else:
+            for i in range(args.steps):
+                step(i)
+        t1.record(stream)
+        barrier()
+    launches = N.launch_count() - launches0
+    ms = t0.elapsed_time(t1) / args.steps
+    if ws > 1:
+        tt = torch.tensor([ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    clocks = clk.summary()
+    # ---- second pass: per-kernel CUDA-event durations (same K steps) ----
+    lib = N.lib()
+    lib.qadic_profile_enable(1)
+    barrier()
+    for i in range(args.steps):
+        step(i)
+    barrier()
+    lib.qadic_profile_enable(0)
+    import ctypes
+
+    buf = ctypes.create_string_buffer(1 << 16)
+    lib.qadic_profile_collect.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+    lib.qadic_profile_collect(buf, len(buf))
+    prof = parse_prof(buf.value.decode())
+    # ---- e2e pass: public API with pinned host buffers (H2D + D2H inside) ----
+    e2e_steps = max(1, min(args.steps, 5))
+    e2e(0)
+    barrier()
+    w0 = time.perf_counter()
+    for i in range(e2e_steps):
+        e2e(i)
+    barrier()
+    e2e_s = (time.perf_counter() - w0) / e2e_steps
+    if ws > 1:
+        tt = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt.item())
+    total_units = units * ws
+    value = total_units / (ms / 1e3)
+    unit = "pairs/s" if cfg == 1 else ("F_p mult-adds/s" if cfg == 4 else "GF mult-adds/s")
+    kname = dominant_kernel(cfg, engine, prof)
+    work = meta["work"]
+    if engine == "f64" and cfg in (3, 5):
+        work["f64_fmas"] = work["madds"]
+    if engine == "f64" and cfg == 4:
+        n = W.CONFIGS[4].shape[0]
+        work["f64_fmas"] = (n // ws) * n * (-(-n // 3))
+    roof = roofline(cfg, engine, kname, prof.get(kname), work, peaks, peak_src)
+    if roof is not None:
+        roof["traffic"] = traffic_from_profiles(cfg, engine, kname)
+        total_ms = sum(v[1] for v in prof.values()) / args.steps
+        roof["kernel_share_of_step"] = round((prof[kname][1] / args.steps) / ms, 4) if ms else None
+        roof["kernels_ms_per_step"] = {k: round(v[1] / args.steps, 4) for k, v in prof.items()}
+    line = {
+        "metric": "GF(p^k) mult-adds/s (packed matmul) and REDQ coeffs/s vs roofline, 1-8 GPU",
+        "value": value, "unit": unit, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if cfg in (3, 4, 5) else "weak",
+        "vs_baseline": None,
+        "dtype": "f64" if (cfg in (1, 2) or engine == "f64") else "u8 x u8 -> s32 (tcgen05 kind::i8)",
+        "data": "synthetic (seeded Philox, BASELINE.json config shapes)",
+        "config": meta["config"],
+        "redq_coeffs_per_s": work["redq_coeffs"] * ws / (ms / 1e3),
+        "roofline": roof,
+        "e2e": {"value": total_units / e2e_s, "unit": unit, "h2d_bytes_per_step": int(io[0]),
+                "d2h_bytes_per_step": int(io[1]), "ms_per_step": e2e_s * 1e3},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_leg(cfg, args)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    """The reference's own CPU implementation on this box's host cores."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import cpu_ref
+    from paper_0809_0063_b200 import workloads as W
+
+    cfg = args.config
+    c = W.CONFIGS[cfg]
+    cores = os.cpu_count() or 1
+    workers = max(1, min(cores, 64))
+    # rows per worker sized for a few seconds of single-core work per step
+    rows = {1: 1 << 17, 2: 1 << 13, 3: 2, 4: 2, 5: 1}[cfg]
+    full = W.make_inputs(c) if cfg not in (3, 5) else _matmul_sample_inputs(c, max(64, rows * workers))
+    pool = cpu_ref.make_pool(cfg, full, workers) if workers > 1 else None
+    try:
+        for _ in range(args.warmup if args.warmup < 2 else 1):
+            cpu_ref.time_reference(cfg, full, rows, workers, pool=pool)
+        tot_u, tot_s, kind = 0, 0.0, "port"
+        for _ in range(args.steps):
+            u, s, kind = cpu_ref.time_reference(cfg, full, rows, workers, pool=pool)
+            tot_u += u
+            tot_s += s
+    finally:
+        if pool is not None:
+            pool.shutdown()
+    value = tot_u / tot_s
+    unit = "pairs/s" if cfg == 1 else ("F_p mult-adds/s" if cfg == 4 else "GF mult-adds/s")
+    sample = f"{workers} processes x {rows} rows/entries of cfg{cfg} per step"
+    line = {"impl": "reference",
+            "metric": "GF(p^k) mult-adds/s (packed matmul) and REDQ coeffs/s vs roofline, 1-8 GPU",
+            "value": value, "unit": unit, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": tot_s / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong" if cfg in (3, 4, 5) else "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (seeded Philox, BASELINE.json config shapes)",
+            "config": {"workload": c.label},
+            "cpu_baseline": {"value": value, "unit": unit, "cores": workers, "kind": kind, "sample": sample},
+            "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="5")
+    ap.add_argument("--engine", default="auto", choices=["auto", "i8", "f64"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="eager launches for cfg1/cfg2")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup) if args.impl == "ours" else args.warmup
+    cfgs = [1, 2, 3, 4, 5] if args.config == "all" else [int(args.config)]
+    for cfg in cfgs:
+        args.config = cfg
+        if args.impl == "reference":
+            run_reference(args)
+        else:
+            run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

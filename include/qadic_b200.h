@@ -47,6 +47,10 @@ QADIC_API int qadic_abi_version(void);
 QADIC_API const char *qadic_last_error(void);
 /* number of kernels this library launched since load (instrumentation) */
 QADIC_API int64_t qadic_launch_count(void);
+/* per-kernel CUDA-event timing on the launching stream (instrumentation):
+ * enable, run, then collect "name,count,total_ms" lines (synchronises). */
+QADIC_API void qadic_profile_enable(int on);
+QADIC_API int qadic_profile_collect(char *buf, size_t len);
 
 /* ---------------------------------------------------------------------------
  * Layer K: the operator/plugin kernels (_kernels/__init__.py:52-69).

@@ -200,6 +200,29 @@ def to_host(x, np_dtype) -> np.ndarray:
     return arr.astype(np_dtype, copy=False)
 
 
+def out_buffer(out, shape, np_dtype):
+    """Device buffer the kernel writes: `out` itself when it is a matching
+    CUDA tensor, else a fresh device tensor (copied into a host `out` by
+    finish())."""
+    if out is not None and is_tensor(out) and out.is_cuda:
+        if tuple(out.shape) != tuple(int(s) for s in shape) or not out.is_contiguous():
+            raise ValueError(f"out must be a contiguous tensor of shape {tuple(shape)}")
+        return out
+    return empty(shape, np_dtype)
+
+
+def finish(dev, out, host: bool, np_dtype):
+    """Return convention of every array API: a host `out` tensor is filled
+    (non-blocking D2H from pinned memory when possible), host inputs give a
+    numpy result, device inputs a device tensor."""
+    if out is not None and is_tensor(out) and not out.is_cuda:
+        out.copy_(dev.view(out.dtype) if dev.dtype != out.dtype else dev, non_blocking=out.is_pinned())
+        return out
+    if out is not None:
+        return out
+    return to_host(dev, np_dtype) if host else dev
+
+
 def ptr(x) -> int:
     return x.data_ptr() if x is not None and x.numel() else 0
 

@@ -33,23 +33,45 @@ ROWS, COLS = "rows", "cols"
 FORWARD, REVERSED = "forward", "reversed"
 
 
-@dataclass(frozen=True)
 class CompressedMatrix:
     """Rows (or columns) packed d+1 entries per word; digit_order FORWARD
-    puts group entry j at digit j, REVERSED at digit d-j."""
+    puts group entry j at digit j, REVERSED at digit d-j (cmm.py:50-69).
 
-    words: np.ndarray
-    params: PackingParams
-    orientation: str
-    digit_order: str
-    logical_shape: tuple
-    # uint8 entries on the device when the matrix was compressed here
-    # (lets the INT8 engine skip re-expanding the words)
-    _entries: object = field(default=None, repr=False, compare=False)
+    When built here from uint8 entries the matrix also keeps those entries
+    on the device and packs `words` lazily (qadic_pack_rows_u8) on first
+    access: the INT8 engine consumes the entries directly, so a right_cmm
+    step never materialises the packed words it does not need."""
+
+    __slots__ = ("_words", "params", "orientation", "digit_order", "logical_shape", "_entries", "_host")
+
+    def __init__(self, words, params: PackingParams, orientation: str, digit_order: str, logical_shape: tuple,
+                 _entries=None, _host: bool = True):
+        self._words = words
+        self.params = params
+        self.orientation = orientation
+        self.digit_order = digit_order
+        self.logical_shape = tuple(logical_shape)
+        self._entries = _entries
+        self._host = _host
+
+    @property
+    def words(self):
+        if self._words is None:
+            prm, rev = self.params, self.digit_order == REVERSED
+            if self.orientation == ROWS:
+                w = _pack_dev(self._entries, prm.k, prm.t, rev)
+            else:
+                w = _pack_dev(self._entries.t().contiguous(), prm.k, prm.t, rev).t().contiguous()
+            self._words = N.to_host(w, np.uint64) if self._host else w
+        return self._words
 
     @property
     def packed_shape(self) -> tuple:
         return tuple(self.words.shape)
+
+    def __repr__(self) -> str:
+        return (f"CompressedMatrix(params={self.params}, orientation={self.orientation!r}, "
+                f"digit_order={self.digit_order!r}, logical_shape={self.logical_shape})")
 
 
 def _entries(m, p: int):
@@ -85,12 +107,8 @@ def compress_rows(a, params: PackingParams, digit_order: str = FORWARD) -> Compr
     a = _entries(a, params.p)
     if params.t is None:
         raise ParamsViolation("compressed matrices need a binary radix")
-    da = _as_u8(a, params.p)
-    words = _pack_dev(da, params.k, params.t, digit_order == REVERSED)
-    host = not N.is_tensor(a)
-    return CompressedMatrix(words=N.to_host(words, np.uint64) if host else words, params=params,
-                            orientation=ROWS, digit_order=digit_order, logical_shape=tuple(a.shape),
-                            _entries=da)
+    return CompressedMatrix(None, params, ROWS, digit_order, tuple(a.shape), _entries=_as_u8(a, params.p),
+                            _host=not N.is_tensor(a))
 
 
 def compress_cols(b, params: PackingParams, digit_order: str = FORWARD) -> CompressedMatrix:
@@ -98,12 +116,8 @@ def compress_cols(b, params: PackingParams, digit_order: str = FORWARD) -> Compr
     b = _entries(b, params.p)
     if params.t is None:
         raise ParamsViolation("compressed matrices need a binary radix")
-    db = _as_u8(b, params.p)
-    words = _pack_dev(db.t().contiguous(), params.k, params.t, digit_order == REVERSED).t().contiguous()
-    host = not N.is_tensor(b)
-    return CompressedMatrix(words=N.to_host(words, np.uint64) if host else words, params=params,
-                            orientation=COLS, digit_order=digit_order, logical_shape=tuple(b.shape),
-                            _entries=db)
+    return CompressedMatrix(None, params, COLS, digit_order, tuple(b.shape), _entries=_as_u8(b, params.p),
+                            _host=not N.is_tensor(b))
 
 
 def _unpack_dev(words, rows: int, cols: int, k: int, t: int, reverse: bool):
@@ -155,11 +169,10 @@ def _right_cmm_raw(da, db, p: int, t: int, d: int, engine: str, out=None):
     eng = N.ENGINES[engine]
     ws_bytes = N.lib().qadic_right_cmm_workspace(m, kd, n, d, eng)
     ws = N.workspace(ws_bytes)
-    if out is None:
-        out = N.empty((m, n), np.uint8)
+    dev = N.out_buffer(out, (m, n), np.uint8)
     N.check(N.lib().qadic_right_cmm_u8(N.ptr(da), N.ptr(db), m, kd, n, p, t, d, eng, N.ptr(ws), ws_bytes,
-                                       N.ptr(out), N.stream_ptr()), DimensionMismatch)
-    return out
+                                       N.ptr(dev), N.stream_ptr()), DimensionMismatch)
+    return dev
 
 
 def right_cmm(a, cb: CompressedMatrix, params: Optional[PackingParams] = None, keep_packed: bool = False,
@@ -179,6 +192,8 @@ def right_cmm(a, cb: CompressedMatrix, params: Optional[PackingParams] = None, k
     da = _as_u8(a, params.p)
     db = cb._entries if cb._entries is not None else _unpack_dev(cb.words, k_dim, n, params.k, params.t, False)
     c = _right_cmm_raw(da, db, params.p, params.t, params.d, engine, out=out)
+    if out is not None:
+        return N.finish(c, out, host, np.uint8)
     if keep_packed:
         words = _pack_dev(c, params.k, params.t, False)
         return CompressedMatrix(words=N.to_host(words, np.uint64) if host else words, params=params,

@@ -249,9 +249,11 @@ int qadic_polymul_batch_u8(const uint8_t* a, const uint8_t* b, int64_t n, int32_
     cudaStream_t s = (cudaStream_t)stream;
     const bool aligned = ((uintptr_t)a % 16 == 0) && ((uintptr_t)b % 16 == 0) && ((uintptr_t)out % 16 == 0);
     if (k == 4 && aligned && 3 * t + 8 <= 32) {  // pack4 keeps words in 32 bits
-        polymul_k4_kernel<<<(unsigned)((n + PM_PAIRS - 1) / PM_PAIRS), PM_THREADS, 0, s>>>(a, b, n, c, out);
+        QADIC_TIMED("polymul_k4", s,
+                    polymul_k4_kernel<<<(unsigned)((n + PM_PAIRS - 1) / PM_PAIRS), PM_THREADS, 0, s>>>(a, b, n, c, out));
     } else {
-        polymul_generic_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, b, n, k, c, out);
+        QADIC_TIMED("polymul_generic", s,
+                    polymul_generic_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, b, n, k, c, out));
     }
     return check_launch("polymul_batch_u8");
 }
@@ -267,12 +269,14 @@ int qadic_gf_dot_batch_u8(const qadic_field_desc* fd, const uint8_t* v1, const u
                   "length %lld exceeds the digit capacity of q=2**%u", (long long)len, f.t);
     if (batch == 0) return QADIC_OK;
     cudaStream_t s = (cudaStream_t)stream;
+    const int pi = prof_begin(s, "gf_dot");
     switch (f.k) {
         case 1: launch_gf_dot<1>(v1, v2, batch, len, f, out, s); break;
         case 2: launch_gf_dot<2>(v1, v2, batch, len, f, out, s); break;
         case 3: launch_gf_dot<3>(v1, v2, batch, len, f, out, s); break;
         default: launch_gf_dot<4>(v1, v2, batch, len, f, out, s); break;
     }
+    prof_end(pi, s);
     return check_launch("gf_dot_batch_u8");
 }
 

@@ -242,15 +242,9 @@ static int launch(const Params& prm, const FieldConst& f, cudaStream_t s) {
     const size_t smem = PIPE_BYTES + (smem_tables ? 2 * TABLE_MAX * sizeof(uint32_t) : 0);
     dim3 grid((unsigned)(prm.Np / BN), (unsigned)((prm.M + BM - 1) / BM));
     QADIC_REQUIRE(grid.y <= 65535, QADIC_ERR_UNSUPPORTED, "m too large");
-    if (smem_tables) {
-        auto kern = dmma_gemm_kernel<K, EPI, true>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<grid, THREADS, smem, s>>>(prm, f);
-    } else {
-        auto kern = dmma_gemm_kernel<K, EPI, false>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<grid, THREADS, smem, s>>>(prm, f);
-    }
+    auto kern = smem_tables ? dmma_gemm_kernel<K, EPI, true> : dmma_gemm_kernel<K, EPI, false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    QADIC_TIMED("f64 dmma gemm", s, kern<<<grid, THREADS, smem, s>>>(prm, f));
     return check_launch("f64 dmma gemm");
 }
 
@@ -276,10 +270,10 @@ int f64_gf_matmul(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64
     QADIC_REQUIRE(ws && ws_bytes >= f64_gf_workspace(m, kdim, n), QADIC_ERR_VALUE, "workspace too small");
     double* aw = static_cast<double*>(ws);
     double* bw = aw + Mp * Kp;
-    pack_gf_kernel<<<(unsigned)((Mp * Kp + 255) / 256), 256, 0, s>>>(a, m, kdim, (int)f.k, (int)f.t, aw, Mp, Kp);
+    QADIC_TIMED("f64 pack A", s, pack_gf_kernel<<<(unsigned)((Mp * Kp + 255) / 256), 256, 0, s>>>(a, m, kdim, (int)f.k, (int)f.t, aw, Mp, Kp));
     int rc = check_launch("f64 pack A");
     if (rc) return rc;
-    pack_gf_kernel<<<(unsigned)((Kp * Np + 255) / 256), 256, 0, s>>>(b, kdim, n, (int)f.k, (int)f.t, bw, Kp, Np);
+    QADIC_TIMED("f64 pack B", s, pack_gf_kernel<<<(unsigned)((Kp * Np + 255) / 256), 256, 0, s>>>(b, kdim, n, (int)f.k, (int)f.t, bw, Kp, Np));
     rc = check_launch("f64 pack B");
     if (rc) return rc;
     Params prm;
@@ -310,10 +304,10 @@ int f64_right_cmm(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, i
     QADIC_REQUIRE(ws && ws_bytes >= f64_cmm_workspace(m, kdim, n, d), QADIC_ERR_VALUE, "workspace too small");
     double* aw = static_cast<double*>(ws);
     double* bw = aw + Mp * Kp;
-    pack_rows_f64_kernel<<<(unsigned)((Mp * Kp + 255) / 256), 256, 0, s>>>(a, m, kdim, 1, t, aw, Mp, Kp);
+    QADIC_TIMED("f64 pack A", s, pack_rows_f64_kernel<<<(unsigned)((Mp * Kp + 255) / 256), 256, 0, s>>>(a, m, kdim, 1, t, aw, Mp, Kp));
     int rc = check_launch("f64 pack A");
     if (rc) return rc;
-    pack_rows_f64_kernel<<<(unsigned)((Kp * Np + 255) / 256), 256, 0, s>>>(b, kdim, n, g, t, bw, Kp, Np);
+    QADIC_TIMED("f64 pack B", s, pack_rows_f64_kernel<<<(unsigned)((Kp * Np + 255) / 256), 256, 0, s>>>(b, kdim, n, g, t, bw, Kp, Np));
     rc = check_launch("f64 pack B");
     if (rc) return rc;
     FieldConst f = {};

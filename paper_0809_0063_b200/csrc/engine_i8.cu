@@ -241,6 +241,108 @@ __global__ void __launch_bounds__(256) expand_b_kernel(const uint8_t* __restrict
     }
 }
 
+// Table-driven expansion (fields with p^K <= XT_CODES): every element code
+// maps to its K x K block, staged in shared memory as K rows of K bytes
+// (T[code*K + l] = bytes i=0..K-1 of output row l).  Tile = 64 kk x 128 j:
+// b rows are read with 16-byte loads, codes are stored j-major so that an
+// output row segment of 16 consecutive kk (16K bytes, K 16-byte stores) is
+// one contiguous smem read.  Grid-stride over tiles amortises the table.
+constexpr int XT_KK = 64, XT_J = 64, XT_CODES = 1024;
+
+template <int K>
+__global__ void __launch_bounds__(256) expand_b_table_kernel(const uint8_t* __restrict__ b, int64_t Kd, int64_t N,
+                                                             FieldConst f, uint8_t* __restrict__ bx, int64_t ldb,
+                                                             int tiles_kk, int tiles_j) {
+    __shared__ uint32_t tab[XT_CODES * K];
+    __shared__ __align__(16) uint8_t raw[XT_KK][XT_J * K + 16];
+    __shared__ __align__(16) uint16_t code[XT_J][XT_KK + 8];
+    const uint32_t p = f.p;
+    int ncodes = 1;
+    for (int s = 0; s < K; ++s) ncodes *= (int)p;
+    // block table: T[c, l] packs coeff_l(X^i * c(X) mod f), i = 0..K-1
+    for (int e = threadIdx.x; e < ncodes * K; e += blockDim.x) {
+        const int c = e / K, l = e % K;
+        uint32_t dig[K];
+        int r = c;
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+            dig[s] = (uint32_t)(r % (int)p);
+            r /= (int)p;
+        }
+        uint32_t w = 0;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            uint32_t acc = 0;
+#pragma unroll
+            for (int s = 0; s < K; ++s) acc += dig[s] * f.xpow[s + i][l];
+            w |= mod_small(acc, p, f.magic) << (8 * i);
+        }
+        tab[e] = w;
+    }
+    const bool vec_rows = ((N * K) % 16 == 0) && ((reinterpret_cast<uintptr_t>(b) & 15) == 0);
+    const int64_t ntiles = (int64_t)tiles_kk * tiles_j;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t kk0 = (tile % tiles_kk) * XT_KK, j0 = (tile / tiles_kk) * XT_J;
+        __syncthreads();  // previous tile's smem fully consumed (and table ready)
+        // phase 1: raw coefficient tile
+        constexpr int ROWB = XT_J * K;
+        if (vec_rows && j0 + XT_J <= N) {
+            for (int i = threadIdx.x; i < XT_KK * (ROWB / 16); i += blockDim.x) {
+                const int r = i / (ROWB / 16), q = i % (ROWB / 16);
+                const int64_t gk = kk0 + r;
+                uint4 v = make_uint4(0, 0, 0, 0);
+                if (gk < Kd) v = __ldg(reinterpret_cast<const uint4*>(b + gk * N * K + j0 * K) + q);
+                *reinterpret_cast<uint4*>(&raw[r][q * 16]) = v;
+            }
+        } else {
+            for (int i = threadIdx.x; i < XT_KK * ROWB; i += blockDim.x) {
+                const int r = i / ROWB, c = i % ROWB;
+                const int64_t gk = kk0 + r, gj = j0 + c / K;
+                raw[r][c] = (gk < Kd && gj < N) ? b[gk * N * K + j0 * K + c] : 0;
+            }
+        }
+        __syncthreads();
+        // phase 2: element codes, transposed to j-major
+        for (int i = threadIdx.x; i < XT_KK * XT_J; i += blockDim.x) {
+            const int r = i / XT_J, jl = i % XT_J;
+            uint32_t cd = 0;
+#pragma unroll
+            for (int s = K - 1; s >= 0; --s) cd = cd * p + raw[r][jl * K + s];
+            code[jl][r] = (uint16_t)cd;
+        }
+        __syncthreads();
+        // phase 3: output rows (j, l), 16 kk per work item -> K 16-byte stores
+        for (int i = threadIdx.x; i < XT_J * K * (XT_KK / 16); i += blockDim.x) {
+            const int ch = i % (XT_KK / 16), row = i / (XT_KK / 16);
+            const int jl = row / K, l = row % K;
+            const int64_t gj = j0 + jl;
+            if (gj >= N) continue;
+            uint32_t w[4 * K];
+#pragma unroll
+            for (int q = 0; q < 4 * K; ++q) w[q] = 0;
+            const uint16_t* cr = &code[jl][ch * 16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const uint32_t v = tab[cr[e] * K + l];
+#pragma unroll
+                for (int ii = 0; ii < K; ++ii) {
+                    const int pos = e * K + ii;
+                    w[pos / 4] |= ((v >> (8 * ii)) & 0xFF) << (8 * (pos % 4));
+                }
+            }
+            const int64_t col = (kk0 + ch * 16) * K;
+            uint8_t* dst = bx + (gj * K + l) * ldb + col;
+            if (col + 16 * K <= ldb) {
+#pragma unroll
+                for (int q = 0; q < K; ++q)
+                    reinterpret_cast<uint4*>(dst)[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+            } else {
+                for (int e = 0; e < 16 * K && col + e < ldb; ++e) dst[e] = (uint8_t)(w[e / 4] >> (8 * (e % 4)));
+            }
+        }
+    }
+}
+
 // rows of width `width` bytes copied into a pitched, zero-padded buffer
 __global__ void pad_rows_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t width, uint8_t* __restrict__ dst,
                                 int64_t ld) {
@@ -327,15 +429,29 @@ static int run(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t 
     if (L.pad_a) {
         uint8_t* ap = bx + L.bx_bytes;
         const int64_t tot = m * L.lda;
-        pad_rows_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(a, m, L.Kb, ap, L.lda);
+        QADIC_TIMED("i8 pad A", s, pad_rows_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(a, m, L.Kb, ap, L.lda));
         int rc = check_launch("i8 pad A");
         if (rc) return rc;
         a_op = ap;
     }
     {
-        dim3 grid((unsigned)((kdim + EX_T - 1) / EX_T), (unsigned)((n + EX_T - 1) / EX_T));
-        QADIC_REQUIRE(grid.y <= 65535, QADIC_ERR_UNSUPPORTED, "n too large");
-        expand_b_kernel<<<grid, 256, 0, s>>>(b, kdim, n, f, bx, L.ldb);
+        int ncodes = 1;
+        for (int s2 = 0; s2 < k; ++s2) ncodes *= (int)f.p;
+        if (ncodes <= XT_CODES) {
+            const int tk = (int)((kdim + XT_KK - 1) / XT_KK), tj = (int)((n + XT_J - 1) / XT_J);
+            const int64_t tiles = (int64_t)tk * tj;
+            const int grid = (int)(tiles < 4 * num_sms() ? tiles : 4 * num_sms());
+            switch (k) {
+                case 1: QADIC_TIMED("i8 expand B", s, expand_b_table_kernel<1><<<grid, 256, 0, s>>>(b, kdim, n, f, bx, L.ldb, tk, tj)); break;
+                case 2: QADIC_TIMED("i8 expand B", s, expand_b_table_kernel<2><<<grid, 256, 0, s>>>(b, kdim, n, f, bx, L.ldb, tk, tj)); break;
+                case 3: QADIC_TIMED("i8 expand B", s, expand_b_table_kernel<3><<<grid, 256, 0, s>>>(b, kdim, n, f, bx, L.ldb, tk, tj)); break;
+                default: QADIC_TIMED("i8 expand B", s, expand_b_table_kernel<4><<<grid, 256, 0, s>>>(b, kdim, n, f, bx, L.ldb, tk, tj)); break;
+            }
+        } else {
+            dim3 grid((unsigned)((kdim + EX_T - 1) / EX_T), (unsigned)((n + EX_T - 1) / EX_T));
+            QADIC_REQUIRE(grid.y <= 65535, QADIC_ERR_UNSUPPORTED, "n too large");
+            QADIC_TIMED("i8 expand B", s, expand_b_kernel<<<grid, 256, 0, s>>>(b, kdim, n, f, bx, L.ldb));
+        }
         int rc = check_launch("i8 expand B");
         if (rc) return rc;
     }
@@ -362,7 +478,7 @@ static int run(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t 
     }
     const int tiles = prm.m_tiles * prm.n_tiles;
     const int grid = tiles < num_sms() ? tiles : num_sms();
-    gemm_u8_modp_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb, prm);
+    QADIC_TIMED("i8 gemm", s, gemm_u8_modp_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(ta, tb, prm));
     return check_launch("i8 gemm");
 }
 

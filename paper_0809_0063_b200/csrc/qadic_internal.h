@@ -17,5 +17,15 @@ double host_case2_bound();
 void set_error(int code, const char* fmt, ...);
 int check_launch(const char* what);
 void count_launch(int n = 1);
+int prof_begin(cudaStream_t s, const char* name);
+void prof_end(int idx, cudaStream_t s);
 
 }  // namespace qadic
+
+// launch a kernel bracketed by the (optional) per-kernel event timer
+#define QADIC_TIMED(name, stream, ...)                          \
+    do {                                                        \
+        int _qadic_pi = ::qadic::prof_begin((stream), (name));  \
+        __VA_ARGS__;                                            \
+        ::qadic::prof_end(_qadic_pi, (stream));                 \
+    } while (0)

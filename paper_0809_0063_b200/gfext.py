@@ -301,11 +301,10 @@ class GFqField:
             raise DimensionMismatch(f"operands must both be [B, n, {self.k}]")
         b, n = d1.shape[0], d1.shape[1]
         self._check_len(n)
-        if out is None:
-            out = N.empty((b, self.k), np.uint8)
-        N.check(N.lib().qadic_gf_dot_batch_u8(self.field_desc(), N.ptr(d1), N.ptr(d2), b, n, N.ptr(out),
+        dev = N.out_buffer(out, (b, self.k), np.uint8)
+        N.check(N.lib().qadic_gf_dot_batch_u8(self.field_desc(), N.ptr(d1), N.ptr(d2), b, n, N.ptr(dev),
                                               N.stream_ptr()), DimensionMismatch)
-        return N.to_host(out, np.uint8) if (h1 or h2) else out
+        return N.finish(dev, out, h1 or h2, np.uint8)
 
     def _lh_lookup(self, u: Sequence[int], stats=None):
         bb = self.u_bits
@@ -364,11 +363,10 @@ class GFqField:
         desc = self.field_desc()
         ws_bytes = N.lib().qadic_gf_matmul_workspace(desc, m, kd, n, eng)
         ws = N.workspace(ws_bytes)
-        if out is None:
-            out = N.empty((m, n, self.k), np.uint8)
+        dev = N.out_buffer(out, (m, n, self.k), np.uint8)
         N.check(N.lib().qadic_gf_matmul_u8(desc, N.ptr(da), N.ptr(db), m, kd, n, eng, fold, N.ptr(ws), ws_bytes,
-                                           N.ptr(out), N.stream_ptr()), DimensionMismatch)
-        return N.to_host(out, np.uint8) if (ha or hb) else out
+                                           N.ptr(dev), N.stream_ptr()), DimensionMismatch)
+        return N.finish(dev, out, ha or hb, np.uint8)
 
     def _add_indices(self, ia: np.ndarray, ib: np.ndarray) -> np.ndarray:
         """Field addition of handle arrays through coefficient codes."""

@@ -1,0 +1,151 @@
+"""CPU-only checks: the C-ABI library loads and exports every symbol of
+include/qadic_b200.h (no compute call without a GPU), the host control
+plane (parameters, field construction, tables) matches the reference's
+golden vectors, and the product path refuses to run without CUDA."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_0809_0063_b200 as Q
+from paper_0809_0063_b200 import _native as N, gfext, params, redq, dqt, fdiv
+from paper_0809_0063_b200 import workloads as W
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+class TestABI:
+    def test_library_loads(self):
+        lib = N.load_library()
+        assert lib.qadic_abi_version() == 1
+        assert N.launch_count() >= 0
+
+    def test_every_header_symbol_exported(self):
+        with open(os.path.join(ROOT, "include", "qadic_b200.h")) as fh:
+            hdr = fh.read()
+        declared = set(re.findall(r"QADIC_API\s+[\w\s\*]+?\b(qadic_\w+)\s*\(", hdr))
+        assert len(declared) >= 20
+        lib = N.load_library()
+        for name in declared:
+            assert hasattr(lib, name), name
+        assert set(N.EXPORTED) <= declared
+
+    def test_error_path_without_device(self):
+        """Argument validation runs before any CUDA call."""
+        lib = N.load_library()
+        rc = lib.qadic_redq_compress_u64(None, 4, 3, 16, 4, None, None)  # d*t = 64
+        assert rc == N.ERR_VALUE
+        assert b"64-bit" in lib.qadic_last_error()
+        with pytest.raises(ValueError):
+            N.check(rc)
+
+    def test_no_cpu_fallback(self):
+        import torch
+
+        if torch.cuda.is_available():
+            pytest.skip("device present")
+        with pytest.raises(RuntimeError, match="CUDA"):
+            Q.polymul.polymul_fqt_batch(np.zeros((4, 4), np.uint8), np.zeros((4, 4), np.uint8),
+                                        params.dqt_params(3, 1, 4))
+        with pytest.raises(RuntimeError, match="CUDA"):
+            Q._kernels.matmul_exact_u64(np.zeros((2, 2), np.uint64), np.zeros((2, 2), np.uint64))
+
+
+class TestParams:
+    def test_config_params(self, golden_scalars):
+        P = golden_scalars["params"]
+
+        def tup(x):
+            return [x.p, x.t, x.d, x.n_max]
+
+        for cfg in (1, 2, 3, 4, 5):
+            assert tup(W.params_for(W.CONFIGS[cfg])) == P[f"cfg{cfg}"]
+        for n, v in P["cmm_table"].items():
+            assert tup(params.cmm_params(3, int(n))) == v
+
+    def test_chunk_budget(self, golden_scalars):
+        prm = W.params_for(W.CONFIGS[5])
+        assert params.chunk_budget(prm, 6, 6) == golden_scalars["cfg5_chunk"] == 9
+        f = W.field_for(W.CONFIGS[5])
+        assert f.max_fold_period() == 8
+
+    def test_bounds(self):
+        with pytest.raises(Q.Infeasible):
+            params.dqt_params(7, n=8192, k=3)  # the reason cfg5 folds
+        prm = params.cmm_params(3, 16384, strict=True)
+        prm.check_middle_product_bounds(16384)
+        assert prm.delayed_sum(16384) < 1 << 53
+        with pytest.raises(Q.ParamsViolation):
+            params.cmm_params(3, 16).check_middle_product_bounds(16)
+        with pytest.raises(ValueError):
+            params.PackingParams(p=4, q=8, d=1)
+
+    def test_fdiv_constants(self, golden_scalars):
+        assert fdiv.case2_bound() == golden_scalars["fdiv_bound_nearest"]
+        assert fdiv.native_reciprocal(3, fdiv.UP).hex() == golden_scalars["fdiv_invp3_up"]
+        assert fdiv.native_reciprocal(7, fdiv.UP).hex() == golden_scalars["fdiv_invp7_up"]
+        rng = np.random.default_rng(1)
+        for r in rng.integers(0, 1 << 53, 3000).tolist():
+            assert fdiv.applied_fdiv(r, 7) == r // 7
+
+
+class TestFields:
+    @pytest.mark.parametrize("name", ["gf9_64", "gf9_8192", "gf343_9", "gf9_auto", "gf25_20", "gf27_20",
+                                      "gf11_64", "gf4_2"])
+    def test_tables_match_reference(self, golden, golden_scalars, name):
+        s = golden_scalars[f"field_{name}"]
+        irr = None if name == "gf9_auto" else s["irreducible"]
+        f = gfext.build_field(s["p"], s["k"], irreducible=irr, max_dot_length=s["n_max"])
+        assert list(f.irreducible) == s["irreducible"]
+        assert f.generator_code == s["generator_code"]
+        for tab in ("code_of_index", "index_of_code", "pack_table", "l_table", "h_table", "zech"):
+            assert np.array_equal(np.asarray(getattr(f, tab)), golden[f"field_{name}_{tab}"]), tab
+
+    def test_scalar_ops(self):
+        f = gfext.build_field(3, 2, irreducible=[1, 0, 1], max_dot_length=8)
+        for i in range(9):
+            a = f.elem(i)
+            assert f.add(a, f.neg(a)).index == 0
+            if i:
+                assert f.mul(a, f.inv(a)).index == 1
+        with pytest.raises(Q.NotIrreducible):
+            gfext.build_field(3, 2, irreducible=[1, 2, 1])
+        with pytest.raises(Q.TooLarge):
+            gfext.build_field(2, 23)
+
+
+class TestScalarRedq:
+    def test_worked_examples(self, golden_scalars):
+        u = redq.redq_compress(40013002800270018, 5, 10**4, 4)
+        assert list(u.u) == golden_scalars["we_u1"]
+        u2 = redq.redq_compress(1234005678009123004567, 23, 10**6, 3)
+        assert list(u2.u) == golden_scalars["we_u2"]
+        assert redq.redq_correct(u2, 23, 10**6) == golden_scalars["we_mu2"]
+        assert redq.reduce_digits(7, 11, 1 << 10, 2) == golden_scalars["we_small"]
+        prm = params.PackingParams(p=5, q=1 << 16, d=2)
+        assert dqt.pack([3, 2, 1], prm).value == golden_scalars["we_pack321"]
+
+    def test_paired_op_count(self):
+        """ceil((k+1)/2) wide multiply-subtracts (reference verify.py:114-130)."""
+        rng = np.random.default_rng(3)
+        for k in range(2, 9):
+            t = 53 // k
+            for p in (3, 5, 7):
+                for r in rng.integers(0, (1 << t) ** k, 20).tolist():
+                    st = redq.CompressionStats()
+                    u = redq.redq_compress(r, p, 1 << t, k - 1, stats=st)
+                    assert st.wide_mul_sub == (k + 2) // 2
+                    assert list(u.u) == [(r >> (i * t)) % p for i in range(k)]
+
+    def test_tabulated_equals_direct(self):
+        for p in (2, 3, 5, 7):
+            for q in (1 << 4, 1 << 13, 10**6):
+                for j in (1, 2):
+                    for idx in (redq.BASE_P, redq.BINARY_BLOCKS):
+                        tab = redq.build_correction_table(p, q, j, idx)
+                        for d in (1, 2, 3):
+                            for code in range(p ** (d + 1)):
+                                u = redq.CompressedDigits(tuple((code // p ** i) % p for i in range(d + 1)))
+                                assert redq.correct_tabulated(u, tab) == redq.redq_correct(u, p, q)
