@@ -1,0 +1,86 @@
+"""World-size-2 gloo tests (CPU) of the multi-GPU partitioning: row blocks
+of A, B broadcast once from rank 0, no reduction; batch sharding for the
+batched configs.  The compute is the CPU oracle here (the CUDA engine on
+the GPU box)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_0809_0063_b200 import shard
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, kind, result_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import qadic_oracle as O
+        from paper_0809_0063_b200 import workloads as W
+
+        if kind == "gf":
+            c = W.CONFIGS[5]
+            x = W.make_inputs(c, (37, 50, 23))  # ragged: 37 rows over 2 ranks
+            f = O.build_field(7, 3, irreducible=[5, 0, 0, 1], max_dot_length=9)
+            s0, s1 = shard.row_block(37, world, rank)
+            a_rows = torch.from_numpy(x["a"][s0:s1])
+            b = torch.from_numpy(x["b"].copy()) if rank == 0 else torch.zeros(x["b"].shape, dtype=torch.uint8)
+            c_rows = shard.sharded_matmul(
+                a_rows, b, lambda ar, bb: torch.from_numpy(O.gf_matmul_folded(f, ar.numpy(), bb.numpy(), 9)))
+            ok_b = torch.equal(b, torch.from_numpy(x["b"]))
+            full = O.gf_matmul_planes(f, x["a"], x["b"])
+            ok = ok_b and np.array_equal(c_rows.numpy(), full[s0:s1])
+        elif kind == "cmm":
+            c = W.CONFIGS[4]
+            a = W.make_inputs(c, (64,))["a"]
+            s0, s1 = shard.row_block(64, world, rank)
+            full_t = torch.from_numpy(a.copy()) if rank == 0 else torch.zeros(a.shape, dtype=torch.uint8)
+            shard.broadcast_once(full_t)
+            rows = full_t[s0:s1]
+            c_rows = torch.from_numpy(O.right_cmm(rows.numpy(), full_t.numpy(), 3, 17, 2))
+            gathered = shard.gather_rows(c_rows)
+            ok = np.array_equal(gathered.numpy(), O.modmatmul_planes(a, a, 3))
+        else:  # batch sharding, no collective
+            c = W.CONFIGS[1]
+            x = W.make_inputs(c, (1001,))
+            s0, s1 = shard.row_block(1001, world, rank)
+            got = O.polymul_batch(x["a"][s0:s1], x["b"][s0:s1], 3, 5)
+            ok = np.array_equal(got, O.polymul_batch(x["a"], x["b"], 3, 5)[s0:s1])
+        result_q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind", ["gf", "cmm", "batch"])
+def test_world2(kind):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, kind, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}
+
+
+def test_row_block_partition():
+    for n in (1, 7, 8192, 16384, 37):
+        for w in (1, 2, 3, 4, 8):
+            spans = [shard.row_block(n, w, r) for r in range(w)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(w - 1))
+            assert max(b - a for a, b in spans) - min(b - a for a, b in spans) <= 1
