@@ -295,6 +295,15 @@ def roofline(cfg, engine, kname, kstats, work, peaks, peak_src):
                 "avg_launch_ms": round(avg_s * 1e3, 4), "algorithmic_ops_per_launch": ops, "peak_source": src,
                 "cublas_int8_measured_tops": round(peaks["int8_tops"], 1) if peaks.get("int8_tops") else None,
                 "two_x_measured_bf16_tops": round(2 * peaks["bf16_tflops"], 1)}
+    if kname == "fp4 gemm":
+        ops = 2 * work["i8_macs"]  # same plane MAC count, E2M1 operands
+        achieved = ops / avg_s / 1e12
+        peak = 9000.0
+        return {"bound": "tensor", "kernel": kname, "achieved": round(achieved, 1), "peak": peak,
+                "unit": "TOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+                "avg_launch_ms": round(avg_s * 1e3, 4), "algorithmic_ops_per_launch": ops,
+                "peak_source": "fallback nominal dense fp4 9 PFLOP/s (B200_PROFILING.md); no measured fp4 peak",
+                "cublas_int8_measured_tops": round(peaks["int8_tops"], 1) if peaks.get("int8_tops") else None}
     if kname == "f64 dmma gemm":
         ops = 2 * work["f64_fmas"]
         achieved = ops / avg_s / 1e12

@@ -38,9 +38,10 @@ typedef enum qadic_status {
 } qadic_status;
 
 typedef enum qadic_engine {
-    QADIC_ENGINE_AUTO = 0,     /* the measured-faster exact engine (tcgen05 INT8 planes) */
+    QADIC_ENGINE_AUTO = 0,     /* the measured-fastest exact engine: F4_TC when valid, else I8_TC */
     QADIC_ENGINE_I8_TC = 1,    /* tcgen05.mma kind::i8 on coefficient planes, int32 TMEM accumulators */
-    QADIC_ENGINE_F64_DMMA = 2  /* the paper's formulation: DQT-packed FP64 words on DMMA tensor cores */
+    QADIC_ENGINE_F64_DMMA = 2, /* the paper's formulation: DQT-packed FP64 words on DMMA tensor cores */
+    QADIC_ENGINE_F4_TC = 3     /* tcgen05.mma kind::mxf4 (E2M1, unit block scales) on centred residues, p <= 7 */
 } qadic_engine;
 
 QADIC_API int qadic_abi_version(void);
@@ -136,7 +137,8 @@ QADIC_API int qadic_gf_matmul_u8(const qadic_field_desc *f, const uint8_t *a, co
 /* cfg4 -- C[m,n] = A[m,kdim] @ B[kdim,n] mod p with B row-compressed d+1
  * entries per word at radix 2^t (cmm.right_cmm(a, compress_rows(b)),
  * cmm.py:244-276, 97-110).  uint8 I/O. */
-QADIC_API size_t qadic_right_cmm_workspace(int64_t m, int64_t kdim, int64_t n, int32_t d, int32_t engine);
+QADIC_API size_t qadic_right_cmm_workspace(int64_t m, int64_t kdim, int64_t n, int64_t p, int32_t d,
+                                           int32_t engine);
 QADIC_API int qadic_right_cmm_u8(const uint8_t *a, const uint8_t *b, int64_t m, int64_t kdim, int64_t n,
                        int64_t p, int32_t t, int32_t d, int32_t engine, void *workspace,
                        size_t workspace_bytes, uint8_t *c, void *stream);

@@ -20,8 +20,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libqadic_b200.so")
 
 QADIC_OK, ERR_SHAPE, ERR_PARAMS, ERR_VALUE, ERR_CUDA, ERR_UNSUPPORTED = range(6)
-ENGINE_AUTO, ENGINE_I8_TC, ENGINE_F64_DMMA = 0, 1, 2
-ENGINES = {"auto": ENGINE_AUTO, "i8": ENGINE_I8_TC, "f64": ENGINE_F64_DMMA}
+ENGINE_AUTO, ENGINE_I8_TC, ENGINE_F64_DMMA, ENGINE_F4_TC = 0, 1, 2, 3
+ENGINES = {"auto": ENGINE_AUTO, "i8": ENGINE_I8_TC, "f64": ENGINE_F64_DMMA, "fp4": ENGINE_F4_TC}
 
 P = ctypes.c_void_p
 I64 = ctypes.c_int64
@@ -59,7 +59,7 @@ _SIGNATURES = {
     "qadic_gf_matmul_workspace": ([ctypes.POINTER(FieldDesc), I64, I64, I64, I32], SZ),
     "qadic_gf_matmul_u8": ([ctypes.POINTER(FieldDesc), P, P, I64, I64, I64, I32, I32, P, SZ, P, P],
                            ctypes.c_int),
-    "qadic_right_cmm_workspace": ([I64, I64, I64, I32, I32], SZ),
+    "qadic_right_cmm_workspace": ([I64, I64, I64, I64, I32, I32], SZ),
     "qadic_right_cmm_u8": ([P, P, I64, I64, I64, I64, I32, I32, I32, P, SZ, P, P], ctypes.c_int),
     "qadic_polymul_batch_u8": ([P, P, I64, I32, I64, I32, P, P], ctypes.c_int),
     "qadic_gather_u8": ([P, I64, P, I64, I32, P, P], ctypes.c_int),

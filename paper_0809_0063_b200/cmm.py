@@ -167,7 +167,7 @@ def _right_cmm_raw(da, db, p: int, t: int, d: int, engine: str, out=None):
     m, kd = da.shape
     n = db.shape[1]
     eng = N.ENGINES[engine]
-    ws_bytes = N.lib().qadic_right_cmm_workspace(m, kd, n, d, eng)
+    ws_bytes = N.lib().qadic_right_cmm_workspace(m, kd, n, p, d, eng)
     ws = N.workspace(ws_bytes)
     dev = N.out_buffer(out, (m, n), np.uint8)
     N.check(N.lib().qadic_right_cmm_u8(N.ptr(da), N.ptr(db), m, kd, n, p, t, d, eng, N.ptr(ws), ws_bytes,

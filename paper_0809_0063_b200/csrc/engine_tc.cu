@@ -1,0 +1,677 @@
+// Tensor-core engines (tcgen05) for exact GF(p^k) / F_p matrix products.
+//
+// Coefficient-plane formulation of the paper's delayed reduction
+// (PAPER.md:216-223 applied to GFqField.matmul, src/gfext.py:311-345, and
+// cmm.right_cmm, src/cmm.py:244-276):
+//
+//   C[m, (j,l)] = sum_{kk,i} A[m, (kk,i)] * Bx[(j,l), (kk,i)]   (mod p)
+//   Bx[(j,l), (kk,i)] = coefficient l of  X^i * b[kk,j](X)  mod (f, p)
+//
+// Every B entry is expanded once into its k x k multiplication matrix over
+// F_p with the X^k fold applied (rows X^i mod f, src/gfext.py:200-205).
+// A needs no transformation for the INT8 kind: the row-major uint8[M, K, k]
+// coefficient tensor IS the K-major A operand.  The delayed sum is exact in
+// the accumulator, so the epilogue is a single `mod p` per output.
+//
+// Two operand kinds share one persistent warp-specialised kernel:
+//   KIND_I8  tcgen05.mma.kind::i8, unsigned residues 0..p-1, s32 accumulate;
+//            exact while K*k*(p-1)^2 < 2^31 (any p <= 127).
+//   KIND_F4  tcgen05.mma.kind::mxf4.block_scale (E2M1, two per byte, block
+//            scales fixed to 2^0) on CENTRED residues in [-(p-1)/2, (p-1)/2];
+//            every such integer for p <= 7 is an exact E2M1 value and the
+//            fp32 accumulator is exact while K*k*((p-1)/2)^2 < 2^24
+//            (cfg3: 16,384; cfg5: 221,184).  Twice the int8 MMA rate, half
+//            the operand bytes.
+//
+// Kernel roles: warp 0 TMA producer (128B-swizzled K-major tiles, 4-stage
+// mbarrier ring), warp 1 single-thread MMA issuer (M=128, K=128 bytes per
+// stage), warp 2 TMEM allocator, warps 4-7 epilogue (tcgen05.ld -> mod p ->
+// uint8) overlapping the next tile through two TMEM accumulators.
+#include <cuda.h>
+
+#include "qadic_common.cuh"
+#include "qadic_internal.h"
+#include "sm100_ptx.cuh"
+
+namespace qadic {
+
+int make_field_const(const qadic_field_desc* d, FieldConst* f);
+
+namespace tc {
+
+enum Kind { KIND_I8 = 0, KIND_F4 = 1 };
+
+constexpr int BM = 128, BK = 128;  // BK in bytes per stage (128 int8 / 256 fp4 elements)
+constexpr int STAGES = 4;
+constexpr int THREADS = 256;
+constexpr int GROUP_M = 16;
+
+template <int KIND>
+struct Cfg;
+template <>
+struct Cfg<KIND_I8> {
+    static constexpr int BN = 256;
+    static constexpr int SF_COL = -1;  // no scale factors
+};
+template <>
+struct Cfg<KIND_F4> {
+    static constexpr int BN = 240;      // 2 x 240 accumulator columns + 32 scale-factor columns = 512
+    static constexpr int SF_COL = 480;
+};
+
+template <int KIND>
+struct Geo {
+    static constexpr int BN = Cfg<KIND>::BN;
+    static constexpr int A_BYTES = BM * BK;
+    static constexpr int B_BYTES = BN * BK;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+struct Params {
+    int64_t M, N;        // output rows / cols (cols = n * k)
+    int64_t ldc;         // output row pitch (bytes)
+    uint32_t p;
+    uint32_t offset;     // multiple of p added before the unsigned mod (centred kinds)
+    uint64_t magic64;
+    int m_tiles, n_tiles, num_kb;
+    uint8_t* c;
+};
+
+__device__ __forceinline__ void tile_coords(int tile, int m_tiles, int n_tiles, int& mt, int& nt) {
+    const int per_group = GROUP_M * n_tiles;
+    const int group = tile / per_group;
+    const int first_m = group * GROUP_M;
+    const int gm = min(m_tiles - first_m, GROUP_M);
+    const int r = tile % per_group;
+    mt = first_m + r % gm;
+    nt = r / gm;
+}
+
+__host__ __device__ constexpr uint32_t idesc_mxf4(uint32_t m, uint32_t n) {
+    return (1u << 7)            // a_format = E2M1
+           | (1u << 10)         // b_format = E2M1
+           | ((n >> 3) << 17)   // N >> 3
+           | (1u << 23)         // scale format = UE8M0
+           | ((m >> 4) << 24);  // M >> 4   (k_size = 0: K = 64 per MMA)
+}
+
+__device__ __forceinline__ void umma_mxf4(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate, uint32_t tsfa, uint32_t tsfb) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(tsfa), "r"(tsfb));
+}
+
+__device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
+
+// every scale factor = 2^0 (UE8M0 0x7F): fill 32 TMEM columns of this warp's lanes
+__device__ __forceinline__ void tmem_fill_sf(uint32_t taddr) {
+    const uint32_t v = 0x7F7F7F7Fu;
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, "
+        "%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(taddr),
+        "r"(v)
+        : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_modp_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
+                     Params prm) {
+    using namespace sm100;
+    using G = Geo<KIND>;
+    constexpr int BN = G::BN;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * G::STAGE_BYTES);
+    uint64_t* empty_bar = full_bar + STAGES;
+    uint64_t* tmem_full = empty_bar + STAGES;
+    uint64_t* tmem_empty = tmem_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    const int num_tiles = prm.m_tiles * prm.n_tiles;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tmap_a);
+        tma_prefetch(&tmap_b);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tmem_full[a], 1);
+            mbar_init(&tmem_empty[a], 128);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) tmem_alloc<512>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    if (KIND == KIND_F4 && warp >= 4) {
+        tmem_fill_sf(tmem_base + ((uint32_t)((warp - 4) * 32) << 16) + Cfg<KIND>::SF_COL);
+        tc_fence_before();
+    }
+    __syncthreads();
+    tc_fence_after();
+
+    if (warp == 0) {
+        // ===== TMA producer =====
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+                int mt, nt;
+                tile_coords(tile, prm.m_tiles, prm.n_tiles, mt, nt);
+                for (int kb = 0; kb < prm.num_kb; ++kb) {
+                    mbar_wait(&empty_bar[stage], phase ^ 1);
+                    uint8_t* sa = smem + stage * G::STAGE_BYTES;
+                    uint8_t* sb = sa + G::A_BYTES;
+                    mbar_arrive_expect_tx(&full_bar[stage], G::STAGE_BYTES);
+                    tma_load_2d(sa, &tmap_a, &full_bar[stage], kb * BK, mt * BM);
+                    tma_load_2d(sb, &tmap_b, &full_bar[stage], kb * BK, nt * BN);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer: 4 MMAs of 32 bytes (K=32 int8 / K=64 fp4) per stage =====
+        constexpr uint32_t idesc = KIND == KIND_I8 ? idesc_u8_s32(BM, BN) : idesc_mxf4(BM, BN);
+        int stage = 0;
+        uint32_t phase = 0;
+        int local = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+            const int acc = local & 1;
+            const uint32_t acc_phase = (local >> 1) & 1;
+            mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+            tc_fence_after();
+            const uint32_t tmem_d = tmem_base + acc * BN;
+            for (int kb = 0; kb < prm.num_kb; ++kb) {
+                mbar_wait(&full_bar[stage], phase);
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint32_t sa = smem_addr(smem + stage * G::STAGE_BYTES);
+                    const uint32_t sb = sa + G::A_BYTES;
+#pragma unroll
+                    for (int k = 0; k < BK / 32; ++k) {
+                        const uint64_t ad = smem_desc_k_sw128(sa + k * 32), bd = smem_desc_k_sw128(sb + k * 32);
+                        if (KIND == KIND_I8) {
+                            umma_i8(tmem_d, ad, bd, idesc, (kb | k) != 0);
+                        } else {
+                            const uint32_t sf = tmem_base + Cfg<KIND>::SF_COL;
+                            umma_mxf4(tmem_d, ad, bd, idesc, (kb | k) != 0, sf, sf);
+                        }
+                    }
+                    umma_commit(&empty_bar[stage]);
+                    if (kb == prm.num_kb - 1) umma_commit(&tmem_full[acc]);
+                }
+                __syncwarp();
+                if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else if (warp >= 4) {
+        // ===== epilogue: TMEM -> registers -> mod p -> uint8 =====
+        const int ew = warp - 4;  // TMEM lane quarter this warp may access
+        int local = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+            int mt, nt;
+            tile_coords(tile, prm.m_tiles, prm.n_tiles, mt, nt);
+            const int acc = local & 1;
+            const uint32_t acc_phase = (local >> 1) & 1;
+            mbar_wait(&tmem_full[acc], acc_phase);
+            tc_fence_after();
+            const int64_t row = (int64_t)mt * BM + ew * 32 + lane;
+            const bool row_ok = row < prm.M;
+            uint8_t* crow = prm.c + row * prm.ldc;
+#pragma unroll 1
+            for (int ch = 0; ch < BN / 16; ++ch) {
+                uint32_t v[16];
+                tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + ch * 16, v);
+                tmem_ld_wait();
+                const int64_t col0 = (int64_t)nt * BN + ch * 16;
+                if (!row_ok || col0 >= prm.N) continue;
+                uint32_t w[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    w[q] = 0;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        uint32_t x;
+                        if (KIND == KIND_I8) x = v[4 * q + e];
+                        else x = (uint32_t)(__float2int_rn(__uint_as_float(v[4 * q + e])) + (int)prm.offset);
+                        w[q] |= mod_u32(x, prm.p, prm.magic64) << (8 * e);
+                    }
+                }
+                if (col0 + 16 <= prm.N && ((reinterpret_cast<uintptr_t>(crow + col0) & 15) == 0)) {
+                    *reinterpret_cast<uint4*>(crow + col0) = make_uint4(w[0], w[1], w[2], w[3]);
+                } else {
+                    for (int e = 0; e < 16 && col0 + e < prm.N; ++e) crow[col0 + e] = (uint8_t)(w[e / 4] >> (8 * (e % 4)));
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&tmem_empty[acc]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem_base);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Operand preparation.
+// I8: Bx bytes = residues.  F4: Bx / A nibbles = E2M1 codes of centred residues.
+// Table-driven expansion (fields with p^K <= XT_CODES): every element code maps
+// to its K x K block, staged in shared memory as K rows (T[code*K + l] = the K
+// output values of row l, bytes for I8 / nibbles for F4).  Tile = 64 kk x 64 j;
+// b rows are read with 16-byte loads, codes stored j-major so that one work item
+// (an output row segment of 16K bytes) reads contiguous smem and issues K
+// 16-byte stores.  Grid-stride over tiles amortises the table build.
+// ---------------------------------------------------------------------------
+constexpr int XT_KK = 64, XT_J = 64, XT_CODES = 1024;
+
+template <int K, int KIND>
+__global__ void __launch_bounds__(256) expand_b_table_kernel(const uint8_t* __restrict__ b, int64_t Kd, int64_t N,
+                                                             FieldConst f, uint32_t nib_lut, uint8_t* __restrict__ bx,
+                                                             int64_t ldb, int tiles_kk, int tiles_j) {
+    constexpr int ELEM_PER_ITEM = KIND == KIND_I8 ? 16 : 32;  // kk per work item (16K output bytes)
+    __shared__ uint32_t tab[XT_CODES * K];
+    __shared__ __align__(16) uint8_t raw[XT_KK][XT_J * K + 16];
+    __shared__ __align__(16) uint16_t code[XT_J][XT_KK + 8];
+    const uint32_t p = f.p;
+    int ncodes = 1;
+    for (int s = 0; s < K; ++s) ncodes *= (int)p;
+    for (int e = threadIdx.x; e < ncodes * K; e += blockDim.x) {
+        const int c = e / K, l = e % K;
+        uint32_t dig[K];
+        int r = c;
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+            dig[s] = (uint32_t)(r % (int)p);
+            r /= (int)p;
+        }
+        uint32_t w = 0;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            uint32_t acc = 0;
+#pragma unroll
+            for (int s = 0; s < K; ++s) acc += dig[s] * f.xpow[s + i][l];
+            const uint32_t res = mod_small(acc, p, f.magic);
+            if (KIND == KIND_I8) w |= res << (8 * i);
+            else w |= ((nib_lut >> (4 * res)) & 0xF) << (4 * i);
+        }
+        tab[e] = w;
+    }
+    const bool vec_rows = ((N * K) % 16 == 0) && ((reinterpret_cast<uintptr_t>(b) & 15) == 0);
+    const int64_t ntiles = (int64_t)tiles_kk * tiles_j;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t kk0 = (tile % tiles_kk) * XT_KK, j0 = (tile / tiles_kk) * XT_J;
+        __syncthreads();
+        constexpr int ROWB = XT_J * K;
+        if (vec_rows && j0 + XT_J <= N) {
+            for (int i = threadIdx.x; i < XT_KK * (ROWB / 16); i += blockDim.x) {
+                const int r = i / (ROWB / 16), q = i % (ROWB / 16);
+                const int64_t gk = kk0 + r;
+                uint4 v = make_uint4(0, 0, 0, 0);
+                if (gk < Kd) v = __ldg(reinterpret_cast<const uint4*>(b + gk * N * K + j0 * K) + q);
+                *reinterpret_cast<uint4*>(&raw[r][q * 16]) = v;
+            }
+        } else {
+            for (int i = threadIdx.x; i < XT_KK * ROWB; i += blockDim.x) {
+                const int r = i / ROWB, c = i % ROWB;
+                const int64_t gk = kk0 + r, gj = j0 + c / K;
+                raw[r][c] = (gk < Kd && gj < N) ? b[gk * N * K + j0 * K + c] : 0;
+            }
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < XT_KK * XT_J; i += blockDim.x) {
+            const int r = i / XT_J, jl = i % XT_J;
+            uint32_t cd = 0;
+#pragma unroll
+            for (int s = K - 1; s >= 0; --s) cd = cd * p + raw[r][jl * K + s];
+            code[jl][r] = (uint16_t)cd;
+        }
+        __syncthreads();
+        constexpr int CHUNKS = XT_KK / ELEM_PER_ITEM;
+        for (int i = threadIdx.x; i < XT_J * K * CHUNKS; i += blockDim.x) {
+            const int ch = i % CHUNKS, row = i / CHUNKS;
+            const int jl = row / K, l = row % K;
+            const int64_t gj = j0 + jl;
+            if (gj >= N) continue;
+            uint32_t w[4 * K];
+#pragma unroll
+            for (int q = 0; q < 4 * K; ++q) w[q] = 0;
+            const uint16_t* cr = &code[jl][ch * ELEM_PER_ITEM];
+#pragma unroll
+            for (int e = 0; e < ELEM_PER_ITEM; ++e) {
+                const uint32_t v = tab[cr[e] * K + l];
+#pragma unroll
+                for (int ii = 0; ii < K; ++ii) {
+                    const int pos = e * K + ii;
+                    if (KIND == KIND_I8) w[pos / 4] |= ((v >> (8 * ii)) & 0xFF) << (8 * (pos % 4));
+                    else w[pos / 8] |= ((v >> (4 * ii)) & 0xF) << (4 * (pos % 8));
+                }
+            }
+            const int64_t col = (kk0 + ch * ELEM_PER_ITEM) * K / (KIND == KIND_I8 ? 1 : 2);  // bytes
+            uint8_t* dst = bx + (gj * K + l) * ldb + col;
+            if (col + 16 * K <= ldb) {
+#pragma unroll
+                for (int q = 0; q < K; ++q)
+                    reinterpret_cast<uint4*>(dst)[q] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+            } else {
+                for (int e = 0; e < 16 * K && col + e < ldb; ++e) dst[e] = (uint8_t)(w[e / 4] >> (8 * (e % 4)));
+            }
+        }
+    }
+}
+
+// Generic arithmetic expansion for large fields (p^K > XT_CODES), INT8 only.
+constexpr int EX_T = 64;
+__global__ void __launch_bounds__(256) expand_b_generic_kernel(const uint8_t* __restrict__ b, int64_t K, int64_t N,
+                                                               FieldConst f, uint8_t* __restrict__ bx, int64_t ldb) {
+    __shared__ uint8_t sb[EX_T][EX_T * kMaxK + 4];
+    __shared__ uint8_t xp[kMaxDigits][kMaxK];
+    const int k = (int)f.k;
+    if (threadIdx.x < kMaxDigits * kMaxK) xp[threadIdx.x / kMaxK][threadIdx.x % kMaxK] = f.xpow[threadIdx.x / kMaxK][threadIdx.x % kMaxK];
+    const int64_t kk0 = (int64_t)blockIdx.x * EX_T, j0 = (int64_t)blockIdx.y * EX_T;
+    const int rowbytes = EX_T * k;
+    for (int i = threadIdx.x; i < EX_T * rowbytes; i += blockDim.x) {
+        const int r = i / rowbytes, c = i % rowbytes;
+        const int64_t gk = kk0 + r, gj = j0 + c / k;
+        sb[r][c] = (gk < K && gj < N) ? b[gk * N * k + j0 * k + c] : 0;
+    }
+    __syncthreads();
+    const int words_per_row = rowbytes / 4;
+    const int64_t colbase = kk0 * k;
+    for (int w = threadIdx.x; w < EX_T * k * words_per_row; w += blockDim.x) {
+        const int orow = w / words_per_row, wq = w % words_per_row;
+        const int jl = orow / k, l = orow % k;
+        const int64_t gj = j0 + jl;
+        if (gj >= N) continue;
+        uint32_t word = 0;
+        for (int e = 0; e < 4; ++e) {
+            const int c = wq * 4 + e;
+            const int kl = c / k, i = c % k;
+            uint32_t acc = 0;
+            for (int s = 0; s < k; ++s) acc += (uint32_t)sb[kl][jl * k + s] * xp[s + i][l];
+            word |= mod_small(acc, f.p, f.magic) << (8 * e);
+        }
+        const int64_t col = colbase + wq * 4;
+        uint8_t* dst = bx + (gj * k + l) * ldb + col;
+        if (col + 4 <= ldb) *reinterpret_cast<uint32_t*>(dst) = word;
+        else
+            for (int e = 0; e < 4 && col + e < ldb; ++e) dst[e] = (uint8_t)(word >> (8 * e));
+    }
+}
+
+// rows of width `width` bytes copied into a pitched, zero-padded buffer (I8 A)
+__global__ void pad_rows_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t width, uint8_t* __restrict__ dst,
+                                int64_t ld) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows * ld) return;
+    const int64_t r = i / ld, c = i % ld;
+    dst[i] = c < width ? src[r * width + c] : 0;
+}
+
+// A residues -> packed E2M1 nibbles of the centred residues, pitched rows (F4 A).
+// Each thread: 32 residues (2 x 16B loads when aligned) -> 16 bytes out.
+__global__ void pack_a_f4_kernel(const uint8_t* __restrict__ src, int64_t rows, int64_t width, uint32_t nib_lut,
+                                 uint8_t* __restrict__ dst, int64_t ld) {
+    const int64_t per_row = ld / 16;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows * per_row) return;
+    const int64_t r = i / per_row, q = i % per_row;
+    const int64_t c0 = q * 32;  // first residue of this 16-byte chunk
+    const uint8_t* s = src + r * width;
+    uint32_t out[4] = {0, 0, 0, 0};
+    if (c0 + 32 <= width && ((reinterpret_cast<uintptr_t>(s + c0) & 15) == 0)) {
+        const uint4 x = __ldg(reinterpret_cast<const uint4*>(s + c0));
+        const uint4 y = __ldg(reinterpret_cast<const uint4*>(s + c0) + 1);
+        const uint32_t in[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+            const uint32_t res = (in[e / 4] >> (8 * (e % 4))) & 0xFF;
+            out[e / 8] |= ((nib_lut >> (4 * res)) & 0xF) << (4 * (e % 8));
+        }
+    } else {
+        for (int e = 0; e < 32; ++e) {
+            if (c0 + e < width) {
+                const uint32_t res = s[c0 + e];
+                out[e / 8] |= ((nib_lut >> (4 * res)) & 0xF) << (4 * (e % 8));
+            }
+        }
+    }
+    *reinterpret_cast<uint4*>(dst + r * ld + q * 16) = make_uint4(out[0], out[1], out[2], out[3]);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+static int make_tmap(CUtensorMap* map, const void* base, int64_t inner_bytes, int64_t rows, int64_t ld,
+                     uint32_t box_rows) {
+    EncodeTiledFn fn = encode_fn();
+    QADIC_REQUIRE(fn != nullptr, QADIC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)inner_bytes, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld};
+    cuuint32_t box[2] = {(cuuint32_t)BK, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    QADIC_REQUIRE(r == CUDA_SUCCESS, QADIC_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return QADIC_OK;
+}
+
+static int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+static inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// E2M1 nibble codes of the centred residues 0..p-1 (p <= 7), packed 4 bits each
+static uint32_t centred_e2m1_lut(uint32_t p) {
+    static const uint32_t pos[4] = {0x0, 0x2, 0x4, 0x5};  // 0, 1, 2, 3
+    uint32_t lut = 0;
+    for (uint32_t r = 0; r < p; ++r) {
+        const int v = (2 * r <= p - 1) ? (int)r : (int)r - (int)p;
+        const uint32_t code = v >= 0 ? pos[v] : (0x8u | pos[-v]);
+        lut |= code << (4 * r);
+    }
+    return lut;
+}
+
+struct Layout {
+    int64_t Kb;      // inner elements (K * k)
+    int64_t inner;   // inner bytes of the operand tensors
+    int64_t lda, ldb;
+    bool prep_a;     // A needs a prepass (padding for I8, conversion for F4)
+    size_t bx_bytes, a_bytes;
+};
+
+static Layout plan(int kind, const uint8_t* a, int64_t m, int64_t kdim, int64_t n, int k) {
+    Layout L;
+    L.Kb = kdim * k;
+    L.inner = kind == KIND_I8 ? L.Kb : (L.Kb + 1) / 2;
+    L.ldb = round_up(L.inner, 16);
+    L.prep_a = kind == KIND_F4 || (L.Kb % 16 != 0) || ((reinterpret_cast<uintptr_t>(a) & 15) != 0);
+    L.lda = L.prep_a ? L.ldb : L.Kb;
+    L.bx_bytes = (size_t)round_up(n * k * L.ldb, 1024);
+    L.a_bytes = L.prep_a ? (size_t)round_up(m * L.lda, 1024) : 0;
+    return L;
+}
+
+template <int KIND>
+static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, Params prm, cudaStream_t s) {
+    using G = Geo<KIND>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(gemm_modp_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+        attr = true;
+    }
+    const int tiles = prm.m_tiles * prm.n_tiles;
+    const int grid = tiles < num_sms() ? tiles : num_sms();
+    QADIC_TIMED(KIND == KIND_I8 ? "i8 gemm" : "fp4 gemm", s,
+                gemm_modp_kernel<KIND><<<grid, THREADS, G::SMEM, s>>>(ta, tb, prm));
+    return check_launch(KIND == KIND_I8 ? "i8 gemm" : "fp4 gemm");
+}
+
+template <int K, int KIND>
+static void launch_expand_table(const uint8_t* b, int64_t kdim, int64_t n, const FieldConst& f, uint32_t lut,
+                                uint8_t* bx, int64_t ldb, cudaStream_t s) {
+    const int tk = (int)((kdim + XT_KK - 1) / XT_KK), tj = (int)((n + XT_J - 1) / XT_J);
+    const int64_t tiles = (int64_t)tk * tj;
+    const int grid = (int)(tiles < 4 * num_sms() ? tiles : 4 * num_sms());
+    QADIC_TIMED("expand B", s,
+                (expand_b_table_kernel<K, KIND><<<grid, 256, 0, s>>>(b, kdim, n, f, lut, bx, ldb, tk, tj)));
+}
+
+template <int KIND>
+static void expand_dispatch(int k, const uint8_t* b, int64_t kdim, int64_t n, const FieldConst& f, uint32_t lut,
+                            uint8_t* bx, int64_t ldb, cudaStream_t s) {
+    switch (k) {
+        case 1: launch_expand_table<1, KIND>(b, kdim, n, f, lut, bx, ldb, s); break;
+        case 2: launch_expand_table<2, KIND>(b, kdim, n, f, lut, bx, ldb, s); break;
+        case 3: launch_expand_table<3, KIND>(b, kdim, n, f, lut, bx, ldb, s); break;
+        default: launch_expand_table<4, KIND>(b, kdim, n, f, lut, bx, ldb, s); break;
+    }
+}
+
+// C[m, n*k] = A[m, K*k] (x) expand(B)  (mod p)
+static int run(int kind, const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
+               void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s) {
+    const int k = (int)f.k;
+    Layout L = plan(kind, a, m, kdim, n, k);
+    QADIC_REQUIRE(ws != nullptr && ws_bytes >= L.bx_bytes + L.a_bytes, QADIC_ERR_VALUE,
+                  "workspace too small (%zu < %zu)", ws_bytes, L.bx_bytes + L.a_bytes);
+    const uint32_t lut = kind == KIND_F4 ? centred_e2m1_lut(f.p) : 0;
+    uint8_t* bx = static_cast<uint8_t*>(ws);
+    const uint8_t* a_op = a;
+    if (L.prep_a) {
+        uint8_t* ap = bx + L.bx_bytes;
+        if (kind == KIND_F4) {
+            const int64_t tot = m * (L.lda / 16);
+            QADIC_TIMED("fp4 pack A", s,
+                        pack_a_f4_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(a, m, L.Kb, lut, ap, L.lda));
+        } else {
+            const int64_t tot = m * L.lda;
+            QADIC_TIMED("i8 pad A", s,
+                        pad_rows_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(a, m, L.Kb, ap, L.lda));
+        }
+        int rc = check_launch("tc prepare A");
+        if (rc) return rc;
+        a_op = ap;
+    }
+    int ncodes = 1;
+    for (int s2 = 0; s2 < k; ++s2) ncodes *= (int)f.p;
+    if (ncodes <= XT_CODES) {
+        if (kind == KIND_I8) expand_dispatch<KIND_I8>(k, b, kdim, n, f, lut, bx, L.ldb, s);
+        else expand_dispatch<KIND_F4>(k, b, kdim, n, f, lut, bx, L.ldb, s);
+    } else {
+        QADIC_REQUIRE(kind == KIND_I8, QADIC_ERR_UNSUPPORTED, "fp4 engine needs p^k <= %d", XT_CODES);
+        dim3 grid((unsigned)((kdim + EX_T - 1) / EX_T), (unsigned)((n + EX_T - 1) / EX_T));
+        QADIC_REQUIRE(grid.y <= 65535, QADIC_ERR_UNSUPPORTED, "n too large");
+        QADIC_TIMED("expand B", s, expand_b_generic_kernel<<<grid, 256, 0, s>>>(b, kdim, n, f, bx, L.ldb));
+    }
+    int rc = check_launch("tc expand B");
+    if (rc) return rc;
+    const int BN = kind == KIND_I8 ? Cfg<KIND_I8>::BN : Cfg<KIND_F4>::BN;
+    CUtensorMap ta, tb;
+    rc = make_tmap(&ta, a_op, L.inner, m, L.lda, BM);
+    if (rc) return rc;
+    rc = make_tmap(&tb, bx, L.inner, n * k, L.ldb, BN);
+    if (rc) return rc;
+    Params prm;
+    prm.M = m;
+    prm.N = n * k;
+    prm.ldc = n * k;
+    prm.p = f.p;
+    prm.offset = f.p * ((1u << 25) / f.p + 1);  // > |centred sum| (< 2^24), multiple of p
+    prm.magic64 = wide_magic(f.p);
+    prm.m_tiles = (int)((m + BM - 1) / BM);
+    prm.n_tiles = (int)((prm.N + BN - 1) / BN);
+    prm.num_kb = (int)((L.inner + BK - 1) / BK);
+    prm.c = c;
+    return kind == KIND_I8 ? launch_gemm<KIND_I8>(ta, tb, prm, s) : launch_gemm<KIND_F4>(ta, tb, prm, s);
+}
+
+}  // namespace tc
+
+// ---- entry points used by matmul_api.cu ---------------------------------------
+size_t tc_workspace(int kind, int64_t m, int64_t kdim, int64_t n, int k) {
+    const int64_t Kb = kdim * k;
+    const int64_t inner = kind == tc::KIND_I8 ? Kb : (Kb + 1) / 2;
+    const int64_t ld = tc::round_up(inner, 16);
+    return (size_t)tc::round_up(n * k * ld, 1024) + (size_t)tc::round_up(m * ld, 1024);
+}
+
+// largest |centred residue| = (p-1)/2; F4 needs p <= 7 and an fp32-exact sum
+bool tc_f4_ok(uint32_t p, int64_t kdim, int k) {
+    if (p > 7) return false;
+    const int64_t h = (p - 1) / 2;
+    return (__int128)kdim * k * h * h < ((__int128)1 << 24);
+}
+
+int tc_gf_matmul(int kind, const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
+                 void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s) {
+    if (kind == tc::KIND_I8) {
+        QADIC_REQUIRE((__int128)kdim * f.k * (f.p - 1) * (f.p - 1) < ((__int128)1 << 31), QADIC_ERR_PARAMS,
+                      "inner dimension %lld overflows the int32 plane accumulator", (long long)kdim);
+    } else {
+        QADIC_REQUIRE(tc_f4_ok(f.p, kdim, (int)f.k), QADIC_ERR_PARAMS,
+                      "fp4 engine needs p <= 7 and K*k*((p-1)/2)^2 < 2^24");
+    }
+    return tc::run(kind, f, a, b, m, kdim, n, ws, ws_bytes, c, s);
+}
+
+int tc_right_cmm(int kind, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n, uint32_t p,
+                 void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s) {
+    FieldConst f = {};
+    f.p = p;
+    f.k = 1;
+    f.t = 8;
+    f.magic = small_magic(p);
+    f.xpow[0][0] = 1;
+    return tc_gf_matmul(kind, f, a, b, m, kdim, n, ws, ws_bytes, c, s);
+}
+
+}  // namespace qadic
