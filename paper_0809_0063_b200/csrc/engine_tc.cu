@@ -59,13 +59,20 @@ struct Cfg<KIND_F4> {
     static constexpr int SF_COL = 480;
 };
 
-template <int KIND>
+// Geometry per operand kind and CTA grouping.  PAIR = cta_group::2: two CTAs
+// of a cluster share one M=256 MMA; each loads its own 128 A rows and half of
+// the BN B rows, so the per-SM operand traffic (TMA writes + MMA reads of
+// shared memory) drops by a third at the same MMA rate.
+template <int KIND, bool PAIR>
 struct Geo {
     static constexpr int BN = Cfg<KIND>::BN;
+    static constexpr int B_ROWS = PAIR ? BN / 2 : BN;  // B rows this CTA loads
     static constexpr int A_BYTES = BM * BK;
-    static constexpr int B_BYTES = BN * BK;
+    static constexpr int B_BYTES = B_ROWS * BK;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
+    static constexpr int STAGES_N = PAIR ? 6 : STAGES;
+    static constexpr size_t SMEM = (size_t)STAGES_N * STAGE_BYTES + 1024 + 256;
+    static constexpr int TILE_M = PAIR ? 2 * BM : BM;
 };
 
 struct Params {
@@ -126,76 +133,96 @@ __device__ __forceinline__ void tmem_fill_sf(uint32_t taddr) {
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
-template <int KIND>
+template <int KIND, bool PAIR>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_modp_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                      Params prm) {
     using namespace sm100;
-    using G = Geo<KIND>;
+    using G = Geo<KIND, PAIR>;
     constexpr int BN = G::BN;
+    constexpr int NST = G::STAGES_N;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * G::STAGE_BYTES);
-    uint64_t* empty_bar = full_bar + STAGES;
-    uint64_t* tmem_full = empty_bar + STAGES;
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + NST * G::STAGE_BYTES);
+    uint64_t* empty_bar = full_bar + NST;
+    uint64_t* tmem_full = empty_bar + NST;
     uint64_t* tmem_empty = tmem_full + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
+    const uint32_t rank = PAIR ? cluster_ctarank() : 0;
+    const bool leader = rank == 0;
+    const int group_id = PAIR ? blockIdx.x / 2 : blockIdx.x;
+    const int num_groups = PAIR ? gridDim.x / 2 : gridDim.x;
     const int num_tiles = prm.m_tiles * prm.n_tiles;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmap_a);
         tma_prefetch(&tmap_b);
-        for (int s = 0; s < STAGES; ++s) {
+        for (int s = 0; s < NST; ++s) {
             mbar_init(&full_bar[s], 1);
             mbar_init(&empty_bar[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tmem_full[a], 1);
-            mbar_init(&tmem_empty[a], 128);
+            mbar_init(&tmem_empty[a], PAIR ? 8 : 4);  // one arrival per epilogue warp (of both CTAs)
         }
         fence_barrier_init();
     }
-    if (warp == 2) tmem_alloc<512>(tmem_slot);
+    if (warp == 2) {
+        if (PAIR) tmem_alloc_pair<512>(tmem_slot);
+        else tmem_alloc<512>(tmem_slot);
+    }
     tc_fence_before();
-    __syncthreads();
+    if (PAIR) cluster_sync();
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     if (KIND == KIND_F4 && warp >= 4) {
         tmem_fill_sf(tmem_base + ((uint32_t)((warp - 4) * 32) << 16) + Cfg<KIND>::SF_COL);
         tc_fence_before();
     }
-    __syncthreads();
+    if (PAIR) cluster_sync();
+    else __syncthreads();
     tc_fence_after();
 
     if (warp == 0) {
-        // ===== TMA producer =====
+        // ===== TMA producer (both CTAs of a pair load their own halves) =====
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            for (int tile = group_id; tile < num_tiles; tile += num_groups) {
                 int mt, nt;
                 tile_coords(tile, prm.m_tiles, prm.n_tiles, mt, nt);
+                const int arow = mt * G::TILE_M + (int)rank * BM;
+                const int brow = nt * BN + (int)rank * G::B_ROWS;
                 for (int kb = 0; kb < prm.num_kb; ++kb) {
                     mbar_wait(&empty_bar[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * G::STAGE_BYTES;
                     uint8_t* sb = sa + G::A_BYTES;
-                    mbar_arrive_expect_tx(&full_bar[stage], G::STAGE_BYTES);
-                    tma_load_2d(sa, &tmap_a, &full_bar[stage], kb * BK, mt * BM);
-                    tma_load_2d(sb, &tmap_b, &full_bar[stage], kb * BK, nt * BN);
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    if (PAIR) {
+                        const uint32_t lbar = map_to_rank(&full_bar[stage], 0);
+                        if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * G::STAGE_BYTES);
+                        tma_load_2d_pair(sa, &tmap_a, lbar, kb * BK, arow);
+                        tma_load_2d_pair(sb, &tmap_b, lbar, kb * BK, brow);
+                    } else {
+                        mbar_arrive_expect_tx(&full_bar[stage], G::STAGE_BYTES);
+                        tma_load_2d(sa, &tmap_a, &full_bar[stage], kb * BK, arow);
+                        tma_load_2d(sb, &tmap_b, &full_bar[stage], kb * BK, brow);
+                    }
+                    if (++stage == NST) { stage = 0; phase ^= 1; }
                 }
             }
         }
-    } else if (warp == 1) {
-        // ===== MMA issuer: 4 MMAs of 32 bytes (K=32 int8 / K=64 fp4) per stage =====
-        constexpr uint32_t idesc = KIND == KIND_I8 ? idesc_u8_s32(BM, BN) : idesc_mxf4(BM, BN);
+    } else if (warp == 1 && leader) {
+        // ===== MMA issuer (pair leader only): 4 MMAs of 32 bytes per stage =====
+        constexpr uint32_t idesc =
+            KIND == KIND_I8 ? idesc_u8_s32(G::TILE_M, BN) : idesc_mxf4(G::TILE_M, BN);
         int stage = 0;
         uint32_t phase = 0;
         int local = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+        for (int tile = group_id; tile < num_tiles; tile += num_groups, ++local) {
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
             mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
@@ -210,32 +237,42 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                     for (int k = 0; k < BK / 32; ++k) {
                         const uint64_t ad = smem_desc_k_sw128(sa + k * 32), bd = smem_desc_k_sw128(sb + k * 32);
+                        const uint32_t accum = (kb | k) != 0;
+                        const uint32_t sf = tmem_base + (Cfg<KIND>::SF_COL > 0 ? Cfg<KIND>::SF_COL : 0);
                         if (KIND == KIND_I8) {
-                            umma_i8(tmem_d, ad, bd, idesc, (kb | k) != 0);
+                            if (PAIR) umma_i8_pair(tmem_d, ad, bd, idesc, accum);
+                            else umma_i8(tmem_d, ad, bd, idesc, accum);
                         } else {
-                            const uint32_t sf = tmem_base + Cfg<KIND>::SF_COL;
-                            umma_mxf4(tmem_d, ad, bd, idesc, (kb | k) != 0, sf, sf);
+                            if (PAIR) umma_mxf4_pair(tmem_d, ad, bd, idesc, accum, sf, sf);
+                            else umma_mxf4(tmem_d, ad, bd, idesc, accum, sf, sf);
                         }
                     }
-                    umma_commit(&empty_bar[stage]);
-                    if (kb == prm.num_kb - 1) umma_commit(&tmem_full[acc]);
+                    if (PAIR) {
+                        umma_commit_pair(&empty_bar[stage], 0x3);
+                        if (kb == prm.num_kb - 1) umma_commit_pair(&tmem_full[acc], 0x3);
+                    } else {
+                        umma_commit(&empty_bar[stage]);
+                        if (kb == prm.num_kb - 1) umma_commit(&tmem_full[acc]);
+                    }
                 }
                 __syncwarp();
-                if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                if (++stage == NST) { stage = 0; phase ^= 1; }
             }
         }
     } else if (warp >= 4) {
         // ===== epilogue: TMEM -> registers -> mod p -> uint8 =====
         const int ew = warp - 4;  // TMEM lane quarter this warp may access
+        const uint32_t empty_addr0 = PAIR ? map_to_rank(&tmem_empty[0], 0) : 0;
+        const uint32_t empty_addr1 = PAIR ? map_to_rank(&tmem_empty[1], 0) : 0;
         int local = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+        for (int tile = group_id; tile < num_tiles; tile += num_groups, ++local) {
             int mt, nt;
             tile_coords(tile, prm.m_tiles, prm.n_tiles, mt, nt);
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
             mbar_wait(&tmem_full[acc], acc_phase);
             tc_fence_after();
-            const int64_t row = (int64_t)mt * BM + ew * 32 + lane;
+            const int64_t row = (int64_t)mt * G::TILE_M + (int)rank * BM + ew * 32 + lane;
             const bool row_ok = row < prm.M;
             uint8_t* crow = prm.c + row * prm.ldc;
 #pragma unroll 1
@@ -264,14 +301,20 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
             }
             tc_fence_before();
-            mbar_arrive(&tmem_empty[acc]);
+            __syncwarp();
+            if (lane == 0) {
+                if (PAIR) mbar_arrive_cluster(acc ? empty_addr1 : empty_addr0);
+                else mbar_arrive(&tmem_empty[acc]);
+            }
         }
     }
     tc_fence_before();
-    __syncthreads();
+    if (PAIR) cluster_sync();
+    else __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc<512>(tmem_base);
+        if (PAIR) tmem_dealloc_pair<512>(tmem_base);
+        else tmem_dealloc<512>(tmem_base);
     }
 }
 
@@ -508,6 +551,16 @@ static int num_sms() {
 
 static inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
+// CTA-pair (cta_group::2) GEMM unless QADIC_TC_PAIR=0
+static bool pair_mode() {
+    static int mode = -1;
+    if (mode < 0) {
+        const char* e = getenv("QADIC_TC_PAIR");
+        mode = (e && e[0] == '0') ? 0 : 1;
+    }
+    return mode == 1;
+}
+
 // E2M1 nibble codes of the centred residues 0..p-1 (p <= 7), packed 4 bits each
 static uint32_t centred_e2m1_lut(uint32_t p) {
     static const uint32_t pos[4] = {0x0, 0x2, 0x4, 0x5};  // 0, 1, 2, 3
@@ -540,19 +593,35 @@ static Layout plan(int kind, const uint8_t* a, int64_t m, int64_t kdim, int64_t 
     return L;
 }
 
-template <int KIND>
+template <int KIND, bool PAIR>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, Params prm, cudaStream_t s) {
-    using G = Geo<KIND>;
+    using G = Geo<KIND, PAIR>;
+    auto kern = gemm_modp_kernel<KIND, PAIR>;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(gemm_modp_kernel<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
         attr = true;
     }
     const int tiles = prm.m_tiles * prm.n_tiles;
-    const int grid = tiles < num_sms() ? tiles : num_sms();
-    QADIC_TIMED(KIND == KIND_I8 ? "i8 gemm" : "fp4 gemm", s,
-                gemm_modp_kernel<KIND><<<grid, THREADS, G::SMEM, s>>>(ta, tb, prm));
-    return check_launch(KIND == KIND_I8 ? "i8 gemm" : "fp4 gemm");
+    const int per = PAIR ? 2 : 1;
+    int grid = num_sms() / per;
+    if (tiles < grid) grid = tiles;
+    grid *= per;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = G::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attrs[1];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = per;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+    const char* name = KIND == KIND_I8 ? "i8 gemm" : "fp4 gemm";
+    QADIC_TIMED(name, s, cudaLaunchKernelEx(&cfg, kern, ta, tb, prm));
+    return check_launch(name);
 }
 
 template <int K, int KIND>
@@ -615,10 +684,11 @@ static int run(int kind, const FieldConst& f, const uint8_t* a, const uint8_t* b
     int rc = check_launch("tc expand B");
     if (rc) return rc;
     const int BN = kind == KIND_I8 ? Cfg<KIND_I8>::BN : Cfg<KIND_F4>::BN;
+    const bool pair = pair_mode();
     CUtensorMap ta, tb;
     rc = make_tmap(&ta, a_op, L.inner, m, L.lda, BM);
     if (rc) return rc;
-    rc = make_tmap(&tb, bx, L.inner, n * k, L.ldb, BN);
+    rc = make_tmap(&tb, bx, L.inner, n * k, L.ldb, pair ? BN / 2 : BN);
     if (rc) return rc;
     Params prm;
     prm.M = m;
@@ -627,11 +697,12 @@ static int run(int kind, const FieldConst& f, const uint8_t* a, const uint8_t* b
     prm.p = f.p;
     prm.offset = f.p * ((1u << 25) / f.p + 1);  // > |centred sum| (< 2^24), multiple of p
     prm.magic64 = wide_magic(f.p);
-    prm.m_tiles = (int)((m + BM - 1) / BM);
+    prm.m_tiles = (int)((m + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM));
     prm.n_tiles = (int)((prm.N + BN - 1) / BN);
     prm.num_kb = (int)((L.inner + BK - 1) / BK);
     prm.c = c;
-    return kind == KIND_I8 ? launch_gemm<KIND_I8>(ta, tb, prm, s) : launch_gemm<KIND_F4>(ta, tb, prm, s);
+    if (pair) return kind == KIND_I8 ? launch_gemm<KIND_I8, true>(ta, tb, prm, s) : launch_gemm<KIND_F4, true>(ta, tb, prm, s);
+    return kind == KIND_I8 ? launch_gemm<KIND_I8, false>(ta, tb, prm, s) : launch_gemm<KIND_F4, false>(ta, tb, prm, s);
 }
 
 }  // namespace tc
