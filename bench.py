@@ -189,6 +189,7 @@ def build_step(cfg, engine, rank, ws, torch, dist, Q, W):
         w = W.work_units(c)
         meta["work"] = {k: v // ws for k, v in w.items() if isinstance(v, int)}
         meta["work"]["i8_macs"] = rows * n * n
+        meta["work"]["kara_macs"] = rows * n * n
         return step, e2e, units, (host.nbytes if rank == 0 else 0, rows * n), meta
     # batched configs: rotate buffer sets totalling > L2 so every step reads HBM
     if cfg == 1:
@@ -295,8 +296,9 @@ def roofline(cfg, engine, kname, kstats, work, peaks, peak_src):
                 "avg_launch_ms": round(avg_s * 1e3, 4), "algorithmic_ops_per_launch": ops, "peak_source": src,
                 "cublas_int8_measured_tops": round(peaks["int8_tops"], 1) if peaks.get("int8_tops") else None,
                 "two_x_measured_bf16_tops": round(2 * peaks["bf16_tflops"], 1)}
-    if kname == "fp4 gemm":
-        ops = 2 * work["i8_macs"]  # same plane MAC count, E2M1 operands
+    if kname in ("fp4 gemm", "fp4k gemm"):
+        # expanded form: M*(N k)*(K k) MACs; Karatsuba planes: k(k+1)/2 * M*N*K
+        ops = 2 * (work["kara_macs"] if kname == "fp4k gemm" else work["i8_macs"])
         achieved = ops / avg_s / 1e12
         peak = 9000.0
         return {"bound": "tensor", "kernel": kname, "achieved": round(achieved, 1), "peak": peak,

@@ -38,10 +38,11 @@ typedef enum qadic_status {
 } qadic_status;
 
 typedef enum qadic_engine {
-    QADIC_ENGINE_AUTO = 0,     /* the measured-fastest exact engine: F4_TC when valid, else I8_TC */
+    QADIC_ENGINE_AUTO = 0,     /* the measured-fastest exact engine: F4K_TC when valid, else I8_TC */
     QADIC_ENGINE_I8_TC = 1,    /* tcgen05.mma kind::i8 on coefficient planes, int32 TMEM accumulators */
     QADIC_ENGINE_F64_DMMA = 2, /* the paper's formulation: DQT-packed FP64 words on DMMA tensor cores */
-    QADIC_ENGINE_F4_TC = 3     /* tcgen05.mma kind::mxf4 (E2M1, unit block scales) on centred residues, p <= 7 */
+    QADIC_ENGINE_F4_TC = 3,    /* tcgen05.mma kind::mxf4 (E2M1, unit block scales) on centred residues, p <= 7 */
+    QADIC_ENGINE_F4K_TC = 4    /* F4 on k(k+1)/2 Karatsuba coefficient planes + mod-p combine (fewest MACs) */
 } qadic_engine;
 
 QADIC_API int qadic_abi_version(void);

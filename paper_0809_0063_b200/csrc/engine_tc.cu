@@ -76,12 +76,15 @@ struct Geo {
 };
 
 struct Params {
-    int64_t M, N;        // output rows / cols (cols = n * k)
+    int64_t M, N;        // output rows / cols of one plane (cols = n * k for the expanded form)
     int64_t ldc;         // output row pitch (bytes)
+    int64_t c_plane;     // output plane stride (bytes)
     uint32_t p;
     uint32_t offset;     // multiple of p added before the unsigned mod (centred kinds)
     uint64_t magic64;
     int m_tiles, n_tiles, num_kb;
+    int planes;          // independent plane products, stacked along the A / B rows
+    int nibble_out;      // 0: uint8 residues; 1: residues packed two per byte
     uint8_t* c;
 };
 
@@ -155,7 +158,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     const bool leader = rank == 0;
     const int group_id = PAIR ? blockIdx.x / 2 : blockIdx.x;
     const int num_groups = PAIR ? gridDim.x / 2 : gridDim.x;
-    const int num_tiles = prm.m_tiles * prm.n_tiles;
+    const int plane_tiles = prm.m_tiles * prm.n_tiles;
+    const int num_tiles = plane_tiles * prm.planes;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmap_a);
@@ -194,9 +198,10 @@ __global__ void __launch_bounds__(THREADS, 1)
             uint32_t phase = 0;
             for (int tile = group_id; tile < num_tiles; tile += num_groups) {
                 int mt, nt;
-                tile_coords(tile, prm.m_tiles, prm.n_tiles, mt, nt);
-                const int arow = mt * G::TILE_M + (int)rank * BM;
-                const int brow = nt * BN + (int)rank * G::B_ROWS;
+                const int pl = tile / plane_tiles;
+                tile_coords(tile % plane_tiles, prm.m_tiles, prm.n_tiles, mt, nt);
+                const int arow = (int)(pl * prm.M) + mt * G::TILE_M + (int)rank * BM;
+                const int brow = (int)(pl * prm.N) + nt * BN + (int)rank * G::B_ROWS;
                 for (int kb = 0; kb < prm.num_kb; ++kb) {
                     mbar_wait(&empty_bar[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * G::STAGE_BYTES;
@@ -267,14 +272,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         int local = 0;
         for (int tile = group_id; tile < num_tiles; tile += num_groups, ++local) {
             int mt, nt;
-            tile_coords(tile, prm.m_tiles, prm.n_tiles, mt, nt);
+            const int pl = tile / plane_tiles;
+            tile_coords(tile % plane_tiles, prm.m_tiles, prm.n_tiles, mt, nt);
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
             mbar_wait(&tmem_full[acc], acc_phase);
             tc_fence_after();
             const int64_t row = (int64_t)mt * G::TILE_M + (int)rank * BM + ew * 32 + lane;
             const bool row_ok = row < prm.M;
-            uint8_t* crow = prm.c + row * prm.ldc;
+            uint8_t* crow = prm.c + pl * prm.c_plane + row * prm.ldc;
 #pragma unroll 1
             for (int ch = 0; ch < BN / 16; ++ch) {
                 uint32_t v[16];
@@ -282,22 +288,40 @@ __global__ void __launch_bounds__(THREADS, 1)
                 tmem_ld_wait();
                 const int64_t col0 = (int64_t)nt * BN + ch * 16;
                 if (!row_ok || col0 >= prm.N) continue;
-                uint32_t w[4];
+                uint32_t r[16];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    w[q] = 0;
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        uint32_t x;
-                        if (KIND == KIND_I8) x = v[4 * q + e];
-                        else x = (uint32_t)(__float2int_rn(__uint_as_float(v[4 * q + e])) + (int)prm.offset);
-                        w[q] |= mod_u32(x, prm.p, prm.magic64) << (8 * e);
-                    }
+                for (int e = 0; e < 16; ++e) {
+                    uint32_t x;
+                    if (KIND == KIND_I8) x = v[e];
+                    else x = (uint32_t)(__float2int_rn(__uint_as_float(v[e])) + (int)prm.offset);
+                    r[e] = mod_u32(x, prm.p, prm.magic64);
                 }
-                if (col0 + 16 <= prm.N && ((reinterpret_cast<uintptr_t>(crow + col0) & 15) == 0)) {
-                    *reinterpret_cast<uint4*>(crow + col0) = make_uint4(w[0], w[1], w[2], w[3]);
+                if (prm.nibble_out) {  // residues < 16: two per byte, 8 bytes per 16 columns
+                    uint32_t w0 = 0, w1 = 0;
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        w0 |= r[e] << (4 * e);
+                        w1 |= r[8 + e] << (4 * e);
+                    }
+                    uint8_t* dst = crow + col0 / 2;
+                    if (col0 + 16 <= prm.N && ((reinterpret_cast<uintptr_t>(dst) & 7) == 0)) {
+                        *reinterpret_cast<uint2*>(dst) = make_uint2(w0, w1);
+                    } else {
+                        for (int e = 0; e < 16 && col0 + e < prm.N; e += 2) {
+                            const uint32_t hi = (col0 + e + 1 < prm.N) ? r[e + 1] : 0;
+                            dst[e / 2] = (uint8_t)(r[e] | (hi << 4));
+                        }
+                    }
                 } else {
-                    for (int e = 0; e < 16 && col0 + e < prm.N; ++e) crow[col0 + e] = (uint8_t)(w[e / 4] >> (8 * (e % 4)));
+                    uint32_t w[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        w[q] = r[4 * q] | (r[4 * q + 1] << 8) | (r[4 * q + 2] << 16) | (r[4 * q + 3] << 24);
+                    if (col0 + 16 <= prm.N && ((reinterpret_cast<uintptr_t>(crow + col0) & 15) == 0)) {
+                        *reinterpret_cast<uint4*>(crow + col0) = make_uint4(w[0], w[1], w[2], w[3]);
+                    } else {
+                        for (int e = 0; e < 16 && col0 + e < prm.N; ++e) crow[col0 + e] = (uint8_t)r[e];
+                    }
                 }
             }
             tc_fence_before();
@@ -594,7 +618,8 @@ static Layout plan(int kind, const uint8_t* a, int64_t m, int64_t kdim, int64_t 
 }
 
 template <int KIND, bool PAIR>
-static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, Params prm, cudaStream_t s) {
+static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, Params prm, cudaStream_t s,
+                       const char* label = nullptr) {
     using G = Geo<KIND, PAIR>;
     auto kern = gemm_modp_kernel<KIND, PAIR>;
     static bool attr = false;
@@ -619,7 +644,7 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, Params prm,
     attrs[0].val.clusterDim.z = 1;
     cfg.attrs = attrs;
     cfg.numAttrs = 1;
-    const char* name = KIND == KIND_I8 ? "i8 gemm" : "fp4 gemm";
+    const char* name = label ? label : (KIND == KIND_I8 ? "i8 gemm" : "fp4 gemm");
     QADIC_TIMED(name, s, cudaLaunchKernelEx(&cfg, kern, ta, tb, prm));
     return check_launch(name);
 }
@@ -701,11 +726,336 @@ static int run(int kind, const FieldConst& f, const uint8_t* a, const uint8_t* b
     prm.n_tiles = (int)((prm.N + BN - 1) / BN);
     prm.num_kb = (int)((L.inner + BK - 1) / BK);
     prm.c = c;
+    prm.c_plane = 0;
+    prm.planes = 1;
+    prm.nibble_out = 0;
     if (pair) return kind == KIND_I8 ? launch_gemm<KIND_I8, true>(ta, tb, prm, s) : launch_gemm<KIND_F4, true>(ta, tb, prm, s);
     return kind == KIND_I8 ? launch_gemm<KIND_I8, false>(ta, tb, prm, s) : launch_gemm<KIND_F4, false>(ta, tb, prm, s);
 }
 
+// ---------------------------------------------------------------------------
+// Karatsuba planes (FP4 kind).  The S = k(k+1)/2 plane products
+//     D_i = A_i B_i,    D_ij = (A_i + A_j)(B_i + B_j)   (i < j)
+// of coefficient planes (operand sums reduced mod p, centred, E2M1) give all
+// product coefficients P_t = sum_{i<j, i+j=t} (D_ij - D_i - D_j) + [t even] D_{t/2};
+// with the field fold C_l = sum_t xpow[t][l] P_t this is ONE mod-p linear map
+// C_l = sum_s W[l][s] D_s, applied by the combine kernel.  Every plane product
+// is an ordinary M x N x K GEMM (inner dimension K, not K*k), so cfg5 (k = 3)
+// runs 6 plane GEMMs where the expanded form runs 9: 1/3 fewer MACs.
+// ---------------------------------------------------------------------------
+// plane s: s < k -> single coefficient s; then the pairs (i, j), i < j, in
+// lexicographic order (k <= 4).  Branch-only so unrolled indices fold.
+__host__ __device__ constexpr int combo_first(int k, int s) {
+    return s < k ? s : (k == 2 ? 0 : k == 3 ? (s <= 4 ? 0 : 1) : (s <= 6 ? 0 : s <= 8 ? 1 : 2));
+}
+__host__ __device__ constexpr int combo_second(int k, int s) {
+    return s < k ? s
+                 : (k == 2 ? 1
+                           : k == 3 ? (s == 3 ? 1 : 2)
+                                    : (s == 4 ? 1 : s == 5 ? 2 : s == 6 ? 3 : s == 7 ? 2 : 3));
+}
+
+constexpr int KMAX_S = 10;
+struct CombineW {
+    uint8_t w[kMaxK][KMAX_S];  // C_l = sum_s w[l][s] * D_s  (mod p)
+};
+
+__device__ __forceinline__ uint32_t byte_of(const uint32_t* in, int idx) { return (in[idx >> 2] >> (8 * (idx & 3))) & 0xFF; }
+
+// A [M, Kd, K] residues -> S planes [S][M][ld] of packed E2M1 nibbles.
+// Thread: one row, 32 consecutive kk (32K input bytes) -> 16 bytes per plane.
+template <int K>
+__global__ void __launch_bounds__(256) planes_a_kernel(const uint8_t* __restrict__ a, int64_t M, int64_t Kd, uint32_t p,
+                                                       uint32_t lut, uint8_t* __restrict__ out, int64_t ld,
+                                                       int64_t plane_stride) {
+    constexpr int S = K * (K + 1) / 2;
+    const int64_t chunks = ld / 16;
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= M * chunks) return;
+    const int64_t m = idx / chunks, q = idx % chunks;
+    const int64_t kk0 = q * 32;
+    const uint8_t* src = a + (m * Kd + kk0) * K;
+    uint32_t in[8 * K];
+    if (kk0 + 32 <= Kd && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+#pragma unroll
+        for (int v = 0; v < 2 * K; ++v) {
+            const uint4 x = __ldg(reinterpret_cast<const uint4*>(src) + v);
+            in[4 * v] = x.x; in[4 * v + 1] = x.y; in[4 * v + 2] = x.z; in[4 * v + 3] = x.w;
+        }
+    } else {
+#pragma unroll
+        for (int v = 0; v < 8 * K; ++v) in[v] = 0;
+#pragma unroll
+        for (int e = 0; e < 32 * K; ++e)  // unrolled: in[] stays in registers
+            if (kk0 + e / K < Kd) in[e >> 2] |= (uint32_t)src[e] << (8 * (e & 3));
+    }
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const int ci = combo_first(K, s), cj = combo_second(K, s);
+        uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+            uint32_t v = byte_of(in, e * K + ci);
+            if (cj != ci) {
+                v += byte_of(in, e * K + cj);
+                if (v >= p) v -= p;
+            }
+            w[e >> 3] |= ((lut >> (4 * v)) & 0xF) << (4 * (e & 7));
+        }
+        *reinterpret_cast<uint4*>(out + s * plane_stride + m * ld + q * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
+// B [Kd, N, K] residues -> S transposed planes [S][N][ld] of packed E2M1 nibbles.
+// Tile: 64 kk x 128 j staged in smem; thread = one j, 32 kk -> 16 bytes per plane.
+constexpr int PB_KK = 64, PB_J = 128;
+template <int K>
+__global__ void __launch_bounds__(256) planes_b_kernel(const uint8_t* __restrict__ b, int64_t Kd, int64_t N, uint32_t p,
+                                                       uint32_t lut, uint8_t* __restrict__ out, int64_t ld,
+                                                       int64_t plane_stride, int tiles_kk, int tiles_j) {
+    constexpr int S = K * (K + 1) / 2;
+    constexpr int ROWB = PB_J * K;
+    __shared__ __align__(16) uint8_t raw[PB_KK][ROWB + 16];
+    const bool vec_rows = ((N * K) % 16 == 0) && ((reinterpret_cast<uintptr_t>(b) & 15) == 0);
+    const int64_t ntiles = (int64_t)tiles_kk * tiles_j;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t kk0 = (tile % tiles_kk) * PB_KK, j0 = (tile / tiles_kk) * PB_J;
+        __syncthreads();
+        if (vec_rows && j0 + PB_J <= N) {
+            for (int i = threadIdx.x; i < PB_KK * (ROWB / 16); i += blockDim.x) {
+                const int r = i / (ROWB / 16), q = i % (ROWB / 16);
+                const int64_t gk = kk0 + r;
+                uint4 v = make_uint4(0, 0, 0, 0);
+                if (gk < Kd) v = __ldg(reinterpret_cast<const uint4*>(b + gk * N * K + j0 * K) + q);
+                *reinterpret_cast<uint4*>(&raw[r][q * 16]) = v;
+            }
+        } else {
+            for (int i = threadIdx.x; i < PB_KK * ROWB; i += blockDim.x) {
+                const int r = i / ROWB, c = i % ROWB;
+                const int64_t gk = kk0 + r, gj = j0 + c / K;
+                raw[r][c] = (gk < Kd && gj < N) ? b[gk * N * K + j0 * K + c] : 0;
+            }
+        }
+        __syncthreads();
+        const int jl = threadIdx.x % PB_J, ch = threadIdx.x / PB_J;  // 2 chunks of 32 kk
+        const int64_t gj = j0 + jl;
+        if (gj >= N) continue;
+        uint32_t w[S][4];
+#pragma unroll
+        for (int s = 0; s < S; ++s) w[s][0] = w[s][1] = w[s][2] = w[s][3] = 0;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+            uint32_t c[K];
+#pragma unroll
+            for (int i = 0; i < K; ++i) c[i] = raw[ch * 32 + e][jl * K + i];
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const int ci = combo_first(K, s), cj = combo_second(K, s);
+                uint32_t v = c[ci];
+                if (cj != ci) {
+                    v += c[cj];
+                    if (v >= p) v -= p;
+                }
+                w[s][e >> 3] |= ((lut >> (4 * v)) & 0xF) << (4 * (e & 7));
+            }
+        }
+        const int64_t col = (kk0 + ch * 32) / 2;
+        if (col + 16 <= ld) {
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                *reinterpret_cast<uint4*>(out + s * plane_stride + gj * ld + col) =
+                    make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
+        }
+    }
+}
+
+// D planes [S][M][ldd] (nibbles, N columns) -> C [M][N][K] uint8 residues.
+// Thread: one row, 32 consecutive columns.
+template <int K>
+__global__ void __launch_bounds__(256) combine_kernel(const uint8_t* __restrict__ d, int64_t M, int64_t N, int64_t ldd,
+                                                      int64_t plane_stride, uint32_t p, uint32_t magic, CombineW cw,
+                                                      uint8_t* __restrict__ c) {
+    constexpr int S = K * (K + 1) / 2;
+    const int64_t chunks = (N + 31) / 32;
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= M * chunks) return;
+    const int64_t m = idx / chunks, q = idx % chunks;
+    const int64_t j0 = q * 32;
+    uint32_t dv[S][4];
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const uint8_t* src = d + s * plane_stride + m * ldd + j0 / 2;
+        const uint4 x = *reinterpret_cast<const uint4*>(src);  // ldd is a multiple of 16 and covers 32 columns
+        dv[s][0] = x.x; dv[s][1] = x.y; dv[s][2] = x.z; dv[s][3] = x.w;
+    }
+    uint32_t o[8 * K];
+#pragma unroll
+    for (int v = 0; v < 8 * K; ++v) o[v] = 0;
+#pragma unroll
+    for (int e = 0; e < 32; ++e) {
+#pragma unroll
+        for (int l = 0; l < K; ++l) {
+            uint32_t acc = 0;
+#pragma unroll
+            for (int s = 0; s < S; ++s) acc += cw.w[l][s] * ((dv[s][e >> 3] >> (4 * (e & 7))) & 0xF);
+            const int pos = e * K + l;
+            o[pos >> 2] |= mod_small(acc, p, magic) << (8 * (pos & 3));
+        }
+    }
+    uint8_t* dst = c + (m * N + j0) * K;
+    if (j0 + 32 <= N && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+        for (int v = 0; v < 2 * K; ++v)
+            reinterpret_cast<uint4*>(dst)[v] = make_uint4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+    } else {
+#pragma unroll
+        for (int e = 0; e < 32 * K; ++e)  // unrolled: o[] stays in registers
+            if (j0 + e / K < N) dst[e] = (uint8_t)(o[e >> 2] >> (8 * (e & 3)));
+    }
+}
+
+struct KaraLayout {
+    int S;
+    int64_t ldk;   // bytes per plane row of A_s / B_s (packed K)
+    int64_t ldd;   // bytes per plane row of D_s (packed N)
+    size_t a_bytes, b_bytes, d_bytes;
+};
+
+static KaraLayout kara_plan(int64_t m, int64_t kdim, int64_t n, int k) {
+    KaraLayout L;
+    L.S = k * (k + 1) / 2;
+    L.ldk = round_up((kdim + 1) / 2, 16);
+    L.ldd = round_up((n + 1) / 2, 16);
+    L.a_bytes = (size_t)round_up(L.S * m * L.ldk, 1024);
+    L.b_bytes = (size_t)round_up(L.S * n * L.ldk, 1024);
+    L.d_bytes = k == 1 ? 0 : (size_t)round_up(L.S * m * L.ldd, 1024);
+    return L;
+}
+
+template <int K>
+static void launch_planes(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n, uint32_t p,
+                          uint32_t lut, const KaraLayout& L, uint8_t* as, uint8_t* bs, cudaStream_t s) {
+    const int64_t ta = m * (L.ldk / 16);
+    QADIC_TIMED("fp4k planes A", s,
+                planes_a_kernel<K><<<(unsigned)((ta + 255) / 256), 256, 0, s>>>(a, m, kdim, p, lut, as, L.ldk,
+                                                                                  m * L.ldk));
+    const int tk = (int)((kdim + PB_KK - 1) / PB_KK), tj = (int)((n + PB_J - 1) / PB_J);
+    const int64_t tiles = (int64_t)tk * tj;
+    const int grid = (int)(tiles < 8 * num_sms() ? tiles : 8 * num_sms());
+    QADIC_TIMED("fp4k planes B", s,
+                planes_b_kernel<K><<<grid, 256, 0, s>>>(b, kdim, n, p, lut, bs, L.ldk, n * L.ldk, tk, tj));
+}
+
+template <int K>
+static void launch_combine(const uint8_t* d, int64_t m, int64_t n, const KaraLayout& L, uint32_t p, uint32_t magic,
+                           const CombineW& cw, uint8_t* c, cudaStream_t s) {
+    const int64_t tot = m * ((n + 31) / 32);
+    QADIC_TIMED("fp4k combine", s,
+                combine_kernel<K><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(d, m, n, L.ldd, m * L.ldd, p, magic,
+                                                                                 cw, c));
+}
+
+// C[m, n, k] = A[m, K, k] B[K, n, k] over GF(p^k) through Karatsuba planes
+static int run_kara(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
+                    void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s) {
+    const int k = (int)f.k;
+    KaraLayout L = kara_plan(m, kdim, n, k);
+    QADIC_REQUIRE(ws != nullptr && ws_bytes >= L.a_bytes + L.b_bytes + L.d_bytes, QADIC_ERR_VALUE,
+                  "workspace too small (%zu < %zu)", ws_bytes, L.a_bytes + L.b_bytes + L.d_bytes);
+    const uint32_t lut = centred_e2m1_lut(f.p);
+    uint8_t* as = static_cast<uint8_t*>(ws);
+    uint8_t* bs = as + L.a_bytes;
+    uint8_t* dd = bs + L.b_bytes;
+    switch (k) {
+        case 1: launch_planes<1>(a, b, m, kdim, n, f.p, lut, L, as, bs, s); break;
+        case 2: launch_planes<2>(a, b, m, kdim, n, f.p, lut, L, as, bs, s); break;
+        case 3: launch_planes<3>(a, b, m, kdim, n, f.p, lut, L, as, bs, s); break;
+        default: launch_planes<4>(a, b, m, kdim, n, f.p, lut, L, as, bs, s); break;
+    }
+    int rc = check_launch("fp4k planes");
+    if (rc) return rc;
+    const bool pair = pair_mode();
+    constexpr int BN = Cfg<KIND_F4>::BN;
+    CUtensorMap ta, tb;
+    rc = make_tmap(&ta, as, (kdim + 1) / 2, L.S * m, L.ldk, BM);
+    if (rc) return rc;
+    rc = make_tmap(&tb, bs, (kdim + 1) / 2, L.S * n, L.ldk, pair ? BN / 2 : BN);
+    if (rc) return rc;
+    Params prm;
+    prm.M = m;
+    prm.N = n;
+    prm.p = f.p;
+    prm.offset = f.p * ((1u << 25) / f.p + 1);
+    prm.magic64 = wide_magic(f.p);
+    prm.m_tiles = (int)((m + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM));
+    prm.n_tiles = (int)((n + BN - 1) / BN);
+    prm.num_kb = (int)(((kdim + 1) / 2 + BK - 1) / BK);
+    prm.planes = L.S;
+    if (k == 1) {  // one plane: the GEMM writes C directly
+        prm.c = c;
+        prm.ldc = n;
+        prm.c_plane = 0;
+        prm.nibble_out = 0;
+    } else {
+        prm.c = dd;
+        prm.ldc = L.ldd;
+        prm.c_plane = m * L.ldd;
+        prm.nibble_out = 1;
+    }
+    rc = pair ? launch_gemm<KIND_F4, true>(ta, tb, prm, s, "fp4k gemm")
+              : launch_gemm<KIND_F4, false>(ta, tb, prm, s, "fp4k gemm");
+    if (rc || k == 1) return rc;
+    // combine weights: W[l][s] = sum_t coef(t, s) * xpow[t][l]  (mod p)
+    CombineW cw = {};
+    for (int l = 0; l < k; ++l) {
+        for (int sidx = 0; sidx < L.S; ++sidx) {
+            const int i = combo_first(k, sidx), j = combo_second(k, sidx);
+            int64_t acc = 0;
+            if (i == j) {
+                acc += f.xpow[2 * i][l];
+                for (int o = 0; o < k; ++o)
+                    if (o != i) acc -= f.xpow[i + o][l];
+            } else {
+                acc += f.xpow[i + j][l];
+            }
+            acc %= (int64_t)f.p;
+            if (acc < 0) acc += f.p;
+            cw.w[l][sidx] = (uint8_t)acc;
+        }
+    }
+    const uint32_t magic = small_magic(f.p);
+    switch (k) {
+        case 2: launch_combine<2>(dd, m, n, L, f.p, magic, cw, c, s); break;
+        case 3: launch_combine<3>(dd, m, n, L, f.p, magic, cw, c, s); break;
+        default: launch_combine<4>(dd, m, n, L, f.p, magic, cw, c, s); break;
+    }
+    return check_launch("fp4k combine");
+}
+
 }  // namespace tc
+
+size_t tc_kara_workspace(int64_t m, int64_t kdim, int64_t n, int k) {
+    tc::KaraLayout L = tc::kara_plan(m, kdim, n, k);
+    return L.a_bytes + L.b_bytes + L.d_bytes;
+}
+
+int tc_kara_gf_matmul(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
+                      void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s) {
+    QADIC_REQUIRE(f.p <= 7 && (__int128)kdim * ((f.p - 1) / 2) * ((f.p - 1) / 2) < ((__int128)1 << 24), QADIC_ERR_PARAMS,
+                  "fp4k engine needs p <= 7 and K*((p-1)/2)^2 < 2^24");
+    return tc::run_kara(f, a, b, m, kdim, n, ws, ws_bytes, c, s);
+}
+
+int tc_kara_right_cmm(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n, uint32_t p, void* ws,
+                      size_t ws_bytes, uint8_t* c, cudaStream_t s) {
+    FieldConst f = {};
+    f.p = p;
+    f.k = 1;
+    f.t = 8;
+    f.magic = small_magic(p);
+    f.xpow[0][0] = 1;
+    return tc_kara_gf_matmul(f, a, b, m, kdim, n, ws, ws_bytes, c, s);
+}
 
 // ---- entry points used by matmul_api.cu ---------------------------------------
 size_t tc_workspace(int kind, int64_t m, int64_t kdim, int64_t n, int k) {

@@ -12,6 +12,11 @@ int tc_gf_matmul(int kind, const FieldConst& f, const uint8_t* a, const uint8_t*
                  void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s);
 int tc_right_cmm(int kind, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n, uint32_t p,
                  void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s);
+size_t tc_kara_workspace(int64_t m, int64_t kdim, int64_t n, int k);
+int tc_kara_gf_matmul(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
+                      void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s);
+int tc_kara_right_cmm(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n, uint32_t p, void* ws,
+                      size_t ws_bytes, uint8_t* c, cudaStream_t s);
 size_t f64_gf_workspace(int64_t m, int64_t kdim, int64_t n);
 size_t f64_cmm_workspace(int64_t m, int64_t kdim, int64_t n, int d);
 int f64_gf_matmul(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
@@ -27,7 +32,8 @@ using namespace qadic;
 // 10-25x faster than the FP64 engine; FP4 runs the MMA at twice the int8 rate)
 static int resolve_engine(int32_t engine, uint32_t p, int64_t kdim, int k) {
     if (engine != QADIC_ENGINE_AUTO) return engine;
-    return tc_f4_ok(p, kdim, k) ? QADIC_ENGINE_F4_TC : QADIC_ENGINE_I8_TC;
+    // Karatsuba planes: inner dimension K per plane (the sums never exceed it)
+    return tc_f4_ok(p, kdim, 1) ? QADIC_ENGINE_F4K_TC : QADIC_ENGINE_I8_TC;
 }
 static int tc_kind(int eng) { return eng == QADIC_ENGINE_F4_TC ? 1 : 0; }
 
@@ -36,6 +42,7 @@ extern "C" {
 size_t qadic_gf_matmul_workspace(const qadic_field_desc* f, int64_t m, int64_t kdim, int64_t n, int32_t engine) {
     if (!f || m < 0 || kdim < 0 || n < 0) return 0;
     const int eng = resolve_engine(engine, (uint32_t)f->p, kdim, f->k);
+    if (eng == QADIC_ENGINE_F4K_TC) return tc_kara_workspace(m, kdim, n, f->k);
     return eng == QADIC_ENGINE_F64_DMMA ? f64_gf_workspace(m, kdim, n) : tc_workspace(tc_kind(eng), m, kdim, n, f->k);
 }
 
@@ -53,6 +60,7 @@ int qadic_gf_matmul_u8(const qadic_field_desc* fd, const uint8_t* a, const uint8
         return check_launch("gf_matmul (empty K)");
     }
     const int eng = resolve_engine(engine, f.p, kdim, (int)f.k);
+    if (eng == QADIC_ENGINE_F4K_TC) return tc_kara_gf_matmul(f, a, b, m, kdim, n, ws, ws_bytes, c, s);
     if (eng == QADIC_ENGINE_I8_TC || eng == QADIC_ENGINE_F4_TC)
         return tc_gf_matmul(tc_kind(eng), f, a, b, m, kdim, n, ws, ws_bytes, c, s);
     QADIC_REQUIRE(eng == QADIC_ENGINE_F64_DMMA, QADIC_ERR_VALUE, "unknown engine %d", engine);
@@ -77,6 +85,7 @@ int qadic_gf_matmul_u8(const qadic_field_desc* fd, const uint8_t* a, const uint8
 size_t qadic_right_cmm_workspace(int64_t m, int64_t kdim, int64_t n, int64_t p, int32_t d, int32_t engine) {
     if (m < 0 || kdim < 0 || n < 0 || d < 0) return 0;
     const int eng = resolve_engine(engine, (uint32_t)p, kdim, 1);
+    if (eng == QADIC_ENGINE_F4K_TC) return tc_kara_workspace(m, kdim, n, 1);
     return eng == QADIC_ENGINE_F64_DMMA ? f64_cmm_workspace(m, kdim, n, d) : tc_workspace(tc_kind(eng), m, kdim, n, 1);
 }
 
@@ -96,6 +105,7 @@ int qadic_right_cmm_u8(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kd
         return check_launch("right_cmm (empty K)");
     }
     const int eng = resolve_engine(engine, (uint32_t)p, kdim, 1);
+    if (eng == QADIC_ENGINE_F4K_TC) return tc_kara_right_cmm(a, b, m, kdim, n, (uint32_t)p, ws, ws_bytes, c, s);
     if (eng == QADIC_ENGINE_I8_TC || eng == QADIC_ENGINE_F4_TC)
         return tc_right_cmm(tc_kind(eng), a, b, m, kdim, n, (uint32_t)p, ws, ws_bytes, c, s);
     QADIC_REQUIRE(eng == QADIC_ENGINE_F64_DMMA, QADIC_ERR_VALUE, "unknown engine %d", engine);

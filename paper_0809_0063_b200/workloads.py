@@ -104,9 +104,9 @@ def work_units(c: Config, shape: Optional[tuple] = None) -> dict:
         m, kd, n = shape
         return {"unit_count": m * kd * n, "unit": "GF mult-adds", "madds": m * kd * n,
                 "redq_coeffs": m * n * (2 * c.k - 1), "io_bytes": (m * kd + kd * n + m * n) * c.k,
-                "i8_macs": m * n * kd * c.k * c.k}
+                "i8_macs": m * n * kd * c.k * c.k, "kara_macs": m * n * kd * c.k * (c.k + 1) // 2}
     if c.cfg == 4:
         (n,) = shape
         return {"unit_count": n ** 3, "unit": "F_p mult-adds", "madds": n ** 3, "redq_coeffs": n * n,
-                "io_bytes": 2 * n * n, "i8_macs": n ** 3}
+                "io_bytes": 2 * n * n, "i8_macs": n ** 3, "kara_macs": n ** 3}
     raise KeyError(c.cfg)

@@ -174,7 +174,7 @@ class TestGFDot:
 # ---------------------------------------------------------------------------
 # cfg3 / cfg5: GF(p^k) matmul, both engines
 # ---------------------------------------------------------------------------
-ENGINES = ["i8", "f64", "fp4"]
+ENGINES = ["i8", "f64", "fp4", "fp4k"]
 
 
 class TestGFMatmul:
@@ -184,7 +184,7 @@ class TestGFMatmul:
     def test_golden(self, golden, golden_scalars, engine, fname, pre):
         f = _field(golden_scalars, fname)
         sfx = "_idx" if pre.startswith("cfg") else ""
-        if engine == "fp4" and f.p > 7:  # centred residues beyond E2M1's exact integers
+        if engine in ("fp4", "fp4k") and f.p > 7:  # centred residues beyond E2M1's exact integers
             with pytest.raises(Q.ParamsViolation):
                 f.matmul(golden[f"{pre}_a{sfx}"], golden[f"{pre}_b{sfx}"], engine=engine)
             return
