@@ -762,115 +762,146 @@ struct CombineW {
 
 __device__ __forceinline__ uint32_t byte_of(const uint32_t* in, int idx) { return (in[idx >> 2] >> (8 * (idx & 3))) & 0xFF; }
 
-// A [M, Kd, K] residues -> S planes [S][M][ld] of packed E2M1 nibbles.
-// Thread: one row, 32 consecutive kk (32K input bytes) -> 16 bytes per plane.
+// ---- SIMD-within-register helpers for residue bytes (values < 16) ----------
+// byte-wise v mod p for v < 2p (no carries between lanes)
+__device__ __forceinline__ uint32_t bytes_mod(uint32_t v, uint32_t p) {
+    const uint32_t t = v + (0x80u - p) * 0x01010101u;  // bit 7 set in lanes with v >= p
+    const uint32_t ge = (t >> 7) & 0x01010101u;
+    return v - ge * p;
+}
+// 4 byte lanes (values < 16) -> 16-bit field of 4 nibbles
+__device__ __forceinline__ uint32_t bytes_to_nibbles(uint32_t v) {
+    const uint32_t x = v | (v >> 4);
+    return __byte_perm(x, 0, 0x0020) & 0xFFFFu;
+}
+// 4 byte lanes of residues (< 8) -> their E2M1 codes (byte table lookup)
+__device__ __forceinline__ uint32_t bytes_to_codes(uint32_t v, uint32_t lut_lo, uint32_t lut_hi) {
+    return __byte_perm(lut_lo, lut_hi, bytes_to_nibbles(v));
+}
+
+// Rows [R, Kd, K] of residues -> S planes [S][R][ld] of packed E2M1 nibbles
+// (used for A directly and for B after an element transpose).
+// Thread: one row, 32 consecutive kk.  Coefficient i of 4 consecutive
+// elements is gathered into one word, the plane sums and mod p run on 4 byte
+// lanes at once, E2M1 codes come from one PRMT table lookup per 4 elements.
 template <int K>
-__global__ void __launch_bounds__(256) planes_a_kernel(const uint8_t* __restrict__ a, int64_t M, int64_t Kd, uint32_t p,
-                                                       uint32_t lut, uint8_t* __restrict__ out, int64_t ld,
-                                                       int64_t plane_stride) {
+__global__ void __launch_bounds__(256) planes_kernel(const uint8_t* __restrict__ src, int64_t R, int64_t Kd, uint32_t p,
+                                                     uint32_t lut_lo, uint32_t lut_hi, uint8_t* __restrict__ out,
+                                                     int64_t ld, int64_t plane_stride) {
     constexpr int S = K * (K + 1) / 2;
     const int64_t chunks = ld / 16;
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= M * chunks) return;
-    const int64_t m = idx / chunks, q = idx % chunks;
+    if (idx >= R * chunks) return;
+    const int64_t r = idx / chunks, q = idx % chunks;
     const int64_t kk0 = q * 32;
-    const uint8_t* src = a + (m * Kd + kk0) * K;
+    const uint8_t* row = src + (r * Kd + kk0) * K;
     uint32_t in[8 * K];
-    if (kk0 + 32 <= Kd && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+    if (kk0 + 32 <= Kd && ((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
 #pragma unroll
         for (int v = 0; v < 2 * K; ++v) {
-            const uint4 x = __ldg(reinterpret_cast<const uint4*>(src) + v);
+            const uint4 x = __ldg(reinterpret_cast<const uint4*>(row) + v);
             in[4 * v] = x.x; in[4 * v + 1] = x.y; in[4 * v + 2] = x.z; in[4 * v + 3] = x.w;
         }
     } else {
 #pragma unroll
         for (int v = 0; v < 8 * K; ++v) in[v] = 0;
 #pragma unroll
-        for (int e = 0; e < 32 * K; ++e)  // unrolled: in[] stays in registers
-            if (kk0 + e / K < Kd) in[e >> 2] |= (uint32_t)src[e] << (8 * (e & 3));
+        for (int e = 0; e < 32 * K; ++e)
+            if (kk0 + e / K < Kd) in[e >> 2] |= (uint32_t)row[e] << (8 * (e & 3));
     }
+    uint32_t w[S][4];
 #pragma unroll
-    for (int s = 0; s < S; ++s) {
-        const int ci = combo_first(K, s), cj = combo_second(K, s);
-        uint32_t w[4] = {0, 0, 0, 0};
+    for (int g = 0; g < 8; ++g) {  // 4 elements per group
+        uint32_t c[K];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-            uint32_t v = byte_of(in, e * K + ci);
-            if (cj != ci) {
-                v += byte_of(in, e * K + cj);
-                if (v >= p) v -= p;
-            }
-            w[e >> 3] |= ((lut >> (4 * v)) & 0xF) << (4 * (e & 7));
+        for (int i = 0; i < K; ++i) {
+            c[i] = 0;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) c[i] |= byte_of(in, (4 * g + e) * K + i) << (8 * e);
         }
-        *reinterpret_cast<uint4*>(out + s * plane_stride + m * ld + q * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int ci = combo_first(K, s), cj = combo_second(K, s);
+            const uint32_t v = ci == cj ? c[ci] : bytes_mod(c[ci] + c[cj], p);
+            const uint32_t nib = bytes_to_nibbles(bytes_to_codes(v, lut_lo, lut_hi));
+            if (g & 1) w[s][g >> 1] |= nib << 16;
+            else w[s][g >> 1] = nib;
+        }
     }
+#pragma unroll
+    for (int s = 0; s < S; ++s)
+        *reinterpret_cast<uint4*>(out + s * plane_stride + r * ld + q * 16) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
 }
 
-// B [Kd, N, K] residues -> S transposed planes [S][N][ld] of packed E2M1 nibbles.
-// Tile: 64 kk x 128 j staged in smem; thread = one j, 32 kk -> 16 bytes per plane.
+// B [Kd, N, K] -> S transposed planes [S][N][ld] of packed E2M1 nibbles.
+// A 64 kk x 128 j tile of B is staged in shared memory with 16-byte loads;
+// each thread then owns one j and 32 kk: it gathers coefficient i of 4
+// consecutive kk straight from the tile into one word and runs the same
+// byte-lane plane code as planes_kernel (16 bytes out per plane).
 constexpr int PB_KK = 64, PB_J = 128;
 template <int K>
 __global__ void __launch_bounds__(256) planes_b_kernel(const uint8_t* __restrict__ b, int64_t Kd, int64_t N, uint32_t p,
-                                                       uint32_t lut, uint8_t* __restrict__ out, int64_t ld,
-                                                       int64_t plane_stride, int tiles_kk, int tiles_j) {
+                                                       uint32_t lut_lo, uint32_t lut_hi, uint8_t* __restrict__ out,
+                                                       int64_t ld, int64_t plane_stride, int tiles_kk, int tiles_j) {
     constexpr int S = K * (K + 1) / 2;
     constexpr int ROWB = PB_J * K;
-    __shared__ __align__(16) uint8_t raw[PB_KK][ROWB + 16];
-    const bool vec_rows = ((N * K) % 16 == 0) && ((reinterpret_cast<uintptr_t>(b) & 15) == 0);
+    __shared__ __align__(16) uint8_t tile[PB_KK][ROWB + 16];
+    const bool vec_in = ((N * K) % 16 == 0) && ((reinterpret_cast<uintptr_t>(b) & 15) == 0);
     const int64_t ntiles = (int64_t)tiles_kk * tiles_j;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t kk0 = (tile % tiles_kk) * PB_KK, j0 = (tile / tiles_kk) * PB_J;
+    const int jl = threadIdx.x % PB_J, ch = threadIdx.x / PB_J;  // 2 chunks of 32 kk
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t kk0 = (t % tiles_kk) * PB_KK, j0 = (t / tiles_kk) * PB_J;
         __syncthreads();
-        if (vec_rows && j0 + PB_J <= N) {
+        if (vec_in && j0 + PB_J <= N) {
             for (int i = threadIdx.x; i < PB_KK * (ROWB / 16); i += blockDim.x) {
-                const int r = i / (ROWB / 16), q = i % (ROWB / 16);
-                const int64_t gk = kk0 + r;
+                const int rr = i / (ROWB / 16), qq = i % (ROWB / 16);
+                const int64_t gk = kk0 + rr;
                 uint4 v = make_uint4(0, 0, 0, 0);
-                if (gk < Kd) v = __ldg(reinterpret_cast<const uint4*>(b + gk * N * K + j0 * K) + q);
-                *reinterpret_cast<uint4*>(&raw[r][q * 16]) = v;
+                if (gk < Kd) v = __ldg(reinterpret_cast<const uint4*>(b + gk * N * K + j0 * K) + qq);
+                *reinterpret_cast<uint4*>(&tile[rr][qq * 16]) = v;
             }
         } else {
             for (int i = threadIdx.x; i < PB_KK * ROWB; i += blockDim.x) {
-                const int r = i / ROWB, c = i % ROWB;
-                const int64_t gk = kk0 + r, gj = j0 + c / K;
-                raw[r][c] = (gk < Kd && gj < N) ? b[gk * N * K + j0 * K + c] : 0;
+                const int rr = i / ROWB, cc = i % ROWB;
+                const int64_t gk = kk0 + rr, gj = j0 + cc / K;
+                tile[rr][cc] = (gk < Kd && gj < N) ? b[gk * N * K + j0 * K + cc] : 0;
             }
         }
         __syncthreads();
-        const int jl = threadIdx.x % PB_J, ch = threadIdx.x / PB_J;  // 2 chunks of 32 kk
         const int64_t gj = j0 + jl;
-        if (gj >= N) continue;
+        const int64_t col = (kk0 + ch * 32) / 2;
+        if (gj >= N || col + 16 > ld) continue;
+        const uint8_t* tcol = &tile[ch * 32][jl * K];
         uint32_t w[S][4];
 #pragma unroll
-        for (int s = 0; s < S; ++s) w[s][0] = w[s][1] = w[s][2] = w[s][3] = 0;
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
+        for (int g = 0; g < 8; ++g) {
             uint32_t c[K];
 #pragma unroll
-            for (int i = 0; i < K; ++i) c[i] = raw[ch * 32 + e][jl * K + i];
+            for (int i = 0; i < K; ++i) {
+                c[i] = 0;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) c[i] |= (uint32_t)tcol[(4 * g + e) * (ROWB + 16) + i] << (8 * e);
+            }
 #pragma unroll
             for (int s = 0; s < S; ++s) {
                 const int ci = combo_first(K, s), cj = combo_second(K, s);
-                uint32_t v = c[ci];
-                if (cj != ci) {
-                    v += c[cj];
-                    if (v >= p) v -= p;
-                }
-                w[s][e >> 3] |= ((lut >> (4 * v)) & 0xF) << (4 * (e & 7));
+                const uint32_t v = ci == cj ? c[ci] : bytes_mod(c[ci] + c[cj], p);
+                const uint32_t nib = bytes_to_nibbles(bytes_to_codes(v, lut_lo, lut_hi));
+                if (g & 1) w[s][g >> 1] |= nib << 16;
+                else w[s][g >> 1] = nib;
             }
         }
-        const int64_t col = (kk0 + ch * 32) / 2;
-        if (col + 16 <= ld) {
 #pragma unroll
-            for (int s = 0; s < S; ++s)
-                *reinterpret_cast<uint4*>(out + s * plane_stride + gj * ld + col) =
-                    make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
-        }
+        for (int s = 0; s < S; ++s)
+            *reinterpret_cast<uint4*>(out + s * plane_stride + gj * ld + col) =
+                make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
     }
 }
 
 // D planes [S][M][ldd] (nibbles, N columns) -> C [M][N][K] uint8 residues.
-// Thread: one row, 32 consecutive columns.
+// Thread: one row, 32 consecutive columns.  The S weighted plane values are
+// summed on 4 byte lanes at once (W[l][s] * d <= 36, S <= 6 -> < 256), then
+// each lane is reduced mod p.
 template <int K>
 __global__ void __launch_bounds__(256) combine_kernel(const uint8_t* __restrict__ d, int64_t M, int64_t N, int64_t ldd,
                                                       int64_t plane_stride, uint32_t p, uint32_t magic, CombineW cw,
@@ -884,22 +915,38 @@ __global__ void __launch_bounds__(256) combine_kernel(const uint8_t* __restrict_
     uint32_t dv[S][4];
 #pragma unroll
     for (int s = 0; s < S; ++s) {
-        const uint8_t* src = d + s * plane_stride + m * ldd + j0 / 2;
-        const uint4 x = *reinterpret_cast<const uint4*>(src);  // ldd is a multiple of 16 and covers 32 columns
+        const uint4 x = *reinterpret_cast<const uint4*>(d + s * plane_stride + m * ldd + j0 / 2);
         dv[s][0] = x.x; dv[s][1] = x.y; dv[s][2] = x.z; dv[s][3] = x.w;
     }
     uint32_t o[8 * K];
 #pragma unroll
     for (int v = 0; v < 8 * K; ++v) o[v] = 0;
 #pragma unroll
-    for (int e = 0; e < 32; ++e) {
+    for (int g = 0; g < 8; ++g) {  // 4 columns per group
+        uint32_t db[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {  // 4 nibbles -> 4 byte lanes
+            const uint32_t h = (dv[s][g >> 1] >> (16 * (g & 1))) & 0xFFFFu;
+            db[s] = (h & 0xF) | ((h & 0xF0) << 4) | ((h & 0xF00) << 8) | ((h & 0xF000) << 12);
+        }
 #pragma unroll
         for (int l = 0; l < K; ++l) {
-            uint32_t acc = 0;
+            uint32_t tot[4] = {0, 0, 0, 0};
 #pragma unroll
-            for (int s = 0; s < S; ++s) acc += cw.w[l][s] * ((dv[s][e >> 3] >> (4 * (e & 7))) & 0xF);
-            const int pos = e * K + l;
-            o[pos >> 2] |= mod_small(acc, p, magic) << (8 * (pos & 3));
+            for (int s0 = 0; s0 < S; s0 += 6) {  // <= 6 terms of <= 36 per lane: < 256
+                uint32_t acc = 0;
+#pragma unroll
+                for (int s = s0; s < S && s < s0 + 6; ++s) acc += db[s] * cw.w[l][s];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) tot[e] += (acc >> (8 * e)) & 0xFF;
+            }
+            // reduce each lane mod p, place at output byte (4g+e)*K + l
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t v = mod_small(tot[e], p, magic);
+                const int pos = (4 * g + e) * K + l;
+                o[pos >> 2] |= v << (8 * (pos & 3));
+            }
         }
     }
     uint8_t* dst = c + (m * N + j0) * K;
@@ -909,7 +956,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const uint8_t* __restrict_
             reinterpret_cast<uint4*>(dst)[v] = make_uint4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
     } else {
 #pragma unroll
-        for (int e = 0; e < 32 * K; ++e)  // unrolled: o[] stays in registers
+        for (int e = 0; e < 32 * K; ++e)
             if (j0 + e / K < N) dst[e] = (uint8_t)(o[e >> 2] >> (8 * (e & 3)));
     }
 }
@@ -934,16 +981,17 @@ static KaraLayout kara_plan(int64_t m, int64_t kdim, int64_t n, int k) {
 
 template <int K>
 static void launch_planes(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n, uint32_t p,
-                          uint32_t lut, const KaraLayout& L, uint8_t* as, uint8_t* bs, cudaStream_t s) {
+                          uint32_t lut_lo, uint32_t lut_hi, const KaraLayout& L, uint8_t* as, uint8_t* bs,
+                          cudaStream_t s) {
     const int64_t ta = m * (L.ldk / 16);
     QADIC_TIMED("fp4k planes A", s,
-                planes_a_kernel<K><<<(unsigned)((ta + 255) / 256), 256, 0, s>>>(a, m, kdim, p, lut, as, L.ldk,
-                                                                                  m * L.ldk));
+                planes_kernel<K><<<(unsigned)((ta + 255) / 256), 256, 0, s>>>(a, m, kdim, p, lut_lo, lut_hi, as,
+                                                                                L.ldk, m * L.ldk));
     const int tk = (int)((kdim + PB_KK - 1) / PB_KK), tj = (int)((n + PB_J - 1) / PB_J);
     const int64_t tiles = (int64_t)tk * tj;
     const int grid = (int)(tiles < 8 * num_sms() ? tiles : 8 * num_sms());
     QADIC_TIMED("fp4k planes B", s,
-                planes_b_kernel<K><<<grid, 256, 0, s>>>(b, kdim, n, p, lut, bs, L.ldk, n * L.ldk, tk, tj));
+                planes_b_kernel<K><<<grid, 256, 0, s>>>(b, kdim, n, p, lut_lo, lut_hi, bs, L.ldk, n * L.ldk, tk, tj));
 }
 
 template <int K>
@@ -960,17 +1008,24 @@ static int run_kara(const FieldConst& f, const uint8_t* a, const uint8_t* b, int
                     void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s) {
     const int k = (int)f.k;
     KaraLayout L = kara_plan(m, kdim, n, k);
-    QADIC_REQUIRE(ws != nullptr && ws_bytes >= L.a_bytes + L.b_bytes + L.d_bytes, QADIC_ERR_VALUE,
-                  "workspace too small (%zu < %zu)", ws_bytes, L.a_bytes + L.b_bytes + L.d_bytes);
+    const size_t need = L.a_bytes + L.b_bytes + L.d_bytes;
+    QADIC_REQUIRE(ws != nullptr && ws_bytes >= need, QADIC_ERR_VALUE, "workspace too small (%zu < %zu)", ws_bytes,
+                  need);
+    // E2M1 codes of the centred residues as an 8-entry byte table (PRMT lookup)
     const uint32_t lut = centred_e2m1_lut(f.p);
+    uint32_t lut_lo = 0, lut_hi = 0;
+    for (int v = 0; v < 4; ++v) {
+        lut_lo |= ((lut >> (4 * v)) & 0xF) << (8 * v);
+        lut_hi |= ((lut >> (4 * (v + 4))) & 0xF) << (8 * v);
+    }
     uint8_t* as = static_cast<uint8_t*>(ws);
     uint8_t* bs = as + L.a_bytes;
     uint8_t* dd = bs + L.b_bytes;
     switch (k) {
-        case 1: launch_planes<1>(a, b, m, kdim, n, f.p, lut, L, as, bs, s); break;
-        case 2: launch_planes<2>(a, b, m, kdim, n, f.p, lut, L, as, bs, s); break;
-        case 3: launch_planes<3>(a, b, m, kdim, n, f.p, lut, L, as, bs, s); break;
-        default: launch_planes<4>(a, b, m, kdim, n, f.p, lut, L, as, bs, s); break;
+        case 1: launch_planes<1>(a, b, m, kdim, n, f.p, lut_lo, lut_hi, L, as, bs, s); break;
+        case 2: launch_planes<2>(a, b, m, kdim, n, f.p, lut_lo, lut_hi, L, as, bs, s); break;
+        case 3: launch_planes<3>(a, b, m, kdim, n, f.p, lut_lo, lut_hi, L, as, bs, s); break;
+        default: launch_planes<4>(a, b, m, kdim, n, f.p, lut_lo, lut_hi, L, as, bs, s); break;
     }
     int rc = check_launch("fp4k planes");
     if (rc) return rc;
