@@ -70,7 +70,10 @@ struct Geo {
     static constexpr int A_BYTES = BM * BK;
     static constexpr int B_BYTES = B_ROWS * BK;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int STAGES_N = PAIR ? 6 : STAGES;
+    // as many stages as 227 KB of shared memory holds (deeper prefetch hides
+    // the L2 misses at tile boundaries of short-K plane products)
+    static constexpr int STAGES_N = PAIR ? ((232448 - 1280) / STAGE_BYTES > 8 ? 8 : (232448 - 1280) / STAGE_BYTES)
+                                         : STAGES;
     static constexpr size_t SMEM = (size_t)STAGES_N * STAGE_BYTES + 1024 + 256;
     static constexpr int TILE_M = PAIR ? 2 * BM : BM;
 };
@@ -755,40 +758,191 @@ __host__ __device__ constexpr int combo_second(int k, int s) {
                                     : (s == 4 ? 1 : s == 5 ? 2 : s == 6 ? 3 : s == 7 ? 2 : 3));
 }
 
-constexpr int KMAX_S = 10;
-struct CombineW {
-    uint8_t w[kMaxK][KMAX_S];  // C_l = sum_s w[l][s] * D_s  (mod p)
-};
-
 __device__ __forceinline__ uint32_t byte_of(const uint32_t* in, int idx) { return (in[idx >> 2] >> (8 * (idx & 3))) & 0xFF; }
 
-// ---- SIMD-within-register helpers for residue bytes (values < 16) ----------
-// byte-wise v mod p for v < 2p (no carries between lanes)
-__device__ __forceinline__ uint32_t bytes_mod(uint32_t v, uint32_t p) {
-    const uint32_t t = v + (0x80u - p) * 0x01010101u;  // bit 7 set in lanes with v >= p
-    const uint32_t ge = (t >> 7) & 0x01010101u;
-    return v - ge * p;
+constexpr int KMAX_S = 8;  // planes per product handled by the nibble transpose
+
+// The plane products of one field: D_s = (sum_i E[s][i] a_i)(sum_i E[s][i] b_i)
+// (all mod p), and C_l = sum_s W[l][s] D_s (mod p).
+//   Toom-Cook over F_p when 2k-1 <= p+1: evaluation at 2k-1 distinct points of
+//     F_p u {inf}, W = (X^t mod f) o Vandermonde^-1  -> S = 2k-1 planes
+//     (cfg5, GF(7^3): 5 plane GEMMs where the expanded form does 9 products);
+//   otherwise Karatsuba: D_i = a_i b_i, D_ij = (a_i + a_j)(b_i + b_j)
+//     -> S = k(k+1)/2 planes (GF(3^3): 6).
+struct PlaneSpec {
+    int S;
+    uint8_t E[KMAX_S][kMaxK];
+    uint8_t W[kMaxK][KMAX_S];
+};
+
+static int64_t pmod(int64_t x, int64_t p) { return ((x % p) + p) % p; }
+static int64_t ipow_mod(int64_t x, int e, int64_t p) {
+    int64_t r = 1;
+    for (int i = 0; i < e; ++i) r = r * x % p;
+    return r;
 }
+
+// inverse of an n x n matrix over F_p (n <= 8); false if singular
+static bool inv_mod_p(int n, int64_t (*a)[KMAX_S], int64_t (*out)[KMAX_S], int64_t p) {
+    int64_t m[KMAX_S][2 * KMAX_S];
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < 2 * n; ++j) m[i][j] = j < n ? pmod(a[i][j], p) : (j - n == i);
+    for (int c = 0; c < n; ++c) {
+        int piv = -1;
+        for (int r = c; r < n; ++r)
+            if (m[r][c]) { piv = r; break; }
+        if (piv < 0) return false;
+        for (int j = 0; j < 2 * n; ++j) { const int64_t t = m[c][j]; m[c][j] = m[piv][j]; m[piv][j] = t; }
+        int64_t iv = 1;
+        for (int64_t e = p - 2, b = m[c][c]; e; e >>= 1, b = b * b % p)
+            if (e & 1) iv = iv * b % p;
+        for (int j = 0; j < 2 * n; ++j) m[c][j] = m[c][j] * iv % p;
+        for (int r = 0; r < n; ++r)
+            if (r != c && m[r][c]) {
+                const int64_t fct = m[r][c];
+                for (int j = 0; j < 2 * n; ++j) m[r][j] = pmod(m[r][j] - fct * m[c][j], p);
+            }
+    }
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) out[i][j] = m[i][n + j];
+    return true;
+}
+
+static bool plan_planes(const FieldConst& f, PlaneSpec* ps) {
+    const int k = (int)f.k;
+    const int64_t p = f.p;
+    const int n = 2 * k - 1;
+    *ps = PlaneSpec{};
+    if (n <= p + 1) {  // Toom-Cook: points inf, 0, 1, -1, 2, -2, ...
+        int64_t pts[KMAX_S];
+        bool inf[KMAX_S] = {};
+        int cnt = 0;
+        inf[cnt++] = true;
+        const int64_t cand[] = {0, 1, -1, 2, -2, 3, -3};
+        for (int64_t c : cand) {
+            if (cnt == n) break;
+            const int64_t v = pmod(c, p);
+            bool dup = false;
+            for (int i = 1; i < cnt; ++i) dup |= (!inf[i] && pts[i] == v);
+            if (!dup) pts[cnt++] = v;
+        }
+        if (cnt != n) return false;
+        int64_t V[KMAX_S][KMAX_S] = {}, Vi[KMAX_S][KMAX_S] = {};
+        for (int s = 0; s < n; ++s) {
+            for (int i = 0; i < k; ++i) ps->E[s][i] = (uint8_t)(inf[s] ? (i == k - 1) : ipow_mod(pts[s], i, p));
+            for (int t = 0; t < n; ++t) V[s][t] = inf[s] ? (t == n - 1) : ipow_mod(pts[s], t, p);
+        }
+        if (!inv_mod_p(n, V, Vi, p)) return false;
+        for (int l = 0; l < k; ++l)
+            for (int s = 0; s < n; ++s) {
+                int64_t acc = 0;
+                for (int t = 0; t < n; ++t) acc += (int64_t)f.xpow[t][l] * Vi[t][s];
+                ps->W[l][s] = (uint8_t)pmod(acc, p);
+            }
+        ps->S = n;
+        return true;
+    }
+    const int S = k * (k + 1) / 2;
+    if (S > KMAX_S) return false;
+    for (int s = 0; s < S; ++s) {
+        const int i = combo_first(k, s), j = combo_second(k, s);
+        ps->E[s][i] = 1;
+        ps->E[s][j] = 1;
+        for (int l = 0; l < k; ++l) {
+            int64_t acc = 0;
+            if (i == j) {
+                acc += f.xpow[2 * i][l];
+                for (int o = 0; o < k; ++o)
+                    if (o != i) acc -= f.xpow[i + o][l];
+            } else {
+                acc += f.xpow[i + j][l];
+            }
+            ps->W[l][s] = (uint8_t)pmod(acc, p);
+        }
+    }
+    ps->S = S;
+    return true;
+}
+
+// T[code] = E2M1 nibble of plane s of the element with this code, at bit 4s
+__global__ void plane_table_kernel(uint32_t p, int k, int S, PlaneSpec ps, uint32_t lut, uint32_t* __restrict__ tab) {
+    int ncodes = 1;
+    for (int i = 0; i < k; ++i) ncodes *= (int)p;
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= ncodes) return;
+    uint32_t dig[kMaxK] = {};
+    int r = c;
+    for (int i = 0; i < k; ++i) {
+        dig[i] = (uint32_t)(r % (int)p);
+        r /= (int)p;
+    }
+    uint32_t w = 0;
+    for (int s = 0; s < S; ++s) {
+        uint32_t v = 0;
+        for (int i = 0; i < k; ++i) v += ps.E[s][i] * dig[i];
+        w |= ((lut >> (4 * (v % p))) & 0xF) << (4 * s);
+    }
+    tab[c] = w;
+}
+
 // 4 byte lanes (values < 16) -> 16-bit field of 4 nibbles
 __device__ __forceinline__ uint32_t bytes_to_nibbles(uint32_t v) {
     const uint32_t x = v | (v >> 4);
     return __byte_perm(x, 0, 0x0020) & 0xFFFFu;
 }
-// 4 byte lanes of residues (< 8) -> their E2M1 codes (byte table lookup)
-__device__ __forceinline__ uint32_t bytes_to_codes(uint32_t v, uint32_t lut_lo, uint32_t lut_hi) {
-    return __byte_perm(lut_lo, lut_hi, bytes_to_nibbles(v));
+// k = 1 (a single plane): 4 residues (< 8) -> 4 E2M1 nibbles by one PRMT table lookup
+__device__ __forceinline__ uint32_t residues_to_e2m1(uint32_t v, uint32_t lut_lo, uint32_t lut_hi) {
+    return bytes_to_nibbles(__byte_perm(lut_lo, lut_hi, bytes_to_nibbles(v)));
+}
+__device__ __forceinline__ void byte_lut_from_table(const uint32_t* tab, uint32_t p, uint32_t& lo, uint32_t& hi) {
+    lo = hi = 0;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+        lo |= ((uint32_t)v < p ? (tab[v] & 0xF) : 0u) << (8 * v);
+        hi |= ((uint32_t)(v + 4) < p ? (tab[v + 4] & 0xF) : 0u) << (8 * v);
+    }
 }
 
-// Rows [R, Kd, K] of residues -> S planes [S][R][ld] of packed E2M1 nibbles
-// (used for A directly and for B after an element transpose).
-// Thread: one row, 32 consecutive kk.  Coefficient i of 4 consecutive
-// elements is gathered into one word, the plane sums and mod p run on 4 byte
-// lanes at once, E2M1 codes come from one PRMT table lookup per 4 elements.
+// 8 x 8 transpose of 4-bit cells: on return nibble e of x[s] = old nibble s of x[e]
+__device__ __forceinline__ void transpose8_nibbles(uint32_t (&x)[8]) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+        if ((r & 4) == 0) {
+            const uint32_t t = ((x[r] >> 16) ^ x[r + 4]) & 0x0000FFFFu;
+            x[r] ^= t << 16;
+            x[r + 4] ^= t;
+        }
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+        if ((r & 2) == 0) {
+            const uint32_t t = ((x[r] >> 8) ^ x[r + 2]) & 0x00FF00FFu;
+            x[r] ^= t << 8;
+            x[r + 2] ^= t;
+        }
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+        if ((r & 1) == 0) {
+            const uint32_t t = ((x[r] >> 4) ^ x[r + 1]) & 0x0F0F0F0Fu;
+            x[r] ^= t << 4;
+            x[r + 1] ^= t;
+        }
+}
+
+constexpr int PT_CODES = 1024;
+
+// Rows [R, Kd, K] of residues -> S planes [S][R][ld] of packed E2M1 nibbles.
+// Thread: one row, 32 consecutive kk.  Per element one shared-memory table
+// lookup yields all S plane nibbles; an 8x8 nibble transpose turns 8
+// elements' lookups into the 8 plane words.
 template <int K>
 __global__ void __launch_bounds__(256) planes_kernel(const uint8_t* __restrict__ src, int64_t R, int64_t Kd, uint32_t p,
-                                                     uint32_t lut_lo, uint32_t lut_hi, uint8_t* __restrict__ out,
-                                                     int64_t ld, int64_t plane_stride) {
-    constexpr int S = K * (K + 1) / 2;
+                                                     const uint32_t* __restrict__ gtab, int S,
+                                                     uint8_t* __restrict__ out, int64_t ld, int64_t plane_stride) {
+    __shared__ uint32_t tab[PT_CODES];
+    int ncodes = 1;
+    for (int i = 0; i < K; ++i) ncodes *= (int)p;
+    for (int i = threadIdx.x; i < ncodes; i += blockDim.x) tab[i] = gtab[i];
+    __syncthreads();
     const int64_t chunks = ld / 16;
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= R * chunks) return;
@@ -809,43 +963,52 @@ __global__ void __launch_bounds__(256) planes_kernel(const uint8_t* __restrict__
         for (int e = 0; e < 32 * K; ++e)
             if (kk0 + e / K < Kd) in[e >> 2] |= (uint32_t)row[e] << (8 * (e & 3));
     }
-    uint32_t w[S][4];
+    if constexpr (K == 1) {  // one plane: 4 residues per PRMT lookup
+        uint32_t lo, hi;
+        byte_lut_from_table(tab, p, lo, hi);
+        uint32_t o[4];
 #pragma unroll
-    for (int g = 0; g < 8; ++g) {  // 4 elements per group
-        uint32_t c[K];
-#pragma unroll
-        for (int i = 0; i < K; ++i) {
-            c[i] = 0;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) c[i] |= byte_of(in, (4 * g + e) * K + i) << (8 * e);
-        }
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            const int ci = combo_first(K, s), cj = combo_second(K, s);
-            const uint32_t v = ci == cj ? c[ci] : bytes_mod(c[ci] + c[cj], p);
-            const uint32_t nib = bytes_to_nibbles(bytes_to_codes(v, lut_lo, lut_hi));
-            if (g & 1) w[s][g >> 1] |= nib << 16;
-            else w[s][g >> 1] = nib;
-        }
+        for (int g = 0; g < 4; ++g)
+            o[g] = residues_to_e2m1(in[2 * g], lo, hi) | (residues_to_e2m1(in[2 * g + 1], lo, hi) << 16);
+        *reinterpret_cast<uint4*>(out + r * ld + q * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+        return;
     }
+    uint32_t w[KMAX_S][4];
 #pragma unroll
-    for (int s = 0; s < S; ++s)
-        *reinterpret_cast<uint4*>(out + s * plane_stride + r * ld + q * 16) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
+    for (int g = 0; g < 4; ++g) {  // 8 elements per group
+        uint32_t x[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            uint32_t code = 0;
+#pragma unroll
+            for (int i = K - 1; i >= 0; --i) code = code * p + byte_of(in, (8 * g + e) * K + i);
+            x[e] = tab[code];
+        }
+        transpose8_nibbles(x);
+#pragma unroll
+        for (int s = 0; s < KMAX_S; ++s) w[s][g] = x[s];
+    }
+    uint8_t* dst = out + r * ld + q * 16;
+#pragma unroll
+    for (int s = 0; s < KMAX_S; ++s)
+        if (s < S) *reinterpret_cast<uint4*>(dst + s * plane_stride) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
 }
 
-// B [Kd, N, K] -> S transposed planes [S][N][ld] of packed E2M1 nibbles.
-// A 64 kk x 128 j tile of B is staged in shared memory with 16-byte loads;
-// each thread then owns one j and 32 kk: it gathers coefficient i of 4
-// consecutive kk straight from the tile into one word and runs the same
-// byte-lane plane code as planes_kernel (16 bytes out per plane).
+// B [Kd, N, K] -> S transposed planes [S][N][ld]: a 64 kk x 128 j tile of B is
+// staged in shared memory with 16-byte loads; each thread then owns one j and
+// 32 kk and builds its plane words like planes_kernel.
 constexpr int PB_KK = 64, PB_J = 128;
 template <int K>
 __global__ void __launch_bounds__(256) planes_b_kernel(const uint8_t* __restrict__ b, int64_t Kd, int64_t N, uint32_t p,
-                                                       uint32_t lut_lo, uint32_t lut_hi, uint8_t* __restrict__ out,
-                                                       int64_t ld, int64_t plane_stride, int tiles_kk, int tiles_j) {
-    constexpr int S = K * (K + 1) / 2;
+                                                       const uint32_t* __restrict__ gtab, int S,
+                                                       uint8_t* __restrict__ out, int64_t ld, int64_t plane_stride,
+                                                       int tiles_kk, int tiles_j) {
     constexpr int ROWB = PB_J * K;
     __shared__ __align__(16) uint8_t tile[PB_KK][ROWB + 16];
+    __shared__ uint32_t tab[PT_CODES];
+    int ncodes = 1;
+    for (int i = 0; i < K; ++i) ncodes *= (int)p;
+    for (int i = threadIdx.x; i < ncodes; i += blockDim.x) tab[i] = gtab[i];
     const bool vec_in = ((N * K) % 16 == 0) && ((reinterpret_cast<uintptr_t>(b) & 15) == 0);
     const int64_t ntiles = (int64_t)tiles_kk * tiles_j;
     const int jl = threadIdx.x % PB_J, ch = threadIdx.x / PB_J;  // 2 chunks of 32 kk
@@ -872,80 +1035,94 @@ __global__ void __launch_bounds__(256) planes_b_kernel(const uint8_t* __restrict
         const int64_t col = (kk0 + ch * 32) / 2;
         if (gj >= N || col + 16 > ld) continue;
         const uint8_t* tcol = &tile[ch * 32][jl * K];
-        uint32_t w[S][4];
+        if constexpr (K == 1) {  // one plane: gather 4 kk per word, PRMT lookup
+            uint32_t lo, hi;
+            byte_lut_from_table(tab, p, lo, hi);
+            uint32_t o[4];
 #pragma unroll
-        for (int g = 0; g < 8; ++g) {
-            uint32_t c[K];
+            for (int g = 0; g < 4; ++g) {
+                uint32_t v0 = 0, v1 = 0;
 #pragma unroll
-            for (int i = 0; i < K; ++i) {
-                c[i] = 0;
-#pragma unroll
-                for (int e = 0; e < 4; ++e) c[i] |= (uint32_t)tcol[(4 * g + e) * (ROWB + 16) + i] << (8 * e);
+                for (int e = 0; e < 4; ++e) {
+                    v0 |= (uint32_t)tcol[(8 * g + e) * (ROWB + 16)] << (8 * e);
+                    v1 |= (uint32_t)tcol[(8 * g + 4 + e) * (ROWB + 16)] << (8 * e);
+                }
+                o[g] = residues_to_e2m1(v0, lo, hi) | (residues_to_e2m1(v1, lo, hi) << 16);
             }
-#pragma unroll
-            for (int s = 0; s < S; ++s) {
-                const int ci = combo_first(K, s), cj = combo_second(K, s);
-                const uint32_t v = ci == cj ? c[ci] : bytes_mod(c[ci] + c[cj], p);
-                const uint32_t nib = bytes_to_nibbles(bytes_to_codes(v, lut_lo, lut_hi));
-                if (g & 1) w[s][g >> 1] |= nib << 16;
-                else w[s][g >> 1] = nib;
-            }
+            *reinterpret_cast<uint4*>(out + gj * ld + col) = make_uint4(o[0], o[1], o[2], o[3]);
+            continue;
         }
+        uint32_t w[KMAX_S][4];
 #pragma unroll
-        for (int s = 0; s < S; ++s)
-            *reinterpret_cast<uint4*>(out + s * plane_stride + gj * ld + col) =
-                make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
+        for (int g = 0; g < 4; ++g) {
+            uint32_t x[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                uint32_t code = 0;
+#pragma unroll
+                for (int i = K - 1; i >= 0; --i) code = code * p + tcol[(8 * g + e) * (ROWB + 16) + i];
+                x[e] = tab[code];
+            }
+            transpose8_nibbles(x);
+#pragma unroll
+            for (int s = 0; s < KMAX_S; ++s) w[s][g] = x[s];
+        }
+        uint8_t* dst = out + gj * ld + col;
+#pragma unroll
+        for (int s = 0; s < KMAX_S; ++s)
+            if (s < S) *reinterpret_cast<uint4*>(dst + s * plane_stride) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
     }
 }
 
 // D planes [S][M][ldd] (nibbles, N columns) -> C [M][N][K] uint8 residues.
-// Thread: one row, 32 consecutive columns.  The S weighted plane values are
-// summed on 4 byte lanes at once (W[l][s] * d <= 36, S <= 6 -> < 256), then
-// each lane is reduced mod p.
+// Thread: one row, 32 consecutive columns.  The even and odd columns of a
+// plane word are split into byte lanes (x & 0x0F0F0F0F, (x >> 4) & ...) and the
+// weighted plane sum runs on 4 lanes at once (<= 6 terms of <= 36 per pass,
+// < 256), then each lane is reduced mod p.
 template <int K>
 __global__ void __launch_bounds__(256) combine_kernel(const uint8_t* __restrict__ d, int64_t M, int64_t N, int64_t ldd,
-                                                      int64_t plane_stride, uint32_t p, uint32_t magic, CombineW cw,
-                                                      uint8_t* __restrict__ c) {
-    constexpr int S = K * (K + 1) / 2;
+                                                      int64_t plane_stride, int S, uint32_t p, uint32_t magic,
+                                                      PlaneSpec ps, uint8_t* __restrict__ c) {
     const int64_t chunks = (N + 31) / 32;
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= M * chunks) return;
     const int64_t m = idx / chunks, q = idx % chunks;
     const int64_t j0 = q * 32;
-    uint32_t dv[S][4];
+    uint32_t dv[KMAX_S][4];
 #pragma unroll
-    for (int s = 0; s < S; ++s) {
-        const uint4 x = *reinterpret_cast<const uint4*>(d + s * plane_stride + m * ldd + j0 / 2);
-        dv[s][0] = x.x; dv[s][1] = x.y; dv[s][2] = x.z; dv[s][3] = x.w;
+    for (int s = 0; s < KMAX_S; ++s) {
+        if (s < S) {
+            const uint4 x = *reinterpret_cast<const uint4*>(d + s * plane_stride + m * ldd + j0 / 2);
+            dv[s][0] = x.x; dv[s][1] = x.y; dv[s][2] = x.z; dv[s][3] = x.w;
+        } else {
+            dv[s][0] = dv[s][1] = dv[s][2] = dv[s][3] = 0;
+        }
     }
     uint32_t o[8 * K];
 #pragma unroll
     for (int v = 0; v < 8 * K; ++v) o[v] = 0;
 #pragma unroll
-    for (int g = 0; g < 8; ++g) {  // 4 columns per group
-        uint32_t db[S];
+    for (int g = 0; g < 4; ++g) {  // one plane word = 8 columns
 #pragma unroll
-        for (int s = 0; s < S; ++s) {  // 4 nibbles -> 4 byte lanes
-            const uint32_t h = (dv[s][g >> 1] >> (16 * (g & 1))) & 0xFFFFu;
-            db[s] = (h & 0xF) | ((h & 0xF0) << 4) | ((h & 0xF00) << 8) | ((h & 0xF000) << 12);
-        }
+        for (int half = 0; half < 2; ++half) {  // even / odd columns
 #pragma unroll
-        for (int l = 0; l < K; ++l) {
-            uint32_t tot[4] = {0, 0, 0, 0};
+            for (int l = 0; l < K; ++l) {
+                uint32_t tot[4] = {0, 0, 0, 0};
 #pragma unroll
-            for (int s0 = 0; s0 < S; s0 += 6) {  // <= 6 terms of <= 36 per lane: < 256
-                uint32_t acc = 0;
+                for (int s0 = 0; s0 < KMAX_S; s0 += 6) {
+                    uint32_t acc = 0;
 #pragma unroll
-                for (int s = s0; s < S && s < s0 + 6; ++s) acc += db[s] * cw.w[l][s];
+                    for (int s = s0; s < KMAX_S && s < s0 + 6; ++s)
+                        acc += ((dv[s][g] >> (4 * half)) & 0x0F0F0F0Fu) * ps.W[l][s];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) tot[e] += (acc >> (8 * e)) & 0xFF;
-            }
-            // reduce each lane mod p, place at output byte (4g+e)*K + l
+                    for (int e = 0; e < 4; ++e) tot[e] += (acc >> (8 * e)) & 0xFF;
+                }
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const uint32_t v = mod_small(tot[e], p, magic);
-                const int pos = (4 * g + e) * K + l;
-                o[pos >> 2] |= v << (8 * (pos & 3));
+                for (int e = 0; e < 4; ++e) {
+                    const int col = 8 * g + 2 * e + half;  // column within the 32-column chunk
+                    const int pos = col * K + l;
+                    o[pos >> 2] |= mod_small(tot[e], p, magic) << (8 * (pos & 3));
+                }
             }
         }
     }
@@ -965,14 +1142,15 @@ struct KaraLayout {
     int S;
     int64_t ldk;   // bytes per plane row of A_s / B_s (packed K)
     int64_t ldd;   // bytes per plane row of D_s (packed N)
-    size_t a_bytes, b_bytes, d_bytes;
+    size_t tab_bytes, a_bytes, b_bytes, d_bytes;
 };
 
-static KaraLayout kara_plan(int64_t m, int64_t kdim, int64_t n, int k) {
+static KaraLayout kara_plan(int S, int64_t m, int64_t kdim, int64_t n, int k) {
     KaraLayout L;
-    L.S = k * (k + 1) / 2;
+    L.S = S;
     L.ldk = round_up((kdim + 1) / 2, 16);
     L.ldd = round_up((n + 1) / 2, 16);
+    L.tab_bytes = PT_CODES * sizeof(uint32_t);
     L.a_bytes = (size_t)round_up(L.S * m * L.ldk, 1024);
     L.b_bytes = (size_t)round_up(L.S * n * L.ldk, 1024);
     L.d_bytes = k == 1 ? 0 : (size_t)round_up(L.S * m * L.ldd, 1024);
@@ -981,51 +1159,51 @@ static KaraLayout kara_plan(int64_t m, int64_t kdim, int64_t n, int k) {
 
 template <int K>
 static void launch_planes(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n, uint32_t p,
-                          uint32_t lut_lo, uint32_t lut_hi, const KaraLayout& L, uint8_t* as, uint8_t* bs,
-                          cudaStream_t s) {
+                          const uint32_t* tab, const KaraLayout& L, uint8_t* as, uint8_t* bs, cudaStream_t s) {
     const int64_t ta = m * (L.ldk / 16);
     QADIC_TIMED("fp4k planes A", s,
-                planes_kernel<K><<<(unsigned)((ta + 255) / 256), 256, 0, s>>>(a, m, kdim, p, lut_lo, lut_hi, as,
-                                                                                L.ldk, m * L.ldk));
+                planes_kernel<K><<<(unsigned)((ta + 255) / 256), 256, 0, s>>>(a, m, kdim, p, tab, L.S, as, L.ldk,
+                                                                                m * L.ldk));
     const int tk = (int)((kdim + PB_KK - 1) / PB_KK), tj = (int)((n + PB_J - 1) / PB_J);
     const int64_t tiles = (int64_t)tk * tj;
     const int grid = (int)(tiles < 8 * num_sms() ? tiles : 8 * num_sms());
     QADIC_TIMED("fp4k planes B", s,
-                planes_b_kernel<K><<<grid, 256, 0, s>>>(b, kdim, n, p, lut_lo, lut_hi, bs, L.ldk, n * L.ldk, tk, tj));
+                planes_b_kernel<K><<<grid, 256, 0, s>>>(b, kdim, n, p, tab, L.S, bs, L.ldk, n * L.ldk, tk, tj));
 }
 
 template <int K>
 static void launch_combine(const uint8_t* d, int64_t m, int64_t n, const KaraLayout& L, uint32_t p, uint32_t magic,
-                           const CombineW& cw, uint8_t* c, cudaStream_t s) {
+                           const PlaneSpec& ps, uint8_t* c, cudaStream_t s) {
     const int64_t tot = m * ((n + 31) / 32);
     QADIC_TIMED("fp4k combine", s,
-                combine_kernel<K><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(d, m, n, L.ldd, m * L.ldd, p, magic,
-                                                                                 cw, c));
+                combine_kernel<K><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(d, m, n, L.ldd, m * L.ldd, L.S, p,
+                                                                                 magic, ps, c));
 }
 
-// C[m, n, k] = A[m, K, k] B[K, n, k] over GF(p^k) through Karatsuba planes
+// C[m, n, k] = A[m, K, k] B[K, n, k] over GF(p^k) through plane products
 static int run_kara(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
                     void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s) {
     const int k = (int)f.k;
-    KaraLayout L = kara_plan(m, kdim, n, k);
-    const size_t need = L.a_bytes + L.b_bytes + L.d_bytes;
+    PlaneSpec ps;
+    QADIC_REQUIRE(plan_planes(f, &ps), QADIC_ERR_UNSUPPORTED, "no plane decomposition with <= %d planes", KMAX_S);
+    KaraLayout L = kara_plan(ps.S, m, kdim, n, k);
+    const size_t need = L.tab_bytes + L.a_bytes + L.b_bytes + L.d_bytes;
     QADIC_REQUIRE(ws != nullptr && ws_bytes >= need, QADIC_ERR_VALUE, "workspace too small (%zu < %zu)", ws_bytes,
                   need);
-    // E2M1 codes of the centred residues as an 8-entry byte table (PRMT lookup)
-    const uint32_t lut = centred_e2m1_lut(f.p);
-    uint32_t lut_lo = 0, lut_hi = 0;
-    for (int v = 0; v < 4; ++v) {
-        lut_lo |= ((lut >> (4 * v)) & 0xF) << (8 * v);
-        lut_hi |= ((lut >> (4 * (v + 4))) & 0xF) << (8 * v);
-    }
-    uint8_t* as = static_cast<uint8_t*>(ws);
+    uint32_t* tab = static_cast<uint32_t*>(ws);
+    uint8_t* as = static_cast<uint8_t*>(ws) + L.tab_bytes;
     uint8_t* bs = as + L.a_bytes;
     uint8_t* dd = bs + L.b_bytes;
+    int ncodes = 1;
+    for (int i = 0; i < k; ++i) ncodes *= (int)f.p;
+    QADIC_REQUIRE(ncodes <= PT_CODES, QADIC_ERR_UNSUPPORTED, "plane table needs p^k <= %d", PT_CODES);
+    QADIC_TIMED("fp4k plane table", s,
+                plane_table_kernel<<<(ncodes + 255) / 256, 256, 0, s>>>(f.p, k, ps.S, ps, centred_e2m1_lut(f.p), tab));
     switch (k) {
-        case 1: launch_planes<1>(a, b, m, kdim, n, f.p, lut_lo, lut_hi, L, as, bs, s); break;
-        case 2: launch_planes<2>(a, b, m, kdim, n, f.p, lut_lo, lut_hi, L, as, bs, s); break;
-        case 3: launch_planes<3>(a, b, m, kdim, n, f.p, lut_lo, lut_hi, L, as, bs, s); break;
-        default: launch_planes<4>(a, b, m, kdim, n, f.p, lut_lo, lut_hi, L, as, bs, s); break;
+        case 1: launch_planes<1>(a, b, m, kdim, n, f.p, tab, L, as, bs, s); break;
+        case 2: launch_planes<2>(a, b, m, kdim, n, f.p, tab, L, as, bs, s); break;
+        case 3: launch_planes<3>(a, b, m, kdim, n, f.p, tab, L, as, bs, s); break;
+        default: launch_planes<4>(a, b, m, kdim, n, f.p, tab, L, as, bs, s); break;
     }
     int rc = check_launch("fp4k planes");
     if (rc) return rc;
@@ -1060,44 +1238,36 @@ static int run_kara(const FieldConst& f, const uint8_t* a, const uint8_t* b, int
     rc = pair ? launch_gemm<KIND_F4, true>(ta, tb, prm, s, "fp4k gemm")
               : launch_gemm<KIND_F4, false>(ta, tb, prm, s, "fp4k gemm");
     if (rc || k == 1) return rc;
-    // combine weights: W[l][s] = sum_t coef(t, s) * xpow[t][l]  (mod p)
-    CombineW cw = {};
-    for (int l = 0; l < k; ++l) {
-        for (int sidx = 0; sidx < L.S; ++sidx) {
-            const int i = combo_first(k, sidx), j = combo_second(k, sidx);
-            int64_t acc = 0;
-            if (i == j) {
-                acc += f.xpow[2 * i][l];
-                for (int o = 0; o < k; ++o)
-                    if (o != i) acc -= f.xpow[i + o][l];
-            } else {
-                acc += f.xpow[i + j][l];
-            }
-            acc %= (int64_t)f.p;
-            if (acc < 0) acc += f.p;
-            cw.w[l][sidx] = (uint8_t)acc;
-        }
-    }
     const uint32_t magic = small_magic(f.p);
     switch (k) {
-        case 2: launch_combine<2>(dd, m, n, L, f.p, magic, cw, c, s); break;
-        case 3: launch_combine<3>(dd, m, n, L, f.p, magic, cw, c, s); break;
-        default: launch_combine<4>(dd, m, n, L, f.p, magic, cw, c, s); break;
+        case 2: launch_combine<2>(dd, m, n, L, f.p, magic, ps, c, s); break;
+        case 3: launch_combine<3>(dd, m, n, L, f.p, magic, ps, c, s); break;
+        default: launch_combine<4>(dd, m, n, L, f.p, magic, ps, c, s); break;
     }
     return check_launch("fp4k combine");
 }
 
 }  // namespace tc
 
-size_t tc_kara_workspace(int64_t m, int64_t kdim, int64_t n, int k) {
-    tc::KaraLayout L = tc::kara_plan(m, kdim, n, k);
-    return L.a_bytes + L.b_bytes + L.d_bytes;
+// planes of the decomposition plan_planes() picks (Toom-Cook when 2k-1 <= p+1)
+static int kara_planes(uint32_t p, int k) { return (2 * k - 1 <= (int)p + 1) ? 2 * k - 1 : k * (k + 1) / 2; }
+
+bool tc_kara_ok(uint32_t p, int64_t kdim, int k) {
+    int ncodes = 1;
+    for (int i = 0; i < k; ++i) ncodes *= (int)p;
+    return p <= 7 && kara_planes(p, k) <= tc::KMAX_S && ncodes <= tc::PT_CODES &&
+           (__int128)kdim * ((p - 1) / 2) * ((p - 1) / 2) < ((__int128)1 << 24);
+}
+
+size_t tc_kara_workspace(uint32_t p, int64_t m, int64_t kdim, int64_t n, int k) {
+    tc::KaraLayout L = tc::kara_plan(kara_planes(p, k), m, kdim, n, k);
+    return L.tab_bytes + L.a_bytes + L.b_bytes + L.d_bytes;
 }
 
 int tc_kara_gf_matmul(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
                       void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s) {
-    QADIC_REQUIRE(f.p <= 7 && (__int128)kdim * ((f.p - 1) / 2) * ((f.p - 1) / 2) < ((__int128)1 << 24), QADIC_ERR_PARAMS,
-                  "fp4k engine needs p <= 7 and K*((p-1)/2)^2 < 2^24");
+    QADIC_REQUIRE(tc_kara_ok(f.p, kdim, (int)f.k), QADIC_ERR_PARAMS,
+                  "fp4k engine needs p <= 7, K*((p-1)/2)^2 < 2^24 and at most %d planes", tc::KMAX_S);
     return tc::run_kara(f, a, b, m, kdim, n, ws, ws_bytes, c, s);
 }
 

@@ -12,7 +12,8 @@ int tc_gf_matmul(int kind, const FieldConst& f, const uint8_t* a, const uint8_t*
                  void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s);
 int tc_right_cmm(int kind, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n, uint32_t p,
                  void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s);
-size_t tc_kara_workspace(int64_t m, int64_t kdim, int64_t n, int k);
+size_t tc_kara_workspace(uint32_t p, int64_t m, int64_t kdim, int64_t n, int k);
+bool tc_kara_ok(uint32_t p, int64_t kdim, int k);
 int tc_kara_gf_matmul(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
                       void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s);
 int tc_kara_right_cmm(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n, uint32_t p, void* ws,
@@ -33,7 +34,8 @@ using namespace qadic;
 static int resolve_engine(int32_t engine, uint32_t p, int64_t kdim, int k) {
     if (engine != QADIC_ENGINE_AUTO) return engine;
     // Karatsuba planes: inner dimension K per plane (the sums never exceed it)
-    return tc_f4_ok(p, kdim, 1) ? QADIC_ENGINE_F4K_TC : QADIC_ENGINE_I8_TC;
+    if (tc_kara_ok(p, kdim, k)) return QADIC_ENGINE_F4K_TC;
+    return tc_f4_ok(p, kdim, k) ? QADIC_ENGINE_F4_TC : QADIC_ENGINE_I8_TC;
 }
 static int tc_kind(int eng) { return eng == QADIC_ENGINE_F4_TC ? 1 : 0; }
 
@@ -42,7 +44,7 @@ extern "C" {
 size_t qadic_gf_matmul_workspace(const qadic_field_desc* f, int64_t m, int64_t kdim, int64_t n, int32_t engine) {
     if (!f || m < 0 || kdim < 0 || n < 0) return 0;
     const int eng = resolve_engine(engine, (uint32_t)f->p, kdim, f->k);
-    if (eng == QADIC_ENGINE_F4K_TC) return tc_kara_workspace(m, kdim, n, f->k);
+    if (eng == QADIC_ENGINE_F4K_TC) return tc_kara_workspace((uint32_t)f->p, m, kdim, n, f->k);
     return eng == QADIC_ENGINE_F64_DMMA ? f64_gf_workspace(m, kdim, n) : tc_workspace(tc_kind(eng), m, kdim, n, f->k);
 }
 
@@ -85,7 +87,7 @@ int qadic_gf_matmul_u8(const qadic_field_desc* fd, const uint8_t* a, const uint8
 size_t qadic_right_cmm_workspace(int64_t m, int64_t kdim, int64_t n, int64_t p, int32_t d, int32_t engine) {
     if (m < 0 || kdim < 0 || n < 0 || d < 0) return 0;
     const int eng = resolve_engine(engine, (uint32_t)p, kdim, 1);
-    if (eng == QADIC_ENGINE_F4K_TC) return tc_kara_workspace(m, kdim, n, 1);
+    if (eng == QADIC_ENGINE_F4K_TC) return tc_kara_workspace((uint32_t)p, m, kdim, n, 1);
     return eng == QADIC_ENGINE_F64_DMMA ? f64_cmm_workspace(m, kdim, n, d) : tc_workspace(tc_kind(eng), m, kdim, n, 1);
 }
 

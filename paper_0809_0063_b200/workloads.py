@@ -87,6 +87,12 @@ def make_inputs(c: Config, shape: Optional[tuple] = None, seed: Optional[int] = 
     raise KeyError(c.cfg)
 
 
+def plane_count(p: int, k: int) -> int:
+    """Plane products of the fp4k engine: Toom-Cook over F_p when 2k-1 <=
+    p+1 (evaluation points F_p u {inf}), else Karatsuba k(k+1)/2."""
+    return 2 * k - 1 if 2 * k - 1 <= p + 1 else k * (k + 1) // 2
+
+
 def work_units(c: Config, shape: Optional[tuple] = None) -> dict:
     """Algorithmic work of one call: the headline unit
     (GF/F_p mult-adds, or pairs for cfg1), REDQ coefficients and the uint8
@@ -104,7 +110,7 @@ def work_units(c: Config, shape: Optional[tuple] = None) -> dict:
         m, kd, n = shape
         return {"unit_count": m * kd * n, "unit": "GF mult-adds", "madds": m * kd * n,
                 "redq_coeffs": m * n * (2 * c.k - 1), "io_bytes": (m * kd + kd * n + m * n) * c.k,
-                "i8_macs": m * n * kd * c.k * c.k, "kara_macs": m * n * kd * c.k * (c.k + 1) // 2}
+                "i8_macs": m * n * kd * c.k * c.k, "kara_macs": m * n * kd * plane_count(c.p, c.k)}
     if c.cfg == 4:
         (n,) = shape
         return {"unit_count": n ** 3, "unit": "F_p mult-adds", "madds": n ** 3, "redq_coeffs": n * n,
