@@ -45,6 +45,9 @@ constexpr int BM = 128, BK = 128;  // BK in bytes per stage (128 int8 / 256 fp4 
 constexpr int STAGES = 4;
 constexpr int THREADS = 256;
 constexpr int GROUP_M = 16;
+#ifndef QADIC_MAX_STAGES
+#define QADIC_MAX_STAGES 8
+#endif
 
 template <int KIND>
 struct Cfg;
@@ -63,18 +66,23 @@ struct Cfg<KIND_F4> {
 // of a cluster share one M=256 MMA; each loads its own 128 A rows and half of
 // the BN B rows, so the per-SM operand traffic (TMA writes + MMA reads of
 // shared memory) drops by a third at the same MMA rate.
-template <int KIND, bool PAIR>
+// FUSE_K > 0: the epilogue applies the plane combination C_l = sum_s W[l][s] D_s
+// itself, accumulating the S plane results of one output tile in shared memory
+// (one padded row of BN*FUSE_K bytes per epilogue thread).
+template <int KIND, bool PAIR, int FUSE_K = 0>
 struct Geo {
     static constexpr int BN = Cfg<KIND>::BN;
     static constexpr int B_ROWS = PAIR ? BN / 2 : BN;  // B rows this CTA loads
     static constexpr int A_BYTES = BM * BK;
     static constexpr int B_BYTES = B_ROWS * BK;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int ACC_PITCH = FUSE_K ? BN * FUSE_K + 4 : 0;  // odd word count: conflict-free rows
+    static constexpr int ACC_BYTES = BM * ACC_PITCH;
     // as many stages as 227 KB of shared memory holds (deeper prefetch hides
     // the L2 misses at tile boundaries of short-K plane products)
-    static constexpr int STAGES_N = PAIR ? ((232448 - 1280) / STAGE_BYTES > 8 ? 8 : (232448 - 1280) / STAGE_BYTES)
-                                         : STAGES;
-    static constexpr size_t SMEM = (size_t)STAGES_N * STAGE_BYTES + 1024 + 256;
+    static constexpr int FIT = (232448 - 1280 - ACC_BYTES) / STAGE_BYTES;
+    static constexpr int STAGES_N = PAIR ? (FIT > QADIC_MAX_STAGES ? QADIC_MAX_STAGES : FIT) : STAGES;
+    static constexpr size_t SMEM = (size_t)STAGES_N * STAGE_BYTES + ACC_BYTES + 1024 + 256;
     static constexpr int TILE_M = PAIR ? 2 * BM : BM;
 };
 
@@ -89,7 +97,13 @@ struct Params {
     int planes;          // independent plane products, stacked along the A / B rows
     int nibble_out;      // 0: uint8 residues; 1: residues packed two per byte
     uint8_t* c;
+    uint8_t W[4][8];     // FUSE_K: combination weights (mod p), C_l = sum_s W[l][s] D_s
 };
+
+// tile index -> (plane, m tile, n tile).  Unfused: planes outermost.  Fused:
+// the planes of one output tile are consecutive so the epilogue can combine them.
+template <int FUSE_K>
+__device__ __forceinline__ void decode_tile(int tile, const Params& prm, int& pl, int& mt, int& nt);
 
 __device__ __forceinline__ void tile_coords(int tile, int m_tiles, int n_tiles, int& mt, int& nt) {
     const int per_group = GROUP_M * n_tiles;
@@ -99,6 +113,18 @@ __device__ __forceinline__ void tile_coords(int tile, int m_tiles, int n_tiles, 
     const int r = tile % per_group;
     mt = first_m + r % gm;
     nt = r / gm;
+}
+
+template <int FUSE_K>
+__device__ __forceinline__ void decode_tile(int tile, const Params& prm, int& pl, int& mt, int& nt) {
+    if (FUSE_K) {
+        pl = tile % prm.planes;
+        tile_coords(tile / prm.planes, prm.m_tiles, prm.n_tiles, mt, nt);
+    } else {
+        const int plane_tiles = prm.m_tiles * prm.n_tiles;
+        pl = tile / plane_tiles;
+        tile_coords(tile % plane_tiles, prm.m_tiles, prm.n_tiles, mt, nt);
+    }
 }
 
 __host__ __device__ constexpr uint32_t idesc_mxf4(uint32_t m, uint32_t n) {
@@ -139,12 +165,12 @@ __device__ __forceinline__ void tmem_fill_sf(uint32_t taddr) {
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
-template <int KIND, bool PAIR>
+template <int KIND, bool PAIR, int FUSE_K = 0>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_modp_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                     Params prm) {
+                     const __grid_constant__ Params prm) {
     using namespace sm100;
-    using G = Geo<KIND, PAIR>;
+    using G = Geo<KIND, PAIR, FUSE_K>;
     constexpr int BN = G::BN;
     constexpr int NST = G::STAGES_N;
     extern __shared__ uint8_t smem_raw[];
@@ -161,8 +187,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     const bool leader = rank == 0;
     const int group_id = PAIR ? blockIdx.x / 2 : blockIdx.x;
     const int num_groups = PAIR ? gridDim.x / 2 : gridDim.x;
+    // work units: one tile of one plane; fused, one output tile with all its
+    // planes processed back to back by the same CTA (group)
     const int plane_tiles = prm.m_tiles * prm.n_tiles;
-    const int num_tiles = plane_tiles * prm.planes;
+    const int per_unit = FUSE_K ? prm.planes : 1;
+    const int units = FUSE_K ? plane_tiles : plane_tiles * prm.planes;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmap_a);
@@ -199,10 +228,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = group_id; tile < num_tiles; tile += num_groups) {
-                int mt, nt;
-                const int pl = tile / plane_tiles;
-                tile_coords(tile % plane_tiles, prm.m_tiles, prm.n_tiles, mt, nt);
+            for (int u = group_id; u < units; u += num_groups)
+            for (int sp = 0; sp < per_unit; ++sp) {
+                const int tile = u * per_unit + sp;
+                int pl, mt, nt;
+                decode_tile<FUSE_K>(tile, prm, pl, mt, nt);
                 const int arow = (int)(pl * prm.M) + mt * G::TILE_M + (int)rank * BM;
                 const int brow = (int)(pl * prm.N) + nt * BN + (int)rank * G::B_ROWS;
                 for (int kb = 0; kb < prm.num_kb; ++kb) {
@@ -230,7 +260,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         int stage = 0;
         uint32_t phase = 0;
         int local = 0;
-        for (int tile = group_id; tile < num_tiles; tile += num_groups, ++local) {
+        for (int u = group_id; u < units; u += num_groups)
+        for (int sp = 0; sp < per_unit; ++sp, ++local) {
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
             mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
@@ -273,16 +304,82 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t empty_addr0 = PAIR ? map_to_rank(&tmem_empty[0], 0) : 0;
         const uint32_t empty_addr1 = PAIR ? map_to_rank(&tmem_empty[1], 0) : 0;
         int local = 0;
-        for (int tile = group_id; tile < num_tiles; tile += num_groups, ++local) {
-            int mt, nt;
-            const int pl = tile / plane_tiles;
-            tile_coords(tile % plane_tiles, prm.m_tiles, prm.n_tiles, mt, nt);
+        uint8_t* accrow = smem + NST * G::STAGE_BYTES + 256 + (ew * 32 + lane) * G::ACC_PITCH;
+        for (int u = group_id; u < units; u += num_groups)
+        for (int sp = 0; sp < per_unit; ++sp, ++local) {
+            const int tile = u * per_unit + sp;
+            int pl, mt, nt;
+            decode_tile<FUSE_K>(tile, prm, pl, mt, nt);
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
             mbar_wait(&tmem_full[acc], acc_phase);
             tc_fence_after();
             const int64_t row = (int64_t)mt * G::TILE_M + (int)rank * BM + ew * 32 + lane;
             const bool row_ok = row < prm.M;
+            if constexpr (FUSE_K > 0) {
+                // plane pl of this tile: acc_row[(col, l)] += W[l][pl] * D_pl[row, col]
+                // on byte lanes (S * (p-1)^2 < 256: no carries); the last plane
+                // reduces mod p and writes the k coefficient bytes of every column
+                uint32_t wl[FUSE_K];
+#pragma unroll
+                for (int l = 0; l < FUSE_K; ++l) wl[l] = prm.W[l][pl];
+#pragma unroll 1
+                for (int ch = 0; ch < BN / 16; ++ch) {
+                    uint32_t v[16];
+                    tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + ch * 16, v);
+                    tmem_ld_wait();
+                    uint32_t add[4 * FUSE_K];
+#pragma unroll
+                    for (int q = 0; q < 4 * FUSE_K; ++q) add[q] = 0;
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) {
+                        const uint32_t x = (uint32_t)(__float2int_rn(__uint_as_float(v[c])) + (int)prm.offset);
+                        const uint32_t r = mod_u32(x, prm.p, prm.magic64);
+#pragma unroll
+                        for (int l = 0; l < FUSE_K; ++l) {
+                            const int pos = c * FUSE_K + l;
+                            add[pos >> 2] |= (wl[l] * r) << (8 * (pos & 3));
+                        }
+                    }
+                    uint32_t* a32 = reinterpret_cast<uint32_t*>(accrow + ch * 16 * FUSE_K);
+#pragma unroll
+                    for (int q = 0; q < 4 * FUSE_K; ++q) a32[q] = (pl == 0) ? add[q] : a32[q] + add[q];
+                }
+                // TMEM fully read: hand the accumulator back to the MMA warp first
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (PAIR) mbar_arrive_cluster(acc ? empty_addr1 : empty_addr0);
+                    else mbar_arrive(&tmem_empty[acc]);
+                }
+                if (pl == prm.planes - 1 && row_ok) {
+                    const int64_t col0 = (int64_t)nt * BN;
+                    const int64_t nbytes = (prm.N - col0 < BN ? prm.N - col0 : BN) * FUSE_K;
+                    uint8_t* dst = prm.c + row * prm.ldc + col0 * FUSE_K;
+                    const uint32_t magic = (uint32_t)(0xFFFFFFFFu / prm.p) + 1u;
+#pragma unroll 1
+                    for (int q = 0; q < BN * FUSE_K / 16; ++q) {
+                        if (q * 16 >= nbytes) break;
+                        const uint32_t* src = reinterpret_cast<const uint32_t*>(accrow + q * 16);
+                        uint32_t o[4];
+#pragma unroll
+                        for (int wq = 0; wq < 4; ++wq) {
+                            const uint32_t xw = src[wq];
+                            o[wq] = mod_small(xw & 0xFF, prm.p, magic) | (mod_small((xw >> 8) & 0xFF, prm.p, magic) << 8) |
+                                    (mod_small((xw >> 16) & 0xFF, prm.p, magic) << 16) |
+                                    (mod_small(xw >> 24, prm.p, magic) << 24);
+                        }
+                        if (q * 16 + 16 <= nbytes && ((reinterpret_cast<uintptr_t>(dst + q * 16) & 15) == 0)) {
+                            *reinterpret_cast<uint4*>(dst + q * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 16; ++e)  // unrolled: o[] stays in registers
+                                if (q * 16 + e < nbytes) dst[q * 16 + e] = (uint8_t)(o[e >> 2] >> (8 * (e & 3)));
+                        }
+                    }
+                }
+                continue;
+            }
             uint8_t* crow = prm.c + pl * prm.c_plane + row * prm.ldc;
 #pragma unroll 1
             for (int ch = 0; ch < BN / 16; ++ch) {
@@ -578,6 +675,11 @@ static int num_sms() {
 
 static inline int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 
+static bool getenv_flag(const char* name) {
+    const char* e = getenv(name);
+    return e && e[0] && e[0] != '0';
+}
+
 // CTA-pair (cta_group::2) GEMM unless QADIC_TC_PAIR=0
 static bool pair_mode() {
     static int mode = -1;
@@ -620,11 +722,11 @@ static Layout plan(int kind, const uint8_t* a, int64_t m, int64_t kdim, int64_t 
     return L;
 }
 
-template <int KIND, bool PAIR>
+template <int KIND, bool PAIR, int FUSE_K = 0>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, Params prm, cudaStream_t s,
                        const char* label = nullptr) {
-    using G = Geo<KIND, PAIR>;
-    auto kern = gemm_modp_kernel<KIND, PAIR>;
+    using G = Geo<KIND, PAIR, FUSE_K>;
+    auto kern = gemm_modp_kernel<KIND, PAIR, FUSE_K>;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
@@ -1224,6 +1326,24 @@ static int run_kara(const FieldConst& f, const uint8_t* a, const uint8_t* b, int
     prm.n_tiles = (int)((n + BN - 1) / BN);
     prm.num_kb = (int)(((kdim + 1) / 2 + BK - 1) / BK);
     prm.planes = L.S;
+    // Fused combine (opt-in, QADIC_FUSE_COMBINE=1): the epilogue accumulates
+    // W[l][s] * D_s per tile in shared memory on byte lanes (needs S*(p-1)^2 <
+    // 256 and the CTA-pair kernel).  Measured slower than the separate combine
+    // pass at cfg5 (epilogue-bound: 1.05 vs 0.82 + 0.12 ms), so off by default.
+    const bool fuse = pair && k >= 2 && (int64_t)L.S * (f.p - 1) * (f.p - 1) < 256 && getenv_flag("QADIC_FUSE_COMBINE");
+    if (fuse) {
+        for (int l = 0; l < k; ++l)
+            for (int sidx = 0; sidx < KMAX_S; ++sidx) prm.W[l][sidx] = sidx < L.S ? ps.W[l][sidx] : 0;
+        prm.c = c;
+        prm.ldc = n * k;
+        prm.c_plane = 0;
+        prm.nibble_out = 0;
+        switch (k) {
+            case 2: return launch_gemm<KIND_F4, true, 2>(ta, tb, prm, s, "fp4k gemm");
+            case 3: return launch_gemm<KIND_F4, true, 3>(ta, tb, prm, s, "fp4k gemm");
+            default: return launch_gemm<KIND_F4, true, 4>(ta, tb, prm, s, "fp4k gemm");
+        }
+    }
     if (k == 1) {  // one plane: the GEMM writes C directly
         prm.c = c;
         prm.ldc = n;

@@ -69,6 +69,9 @@ def test_gf_matmul_full(cfg):
     got = fld.matmul_coeffs(da, db, engine="i8").cpu().numpy()
     _freivalds_gf(x["a"], x["b"], got, of)
     _rows_check(x["a"], x["b"], got, of)
+    for eng in ("auto", "fp4k", "fp4"):  # FP4 engines: Toom/Karatsuba planes and expanded form
+        alt = fld.matmul_coeffs(da, db, engine=eng).cpu().numpy()
+        assert np.array_equal(alt, got), eng
     if cfg == 3:  # independent engine, whole output
         f64 = fld.matmul_coeffs(da, db, engine="f64").cpu().numpy()
         assert np.array_equal(f64, got)
@@ -93,6 +96,9 @@ def test_right_cmm_full():
     assert np.array_equal(got[rows], O.modmatmul_planes(a[rows], a, 3))
     f64 = cmm.right_cmm(da, cmm.compress_rows(da, prm), engine="f64").cpu().numpy()
     assert np.array_equal(f64, got)
+    for eng in ("auto", "fp4k", "fp4"):
+        alt = cmm.right_cmm(da, cmm.compress_rows(da, prm), engine=eng).cpu().numpy()
+        assert np.array_equal(alt, got), eng
 
 
 def test_cfg1_cfg2_full():
