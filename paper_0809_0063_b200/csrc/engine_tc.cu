@@ -1096,84 +1096,111 @@ __global__ void __launch_bounds__(256) planes_kernel(const uint8_t* __restrict__
         if (s < S) *reinterpret_cast<uint4*>(dst + s * plane_stride) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
 }
 
-// B [Kd, N, K] -> S transposed planes [S][N][ld]: a 64 kk x 128 j tile of B is
-// staged in shared memory with 16-byte loads; each thread then owns one j and
-// 32 kk and builds its plane words like planes_kernel.
+// B [Kd, N, K] -> S transposed planes [S][N][ld]: 64 kk x 128 j tiles of B are
+// staged in shared memory by cp.async into two buffers (the next tile streams
+// in while this one is converted); each thread then owns one j and 32 kk and
+// builds its plane words like planes_kernel.
 constexpr int PB_KK = 64, PB_J = 128;
+template <int K>
+constexpr size_t planes_b_smem() {
+    return (size_t)2 * PB_KK * (PB_J * K + 16) + PT_CODES * sizeof(uint32_t);
+}
+
+__device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+                 "l"(gmem), "r"(valid ? 16 : 0));
+}
+
 template <int K>
 __global__ void __launch_bounds__(256) planes_b_kernel(const uint8_t* __restrict__ b, int64_t Kd, int64_t N, uint32_t p,
                                                        const uint32_t* __restrict__ gtab, int S,
                                                        uint8_t* __restrict__ out, int64_t ld, int64_t plane_stride,
                                                        int tiles_kk, int tiles_j) {
     constexpr int ROWB = PB_J * K;
-    __shared__ __align__(16) uint8_t tile[PB_KK][ROWB + 16];
-    __shared__ uint32_t tab[PT_CODES];
+    constexpr int PITCH = ROWB + 16;
+    extern __shared__ __align__(16) uint8_t dsm[];
+    uint8_t* tiles = dsm;                                                   // 2 x [PB_KK][PITCH]
+    uint32_t* tab = reinterpret_cast<uint32_t*>(dsm + 2 * PB_KK * PITCH);  // plane table
     int ncodes = 1;
     for (int i = 0; i < K; ++i) ncodes *= (int)p;
     for (int i = threadIdx.x; i < ncodes; i += blockDim.x) tab[i] = gtab[i];
     const bool vec_in = ((N * K) % 16 == 0) && ((reinterpret_cast<uintptr_t>(b) & 15) == 0);
     const int64_t ntiles = (int64_t)tiles_kk * tiles_j;
     const int jl = threadIdx.x % PB_J, ch = threadIdx.x / PB_J;  // 2 chunks of 32 kk
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+
+    auto stage = [&](int64_t t, int buf) {
+        uint8_t* tb = tiles + buf * PB_KK * PITCH;
         const int64_t kk0 = (t % tiles_kk) * PB_KK, j0 = (t / tiles_kk) * PB_J;
-        __syncthreads();
         if (vec_in && j0 + PB_J <= N) {
             for (int i = threadIdx.x; i < PB_KK * (ROWB / 16); i += blockDim.x) {
                 const int rr = i / (ROWB / 16), qq = i % (ROWB / 16);
                 const int64_t gk = kk0 + rr;
-                uint4 v = make_uint4(0, 0, 0, 0);
-                if (gk < Kd) v = __ldg(reinterpret_cast<const uint4*>(b + gk * N * K + j0 * K) + qq);
-                *reinterpret_cast<uint4*>(&tile[rr][qq * 16]) = v;
+                const uint8_t* src = b + (gk < Kd ? gk : 0) * N * K + j0 * K + qq * 16;
+                cp_async16_zfill(tb + rr * PITCH + qq * 16, src, gk < Kd);
             }
         } else {
             for (int i = threadIdx.x; i < PB_KK * ROWB; i += blockDim.x) {
                 const int rr = i / ROWB, cc = i % ROWB;
                 const int64_t gk = kk0 + rr, gj = j0 + cc / K;
-                tile[rr][cc] = (gk < Kd && gj < N) ? b[gk * N * K + j0 * K + cc] : 0;
+                tb[rr * PITCH + cc] = (gk < Kd && gj < N) ? b[gk * N * K + j0 * K + cc] : 0;
             }
         }
+        asm volatile("cp.async.commit_group;");
+    };
+
+    if ((int64_t)blockIdx.x < ntiles) stage(blockIdx.x, 0);
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int64_t nxt = t + gridDim.x;
+        if (nxt < ntiles) stage(nxt, (it + 1) & 1);
+        else asm volatile("cp.async.commit_group;");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
         __syncthreads();
+        const int64_t kk0 = (t % tiles_kk) * PB_KK, j0 = (t / tiles_kk) * PB_J;
         const int64_t gj = j0 + jl;
         const int64_t col = (kk0 + ch * 32) / 2;
-        if (gj >= N || col + 16 > ld) continue;
-        const uint8_t* tcol = &tile[ch * 32][jl * K];
-        if constexpr (K == 1) {  // one plane: gather 4 kk per word, PRMT lookup
-            uint32_t lo, hi;
-            byte_lut_from_table(tab, p, lo, hi);
-            uint32_t o[4];
+        if (gj < N && col + 16 <= ld) {
+            const uint8_t* tcol = tiles + (it & 1) * PB_KK * PITCH + (ch * 32) * PITCH + jl * K;
+            if constexpr (K == 1) {  // one plane: gather 4 kk per word, PRMT lookup
+                uint32_t lo, hi;
+                byte_lut_from_table(tab, p, lo, hi);
+                uint32_t o[4];
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
-                uint32_t v0 = 0, v1 = 0;
+                for (int g = 0; g < 4; ++g) {
+                    uint32_t v0 = 0, v1 = 0;
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    v0 |= (uint32_t)tcol[(8 * g + e) * (ROWB + 16)] << (8 * e);
-                    v1 |= (uint32_t)tcol[(8 * g + 4 + e) * (ROWB + 16)] << (8 * e);
+                    for (int e = 0; e < 4; ++e) {
+                        v0 |= (uint32_t)tcol[(8 * g + e) * PITCH] << (8 * e);
+                        v1 |= (uint32_t)tcol[(8 * g + 4 + e) * PITCH] << (8 * e);
+                    }
+                    o[g] = residues_to_e2m1(v0, lo, hi) | (residues_to_e2m1(v1, lo, hi) << 16);
                 }
-                o[g] = residues_to_e2m1(v0, lo, hi) | (residues_to_e2m1(v1, lo, hi) << 16);
+                *reinterpret_cast<uint4*>(out + gj * ld + col) = make_uint4(o[0], o[1], o[2], o[3]);
+            } else {
+                uint32_t w[KMAX_S][4];
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    uint32_t x[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        uint32_t code = 0;
+#pragma unroll
+                        for (int i = K - 1; i >= 0; --i) code = code * p + tcol[(8 * g + e) * PITCH + i];
+                        x[e] = tab[code];
+                    }
+                    transpose8_nibbles(x);
+#pragma unroll
+                    for (int s = 0; s < KMAX_S; ++s) w[s][g] = x[s];
+                }
+                uint8_t* dst = out + gj * ld + col;
+#pragma unroll
+                for (int s = 0; s < KMAX_S; ++s)
+                    if (s < S) *reinterpret_cast<uint4*>(dst + s * plane_stride) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
             }
-            *reinterpret_cast<uint4*>(out + gj * ld + col) = make_uint4(o[0], o[1], o[2], o[3]);
-            continue;
         }
-        uint32_t w[KMAX_S][4];
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-            uint32_t x[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                uint32_t code = 0;
-#pragma unroll
-                for (int i = K - 1; i >= 0; --i) code = code * p + tcol[(8 * g + e) * (ROWB + 16) + i];
-                x[e] = tab[code];
-            }
-            transpose8_nibbles(x);
-#pragma unroll
-            for (int s = 0; s < KMAX_S; ++s) w[s][g] = x[s];
-        }
-        uint8_t* dst = out + gj * ld + col;
-#pragma unroll
-        for (int s = 0; s < KMAX_S; ++s)
-            if (s < S) *reinterpret_cast<uint4*>(dst + s * plane_stride) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
+        __syncthreads();  // this buffer is refilled two tiles later
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
 // D planes [S][M][ldd] (nibbles, N columns) -> C [M][N][K] uint8 residues.
@@ -1269,8 +1296,14 @@ static void launch_planes(const uint8_t* a, const uint8_t* b, int64_t m, int64_t
     const int tk = (int)((kdim + PB_KK - 1) / PB_KK), tj = (int)((n + PB_J - 1) / PB_J);
     const int64_t tiles = (int64_t)tk * tj;
     const int grid = (int)(tiles < 8 * num_sms() ? tiles : 8 * num_sms());
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(planes_b_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)planes_b_smem<K>());
+        attr = true;
+    }
     QADIC_TIMED("fp4k planes B", s,
-                planes_b_kernel<K><<<grid, 256, 0, s>>>(b, kdim, n, p, tab, L.S, bs, L.ldk, n * L.ldk, tk, tj));
+                planes_b_kernel<K><<<grid, 256, planes_b_smem<K>(), s>>>(b, kdim, n, p, tab, L.S, bs, L.ldk, n * L.ldk,
+                                                                          tk, tj));
 }
 
 template <int K>
