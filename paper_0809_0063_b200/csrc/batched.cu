@@ -30,51 +30,108 @@ struct PolyConst {
     double invp_up, bound;
 };
 
-// ---- cfg1 fast path: k = 4 (degree-3 operands), 4 pairs per thread ----------
+// ---- cfg1 fast path: k = 4 (degree-3 operands), 16 pairs per thread ----------
+// One thread: 8 pairs = 2 x 16 B of a and of b in, 7 x 8 B out -- every HBM
+// access a full vector, no shared memory.  Per pair: DQT-pack both operands
+// in registers, one FP64 product, s = floor(r * RU(1/p)) by a round-down add of
+// 2^52 (the low mantissa bits are then the integer), 7 digits by the 32-bit
+// wrap trick, correction on 4 byte lanes at once.
 constexpr int PM_THREADS = 256;
-constexpr int PM_PAIRS = 4 * PM_THREADS;  // pairs per block
+constexpr int PM_PER = 8;  // pairs per thread (56 output bytes = 7 x 8-byte stores)
 
-__global__ void __launch_bounds__(PM_THREADS) polymul_k4_kernel(const uint8_t* __restrict__ a,
+QADIC_D uint32_t pack4_bytes(uint32_t x, int t, uint32_t m) {
+    return (x & m) | (((x >> 8) & m) << t) | (((x >> 16) & m) << (2 * t)) | (((x >> 24) & m) << (3 * t));
+}
+
+// byte-lane v mod p for lanes < 2p
+QADIC_D uint32_t lanes_mod_2p(uint32_t v, uint32_t p) {
+    const uint32_t t = v + (0x80u - p) * 0x01010101u;
+    return v - ((t >> 7) & 0x01010101u) * p;
+}
+
+template <int T, bool CORR1>
+__global__ void __launch_bounds__(PM_THREADS, 4) polymul_k4_kernel(const uint8_t* __restrict__ a,
                                                                 const uint8_t* __restrict__ b, int64_t n,
                                                                 PolyConst c, uint8_t* __restrict__ out) {
-    __shared__ __align__(16) uint8_t sout[PM_PAIRS * 7];
-    const int64_t base = (int64_t)blockIdx.x * PM_PAIRS;
-    const int64_t my = base + 4 * threadIdx.x;
-    uint32_t av[4] = {0, 0, 0, 0}, bv[4] = {0, 0, 0, 0};
-    if (my + 4 <= n) {
-        const uint4 va = __ldg(reinterpret_cast<const uint4*>(a + my * 4));
-        const uint4 vb = __ldg(reinterpret_cast<const uint4*>(b + my * 4));
-        av[0] = va.x; av[1] = va.y; av[2] = va.z; av[3] = va.w;
-        bv[0] = vb.x; bv[1] = vb.y; bv[2] = vb.z; bv[3] = vb.w;
-    } else {
-        for (int i = 0; i < 4; ++i)
-            if (my + i < n) {
-                av[i] = *reinterpret_cast<const uint32_t*>(a + (my + i) * 4);
-                bv[i] = *reinterpret_cast<const uint32_t*>(b + (my + i) * 4);
-            }
-    }
-    const double pd = (double)c.p;
+    const int64_t p0 = ((int64_t)blockIdx.x * PM_THREADS + threadIdx.x) * PM_PER;
+    if (p0 >= n) return;
+    uint32_t av[PM_PER], bv[PM_PER];
+    const bool full = p0 + PM_PER <= n;
+    if (full) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const double r = u52_to_f64(pack4(av[i], c.t)) * u52_to_f64(pack4(bv[i], c.t));
+        for (int v = 0; v < PM_PER / 4; ++v) {
+            const uint4 x = __ldg(reinterpret_cast<const uint4*>(a + p0 * 4) + v);
+            const uint4 y = __ldg(reinterpret_cast<const uint4*>(b + p0 * 4) + v);
+            av[4 * v] = x.x; av[4 * v + 1] = x.y; av[4 * v + 2] = x.z; av[4 * v + 3] = x.w;
+            bv[4 * v] = y.x; bv[4 * v + 1] = y.y; bv[4 * v + 2] = y.z; bv[4 * v + 3] = y.w;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < PM_PER; ++j) {
+            av[j] = p0 + j < n ? *reinterpret_cast<const uint32_t*>(a + (p0 + j) * 4) : 0u;
+            bv[j] = p0 + j < n ? *reinterpret_cast<const uint32_t*>(b + (p0 + j) * 4) : 0u;
+        }
+    }
+    constexpr uint32_t M = (1u << T) - 1;
+    const double two52 = 4503599627370496.0;
+    uint32_t o[PM_PER * 7 / 4];
+#pragma unroll
+    for (int q = 0; q < PM_PER * 7 / 4; ++q) o[q] = 0;
+#pragma unroll
+    for (int j = 0; j < PM_PER; ++j) {
+        const uint32_t x = av[j], y = bv[j];
+        const uint32_t wa = (x & M) | ((x >> (8 - T)) & (M << T)) | ((x >> (16 - 2 * T)) & (M << (2 * T))) |
+                            ((x >> (24 - 3 * T)) & (M << (3 * T)));
+        const uint32_t wb = (y & M) | ((y >> (8 - T)) & (M << T)) | ((y >> (16 - 2 * T)) & (M << (2 * T))) |
+                            ((y >> (24 - 3 * T)) & (M << (3 * T)));
+        // every digit of the product is < q (checked on the host), so r < q^7 <= 2^49
+        const double rr = __dmul_rn(__hiloint2double(0x43300000, (int)wa) - two52,
+                                    __hiloint2double(0x43300000, (int)wb) - two52);
+        // r < 2^49 < fdiv bound B: floor(RN(r * RU(1/p))) = r // p with no correction branch
+        const uint64_t si = (uint64_t)__double_as_longlong(__dadd_rd(__dmul_rn(rr, c.invp_up), two52));
+        const uint64_t ri = (uint64_t)__double_as_longlong(__dadd_rn(rr, two52));
+        // u_i only matters mod 2^8 (it is small): byte windows of r and s
         uint32_t u[7];
-        redq_compress_f64<6>(r, c.invp_up, pd, c.bound, c.p, c.t, u);
-        uint8_t* o = sout + (4 * threadIdx.x + i) * 7;
 #pragma unroll
-        for (int j = 0; j < 6; ++j) o[j] = (uint8_t)mod_small(u[j] + c.corr * u[j + 1], c.p, c.magic);
-        o[6] = (uint8_t)u[6];
+        for (int i = 0; i < 7; ++i) u[i] = (uint32_t)(ri >> (i * T)) - c.p * (uint32_t)(si >> (i * T));
+        uint64_t v;  // the 7 result bytes
+        if (CORR1) {  // mu_i = (u_i + u_{i+1}) mod p on byte lanes
+            const uint32_t U0 = __byte_perm(__byte_perm(u[0], u[1], 0x0040), __byte_perm(u[2], u[3], 0x0040), 0x5410);
+            const uint32_t U1 = __byte_perm(__byte_perm(u[1], u[2], 0x0040), __byte_perm(u[3], u[4], 0x0040), 0x5410);
+            const uint32_t W0 = __byte_perm(__byte_perm(u[4], u[5], 0x0040), u[6], 0x0410);
+            const uint32_t W1 = __byte_perm(u[5], u[6], 0x0040) & 0xFFFFu;
+            const uint32_t V0 = lanes_mod_2p(U0 + U1, c.p), V1 = lanes_mod_2p(W0 + W1, c.p) & 0xFFFFFFu;
+            v = (uint64_t)V0 | ((uint64_t)V1 << 32);
+        } else {
+            v = 0;
+#pragma unroll
+            for (int i = 0; i < 6; ++i) v |= (uint64_t)mod_small(u[i] + c.corr * u[i + 1], c.p, c.magic) << (8 * i);
+            v |= (uint64_t)(u[6] & 0xFF) << 48;
+        }
+        // bytes 7j .. 7j+6 of the thread's output stream
+        const int pos = j * 7, w = pos >> 2, sh = 8 * (pos & 3);
+        const uint64_t lo = v << sh;
+        o[w] |= (uint32_t)lo;
+        o[w + 1] |= (uint32_t)(lo >> 32);
+        if (sh > 8) o[w + 2] |= (uint32_t)(v >> (64 - sh));
     }
-    __syncthreads();
-    const int64_t npairs = (n - base) < PM_PAIRS ? (n - base) : PM_PAIRS;
-    const int64_t nbytes = npairs * 7;
-    uint8_t* gout = out + base * 7;
-    if (nbytes == PM_PAIRS * 7) {
-        const uint4* s4 = reinterpret_cast<const uint4*>(sout);
-        uint4* g4 = reinterpret_cast<uint4*>(gout);
-        for (int i = threadIdx.x; i < PM_PAIRS * 7 / 16; i += PM_THREADS) g4[i] = s4[i];
+    uint8_t* dst = out + p0 * 7;
+    if (full && ((reinterpret_cast<uintptr_t>(dst) & 7) == 0)) {
+#pragma unroll
+        for (int q = 0; q < PM_PER * 7 / 8; ++q) reinterpret_cast<uint2*>(dst)[q] = make_uint2(o[2 * q], o[2 * q + 1]);
     } else {
-        for (int64_t i = threadIdx.x; i < nbytes; i += PM_THREADS) gout[i] = sout[i];
+#pragma unroll
+        for (int e = 0; e < PM_PER * 7; ++e)
+            if (p0 + e / 7 < n) dst[e] = (uint8_t)(o[e >> 2] >> (8 * (e & 3)));
     }
+}
+
+template <int T>
+static void launch_polymul_k4(const uint8_t* a, const uint8_t* b, int64_t n, const PolyConst& c, uint8_t* out,
+                              cudaStream_t s) {
+    const unsigned blocks = (unsigned)((n + (int64_t)PM_THREADS * PM_PER - 1) / ((int64_t)PM_THREADS * PM_PER));
+    if (c.corr == 1 || c.p == 2) polymul_k4_kernel<T, true><<<blocks, PM_THREADS, 0, s>>>(a, b, n, c, out);
+    else polymul_k4_kernel<T, false><<<blocks, PM_THREADS, 0, s>>>(a, b, n, c, out);
 }
 
 // ---- generic k (1..8): one pair per thread ---------------------------------------
@@ -101,98 +158,108 @@ __global__ void polymul_generic_kernel(const uint8_t* __restrict__ a, const uint
 }
 
 // ---- cfg2: GF(p^k) dot products ----------------------------------------------------
+// G lanes per dot product (G = 4 on the vector path: a warp covers 8 dots, each
+// load instruction reads 64 contiguous bytes per dot).  Each element pair is
+// DQT-packed into 32-bit words and multiplied with one IMAD.WIDE into a 64-bit
+// accumulator (the delayed reduction: no modular work inside the sum); the
+// sum is < q^(2k-1) <= 2^53, so REDQ (FP64 reciprocal + correction) and the
+// L/H fold tables finish it exactly as in src/gfext.py:fgdp.
 constexpr int GD_THREADS = 256;
-constexpr int GD_GROUP = 8;  // lanes per dot product
-constexpr int GD_SMEM_TABLE = 4096;
 
-template <int K, bool VEC, bool SMEM_TABLES>
+template <int K, int G, bool VEC>
 __global__ void __launch_bounds__(GD_THREADS) gf_dot_kernel(const uint8_t* __restrict__ v1,
                                                             const uint8_t* __restrict__ v2, int64_t batch,
                                                             int64_t len, FieldConst f,
                                                             uint8_t* __restrict__ out) {
-    __shared__ uint32_t s_l[SMEM_TABLES ? GD_SMEM_TABLE : 1];
-    __shared__ uint32_t s_h[SMEM_TABLES ? GD_SMEM_TABLE : 1];
-    const uint32_t* ltab = f.l_table;
-    const uint32_t* htab = f.h_table;
-    if (SMEM_TABLES) {
-        const int size = 1 << (f.bb * K);
-        for (int i = threadIdx.x; i < size; i += GD_THREADS) {
-            s_l[i] = f.l_table[i];
-            s_h[i] = f.h_table[i];
-        }
-        __syncthreads();
-        ltab = s_l;
-        htab = s_h;
-    }
-    const int lane = threadIdx.x % GD_GROUP;
-    const int64_t dot = ((int64_t)blockIdx.x * GD_THREADS + threadIdx.x) / GD_GROUP;
+    const int lane = threadIdx.x % G;
+    const int64_t dot = ((int64_t)blockIdx.x * GD_THREADS + threadIdx.x) / G;
     const bool live = dot < batch;
     const int t = (int)f.t;
-    double acc = 0.0;
+    uint64_t acc = 0;
     if (live) {
         const int64_t row_bytes = len * K;
         const uint8_t* r1 = v1 + dot * row_bytes;
         const uint8_t* r2 = v2 + dot * row_bytes;
-        if (VEC) {  // 16-byte chunks hold 16/K whole elements (K | 16)
+        if (VEC) {  // 16-byte chunks hold 16/K whole elements (K | 16); words fit 32 bits
             const int64_t nchunks = row_bytes / 16;
-            for (int64_t ch = lane; ch < nchunks; ch += GD_GROUP) {
-                const uint4 x = __ldg(reinterpret_cast<const uint4*>(r1) + ch);
-                const uint4 y = __ldg(reinterpret_cast<const uint4*>(r2) + ch);
+            int64_t ch = lane;
+            auto body = [&](const uint4& x, const uint4& y) {
                 const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
 #pragma unroll
                     for (int e = 0; e < 4 / K; ++e) {
-                        uint64_t wx = 0, wy = 0;
+                        uint32_t wx = 0, wy = 0;
 #pragma unroll
                         for (int l = 0; l < K; ++l) {
-                            wx |= (uint64_t)((xs[q] >> (8 * (e * K + l))) & 0xFF) << (l * t);
-                            wy |= (uint64_t)((ys[q] >> (8 * (e * K + l))) & 0xFF) << (l * t);
+                            wx |= ((xs[q] >> (8 * (e * K + l))) & 0xFFu) << (l * t);
+                            wy |= ((ys[q] >> (8 * (e * K + l))) & 0xFFu) << (l * t);
                         }
-                        acc = fma(u52_to_f64(wx), u52_to_f64(wy), acc);
+                        acc += (uint64_t)wx * wy;  // IMAD.WIDE.U32
                     }
                 }
+            };
+            for (; ch + 3 * G < nchunks; ch += 4 * G) {  // 8 loads in flight per lane
+                uint4 x[4], y[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    x[i] = __ldg(reinterpret_cast<const uint4*>(r1) + ch + i * G);
+                    y[i] = __ldg(reinterpret_cast<const uint4*>(r2) + ch + i * G);
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i) body(x[i], y[i]);
             }
+            for (; ch < nchunks; ch += G)
+                body(__ldg(reinterpret_cast<const uint4*>(r1) + ch), __ldg(reinterpret_cast<const uint4*>(r2) + ch));
         } else {
-            for (int64_t e = lane; e < len; e += GD_GROUP) {
+            for (int64_t e = lane; e < len; e += G) {
                 uint64_t wx = 0, wy = 0;
 #pragma unroll
                 for (int l = 0; l < K; ++l) {
                     wx |= (uint64_t)r1[e * K + l] << (l * t);
                     wy |= (uint64_t)r2[e * K + l] << (l * t);
                 }
-                acc = fma(u52_to_f64(wx), u52_to_f64(wy), acc);
+                acc += wx * wy;  // < q^(2k-1) <= 2^53: exact
             }
         }
     }
 #pragma unroll
-    for (int off = GD_GROUP / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
     if (!live || lane != 0) return;
     constexpr int ND = 2 * K - 2;
     uint32_t u[ND + 1];
-    redq_compress_f64<ND>(acc, f.invp_up, (double)f.p, f.bound, f.p, t, u);
+    redq_compress_f64<ND>((double)acc, f.invp_up, (double)f.p, f.bound, f.p, t, u);
     uint32_t li = 0, hi = 0;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
         li |= u[i] << (f.bb * i);
         hi |= u[K - 1 + i] << (f.bb * i);
     }
-    const uint32_t res = add_coeff_bytes(ltab[li], htab[hi], f.p, K);
+    const uint32_t res = add_coeff_bytes(__ldg(f.l_table + li), __ldg(f.h_table + hi), f.p, K);
+    if (K == 2 && (reinterpret_cast<uintptr_t>(out) & 1) == 0) {
+        reinterpret_cast<uint16_t*>(out)[dot] = (uint16_t)res;
+    } else if (K == 4 && (reinterpret_cast<uintptr_t>(out) & 3) == 0) {
+        reinterpret_cast<uint32_t*>(out)[dot] = res;
+    } else {
 #pragma unroll
-    for (int l = 0; l < K; ++l) out[dot * K + l] = (uint8_t)(res >> (8 * l));
+        for (int l = 0; l < K; ++l) out[dot * K + l] = (uint8_t)(res >> (8 * l));
+    }
 }
 
 template <int K>
 static void launch_gf_dot(const uint8_t* v1, const uint8_t* v2, int64_t batch, int64_t len, const FieldConst& f,
                           uint8_t* out, cudaStream_t s) {
     const bool vec = (16 % K == 0) && ((len * K) % 16 == 0) && ((uintptr_t)v1 % 16 == 0) &&
-                     ((uintptr_t)v2 % 16 == 0);
-    const bool smem = (1 << (f.bb * K)) <= GD_SMEM_TABLE;
-    const unsigned blocks = (unsigned)((batch * GD_GROUP + GD_THREADS - 1) / GD_THREADS);
-    if (vec && smem) gf_dot_kernel<K, (16 % K == 0), true><<<blocks, GD_THREADS, 0, s>>>(v1, v2, batch, len, f, out);
-    else if (vec) gf_dot_kernel<K, (16 % K == 0), false><<<blocks, GD_THREADS, 0, s>>>(v1, v2, batch, len, f, out);
-    else if (smem) gf_dot_kernel<K, false, true><<<blocks, GD_THREADS, 0, s>>>(v1, v2, batch, len, f, out);
-    else gf_dot_kernel<K, false, false><<<blocks, GD_THREADS, 0, s>>>(v1, v2, batch, len, f, out);
+                     ((uintptr_t)v2 % 16 == 0) && K * f.t <= 32;
+    if (vec) {
+        constexpr int G = 4;  // 4 lanes per dot: a warp reads 64 contiguous bytes per dot per load
+        const unsigned blocks = (unsigned)((batch * G + GD_THREADS - 1) / GD_THREADS);
+        gf_dot_kernel<K, G, (16 % K == 0)><<<blocks, GD_THREADS, 0, s>>>(v1, v2, batch, len, f, out);
+    } else {
+        constexpr int G = 8;
+        const unsigned blocks = (unsigned)((batch * G + GD_THREADS - 1) / GD_THREADS);
+        gf_dot_kernel<K, G, false><<<blocks, GD_THREADS, 0, s>>>(v1, v2, batch, len, f, out);
+    }
 }
 
 }  // namespace qadic
@@ -248,9 +315,18 @@ int qadic_polymul_batch_u8(const uint8_t* a, const uint8_t* b, int64_t n, int32_
     c.bound = host_case2_bound();
     cudaStream_t s = (cudaStream_t)stream;
     const bool aligned = ((uintptr_t)a % 16 == 0) && ((uintptr_t)b % 16 == 0) && ((uintptr_t)out % 16 == 0);
-    if (k == 4 && aligned && 3 * t + 8 <= 32) {  // pack4 keeps words in 32 bits
-        QADIC_TIMED("polymul_k4", s,
-                    polymul_k4_kernel<<<(unsigned)((n + PM_PAIRS - 1) / PM_PAIRS), PM_THREADS, 0, s>>>(a, b, n, c, out));
+    if (k == 4 && aligned && t <= 7) {  // words < 2^28, products < 2^49 (exact, below the fdiv bound)
+        const int pi = prof_begin(s, "polymul_k4");
+        switch (t) {
+            case 1: launch_polymul_k4<1>(a, b, n, c, out, s); break;
+            case 2: launch_polymul_k4<2>(a, b, n, c, out, s); break;
+            case 3: launch_polymul_k4<3>(a, b, n, c, out, s); break;
+            case 4: launch_polymul_k4<4>(a, b, n, c, out, s); break;
+            case 5: launch_polymul_k4<5>(a, b, n, c, out, s); break;
+            case 6: launch_polymul_k4<6>(a, b, n, c, out, s); break;
+            default: launch_polymul_k4<7>(a, b, n, c, out, s); break;
+        }
+        prof_end(pi, s);
     } else {
         QADIC_TIMED("polymul_generic", s,
                     polymul_generic_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, b, n, k, c, out));
