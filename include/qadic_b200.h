@@ -42,7 +42,8 @@ typedef enum qadic_engine {
     QADIC_ENGINE_I8_TC = 1,    /* tcgen05.mma kind::i8 on coefficient planes, int32 TMEM accumulators */
     QADIC_ENGINE_F64_DMMA = 2, /* the paper's formulation: DQT-packed FP64 words on DMMA tensor cores */
     QADIC_ENGINE_F4_TC = 3,    /* tcgen05.mma kind::mxf4 (E2M1, unit block scales) on centred residues, p <= 7 */
-    QADIC_ENGINE_F4K_TC = 4    /* F4 on k(k+1)/2 Karatsuba coefficient planes + mod-p combine (fewest MACs) */
+    QADIC_ENGINE_F4K_TC = 4    /* F4 on evaluation planes (Toom-Cook over F_p: 2k-1 when 2k-1 <= p+1, else
+                                  k(k+1)/2 Karatsuba) + mod-p combine: the fewest MACs */
 } qadic_engine;
 
 QADIC_API int qadic_abi_version(void);
@@ -134,6 +135,21 @@ QADIC_API size_t qadic_gf_matmul_workspace(const qadic_field_desc *f, int64_t m,
 QADIC_API int qadic_gf_matmul_u8(const qadic_field_desc *f, const uint8_t *a, const uint8_t *b,
                        int64_t m, int64_t kdim, int64_t n, int32_t engine, int32_t fold_period,
                        void *workspace, size_t workspace_bytes, uint8_t *c, void *stream);
+
+/* cfg3 / cfg5 end to end -- the same product with HOST operands (pinned or
+ * pageable; any of a, b, c may also be a device pointer).  B is copied once,
+ * A and C move in row panels of `panel_rows` (0 = about sixteen panels) on two
+ * internal copy streams, so the H2D of panel i+1, the compute of panel i and the
+ * D2H of panel i-1 overlap.  Work is ordered on `stream`: when it completes, c
+ * holds the result.  `workspace` (device) must hold
+ * qadic_gf_matmul_host_workspace() bytes.  Replaces the host round trip around
+ * GFqField.matmul (gfext.py:311-345) that a caller with numpy arrays makes. */
+QADIC_API size_t qadic_gf_matmul_host_workspace(const qadic_field_desc *f, int64_t m, int64_t kdim, int64_t n,
+                                                int32_t engine, int64_t panel_rows);
+QADIC_API int qadic_gf_matmul_host_u8(const qadic_field_desc *f, const uint8_t *a, const uint8_t *b,
+                                      int64_t m, int64_t kdim, int64_t n, int32_t engine, int32_t fold_period,
+                                      int64_t panel_rows, void *workspace, size_t workspace_bytes, uint8_t *c,
+                                      void *stream);
 
 /* cfg4 -- C[m,n] = A[m,kdim] @ B[kdim,n] mod p with B row-compressed d+1
  * entries per word at radix 2^t (cmm.right_cmm(a, compress_rows(b)),

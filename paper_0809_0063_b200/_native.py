@@ -59,6 +59,9 @@ _SIGNATURES = {
     "qadic_gf_matmul_workspace": ([ctypes.POINTER(FieldDesc), I64, I64, I64, I32], SZ),
     "qadic_gf_matmul_u8": ([ctypes.POINTER(FieldDesc), P, P, I64, I64, I64, I32, I32, P, SZ, P, P],
                            ctypes.c_int),
+    "qadic_gf_matmul_host_workspace": ([ctypes.POINTER(FieldDesc), I64, I64, I64, I32, I64], SZ),
+    "qadic_gf_matmul_host_u8": ([ctypes.POINTER(FieldDesc), P, P, I64, I64, I64, I32, I32, I64, P, SZ, P, P],
+                                ctypes.c_int),
     "qadic_right_cmm_workspace": ([I64, I64, I64, I64, I32, I32], SZ),
     "qadic_right_cmm_u8": ([P, P, I64, I64, I64, I64, I32, I32, I32, P, SZ, P, P], ctypes.c_int),
     "qadic_polymul_batch_u8": ([P, P, I64, I32, I64, I32, P, P], ctypes.c_int),
@@ -198,6 +201,22 @@ def to_host(x, np_dtype) -> np.ndarray:
     if np.dtype(np_dtype) == np.dtype(np.uint64):
         return arr.view(np.uint64)
     return arr.astype(np_dtype, copy=False)
+
+
+def host_operand(x, np_dtype):
+    """(keep-alive object, pointer, shape) of a host operand for the C ABI's
+    host-buffer entry points -- numpy arrays and CPU tensors are used in place
+    (pinned CPU tensors give the fastest copies); None for CUDA tensors."""
+    t = torch()
+    npd = np.dtype(np_dtype)
+    if isinstance(x, t.Tensor):
+        if x.is_cuda:
+            return None
+        if x.dtype != getattr(t, _NP2T[npd]) or not x.is_contiguous():
+            x = x.to(getattr(t, _NP2T[npd])).contiguous()
+        return x, x.data_ptr(), tuple(x.shape)
+    a = np.ascontiguousarray(np.asarray(x), dtype=npd)
+    return a, a.ctypes.data, a.shape
 
 
 def out_buffer(out, shape, np_dtype):

@@ -317,6 +317,7 @@ int qadic_polymul_batch_u8(const uint8_t* a, const uint8_t* b, int64_t n, int32_
     const bool aligned = ((uintptr_t)a % 16 == 0) && ((uintptr_t)b % 16 == 0) && ((uintptr_t)out % 16 == 0);
     if (k == 4 && aligned && t <= 7) {  // words < 2^28, products < 2^49 (exact, below the fdiv bound)
         const int pi = prof_begin(s, "polymul_k4");
+        count_launch(1);
         switch (t) {
             case 1: launch_polymul_k4<1>(a, b, n, c, out, s); break;
             case 2: launch_polymul_k4<2>(a, b, n, c, out, s); break;
@@ -346,6 +347,7 @@ int qadic_gf_dot_batch_u8(const qadic_field_desc* fd, const uint8_t* v1, const u
     if (batch == 0) return QADIC_OK;
     cudaStream_t s = (cudaStream_t)stream;
     const int pi = prof_begin(s, "gf_dot");
+    count_launch(1);
     switch (f.k) {
         case 1: launch_gf_dot<1>(v1, v2, batch, len, f, out, s); break;
         case 2: launch_gf_dot<2>(v1, v2, batch, len, f, out, s); break;

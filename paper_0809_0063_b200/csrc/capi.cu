@@ -65,8 +65,8 @@ void set_error(int code, const char* fmt, ...) {
 
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
-int check_launch(const char* what) {
-    count_launch(1);
+int check_launch(const char* what, int launched) {
+    count_launch(launched);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         set_error(QADIC_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));

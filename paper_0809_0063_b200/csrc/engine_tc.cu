@@ -1293,6 +1293,7 @@ static void launch_planes(const uint8_t* a, const uint8_t* b, int64_t m, int64_t
     QADIC_TIMED("fp4k planes A", s,
                 planes_kernel<K><<<(unsigned)((ta + 255) / 256), 256, 0, s>>>(a, m, kdim, p, tab, L.S, as, L.ldk,
                                                                                 m * L.ldk));
+    if (b == nullptr) return;  // B planes already in the workspace
     const int tk = (int)((kdim + PB_KK - 1) / PB_KK), tj = (int)((n + PB_J - 1) / PB_J);
     const int64_t tiles = (int64_t)tk * tj;
     const int grid = (int)(tiles < 8 * num_sms() ? tiles : 8 * num_sms());
@@ -1315,9 +1316,12 @@ static void launch_combine(const uint8_t* d, int64_t m, int64_t n, const KaraLay
                                                                                  magic, ps, c));
 }
 
-// C[m, n, k] = A[m, K, k] B[K, n, k] over GF(p^k) through plane products
+// C[m, n, k] = A[m, K, k] B[K, n, k] over GF(p^k) through plane products.
+// Workspace: [plane table | B planes | A planes | D planes]; the table and the B
+// planes sit at offsets independent of m, so a row-panelled caller (the host
+// pipeline) prepares them once and passes b_ready for the later panels.
 static int run_kara(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
-                    void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s) {
+                    void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s, bool b_ready) {
     const int k = (int)f.k;
     PlaneSpec ps;
     QADIC_REQUIRE(plan_planes(f, &ps), QADIC_ERR_UNSUPPORTED, "no plane decomposition with <= %d planes", KMAX_S);
@@ -1326,19 +1330,21 @@ static int run_kara(const FieldConst& f, const uint8_t* a, const uint8_t* b, int
     QADIC_REQUIRE(ws != nullptr && ws_bytes >= need, QADIC_ERR_VALUE, "workspace too small (%zu < %zu)", ws_bytes,
                   need);
     uint32_t* tab = static_cast<uint32_t*>(ws);
-    uint8_t* as = static_cast<uint8_t*>(ws) + L.tab_bytes;
-    uint8_t* bs = as + L.a_bytes;
-    uint8_t* dd = bs + L.b_bytes;
+    uint8_t* bs = static_cast<uint8_t*>(ws) + L.tab_bytes;
+    uint8_t* as = bs + L.b_bytes;
+    uint8_t* dd = as + L.a_bytes;
     int ncodes = 1;
     for (int i = 0; i < k; ++i) ncodes *= (int)f.p;
     QADIC_REQUIRE(ncodes <= PT_CODES, QADIC_ERR_UNSUPPORTED, "plane table needs p^k <= %d", PT_CODES);
-    QADIC_TIMED("fp4k plane table", s,
-                plane_table_kernel<<<(ncodes + 255) / 256, 256, 0, s>>>(f.p, k, ps.S, ps, centred_e2m1_lut(f.p), tab));
+    if (!b_ready)
+        QADIC_TIMED("fp4k plane table", s,
+                    plane_table_kernel<<<(ncodes + 255) / 256, 256, 0, s>>>(f.p, k, ps.S, ps, centred_e2m1_lut(f.p), tab));
+    const uint8_t* bsrc = b_ready ? nullptr : b;
     switch (k) {
-        case 1: launch_planes<1>(a, b, m, kdim, n, f.p, tab, L, as, bs, s); break;
-        case 2: launch_planes<2>(a, b, m, kdim, n, f.p, tab, L, as, bs, s); break;
-        case 3: launch_planes<3>(a, b, m, kdim, n, f.p, tab, L, as, bs, s); break;
-        default: launch_planes<4>(a, b, m, kdim, n, f.p, tab, L, as, bs, s); break;
+        case 1: launch_planes<1>(a, bsrc, m, kdim, n, f.p, tab, L, as, bs, s); break;
+        case 2: launch_planes<2>(a, bsrc, m, kdim, n, f.p, tab, L, as, bs, s); break;
+        case 3: launch_planes<3>(a, bsrc, m, kdim, n, f.p, tab, L, as, bs, s); break;
+        default: launch_planes<4>(a, bsrc, m, kdim, n, f.p, tab, L, as, bs, s); break;
     }
     int rc = check_launch("fp4k planes");
     if (rc) return rc;
@@ -1418,10 +1424,10 @@ size_t tc_kara_workspace(uint32_t p, int64_t m, int64_t kdim, int64_t n, int k) 
 }
 
 int tc_kara_gf_matmul(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
-                      void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s) {
+                      void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s, bool b_ready) {
     QADIC_REQUIRE(tc_kara_ok(f.p, kdim, (int)f.k), QADIC_ERR_PARAMS,
                   "fp4k engine needs p <= 7, K*((p-1)/2)^2 < 2^24 and at most %d planes", tc::KMAX_S);
-    return tc::run_kara(f, a, b, m, kdim, n, ws, ws_bytes, c, s);
+    return tc::run_kara(f, a, b, m, kdim, n, ws, ws_bytes, c, s, b_ready);
 }
 
 int tc_kara_right_cmm(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n, uint32_t p, void* ws,
@@ -1432,7 +1438,7 @@ int tc_kara_right_cmm(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdi
     f.t = 8;
     f.magic = small_magic(p);
     f.xpow[0][0] = 1;
-    return tc_kara_gf_matmul(f, a, b, m, kdim, n, ws, ws_bytes, c, s);
+    return tc_kara_gf_matmul(f, a, b, m, kdim, n, ws, ws_bytes, c, s, false);
 }
 
 // ---- entry points used by matmul_api.cu ---------------------------------------

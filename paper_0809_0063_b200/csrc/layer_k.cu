@@ -205,7 +205,7 @@ int qadic_matmul_exact_u64(const uint64_t* a, const uint64_t* b, uint64_t* c, in
     dim3 grid(blocks_for(n, MM_T), blocks_for(m, MM_T));
     QADIC_REQUIRE(grid.y <= 65535, QADIC_ERR_UNSUPPORTED, "m too large for this kernel");
     mm_wrap_kernel<uint64_t><<<grid, 256, 0, s>>>(a, b, c, m, k, n, 0, 0);
-    return check_launch("matmul_exact_u64");
+    return check_launch("matmul_exact_u64", 1);
 }
 
 int qadic_matmul_mod_i64(const int64_t* a, const int64_t* b, int64_t* c, int64_t m, int64_t k, int64_t n,
@@ -221,21 +221,21 @@ int qadic_matmul_mod_i64(const int64_t* a, const int64_t* b, int64_t* c, int64_t
     dim3 grid(blocks_for(n, MM_T), blocks_for(m, MM_T));
     QADIC_REQUIRE(grid.y <= 65535, QADIC_ERR_UNSUPPORTED, "m too large for this kernel");
     mm_wrap_kernel<int64_t><<<grid, 256, 0, s>>>(a, b, c, m, k, n, p, chunk);
-    return check_launch("matmul_mod_i64");
+    return check_launch("matmul_mod_i64", 1);
 }
 
 int qadic_conv_exact_u64(const uint64_t* a, int64_t na, const uint64_t* b, int64_t nb, uint64_t* out,
                          void* stream) {
     QADIC_REQUIRE(na >= 1 && nb >= 1, QADIC_ERR_SHAPE, "convolution needs non-empty operands");
     conv_kernel<uint64_t><<<blocks_for(na + nb - 1, 256), 256, 0, (cudaStream_t)stream>>>(a, na, b, nb, out);
-    return check_launch("conv_exact_u64");
+    return check_launch("conv_exact_u64", 1);
 }
 
 int qadic_conv_exact_i64(const int64_t* a, int64_t na, const int64_t* b, int64_t nb, int64_t* out,
                          void* stream) {
     QADIC_REQUIRE(na >= 1 && nb >= 1, QADIC_ERR_SHAPE, "convolution needs non-empty operands");
     conv_kernel<int64_t><<<blocks_for(na + nb - 1, 256), 256, 0, (cudaStream_t)stream>>>(a, na, b, nb, out);
-    return check_launch("conv_exact_i64");
+    return check_launch("conv_exact_i64", 1);
 }
 
 static int redq_launch(const uint64_t* r, int64_t n, int64_t p, int32_t t, int32_t d, int mode,
@@ -248,7 +248,7 @@ static int redq_launch(const uint64_t* r, int64_t n, int64_t p, int32_t t, int32
     const uint64_t corr = (q % (uint64_t)p == 0) ? 0 : ((uint64_t)p - q % (uint64_t)p) % (uint64_t)p;
     redq_words_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
         r, n, (uint64_t)p, t, d, host_reciprocal_up(p), host_case2_bound(), corr, mode, digits, packed);
-    return check_launch(what);
+    return check_launch(what, 1);
 }
 
 int qadic_redq_compress_u64(const uint64_t* r, int64_t n, int64_t p, int32_t t, int32_t d, uint64_t* out,
@@ -268,7 +268,7 @@ int qadic_pack_rows_u8(const uint8_t* m, int64_t rows, int64_t cols, int32_t k, 
     const int64_t total = rows * ((cols + k - 1) / k);
     if (total == 0) return QADIC_OK;
     pack_rows_kernel<<<blocks_for(total, 256), 256, 0, (cudaStream_t)stream>>>(m, rows, cols, k, t, reverse, words);
-    return check_launch("pack_rows_u8");
+    return check_launch("pack_rows_u8", 1);
 }
 
 int qadic_unpack_rows_u8(const uint64_t* words, int64_t rows, int64_t cols, int32_t k, int32_t t,
@@ -277,7 +277,7 @@ int qadic_unpack_rows_u8(const uint64_t* words, int64_t rows, int64_t cols, int3
     if (rows * cols == 0) return QADIC_OK;
     unpack_rows_kernel<<<blocks_for(rows * cols, 256), 256, 0, (cudaStream_t)stream>>>(words, rows, cols, k, t,
                                                                                         reverse, out);
-    return check_launch("unpack_rows_u8");
+    return check_launch("unpack_rows_u8", 1);
 }
 
 int qadic_gather_u8(const int64_t* idx, int64_t n, const uint8_t* table, int64_t table_rows, int32_t width,
@@ -285,7 +285,7 @@ int qadic_gather_u8(const int64_t* idx, int64_t n, const uint8_t* table, int64_t
     QADIC_REQUIRE(n >= 0 && width >= 1, QADIC_ERR_VALUE, "bad gather geometry");
     if (n == 0) return QADIC_OK;
     gather_u8_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(idx, n, table, table_rows, width, out);
-    return check_launch("gather_u8");
+    return check_launch("gather_u8", 1);
 }
 
 int qadic_index_of_coeffs(const uint8_t* c, int64_t n, int32_t k, int32_t p, const int64_t* index_of_code,
@@ -293,7 +293,7 @@ int qadic_index_of_coeffs(const uint8_t* c, int64_t n, int32_t k, int32_t p, con
     QADIC_REQUIRE(n >= 0 && k >= 1 && p >= 2, QADIC_ERR_VALUE, "bad conversion geometry");
     if (n == 0) return QADIC_OK;
     index_of_coeffs_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(c, n, k, p, index_of_code, out);
-    return check_launch("index_of_coeffs");
+    return check_launch("index_of_coeffs", 1);
 }
 
 }  // extern "C"

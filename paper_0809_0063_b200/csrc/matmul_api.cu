@@ -1,6 +1,8 @@
 // Operation-level matmul entry points: bound checks (the reference's
 // a-priori conditions, src/params.py:99-141, src/gfext.py:320-325,
 // src/cmm.py:170-175) and engine selection.
+#include <vector>
+
 #include "qadic_common.cuh"
 #include "qadic_internal.h"
 
@@ -15,7 +17,7 @@ int tc_right_cmm(int kind, const uint8_t* a, const uint8_t* b, int64_t m, int64_
 size_t tc_kara_workspace(uint32_t p, int64_t m, int64_t kdim, int64_t n, int k);
 bool tc_kara_ok(uint32_t p, int64_t kdim, int k);
 int tc_kara_gf_matmul(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
-                      void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s);
+                      void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s, bool b_ready);
 int tc_kara_right_cmm(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n, uint32_t p, void* ws,
                       size_t ws_bytes, uint8_t* c, cudaStream_t s);
 size_t f64_gf_workspace(int64_t m, int64_t kdim, int64_t n);
@@ -39,6 +41,34 @@ static int resolve_engine(int32_t engine, uint32_t p, int64_t kdim, int k) {
 }
 static int tc_kind(int eng) { return eng == QADIC_ENGINE_F4_TC ? 1 : 0; }
 
+// device-pointer GF(p^k) matmul on the resolved engine; b_ready: the fp4k
+// engine's B planes are already in `ws` (row panels of one host call)
+static int gf_matmul_dev(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
+                         int32_t engine, int32_t fold_period, void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s,
+                         bool b_ready) {
+    const int eng = resolve_engine(engine, f.p, kdim, (int)f.k);
+    if (eng == QADIC_ENGINE_F4K_TC) return tc_kara_gf_matmul(f, a, b, m, kdim, n, ws, ws_bytes, c, s, b_ready);
+    if (eng == QADIC_ENGINE_I8_TC || eng == QADIC_ENGINE_F4_TC)
+        return tc_gf_matmul(tc_kind(eng), f, a, b, m, kdim, n, ws, ws_bytes, c, s);
+    QADIC_REQUIRE(eng == QADIC_ENGINE_F64_DMMA, QADIC_ERR_VALUE, "unknown engine %d", engine);
+    // accumulation bound of the packed words between folds:
+    // carry digit (< p) + span * k * (p-1)^2 must stay below q (polymul.py:159-167)
+    const int64_t q = 1ll << f.t;
+    const int64_t per = (int64_t)f.k * (f.p - 1) * (f.p - 1);
+    if (fold_period <= 0) {
+        QADIC_REQUIRE(kdim * per < q, QADIC_ERR_PARAMS,
+                      "inner dimension %lld exceeds the digit capacity of q=2**%u; give a fold period",
+                      (long long)kdim, f.t);
+        fold_period = 0;
+    } else {
+        QADIC_REQUIRE(fold_period % 4 == 0, QADIC_ERR_VALUE, "F64 fold period must be a multiple of 4 (DMMA k4)");
+        QADIC_REQUIRE((int64_t)fold_period * per <= q - 1 - (f.p - 1), QADIC_ERR_PARAMS,
+                      "fold period %d exceeds the accumulation budget", fold_period);
+        if (kdim <= fold_period) fold_period = 0;
+    }
+    return f64_gf_matmul(f, a, b, m, kdim, n, fold_period, ws, ws_bytes, c, s);
+}
+
 extern "C" {
 
 size_t qadic_gf_matmul_workspace(const qadic_field_desc* f, int64_t m, int64_t kdim, int64_t n, int32_t engine) {
@@ -61,27 +91,7 @@ int qadic_gf_matmul_u8(const qadic_field_desc* fd, const uint8_t* a, const uint8
         cudaMemsetAsync(c, 0, (size_t)(m * n * f.k), s);
         return check_launch("gf_matmul (empty K)");
     }
-    const int eng = resolve_engine(engine, f.p, kdim, (int)f.k);
-    if (eng == QADIC_ENGINE_F4K_TC) return tc_kara_gf_matmul(f, a, b, m, kdim, n, ws, ws_bytes, c, s);
-    if (eng == QADIC_ENGINE_I8_TC || eng == QADIC_ENGINE_F4_TC)
-        return tc_gf_matmul(tc_kind(eng), f, a, b, m, kdim, n, ws, ws_bytes, c, s);
-    QADIC_REQUIRE(eng == QADIC_ENGINE_F64_DMMA, QADIC_ERR_VALUE, "unknown engine %d", engine);
-    // accumulation bound of the packed words between folds:
-    // carry digit (< p) + span * k * (p-1)^2 must stay below q (polymul.py:159-167)
-    const int64_t q = 1ll << f.t;
-    const int64_t per = (int64_t)f.k * (f.p - 1) * (f.p - 1);
-    if (fold_period <= 0) {
-        QADIC_REQUIRE(kdim * per < q, QADIC_ERR_PARAMS,
-                      "inner dimension %lld exceeds the digit capacity of q=2**%u; give a fold period",
-                      (long long)kdim, f.t);
-        fold_period = 0;
-    } else {
-        QADIC_REQUIRE(fold_period % 4 == 0, QADIC_ERR_VALUE, "F64 fold period must be a multiple of 4 (DMMA k4)");
-        QADIC_REQUIRE((int64_t)fold_period * per <= q - 1 - (f.p - 1), QADIC_ERR_PARAMS,
-                      "fold period %d exceeds the accumulation budget", fold_period);
-        if (kdim <= fold_period) fold_period = 0;
-    }
-    return f64_gf_matmul(f, a, b, m, kdim, n, fold_period, ws, ws_bytes, c, s);
+    return gf_matmul_dev(f, a, b, m, kdim, n, engine, fold_period, ws, ws_bytes, c, s, false);
 }
 
 size_t qadic_right_cmm_workspace(int64_t m, int64_t kdim, int64_t n, int64_t p, int32_t d, int32_t engine) {
@@ -112,6 +122,140 @@ int qadic_right_cmm_u8(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kd
         return tc_right_cmm(tc_kind(eng), a, b, m, kdim, n, (uint32_t)p, ws, ws_bytes, c, s);
     QADIC_REQUIRE(eng == QADIC_ENGINE_F64_DMMA, QADIC_ERR_VALUE, "unknown engine %d", engine);
     return f64_right_cmm(a, b, m, kdim, n, (uint32_t)p, t, d, ws, ws_bytes, c, s);
+}
+
+// ---- host-buffer pipeline ---------------------------------------------------------
+// C = A B with host (or mixed host/device) operands: B is copied once, A and C
+// travel in row panels on two copy streams so that H2D of panel i+1, the
+// compute of panel i and the D2H of panel i-1 overlap (PCIe is full duplex).
+// Device scratch: [engine workspace for one panel | B | 2 A panels | 2 C panels].
+
+static int64_t host_panel_rows(int64_t m, int64_t panel_rows) {
+    // default ~16 panels of >= 256 rows (measured at cfg3/cfg5: 512-1024-row panels
+    // bring the call to within ~15% of the H2D time of A and B alone)
+    int64_t pr = panel_rows > 0 ? panel_rows : ((m + 15) / 16 + 127) / 128 * 128;
+    if (panel_rows <= 0 && pr < 256) pr = 256;
+    if (pr < 1) pr = 1;
+    return pr < m ? pr : m;
+}
+static size_t align_up(size_t x) { return (x + 1023) / 1024 * 1024; }
+
+static bool is_device_ptr(const void* p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+struct CopyStreams {
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+};
+static CopyStreams& copy_streams() {
+    static CopyStreams cs[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    CopyStreams& c = cs[dev & 63];
+    if (!c.h2d) {
+        cudaStreamCreateWithFlags(&c.h2d, cudaStreamNonBlocking);
+        cudaStreamCreateWithFlags(&c.d2h, cudaStreamNonBlocking);
+    }
+    return c;
+}
+
+size_t qadic_gf_matmul_host_workspace(const qadic_field_desc* f, int64_t m, int64_t kdim, int64_t n, int32_t engine,
+                                      int64_t panel_rows) {
+    if (!f || m < 0 || kdim < 0 || n < 0) return 0;
+    const int64_t pr = host_panel_rows(m, panel_rows);
+    const int64_t k = f->k;
+    return align_up(qadic_gf_matmul_workspace(f, pr, kdim, n, engine)) + align_up((size_t)(kdim * n * k)) +
+           2 * align_up((size_t)(pr * kdim * k)) + 2 * align_up((size_t)(pr * n * k));
+}
+
+int qadic_gf_matmul_host_u8(const qadic_field_desc* fd, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim,
+                            int64_t n, int32_t engine, int32_t fold_period, int64_t panel_rows, void* ws,
+                            size_t ws_bytes, uint8_t* c, void* stream) {
+    FieldConst f;
+    int rc = make_field_const(fd, &f);
+    if (rc) return rc;
+    QADIC_REQUIRE(m >= 0 && kdim >= 0 && n >= 0, QADIC_ERR_SHAPE, "incompatible shapes");
+    if (m == 0 || n == 0) return QADIC_OK;
+    QADIC_REQUIRE(a && b && c, QADIC_ERR_VALUE, "null operand");
+    const int64_t k = f.k;
+    const int64_t pr = host_panel_rows(m, panel_rows);
+    const size_t need = qadic_gf_matmul_host_workspace(fd, m, kdim, n, engine, panel_rows);
+    QADIC_REQUIRE(ws != nullptr && ws_bytes >= need, QADIC_ERR_VALUE, "workspace too small (%zu < %zu)", ws_bytes, need);
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool a_dev = is_device_ptr(a), b_dev = is_device_ptr(b), c_dev = is_device_ptr(c);
+    const size_t eng_ws = align_up(qadic_gf_matmul_workspace(fd, pr, kdim, n, engine));
+    uint8_t* base = static_cast<uint8_t*>(ws);
+    uint8_t* bbuf = base + eng_ws;
+    uint8_t* abuf[2] = {bbuf + align_up((size_t)(kdim * n * k)), nullptr};
+    abuf[1] = abuf[0] + align_up((size_t)(pr * kdim * k));
+    uint8_t* cbuf[2] = {abuf[1] + align_up((size_t)(pr * kdim * k)), nullptr};
+    cbuf[1] = cbuf[0] + align_up((size_t)(pr * n * k));
+    CopyStreams& cs = copy_streams();
+    const int64_t panels = (m + pr - 1) / pr;
+    std::vector<cudaEvent_t> evs;
+    auto event = [&]() {
+        cudaEvent_t e;
+        cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        evs.push_back(e);
+        return e;
+    };
+    auto after = [&](cudaStream_t waiter, cudaStream_t producer) {
+        cudaEvent_t e = event();
+        cudaEventRecord(e, producer);
+        cudaStreamWaitEvent(waiter, e, 0);
+        return e;
+    };
+    // the scratch buffers may still be in use by earlier work on s
+    after(cs.h2d, s);
+    after(cs.d2h, s);
+    const uint8_t* bsrc = b;
+    if (!b_dev && kdim > 0) {
+        cudaMemcpyAsync(bbuf, b, (size_t)(kdim * n * k), cudaMemcpyHostToDevice, cs.h2d);
+        bsrc = bbuf;
+        after(s, cs.h2d);
+    }
+    std::vector<cudaEvent_t> done_c(panels), done_d(panels);
+    auto d2h = [&](int64_t i) {
+        const int64_t r0 = i * pr, rows = (r0 + pr <= m ? pr : m - r0);
+        cudaStreamWaitEvent(cs.d2h, done_c[i], 0);
+        cudaMemcpyAsync(c + r0 * n * k, cbuf[i & 1], (size_t)(rows * n * k), cudaMemcpyDeviceToHost, cs.d2h);
+        done_d[i] = event();
+        cudaEventRecord(done_d[i], cs.d2h);
+    };
+    for (int64_t i = 0; i < panels && rc == QADIC_OK; ++i) {
+        const int64_t r0 = i * pr, rows = (r0 + pr <= m ? pr : m - r0);
+        const uint8_t* ap = a + r0 * kdim * k;
+        if (!a_dev && kdim > 0) {
+            if (i >= 2) cudaStreamWaitEvent(cs.h2d, done_c[i - 2], 0);  // panel i-2 no longer reads this buffer
+            cudaMemcpyAsync(abuf[i & 1], ap, (size_t)(rows * kdim * k), cudaMemcpyHostToDevice, cs.h2d);
+            ap = abuf[i & 1];
+            after(s, cs.h2d);
+        }
+        uint8_t* cp = c_dev ? c + r0 * n * k : cbuf[i & 1];
+        if (!c_dev && i >= 2) cudaStreamWaitEvent(s, done_d[i - 2], 0);  // its D2H has drained this buffer
+        if (kdim == 0) {
+            cudaMemsetAsync(cp, 0, (size_t)(rows * n * k), s);
+            rc = check_launch("gf_matmul_host (empty K)");
+        } else {
+            rc = gf_matmul_dev(f, ap, bsrc, rows, kdim, n, engine, fold_period, base, eng_ws, cp, s, i > 0);
+        }
+        done_c[i] = event();
+        cudaEventRecord(done_c[i], s);
+        // D2H lags one panel so a pageable destination does not serialise the loop
+        if (!c_dev && i >= 1) d2h(i - 1);
+    }
+    if (rc == QADIC_OK && !c_dev) {
+        d2h(panels - 1);
+        after(s, cs.d2h);  // stream-ordered completion: s sees every copy
+    }
+    for (cudaEvent_t e : evs) cudaEventDestroy(e);
+    if (rc) return rc;
+    return check_launch("gf_matmul_host_u8");
 }
 
 }  // extern "C"

@@ -108,7 +108,7 @@ QADIC_D uint32_t add_coeff_bytes(uint32_t a, uint32_t b, uint32_t p, int k) {
 // ---------------------------------------------------------------------------
 namespace qadic {
 void set_error(int code, const char* fmt, ...);
-int check_launch(const char* what);
+int check_launch(const char* what, int launched = 0);
 }  // namespace qadic
 
 #define QADIC_REQUIRE(cond, code, ...)            \

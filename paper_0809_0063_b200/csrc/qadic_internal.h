@@ -15,7 +15,8 @@ double host_reciprocal_up(int64_t p);
 double host_case2_bound();
 
 void set_error(int code, const char* fmt, ...);
-int check_launch(const char* what);
+// `launched`: kernels this call site launched outside QADIC_TIMED (those count themselves)
+int check_launch(const char* what, int launched);
 void count_launch(int n = 1);
 int prof_begin(cudaStream_t s, const char* name);
 void prof_end(int idx, cudaStream_t s);
@@ -26,6 +27,7 @@ void prof_end(int idx, cudaStream_t s);
 #define QADIC_TIMED(name, stream, ...)                          \
     do {                                                        \
         int _qadic_pi = ::qadic::prof_begin((stream), (name));  \
+        ::qadic::count_launch(1);                               \
         __VA_ARGS__;                                            \
         ::qadic::prof_end(_qadic_pi, (stream));                 \
     } while (0)

@@ -347,6 +347,8 @@ class GFqField:
         in-register REDQ fold every `fold_period` inner terms (default: the
         largest multiple of 4 within the accumulation budget), i.e. the
         K-chunked GFqField.matmul of SURVEY.md 8(b)."""
+        if not (N.is_tensor(a) and a.is_cuda):  # host A: panelled H2D / compute / D2H pipeline
+            return self._matmul_host(a, b, engine, fold_period, out)
         da, ha = N.to_dev(a, np.uint8)
         db, hb = N.to_dev(b, np.uint8)
         if da.dim() != 3 or db.dim() != 3 or da.shape[1] != db.shape[0] or da.shape[2] != self.k \
@@ -367,6 +369,54 @@ class GFqField:
         N.check(N.lib().qadic_gf_matmul_u8(desc, N.ptr(da), N.ptr(db), m, kd, n, eng, fold, N.ptr(ws), ws_bytes,
                                            N.ptr(dev), N.stream_ptr()), DimensionMismatch)
         return N.finish(dev, out, ha or hb, np.uint8)
+
+    def _matmul_host(self, a, b, engine, fold_period, out, panel_rows: int = 0):
+        """matmul_coeffs with a host A (B and `out` host or device): one call of
+        qadic_gf_matmul_host_u8, which copies B once and streams A / C in row
+        panels so the PCIe transfers overlap the tensor-core work."""
+        ha = N.host_operand(a, np.uint8)
+        hb = N.host_operand(b, np.uint8)
+        db = None
+        if hb is None:
+            db = b.contiguous() if b.dtype == N.torch().uint8 else b.to(N.torch().uint8).contiguous()
+            bshape, bptr = tuple(db.shape), db.data_ptr()
+        else:
+            bshape, bptr = hb[2], hb[1]
+        ashape, aptr = ha[2], ha[1]
+        if len(ashape) != 3 or len(bshape) != 3 or ashape[1] != bshape[0] or ashape[2] != self.k \
+                or bshape[2] != self.k:
+            raise DimensionMismatch("incompatible shapes")
+        m, kd, n = ashape[0], ashape[1], bshape[1]
+        eng = N.ENGINES[engine]
+        fold = 0
+        if eng == N.ENGINE_F64_DMMA and kd * self.k * (self.p - 1) ** 2 >= self.params.q:
+            fold = self.max_fold_period() if fold_period is None else int(fold_period)
+            if fold < 4:
+                raise ParamsViolation("accumulation budget below one DMMA k-step")
+        if out is None:
+            res = np.empty((m, n, self.k), dtype=np.uint8)
+            cptr, keep = res.ctypes.data, res
+        else:
+            if tuple(out.shape) != (m, n, self.k):
+                raise ValueError(f"out must have shape {(m, n, self.k)}")
+            if N.is_tensor(out):
+                if not out.is_contiguous() or out.dtype != N.torch().uint8:
+                    raise ValueError("out must be a contiguous uint8 tensor")
+                cptr, keep = out.data_ptr(), out
+            else:
+                if not (out.flags.c_contiguous and out.dtype == np.uint8):
+                    raise ValueError("out must be a C-contiguous uint8 array")
+                cptr, keep = out.ctypes.data, out
+        desc = self.field_desc()
+        L = N.lib()
+        ws_bytes = L.qadic_gf_matmul_host_workspace(desc, m, kd, n, eng, panel_rows)
+        ws = N.workspace(ws_bytes)
+        N.check(L.qadic_gf_matmul_host_u8(desc, aptr, bptr, m, kd, n, eng, fold, panel_rows, N.ptr(ws), ws_bytes,
+                                          cptr, N.stream_ptr()), DimensionMismatch)
+        if out is None or not (N.is_tensor(out) and out.is_cuda):
+            N.torch().cuda.current_stream().synchronize()  # host result complete on return
+        del ha, hb, db, keep
+        return res if out is None else out
 
     def _add_indices(self, ia: np.ndarray, ib: np.ndarray) -> np.ndarray:
         """Field addition of handle arrays through coefficient codes."""

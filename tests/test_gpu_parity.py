@@ -234,6 +234,40 @@ class TestGFMatmul:
         for e in ENGINES:
             assert np.array_equal(f.matmul_coeffs(a, b, engine=e), ref)
 
+    @pytest.mark.parametrize("engine", ENGINES)
+    @pytest.mark.parametrize("panel", [7, 100, 256, 0])
+    def test_host_pipeline_panels(self, engine, panel):
+        """qadic_gf_matmul_host_u8: row panels (ragged last panel, B planes
+        prepared once and reused) give the device-path result."""
+        f = W.field_for(W.CONFIGS[5])
+        of = O.build_field(7, 3, irreducible=[5, 0, 0, 1], max_dot_length=9)
+        g = W.rng(panel + 5)
+        a = g.integers(0, 7, (300, 260, 3), dtype=np.uint8)
+        b = g.integers(0, 7, (260, 130, 3), dtype=np.uint8)
+        got = f._matmul_host(a, b, engine, None, None, panel_rows=panel)
+        assert np.array_equal(got, O.gf_matmul_planes(of, a, b))
+
+    def test_host_pipeline_mixed_buffers(self):
+        """pinned / pageable / device operands in every combination the API allows."""
+        import torch
+
+        f = W.field_for(W.CONFIGS[3])
+        g = W.rng(77)
+        a = g.integers(0, 3, (513, 640, 2), dtype=np.uint8)
+        b = g.integers(0, 3, (640, 300, 2), dtype=np.uint8)
+        ref = f.matmul_coeffs(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()).cpu().numpy()
+        a_pin, b_pin = torch.from_numpy(a).pin_memory(), torch.from_numpy(b).pin_memory()
+        o_pin = torch.empty((513, 300, 2), dtype=torch.uint8).pin_memory()
+        assert f.matmul_coeffs(a_pin, b_pin, out=o_pin) is o_pin
+        assert np.array_equal(o_pin.numpy(), ref)
+        o_dev = torch.empty((513, 300, 2), dtype=torch.uint8, device="cuda")
+        f.matmul_coeffs(a_pin, torch.from_numpy(b).cuda(), out=o_dev)
+        assert np.array_equal(o_dev.cpu().numpy(), ref)
+        o_np = np.empty((513, 300, 2), np.uint8)
+        f._matmul_host(a, b_pin, "auto", None, o_np, panel_rows=128)
+        assert np.array_equal(o_np, ref)
+        assert np.array_equal(f.matmul_coeffs(a, b), ref)
+
     def test_guards(self, golden_scalars):
         f = _field(golden_scalars, "gf9_64")
         with pytest.raises(Q.ParamsViolation):
