@@ -1,7 +1,7 @@
 """Benchmark of the qadic hot path on B200 (contract: see DESIGN.md section 6).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5|all]
-                    [--engine auto|i8|f64] [--impl ours|reference]
+                    [--engine auto|i8|f64|fp4|fp4k] [--impl ours|reference]
 
 One "step" is one pass of the hot path over one batch of the config's
 synthetic seeded input (BASELINE.json configs).  Default workload: cfg5 --
@@ -569,7 +569,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="5")
-    ap.add_argument("--engine", default="auto", choices=["auto", "i8", "f64"])
+    ap.add_argument("--engine", default="auto", choices=["auto", "i8", "f64", "fp4", "fp4k"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager launches for cfg1/cfg2")

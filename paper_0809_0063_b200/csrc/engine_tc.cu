@@ -98,6 +98,7 @@ struct Params {
     int nibble_out;      // 0: uint8 residues; 1: residues packed two per byte
     uint8_t* c;
     uint8_t W[4][8];     // FUSE_K: combination weights (mod p), C_l = sum_s W[l][s] D_s
+    uint32_t sf;         // 4 x UE8M0 block scale bytes (0x7F7F7F7F: every scale 2^0)
 };
 
 // tile index -> (plane, m tile, n tile).  Unfused: planes outermost.  Fused:
@@ -154,8 +155,7 @@ __device__ __forceinline__ void tmem_ld_32x32b_x16(uint32_t taddr, uint32_t (&v)
 }
 
 // every scale factor = 2^0 (UE8M0 0x7F): fill 32 TMEM columns of this warp's lanes
-__device__ __forceinline__ void tmem_fill_sf(uint32_t taddr) {
-    const uint32_t v = 0x7F7F7F7Fu;
+__device__ __forceinline__ void tmem_fill_sf(uint32_t taddr, uint32_t v) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
         "{%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, "
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     if (KIND == KIND_F4 && warp >= 4) {
-        tmem_fill_sf(tmem_base + ((uint32_t)((warp - 4) * 32) << 16) + Cfg<KIND>::SF_COL);
+        tmem_fill_sf(tmem_base + ((uint32_t)((warp - 4) * 32) << 16) + Cfg<KIND>::SF_COL, prm.sf);
         tc_fence_before();
     }
     if (PAIR) cluster_sync();
@@ -691,8 +691,21 @@ static bool pair_mode() {
 }
 
 // E2M1 nibble codes of the centred residues 0..p-1 (p <= 7), packed 4 bits each
+// E2M1 codes of the centred residues.  Default: the halves 0, 0.5, 1, 1.5
+// (codes 0..3) under block scales 2^1 on both operands, so every product is
+// (x/2)(y/2) * 4 = x*y exactly.  QADIC_E2M1_INT=1: the integers 0..3 themselves
+// (codes 0, 2, 4, 5) under unit scales.  Same exact sums; the half codes toggle
+// fewer operand bits and the power-capped GEMM clocks higher (cfg5: 0.787 vs
+// 0.819 ms per fp4k GEMM).
+static bool e2m1_half() {
+    static const bool on = !(getenv("QADIC_E2M1_INT") && atoi(getenv("QADIC_E2M1_INT")) != 0);
+    return on;
+}
+static uint32_t e2m1_scale_word() { return e2m1_half() ? 0x80808080u : 0x7F7F7F7Fu; }
 static uint32_t centred_e2m1_lut(uint32_t p) {
-    static const uint32_t pos[4] = {0x0, 0x2, 0x4, 0x5};  // 0, 1, 2, 3
+    static const uint32_t pos_int[4] = {0x0, 0x2, 0x4, 0x5};   // 0, 1, 2, 3
+    static const uint32_t pos_half[4] = {0x0, 0x1, 0x2, 0x3};  // 0, 0.5, 1, 1.5
+    const uint32_t* pos = e2m1_half() ? pos_half : pos_int;
     uint32_t lut = 0;
     for (uint32_t r = 0; r < p; ++r) {
         const int v = (2 * r <= p - 1) ? (int)r : (int)r - (int)p;
@@ -820,7 +833,8 @@ static int run(int kind, const FieldConst& f, const uint8_t* a, const uint8_t* b
     if (rc) return rc;
     rc = make_tmap(&tb, bx, L.inner, n * k, L.ldb, pair ? BN / 2 : BN);
     if (rc) return rc;
-    Params prm;
+    Params prm = {};
+    prm.sf = e2m1_scale_word();
     prm.M = m;
     prm.N = n * k;
     prm.ldc = n * k;
@@ -1267,6 +1281,114 @@ __global__ void __launch_bounds__(256) combine_kernel(const uint8_t* __restrict_
     }
 }
 
+// SWAR variant (S*(p-1)^2 < 256): every byte lane of the weighted plane sum
+// stays below 256, so the sum, the reduction mod p and the interleave into
+// coefficient-minor order all run on 4 lanes per instruction:
+//   x mod p = x - p * floor(x / p),  floor(x / p) = (x * lm) >> ls per 16-bit lane
+//   (host-checked exact for every lane value that can occur), then PRMT places
+//   the K coefficient words of 4 columns into K output words.
+struct LaneDiv {
+    uint32_t m, sh, qmask;  // qmask: per 16-bit lane, bits that can hold the quotient
+};
+
+__device__ __forceinline__ uint32_t lanes_mod_div(uint32_t x, uint32_t p, LaneDiv d) {
+    const uint32_t e = x & 0x00FF00FFu, o = (x >> 8) & 0x00FF00FFu;
+    const uint32_t qe = ((e * d.m) >> d.sh) & d.qmask, qo = ((o * d.m) >> d.sh) & d.qmask;
+    return x - (qe | (qo << 8)) * p;
+}
+
+// T[l] lanes = columns c0..c3 of coefficient l -> out[w] = bytes 4w..4w+3 of the
+// coefficient-minor stream (column-major over l)
+template <int K>
+__device__ __forceinline__ void place_coeffs(const uint32_t* T, uint32_t* out) {
+    if constexpr (K == 2) {
+        out[0] = __byte_perm(T[0], T[1], 0x5140);
+        out[1] = __byte_perm(T[0], T[1], 0x7362);
+    } else if constexpr (K == 3) {
+        out[0] = __byte_perm(__byte_perm(T[0], T[1], 0x1040), T[2], 0x3410);
+        out[1] = __byte_perm(__byte_perm(T[1], T[0], 0x2601), T[2], 0x3250);
+        out[2] = __byte_perm(__byte_perm(T[2], T[0], 0x3072), T[1], 0x3710);
+    } else {
+#pragma unroll
+        for (int w = 0; w < K; ++w) {
+            uint32_t r = 0;
+#pragma unroll
+            for (int bi = 0; bi < 4; ++bi) {
+                const int b = 4 * w + bi, col = b / K, l = b % K;
+                r |= ((T[l] >> (8 * col)) & 0xFFu) << (8 * bi);
+            }
+            out[w] = r;
+        }
+    }
+}
+
+template <int K, int S>
+__global__ void __launch_bounds__(256) combine_swar_kernel(const uint8_t* __restrict__ d, int64_t M, int64_t N,
+                                                           int64_t ldd, int64_t plane_stride, uint32_t p,
+                                                           LaneDiv ld, PlaneSpec ps, uint8_t* __restrict__ c) {
+    const int64_t chunks = (N + 31) / 32;
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= M * chunks) return;
+    const int64_t m = idx / chunks, q = idx % chunks;
+    const int64_t j0 = q * 32;
+    uint32_t dv[S][4];
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+        const uint4 x = __ldg(reinterpret_cast<const uint4*>(d + s * plane_stride + m * ldd + j0 / 2));
+        dv[s][0] = x.x; dv[s][1] = x.y; dv[s][2] = x.z; dv[s][3] = x.w;
+    }
+    uint32_t o[8 * K];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {  // one plane word = 8 columns (nibbles; even / odd columns -> byte lanes)
+        uint32_t lo[K], hi[K];
+#pragma unroll
+        for (int l = 0; l < K; ++l) {
+            uint32_t ev = 0, od = 0;
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const uint32_t w = ps.W[l][s];
+                ev += (dv[s][g] & 0x0F0F0F0Fu) * w;
+                od += ((dv[s][g] >> 4) & 0x0F0F0F0Fu) * w;
+            }
+            ev = lanes_mod_div(ev, p, ld);
+            od = lanes_mod_div(od, p, ld);
+            lo[l] = __byte_perm(ev, od, 0x5140);  // columns 0..3 of this word
+            hi[l] = __byte_perm(ev, od, 0x7362);  // columns 4..7
+        }
+        place_coeffs<K>(lo, o + g * 2 * K);
+        place_coeffs<K>(hi, o + g * 2 * K + K);
+    }
+    uint8_t* dst = c + (m * N + j0) * K;
+    if (j0 + 32 <= N && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+        for (int v = 0; v < 2 * K; ++v)
+            reinterpret_cast<uint4*>(dst)[v] = make_uint4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+    } else {
+#pragma unroll
+        for (int e = 0; e < 32 * K; ++e)
+            if (j0 + e / K < N) dst[e] = (uint8_t)(o[e >> 2] >> (8 * (e & 3)));
+    }
+}
+
+// exact per-16-bit-lane division by p for lane values <= xmax (false: none found)
+static bool lane_div_plan(uint32_t p, uint32_t xmax, LaneDiv* d) {
+    for (uint32_t sh = 4; sh <= 15; ++sh) {
+        const uint32_t m = ((1u << sh) + p - 1) / p;  // ceil(2^sh / p)
+        if ((uint64_t)xmax * m >= 65536) break;
+        const uint32_t qmax = xmax / p;
+        if (qmax >= (1u << (16 - sh))) continue;  // quotient must stay below the spill-in bits
+        bool ok = true;
+        for (uint32_t x = 0; x <= xmax && ok; ++x) ok = ((x * m) >> sh) == x / p;
+        if (ok) {
+            d->m = m;
+            d->sh = sh;
+            d->qmask = ((1u << (16 - sh)) - 1) * 0x00010001u;
+            return true;
+        }
+    }
+    return false;
+}
+
 struct KaraLayout {
     int S;
     int64_t ldk;   // bytes per plane row of A_s / B_s (packed K)
@@ -1286,31 +1408,74 @@ static KaraLayout kara_plan(int S, int64_t m, int64_t kdim, int64_t n, int k) {
     return L;
 }
 
+// A side stream per device: the B-plane conversion (shared-memory bound) runs
+// concurrently with the A-plane conversion (HBM bound); joined before the GEMM.
+struct SideStream {
+    cudaStream_t st = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+static SideStream& side_stream() {
+    static SideStream ss[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    SideStream& x = ss[dev & 63];
+    if (!x.st) {
+        cudaStreamCreateWithFlags(&x.st, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming);
+    }
+    return x;
+}
+
 template <int K>
 static void launch_planes(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n, uint32_t p,
                           const uint32_t* tab, const KaraLayout& L, uint8_t* as, uint8_t* bs, cudaStream_t s) {
+    const bool concurrent = b != nullptr && !getenv_flag("QADIC_SERIAL_PLANES");
+    if (b != nullptr) {  // (b == nullptr: B planes already in the workspace)
+        const int tk = (int)((kdim + PB_KK - 1) / PB_KK), tj = (int)((n + PB_J - 1) / PB_J);
+        const int64_t tiles = (int64_t)tk * tj;
+        const int grid = (int)(tiles < 8 * num_sms() ? tiles : 8 * num_sms());
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(planes_b_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)planes_b_smem<K>());
+            attr = true;
+        }
+        cudaStream_t sb = s;
+        if (concurrent) {
+            SideStream& ss = side_stream();
+            cudaEventRecord(ss.fork, s);
+            cudaStreamWaitEvent(ss.st, ss.fork, 0);
+            sb = ss.st;
+        }
+        QADIC_TIMED("fp4k planes B", sb,
+                    planes_b_kernel<K><<<grid, 256, planes_b_smem<K>(), sb>>>(b, kdim, n, p, tab, L.S, bs, L.ldk,
+                                                                               n * L.ldk, tk, tj));
+        if (concurrent) cudaEventRecord(side_stream().join, sb);
+    }
     const int64_t ta = m * (L.ldk / 16);
     QADIC_TIMED("fp4k planes A", s,
                 planes_kernel<K><<<(unsigned)((ta + 255) / 256), 256, 0, s>>>(a, m, kdim, p, tab, L.S, as, L.ldk,
                                                                                 m * L.ldk));
-    if (b == nullptr) return;  // B planes already in the workspace
-    const int tk = (int)((kdim + PB_KK - 1) / PB_KK), tj = (int)((n + PB_J - 1) / PB_J);
-    const int64_t tiles = (int64_t)tk * tj;
-    const int grid = (int)(tiles < 8 * num_sms() ? tiles : 8 * num_sms());
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(planes_b_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)planes_b_smem<K>());
-        attr = true;
-    }
-    QADIC_TIMED("fp4k planes B", s,
-                planes_b_kernel<K><<<grid, 256, planes_b_smem<K>(), s>>>(b, kdim, n, p, tab, L.S, bs, L.ldk, n * L.ldk,
-                                                                          tk, tj));
+    if (concurrent) cudaStreamWaitEvent(s, side_stream().join, 0);
 }
 
 template <int K>
 static void launch_combine(const uint8_t* d, int64_t m, int64_t n, const KaraLayout& L, uint32_t p, uint32_t magic,
                            const PlaneSpec& ps, uint8_t* c, cudaStream_t s) {
     const int64_t tot = m * ((n + 31) / 32);
+    LaneDiv ld;
+    if ((uint32_t)L.S * (p - 1) * (p - 1) < 256 && lane_div_plan(p, (uint32_t)L.S * (p - 1) * (p - 1), &ld) &&
+        !getenv_flag("QADIC_COMBINE_SCALAR")) {
+        const unsigned blocks = (unsigned)((tot + 255) / 256);
+        auto go = [&](auto kern) {
+            QADIC_TIMED("fp4k combine", s, kern<<<blocks, 256, 0, s>>>(d, m, n, L.ldd, m * L.ldd, p, ld, ps, c));
+        };
+        // the plane counts plan_planes() produces: Toom 2K-1, Karatsuba K(K+1)/2
+        constexpr int S_TOOM = 2 * K - 1, S_KARA = K * (K + 1) / 2 <= KMAX_S ? K * (K + 1) / 2 : 2 * K - 1;
+        if (L.S == S_TOOM) { go(combine_swar_kernel<K, S_TOOM>); return; }
+        if (L.S == S_KARA) { go(combine_swar_kernel<K, S_KARA>); return; }
+    }
     QADIC_TIMED("fp4k combine", s,
                 combine_kernel<K><<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(d, m, n, L.ldd, m * L.ldd, L.S, p,
                                                                                  magic, ps, c));
@@ -1355,7 +1520,8 @@ static int run_kara(const FieldConst& f, const uint8_t* a, const uint8_t* b, int
     if (rc) return rc;
     rc = make_tmap(&tb, bs, (kdim + 1) / 2, L.S * n, L.ldk, pair ? BN / 2 : BN);
     if (rc) return rc;
-    Params prm;
+    Params prm = {};
+    prm.sf = e2m1_scale_word();
     prm.M = m;
     prm.N = n;
     prm.p = f.p;

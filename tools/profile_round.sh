@@ -1,0 +1,40 @@
+#!/bin/bash
+# Measurement campaign for one round (run on the GPU box from the repo root):
+#   1. bench lines for every config / engine (no profiler attached);
+#   2. the ncu launch list of the default bench command;
+#   3. one `ncu --set full` capture per hot kernel of the headline (cfg5) and of cfg1-4.
+# Every ncu command runs only after the same program exited 0 without ncu.
+set -u
+R=${1:-r01}
+O=gpurun_out/$R
+mkdir -p $O
+NCU="ncu --clock-control none"
+B="python bench.py --no-cpu-baseline"
+ok=1
+for c in 1 2; do $B --config $c --steps 20 --warmup 5 > $O/bench_cfg$c.json 2>>$O/bench.err || ok=0; done
+for c in 3 4 5; do
+  for e in auto i8 fp4 fp4k; do $B --config $c --engine $e --steps 10 --warmup 3 > $O/bench_cfg${c}_$e.json 2>>$O/bench.err || ok=0; done
+done
+$B --config 3 --engine f64 --steps 3 --warmup 3 > $O/bench_cfg3_f64.json 2>>$O/bench.err || ok=0
+$B --config 5 --engine f64 --steps 3 --warmup 3 > $O/bench_cfg5_f64.json 2>>$O/bench.err || ok=0
+python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $O/launch_cmd.json 2>>$O/bench.err && \
+  $NCU --metrics gpu__time_duration.sum -c 400 --csv --log-file $O/launches_cfg5.csv \
+    python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+T="python tools/ncu_target.py"
+full() {  # name config engine kernel-regex
+  $T --config $2 --engine $3 > /dev/null 2>&1 && \
+  $NCU --set full --import-source on -k "regex:$4" -s 0 -c 1 -o $O/$1 -f $T --config $2 --engine $3 > $O/$1.log 2>&1
+  ncu -i $O/$1.ncu-rep --page raw --csv > $O/$1_raw.csv 2>/dev/null
+  ncu -i $O/$1.ncu-rep --page details --csv > $O/$1_details.csv 2>/dev/null
+}
+full cfg5_fp4k_gemm 5 auto gemm_modp
+full cfg5_planes_b 5 auto planes_b
+full cfg5_planes_a 5 auto "planes_kernel"
+full cfg5_combine 5 auto combine
+full cfg3_fp4k_gemm 3 auto gemm_modp
+full cfg4_fp4k_gemm 4 auto gemm_modp
+full cfg1_polymul 1 auto polymul
+full cfg2_gf_dot 2 auto gf_dot
+full cfg5_i8_gemm 5 i8 gemm_modp
+echo "bench ok=$ok"
+ls -la $O | head -80
