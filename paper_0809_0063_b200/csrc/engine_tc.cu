@@ -29,6 +29,8 @@
 // uint8) overlapping the next tile through two TMEM accumulators.
 #include <cuda.h>
 
+#include <utility>
+
 #include "qadic_common.cuh"
 #include "qadic_internal.h"
 #include "sm100_ptx.cuh"
@@ -94,6 +96,7 @@ struct Params {
     uint32_t offset;     // multiple of p added before the unsigned mod (centred kinds)
     uint64_t magic64;
     int m_tiles, n_tiles, num_kb;
+    int n_full;          // column tiles of full width BN (n_tiles - 1 when N % BN != 0)
     int planes;          // independent plane products, stacked along the A / B rows
     int nibble_out;      // 0: uint8 residues; 1: residues packed two per byte
     uint8_t* c;
@@ -116,15 +119,35 @@ __device__ __forceinline__ void tile_coords(int tile, int m_tiles, int n_tiles, 
     nt = r / gm;
 }
 
+// MMA width of column tile nt: BN, or the last tile's remainder rounded up to
+// 16 (the instruction's N granularity) -- a narrow tail costs its own width,
+// not a full BN (cfg5: N = 8192 = 34 x 240 + 32)
+template <int BN>
+__device__ __forceinline__ int tile_n(const Params& prm, int nt) {
+    const int64_t rem = prm.N - (int64_t)nt * BN;
+    return rem >= BN ? BN : (int)((rem + 15) / 16 * 16);
+}
+
 template <int FUSE_K>
 __device__ __forceinline__ void decode_tile(int tile, const Params& prm, int& pl, int& mt, int& nt) {
     if (FUSE_K) {
         pl = tile % prm.planes;
         tile_coords(tile / prm.planes, prm.m_tiles, prm.n_tiles, mt, nt);
     } else {
-        const int plane_tiles = prm.m_tiles * prm.n_tiles;
-        pl = tile / plane_tiles;
-        tile_coords(tile % plane_tiles, prm.m_tiles, prm.n_tiles, mt, nt);
+        // full-width tiles first (plane-major, grouped raster), then the narrow
+        // tail tiles of every plane: the round-robin assignment then hands the
+        // cheap tails to the CTAs that got one full tile fewer
+        const int full_tiles = prm.m_tiles * prm.n_full;
+        const int F = full_tiles * prm.planes;
+        if (tile < F) {
+            pl = tile / full_tiles;
+            tile_coords(tile % full_tiles, prm.m_tiles, prm.n_full, mt, nt);
+        } else {
+            const int i = tile - F;
+            pl = i / prm.m_tiles;
+            mt = i % prm.m_tiles;
+            nt = prm.n_tiles - 1;
+        }
     }
 }
 
@@ -234,7 +257,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                 int pl, mt, nt;
                 decode_tile<FUSE_K>(tile, prm, pl, mt, nt);
                 const int arow = (int)(pl * prm.M) + mt * G::TILE_M + (int)rank * BM;
-                const int brow = (int)(pl * prm.N) + nt * BN + (int)rank * G::B_ROWS;
+                // the pair splits the tile's (possibly narrowed, see tile_n) columns in halves
+                const int brow = (int)(pl * prm.N) + nt * BN + (int)rank * (tile_n<BN>(prm, nt) / 2);
                 for (int kb = 0; kb < prm.num_kb; ++kb) {
                     mbar_wait(&empty_bar[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * G::STAGE_BYTES;
@@ -255,13 +279,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
     } else if (warp == 1 && leader) {
         // ===== MMA issuer (pair leader only): 4 MMAs of 32 bytes per stage =====
-        constexpr uint32_t idesc =
-            KIND == KIND_I8 ? idesc_u8_s32(G::TILE_M, BN) : idesc_mxf4(G::TILE_M, BN);
         int stage = 0;
         uint32_t phase = 0;
         int local = 0;
         for (int u = group_id; u < units; u += num_groups)
         for (int sp = 0; sp < per_unit; ++sp, ++local) {
+            int pl, mt, nt;
+            decode_tile<FUSE_K>(u * per_unit + sp, prm, pl, mt, nt);
+            const uint32_t nn = (uint32_t)tile_n<BN>(prm, nt);
+            const uint32_t idesc = KIND == KIND_I8 ? idesc_u8_s32(G::TILE_M, nn) : idesc_mxf4(G::TILE_M, nn);
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
             mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
@@ -381,8 +407,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                 continue;
             }
             uint8_t* crow = prm.c + pl * prm.c_plane + row * prm.ldc;
+            const int nch = tile_n<BN>(prm, nt) / 16;  // accumulator columns the MMA wrote
 #pragma unroll 1
-            for (int ch = 0; ch < BN / 16; ++ch) {
+            for (int ch = 0; ch < nch; ++ch) {
                 uint32_t v[16];
                 tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + ch * 16, v);
                 tmem_ld_wait();
@@ -843,6 +870,7 @@ static int run(int kind, const FieldConst& f, const uint8_t* a, const uint8_t* b
     prm.magic64 = wide_magic(f.p);
     prm.m_tiles = (int)((m + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM));
     prm.n_tiles = (int)((prm.N + BN - 1) / BN);
+    prm.n_full = (int)(prm.N / BN);
     prm.num_kb = (int)((L.inner + BK - 1) / BK);
     prm.c = c;
     prm.c_plane = 0;
@@ -1020,28 +1048,73 @@ __device__ __forceinline__ void byte_lut_from_table(const uint32_t* tab, uint32_
 }
 
 // 8 x 8 transpose of 4-bit cells: on return nibble e of x[s] = old nibble s of x[e]
+// 8 words x 8 nibbles -> transposed (word s = nibble s of the 8 inputs):
+// 16-bit and 8-bit stages are byte permutes, the 4-bit stage two SHF+LOP3 pairs.
 __device__ __forceinline__ void transpose8_nibbles(uint32_t (&x)[8]) {
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
-        if ((r & 4) == 0) {
-            const uint32_t t = ((x[r] >> 16) ^ x[r + 4]) & 0x0000FFFFu;
-            x[r] ^= t << 16;
-            x[r + 4] ^= t;
-        }
+    for (int r = 0; r < 4; ++r) {
+        const uint32_t a = x[r], b = x[r + 4];
+        x[r] = __byte_perm(a, b, 0x5410);
+        x[r + 4] = __byte_perm(a, b, 0x7632);
+    }
 #pragma unroll
     for (int r = 0; r < 8; ++r)
         if ((r & 2) == 0) {
-            const uint32_t t = ((x[r] >> 8) ^ x[r + 2]) & 0x00FF00FFu;
-            x[r] ^= t << 8;
-            x[r + 2] ^= t;
+            const uint32_t a = x[r], b = x[r + 2];
+            x[r] = __byte_perm(a, b, 0x6240);
+            x[r + 2] = __byte_perm(a, b, 0x7351);
         }
 #pragma unroll
-    for (int r = 0; r < 8; ++r)
-        if ((r & 1) == 0) {
-            const uint32_t t = ((x[r] >> 4) ^ x[r + 1]) & 0x0F0F0F0Fu;
-            x[r] ^= t << 4;
-            x[r + 1] ^= t;
+    for (int r = 0; r < 8; r += 2) {
+        const uint32_t a = x[r], b = x[r + 1];
+        x[r] = (a & 0x0F0F0F0Fu) | ((b << 4) & 0xF0F0F0F0u);
+        x[r + 1] = ((a >> 4) & 0x0F0F0F0Fu) | (b & 0xF0F0F0F0u);
+    }
+}
+
+// Element codes sum_i p^i b_i of K-byte elements packed back to back in 32-bit
+// words, by byte dot products: an element at byte offset o of word w is
+// dp4a(w, A[o]) (+ dp4a(w+1, B[o]) when it straddles), A/B holding p^i in the
+// element's byte slots.  K = 4 (word aligned) keeps p^3 (up to 343) out of the
+// byte weights: dp4a(w, [1, p, p^2, 0]) + p^3 * (w >> 24).
+template <int K>
+struct CodeCoef {
+    uint32_t a[4], b[4], p3;
+};
+template <int K>
+__device__ __forceinline__ CodeCoef<K> make_code_coef(uint32_t p) {
+    CodeCoef<K> c;
+    uint32_t pw[4] = {1, p, p * p, p * p * p};
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+        c.a[o] = c.b[o] = 0;
+#pragma unroll
+        for (int i = 0; i < K; ++i) {
+            if (K == 4 && i == 3) continue;
+            if (o + i < 4) c.a[o] |= pw[i] << (8 * (o + i));
+            else c.b[o] |= pw[i] << (8 * (o + i - 4));
         }
+    }
+    c.p3 = pw[3];
+    return c;
+}
+template <int K, int E, int NW>
+__device__ __forceinline__ uint32_t elem_code(const uint32_t (&w)[NW], const CodeCoef<K>& c) {
+    constexpr int off = E * K, wi = off >> 2, o = off & 3;
+    uint32_t code = __dp4a(w[wi], c.a[o], 0u);
+    if constexpr (K == 4) code += c.p3 * (w[wi] >> 24);
+    if constexpr (o + K > 4 && K != 4) code = __dp4a(w[wi + 1], c.b[o], code);
+    return code;
+}
+template <int K, int NW, int... Es>
+__device__ __forceinline__ void elem_codes_seq(const uint32_t (&w)[NW], const CodeCoef<K>& c, uint32_t* out,
+                                               std::integer_sequence<int, Es...>) {
+    ((out[Es] = elem_code<K, Es>(w, c)), ...);
+}
+// codes of the NE = 4 * NW / K elements held in w[]
+template <int K, int NW>
+__device__ __forceinline__ void elem_codes(const uint32_t (&w)[NW], const CodeCoef<K>& c, uint32_t* out) {
+    elem_codes_seq<K, NW>(w, c, out, std::make_integer_sequence<int, 4 * NW / K>{});
 }
 
 constexpr int PT_CODES = 1024;
@@ -1090,16 +1163,13 @@ __global__ void __launch_bounds__(256) planes_kernel(const uint8_t* __restrict__
         return;
     }
     uint32_t w[KMAX_S][4];
+    uint32_t code[32];
+    elem_codes<K, 8 * K>(in, make_code_coef<K>(p), code);
 #pragma unroll
     for (int g = 0; g < 4; ++g) {  // 8 elements per group
         uint32_t x[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            uint32_t code = 0;
-#pragma unroll
-            for (int i = K - 1; i >= 0; --i) code = code * p + byte_of(in, (8 * g + e) * K + i);
-            x[e] = tab[code];
-        }
+        for (int e = 0; e < 8; ++e) x[e] = tab[code[8 * g + e]];
         transpose8_nibbles(x);
 #pragma unroll
         for (int s = 0; s < KMAX_S; ++s) w[s][g] = x[s];
@@ -1215,6 +1285,212 @@ __global__ void __launch_bounds__(256) planes_b_kernel(const uint8_t* __restrict
         __syncthreads();  // this buffer is refilled two tiles later
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+// B [Kd, N, K] -> S transposed planes [S][N][ld], two passes per 256 kk x 32 j tile:
+//  1. a warp reads 4 B-row segments per instruction (a lane = 4 consecutive
+//     elements = K aligned 32-bit words straight from global memory), forms the
+//     4 element codes on 16-bit lanes (code = sum_i p^i b_i) and stores them
+//     (8 bytes) into a [kk][j] uint16 tile whose 4-column chunks are XOR-swizzled
+//     by kk/32, so that pass 2 reads it without bank conflicts;
+//  2. lane = (32-kk chunk, j): plane-table lookup of 8 codes per plane word,
+//     8x8 nibble transpose, S 16-byte stores -- every store instruction writes
+//     4 rows x 128 contiguous bytes of each plane (whole lines, no partial sectors).
+constexpr int P2_KK = 256, P2_J = 32;
+
+// pass 2 of the B-plane kernels: lane = (32-kk chunk, column) of the code tile
+template <int K>
+__device__ __forceinline__ void planes_b_pass2(const uint16_t (*codes)[P2_J], const uint32_t* tab, uint32_t lo,
+                                               uint32_t hi, int64_t j0, int64_t kk0, int64_t N, int64_t ld,
+                                               int64_t plane_stride, int S, uint8_t* __restrict__ out) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int kc = lane & 7, jl = 4 * warp + (lane >> 3);
+    const int64_t gj = j0 + jl;
+    const int64_t col = (kk0 + kc * 32) / 2;
+    const int cidx = 4 * ((jl >> 2) ^ kc) + (jl & 3);  // swizzled column in rows 32kc .. 32kc+31
+    if (gj < N && col + 16 <= ld) {
+        if constexpr (K == 1) {
+            uint32_t o[4];
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+                uint32_t c[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) c[e] = codes[kc * 32 + 8 * g + e][cidx];
+                const uint32_t v0 = __byte_perm(c[0] | (c[1] << 16), c[2] | (c[3] << 16), 0x6420);
+                const uint32_t v1 = __byte_perm(c[4] | (c[5] << 16), c[6] | (c[7] << 16), 0x6420);
+                o[g] = residues_to_e2m1(v0, lo, hi) | (residues_to_e2m1(v1, lo, hi) << 16);
+            }
+            *reinterpret_cast<uint4*>(out + gj * ld + col) = make_uint4(o[0], o[1], o[2], o[3]);
+        } else {
+            uint32_t w[KMAX_S][4];
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+                uint32_t x[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) x[e] = tab[codes[kc * 32 + 8 * g + e][cidx]];
+                transpose8_nibbles(x);
+#pragma unroll
+                for (int s = 0; s < KMAX_S; ++s) w[s][g] = x[s];
+            }
+            uint8_t* dst = out + gj * ld + col;
+#pragma unroll
+            for (int s = 0; s < KMAX_S; ++s)
+                if (s < S)
+                    *reinterpret_cast<uint4*>(dst + s * plane_stride) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
+        }
+    }
+}
+
+template <int K>
+__global__ void __launch_bounds__(256) planes_b2_kernel(const uint8_t* __restrict__ b, int64_t Kd, int64_t N,
+                                                        uint32_t p, const uint32_t* __restrict__ gtab, int S,
+                                                        uint8_t* __restrict__ out, int64_t ld, int64_t plane_stride,
+                                                        int tiles_kk, int tiles_j) {
+    __shared__ __align__(16) uint16_t codes[P2_KK][P2_J];
+    __shared__ uint32_t tab[PT_CODES];
+    int ncodes = 1;
+    for (int i = 0; i < K; ++i) ncodes *= (int)p;
+    for (int i = threadIdx.x; i < ncodes; i += blockDim.x) tab[i] = gtab[i];
+    const CodeCoef<K> cc = make_code_coef<K>(p);
+    const bool vec = ((N * K) % 4 == 0) && ((reinterpret_cast<uintptr_t>(b) & 3) == 0);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r4 = lane >> 3, c8 = lane & 7;  // pass 1: row of the warp's 4, 4-element chunk
+    uint32_t lo = 0, hi = 0;
+    if (K == 1) {
+        __syncthreads();
+        byte_lut_from_table(tab, p, lo, hi);
+    }
+    const int64_t ntiles = (int64_t)tiles_kk * tiles_j;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t kk0 = (t % tiles_kk) * P2_KK, j0 = (t / tiles_kk) * P2_J;
+        // ---- pass 1: codes ----
+        const int64_t jj = j0 + 4 * c8;
+        constexpr int ROUNDS = P2_KK / 32;  // 8 warps x 4 rows per round
+        uint32_t wv[ROUNDS][K];
+        if (vec && kk0 + P2_KK <= Kd && j0 + P2_J <= N) {  // whole tile in range: all loads in flight at once
+            const uint32_t* src = reinterpret_cast<const uint32_t*>(b + ((kk0 + 4 * warp + r4) * N + jj) * K);
+            const int64_t rstride = 8 * N * K;  // 32 rows, in 32-bit words
+#pragma unroll
+            for (int r = 0; r < ROUNDS; ++r)
+#pragma unroll
+                for (int i = 0; i < K; ++i) wv[r][i] = __ldg(src + r * rstride + i);
+        } else
+#pragma unroll
+        for (int r = 0; r < ROUNDS; ++r) {
+            const int64_t gk = kk0 + 32 * r + 4 * warp + r4;
+            const uint8_t* src = b + (gk * N + jj) * K;
+            if (vec && gk < Kd && jj + 4 <= N) {
+#pragma unroll
+                for (int i = 0; i < K; ++i) wv[r][i] = __ldg(reinterpret_cast<const uint32_t*>(src) + i);
+            } else {
+#pragma unroll
+                for (int i = 0; i < K; ++i) {
+                    uint32_t w = 0;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int e = (4 * i + q) / K;  // element within the 4
+                        if (gk < Kd && jj + e < N) w |= (uint32_t)src[4 * i + q] << (8 * q);
+                    }
+                    wv[r][i] = w;
+                }
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < ROUNDS; ++r) {
+            uint32_t cd[4];
+            elem_codes<K, K>(wv[r], cc, cd);
+            const int row = 32 * r + 4 * warp + r4;  // row >> 5 == r
+            *reinterpret_cast<uint2*>(&codes[row][4 * (c8 ^ (r & 7))]) =
+                make_uint2(__byte_perm(cd[0], cd[1], 0x5410), __byte_perm(cd[2], cd[3], 0x5410));
+        }
+        __syncthreads();
+        // ---- pass 2: planes ----
+        planes_b_pass2<K>(codes, tab, lo, hi, j0, kk0, N, ld, plane_stride, S, out);
+        __syncthreads();  // the code tile is rewritten by the next tile's pass 1
+    }
+}
+
+// TMA-fed variant of planes_b2_kernel: the 256 kk x (32 j * K bytes) input box
+// of the next tile streams into shared memory (cp.async.bulk.tensor, zero fill
+// outside B) while the current tile is converted, so the strided B rows are
+// fetched by the copy engine in whole sectors instead of 4-byte lane loads.
+template <int K>
+__global__ void __launch_bounds__(256) planes_b3_kernel(const __grid_constant__ CUtensorMap tmap, int64_t Kd,
+                                                        int64_t N, uint32_t p, const uint32_t* __restrict__ gtab,
+                                                        int S, uint8_t* __restrict__ out, int64_t ld,
+                                                        int64_t plane_stride, int tiles_kk, int tiles_j) {
+    using namespace sm100;
+    constexpr int ROWB = P2_J * K;  // bytes per box row
+    extern __shared__ __align__(128) uint8_t dsm3[];
+    uint8_t* inb = dsm3;                                                     // 2 x [P2_KK][ROWB]
+    uint16_t (*codes)[P2_J] = reinterpret_cast<uint16_t (*)[P2_J]>(dsm3 + 2 * P2_KK * ROWB);
+    uint32_t* tab = reinterpret_cast<uint32_t*>(dsm3 + 2 * P2_KK * ROWB + P2_KK * P2_J * 2);
+    __shared__ __align__(8) uint64_t bar[2];
+    int ncodes = 1;
+    for (int i = 0; i < K; ++i) ncodes *= (int)p;
+    for (int i = threadIdx.x; i < ncodes; i += blockDim.x) tab[i] = gtab[i];
+    const CodeCoef<K> cc = make_code_coef<K>(p);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int r4 = lane >> 3, c8 = lane & 7;
+    const int64_t ntiles = (int64_t)tiles_kk * tiles_j;
+    if (threadIdx.x == 0) {
+        tma_prefetch(&tmap);
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    uint32_t lo = 0, hi = 0;
+    if (K == 1) byte_lut_from_table(tab, p, lo, hi);
+    auto issue = [&](int64_t t, int buf) {
+        const int64_t kk0 = (t % tiles_kk) * P2_KK, j0 = (t / tiles_kk) * P2_J;
+        mbar_arrive_expect_tx(&bar[buf], P2_KK * ROWB);
+        tma_load_2d(inb + buf * P2_KK * ROWB, &tmap, &bar[buf], (int32_t)(j0 * K), (int32_t)kk0);
+    };
+    if (threadIdx.x == 0 && (int64_t)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int buf = it & 1;
+        // the other buffer was last read in the previous iteration's pass 1 (fenced by its barrier)
+        if (threadIdx.x == 0 && t + gridDim.x < ntiles) issue(t + gridDim.x, buf ^ 1);
+        mbar_wait(&bar[buf], (uint32_t)((it >> 1) & 1));
+        const int64_t kk0 = (t % tiles_kk) * P2_KK, j0 = (t / tiles_kk) * P2_J;
+        const uint8_t* tb = inb + buf * P2_KK * ROWB;
+#pragma unroll
+        for (int r = 0; r < P2_KK / 32; ++r) {
+            const int row = 32 * r + 4 * warp + r4;
+            uint32_t w[K];
+#pragma unroll
+            for (int i = 0; i < K; ++i) w[i] = reinterpret_cast<const uint32_t*>(tb + row * ROWB + 4 * K * c8)[i];
+            uint32_t cd[4];
+            elem_codes<K, K>(w, cc, cd);
+            *reinterpret_cast<uint2*>(&codes[row][4 * (c8 ^ (r & 7))]) =
+                make_uint2(__byte_perm(cd[0], cd[1], 0x5410), __byte_perm(cd[2], cd[3], 0x5410));
+        }
+        __syncthreads();
+        planes_b_pass2<K>(codes, tab, lo, hi, j0, kk0, N, ld, plane_stride, S, out);
+        __syncthreads();  // code tile rewritten next iteration
+    }
+}
+
+template <int K>
+constexpr size_t planes_b3_smem() {
+    return (size_t)2 * P2_KK * P2_J * K + (size_t)P2_KK * P2_J * 2 + PT_CODES * sizeof(uint32_t) + 128;
+}
+
+static int make_tmap_rows(CUtensorMap* map, const void* base, int64_t inner_bytes, int64_t rows, int64_t ld,
+                          uint32_t box_inner, uint32_t box_rows) {
+    EncodeTiledFn fn = encode_fn();
+    QADIC_REQUIRE(fn != nullptr, QADIC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {(cuuint64_t)inner_bytes, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld};
+    cuuint32_t box[2] = {box_inner, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    QADIC_REQUIRE(r == CUDA_SUCCESS, QADIC_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return QADIC_OK;
 }
 
 // D planes [S][M][ldd] (nibbles, N columns) -> C [M][N][K] uint8 residues.
@@ -1408,8 +1684,8 @@ static KaraLayout kara_plan(int S, int64_t m, int64_t kdim, int64_t n, int k) {
     return L;
 }
 
-// A side stream per device: the B-plane conversion (shared-memory bound) runs
-// concurrently with the A-plane conversion (HBM bound); joined before the GEMM.
+// A side stream per device (QADIC_CONCURRENT_PLANES=1): the B-plane conversion
+// runs concurrently with the A-plane conversion; joined before the GEMM.
 struct SideStream {
     cudaStream_t st = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
@@ -1430,7 +1706,9 @@ static SideStream& side_stream() {
 template <int K>
 static void launch_planes(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n, uint32_t p,
                           const uint32_t* tab, const KaraLayout& L, uint8_t* as, uint8_t* bs, cudaStream_t s) {
-    const bool concurrent = b != nullptr && !getenv_flag("QADIC_SERIAL_PLANES");
+    // measured: with the two-pass B kernel the overlap no longer pays (cfg3/4 run
+    // faster serialised), so it is opt-in
+    const bool concurrent = b != nullptr && getenv_flag("QADIC_CONCURRENT_PLANES");
     if (b != nullptr) {  // (b == nullptr: B planes already in the workspace)
         const int tk = (int)((kdim + PB_KK - 1) / PB_KK), tj = (int)((n + PB_J - 1) / PB_J);
         const int64_t tiles = (int64_t)tk * tj;
@@ -1448,9 +1726,41 @@ static void launch_planes(const uint8_t* a, const uint8_t* b, int64_t m, int64_t
             cudaStreamWaitEvent(ss.st, ss.fork, 0);
             sb = ss.st;
         }
-        QADIC_TIMED("fp4k planes B", sb,
-                    planes_b_kernel<K><<<grid, 256, planes_b_smem<K>(), sb>>>(b, kdim, n, p, tab, L.S, bs, L.ldk,
-                                                                               n * L.ldk, tk, tj));
+        CUtensorMap tm;
+        const bool use_tma = ((n * K) % 16 == 0) && ((reinterpret_cast<uintptr_t>(b) & 15) == 0) &&
+                             !getenv_flag("QADIC_PLANES_B2") &&
+                             make_tmap_rows(&tm, b, n * K, kdim, n * K, P2_J * K, P2_KK) == QADIC_OK;
+        if (getenv_flag("QADIC_PLANES_B1")) {
+            QADIC_TIMED("fp4k planes B", sb,
+                        planes_b_kernel<K><<<grid, 256, planes_b_smem<K>(), sb>>>(b, kdim, n, p, tab, L.S, bs, L.ldk,
+                                                                                   n * L.ldk, tk, tj));
+        } else if (use_tma) {
+            const int tk2 = (int)((kdim + P2_KK - 1) / P2_KK), tj2 = (int)((n + P2_J - 1) / P2_J);
+            const int64_t tiles2 = (int64_t)tk2 * tj2;
+            static int occ = 0;
+            if (!occ) {
+                cudaFuncSetAttribute(planes_b3_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)planes_b3_smem<K>());
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, planes_b3_kernel<K>, 256, planes_b3_smem<K>());
+                if (occ < 1) occ = 1;
+            }
+            const int grid3 = (int)(tiles2 < (int64_t)occ * num_sms() ? tiles2 : (int64_t)occ * num_sms());
+            QADIC_TIMED("fp4k planes B", sb,
+                        planes_b3_kernel<K><<<grid3, 256, planes_b3_smem<K>(), sb>>>(tm, kdim, n, p, tab, L.S, bs,
+                                                                                    L.ldk, n * L.ldk, tk2, tj2));
+        } else {
+            const int tk2 = (int)((kdim + P2_KK - 1) / P2_KK), tj2 = (int)((n + P2_J - 1) / P2_J);
+            const int64_t tiles2 = (int64_t)tk2 * tj2;
+            static int occ = 0;  // resident blocks per SM: the grid is exactly one wave
+            if (!occ) {
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, planes_b2_kernel<K>, 256, 0);
+                if (occ < 1) occ = 1;
+            }
+            const int grid2 = (int)(tiles2 < (int64_t)occ * num_sms() ? tiles2 : (int64_t)occ * num_sms());
+            QADIC_TIMED("fp4k planes B", sb,
+                        planes_b2_kernel<K><<<grid2, 256, 0, sb>>>(b, kdim, n, p, tab, L.S, bs, L.ldk, n * L.ldk, tk2,
+                                                                    tj2));
+        }
         if (concurrent) cudaEventRecord(side_stream().join, sb);
     }
     const int64_t ta = m * (L.ldk / 16);
@@ -1529,6 +1839,7 @@ static int run_kara(const FieldConst& f, const uint8_t* a, const uint8_t* b, int
     prm.magic64 = wide_magic(f.p);
     prm.m_tiles = (int)((m + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM));
     prm.n_tiles = (int)((n + BN - 1) / BN);
+    prm.n_full = (int)(n / BN);
     prm.num_kb = (int)(((kdim + 1) / 2 + BK - 1) / BK);
     prm.planes = L.S;
     // Fused combine (opt-in, QADIC_FUSE_COMBINE=1): the epilogue accumulates
