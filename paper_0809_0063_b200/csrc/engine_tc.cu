@@ -1009,24 +1009,30 @@ static bool plan_planes(const FieldConst& f, PlaneSpec* ps) {
 }
 
 // T[code] = E2M1 nibble of plane s of the element with this code, at bit 4s
-__global__ void plane_table_kernel(uint32_t p, int k, int S, PlaneSpec ps, uint32_t lut, uint32_t* __restrict__ tab) {
+
+// The plane table built inside the B-plane kernels (each block into its own
+// shared memory; block 0 also publishes it for the A-plane kernel that follows
+// on the stream) -- saves the separate table launch.
+__device__ __forceinline__ void build_plane_table(uint32_t* tab, uint32_t p, int k, int S, const PlaneSpec& ps,
+                                                  uint32_t lut, uint32_t* __restrict__ gout) {
     int ncodes = 1;
     for (int i = 0; i < k; ++i) ncodes *= (int)p;
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= ncodes) return;
-    uint32_t dig[kMaxK] = {};
-    int r = c;
-    for (int i = 0; i < k; ++i) {
-        dig[i] = (uint32_t)(r % (int)p);
-        r /= (int)p;
+    for (int c = threadIdx.x; c < ncodes; c += blockDim.x) {
+        int r = c;
+        uint32_t dig[kMaxK] = {};
+        for (int i = 0; i < k; ++i) {
+            dig[i] = (uint32_t)(r % (int)p);
+            r /= (int)p;
+        }
+        uint32_t w = 0;
+        for (int s = 0; s < S; ++s) {
+            uint32_t v = 0;
+            for (int i = 0; i < k; ++i) v += ps.E[s][i] * dig[i];
+            w |= ((lut >> (4 * (v % p))) & 0xF) << (4 * s);
+        }
+        tab[c] = w;
+        if (blockIdx.x == 0) gout[c] = w;
     }
-    uint32_t w = 0;
-    for (int s = 0; s < S; ++s) {
-        uint32_t v = 0;
-        for (int i = 0; i < k; ++i) v += ps.E[s][i] * dig[i];
-        w |= ((lut >> (4 * (v % p))) & 0xF) << (4 * s);
-    }
-    tab[c] = w;
 }
 
 // 4 byte lanes (values < 16) -> 16-bit field of 4 nibbles
@@ -1180,122 +1186,16 @@ __global__ void __launch_bounds__(256) planes_kernel(const uint8_t* __restrict__
         if (s < S) *reinterpret_cast<uint4*>(dst + s * plane_stride) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
 }
 
-// B [Kd, N, K] -> S transposed planes [S][N][ld]: 64 kk x 128 j tiles of B are
-// staged in shared memory by cp.async into two buffers (the next tile streams
-// in while this one is converted); each thread then owns one j and 32 kk and
-// builds its plane words like planes_kernel.
-constexpr int PB_KK = 64, PB_J = 128;
-template <int K>
-constexpr size_t planes_b_smem() {
-    return (size_t)2 * PB_KK * (PB_J * K + 16) + PT_CODES * sizeof(uint32_t);
-}
-
-__device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
-                 "l"(gmem), "r"(valid ? 16 : 0));
-}
-
-template <int K>
-__global__ void __launch_bounds__(256) planes_b_kernel(const uint8_t* __restrict__ b, int64_t Kd, int64_t N, uint32_t p,
-                                                       const uint32_t* __restrict__ gtab, int S,
-                                                       uint8_t* __restrict__ out, int64_t ld, int64_t plane_stride,
-                                                       int tiles_kk, int tiles_j) {
-    constexpr int ROWB = PB_J * K;
-    constexpr int PITCH = ROWB + 16;
-    extern __shared__ __align__(16) uint8_t dsm[];
-    uint8_t* tiles = dsm;                                                   // 2 x [PB_KK][PITCH]
-    uint32_t* tab = reinterpret_cast<uint32_t*>(dsm + 2 * PB_KK * PITCH);  // plane table
-    int ncodes = 1;
-    for (int i = 0; i < K; ++i) ncodes *= (int)p;
-    for (int i = threadIdx.x; i < ncodes; i += blockDim.x) tab[i] = gtab[i];
-    const bool vec_in = ((N * K) % 16 == 0) && ((reinterpret_cast<uintptr_t>(b) & 15) == 0);
-    const int64_t ntiles = (int64_t)tiles_kk * tiles_j;
-    const int jl = threadIdx.x % PB_J, ch = threadIdx.x / PB_J;  // 2 chunks of 32 kk
-
-    auto stage = [&](int64_t t, int buf) {
-        uint8_t* tb = tiles + buf * PB_KK * PITCH;
-        const int64_t kk0 = (t % tiles_kk) * PB_KK, j0 = (t / tiles_kk) * PB_J;
-        if (vec_in && j0 + PB_J <= N) {
-            for (int i = threadIdx.x; i < PB_KK * (ROWB / 16); i += blockDim.x) {
-                const int rr = i / (ROWB / 16), qq = i % (ROWB / 16);
-                const int64_t gk = kk0 + rr;
-                const uint8_t* src = b + (gk < Kd ? gk : 0) * N * K + j0 * K + qq * 16;
-                cp_async16_zfill(tb + rr * PITCH + qq * 16, src, gk < Kd);
-            }
-        } else {
-            for (int i = threadIdx.x; i < PB_KK * ROWB; i += blockDim.x) {
-                const int rr = i / ROWB, cc = i % ROWB;
-                const int64_t gk = kk0 + rr, gj = j0 + cc / K;
-                tb[rr * PITCH + cc] = (gk < Kd && gj < N) ? b[gk * N * K + j0 * K + cc] : 0;
-            }
-        }
-        asm volatile("cp.async.commit_group;");
-    };
-
-    if ((int64_t)blockIdx.x < ntiles) stage(blockIdx.x, 0);
-    int it = 0;
-    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-        const int64_t nxt = t + gridDim.x;
-        if (nxt < ntiles) stage(nxt, (it + 1) & 1);
-        else asm volatile("cp.async.commit_group;");
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-        __syncthreads();
-        const int64_t kk0 = (t % tiles_kk) * PB_KK, j0 = (t / tiles_kk) * PB_J;
-        const int64_t gj = j0 + jl;
-        const int64_t col = (kk0 + ch * 32) / 2;
-        if (gj < N && col + 16 <= ld) {
-            const uint8_t* tcol = tiles + (it & 1) * PB_KK * PITCH + (ch * 32) * PITCH + jl * K;
-            if constexpr (K == 1) {  // one plane: gather 4 kk per word, PRMT lookup
-                uint32_t lo, hi;
-                byte_lut_from_table(tab, p, lo, hi);
-                uint32_t o[4];
-#pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    uint32_t v0 = 0, v1 = 0;
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        v0 |= (uint32_t)tcol[(8 * g + e) * PITCH] << (8 * e);
-                        v1 |= (uint32_t)tcol[(8 * g + 4 + e) * PITCH] << (8 * e);
-                    }
-                    o[g] = residues_to_e2m1(v0, lo, hi) | (residues_to_e2m1(v1, lo, hi) << 16);
-                }
-                *reinterpret_cast<uint4*>(out + gj * ld + col) = make_uint4(o[0], o[1], o[2], o[3]);
-            } else {
-                uint32_t w[KMAX_S][4];
-#pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    uint32_t x[8];
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        uint32_t code = 0;
-#pragma unroll
-                        for (int i = K - 1; i >= 0; --i) code = code * p + tcol[(8 * g + e) * PITCH + i];
-                        x[e] = tab[code];
-                    }
-                    transpose8_nibbles(x);
-#pragma unroll
-                    for (int s = 0; s < KMAX_S; ++s) w[s][g] = x[s];
-                }
-                uint8_t* dst = out + gj * ld + col;
-#pragma unroll
-                for (int s = 0; s < KMAX_S; ++s)
-                    if (s < S) *reinterpret_cast<uint4*>(dst + s * plane_stride) = make_uint4(w[s][0], w[s][1], w[s][2], w[s][3]);
-            }
-        }
-        __syncthreads();  // this buffer is refilled two tiles later
-    }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-}
-
 // B [Kd, N, K] -> S transposed planes [S][N][ld], two passes per 256 kk x 32 j tile:
 //  1. a warp reads 4 B-row segments per instruction (a lane = 4 consecutive
-//     elements = K aligned 32-bit words straight from global memory), forms the
-//     4 element codes on 16-bit lanes (code = sum_i p^i b_i) and stores them
-//     (8 bytes) into a [kk][j] uint16 tile whose 4-column chunks are XOR-swizzled
-//     by kk/32, so that pass 2 reads it without bank conflicts;
+//     elements = K aligned 32-bit words), forms the 4 element codes (sum_i p^i b_i,
+//     byte dot products) and stores them (8 bytes) into a [kk][j] uint16 tile
+//     whose 4-column chunks are XOR-swizzled by kk/32, so that pass 2 reads it
+//     without bank conflicts;
 //  2. lane = (32-kk chunk, j): plane-table lookup of 8 codes per plane word,
 //     8x8 nibble transpose, S 16-byte stores -- every store instruction writes
 //     4 rows x 128 contiguous bytes of each plane (whole lines, no partial sectors).
+// planes_b3_kernel feeds pass 1 by TMA; planes_b2_kernel (unaligned B) by lane loads.
 constexpr int P2_KK = 256, P2_J = 32;
 
 // pass 2 of the B-plane kernels: lane = (32-kk chunk, column) of the code tile
@@ -1343,14 +1243,12 @@ __device__ __forceinline__ void planes_b_pass2(const uint16_t (*codes)[P2_J], co
 
 template <int K>
 __global__ void __launch_bounds__(256) planes_b2_kernel(const uint8_t* __restrict__ b, int64_t Kd, int64_t N,
-                                                        uint32_t p, const uint32_t* __restrict__ gtab, int S,
+                                                        uint32_t p, uint32_t* __restrict__ gtab, PlaneSpec ps, uint32_t lut, int S,
                                                         uint8_t* __restrict__ out, int64_t ld, int64_t plane_stride,
                                                         int tiles_kk, int tiles_j) {
     __shared__ __align__(16) uint16_t codes[P2_KK][P2_J];
     __shared__ uint32_t tab[PT_CODES];
-    int ncodes = 1;
-    for (int i = 0; i < K; ++i) ncodes *= (int)p;
-    for (int i = threadIdx.x; i < ncodes; i += blockDim.x) tab[i] = gtab[i];
+    build_plane_table(tab, p, K, S, ps, lut, gtab);
     const CodeCoef<K> cc = make_code_coef<K>(p);
     const bool vec = ((N * K) % 4 == 0) && ((reinterpret_cast<uintptr_t>(b) & 3) == 0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1416,7 +1314,7 @@ __global__ void __launch_bounds__(256) planes_b2_kernel(const uint8_t* __restric
 // fetched by the copy engine in whole sectors instead of 4-byte lane loads.
 template <int K>
 __global__ void __launch_bounds__(256) planes_b3_kernel(const __grid_constant__ CUtensorMap tmap, int64_t Kd,
-                                                        int64_t N, uint32_t p, const uint32_t* __restrict__ gtab,
+                                                        int64_t N, uint32_t p, uint32_t* __restrict__ gtab, PlaneSpec ps, uint32_t lut,
                                                         int S, uint8_t* __restrict__ out, int64_t ld,
                                                         int64_t plane_stride, int tiles_kk, int tiles_j) {
     using namespace sm100;
@@ -1426,9 +1324,7 @@ __global__ void __launch_bounds__(256) planes_b3_kernel(const __grid_constant__ 
     uint16_t (*codes)[P2_J] = reinterpret_cast<uint16_t (*)[P2_J]>(dsm3 + 2 * P2_KK * ROWB);
     uint32_t* tab = reinterpret_cast<uint32_t*>(dsm3 + 2 * P2_KK * ROWB + P2_KK * P2_J * 2);
     __shared__ __align__(8) uint64_t bar[2];
-    int ncodes = 1;
-    for (int i = 0; i < K; ++i) ncodes *= (int)p;
-    for (int i = threadIdx.x; i < ncodes; i += blockDim.x) tab[i] = gtab[i];
+    build_plane_table(tab, p, K, S, ps, lut, gtab);
     const CodeCoef<K> cc = make_code_coef<K>(p);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int r4 = lane >> 3, c8 = lane & 7;
@@ -1684,59 +1580,20 @@ static KaraLayout kara_plan(int S, int64_t m, int64_t kdim, int64_t n, int k) {
     return L;
 }
 
-// A side stream per device (QADIC_CONCURRENT_PLANES=1): the B-plane conversion
-// runs concurrently with the A-plane conversion; joined before the GEMM.
-struct SideStream {
-    cudaStream_t st = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
-};
-static SideStream& side_stream() {
-    static SideStream ss[64];
-    int dev = 0;
-    cudaGetDevice(&dev);
-    SideStream& x = ss[dev & 63];
-    if (!x.st) {
-        cudaStreamCreateWithFlags(&x.st, cudaStreamNonBlocking);
-        cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming);
-    }
-    return x;
-}
-
+// B planes (which also build the plane table: smem per block, global for the
+// A kernel) then A planes, in stream order.  b == nullptr: the B planes and the
+// table are already in the workspace (later row panels of a host call).
 template <int K>
 static void launch_planes(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n, uint32_t p,
-                          const uint32_t* tab, const KaraLayout& L, uint8_t* as, uint8_t* bs, cudaStream_t s) {
-    // measured: with the two-pass B kernel the overlap no longer pays (cfg3/4 run
-    // faster serialised), so it is opt-in
-    const bool concurrent = b != nullptr && getenv_flag("QADIC_CONCURRENT_PLANES");
-    if (b != nullptr) {  // (b == nullptr: B planes already in the workspace)
-        const int tk = (int)((kdim + PB_KK - 1) / PB_KK), tj = (int)((n + PB_J - 1) / PB_J);
+                          uint32_t* tab, const PlaneSpec& ps, uint32_t lut, const KaraLayout& L, uint8_t* as,
+                          uint8_t* bs, cudaStream_t s) {
+    if (b != nullptr) {
+        const int tk = (int)((kdim + P2_KK - 1) / P2_KK), tj = (int)((n + P2_J - 1) / P2_J);
         const int64_t tiles = (int64_t)tk * tj;
-        const int grid = (int)(tiles < 8 * num_sms() ? tiles : 8 * num_sms());
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(planes_b_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)planes_b_smem<K>());
-            attr = true;
-        }
-        cudaStream_t sb = s;
-        if (concurrent) {
-            SideStream& ss = side_stream();
-            cudaEventRecord(ss.fork, s);
-            cudaStreamWaitEvent(ss.st, ss.fork, 0);
-            sb = ss.st;
-        }
         CUtensorMap tm;
         const bool use_tma = ((n * K) % 16 == 0) && ((reinterpret_cast<uintptr_t>(b) & 15) == 0) &&
-                             !getenv_flag("QADIC_PLANES_B2") &&
                              make_tmap_rows(&tm, b, n * K, kdim, n * K, P2_J * K, P2_KK) == QADIC_OK;
-        if (getenv_flag("QADIC_PLANES_B1")) {
-            QADIC_TIMED("fp4k planes B", sb,
-                        planes_b_kernel<K><<<grid, 256, planes_b_smem<K>(), sb>>>(b, kdim, n, p, tab, L.S, bs, L.ldk,
-                                                                                   n * L.ldk, tk, tj));
-        } else if (use_tma) {
-            const int tk2 = (int)((kdim + P2_KK - 1) / P2_KK), tj2 = (int)((n + P2_J - 1) / P2_J);
-            const int64_t tiles2 = (int64_t)tk2 * tj2;
+        if (use_tma) {  // TMA-fed; the grid is exactly one wave of resident blocks
             static int occ = 0;
             if (!occ) {
                 cudaFuncSetAttribute(planes_b3_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1744,30 +1601,26 @@ static void launch_planes(const uint8_t* a, const uint8_t* b, int64_t m, int64_t
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, planes_b3_kernel<K>, 256, planes_b3_smem<K>());
                 if (occ < 1) occ = 1;
             }
-            const int grid3 = (int)(tiles2 < (int64_t)occ * num_sms() ? tiles2 : (int64_t)occ * num_sms());
-            QADIC_TIMED("fp4k planes B", sb,
-                        planes_b3_kernel<K><<<grid3, 256, planes_b3_smem<K>(), sb>>>(tm, kdim, n, p, tab, L.S, bs,
-                                                                                    L.ldk, n * L.ldk, tk2, tj2));
-        } else {
-            const int tk2 = (int)((kdim + P2_KK - 1) / P2_KK), tj2 = (int)((n + P2_J - 1) / P2_J);
-            const int64_t tiles2 = (int64_t)tk2 * tj2;
-            static int occ = 0;  // resident blocks per SM: the grid is exactly one wave
+            const int grid = (int)(tiles < (int64_t)occ * num_sms() ? tiles : (int64_t)occ * num_sms());
+            QADIC_TIMED("fp4k planes B", s,
+                        planes_b3_kernel<K><<<grid, 256, planes_b3_smem<K>(), s>>>(tm, kdim, n, p, tab, ps, lut, L.S,
+                                                                                  bs, L.ldk, n * L.ldk, tk, tj));
+        } else {  // unaligned B: lane loads
+            static int occ = 0;
             if (!occ) {
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, planes_b2_kernel<K>, 256, 0);
                 if (occ < 1) occ = 1;
             }
-            const int grid2 = (int)(tiles2 < (int64_t)occ * num_sms() ? tiles2 : (int64_t)occ * num_sms());
-            QADIC_TIMED("fp4k planes B", sb,
-                        planes_b2_kernel<K><<<grid2, 256, 0, sb>>>(b, kdim, n, p, tab, L.S, bs, L.ldk, n * L.ldk, tk2,
-                                                                    tj2));
+            const int grid = (int)(tiles < (int64_t)occ * num_sms() ? tiles : (int64_t)occ * num_sms());
+            QADIC_TIMED("fp4k planes B", s,
+                        planes_b2_kernel<K><<<grid, 256, 0, s>>>(b, kdim, n, p, tab, ps, lut, L.S, bs, L.ldk,
+                                                                  n * L.ldk, tk, tj));
         }
-        if (concurrent) cudaEventRecord(side_stream().join, sb);
     }
     const int64_t ta = m * (L.ldk / 16);
     QADIC_TIMED("fp4k planes A", s,
                 planes_kernel<K><<<(unsigned)((ta + 255) / 256), 256, 0, s>>>(a, m, kdim, p, tab, L.S, as, L.ldk,
                                                                                 m * L.ldk));
-    if (concurrent) cudaStreamWaitEvent(s, side_stream().join, 0);
 }
 
 template <int K>
@@ -1811,15 +1664,13 @@ static int run_kara(const FieldConst& f, const uint8_t* a, const uint8_t* b, int
     int ncodes = 1;
     for (int i = 0; i < k; ++i) ncodes *= (int)f.p;
     QADIC_REQUIRE(ncodes <= PT_CODES, QADIC_ERR_UNSUPPORTED, "plane table needs p^k <= %d", PT_CODES);
-    if (!b_ready)
-        QADIC_TIMED("fp4k plane table", s,
-                    plane_table_kernel<<<(ncodes + 255) / 256, 256, 0, s>>>(f.p, k, ps.S, ps, centred_e2m1_lut(f.p), tab));
     const uint8_t* bsrc = b_ready ? nullptr : b;
+    const uint32_t lut = centred_e2m1_lut(f.p);
     switch (k) {
-        case 1: launch_planes<1>(a, bsrc, m, kdim, n, f.p, tab, L, as, bs, s); break;
-        case 2: launch_planes<2>(a, bsrc, m, kdim, n, f.p, tab, L, as, bs, s); break;
-        case 3: launch_planes<3>(a, bsrc, m, kdim, n, f.p, tab, L, as, bs, s); break;
-        default: launch_planes<4>(a, bsrc, m, kdim, n, f.p, tab, L, as, bs, s); break;
+        case 1: launch_planes<1>(a, bsrc, m, kdim, n, f.p, tab, ps, lut, L, as, bs, s); break;
+        case 2: launch_planes<2>(a, bsrc, m, kdim, n, f.p, tab, ps, lut, L, as, bs, s); break;
+        case 3: launch_planes<3>(a, bsrc, m, kdim, n, f.p, tab, ps, lut, L, as, bs, s); break;
+        default: launch_planes<4>(a, bsrc, m, kdim, n, f.p, tab, ps, lut, L, as, bs, s); break;
     }
     int rc = check_launch("fp4k planes");
     if (rc) return rc;
