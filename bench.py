@@ -297,15 +297,15 @@ def roofline(cfg, engine, kname, kstats, work, peaks, peak_src):
                 "cublas_int8_measured_tops": round(peaks["int8_tops"], 1) if peaks.get("int8_tops") else None,
                 "two_x_measured_bf16_tops": round(2 * peaks["bf16_tflops"], 1)}
     if kname in ("fp4 gemm", "fp4k gemm"):
-        # expanded form: M*(N k)*(K k) MACs; Karatsuba planes: k(k+1)/2 * M*N*K
+        # expanded form: M*(N k)*(K k) MACs; evaluation planes (Toom-Cook 2k-1 or
+        # Karatsuba k(k+1)/2 plane products): S * M*N*K MACs
         ops = 2 * (work["kara_macs"] if kname == "fp4k gemm" else work["i8_macs"])
         achieved = ops / avg_s / 1e12
         peak = 9000.0
         return {"bound": "tensor", "kernel": kname, "achieved": round(achieved, 1), "peak": peak,
                 "unit": "TOP/s", "frac": round(achieved / peak, 4), "traffic": None,
                 "avg_launch_ms": round(avg_s * 1e3, 4), "algorithmic_ops_per_launch": ops,
-                "peak_source": "fallback nominal dense fp4 9 PFLOP/s (B200_PROFILING.md); no measured fp4 peak",
-                "cublas_int8_measured_tops": round(peaks["int8_tops"], 1) if peaks.get("int8_tops") else None}
+                "peak_source": "fallback nominal dense fp4 9 PFLOP/s (B200_PROFILING.md); no measured fp4 peak"}
     if kname == "f64 dmma gemm":
         ops = 2 * work["f64_fmas"]
         achieved = ops / avg_s / 1e12
@@ -402,7 +402,7 @@ def run_ours(args):
     engine = args.engine
     step, e2e, units, io, meta = build_step(cfg, engine, rank, ws, torch, dist, Q, W)
     peaks, peak_src = load_peaks()
-    if cfg in (3, 4, 5) and engine != "f64":
+    if cfg in (3, 4, 5) and engine == "i8":  # context for the i8 roofline only
         peaks["int8_tops"] = measure_int8_peak(torch)
     stream = torch.cuda.current_stream()
 

@@ -28,7 +28,7 @@ full() {  # name config engine kernel-regex
   ncu -i $O/$1.ncu-rep --page details --csv > $O/$1_details.csv 2>/dev/null
 }
 full cfg5_fp4k_gemm 5 auto gemm_modp
-full cfg5_planes_b 5 auto planes_b
+full cfg5_planes_b 5 auto planes_b3
 full cfg5_planes_a 5 auto "planes_kernel"
 full cfg5_combine 5 auto combine
 full cfg3_fp4k_gemm 3 auto gemm_modp
