@@ -53,6 +53,8 @@ template <int T, bool CORR1>
 __global__ void __launch_bounds__(PM_THREADS, 4) polymul_k4_kernel(const uint8_t* __restrict__ a,
                                                                 const uint8_t* __restrict__ b, int64_t n,
                                                                 PolyConst c, uint8_t* __restrict__ out) {
+    pdl_wait();  // predecessor complete before any global access
+    pdl_trigger();
     const int64_t p0 = ((int64_t)blockIdx.x * PM_THREADS + threadIdx.x) * PM_PER;
     if (p0 >= n) return;
     uint32_t av[PM_PER], bv[PM_PER];
@@ -130,8 +132,8 @@ template <int T>
 static void launch_polymul_k4(const uint8_t* a, const uint8_t* b, int64_t n, const PolyConst& c, uint8_t* out,
                               cudaStream_t s) {
     const unsigned blocks = (unsigned)((n + (int64_t)PM_THREADS * PM_PER - 1) / ((int64_t)PM_THREADS * PM_PER));
-    if (c.corr == 1 || c.p == 2) polymul_k4_kernel<T, true><<<blocks, PM_THREADS, 0, s>>>(a, b, n, c, out);
-    else polymul_k4_kernel<T, false><<<blocks, PM_THREADS, 0, s>>>(a, b, n, c, out);
+    if (c.corr == 1 || c.p == 2) launch_pdl(polymul_k4_kernel<T, true>, dim3(blocks), dim3(PM_THREADS), 0, s, a, b, n, c, out);
+    else launch_pdl(polymul_k4_kernel<T, false>, dim3(blocks), dim3(PM_THREADS), 0, s, a, b, n, c, out);
 }
 
 // ---- generic k (1..8): one pair per thread ---------------------------------------
@@ -171,6 +173,8 @@ __global__ void __launch_bounds__(GD_THREADS) gf_dot_kernel(const uint8_t* __res
                                                             const uint8_t* __restrict__ v2, int64_t batch,
                                                             int64_t len, FieldConst f,
                                                             uint8_t* __restrict__ out) {
+    pdl_wait();  // predecessor complete before any global access
+    pdl_trigger();
     const int lane = threadIdx.x % G;
     const int64_t dot = ((int64_t)blockIdx.x * GD_THREADS + threadIdx.x) / G;
     const bool live = dot < batch;
@@ -254,11 +258,11 @@ static void launch_gf_dot(const uint8_t* v1, const uint8_t* v2, int64_t batch, i
     if (vec) {
         constexpr int G = 4;  // 4 lanes per dot: a warp reads 64 contiguous bytes per dot per load
         const unsigned blocks = (unsigned)((batch * G + GD_THREADS - 1) / GD_THREADS);
-        gf_dot_kernel<K, G, (16 % K == 0)><<<blocks, GD_THREADS, 0, s>>>(v1, v2, batch, len, f, out);
+        launch_pdl(gf_dot_kernel<K, G, (16 % K == 0)>, dim3(blocks), dim3(GD_THREADS), 0, s, v1, v2, batch, len, f, out);
     } else {
         constexpr int G = 8;
         const unsigned blocks = (unsigned)((batch * G + GD_THREADS - 1) / GD_THREADS);
-        gf_dot_kernel<K, G, false><<<blocks, GD_THREADS, 0, s>>>(v1, v2, batch, len, f, out);
+        launch_pdl(gf_dot_kernel<K, G, false>, dim3(blocks), dim3(GD_THREADS), 0, s, v1, v2, batch, len, f, out);
     }
 }
 

@@ -2,6 +2,7 @@
 // and the exact host constants of the FP64 reciprocal division.
 #include <math.h>
 #include <stdarg.h>
+#include <stdlib.h>
 #include <stdio.h>
 
 #include <atomic>
@@ -61,6 +62,11 @@ void set_error(int code, const char* fmt, ...) {
     int n = snprintf(g_err, sizeof g_err, "[qadic status %d] ", code);
     vsnprintf(g_err + n, sizeof g_err - n, fmt, ap);
     va_end(ap);
+}
+
+bool pdl_enabled() {
+    static const bool on = !(getenv("QADIC_NO_PDL") && atoi(getenv("QADIC_NO_PDL")) != 0);
+    return on;
 }
 
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }

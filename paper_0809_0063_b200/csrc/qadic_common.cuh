@@ -22,6 +22,17 @@
 
 namespace qadic {
 
+// Programmatic dependent launch (the batched cfg1/cfg2 kernels: back-to-back
+// single-wave launches): kernels launched with launch_pdl() may start while their
+// stream predecessor drains; pdl_wait() (first thing, before any global memory
+// access) blocks until the predecessor grid has completed and its writes are
+// visible, pdl_trigger() lets this grid's successor begin launching.  Both are
+// no-ops for an ordinary launch.  Not used for the tensor-core chain: there an
+// early-resident GEMM CTA (227 KB smem) starves the preceding plane kernel's
+// tail of SMs (measured 2% slower at cfg5).
+QADIC_D void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+QADIC_D void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 constexpr int kMaxK = 4;             // extension degree supported by the GF kernels
 constexpr int kMaxDigits = 2 * kMaxK - 1;
 

@@ -21,6 +21,26 @@ void count_launch(int n = 1);
 int prof_begin(cudaStream_t s, const char* name);
 void prof_end(int idx, cudaStream_t s);
 
+// PDL launches are on unless QADIC_NO_PDL=1
+bool pdl_enabled();
+
+// Launch with programmatic stream serialisation (see pdl_wait in qadic_common.cuh).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 }  // namespace qadic
 
 // launch a kernel bracketed by the (optional) per-kernel event timer
