@@ -45,7 +45,8 @@ enum Kind { KIND_I8 = 0, KIND_F4 = 1 };
 
 constexpr int BM = 128, BK = 128;  // BK in bytes per stage (128 int8 / 256 fp4 elements)
 constexpr int STAGES = 4;
-constexpr int THREADS = 256;
+constexpr int THREADS = 256;        // warps: 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle, 4-7 epilogue
+constexpr int THREADS_FUSED = 384;  // fused combine: 8 epilogue warps (4-11)
 constexpr int GROUP_M = 16;
 #ifndef QADIC_MAX_STAGES
 #define QADIC_MAX_STAGES 8
@@ -69,8 +70,8 @@ struct Cfg<KIND_F4> {
 // the BN B rows, so the per-SM operand traffic (TMA writes + MMA reads of
 // shared memory) drops by a third at the same MMA rate.
 // FUSE_K > 0: the epilogue applies the plane combination C_l = sum_s W[l][s] D_s
-// itself, accumulating the S plane results of one output tile in shared memory
-// (one padded row of BN*FUSE_K bytes per epilogue thread).
+// itself, accumulating the S plane results of one output tile in registers
+// (8 epilogue warps, byte lanes).
 template <int KIND, bool PAIR, int FUSE_K = 0>
 struct Geo {
     static constexpr int BN = Cfg<KIND>::BN;
@@ -78,8 +79,7 @@ struct Geo {
     static constexpr int A_BYTES = BM * BK;
     static constexpr int B_BYTES = B_ROWS * BK;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int ACC_PITCH = FUSE_K ? BN * FUSE_K + 4 : 0;  // odd word count: conflict-free rows
-    static constexpr int ACC_BYTES = BM * ACC_PITCH;
+    static constexpr int ACC_BYTES = 0;
     // as many stages as 227 KB of shared memory holds (deeper prefetch hides
     // the L2 misses at tile boundaries of short-K plane products)
     static constexpr int FIT = (232448 - 1280 - ACC_BYTES) / STAGE_BYTES;
@@ -87,6 +87,22 @@ struct Geo {
     static constexpr size_t SMEM = (size_t)STAGES_N * STAGE_BYTES + ACC_BYTES + 1024 + 256;
     static constexpr int TILE_M = PAIR ? 2 * BM : BM;
 };
+
+// SWAR variant (S*(p-1)^2 < 256): every byte lane of the weighted plane sum
+// stays below 256, so the sum, the reduction mod p and the interleave into
+// coefficient-minor order all run on 4 lanes per instruction:
+//   x mod p = x - p * floor(x / p),  floor(x / p) = (x * lm) >> ls per 16-bit lane
+//   (host-checked exact for every lane value that can occur), then PRMT places
+//   the K coefficient words of 4 columns into K output words.
+struct LaneDiv {
+    uint32_t m, sh, qmask;  // qmask: per 16-bit lane, bits that can hold the quotient
+};
+
+__device__ __forceinline__ uint32_t lanes_mod_div(uint32_t x, uint32_t p, LaneDiv d) {
+    const uint32_t e = x & 0x00FF00FFu, o = (x >> 8) & 0x00FF00FFu;
+    const uint32_t qe = ((e * d.m) >> d.sh) & d.qmask, qo = ((o * d.m) >> d.sh) & d.qmask;
+    return x - (qe | (qo << 8)) * p;
+}
 
 struct Params {
     int64_t M, N;        // output rows / cols of one plane (cols = n * k for the expanded form)
@@ -102,6 +118,8 @@ struct Params {
     uint8_t* c;
     uint8_t W[4][8];     // FUSE_K: combination weights (mod p), C_l = sum_s W[l][s] D_s
     uint32_t sf;         // 4 x UE8M0 block scale bytes (0x7F7F7F7F: every scale 2^0)
+    uint32_t lane_m, lane_sh, lane_qmask;  // FUSE_K: per-16-bit-lane division by p (LaneDiv)
+    int group_m;                           // FUSE_K: m tiles per raster group
     int diag_noload;     // diagnostics only (QADIC_DIAG_NOLOAD): stages after the first pass skip the TMA
 };
 
@@ -110,11 +128,12 @@ struct Params {
 template <int FUSE_K>
 __device__ __forceinline__ void decode_tile(int tile, const Params& prm, int& pl, int& mt, int& nt);
 
-__device__ __forceinline__ void tile_coords(int tile, int m_tiles, int n_tiles, int& mt, int& nt) {
-    const int per_group = GROUP_M * n_tiles;
+__device__ __forceinline__ void tile_coords(int tile, int m_tiles, int n_tiles, int& mt, int& nt,
+                                            int group_m = GROUP_M) {
+    const int per_group = group_m * n_tiles;
     const int group = tile / per_group;
-    const int first_m = group * GROUP_M;
-    const int gm = min(m_tiles - first_m, GROUP_M);
+    const int first_m = group * group_m;
+    const int gm = min(m_tiles - first_m, group_m);
     const int r = tile % per_group;
     mt = first_m + r % gm;
     nt = r / gm;
@@ -133,7 +152,7 @@ template <int FUSE_K>
 __device__ __forceinline__ void decode_tile(int tile, const Params& prm, int& pl, int& mt, int& nt) {
     if (FUSE_K) {
         pl = tile % prm.planes;
-        tile_coords(tile / prm.planes, prm.m_tiles, prm.n_tiles, mt, nt);
+        tile_coords(tile / prm.planes, prm.m_tiles, prm.n_tiles, mt, nt, prm.group_m);
     } else {
         // full-width tiles first (plane-major, grouped raster), then the narrow
         // tail tiles of every plane: the round-robin assignment then hands the
@@ -190,7 +209,7 @@ __device__ __forceinline__ void tmem_fill_sf(uint32_t taddr, uint32_t v) {
 }
 
 template <int KIND, bool PAIR, int FUSE_K = 0>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
     gemm_modp_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
                      const __grid_constant__ Params prm) {
     using namespace sm100;
@@ -226,7 +245,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tmem_full[a], 1);
-            mbar_init(&tmem_empty[a], PAIR ? 8 : 4);  // one arrival per epilogue warp (of both CTAs)
+            // one arrival per epilogue warp (of both CTAs)
+            mbar_init(&tmem_empty[a], (FUSE_K ? 8 : 4) * (PAIR ? 2 : 1));
         }
         fence_barrier_init();
     }
@@ -239,7 +259,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    if (KIND == KIND_F4 && warp >= 4) {
+    if (KIND == KIND_F4 && warp >= 4 && warp < 8) {
         tmem_fill_sf(tmem_base + ((uint32_t)((warp - 4) * 32) << 16) + Cfg<KIND>::SF_COL, prm.sf);
         tc_fence_before();
     }
@@ -329,11 +349,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
     } else if (warp >= 4) {
         // ===== epilogue: TMEM -> registers -> mod p -> uint8 =====
-        const int ew = warp - 4;  // TMEM lane quarter this warp may access
+        const int ew = warp - 4;   // TMEM lane quarter this warp may access (unfused: 4 warps)
+        const int ew4 = warp & 3;  // fused (8 warps): warps 4+q and 8+q share lane quarter q
         const uint32_t empty_addr0 = PAIR ? map_to_rank(&tmem_empty[0], 0) : 0;
         const uint32_t empty_addr1 = PAIR ? map_to_rank(&tmem_empty[1], 0) : 0;
         int local = 0;
-        uint8_t* accrow = smem + NST * G::STAGE_BYTES + 256 + (ew * 32 + lane) * G::ACC_PITCH;
+        // fused: this thread's byte-lane plane sums, 16 columns x FUSE_K bytes per chunk
+        uint32_t facc[FUSE_K ? (BN / 16 + 1) / 2 : 1][FUSE_K ? 4 * FUSE_K : 1];
+        (void)facc;
         for (int u = group_id; u < units; u += num_groups)
         for (int sp = 0; sp < per_unit; ++sp, ++local) {
             const int tile = u * per_unit + sp;
@@ -343,36 +366,45 @@ __global__ void __launch_bounds__(THREADS, 1)
             const uint32_t acc_phase = (local >> 1) & 1;
             mbar_wait(&tmem_full[acc], acc_phase);
             tc_fence_after();
-            const int64_t row = (int64_t)mt * G::TILE_M + (int)rank * BM + ew * 32 + lane;
+            const int64_t row = (int64_t)mt * G::TILE_M + (int)rank * BM + (FUSE_K ? ew4 : ew) * 32 + lane;
             const bool row_ok = row < prm.M;
             if constexpr (FUSE_K > 0) {
-                // plane pl of this tile: acc_row[(col, l)] += W[l][pl] * D_pl[row, col]
-                // on byte lanes (S * (p-1)^2 < 256: no carries); the last plane
-                // reduces mod p and writes the k coefficient bytes of every column
-                uint32_t wl[FUSE_K];
+                // plane pl of this tile: acc[(col, l)] += W[l][pl] * (D_pl[row, col] mod p)
+                // on byte lanes held in registers (S * (p-1)^2 < 256: no carries).
+                // 8 epilogue warps: lane quarter q = warp & 3, 16-column chunks of
+                // parity h; the last plane reduces mod p and writes the coefficients.
+                constexpr int NCH = BN / 16, MYCH = (NCH + 1) / 2, W4 = 4 * FUSE_K;
+                const int h = (warp - 4) >> 2;
+                uint32_t mult[FUSE_K][4];  // W[l][pl] placed in byte lane j
 #pragma unroll
-                for (int l = 0; l < FUSE_K; ++l) wl[l] = prm.W[l][pl];
-#pragma unroll 1
-                for (int ch = 0; ch < BN / 16; ++ch) {
-                    uint32_t v[16];
-                    tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + ch * 16, v);
-                    tmem_ld_wait();
-                    uint32_t add[4 * FUSE_K];
+                for (int l = 0; l < FUSE_K; ++l)
 #pragma unroll
-                    for (int q = 0; q < 4 * FUSE_K; ++q) add[q] = 0;
+                    for (int j = 0; j < 4; ++j) mult[l][j] = (uint32_t)prm.W[l][pl] << (8 * j);
+                if (sp == 0) {
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) {
-                        const uint32_t x = (uint32_t)(__float2int_rn(__uint_as_float(v[c])) + (int)prm.offset);
-                        const uint32_t r = mod_u32(x, prm.p, prm.magic64);
+                    for (int i = 0; i < MYCH; ++i)
 #pragma unroll
-                        for (int l = 0; l < FUSE_K; ++l) {
-                            const int pos = c * FUSE_K + l;
-                            add[pos >> 2] |= (wl[l] * r) << (8 * (pos & 3));
+                        for (int q = 0; q < W4; ++q) facc[i][q] = 0;
+                }
+                const int nch = tile_n<BN>(prm, nt) / 16;
+#pragma unroll
+                for (int i = 0; i < MYCH; ++i) {
+                    const int ch = 2 * i + h;
+                    if (ch < NCH && ch < nch) {
+                        uint32_t v[16];
+                        tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(ew4 * 32) << 16) + acc * BN + ch * 16, v);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int c = 0; c < 16; ++c) {
+                            const uint32_t x = (uint32_t)(__float2int_rn(__uint_as_float(v[c])) + (int)prm.offset);
+                            const uint32_t r = mod_u32(x, prm.p, prm.magic64);
+#pragma unroll
+                            for (int l = 0; l < FUSE_K; ++l) {
+                                const int pos = c * FUSE_K + l;
+                                facc[i][pos >> 2] += r * mult[l][pos & 3];
+                            }
                         }
                     }
-                    uint32_t* a32 = reinterpret_cast<uint32_t*>(accrow + ch * 16 * FUSE_K);
-#pragma unroll
-                    for (int q = 0; q < 4 * FUSE_K; ++q) a32[q] = (pl == 0) ? add[q] : a32[q] + add[q];
                 }
                 // TMEM fully read: hand the accumulator back to the MMA warp first
                 tc_fence_before();
@@ -382,28 +414,25 @@ __global__ void __launch_bounds__(THREADS, 1)
                     else mbar_arrive(&tmem_empty[acc]);
                 }
                 if (pl == prm.planes - 1 && row_ok) {
-                    const int64_t col0 = (int64_t)nt * BN;
-                    const int64_t nbytes = (prm.N - col0 < BN ? prm.N - col0 : BN) * FUSE_K;
-                    uint8_t* dst = prm.c + row * prm.ldc + col0 * FUSE_K;
-                    const uint32_t magic = (uint32_t)(0xFFFFFFFFu / prm.p) + 1u;
-#pragma unroll 1
-                    for (int q = 0; q < BN * FUSE_K / 16; ++q) {
-                        if (q * 16 >= nbytes) break;
-                        const uint32_t* src = reinterpret_cast<const uint32_t*>(accrow + q * 16);
-                        uint32_t o[4];
+                    const LaneDiv ldv = {prm.lane_m, prm.lane_sh, prm.lane_qmask};
 #pragma unroll
-                        for (int wq = 0; wq < 4; ++wq) {
-                            const uint32_t xw = src[wq];
-                            o[wq] = mod_small(xw & 0xFF, prm.p, magic) | (mod_small((xw >> 8) & 0xFF, prm.p, magic) << 8) |
-                                    (mod_small((xw >> 16) & 0xFF, prm.p, magic) << 16) |
-                                    (mod_small(xw >> 24, prm.p, magic) << 24);
-                        }
-                        if (q * 16 + 16 <= nbytes && ((reinterpret_cast<uintptr_t>(dst + q * 16) & 15) == 0)) {
-                            *reinterpret_cast<uint4*>(dst + q * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+                    for (int i = 0; i < MYCH; ++i) {
+                        const int ch = 2 * i + h;
+                        const int64_t col0 = (int64_t)nt * BN + ch * 16;
+                        if (ch >= NCH || col0 >= prm.N) continue;
+                        uint32_t o[W4];
+#pragma unroll
+                        for (int q = 0; q < W4; ++q) o[q] = lanes_mod_div(facc[i][q], prm.p, ldv);
+                        uint8_t* dst = prm.c + row * prm.ldc + col0 * FUSE_K;
+                        if (col0 + 16 <= prm.N && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+                            for (int q = 0; q < FUSE_K; ++q)
+                                reinterpret_cast<uint4*>(dst)[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
                         } else {
+                            const int64_t nb = (prm.N - col0 < 16 ? prm.N - col0 : 16) * FUSE_K;
 #pragma unroll
-                            for (int e = 0; e < 16; ++e)  // unrolled: o[] stays in registers
-                                if (q * 16 + e < nbytes) dst[q * 16 + e] = (uint8_t)(o[e >> 2] >> (8 * (e & 3)));
+                            for (int e = 0; e < W4 * 4; ++e)  // unrolled: o[] stays in registers
+                                if (e < nb) dst[e] = (uint8_t)(o[e >> 2] >> (8 * (e & 3)));
                         }
                     }
                 }
@@ -782,7 +811,7 @@ static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, Params prm,
     grid *= per;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(THREADS);
+    cfg.blockDim = dim3(FUSE_K ? THREADS_FUSED : THREADS);
     cfg.dynamicSmemBytes = G::SMEM;
     cfg.stream = s;
     cudaLaunchAttribute attrs[1];
@@ -1460,22 +1489,6 @@ __global__ void __launch_bounds__(256) combine_kernel(const uint8_t* __restrict_
     }
 }
 
-// SWAR variant (S*(p-1)^2 < 256): every byte lane of the weighted plane sum
-// stays below 256, so the sum, the reduction mod p and the interleave into
-// coefficient-minor order all run on 4 lanes per instruction:
-//   x mod p = x - p * floor(x / p),  floor(x / p) = (x * lm) >> ls per 16-bit lane
-//   (host-checked exact for every lane value that can occur), then PRMT places
-//   the K coefficient words of 4 columns into K output words.
-struct LaneDiv {
-    uint32_t m, sh, qmask;  // qmask: per 16-bit lane, bits that can hold the quotient
-};
-
-__device__ __forceinline__ uint32_t lanes_mod_div(uint32_t x, uint32_t p, LaneDiv d) {
-    const uint32_t e = x & 0x00FF00FFu, o = (x >> 8) & 0x00FF00FFu;
-    const uint32_t qe = ((e * d.m) >> d.sh) & d.qmask, qo = ((o * d.m) >> d.sh) & d.qmask;
-    return x - (qe | (qo << 8)) * p;
-}
-
 // T[l] lanes = columns c0..c3 of coefficient l -> out[w] = bytes 4w..4w+3 of the
 // coefficient-minor stream (column-major over l)
 template <int K>
@@ -1702,23 +1715,32 @@ static int run_kara(const FieldConst& f, const uint8_t* a, const uint8_t* b, int
     prm.n_full = (int)(n / BN);
     prm.num_kb = (int)(((kdim + 1) / 2 + BK - 1) / BK);
     prm.planes = L.S;
-    // Fused combine (opt-in, QADIC_FUSE_COMBINE=1): the epilogue accumulates
-    // W[l][s] * D_s per tile in shared memory on byte lanes (needs S*(p-1)^2 <
-    // 256 and the CTA-pair kernel).  Measured slower than the separate combine
-    // pass at cfg5 (epilogue-bound: 1.05 vs 0.82 + 0.12 ms), so off by default.
-    const bool fuse = pair && k >= 2 && (int64_t)L.S * (f.p - 1) * (f.p - 1) < 256 && getenv_flag("QADIC_FUSE_COMBINE");
+    // Fused combine: the GEMM epilogue accumulates W[l][s] * (D_s mod p) per output
+    // tile in registers on byte lanes (needs S*(p-1)^2 < 256, k in {2, 3} and the
+    // CTA-pair kernel) and writes C directly -- no D planes, no combine pass.  Its
+    // tiles run plane-inner, so the L2 must hold S planes of operands: measured a
+    // win at S = 3 (cfg3: 0.570 vs 0.586 ms) and a loss at S = 5 (cfg5: 1.047 vs
+    // 1.012 ms; DRAM reads 1.6 vs 0.6 GB, tensor pipe 88 vs 94% active), hence the
+    // default S <= 3; QADIC_FUSE_COMBINE=0/1 forces it off/on.
+    const char* fuse_env = getenv("QADIC_FUSE_COMBINE");
+    const bool want_fuse = fuse_env ? atoi(fuse_env) != 0 : L.S <= 3;
+    LaneDiv ldv = {};
+    const bool fuse = pair && (k == 2 || k == 3) && (int64_t)L.S * (f.p - 1) * (f.p - 1) < 256 &&
+                      lane_div_plan(f.p, (uint32_t)L.S * (f.p - 1) * (f.p - 1), &ldv) && want_fuse;
     if (fuse) {
+        prm.lane_m = ldv.m;
+        prm.lane_sh = ldv.sh;
+        prm.lane_qmask = ldv.qmask;
+        prm.group_m = getenv("QADIC_FUSE_GROUP") ? atoi(getenv("QADIC_FUSE_GROUP")) : 8;
+        if (prm.group_m < 1) prm.group_m = 1;
         for (int l = 0; l < k; ++l)
             for (int sidx = 0; sidx < KMAX_S; ++sidx) prm.W[l][sidx] = sidx < L.S ? ps.W[l][sidx] : 0;
         prm.c = c;
         prm.ldc = n * k;
         prm.c_plane = 0;
         prm.nibble_out = 0;
-        switch (k) {
-            case 2: return launch_gemm<KIND_F4, true, 2>(ta, tb, prm, s, "fp4k gemm");
-            case 3: return launch_gemm<KIND_F4, true, 3>(ta, tb, prm, s, "fp4k gemm");
-            default: return launch_gemm<KIND_F4, true, 4>(ta, tb, prm, s, "fp4k gemm");
-        }
+        return k == 2 ? launch_gemm<KIND_F4, true, 2>(ta, tb, prm, s, "fp4k gemm")
+                      : launch_gemm<KIND_F4, true, 3>(ta, tb, prm, s, "fp4k gemm");
     }
     if (k == 1) {  // one plane: the GEMM writes C directly
         prm.c = c;

@@ -234,6 +234,21 @@ class TestGFMatmul:
         for e in ENGINES:
             assert np.array_equal(f.matmul_coeffs(a, b, engine=e), ref)
 
+    @pytest.mark.parametrize("fuse", ["0", "1"])
+    @pytest.mark.parametrize("cfg,m,kd,n", [(3, 300, 520, 250), (3, 513, 96, 481), (5, 257, 300, 500),
+                                            (5, 64, 1000, 16)])
+    def test_fp4k_fused_and_separate_combine(self, monkeypatch, fuse, cfg, m, kd, n):
+        """the GEMM-epilogue plane combination (QADIC_FUSE_COMBINE=1) and the
+        separate combine pass give the same bits (ragged tiles, narrow tails)."""
+        monkeypatch.setenv("QADIC_FUSE_COMBINE", fuse)
+        c = W.CONFIGS[cfg]
+        f = W.field_for(c)
+        of = O.build_field(c.p, c.k, irreducible=list(c.irreducible), max_dot_length=c.dot_bound)
+        g = W.rng(m + kd + n + cfg)
+        a = g.integers(0, c.p, (m, kd, c.k), dtype=np.uint8)
+        b = g.integers(0, c.p, (kd, n, c.k), dtype=np.uint8)
+        assert np.array_equal(f.matmul_coeffs(a, b, engine="fp4k"), O.gf_matmul_planes(of, a, b))
+
     @pytest.mark.parametrize("engine", ENGINES)
     @pytest.mark.parametrize("panel", [7, 100, 256, 0])
     def test_host_pipeline_panels(self, engine, panel):
