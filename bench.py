@@ -50,7 +50,7 @@ def dist_env():
 # clocks sampled during the timed region
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -65,7 +65,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+                 "-lms", "20"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
         time.sleep(0.25)
@@ -79,13 +79,15 @@ class ClockSampler:
             except subprocess.TimeoutExpired:
                 self.proc.kill()
 
-    def summary(self):
+    def summary(self, t_begin=None, t_end=None):
+        """Clocks over the samples taken inside [t_begin, t_end] (host wall time
+        of the timed region); all samples if none fall inside."""
         rows = []
         try:
             with open(self.path) as fh:
                 for line in fh:
                     parts = [x.strip() for x in line.split(",")]
-                    if len(parts) >= 9:
+                    if len(parts) >= 10:
                         rows.append(parts)
         except OSError:
             pass
@@ -101,14 +103,26 @@ class ClockSampler:
             except ValueError:
                 return None
 
-        sm = [num(r[1]) for r in rows if num(r[1]) is not None]
-        mx = [num(r[2]) for r in rows if num(r[2]) is not None]
-        busy = [s for s in sm if s and mx and s > 0.3 * max(mx)] or sm
+        def stamp(x):
+            import datetime
+            for fmt in ("%Y/%m/%d %H:%M:%S.%f", "%Y/%m/%d %H:%M:%S"):
+                try:
+                    return datetime.datetime.strptime(x, fmt).timestamp()
+                except ValueError:
+                    pass
+            return None
+
+        inside = rows
+        if t_begin is not None and t_end is not None:
+            sel = [r for r in rows if (stamp(r[0]) or 0.0) >= t_begin and (stamp(r[0]) or 0.0) <= t_end]
+            inside = sel or rows
+        sm = [num(r[2]) for r in inside if num(r[2]) is not None]
+        mx = [num(r[3]) for r in rows if num(r[3]) is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
-        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows),
-                "power_w_max": max((num(r[3]) or 0.0) for r in rows)}
+        reasons = sorted({names[i] for r in inside for i in range(4) if r[6 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(inside), "samples_in_timed_region": inside is not rows,
+                "power_w_max": max((num(r[4]) or 0.0) for r in inside)}
 
 
 # ---------------------------------------------------------------------------
@@ -430,6 +444,7 @@ def run_ours(args):
         barrier()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
+        wall0 = time.time()
         t0.record(stream)
         if graph is not None:
             graph.replay()
@@ -438,13 +453,14 @@ def run_ours(args):
                 step(i)
         t1.record(stream)
         barrier()
+        wall1 = time.time()
     launches = N.launch_count() - launches0
     ms = t0.elapsed_time(t1) / args.steps
     if ws > 1:
         tt = torch.tensor([ms], device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
-    clocks = clk.summary()
+    clocks = clk.summary(wall0, wall1)
     # ---- second pass: per-kernel CUDA-event durations (same K steps) ----
     lib = N.lib()
     lib.qadic_profile_enable(1)
@@ -520,6 +536,9 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+REF_BUDGET_S = 90.0  # wall budget of the whole reference-arm run
+
+
 def run_reference(args):
     """The reference's own CPU implementation on this box's host cores."""
     ws, rank, _ = dist_env()
@@ -536,12 +555,23 @@ def run_reference(args):
     rows = {1: 1 << 17, 2: 1 << 13, 3: 2, 4: 2, 5: 1}[cfg]
     full = W.make_inputs(c) if cfg not in (3, 5) else _matmul_sample_inputs(c, max(64, rows * workers))
     pool = cpu_ref.make_pool(cfg, full, workers) if workers > 1 else None
+    cols = None
     try:
-        for _ in range(args.warmup if args.warmup < 2 else 1):
-            cpu_ref.time_reference(cfg, full, rows, workers, pool=pool)
+        # one probe step sizes the sample so the whole --steps K --warmup W run takes
+        # about REF_BUDGET_S seconds (fewer batch entries, or fewer B columns)
+        _, t_probe, _ = cpu_ref.time_reference(cfg, full, rows, workers, pool=pool)
+        scale = min(1.0, REF_BUDGET_S / max(1e-9, t_probe * (args.steps + args.warmup)))
+        if scale < 1.0:
+            if cfg in (1, 2):
+                rows = max(256, int(rows * scale))
+            else:
+                n = c.shape[-1] if cfg != 4 else c.shape[0]
+                cols = max(64, int(n * scale) // 64 * 64)
+        for _ in range(args.warmup):
+            cpu_ref.time_reference(cfg, full, rows, workers, pool=pool, cols=cols)
         tot_u, tot_s, kind = 0, 0.0, "port"
         for _ in range(args.steps):
-            u, s, kind = cpu_ref.time_reference(cfg, full, rows, workers, pool=pool)
+            u, s, kind = cpu_ref.time_reference(cfg, full, rows, workers, pool=pool, cols=cols)
             tot_u += u
             tot_s += s
     finally:
@@ -549,7 +579,8 @@ def run_reference(args):
             pool.shutdown()
     value = tot_u / tot_s
     unit = "pairs/s" if cfg == 1 else ("F_p mult-adds/s" if cfg == 4 else "GF mult-adds/s")
-    sample = f"{workers} processes x {rows} rows/entries of cfg{cfg} per step"
+    sample = f"{workers} processes x {rows} rows/entries of cfg{cfg} per step" + \
+        (f" against the first {cols} columns of B" if cols else "")
     line = {"impl": "reference",
             "metric": "GF(p^k) mult-adds/s (packed matmul) and REDQ coeffs/s vs roofline, 1-8 GPU",
             "value": value, "unit": unit, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
@@ -566,7 +597,9 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: enough for >= ~0.2 s of timed region, so the "
+                         "nvidia-smi clock samples fall inside it)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="5")
     ap.add_argument("--engine", default="auto", choices=["auto", "i8", "f64", "fp4", "fp4k"])
@@ -576,8 +609,11 @@ def main():
     args = ap.parse_args()
     args.warmup = max(3, args.warmup) if args.impl == "ours" else args.warmup
     cfgs = [1, 2, 3, 4, 5] if args.config == "all" else [int(args.config)]
+    steps_given = args.steps
     for cfg in cfgs:
         args.config = cfg
+        if steps_given is None:  # ~0.2 s of timed region per config
+            args.steps = {1: 2000, 2: 2000, 3: 300, 4: 150, 5: 200}[cfg]
         if args.impl == "reference":
             run_reference(args)
         else:

@@ -107,16 +107,17 @@ def run_block(cfg: int, inputs: dict, K: Kernels) -> np.ndarray:
     raise KeyError(cfg)
 
 
-def sample_inputs(cfg: int, full: dict, rows: int, start: int = 0) -> dict:
+def sample_inputs(cfg: int, full: dict, rows: int, start: int = 0, cols=None) -> dict:
     """A bounded sample of the full workload: leading batch entries (cfg1/2)
-    or `rows` rows of A against the full B (cfg3/4/5)."""
+    or `rows` rows of A against the full B -- or its first `cols` columns
+    (cfg3/4/5)."""
     if cfg == 1:
         return {"a": full["a"][start:start + rows], "b": full["b"][start:start + rows]}
     if cfg == 2:
         return {"v1": full["v1"][start:start + rows], "v2": full["v2"][start:start + rows]}
     if cfg == 4:
-        return {"a": full["a"][start:start + rows], "b": full["a"]}
-    return {"a": full["a"][start:start + rows], "b": full["b"]}
+        return {"a": full["a"][start:start + rows], "b": full["a"][:, :cols] if cols else full["a"]}
+    return {"a": full["a"][start:start + rows], "b": full["b"][:, :cols] if cols else full["b"]}
 
 
 def units_of(cfg: int, sample: dict) -> int:
@@ -141,31 +142,32 @@ def _worker_init(cfg, full, prefer_reference):
 
 
 def _worker_run(args):
-    rows, start = args
+    rows, start, cols = args
     cfg, full, K = _POOL_STATE["cfg"], _POOL_STATE["full"], _POOL_STATE["K"]
     t0 = time.perf_counter()
-    run_block(cfg, sample_inputs(cfg, full, rows, start), K)
+    run_block(cfg, sample_inputs(cfg, full, rows, start, cols), K)
     return time.perf_counter() - t0
 
 
 def time_reference(cfg: int, full: dict, rows_per_worker: int, workers: int = 1,
-                   prefer_reference: bool = True, pool=None):
+                   prefer_reference: bool = True, pool=None, cols=None):
     """Run `workers` disjoint blocks of `rows_per_worker` rows in parallel
     processes (1 = in-process, single core) and return
     (units processed, wall seconds, kind)."""
     kind = Kernels(prefer_reference).kind
     if workers <= 1:
         K = Kernels(prefer_reference)
-        s = sample_inputs(cfg, full, rows_per_worker, 0)
+        s = sample_inputs(cfg, full, rows_per_worker, 0, cols)
         t0 = time.perf_counter()
         run_block(cfg, s, K)
         return units_of(cfg, s), time.perf_counter() - t0, kind
     n_rows = next(iter(full.values())).shape[0]
-    jobs = [(rows_per_worker, (i * rows_per_worker) % max(1, n_rows - rows_per_worker + 1)) for i in range(workers)]
+    jobs = [(rows_per_worker, (i * rows_per_worker) % max(1, n_rows - rows_per_worker + 1), cols)
+            for i in range(workers)]
     t0 = time.perf_counter()
     list(pool.map(_worker_run, jobs))
     wall = time.perf_counter() - t0
-    units = workers * units_of(cfg, sample_inputs(cfg, full, rows_per_worker, 0))
+    units = workers * units_of(cfg, sample_inputs(cfg, full, rows_per_worker, 0, cols))
     return units, wall, kind
 
 
