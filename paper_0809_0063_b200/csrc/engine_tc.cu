@@ -750,25 +750,53 @@ static bool pair_mode() {
 }
 
 // E2M1 nibble codes of the centred residues 0..p-1 (p <= 7), packed 4 bits each
-// E2M1 codes of the centred residues.  Default: the halves 0, 0.5, 1, 1.5
-// (codes 0..3) under block scales 2^1 on both operands, so every product is
-// (x/2)(y/2) * 4 = x*y exactly.  QADIC_E2M1_INT=1: the integers 0..3 themselves
-// (codes 0, 2, 4, 5) under unit scales.  Same exact sums; the half codes toggle
-// fewer operand bits and the power-capped GEMM clocks higher (cfg5: 0.787 vs
-// 0.819 ms per fp4k GEMM).
+// E2M1 codes of the residue representatives (4-bit code of residue r at nibble r).
+// Every operand value is a half-integer code under block scales 2^1 on both
+// operands, so each product is (x/2)(y/2) * 4 = x*y exactly; the representable
+// integers are +-{0, 1, 2, 3, 4, 6, 8, 12}.  Preferred: the smallest NON-NEGATIVE
+// representative of each residue (p = 7: 0, 1, 2, 3, 4, 12, 6) -- no sign bits,
+// fewer operand bit toggles, and the power-capped GEMM clocks higher (cfg5 GEMM
+// 0.749 vs 0.782 ms centred; cfg3 0.446 vs 0.474) -- while K * max_v^2 stays below
+// 2^24 (exact fp32 sums); else the centred residues (|v| <= 3).
+// QADIC_E2M1_CENTRED=1 forces centred, QADIC_E2M1_INT=1 the integer codes with
+// unit scales (both for measurements).
 static bool e2m1_half() {
     static const bool on = !(getenv("QADIC_E2M1_INT") && atoi(getenv("QADIC_E2M1_INT")) != 0);
     return on;
 }
 static uint32_t e2m1_scale_word() { return e2m1_half() ? 0x80808080u : 0x7F7F7F7Fu; }
-static uint32_t centred_e2m1_lut(uint32_t p) {
+static int nonneg_rep(uint32_t r, uint32_t p) {  // smallest representable v >= 0 with v = r mod p, or -1
+    static const int vals[8] = {0, 1, 2, 3, 4, 6, 8, 12};
+    for (int v : vals)
+        if ((uint32_t)v % p == r) return v;
+    return -1;
+}
+static uint32_t e2m1_lut(uint32_t p, int64_t kdim) {
+    static const bool force_centred = getenv("QADIC_E2M1_CENTRED") && atoi(getenv("QADIC_E2M1_CENTRED")) != 0;
+    int maxv = 0;
+    bool nonneg = e2m1_half() && !force_centred;
+    for (uint32_t r = 0; r < p && nonneg; ++r) {
+        const int v = nonneg_rep(r, p);
+        if (v < 0) nonneg = false;
+        else if (v > maxv) maxv = v;
+    }
+    if (nonneg && (__int128)kdim * maxv * maxv >= ((__int128)1 << 24)) nonneg = false;
     static const uint32_t pos_int[4] = {0x0, 0x2, 0x4, 0x5};   // 0, 1, 2, 3
     static const uint32_t pos_half[4] = {0x0, 0x1, 0x2, 0x3};  // 0, 0.5, 1, 1.5
-    const uint32_t* pos = e2m1_half() ? pos_half : pos_int;
     uint32_t lut = 0;
     for (uint32_t r = 0; r < p; ++r) {
-        const int v = (2 * r <= p - 1) ? (int)r : (int)r - (int)p;
-        const uint32_t code = v >= 0 ? pos[v] : (0x8u | pos[-v]);
+        uint32_t code;
+        if (nonneg) {
+            static const int vals[8] = {0, 1, 2, 3, 4, 6, 8, 12};
+            const int v = nonneg_rep(r, p);
+            code = 0;
+            for (uint32_t c = 0; c < 8; ++c)
+                if (vals[c] == v) code = c;  // half codes 0..7 = 0, 0.5, 1, 1.5, 2, 3, 4, 6
+        } else {
+            const uint32_t* pos = e2m1_half() ? pos_half : pos_int;
+            const int v = (2 * r <= p - 1) ? (int)r : (int)r - (int)p;
+            code = v >= 0 ? pos[v] : (0x8u | pos[-v]);
+        }
         lut |= code << (4 * r);
     }
     return lut;
@@ -854,7 +882,7 @@ static int run(int kind, const FieldConst& f, const uint8_t* a, const uint8_t* b
     Layout L = plan(kind, a, m, kdim, n, k);
     QADIC_REQUIRE(ws != nullptr && ws_bytes >= L.bx_bytes + L.a_bytes, QADIC_ERR_VALUE,
                   "workspace too small (%zu < %zu)", ws_bytes, L.bx_bytes + L.a_bytes);
-    const uint32_t lut = kind == KIND_F4 ? centred_e2m1_lut(f.p) : 0;
+    const uint32_t lut = kind == KIND_F4 ? e2m1_lut(f.p, kdim * k) : 0;
     uint8_t* bx = static_cast<uint8_t*>(ws);
     const uint8_t* a_op = a;
     if (L.prep_a) {
@@ -1686,7 +1714,7 @@ static int run_kara(const FieldConst& f, const uint8_t* a, const uint8_t* b, int
     for (int i = 0; i < k; ++i) ncodes *= (int)f.p;
     QADIC_REQUIRE(ncodes <= PT_CODES, QADIC_ERR_UNSUPPORTED, "plane table needs p^k <= %d", PT_CODES);
     const uint8_t* bsrc = b_ready ? nullptr : b;
-    const uint32_t lut = centred_e2m1_lut(f.p);
+    const uint32_t lut = e2m1_lut(f.p, kdim);
     switch (k) {
         case 1: launch_planes<1>(a, bsrc, m, kdim, n, f.p, tab, ps, lut, L, as, bs, s); break;
         case 2: launch_planes<2>(a, bsrc, m, kdim, n, f.p, tab, ps, lut, L, as, bs, s); break;
