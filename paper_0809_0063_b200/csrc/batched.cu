@@ -171,10 +171,23 @@ constexpr int GD_THREADS = 256;
 template <int K, int G, bool VEC>
 __global__ void __launch_bounds__(GD_THREADS) gf_dot_kernel(const uint8_t* __restrict__ v1,
                                                             const uint8_t* __restrict__ v2, int64_t batch,
-                                                            int64_t len, FieldConst f,
+                                                            int64_t len, FieldConst f, int tab_smem,
                                                             uint8_t* __restrict__ out) {
     pdl_wait();  // predecessor complete before any global access
     pdl_trigger();
+    // the L/H correction tables (gfext.py:176-213) staged in shared memory when small
+    extern __shared__ uint32_t gd_tab[];
+    const uint32_t* ltab = f.l_table;
+    const uint32_t* htab = f.h_table;
+    if (tab_smem > 0) {
+        for (int i = threadIdx.x; i < tab_smem; i += GD_THREADS) {
+            gd_tab[i] = __ldg(f.l_table + i);
+            gd_tab[tab_smem + i] = __ldg(f.h_table + i);
+        }
+        __syncthreads();
+        ltab = gd_tab;
+        htab = gd_tab + tab_smem;
+    }
     const int lane = threadIdx.x % G;
     const int64_t dot = ((int64_t)blockIdx.x * GD_THREADS + threadIdx.x) / G;
     const bool live = dot < batch;
@@ -239,7 +252,7 @@ __global__ void __launch_bounds__(GD_THREADS) gf_dot_kernel(const uint8_t* __res
         li |= u[i] << (f.bb * i);
         hi |= u[K - 1 + i] << (f.bb * i);
     }
-    const uint32_t res = add_coeff_bytes(__ldg(f.l_table + li), __ldg(f.h_table + hi), f.p, K);
+    const uint32_t res = add_coeff_bytes(ltab[li], htab[hi], f.p, K);
     if (K == 2 && (reinterpret_cast<uintptr_t>(out) & 1) == 0) {
         reinterpret_cast<uint16_t*>(out)[dot] = (uint16_t)res;
     } else if (K == 4 && (reinterpret_cast<uintptr_t>(out) & 3) == 0) {
@@ -255,14 +268,19 @@ static void launch_gf_dot(const uint8_t* v1, const uint8_t* v2, int64_t batch, i
                           uint8_t* out, cudaStream_t s) {
     const bool vec = (16 % K == 0) && ((len * K) % 16 == 0) && ((uintptr_t)v1 % 16 == 0) &&
                      ((uintptr_t)v2 % 16 == 0) && K * f.t <= 32;
+    const int entries = 1 << (f.bb * K);
+    const int ntab = entries <= 2048 ? entries : 0;  // <= 16 KB of tables: shared memory
+    const size_t smem = (size_t)ntab * 2 * sizeof(uint32_t);
     if (vec) {
         constexpr int G = 4;  // 4 lanes per dot: a warp reads 64 contiguous bytes per dot per load
         const unsigned blocks = (unsigned)((batch * G + GD_THREADS - 1) / GD_THREADS);
-        launch_pdl(gf_dot_kernel<K, G, (16 % K == 0)>, dim3(blocks), dim3(GD_THREADS), 0, s, v1, v2, batch, len, f, out);
+        launch_pdl(gf_dot_kernel<K, G, (16 % K == 0)>, dim3(blocks), dim3(GD_THREADS), smem, s, v1, v2, batch, len,
+                   f, ntab, out);
     } else {
         constexpr int G = 8;
         const unsigned blocks = (unsigned)((batch * G + GD_THREADS - 1) / GD_THREADS);
-        launch_pdl(gf_dot_kernel<K, G, false>, dim3(blocks), dim3(GD_THREADS), 0, s, v1, v2, batch, len, f, out);
+        launch_pdl(gf_dot_kernel<K, G, false>, dim3(blocks), dim3(GD_THREADS), smem, s, v1, v2, batch, len, f, ntab,
+                   out);
     }
 }
 
