@@ -555,7 +555,7 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-REF_BUDGET_S = 90.0  # wall budget of the whole reference-arm run
+REF_BUDGET_S = float(os.environ.get("QADIC_REF_BUDGET_S", "90"))  # wall budget of the whole reference-arm run
 
 
 def run_reference(args):

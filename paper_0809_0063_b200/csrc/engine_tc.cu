@@ -161,7 +161,7 @@ __device__ __forceinline__ void decode_tile(int tile, const Params& prm, int& pl
         const int F = full_tiles * prm.planes;
         if (tile < F) {
             pl = tile / full_tiles;
-            tile_coords(tile % full_tiles, prm.m_tiles, prm.n_full, mt, nt);
+            tile_coords(tile % full_tiles, prm.m_tiles, prm.n_full, mt, nt, prm.group_m);
         } else {
             const int i = tile - F;
             pl = i / prm.m_tiles;
@@ -922,6 +922,8 @@ static int run(int kind, const FieldConst& f, const uint8_t* a, const uint8_t* b
     if (rc) return rc;
     Params prm = {};
     prm.sf = e2m1_scale_word();
+    prm.group_m = getenv("QADIC_GROUP_M") ? atoi(getenv("QADIC_GROUP_M")) : GROUP_M;
+    if (prm.group_m < 1) prm.group_m = 1;
     prm.diag_noload = getenv_flag("QADIC_DIAG_NOLOAD");
     prm.M = m;
     prm.N = n * k;
@@ -1732,6 +1734,8 @@ static int run_kara(const FieldConst& f, const uint8_t* a, const uint8_t* b, int
     if (rc) return rc;
     Params prm = {};
     prm.sf = e2m1_scale_word();
+    prm.group_m = getenv("QADIC_GROUP_M") ? atoi(getenv("QADIC_GROUP_M")) : GROUP_M;
+    if (prm.group_m < 1) prm.group_m = 1;
     prm.diag_noload = getenv_flag("QADIC_DIAG_NOLOAD");
     prm.M = m;
     prm.N = n;

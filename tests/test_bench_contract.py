@@ -1,0 +1,63 @@
+"""bench.py's JSON-line contract: the reference arm on CPU (here), our arm
+on the GPU (-m gpu)."""
+
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+             "scaling", "vs_baseline", "dtype", "data", "config", "e2e", "gpu_launches"}
+
+
+def _run(args, env=None, timeout=600):
+    e = dict(os.environ, **(env or {}))
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py")] + args, cwd=ROOT, env=e,
+                         capture_output=True, text=True, timeout=timeout)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    return json.loads(lines[0])
+
+
+def test_reference_arm_line():
+    d = _run(["--impl", "reference", "--config", "1", "--steps", "3", "--warmup", "1"],
+             env={"QADIC_REF_BUDGET_S": "4"})
+    assert BASE_KEYS <= set(d)
+    assert d["impl"] == "reference" and d["gpu_launches"] == 0 and d["steps"] == 3
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    assert d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["kind"] in ("reference", "port")
+    assert d["value"] > 0 and d["unit"] == "pairs/s"
+
+
+def test_clock_summary_uses_timed_region(tmp_path):
+    sys.path.insert(0, ROOT)
+    import bench
+
+    cs = bench.ClockSampler(0)
+    cs.path = str(tmp_path / "c.csv")
+    rows = ["2026/10/20 01:00:00.000, 0, 1965, 1965, 100.0, 0x0, Not Active, Not Active, Not Active, Not Active",
+            "2026/10/20 01:00:01.000, 0, 1500, 1965, 900.0, 0x4, Not Active, Not Active, Not Active, Active",
+            "2026/10/20 01:00:02.000, 0, 1965, 1965, 100.0, 0x0, Not Active, Not Active, Not Active, Not Active"]
+    open(cs.path, "w").write("\n".join(rows) + "\n")
+    import datetime
+
+    t = datetime.datetime(2026, 10, 20, 1, 0, 1).timestamp()
+    s = cs.summary(t - 0.5, t + 0.5)
+    assert s["samples"] == 1 and s["samples_in_timed_region"] and s["sm_mhz"] == 1500.0
+    assert s["reasons"] == ["sw_power_cap"]
+
+
+@pytest.mark.gpu
+def test_our_arm_line():
+    d = _run(["--config", "1", "--steps", "200", "--warmup", "3", "--no-cpu-baseline"])
+    assert BASE_KEYS <= set(d) and "impl" not in d
+    r = d["roofline"]
+    assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(r)
+    assert r["bound"] == "hbm" and 0 < r["frac"] < 1
+    assert d["gpu_launches"] == 200
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+    assert d["e2e"]["h2d_bytes_per_step"] == 2 * (1 << 20) * 4
