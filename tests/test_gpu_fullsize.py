@@ -1,12 +1,12 @@
-"""Full-size parity at the BASELINE.json shapes (cfg3/4/5), through
-size-independent checks:
+"""Full-size parity at the BASELINE.json shapes (cfg3/4/5):
 
-* Freivalds identity over F_p on the WHOLE output: C*r == A*(B*r) (mod p,
-  field fold applied) for random r in F_p^N -- catches any wrong entry with
-  probability >= 1 - 1/p per vector; two vectors are used;
-* sampled rows (first, last and random) against the independent plane oracle;
-* the two independent engines (tcgen05 INT8 planes vs FP64 DMMA words with
-  REDQ) agree bit-for-bit on the whole output (cfg3, cfg4);
+* the WHOLE output against the independent exact plane oracle (float64 BLAS
+  coefficient-plane products, exact below 2^53, then the X^k fold and mod p;
+  SURVEY.md 8(c)(ii)) -- 6-12 s of host BLAS per config;
+* Freivalds identity over F_p: C*r == A*(B*r) (mod p, field fold applied) for
+  two random r in F_p^N (size-independent, cheap);
+* every engine (fp4k evaluation planes, fp4 and i8 expanded planes, f64 DQT
+  words with REDQ) agrees bit-for-bit on the whole output;
 * cfg1/cfg2 at full size against the oracle directly.
 """
 
@@ -52,13 +52,6 @@ def _freivalds_gf(a, b, c, f, seeds=(11, 12)):
         assert np.array_equal(lhs, rhs), f"Freivalds check failed (seed {sd})"
 
 
-def _rows_check(a, b, c, f, nrows=24):
-    m = a.shape[0]
-    rows = np.unique(np.concatenate([[0, m - 1], np.random.default_rng(0).integers(0, m, nrows)]))
-    ref = O.gf_matmul_planes(f, a[rows], b)
-    assert np.array_equal(c[rows], ref)
-
-
 @pytest.mark.parametrize("cfg", [3, 5])
 def test_gf_matmul_full(cfg):
     c = W.CONFIGS[cfg]
@@ -68,7 +61,7 @@ def test_gf_matmul_full(cfg):
     da, db = torch.from_numpy(x["a"]).cuda(), torch.from_numpy(x["b"]).cuda()
     got = fld.matmul_coeffs(da, db, engine="i8").cpu().numpy()
     _freivalds_gf(x["a"], x["b"], got, of)
-    _rows_check(x["a"], x["b"], got, of)
+    assert np.array_equal(got, O.gf_matmul_planes(of, x["a"], x["b"]))  # whole output
     for eng in ("auto", "fp4k", "fp4"):  # FP4 engines: Toom/Karatsuba planes and expanded form
         alt = fld.matmul_coeffs(da, db, engine=eng).cpu().numpy()
         assert np.array_equal(alt, got), eng
@@ -92,8 +85,7 @@ def test_right_cmm_full():
         lhs = (got.astype(np.int64) @ r) % 3
         rhs = (a.astype(np.int64) @ ((a.astype(np.int64) @ r) % 3)) % 3
         assert np.array_equal(lhs, rhs)
-    rows = np.array([0, 1, n // 2, n - 1])
-    assert np.array_equal(got[rows], O.modmatmul_planes(a[rows], a, 3))
+    assert np.array_equal(got, O.modmatmul_planes(a, a, 3))  # whole output, float64 BLAS oracle
     f64 = cmm.right_cmm(da, cmm.compress_rows(da, prm), engine="f64").cpu().numpy()
     assert np.array_equal(f64, got)
     for eng in ("auto", "fp4k", "fp4"):
