@@ -177,6 +177,13 @@ class TestGFDot:
 ENGINES = ["i8", "f64", "fp4", "fp4k"]
 
 
+def _fp4k_plan_fits(p, k):
+    """plan_planes (engine_tc.cu): Toom-Cook 2k-1 planes when 2k-1 <= p+1, else
+    Karatsuba k(k+1)/2; at most 8 planes and p^k <= 1024 codes."""
+    s = 2 * k - 1 if 2 * k - 1 <= p + 1 else k * (k + 1) // 2
+    return p <= 7 and s <= 8 and p ** k <= 1024
+
+
 class TestGFMatmul:
     @pytest.mark.parametrize("engine", ENGINES)
     @pytest.mark.parametrize("fname,pre", [("gf9_8192", "cfg3"), ("gf9_8192", "cfg3s"), ("gf11_64", "gf11"),
@@ -233,6 +240,31 @@ class TestGFMatmul:
         ref = O.gf_matmul_planes(of, a, b)
         for e in ENGINES:
             assert np.array_equal(f.matmul_coeffs(a, b, engine=e), ref)
+
+    @pytest.mark.parametrize("p,k", [(2, 2), (2, 3), (3, 4), (5, 3), (5, 4), (13, 2)])
+    def test_more_fields_all_engines(self, p, k):
+        """fields beyond the five configs: Toom-Cook (GF(4), GF(125)), Karatsuba
+        (GF(8)), the expanded form when no plane plan fits (GF(81), GF(625)),
+        INT8 when the residues exceed E2M1 (GF(169))."""
+        from paper_0809_0063_b200.gfext import build_field
+
+        f = build_field(p, k, max_dot_length=1)
+        of = O.build_field(p, k, irreducible=list(f.irreducible), max_dot_length=1)
+        g = W.rng(p * 10 + k)
+        m, kd, n = 70, 150, 90
+        a = g.integers(0, p, (m, kd, k), dtype=np.uint8)
+        b = g.integers(0, p, (kd, n, k), dtype=np.uint8)
+        ref = O.gf_matmul_planes(of, a, b)
+        for eng in ("auto", "i8", "fp4", "fp4k"):
+            if eng in ("fp4", "fp4k") and p > 7:
+                with pytest.raises(Q.ParamsViolation):
+                    f.matmul_coeffs(a, b, engine=eng)
+                continue
+            if eng == "fp4k" and not _fp4k_plan_fits(p, k):
+                with pytest.raises(Q.ParamsViolation):
+                    f.matmul_coeffs(a, b, engine=eng)
+                continue
+            assert np.array_equal(f.matmul_coeffs(a, b, engine=eng), ref), eng
 
     @pytest.mark.parametrize("fuse", ["0", "1"])
     @pytest.mark.parametrize("cfg,m,kd,n", [(3, 300, 520, 250), (3, 513, 96, 481), (5, 257, 300, 500),
