@@ -5,9 +5,11 @@
 // (src/gfext.py:136-146).
 //
 // These are exact-semantics primitives (uint64 wrap-around GEMM, any-width
-// REDQ); the throughput engines for the configs live in engine_i8.cu,
+// REDQ); the throughput engines for the configs live in engine_tc.cu,
 // engine_f64.cu and batched.cu, behind the operation-level API where the
 // parameters prove the digit bounds.
+#include <algorithm>
+
 #include "qadic_common.cuh"
 #include "qadic_internal.h"
 
@@ -130,6 +132,77 @@ __global__ void redq_words_kernel(const uint64_t* __restrict__ r, int64_t n, uin
     if (packed) packed[idx] = word;
 }
 
+// Vectorised REDQ for D = d (compile time): each thread takes two consecutive
+// words (one 16-byte load), emits 2(D+1) digits as D+1 16-byte stores and/or
+// the two repacked words as one 16-byte store; grid-stride over a one-wave grid.
+// The correction mu_i = (u_i + c*u_{i+1}) mod p is a lookup in the tabulated
+// correction (redq.py:194-300 with one-digit blocks) staged in shared memory
+// (p*p bytes, p <= 127) whenever both digits are reduced (u < p, always so for
+// in-range words); anything else takes the exact uint64 path of _speed.pyx.
+constexpr int RQ_THREADS = 256;
+constexpr int RQ_TAB = 127 * 127;
+
+template <int D>
+__device__ __forceinline__ void redq_word(uint64_t ri, uint64_t p, int t, double invp_up, double bound, uint64_t corr,
+                                          int mode, const uint8_t* tab, uint64_t (&out)[D + 1], uint64_t& word) {
+    const uint64_t s = div_p(ri, p, invp_up, bound);
+    uint64_t u[D + 1];
+#pragma unroll
+    for (int i = 0; i <= D; ++i) u[i] = (ri >> (i * t)) - p * (s >> (i * t));
+    word = 0;
+#pragma unroll
+    for (int i = 0; i <= D; ++i) {
+        uint64_t o = u[i];
+        if (mode >= 1 && i < D) {
+            if (tab != nullptr && u[i] < p && u[i + 1] < p) o = tab[u[i] * p + u[i + 1]];
+            else o = (u[i] + corr * u[i + 1]) % p;
+        }
+        out[i] = o;
+        word += o << (i * t);
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(RQ_THREADS) redq_vec_kernel(const uint64_t* __restrict__ r, int64_t n, uint64_t p,
+                                                              int t, double invp_up, double bound, uint64_t corr,
+                                                              int mode, uint64_t* __restrict__ digits,
+                                                              uint64_t* __restrict__ packed) {
+    __shared__ uint8_t stab[RQ_TAB];
+    const bool use_tab = mode >= 1 && p * p <= (uint64_t)RQ_TAB;
+    if (use_tab) {
+        for (int i = threadIdx.x; i < (int)(p * p); i += RQ_THREADS)
+            stab[i] = (uint8_t)(((uint64_t)(i / (int)p) + corr * (uint64_t)(i % (int)p)) % p);
+        __syncthreads();
+    }
+    const uint8_t* tab = use_tab ? stab : nullptr;
+    const int64_t pairs = n / 2;
+    for (int64_t q = (int64_t)blockIdx.x * RQ_THREADS + threadIdx.x; q < pairs; q += (int64_t)gridDim.x * RQ_THREADS) {
+        const ulonglong2 x = __ldcs(reinterpret_cast<const ulonglong2*>(r) + q);
+        uint64_t o0[D + 1], o1[D + 1], w0, w1;
+        redq_word<D>(x.x, p, t, invp_up, bound, corr, mode, tab, o0, w0);
+        redq_word<D>(x.y, p, t, invp_up, bound, corr, mode, tab, o1, w1);
+        if (digits) {
+            uint64_t all[2 * (D + 1)];
+#pragma unroll
+            for (int i = 0; i <= D; ++i) {
+                all[i] = o0[i];
+                all[D + 1 + i] = o1[i];
+            }
+            ulonglong2* dst = reinterpret_cast<ulonglong2*>(digits + 2 * q * (D + 1));
+#pragma unroll
+            for (int i = 0; i <= D; ++i) __stcs(dst + i, make_ulonglong2(all[2 * i], all[2 * i + 1]));
+        }
+        if (packed) __stcs(reinterpret_cast<ulonglong2*>(packed) + q, make_ulonglong2(w0, w1));
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd tail word
+        uint64_t o[D + 1], w;
+        redq_word<D>(r[n - 1], p, t, invp_up, bound, corr, mode, tab, o, w);
+        if (digits)
+            for (int i = 0; i <= D; ++i) digits[(n - 1) * (D + 1) + i] = o[i];
+        if (packed) packed[n - 1] = w;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // DQT row packing (cmm.py:72-85) and unpacking (cmm.py:130-145).
 // ---------------------------------------------------------------------------
@@ -160,6 +233,123 @@ __global__ void unpack_rows_kernel(const uint64_t* __restrict__ words, int64_t r
     const int e = reverse ? (k - 1 - j) : j;
     const uint64_t w = words[r * width + c / k];
     out[idx] = (uint8_t)((w >> (e * t)) & ((1ull << t) - 1));
+}
+
+// Tiled pack / unpack: a block owns PK_WORDS consecutive words of one row.
+// The row's uint8 segment moves between HBM and shared memory as 16-byte chunks
+// (aligned to the global address, so any row offset works); each thread packs
+// or unpacks two words and writes / reads them as one 16-byte vector.
+constexpr int PK_THREADS = 256, PK_WORDS = 2 * PK_THREADS;
+
+__global__ void __launch_bounds__(PK_THREADS) pack_rows_tile_kernel(const uint8_t* __restrict__ m, int64_t rows,
+                                                                     int64_t cols, int k, int t, int reverse,
+                                                                     uint64_t* __restrict__ words,
+                                                                     int64_t tiles_per_row) {
+    __shared__ __align__(16) uint8_t buf[PK_WORDS * 8 + 32];
+    const int64_t width = (cols + k - 1) / k;
+    const uint8_t* mend = m + rows * cols;
+    for (int64_t tile = blockIdx.x; tile < rows * tiles_per_row; tile += gridDim.x) {
+        const int64_t r = tile / tiles_per_row, g0 = (tile % tiles_per_row) * PK_WORDS;
+        const int nw = (int)(width - g0 < PK_WORDS ? width - g0 : PK_WORDS);
+        const int64_t c0 = g0 * k;
+        const int64_t nbytes = (cols - c0 < (int64_t)nw * k) ? cols - c0 : (int64_t)nw * k;
+        const uint8_t* src = m + r * cols + c0;
+        const uint8_t* base = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15));
+        const int lead = (int)(src - base);
+        const int nchunks = (int)((lead + nbytes + 15) / 16);
+        for (int i = threadIdx.x; i < nchunks; i += PK_THREADS) {
+            const uint8_t* ch = base + 16 * i;
+            if (ch >= m && ch + 16 <= mend) {
+                *reinterpret_cast<uint4*>(buf + 16 * i) = __ldcs(reinterpret_cast<const uint4*>(ch));
+            } else {
+                for (int b = 0; b < 16; ++b) buf[16 * i + b] = (ch + b >= m && ch + b < mend) ? ch[b] : 0;
+            }
+        }
+        __syncthreads();
+        uint64_t w2[2] = {0, 0};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int w = 2 * threadIdx.x + h;
+            if (w < nw) {
+                for (int j = 0; j < k; ++j) {
+                    const int64_t off = (int64_t)w * k + j;
+                    if (off < nbytes) {
+                        const int e = reverse ? (k - 1 - j) : j;
+                        w2[h] += (uint64_t)buf[lead + off] << (e * t);
+                    }
+                }
+            }
+        }
+        uint64_t* dst = words + r * width + g0 + 2 * threadIdx.x;
+        if (2 * threadIdx.x + 1 < nw && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+            __stcs(reinterpret_cast<ulonglong2*>(dst), make_ulonglong2(w2[0], w2[1]));
+        } else {
+            if (2 * threadIdx.x < nw) dst[0] = w2[0];
+            if (2 * threadIdx.x + 1 < nw) dst[1] = w2[1];
+        }
+        __syncthreads();  // buf is refilled by the next tile
+    }
+}
+
+__global__ void __launch_bounds__(PK_THREADS) unpack_rows_tile_kernel(const uint64_t* __restrict__ words,
+                                                                       int64_t rows, int64_t cols, int k, int t,
+                                                                       int reverse, uint8_t* __restrict__ out,
+                                                                       int64_t tiles_per_row) {
+    __shared__ __align__(16) uint8_t buf[PK_WORDS * 8 + 32];
+    const int64_t width = (cols + k - 1) / k;
+    const uint64_t mask = t >= 64 ? ~0ull : ((1ull << t) - 1);
+    for (int64_t tile = blockIdx.x; tile < rows * tiles_per_row; tile += gridDim.x) {
+        const int64_t r = tile / tiles_per_row, g0 = (tile % tiles_per_row) * PK_WORDS;
+        const int nw = (int)(width - g0 < PK_WORDS ? width - g0 : PK_WORDS);
+        const int64_t c0 = g0 * k;
+        const int64_t nbytes = (cols - c0 < (int64_t)nw * k) ? cols - c0 : (int64_t)nw * k;
+        uint8_t* dst = out + r * cols + c0;
+        const int lead = (int)(reinterpret_cast<uintptr_t>(dst) & 15);  // buf[lead + x] <-> dst[x]
+        const uint64_t* srcw = words + r * width + g0 + 2 * threadIdx.x;
+        uint64_t w2[2] = {0, 0};
+        if (2 * threadIdx.x + 1 < nw && (reinterpret_cast<uintptr_t>(srcw) & 15) == 0) {
+            const ulonglong2 x = __ldcs(reinterpret_cast<const ulonglong2*>(srcw));
+            w2[0] = x.x;
+            w2[1] = x.y;
+        } else {
+            if (2 * threadIdx.x < nw) w2[0] = srcw[0];
+            if (2 * threadIdx.x + 1 < nw) w2[1] = srcw[1];
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int w = 2 * threadIdx.x + h;
+            if (w < nw) {
+                for (int j = 0; j < k; ++j) {
+                    const int64_t off = (int64_t)w * k + j;
+                    const int e = reverse ? (k - 1 - j) : j;
+                    if (off < nbytes) buf[lead + off] = (uint8_t)((w2[h] >> (e * t)) & mask);
+                }
+            }
+        }
+        __syncthreads();
+        const int nchunks = (int)((lead + nbytes + 15) / 16);
+        uint8_t* base = dst - lead;
+        for (int i = threadIdx.x; i < nchunks; i += PK_THREADS) {
+            const int lo = 16 * i, hi = lo + 16;
+            if (lo >= lead && hi <= lead + nbytes) {
+                __stcs(reinterpret_cast<uint4*>(base + lo), *reinterpret_cast<const uint4*>(buf + lo));
+            } else {
+                for (int b = lo; b < hi; ++b)
+                    if (b >= lead && b < lead + nbytes) base[b] = buf[b];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+static int grid_for_tiles(int64_t tiles) {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return (int)std::min<int64_t>(tiles, (int64_t)sms * 8);
 }
 
 // ---------------------------------------------------------------------------
@@ -246,8 +436,32 @@ static int redq_launch(const uint64_t* r, int64_t n, int64_t p, int32_t t, int32
     if (n == 0) return QADIC_OK;
     const uint64_t q = 1ull << t;
     const uint64_t corr = (q % (uint64_t)p == 0) ? 0 : ((uint64_t)p - q % (uint64_t)p) % (uint64_t)p;
-    redq_words_kernel<<<blocks_for(n, 256), 256, 0, (cudaStream_t)stream>>>(
-        r, n, (uint64_t)p, t, d, host_reciprocal_up(p), host_case2_bound(), corr, mode, digits, packed);
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool aligned = ((uintptr_t)r % 16 == 0) && (!digits || (uintptr_t)digits % 16 == 0) &&
+                         (!packed || (uintptr_t)packed % 16 == 0);
+    if (aligned && d >= 1 && d <= 6) {
+        static int sms = 0;
+        if (!sms) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        }
+        const int64_t pairs = (n + 1) / 2;
+        const int grid = (int)std::min<int64_t>((pairs + RQ_THREADS - 1) / RQ_THREADS, (int64_t)sms * 8);
+        const double inv = host_reciprocal_up(p), bnd = host_case2_bound();
+        const uint64_t pp = (uint64_t)p;
+        switch (d) {
+#define QADIC_RQ(DD)                                                                                       \
+    case DD:                                                                                               \
+        redq_vec_kernel<DD><<<grid, RQ_THREADS, 0, s>>>(r, n, pp, t, inv, bnd, corr, mode, digits, packed); \
+        break;
+            QADIC_RQ(1) QADIC_RQ(2) QADIC_RQ(3) QADIC_RQ(4) QADIC_RQ(5) QADIC_RQ(6)
+#undef QADIC_RQ
+        }
+        return check_launch(what, 1);
+    }
+    redq_words_kernel<<<blocks_for(n, 256), 256, 0, s>>>(r, n, (uint64_t)p, t, d, host_reciprocal_up(p),
+                                                         host_case2_bound(), corr, mode, digits, packed);
     return check_launch(what, 1);
 }
 
@@ -265,9 +479,16 @@ int qadic_pack_rows_u8(const uint8_t* m, int64_t rows, int64_t cols, int32_t k, 
                        uint64_t* words, void* stream) {
     QADIC_REQUIRE(rows >= 0 && cols >= 0 && k >= 1 && t >= 1 && (int64_t)k * t <= 64, QADIC_ERR_VALUE,
                   "bad pack geometry");
-    const int64_t total = rows * ((cols + k - 1) / k);
+    const int64_t width = (cols + k - 1) / k, total = rows * width;
     if (total == 0) return QADIC_OK;
-    pack_rows_kernel<<<blocks_for(total, 256), 256, 0, (cudaStream_t)stream>>>(m, rows, cols, k, t, reverse, words);
+    if (k <= 8) {
+        const int64_t tpr = (width + PK_WORDS - 1) / PK_WORDS;
+        pack_rows_tile_kernel<<<grid_for_tiles(rows * tpr), PK_THREADS, 0, (cudaStream_t)stream>>>(
+            m, rows, cols, k, t, reverse, words, tpr);
+    } else {
+        pack_rows_kernel<<<blocks_for(total, 256), 256, 0, (cudaStream_t)stream>>>(m, rows, cols, k, t, reverse,
+                                                                                    words);
+    }
     return check_launch("pack_rows_u8", 1);
 }
 
@@ -275,6 +496,12 @@ int qadic_unpack_rows_u8(const uint64_t* words, int64_t rows, int64_t cols, int3
                          int32_t reverse, uint8_t* out, void* stream) {
     QADIC_REQUIRE(rows >= 0 && cols >= 0 && k >= 1 && t >= 1 && t <= 8 * 8, QADIC_ERR_VALUE, "bad unpack geometry");
     if (rows * cols == 0) return QADIC_OK;
+    if (k <= 8) {
+        const int64_t width = (cols + k - 1) / k, tpr = (width + PK_WORDS - 1) / PK_WORDS;
+        unpack_rows_tile_kernel<<<grid_for_tiles(rows * tpr), PK_THREADS, 0, (cudaStream_t)stream>>>(
+            words, rows, cols, k, t, reverse, out, tpr);
+        return check_launch("unpack_rows_u8", 1);
+    }
     unpack_rows_kernel<<<blocks_for(rows * cols, 256), 256, 0, (cudaStream_t)stream>>>(words, rows, cols, k, t,
                                                                                         reverse, out);
     return check_launch("unpack_rows_u8", 1);

@@ -328,6 +328,28 @@ class TestGFMatmul:
 # ---------------------------------------------------------------------------
 # cfg4: right-compressed matmul
 # ---------------------------------------------------------------------------
+class TestPackRows:
+    """qadic_pack_rows_u8 / qadic_unpack_rows_u8 (cmm.py:72-85, 130-145): tiled
+    16-byte kernels at ragged shapes and odd row offsets, both digit orders."""
+
+    @pytest.mark.parametrize("rows,cols", [(1, 1), (3, 7), (5, 1023), (17, 1537), (2, 4100), (64, 3000)])
+    @pytest.mark.parametrize("k,t", [(1, 8), (2, 17), (3, 17), (5, 12), (8, 8)])
+    def test_pack_unpack(self, rows, cols, k, t):
+        import torch
+
+        g = W.rng(rows * cols + k)
+        m = g.integers(0, 1 << min(t, 8), (rows, cols), dtype=np.uint8)
+        dm = torch.from_numpy(m).cuda()
+        for reverse in (False, True):
+            w = cmm._pack_dev(dm, k, t, reverse).cpu().numpy().view(np.uint64)
+            padded = np.zeros((rows, -(-cols // k) * k), np.uint8)
+            padded[:, :cols] = m
+            ref = O.pack_last_axis(padded.reshape(rows, -1, k), t, reverse=reverse)
+            assert np.array_equal(w, ref), reverse
+            back = cmm._unpack_dev(torch.from_numpy(w.view(np.int64)).cuda(), rows, cols, k, t, reverse)
+            assert np.array_equal(back.cpu().numpy(), m), reverse
+
+
 class TestRightCMM:
     @pytest.mark.parametrize("engine", ENGINES)
     @pytest.mark.parametrize("n", [250, 97])
