@@ -558,6 +558,90 @@ def run_ours(args):
 REF_BUDGET_S = float(os.environ.get("QADIC_REF_BUDGET_S", "90"))  # wall budget of the whole reference-arm run
 
 
+# ---------------------------------------------------------------------------
+# Layer-K primitives at config scale (HBM-bound): --config redq | pack
+# ---------------------------------------------------------------------------
+PRIMS = {
+    # REDQ of cfg3's accumulators: 8192^2 words, p=3, q=2^17, d=2 -> digits uint64[n, 3]
+    "redq": {"n": 1 << 26, "p": 3, "t": 17, "d": 2},
+    # cfg4's row compression: uint8[16384, 16384] -> uint64[16384, 5462] (k=3, q=2^17)
+    "pack": {"rows": 16384, "cols": 16384, "k": 3, "t": 17},
+}
+
+
+def run_primitive(args, kind):
+    import torch
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    sys.path.insert(0, ROOT)
+    import paper_0809_0063_b200 as Q
+    from paper_0809_0063_b200 import _native as N
+
+    N.load_library()
+    cfgp = PRIMS[kind]
+    g = np.random.default_rng(7)
+    if kind == "redq":
+        n, p, t, d = cfgp["n"], cfgp["p"], cfgp["t"], cfgp["d"]
+        # in-range accumulators: every base-2^t digit below q
+        host = sum(g.integers(0, 1 << t, n, dtype=np.uint64) << np.uint64(i * t) for i in range(d + 1))
+        sets = [torch.from_numpy(host.view(np.int64)).cuda(), torch.from_numpy(host.view(np.int64)).cuda()]
+        outs = [torch.empty((n, d + 1), dtype=torch.int64, device="cuda") for _ in sets]
+        L = N.lib()
+
+        def step(i):
+            N.check(L.qadic_reduce_words(N.ptr(sets[i % 2]), n, p, t, d, 0, N.ptr(outs[i % 2]), N.stream_ptr()))
+
+        byts, units, unit = 8 * n + 8 * n * (d + 1), n, "words/s"
+        workload = f"redq:reduce_words_digits n=2^26 p={p} q=2^{t} d={d} (cfg3 accumulators)"
+        kname = "reduce_words"
+    else:
+        rows, cols, k, t = cfgp["rows"], cfgp["cols"], cfgp["k"], cfgp["t"]
+        host = g.integers(0, 2, (rows, cols), dtype=np.uint8)
+        sets = [torch.from_numpy(host).cuda(), torch.from_numpy(host).cuda()]
+        width = -(-cols // k)
+        outs = [torch.empty((rows, width), dtype=torch.int64, device="cuda") for _ in sets]
+        L = N.lib()
+
+        def step(i):
+            N.check(L.qadic_pack_rows_u8(N.ptr(sets[i % 2]), rows, cols, k, t, 0, N.ptr(outs[i % 2]),
+                                         N.stream_ptr()))
+
+        byts, units, unit = rows * cols + 8 * rows * width, rows * cols, "entries/s"
+        workload = f"pack:compress_rows uint8[{rows},{cols}] k={k} q=2^{t} (cfg4 B operand)"
+        kname = "pack_rows_u8"
+    steps = args.steps or 100
+    for i in range(max(3, args.warmup)):
+        step(i)
+    torch.cuda.synchronize()
+    launches0 = N.launch_count()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        w0 = time.time()
+        e0.record()
+        for i in range(steps):
+            step(i)
+        e1.record()
+        torch.cuda.synchronize()
+        w1 = time.time()
+    ms = e0.elapsed_time(e1) / steps
+    launches = N.launch_count() - launches0
+    peaks, peak_src = load_peaks()
+    achieved = byts / (ms / 1e3) / 1e9
+    line = {"metric": "GF(p^k) mult-adds/s (packed matmul) and REDQ coeffs/s vs roofline, 1-8 GPU",
+            "value": units / (ms / 1e3), "unit": unit, "n_gpus": 1, "steps": steps, "warmup": max(3, args.warmup),
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (seeded)", "config": {"workload": workload, "l2": "2 rotating sets > L2"},
+            "roofline": {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
+                         "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
+                         "avg_launch_ms": round(ms, 5), "algorithmic_bytes_per_launch": byts,
+                         "avg_launch_source": "timed region / K (one launch per step)",
+                         "peak_source": f"{peak_src} hbm_gbs (copy)"},
+            "e2e": None, "gpu_launches": int(launches), "clocks": clk.summary(w0, w1)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def run_reference(args):
     """The reference's own CPU implementation on this box's host cores."""
     ws, rank, _ = dist_env()
@@ -627,6 +711,12 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="eager launches for cfg1/cfg2")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup) if args.impl == "ours" else args.warmup
+    if args.config in PRIMS:
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "Layer-K primitive lines have no reference arm"}))
+        else:
+            run_primitive(args, args.config)
+        return
     cfgs = [1, 2, 3, 4, 5] if args.config == "all" else [int(args.config)]
     steps_given = args.steps
     for cfg in cfgs:

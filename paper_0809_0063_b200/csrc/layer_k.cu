@@ -133,8 +133,9 @@ __global__ void redq_words_kernel(const uint64_t* __restrict__ r, int64_t n, uin
 }
 
 // Vectorised REDQ for D = d (compile time): each thread takes two consecutive
-// words (one 16-byte load), emits 2(D+1) digits as D+1 16-byte stores and/or
-// the two repacked words as one 16-byte store; grid-stride over a one-wave grid.
+// words (one 16-byte load); a warp's 64(D+1) digits are staged in shared memory
+// and stored as lane-consecutive 16-byte vectors, the repacked words as one
+// 16-byte store per thread; grid-stride over a one-wave grid.
 // The correction mu_i = (u_i + c*u_{i+1}) mod p is a lookup in the tabulated
 // correction (redq.py:194-300 with one-digit blocks) staged in shared memory
 // (p*p bytes, p <= 127) whenever both digits are reduced (u < p, always so for
@@ -175,24 +176,40 @@ __global__ void __launch_bounds__(RQ_THREADS) redq_vec_kernel(const uint64_t* __
         __syncthreads();
     }
     const uint8_t* tab = use_tab ? stab : nullptr;
+    // digits of a warp's 64 words are one contiguous run: stage them in shared
+    // memory and store the run with lane-consecutive 16-byte vectors
+    __shared__ __align__(16) uint64_t stage[RQ_THREADS / 32][64 * (D + 1)];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t pairs = n / 2;
-    for (int64_t q = (int64_t)blockIdx.x * RQ_THREADS + threadIdx.x; q < pairs; q += (int64_t)gridDim.x * RQ_THREADS) {
-        const ulonglong2 x = __ldcs(reinterpret_cast<const ulonglong2*>(r) + q);
-        uint64_t o0[D + 1], o1[D + 1], w0, w1;
-        redq_word<D>(x.x, p, t, invp_up, bound, corr, mode, tab, o0, w0);
-        redq_word<D>(x.y, p, t, invp_up, bound, corr, mode, tab, o1, w1);
-        if (digits) {
-            uint64_t all[2 * (D + 1)];
-#pragma unroll
-            for (int i = 0; i <= D; ++i) {
-                all[i] = o0[i];
-                all[D + 1 + i] = o1[i];
-            }
-            ulonglong2* dst = reinterpret_cast<ulonglong2*>(digits + 2 * q * (D + 1));
-#pragma unroll
-            for (int i = 0; i <= D; ++i) __stcs(dst + i, make_ulonglong2(all[2 * i], all[2 * i + 1]));
+    const int64_t stride = (int64_t)gridDim.x * RQ_THREADS;
+    for (int64_t q0 = (int64_t)blockIdx.x * RQ_THREADS; q0 < pairs; q0 += stride) {
+        const int64_t q = q0 + threadIdx.x;
+        const int64_t qw = q0 + 32 * wid;  // first pair of this warp
+        const bool live = q < pairs;
+        uint64_t o0[D + 1], o1[D + 1], w0 = 0, w1 = 0;
+        if (live) {
+            const ulonglong2 x = __ldcs(reinterpret_cast<const ulonglong2*>(r) + q);
+            redq_word<D>(x.x, p, t, invp_up, bound, corr, mode, tab, o0, w0);
+            redq_word<D>(x.y, p, t, invp_up, bound, corr, mode, tab, o1, w1);
         }
-        if (packed) __stcs(reinterpret_cast<ulonglong2*>(packed) + q, make_ulonglong2(w0, w1));
+        if (digits) {
+            uint64_t* st = stage[wid];
+            if (live) {
+#pragma unroll
+                for (int i = 0; i <= D; ++i) {
+                    st[2 * lane * (D + 1) + i] = o0[i];
+                    st[(2 * lane + 1) * (D + 1) + i] = o1[i];
+                }
+            }
+            __syncwarp();
+            const int64_t npairs = pairs - qw < 32 ? pairs - qw : 32;  // pairs of this warp in range
+            const int nvec = (int)(npairs > 0 ? npairs * (D + 1) : 0);  // 16-byte vectors
+            ulonglong2* dst = reinterpret_cast<ulonglong2*>(digits + 2 * qw * (D + 1));
+            for (int v = lane; v < nvec; v += 32)
+                __stcs(dst + v, *reinterpret_cast<const ulonglong2*>(st + 2 * v));
+            __syncwarp();
+        }
+        if (packed && live) __stcs(reinterpret_cast<ulonglong2*>(packed) + q, make_ulonglong2(w0, w1));
     }
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd tail word
         uint64_t o[D + 1], w;
@@ -238,61 +255,94 @@ __global__ void unpack_rows_kernel(const uint64_t* __restrict__ words, int64_t r
 // Tiled pack / unpack: a block owns PK_WORDS consecutive words of one row.
 // The row's uint8 segment moves between HBM and shared memory as 16-byte chunks
 // (aligned to the global address, so any row offset works); each thread packs
-// or unpacks two words and writes / reads them as one 16-byte vector.
-constexpr int PK_THREADS = 256, PK_WORDS = 2 * PK_THREADS;
+// or unpacks PK_WPT consecutive words and writes / reads them as 16-byte vectors.
+constexpr int PK_THREADS = 256, PK_WPT = 8, PK_WORDS = PK_WPT * PK_THREADS;
 
+template <int k>
 __global__ void __launch_bounds__(PK_THREADS) pack_rows_tile_kernel(const uint8_t* __restrict__ m, int64_t rows,
-                                                                     int64_t cols, int k, int t, int reverse,
+                                                                     int64_t cols, int t, int reverse,
                                                                      uint64_t* __restrict__ words,
                                                                      int64_t tiles_per_row) {
-    __shared__ __align__(16) uint8_t buf[PK_WORDS * 8 + 32];
+    constexpr int BUF = PK_WORDS * 8 + 32;
+    __shared__ __align__(16) uint8_t buf[2][BUF];  // the next tile streams in (cp.async) during this one
     const int64_t width = (cols + k - 1) / k;
     const uint8_t* mend = m + rows * cols;
-    for (int64_t tile = blockIdx.x; tile < rows * tiles_per_row; tile += gridDim.x) {
-        const int64_t r = tile / tiles_per_row, g0 = (tile % tiles_per_row) * PK_WORDS;
-        const int nw = (int)(width - g0 < PK_WORDS ? width - g0 : PK_WORDS);
-        const int64_t c0 = g0 * k;
-        const int64_t nbytes = (cols - c0 < (int64_t)nw * k) ? cols - c0 : (int64_t)nw * k;
-        const uint8_t* src = m + r * cols + c0;
-        const uint8_t* base = reinterpret_cast<const uint8_t*>(reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15));
-        const int lead = (int)(src - base);
-        const int nchunks = (int)((lead + nbytes + 15) / 16);
+    const int64_t ntiles = rows * tiles_per_row;
+    struct Geo {
+        int64_t r, g0, nbytes;
+        int nw, lead;
+    };
+    auto geo = [&](int64_t tile) {
+        Geo g;
+        g.r = tile / tiles_per_row;
+        g.g0 = (tile % tiles_per_row) * PK_WORDS;
+        g.nw = (int)(width - g.g0 < PK_WORDS ? width - g.g0 : PK_WORDS);
+        const int64_t c0 = g.g0 * k;
+        g.nbytes = (cols - c0 < (int64_t)g.nw * k) ? cols - c0 : (int64_t)g.nw * k;
+        g.lead = (int)(reinterpret_cast<uintptr_t>(m + g.r * cols + c0) & 15);
+        return g;
+    };
+    auto stage = [&](int64_t tile, int bi) {
+        const Geo g = geo(tile);
+        const uint8_t* base = m + g.r * cols + g.g0 * k - g.lead;
+        const int nchunks = (int)((g.lead + g.nbytes + 15) / 16);
         for (int i = threadIdx.x; i < nchunks; i += PK_THREADS) {
             const uint8_t* ch = base + 16 * i;
             if (ch >= m && ch + 16 <= mend) {
-                *reinterpret_cast<uint4*>(buf + 16 * i) = __ldcs(reinterpret_cast<const uint4*>(ch));
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                                 (uint32_t)__cvta_generic_to_shared(buf[bi] + 16 * i)),
+                             "l"(ch));
             } else {
-                for (int b = 0; b < 16; ++b) buf[16 * i + b] = (ch + b >= m && ch + b < mend) ? ch[b] : 0;
+                for (int q = 0; q < 16; ++q) buf[bi][16 * i + q] = (ch + q >= m && ch + q < mend) ? ch[q] : 0;
             }
         }
+        asm volatile("cp.async.commit_group;");
+    };
+    if ((int64_t)blockIdx.x < ntiles) stage(blockIdx.x, 0);
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int bi = it & 1;
+        if (tile + gridDim.x < ntiles) stage(tile + gridDim.x, bi ^ 1);
+        else asm volatile("cp.async.commit_group;");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
         __syncthreads();
-        uint64_t w2[2] = {0, 0};
+        const Geo g = geo(tile);
+        uint64_t wv[PK_WPT];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int w = 2 * threadIdx.x + h;
-            if (w < nw) {
+        for (int h = 0; h < PK_WPT; ++h) {
+            const int w = 2 * threadIdx.x + (h & 1) + 2 * PK_THREADS * (h >> 1);  // lane-consecutive pairs
+            wv[h] = 0;
+            if (w < g.nw) {
+                const bool whole = (int64_t)w * k + k <= g.nbytes;
+#pragma unroll
                 for (int j = 0; j < k; ++j) {
                     const int64_t off = (int64_t)w * k + j;
-                    if (off < nbytes) {
+                    if (whole || off < g.nbytes) {
                         const int e = reverse ? (k - 1 - j) : j;
-                        w2[h] += (uint64_t)buf[lead + off] << (e * t);
+                        wv[h] += (uint64_t)buf[bi][g.lead + off] << (e * t);
                     }
                 }
             }
         }
-        uint64_t* dst = words + r * width + g0 + 2 * threadIdx.x;
-        if (2 * threadIdx.x + 1 < nw && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-            __stcs(reinterpret_cast<ulonglong2*>(dst), make_ulonglong2(w2[0], w2[1]));
-        } else {
-            if (2 * threadIdx.x < nw) dst[0] = w2[0];
-            if (2 * threadIdx.x + 1 < nw) dst[1] = w2[1];
+        uint64_t* rowp = words + g.r * width + g.g0;
+#pragma unroll
+        for (int h = 0; h < PK_WPT; h += 2) {
+            const int w = 2 * threadIdx.x + 2 * PK_THREADS * (h >> 1);
+            if (w + 1 < g.nw && (reinterpret_cast<uintptr_t>(rowp + w) & 15) == 0) {
+                __stcs(reinterpret_cast<ulonglong2*>(rowp + w), make_ulonglong2(wv[h], wv[h + 1]));
+            } else {
+                if (w < g.nw) rowp[w] = wv[h];
+                if (w + 1 < g.nw) rowp[w + 1] = wv[h + 1];
+            }
         }
-        __syncthreads();  // buf is refilled by the next tile
+        __syncthreads();  // this buffer is refilled two tiles later
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
 }
 
+template <int k>
 __global__ void __launch_bounds__(PK_THREADS) unpack_rows_tile_kernel(const uint64_t* __restrict__ words,
-                                                                       int64_t rows, int64_t cols, int k, int t,
+                                                                       int64_t rows, int64_t cols, int t,
                                                                        int reverse, uint8_t* __restrict__ out,
                                                                        int64_t tiles_per_row) {
     __shared__ __align__(16) uint8_t buf[PK_WORDS * 8 + 32];
@@ -305,24 +355,30 @@ __global__ void __launch_bounds__(PK_THREADS) unpack_rows_tile_kernel(const uint
         const int64_t nbytes = (cols - c0 < (int64_t)nw * k) ? cols - c0 : (int64_t)nw * k;
         uint8_t* dst = out + r * cols + c0;
         const int lead = (int)(reinterpret_cast<uintptr_t>(dst) & 15);  // buf[lead + x] <-> dst[x]
-        const uint64_t* srcw = words + r * width + g0 + 2 * threadIdx.x;
-        uint64_t w2[2] = {0, 0};
-        if (2 * threadIdx.x + 1 < nw && (reinterpret_cast<uintptr_t>(srcw) & 15) == 0) {
-            const ulonglong2 x = __ldcs(reinterpret_cast<const ulonglong2*>(srcw));
-            w2[0] = x.x;
-            w2[1] = x.y;
-        } else {
-            if (2 * threadIdx.x < nw) w2[0] = srcw[0];
-            if (2 * threadIdx.x + 1 < nw) w2[1] = srcw[1];
+        const uint64_t* roww = words + r * width + g0;
+        uint64_t wv[PK_WPT];
+#pragma unroll
+        for (int h = 0; h < PK_WPT; h += 2) {  // lane-consecutive 16-byte pairs
+            const int w = 2 * threadIdx.x + 2 * PK_THREADS * (h >> 1);
+            if (w + 1 < nw && (reinterpret_cast<uintptr_t>(roww + w) & 15) == 0) {
+                const ulonglong2 x = __ldcs(reinterpret_cast<const ulonglong2*>(roww + w));
+                wv[h] = x.x;
+                wv[h + 1] = x.y;
+            } else {
+                wv[h] = w < nw ? roww[w] : 0;
+                wv[h + 1] = w + 1 < nw ? roww[w + 1] : 0;
+            }
         }
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int w = 2 * threadIdx.x + h;
+        for (int h = 0; h < PK_WPT; ++h) {
+            const int w = 2 * threadIdx.x + (h & 1) + 2 * PK_THREADS * (h >> 1);
             if (w < nw) {
+                const bool whole = (int64_t)w * k + k <= nbytes;
+#pragma unroll
                 for (int j = 0; j < k; ++j) {
                     const int64_t off = (int64_t)w * k + j;
                     const int e = reverse ? (k - 1 - j) : j;
-                    if (off < nbytes) buf[lead + off] = (uint8_t)((w2[h] >> (e * t)) & mask);
+                    if (whole || off < nbytes) buf[lead + off] = (uint8_t)((wv[h] >> (e * t)) & mask);
                 }
             }
         }
@@ -342,14 +398,35 @@ __global__ void __launch_bounds__(PK_THREADS) unpack_rows_tile_kernel(const uint
     }
 }
 
-static int grid_for_tiles(int64_t tiles) {
+// one wave of resident blocks (grid-stride over the tiles)
+template <typename F>
+static int grid_for_tiles(F kern, int64_t tiles) {
     static int sms = 0;
     if (!sms) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    return (int)std::min<int64_t>(tiles, (int64_t)sms * 8);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PK_THREADS, 0);
+    if (occ < 1) occ = 1;
+    return (int)std::min<int64_t>(tiles, (int64_t)sms * occ);
+}
+
+template <int K>
+static void launch_pack_tiles(const uint8_t* m, int64_t rows, int64_t cols, int t, int reverse, uint64_t* words,
+                              cudaStream_t s) {
+    const int64_t width = (cols + K - 1) / K, tpr = (width + PK_WORDS - 1) / PK_WORDS;
+    pack_rows_tile_kernel<K><<<grid_for_tiles(pack_rows_tile_kernel<K>, rows * tpr), PK_THREADS, 0, s>>>(
+        m, rows, cols, t, reverse, words, tpr);
+}
+
+template <int K>
+static void launch_unpack_tiles(const uint64_t* words, int64_t rows, int64_t cols, int t, int reverse, uint8_t* out,
+                                cudaStream_t s) {
+    const int64_t width = (cols + K - 1) / K, tpr = (width + PK_WORDS - 1) / PK_WORDS;
+    unpack_rows_tile_kernel<K><<<grid_for_tiles(unpack_rows_tile_kernel<K>, rows * tpr), PK_THREADS, 0, s>>>(
+        words, rows, cols, t, reverse, out, tpr);
 }
 
 // ---------------------------------------------------------------------------
@@ -481,13 +558,20 @@ int qadic_pack_rows_u8(const uint8_t* m, int64_t rows, int64_t cols, int32_t k, 
                   "bad pack geometry");
     const int64_t width = (cols + k - 1) / k, total = rows * width;
     if (total == 0) return QADIC_OK;
+    cudaStream_t s = (cudaStream_t)stream;
     if (k <= 8) {
-        const int64_t tpr = (width + PK_WORDS - 1) / PK_WORDS;
-        pack_rows_tile_kernel<<<grid_for_tiles(rows * tpr), PK_THREADS, 0, (cudaStream_t)stream>>>(
-            m, rows, cols, k, t, reverse, words, tpr);
+        switch (k) {
+            case 1: launch_pack_tiles<1>(m, rows, cols, t, reverse, words, s); break;
+            case 2: launch_pack_tiles<2>(m, rows, cols, t, reverse, words, s); break;
+            case 3: launch_pack_tiles<3>(m, rows, cols, t, reverse, words, s); break;
+            case 4: launch_pack_tiles<4>(m, rows, cols, t, reverse, words, s); break;
+            case 5: launch_pack_tiles<5>(m, rows, cols, t, reverse, words, s); break;
+            case 6: launch_pack_tiles<6>(m, rows, cols, t, reverse, words, s); break;
+            case 7: launch_pack_tiles<7>(m, rows, cols, t, reverse, words, s); break;
+            default: launch_pack_tiles<8>(m, rows, cols, t, reverse, words, s); break;
+        }
     } else {
-        pack_rows_kernel<<<blocks_for(total, 256), 256, 0, (cudaStream_t)stream>>>(m, rows, cols, k, t, reverse,
-                                                                                    words);
+        pack_rows_kernel<<<blocks_for(total, 256), 256, 0, s>>>(m, rows, cols, k, t, reverse, words);
     }
     return check_launch("pack_rows_u8", 1);
 }
@@ -497,9 +581,17 @@ int qadic_unpack_rows_u8(const uint64_t* words, int64_t rows, int64_t cols, int3
     QADIC_REQUIRE(rows >= 0 && cols >= 0 && k >= 1 && t >= 1 && t <= 8 * 8, QADIC_ERR_VALUE, "bad unpack geometry");
     if (rows * cols == 0) return QADIC_OK;
     if (k <= 8) {
-        const int64_t width = (cols + k - 1) / k, tpr = (width + PK_WORDS - 1) / PK_WORDS;
-        unpack_rows_tile_kernel<<<grid_for_tiles(rows * tpr), PK_THREADS, 0, (cudaStream_t)stream>>>(
-            words, rows, cols, k, t, reverse, out, tpr);
+        cudaStream_t s = (cudaStream_t)stream;
+        switch (k) {
+            case 1: launch_unpack_tiles<1>(words, rows, cols, t, reverse, out, s); break;
+            case 2: launch_unpack_tiles<2>(words, rows, cols, t, reverse, out, s); break;
+            case 3: launch_unpack_tiles<3>(words, rows, cols, t, reverse, out, s); break;
+            case 4: launch_unpack_tiles<4>(words, rows, cols, t, reverse, out, s); break;
+            case 5: launch_unpack_tiles<5>(words, rows, cols, t, reverse, out, s); break;
+            case 6: launch_unpack_tiles<6>(words, rows, cols, t, reverse, out, s); break;
+            case 7: launch_unpack_tiles<7>(words, rows, cols, t, reverse, out, s); break;
+            default: launch_unpack_tiles<8>(words, rows, cols, t, reverse, out, s); break;
+        }
         return check_launch("unpack_rows_u8", 1);
     }
     unpack_rows_kernel<<<blocks_for(rows * cols, 256), 256, 0, (cudaStream_t)stream>>>(words, rows, cols, k, t,
