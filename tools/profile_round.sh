@@ -11,9 +11,10 @@ mkdir -p $O
 NCU="ncu --clock-control none"
 B="python bench.py --no-cpu-baseline"
 ok=1
-for c in 1 2; do $B --config $c --steps 20 --warmup 5 > $O/bench_cfg$c.json 2>>$O/bench.err || ok=0; done
+for c in 1 2; do $B --config $c --warmup 5 > $O/bench_cfg$c.json 2>>$O/bench.err || ok=0; done
+for c in redq pack; do python bench.py --config $c > $O/bench_$c.json 2>>$O/bench.err || ok=0; done
 for c in 3 4 5; do
-  for e in auto i8 fp4 fp4k; do $B --config $c --engine $e --steps 10 --warmup 3 > $O/bench_cfg${c}_$e.json 2>>$O/bench.err || ok=0; done
+  for e in auto i8 fp4 fp4k; do $B --config $c --engine $e --steps 20 --warmup 3 > $O/bench_cfg${c}_$e.json 2>>$O/bench.err || ok=0; done
 done
 $B --config 3 --engine f64 --steps 3 --warmup 3 > $O/bench_cfg3_f64.json 2>>$O/bench.err || ok=0
 $B --config 5 --engine f64 --steps 3 --warmup 3 > $O/bench_cfg5_f64.json 2>>$O/bench.err || ok=0
@@ -35,6 +36,8 @@ full cfg3_fp4k_gemm 3 auto gemm_modp
 full cfg4_fp4k_gemm 4 auto gemm_modp
 full cfg1_polymul 1 auto polymul
 full cfg2_gf_dot 2 auto gf_dot
+python bench.py --config redq --steps 3 > /dev/null 2>&1 && $NCU --set full -k regex:redq_vec -s 2 -c 1 -o $O/redq -f python bench.py --config redq --steps 3 > $O/redq.log 2>&1
+ncu -i $O/redq.ncu-rep --page raw --csv > $O/redq_raw.csv 2>/dev/null
 full cfg5_i8_gemm 5 i8 gemm_modp
 echo "bench ok=$ok"
 ls -la $O | head -80

@@ -60,7 +60,8 @@ def main():
         r = d.get("roofline") or {}
         lines.append("| %s | %.4f | %.4g %s | %s | %s %s | %s | %.2f | %s |" % (
             os.path.basename(f), d["ms_per_step"], d["value"], d["unit"], r.get("kernel"), r.get("achieved"),
-            r.get("unit"), r.get("frac"), d["e2e"]["ms_per_step"], json.dumps(r.get("kernels_ms_per_step"))))
+            r.get("unit"), r.get("frac"), (d.get("e2e") or {}).get("ms_per_step", float("nan")),
+            json.dumps(r.get("kernels_ms_per_step"))))
     lines += ["", "## ncu (one `--set full` capture per kernel)", "",
               "| capture | " + " | ".join(m[1] for m in METRICS) + " |", "|---" * (len(METRICS) + 1) + "|"]
     traffic = {"_doc": "dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel, from one "
