@@ -15,22 +15,12 @@
 
 namespace qadic {
 
-// exact double of an integer w < 2^52 without the FP64 conversion unit
-QADIC_D double u52_to_f64(uint64_t w) {
-    return __longlong_as_double((long long)(0x4330000000000000ull | w)) - 4503599627370496.0;
-}
-
-QADIC_D uint32_t pack4(uint32_t bytes, int t) {
-    return (bytes & 0xFF) | (((bytes >> 8) & 0xFF) << t) | (((bytes >> 16) & 0xFF) << (2 * t)) |
-           ((bytes >> 24) << (3 * t));
-}
-
 struct PolyConst {
     uint32_t p, t, corr, magic;
     double invp_up, bound;
 };
 
-// ---- cfg1 fast path: k = 4 (degree-3 operands), 16 pairs per thread ----------
+// ---- cfg1 fast path: k = 4 (degree-3 operands), 8 pairs per thread -----------
 // One thread: 8 pairs = 2 x 16 B of a and of b in, 7 x 8 B out -- every HBM
 // access a full vector, no shared memory.  Per pair: DQT-pack both operands
 // in registers, one FP64 product, s = floor(r * RU(1/p)) by a round-down add of

@@ -2,31 +2,34 @@
 //
 // Coefficient-plane formulation of the paper's delayed reduction
 // (PAPER.md:216-223 applied to GFqField.matmul, src/gfext.py:311-345, and
-// cmm.right_cmm, src/cmm.py:244-276):
+// cmm.right_cmm, src/cmm.py:244-276).  Two decompositions:
 //
-//   C[m, (j,l)] = sum_{kk,i} A[m, (kk,i)] * Bx[(j,l), (kk,i)]   (mod p)
-//   Bx[(j,l), (kk,i)] = coefficient l of  X^i * b[kk,j](X)  mod (f, p)
+// * Expanded form (I8, FP4):
+//     C[m, (j,l)] = sum_{kk,i} A[m, (kk,i)] * Bx[(j,l), (kk,i)]   (mod p)
+//     Bx[(j,l), (kk,i)] = coefficient l of  X^i * b[kk,j](X)  mod (f, p)
+//   every B entry expanded once into its k x k multiplication matrix over F_p
+//   with the X^k fold applied (rows X^i mod f, src/gfext.py:200-205): one GEMM
+//   of M x (N k) x (K k).
+// * Evaluation planes (FP4K, the default for p <= 7): S = 2k-1 Toom-Cook points
+//   over F_p (Karatsuba k(k+1)/2 when 2k-1 > p+1); plane s of A and of B is an
+//   F_p-linear combination of the coefficients (a plane-table lookup per element
+//   code), the S plane products are independent F_p GEMMs of M x N x K, and
+//   C_l = sum_s W[l][s] D_s mod p recombines them (separate SWAR pass, or in the
+//   GEMM epilogue for S <= 3).
 //
-// Every B entry is expanded once into its k x k multiplication matrix over
-// F_p with the X^k fold applied (rows X^i mod f, src/gfext.py:200-205).
-// A needs no transformation for the INT8 kind: the row-major uint8[M, K, k]
-// coefficient tensor IS the K-major A operand.  The delayed sum is exact in
-// the accumulator, so the epilogue is a single `mod p` per output.
+// The delayed sum is exact in the accumulator, so no intermediate reduction:
+//   KIND_I8  tcgen05.mma.kind::i8, residues 0..p-1, s32 accumulate; exact while
+//            K*k*(p-1)^2 < 2^31 (any p <= 127).
+//   KIND_F4  tcgen05.mma.kind::mxf4.block_scale (E2M1, two per byte) on residue
+//            representatives that E2M1 holds exactly (half-integer codes under
+//            2^1 block scales, see e2m1_lut); the fp32 accumulator is exact while
+//            K * max|v|^2 < 2^24.  Twice the int8 MMA rate, half the bytes.
 //
-// Two operand kinds share one persistent warp-specialised kernel:
-//   KIND_I8  tcgen05.mma.kind::i8, unsigned residues 0..p-1, s32 accumulate;
-//            exact while K*k*(p-1)^2 < 2^31 (any p <= 127).
-//   KIND_F4  tcgen05.mma.kind::mxf4.block_scale (E2M1, two per byte, block
-//            scales fixed to 2^0) on CENTRED residues in [-(p-1)/2, (p-1)/2];
-//            every such integer for p <= 7 is an exact E2M1 value and the
-//            fp32 accumulator is exact while K*k*((p-1)/2)^2 < 2^24
-//            (cfg3: 16,384; cfg5: 221,184).  Twice the int8 MMA rate, half
-//            the operand bytes.
-//
-// Kernel roles: warp 0 TMA producer (128B-swizzled K-major tiles, 4-stage
-// mbarrier ring), warp 1 single-thread MMA issuer (M=128, K=128 bytes per
-// stage), warp 2 TMEM allocator, warps 4-7 epilogue (tcgen05.ld -> mod p ->
-// uint8) overlapping the next tile through two TMEM accumulators.
+// Kernel roles (gemm_modp_kernel): warp 0 TMA producer (128B-swizzled K-major
+// tiles, up to 8-stage mbarrier ring), warp 1 single-thread MMA issuer (M=256
+// over a CTA pair with cta_group::2, N=240), warp 2 TMEM allocator, warps 4-7
+// (4-11 when fused) epilogue (tcgen05.ld -> mod p -> residues) overlapping the
+// next tile through two TMEM accumulators.
 #include <cuda.h>
 
 #include <utility>
@@ -964,8 +967,6 @@ __host__ __device__ constexpr int combo_second(int k, int s) {
                            : k == 3 ? (s == 3 ? 1 : 2)
                                     : (s == 4 ? 1 : s == 5 ? 2 : s == 6 ? 3 : s == 7 ? 2 : 3));
 }
-
-__device__ __forceinline__ uint32_t byte_of(const uint32_t* in, int idx) { return (in[idx >> 2] >> (8 * (idx & 3))) & 0xFF; }
 
 constexpr int KMAX_S = 8;  // planes per product handled by the nibble transpose
 
