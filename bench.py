@@ -519,7 +519,10 @@ def run_ours(args):
         avg_src = "timed region / K (one launch per step)"
     work = meta["work"]
     if engine == "f64" and cfg in (3, 5):
-        work["f64_fmas"] = work["madds"]
+        # cfg5 runs the one-sided DQT form (two-sided would fold every 8 terms):
+        # k FP64 FMAs per GF mult-add; cfg3 the two-sided form, one FMA each
+        c_ = W.CONFIGS[cfg]
+        work["f64_fmas"] = work["madds"] * (c_.k if cfg == 5 else 1)
     if engine == "f64" and cfg == 4:
         n = W.CONFIGS[4].shape[0]
         work["f64_fmas"] = (n // ws) * n * (-(-n // 3))

@@ -50,7 +50,12 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
-enum Epi { EPI_GF = 0, EPI_CMM = 1 };
+// EPI_GF: two-sided DQT words (both operands packed), REDQ + L/H fold per output.
+// EPI_CMM: right_cmm, corrected digits of B-packed words.
+// EPI_GF1: one-sided DQT (only A packed, B's coefficient planes side by side
+//          in N): corrected digits of each word to a [M][N][k][k] byte buffer
+//          that gf1_combine_kernel turns into coefficients.
+enum Epi { EPI_GF = 0, EPI_CMM = 1, EPI_GF1 = 2 };
 
 struct Params {
     const double* a;  // [Mp, Kp] packed words
@@ -75,7 +80,7 @@ __device__ __forceinline__ double fold_word(double r, const FieldConst& f) {
 
 template <int K, Epi EPI, bool SMEM_TABLES>
 __global__ void __launch_bounds__(THREADS, 1) dmma_gemm_kernel(Params prm, FieldConst f) {
-    constexpr int ND = EPI == EPI_GF ? 2 * K - 2 : 0;
+    constexpr int ND = EPI == EPI_GF ? 2 * K - 2 : (EPI == EPI_GF1 ? K - 1 : 0);
     extern __shared__ __align__(16) uint8_t smem_raw[];
     double* sA = reinterpret_cast<double*>(smem_raw);
     double* sB = sA + STAGES * BM * SA;
@@ -139,7 +144,7 @@ __global__ void __launch_bounds__(THREADS, 1) dmma_gemm_kernel(Params prm, Field
             for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-            if (EPI == EPI_GF && prm.fold) {
+            if ((EPI == EPI_GF || EPI == EPI_GF1) && prm.fold) {
                 const int64_t kdone = (int64_t)kt * BK + (k4 + 1) * 4;
                 if (kdone % prm.fold == 0 && kdone < prm.Kp) {
 #pragma unroll
@@ -183,6 +188,14 @@ __global__ void __launch_bounds__(THREADS, 1) dmma_gemm_kernel(Params prm, Field
                     uint8_t* dst = prm.c + (row * prm.n_out + col) * K;
 #pragma unroll
                     for (int l = 0; l < K; ++l) dst[l] = (uint8_t)(res >> (8 * l));
+                } else if (EPI == EPI_GF1) {
+                    // one-sided word: K corrected digits = P_{i,j} mod p, i = 0..K-1
+                    uint32_t u[ND + 1];
+                    redq_compress_f64<ND>(r, f.invp_up, (double)f.p, f.bound, f.p, (int)f.t, u);
+                    uint8_t* dst = prm.c + row * prm.n_out + col * K;
+#pragma unroll
+                    for (int q = 0; q <= ND; ++q)
+                        dst[q] = (uint8_t)(q < ND ? mod_small(u[q] + f.corr * u[q + 1], f.p, f.magic) : u[q]);
                 } else {
                     // right_cmm: d+1 corrected digits of one word = d+1 output entries
                     const int dd = prm.d;
@@ -234,7 +247,51 @@ __global__ void pack_rows_f64_kernel(const uint8_t* __restrict__ src, int64_t R,
     dst[i] = (double)v;
 }
 
+// one-sided combine: T[m][n][j][i] = (sum_kk a_i b_j) mod p  ->
+// c_s = sum_{i+j=s} T[..][j][i], folded by X^s mod f (gfext.py:200-205) -> k bytes
+template <int K>
+__global__ void gf1_combine_kernel(const uint8_t* __restrict__ T, int64_t total, FieldConst f,
+                                   uint8_t* __restrict__ c) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= total) return;
+    const uint8_t* t = T + e * K * K;
+    uint32_t cs[2 * K - 1];
+#pragma unroll
+    for (int q = 0; q < 2 * K - 1; ++q) cs[q] = 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+#pragma unroll
+        for (int i = 0; i < K; ++i) cs[i + j] += t[j * K + i];
+    uint32_t out[K];
+#pragma unroll
+    for (int l = 0; l < K; ++l) out[l] = 0;
+#pragma unroll
+    for (int q = 0; q < 2 * K - 1; ++q) {
+        const uint32_t v = mod_small(cs[q], f.p, f.magic);
+#pragma unroll
+        for (int l = 0; l < K; ++l) out[l] += v * f.xpow[q][l];
+    }
+#pragma unroll
+    for (int l = 0; l < K; ++l) c[e * K + l] = (uint8_t)mod_small(out[l], f.p, f.magic);
+}
+
 static inline int64_t rup(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+// one-sided parameters: radix 2^t1 with k digits in 53 bits, and the largest
+// fold period (multiple of the DMMA k-step 4) keeping every digit below 2^t1
+struct OneSided {
+    int t1, fold;
+};
+static OneSided one_sided(uint32_t p, int k) {
+    OneSided o;
+    o.t1 = 53 / k;
+    if (o.t1 > 30) o.t1 = 30;
+    const int64_t q = 1ll << o.t1, per = (int64_t)(p - 1) * (p - 1);
+    o.fold = per ? (int)(((q - 1 - (p - 1)) / per) / 4 * 4) : 1 << 30;
+    return o;
+}
+// two-sided fold periods below this make the in-register folds the bottleneck
+constexpr int ONE_SIDED_BELOW = 64;
 
 template <int K, Epi EPI>
 static int launch(const Params& prm, const FieldConst& f, cudaStream_t s) {
@@ -250,10 +307,13 @@ static int launch(const Params& prm, const FieldConst& f, cudaStream_t s) {
 
 }  // namespace f64
 
-size_t f64_gf_workspace(int64_t m, int64_t kdim, int64_t n) {
+size_t f64_gf_workspace(int64_t m, int64_t kdim, int64_t n, int k) {
     using namespace f64;
     const int64_t Mp = rup(m, BM), Kp = rup(kdim, BK), Np = rup(n, BN);
-    return (size_t)(Mp * Kp + Kp * Np) * sizeof(double);
+    const size_t two = (size_t)(Mp * Kp + Kp * Np) * sizeof(double);
+    const int64_t Np1 = rup(n * k, BN);  // one-sided: B planes side by side, plus the digit buffer
+    const size_t one = (size_t)(Mp * Kp + Kp * Np1) * sizeof(double) + (size_t)(m * n * k * k);
+    return two > one ? two : one;
 }
 
 size_t f64_cmm_workspace(int64_t m, int64_t kdim, int64_t n, int d) {
@@ -263,11 +323,68 @@ size_t f64_cmm_workspace(int64_t m, int64_t kdim, int64_t n, int d) {
     return (size_t)(Mp * Kp + Kp * Np) * sizeof(double);
 }
 
+// One-sided DQT (only A's polynomials packed; B's k coefficient planes side by
+// side along N): S[m][(n,j)] = sum_kk W_a[m,kk] b_j[kk,n] has k digits
+// P_{i,j} = sum a_i b_j, so the radix can be 2^(53/k) and a fold is needed only
+// every ~2^(53/k)/(p-1)^2 terms instead of every 2^(53/(2k-1))/(k(p-1)^2) -- k
+// times the DMMA work, but no fold-bound ALU phase (cfg5: fold 3636 vs 9).
+static int f64_gf_matmul_one_sided(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m,
+                                   int64_t kdim, int64_t n, void* ws, uint8_t* c, cudaStream_t s) {
+    using namespace f64;
+    const int k = (int)f.k;
+    const OneSided o = one_sided(f.p, k);
+    FieldConst f1 = f;
+    f1.t = (uint32_t)o.t1;
+    const uint64_t q = 1ull << o.t1;
+    f1.corr = (q % f.p == 0) ? 0u : (uint32_t)((f.p - q % f.p) % f.p);
+    const int64_t Mp = rup(m, BM), Kp = rup(kdim, BK), Np1 = rup(n * k, BN);
+    double* aw = static_cast<double*>(ws);
+    double* bw = aw + Mp * Kp;
+    uint8_t* T = reinterpret_cast<uint8_t*>(bw + Kp * Np1);
+    QADIC_TIMED("f64 pack A", s, pack_gf_kernel<<<(unsigned)((Mp * Kp + 255) / 256), 256, 0, s>>>(a, m, kdim, k, o.t1, aw, Mp, Kp));
+    int rc = check_launch("f64 pack A");
+    if (rc) return rc;
+    // B [K, N, k] read as [K, N*k] single entries: the planes side by side
+    QADIC_TIMED("f64 pack B", s, pack_gf_kernel<<<(unsigned)((Kp * Np1 + 255) / 256), 256, 0, s>>>(b, kdim, n * k, 1, o.t1, bw, Kp, Np1));
+    rc = check_launch("f64 pack B");
+    if (rc) return rc;
+    Params prm;
+    prm.a = aw;
+    prm.b = bw;
+    prm.M = m;
+    prm.Nw = n * k;
+    prm.Kp = Kp;
+    prm.Np = Np1;
+    prm.n_out = n * k * k;
+    prm.fold = kdim > o.fold ? o.fold : 0;
+    prm.d = k - 1;
+    prm.c = T;
+    switch (k) {
+        case 1: rc = launch<1, EPI_GF1>(prm, f1, s); break;
+        case 2: rc = launch<2, EPI_GF1>(prm, f1, s); break;
+        case 3: rc = launch<3, EPI_GF1>(prm, f1, s); break;
+        default: rc = launch<4, EPI_GF1>(prm, f1, s); break;
+    }
+    if (rc) return rc;
+    const int64_t total = m * n;
+    const unsigned blocks = (unsigned)((total + 255) / 256);
+    switch (k) {
+        case 1: QADIC_TIMED("f64 combine", s, gf1_combine_kernel<1><<<blocks, 256, 0, s>>>(T, total, f, c)); break;
+        case 2: QADIC_TIMED("f64 combine", s, gf1_combine_kernel<2><<<blocks, 256, 0, s>>>(T, total, f, c)); break;
+        case 3: QADIC_TIMED("f64 combine", s, gf1_combine_kernel<3><<<blocks, 256, 0, s>>>(T, total, f, c)); break;
+        default: QADIC_TIMED("f64 combine", s, gf1_combine_kernel<4><<<blocks, 256, 0, s>>>(T, total, f, c)); break;
+    }
+    return check_launch("f64 combine");
+}
+
 int f64_gf_matmul(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
                   int fold, void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s) {
     using namespace f64;
     const int64_t Mp = rup(m, BM), Kp = rup(kdim, BK), Np = rup(n, BN);
-    QADIC_REQUIRE(ws && ws_bytes >= f64_gf_workspace(m, kdim, n), QADIC_ERR_VALUE, "workspace too small");
+    QADIC_REQUIRE(ws && ws_bytes >= f64_gf_workspace(m, kdim, n, (int)f.k), QADIC_ERR_VALUE, "workspace too small");
+    const char* env = getenv("QADIC_F64_ONE_SIDED");
+    const bool one = env ? atoi(env) != 0 : (fold > 0 && fold < ONE_SIDED_BELOW && f.k > 1);
+    if (one) return f64_gf_matmul_one_sided(f, a, b, m, kdim, n, ws, c, s);
     double* aw = static_cast<double*>(ws);
     double* bw = aw + Mp * Kp;
     QADIC_TIMED("f64 pack A", s, pack_gf_kernel<<<(unsigned)((Mp * Kp + 255) / 256), 256, 0, s>>>(a, m, kdim, (int)f.k, (int)f.t, aw, Mp, Kp));

@@ -20,7 +20,7 @@ int tc_kara_gf_matmul(const FieldConst& f, const uint8_t* a, const uint8_t* b, i
                       void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s, bool b_ready);
 int tc_kara_right_cmm(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n, uint32_t p, void* ws,
                       size_t ws_bytes, uint8_t* c, cudaStream_t s);
-size_t f64_gf_workspace(int64_t m, int64_t kdim, int64_t n);
+size_t f64_gf_workspace(int64_t m, int64_t kdim, int64_t n, int k);
 size_t f64_cmm_workspace(int64_t m, int64_t kdim, int64_t n, int d);
 int f64_gf_matmul(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
                   int fold, void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s);
@@ -75,7 +75,8 @@ size_t qadic_gf_matmul_workspace(const qadic_field_desc* f, int64_t m, int64_t k
     if (!f || m < 0 || kdim < 0 || n < 0) return 0;
     const int eng = resolve_engine(engine, (uint32_t)f->p, kdim, f->k);
     if (eng == QADIC_ENGINE_F4K_TC) return tc_kara_workspace((uint32_t)f->p, m, kdim, n, f->k);
-    return eng == QADIC_ENGINE_F64_DMMA ? f64_gf_workspace(m, kdim, n) : tc_workspace(tc_kind(eng), m, kdim, n, f->k);
+    return eng == QADIC_ENGINE_F64_DMMA ? f64_gf_workspace(m, kdim, n, f->k)
+                                        : tc_workspace(tc_kind(eng), m, kdim, n, f->k);
 }
 
 int qadic_gf_matmul_u8(const qadic_field_desc* fd, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim,
