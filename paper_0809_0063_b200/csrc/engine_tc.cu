@@ -1551,8 +1551,10 @@ __global__ void __launch_bounds__(256, 4) combine_swar_kernel(const uint8_t* __r
                                                            LaneDiv ld, PlaneSpec ps, uint8_t* __restrict__ c) {
 
     const int64_t chunks = (N + 31) / 32;
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= M * chunks) return;
+    int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool live = idx < M * chunks;
+    if (__all_sync(0xffffffffu, !live)) return;
+    if (!live) idx = M * chunks - 1;  // duplicate the last chunk (identical bytes, warp stays converged)
     const int64_t m = idx / chunks, q = idx % chunks;
     const int64_t j0 = q * 32;
     uint32_t dv[S][4];
@@ -1583,7 +1585,28 @@ __global__ void __launch_bounds__(256, 4) combine_swar_kernel(const uint8_t* __r
         place_coeffs<K>(hi, o + g * 2 * K + K);
     }
     uint8_t* dst = c + (m * N + j0) * K;
-    if (j0 + 32 <= N && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+    // a warp whose 32 chunks are whole and contiguous (same row) stages its
+    // 32 x 32K output bytes in shared memory and stores them as lane-consecutive
+    // 16-byte vectors (each thread's own 32K bytes would be a 32K-byte-strided,
+    // partial-line store pattern)
+    __shared__ __align__(16) uint32_t cstage[256 / 32][32 * 8 * K];
+    const int lane = threadIdx.x & 31;
+    const bool whole = live && j0 + 32 <= N && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0);
+    const int64_t m_lane0 = __shfl_sync(0xffffffffu, m, 0);
+    if (__all_sync(0xffffffffu, whole && m == m_lane0 && N % 32 == 0)) {
+        uint32_t* st = cstage[threadIdx.x >> 5];
+#pragma unroll
+        for (int v = 0; v < 2 * K; ++v)
+            *reinterpret_cast<uint4*>(st + lane * 8 * K + 4 * v) =
+                make_uint4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
+        __syncwarp();
+        uint4* wdst = reinterpret_cast<uint4*>(dst - (int64_t)lane * 32 * K);  // the warp's first chunk
+#pragma unroll
+        for (int v = 0; v < 2 * K; ++v)
+            __stcs(wdst + v * 32 + lane, *reinterpret_cast<const uint4*>(st + (v * 32 + lane) * 4));
+    } else if (!live) {
+        return;
+    } else if (j0 + 32 <= N && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
 #pragma unroll
         for (int v = 0; v < 2 * K; ++v)
             reinterpret_cast<uint4*>(dst)[v] = make_uint4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
