@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(PM_THREADS, 4) polymul_k4_kernel(const uint8_t
     pdl_wait();  // predecessor complete before any global access
     pdl_trigger();
     const int64_t p0 = ((int64_t)blockIdx.x * PM_THREADS + threadIdx.x) * PM_PER;
-    if (p0 >= n) return;
+    if (__all_sync(0xffffffffu, p0 >= n)) return;  // whole warp past the end (warps stay converged)
     uint32_t av[PM_PER], bv[PM_PER];
     const bool full = p0 + PM_PER <= n;
     if (full) {
@@ -108,7 +108,24 @@ __global__ void __launch_bounds__(PM_THREADS, 4) polymul_k4_kernel(const uint8_t
         if (sh > 8) o[w + 2] |= (uint32_t)(v >> (64 - sh));
     }
     uint8_t* dst = out + p0 * 7;
-    if (full && ((reinterpret_cast<uintptr_t>(dst) & 7) == 0)) {
+    // a warp with all its pairs in range stages its 32 x 56 output bytes in shared
+    // memory and stores them as lane-consecutive 16-byte vectors
+    __shared__ __align__(16) uint32_t pstage[PM_THREADS / 32][32 * PM_PER * 7 / 4];
+    const int lane = threadIdx.x & 31;
+    uint8_t* wbase = dst - (int64_t)lane * PM_PER * 7;  // the warp's first output byte
+    if (__all_sync(0xffffffffu, full) && ((reinterpret_cast<uintptr_t>(wbase) & 15) == 0)) {
+        uint32_t* st = pstage[threadIdx.x >> 5];
+#pragma unroll
+        for (int q = 0; q < PM_PER * 7 / 8; ++q)
+            *reinterpret_cast<uint2*>(st + lane * (PM_PER * 7 / 4) + 2 * q) = make_uint2(o[2 * q], o[2 * q + 1]);
+        __syncwarp();
+        constexpr int NV = 32 * PM_PER * 7 / 16;  // 16-byte vectors per warp
+#pragma unroll
+        for (int v = lane; v < NV; v += 32)
+            reinterpret_cast<uint4*>(wbase)[v] = *reinterpret_cast<const uint4*>(st + 4 * v);
+    } else if (p0 >= n) {
+        return;
+    } else if (full && ((reinterpret_cast<uintptr_t>(dst) & 7) == 0)) {
 #pragma unroll
         for (int q = 0; q < PM_PER * 7 / 8; ++q) reinterpret_cast<uint2*>(dst)[q] = make_uint2(o[2 * q], o[2 * q + 1]);
     } else {
