@@ -407,3 +407,51 @@ class TestRightCMM:
         a = np.ones((4, 16), np.int64)
         with pytest.raises(Q.ParamsViolation):
             cmm.right_cmm(a, cmm.compress_rows(np.ones((16, 4), np.int64), prm))
+
+
+# ---------------------------------------------------------------------------
+# C ABI error contract: status codes + qadic_last_error, no launch on bad input
+# ---------------------------------------------------------------------------
+class TestABIErrors:
+    def test_status_codes(self):
+        import ctypes
+
+        import torch
+
+        from paper_0809_0063_b200 import _native as N
+
+        L = N.lib()
+        f = W.field_for(W.CONFIGS[5])
+        desc = f.field_desc()
+        a = torch.zeros((64, 64, 3), dtype=torch.uint8, device="cuda")
+        c = torch.empty((64, 64, 3), dtype=torch.uint8, device="cuda")
+        need = L.qadic_gf_matmul_workspace(desc, 64, 64, 64, 0)
+        ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+        s = N.stream_ptr()
+        # workspace too small
+        rc = L.qadic_gf_matmul_u8(desc, N.ptr(a), N.ptr(a), 64, 64, 64, 0, 0, N.ptr(ws), need // 2, N.ptr(c), s)
+        assert rc == N.ERR_VALUE and b"workspace" in L.qadic_last_error()
+        # unknown engine
+        rc = L.qadic_gf_matmul_u8(desc, N.ptr(a), N.ptr(a), 64, 64, 64, 9, 0, N.ptr(ws), need, N.ptr(c), s)
+        assert rc != N.QADIC_OK
+        # null operand through the host pipeline
+        hneed = L.qadic_gf_matmul_host_workspace(desc, 64, 64, 64, 0, 0)
+        hws = torch.empty(hneed, dtype=torch.uint8, device="cuda")
+        rc = L.qadic_gf_matmul_host_u8(desc, N.ptr(a), None, 64, 64, 64, 0, 0, 0, N.ptr(hws), hneed, N.ptr(c), s)
+        assert rc == N.ERR_VALUE
+        # REDQ digit span beyond the 64-bit word
+        r = torch.zeros(8, dtype=torch.int64, device="cuda")
+        o = torch.zeros((8, 5), dtype=torch.int64, device="cuda")
+        assert L.qadic_redq_compress_u64(N.ptr(r), 8, 3, 16, 4, N.ptr(o), s) == N.ERR_VALUE
+        # packing width out of range; q too small for the digit bound
+        x = torch.zeros((8, 9), dtype=torch.uint8, device="cuda")
+        y = torch.zeros((8, 17), dtype=torch.uint8, device="cuda")
+        assert L.qadic_polymul_batch_u8(N.ptr(x), N.ptr(x), 8, 9, 3, 5, N.ptr(y), s) == N.ERR_UNSUPPORTED
+        assert L.qadic_polymul_batch_u8(N.ptr(x), N.ptr(x), 8, 4, 3, 2, N.ptr(y), s) == N.ERR_PARAMS
+        # field descriptor outside the GPU path
+        bad = N.FieldDesc()
+        ctypes.memmove(ctypes.byref(bad), ctypes.byref(desc), ctypes.sizeof(bad))
+        bad.k = 7
+        assert L.qadic_gf_matmul_u8(ctypes.byref(bad), N.ptr(a), N.ptr(a), 64, 64, 64, 0, 0, N.ptr(ws), need,
+                                    N.ptr(c), s) == N.ERR_UNSUPPORTED
+        torch.cuda.synchronize()
