@@ -124,6 +124,9 @@ struct Params {
     uint32_t lane_m, lane_sh, lane_qmask;  // FUSE_K: per-16-bit-lane division by p (LaneDiv)
     int group_m;                           // FUSE_K: m tiles per raster group
     int diag_noload;     // diagnostics only (QADIC_DIAG_NOLOAD): stages after the first pass skip the TMA
+    // exact uint64 GEMM through byte planes (KIND_I8): C64 = (acc64 ? C64 : 0) + (u32 D << shift)
+    uint64_t* c64;
+    int shift, acc64;
 };
 
 // tile index -> (plane, m tile, n tile).  Unfused: planes outermost.  Fused:
@@ -450,6 +453,28 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                 tmem_ld_wait();
                 const int64_t col0 = (int64_t)nt * BN + ch * 16;
                 if (!row_ok || col0 >= prm.N) continue;
+                if (KIND == KIND_I8 && prm.c64 != nullptr) {  // byte-plane uint64 GEMM (mod 2^64)
+                    uint64_t* crow64 = prm.c64 + row * prm.ldc + col0;
+                    const int ncol = (int)(prm.N - col0 < 16 ? prm.N - col0 : 16);
+                    if (ncol == 16 && ((reinterpret_cast<uintptr_t>(crow64) & 15) == 0)) {
+#pragma unroll
+                        for (int e = 0; e < 16; e += 2) {
+                            ulonglong2 o = make_ulonglong2((uint64_t)v[e] << prm.shift, (uint64_t)v[e + 1] << prm.shift);
+                            if (prm.acc64) {
+                                const ulonglong2 old = *reinterpret_cast<const ulonglong2*>(crow64 + e);
+                                o.x += old.x;
+                                o.y += old.y;
+                            }
+                            *reinterpret_cast<ulonglong2*>(crow64 + e) = o;
+                        }
+                    } else {
+                        for (int e = 0; e < ncol; ++e) {
+                            const uint64_t o = (uint64_t)v[e] << prm.shift;
+                            crow64[e] = prm.acc64 ? crow64[e] + o : o;
+                        }
+                    }
+                    continue;
+                }
                 uint32_t r[16];
 #pragma unroll
                 for (int e = 0; e < 16; ++e) {
@@ -1821,7 +1846,110 @@ static int run_kara(const FieldConst& f, const uint8_t* a, const uint8_t* b, int
     return check_launch("fp4k combine");
 }
 
+// ---------------------------------------------------------------------------
+// Exact uint64 GEMM (Layer K matmul_exact_u64, wraps mod 2^64) on INT8 tensor
+// cores through byte planes.  With a = sum_i a_i 256^i, b = sum_j b_j 256^j:
+//   C = sum_{s=0..7} 256^s D_s  (mod 2^64),   D_s = sum_{i+j=s} A_i B_j.
+// The uint64 A matrix read as bytes IS the K-major operand A8 [M][8K] (byte i of
+// element k at 8k+i); each D_s is ONE u8 x u8 GEMM of K'' = 8K against
+// B^(s) [N][8K] with B^(s)[n][8k+i] = byte_{s-i}(B[k][n]) (0 when i > s), i.e.
+// the 8 bytes bswap(B[k][n]) >> 8(7-s).  Only D_s mod 2^(64-8s) matters: exact
+// in the u32 view of the s32 accumulator for s <= 3 while 4 * Kc * 255^2 < 2^32
+// (K chunks of <= 16384), and the accumulator's wrap-around is exactly the
+// needed mod 2^32 for s >= 4.  The epilogue adds D_s << 8s into C (uint64).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) u64_bplanes_kernel(const uint64_t* __restrict__ b, int64_t K, int64_t N,
+                                                           int64_t k0, int64_t kc, uint8_t* __restrict__ out,
+                                                           int64_t ld, int64_t plane_stride) {
+    __shared__ uint64_t tile[32][33];
+    const int64_t n0 = (int64_t)blockIdx.x * 32, kk0 = k0 + (int64_t)blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps
+#pragma unroll
+    for (int r = ty; r < 32; r += 8) {
+        const int64_t k = kk0 + r, n = n0 + tx;
+        tile[r][tx] = (k < k0 + kc && n < N) ? b[k * N + n] : 0ull;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = ty; r < 32; r += 8) {  // output row n = n0 + r, 32 k values (lane tx)
+        const int64_t n = n0 + r, k = kk0 + tx;
+        if (n >= N || k >= k0 + kc) continue;
+        const uint64_t v = tile[tx][r];
+        const uint64_t rv = ((uint64_t)__byte_perm((uint32_t)v, 0, 0x0123) << 32) |
+                            __byte_perm((uint32_t)(v >> 32), 0, 0x0123);  // bswap64
+        uint64_t* dst = reinterpret_cast<uint64_t*>(out + n * ld) + (k - k0);
+#pragma unroll
+        for (int sp = 0; sp < 8; ++sp) dst[sp * plane_stride / 8] = rv >> (8 * (7 - sp));
+    }
+}
+
 }  // namespace tc
+
+bool tc_u64_ok(int64_t m, int64_t k, int64_t n, const void* a) {
+    return m >= 128 && n >= 128 && k >= 16 && (k % 2 == 0) && ((reinterpret_cast<uintptr_t>(a) & 15) == 0);
+}
+
+int tc_matmul_u64(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_t m, int64_t k, int64_t n,
+                  cudaStream_t s) {
+    using namespace tc;
+    constexpr int64_t KC = 16384;  // 4 * KC * 255^2 < 2^32
+    const int64_t kc_max = k < KC ? k : KC;
+    const int64_t ld = 8 * kc_max;  // bytes per B^(s) row (8 * kc_max is a multiple of 16)
+    const size_t plane = (size_t)n * ld;
+    uint8_t* bs = nullptr;
+    static bool pool_kept = false;  // keep freed blocks in the stream-ordered pool across calls
+    if (!pool_kept) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        cudaGetLastError();
+        pool_kept = true;
+    }
+    if (cudaMallocAsync(reinterpret_cast<void**>(&bs), 8 * plane, s) != cudaSuccess) {
+        cudaGetLastError();
+        set_error(QADIC_ERR_CUDA, "matmul_exact_u64: cannot allocate %zu bytes of byte planes", 8 * plane);
+        return QADIC_ERR_CUDA;
+    }
+    const bool pair = pair_mode();
+    constexpr int BN = Cfg<KIND_I8>::BN;
+    int rc = QADIC_OK;
+    for (int64_t k0 = 0; k0 < k && rc == QADIC_OK; k0 += KC) {
+        const int64_t kc = (k - k0 < KC) ? k - k0 : KC;
+        dim3 grid((unsigned)((n + 31) / 32), (unsigned)((kc + 31) / 32));
+        QADIC_TIMED("u64 byte planes", s, u64_bplanes_kernel<<<grid, 256, 0, s>>>(b, k, n, k0, kc, bs, ld, plane));
+        rc = check_launch("u64 byte planes");
+        if (rc) break;
+        CUtensorMap ta, tb;
+        rc = make_tmap(&ta, reinterpret_cast<const uint8_t*>(a) + 8 * k0, 8 * kc, m, 8 * k, BM);
+        if (rc) break;
+        for (int sp = 0; sp < 8 && rc == QADIC_OK; ++sp) {
+            rc = make_tmap(&tb, bs + sp * plane, 8 * kc, n, ld, pair ? BN / 2 : BN);
+            if (rc) break;
+            Params prm = {};
+            prm.M = m;
+            prm.N = n;
+            prm.ldc = n;
+            prm.p = 2;
+            prm.m_tiles = (int)((m + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM));
+            prm.n_tiles = (int)((n + BN - 1) / BN);
+            prm.n_full = (int)(n / BN);
+            prm.num_kb = (int)((8 * kc + BK - 1) / BK);
+            prm.planes = 1;
+            prm.group_m = GROUP_M;
+            prm.c64 = c;
+            prm.shift = 8 * sp;
+            prm.acc64 = (sp > 0 || k0 > 0) ? 1 : 0;
+            rc = pair ? launch_gemm<KIND_I8, true>(ta, tb, prm, s, "u64 byte-plane gemm")
+                      : launch_gemm<KIND_I8, false>(ta, tb, prm, s, "u64 byte-plane gemm");
+        }
+    }
+    cudaFreeAsync(bs, s);
+    return rc;
+}
 
 // planes of the decomposition plan_planes() picks (Toom-Cook when 2k-1 <= p+1)
 static int kara_planes(uint32_t p, int k) { return (2 * k - 1 <= (int)p + 1) ? 2 * k - 1 : k * (k + 1) / 2; }

@@ -15,6 +15,10 @@
 
 namespace qadic {
 
+bool tc_u64_ok(int64_t m, int64_t k, int64_t n, const void* a);
+int tc_matmul_u64(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_t m, int64_t k, int64_t n,
+                  cudaStream_t s);
+
 // ---------------------------------------------------------------------------
 // uint64 GEMM, wraps mod 2^64 (_speed.pyx:15-30).  64x64 tile, 4x4 per thread.
 // ---------------------------------------------------------------------------
@@ -469,6 +473,8 @@ int qadic_matmul_exact_u64(const uint64_t* a, const uint64_t* b, uint64_t* c, in
         cudaMemsetAsync(c, 0, (size_t)(m * n) * sizeof(uint64_t), s);
         return check_launch("matmul_exact_u64 (memset)");
     }
+    if (tc_u64_ok(m, k, n, a) && !(getenv("QADIC_U64_SIMT") && atoi(getenv("QADIC_U64_SIMT")) != 0))
+        return tc_matmul_u64(a, b, c, m, k, n, s);  // INT8 tensor cores on byte planes
     dim3 grid(blocks_for(n, MM_T), blocks_for(m, MM_T));
     QADIC_REQUIRE(grid.y <= 65535, QADIC_ERR_UNSUPPORTED, "m too large for this kernel");
     mm_wrap_kernel<uint64_t><<<grid, 256, 0, s>>>(a, b, c, m, k, n, 0, 0);

@@ -39,6 +39,18 @@ class TestLayerK:
             b = rng.integers(0, 1 << 63, (k, n), dtype=np.uint64)
             assert np.array_equal(_kernels.matmul_exact_u64(a, b), O.matmul_exact_u64(a, b))
 
+    @pytest.mark.parametrize("m,k,n", [(128, 16, 128), (256, 64, 256), (300, 1000, 129), (130, 17000, 140),
+                                        (513, 200, 1024)])
+    def test_matmul_u64_tensor_core_path(self, m, k, n):
+        """the INT8 byte-plane path (tc_matmul_u64): full-range words (wrap mod 2^64),
+        K chunks above 16384, ragged M/N, against numpy's uint64 matmul."""
+        rng = np.random.default_rng(m + k + n)
+        a = rng.integers(0, 1 << 64, (m, k), dtype=np.uint64)
+        b = rng.integers(0, 1 << 64, (k, n), dtype=np.uint64)
+        assert np.array_equal(_kernels.matmul_exact_u64(a, b), O.matmul_exact_u64(a, b))
+        small = rng.integers(0, 1 << 20, (m, k), dtype=np.uint64)  # typical packed words
+        assert np.array_equal(_kernels.matmul_exact_u64(small, b), O.matmul_exact_u64(small, b))
+
     def test_matmul_mod(self, golden):
         for chunk in (7, 64, 10**6):
             c = _kernels.matmul_mod_i64(golden["k_mm_mod_a"], golden["k_mm_mod_b"], 7, chunk)
