@@ -7,16 +7,20 @@ multiply-back decrement above it.  This module computes the two constants the
 kernels take (RU(1/p), B) and restates the scalar procedure.
 
 Reference: /root/reference/pkg/src/qadic/fdiv.py:166-180 (native_reciprocal),
-:250-260 (bounds), :317-363 (precompute_inverses / applied_fdiv).  The
-small-mantissa simulator and exhaustive scans of the reference are
-certification tooling, out of scope here.
+:183-210 (fdiv), :218-295 (the mode-pair case table), :298-363
+(precompute_inverses / applied_fdiv).  The "sim" backend here is a restatement
+of the beta-bit rounding (exact rationals, ties to even) so the reference's
+default-backend calls keep working; the exhaustive scans of the reference are
+certification tooling, out of scope.
 """
 
 from __future__ import annotations
 
 import enum
 import math
+from dataclasses import dataclass, field
 from fractions import Fraction
+from typing import Optional
 
 NATIVE_BETA = 53
 
@@ -47,12 +51,194 @@ def case2_bound(beta: int = NATIVE_BETA) -> int:
     return math.ceil(Fraction(1 << (2 * beta), 3 * (1 << beta) + 2))
 
 
-def applied_fdiv(r: int, p: int) -> int:
-    """floor(r/p) for 0 <= r < 2^53 by the reciprocal product plus the
-    (cold) multiply-back test -- the scalar twin of qadic::fdiv_floor."""
-    if not 0 <= r < 1 << NATIVE_BETA:
+# ---------------------------------------------------------------------------
+# beta-bit binary floats (the reference's "sim" backend, fdiv.py:63-160)
+# ---------------------------------------------------------------------------
+@dataclass(frozen=True)
+class SimFloat:
+    """sign * mantissa * 2**exponent, mantissa normalised to beta bits (or zero)."""
+
+    sign: int
+    mantissa: int
+    exponent: int
+    beta: int
+
+    @property
+    def is_zero(self) -> bool:
+        return self.mantissa == 0
+
+    def as_fraction(self) -> Fraction:
+        if self.is_zero:
+            return Fraction(0)
+        return self.sign * Fraction(self.mantissa) * Fraction(2) ** self.exponent
+
+    def __float__(self) -> float:
+        return float(self.as_fraction())
+
+    def floor(self) -> int:
+        return math.floor(self.as_fraction())
+
+
+def _round_positive(x: Fraction, beta: int, mode: RoundingMode) -> SimFloat:
+    """x > 0 correctly rounded to beta significant bits (nearest: ties to even)."""
+    e = x.numerator.bit_length() - x.denominator.bit_length() - beta
+    while True:  # scale so that floor(x / 2^e) has exactly beta bits
+        q = x / (Fraction(2) ** e)
+        m = q.numerator // q.denominator
+        if m >= 1 << beta:
+            e += 1
+        elif m < 1 << (beta - 1):
+            e -= 1
+        else:
+            break
+    frac = q - m
+    if frac:
+        if mode is UP or (mode is NEAREST and (frac > Fraction(1, 2) or (frac == Fraction(1, 2) and m & 1))):
+            m += 1
+    if m == 1 << beta:
+        m, e = m >> 1, e + 1
+    return SimFloat(1, m, e, beta)
+
+
+def sim_div(r: int, p: int, mode: RoundingMode, beta: int) -> SimFloat:
+    if r < 0 or p < 1:
+        raise ValueError("need r >= 0 and p >= 1")
+    return SimFloat(0, 0, 0, beta) if r == 0 else _round_positive(Fraction(r, p), beta, mode)
+
+
+def sim_reciprocal(p: int, mode: RoundingMode, beta: int) -> SimFloat:
+    return _round_positive(Fraction(1, p), beta, mode)
+
+
+def sim_mul_int(f: SimFloat, r: int, mode: RoundingMode) -> SimFloat:
+    """f * r rounded to f's precision."""
+    if f.is_zero or r == 0:
+        return SimFloat(0, 0, 0, f.beta)
+    if r < 0:
+        raise ValueError("only nonnegative products occur")
+    return _round_positive(f.as_fraction() * r, f.beta, mode)
+
+
+def fdiv(r: int, p: int, mode1: RoundingMode, mode2: RoundingMode, beta: int = NATIVE_BETA,
+         backend: str = "sim") -> int:
+    """floor(round2(r * round1(1/p))): within [k-1, k+1] of k = r // p."""
+    if not 0 <= r < (1 << beta) or not 1 <= p < (1 << beta):
+        raise ValueError("r and p must fit the mantissa range")
+    if backend == "sim":
+        return sim_mul_int(sim_reciprocal(p, mode1, beta), r, mode2).floor()
+    if backend == "native":
+        if beta != NATIVE_BETA:
+            raise ValueError("native backend is fixed at beta=53")
+        if mode2 is not NEAREST:
+            raise ValueError("native multiplication only rounds to nearest; use the sim backend")
+        return math.floor(r * native_reciprocal(p, mode1))
+    raise ValueError(f"unknown backend {backend!r}")
+
+
+# ---------------------------------------------------------------------------
+# the mode-pair table (PAPER.md:627-663): result range around k = r // p and the
+# strict bound on r below which the result never exceeds k
+# ---------------------------------------------------------------------------
+_MODE_ORDER = (UP, NEAREST, DOWN)  # round1 major, round2 minor
+
+
+@dataclass(frozen=True)
+class CaseSpec:
+    case_id: int
+    mode1: RoundingMode
+    mode2: RoundingMode
+    range_lo: int
+    range_hi: int
+    bound_on_r: Optional[Fraction]
+    lost_bits: int
+
+    def bound_threshold(self) -> Optional[int]:
+        """Largest integer r strictly below bound_on_r (None: no bound needed)."""
+        return None if self.bound_on_r is None else math.ceil(self.bound_on_r) - 1
+
+
+def case_id_of(mode1: RoundingMode, mode2: RoundingMode) -> int:
+    return 3 * _MODE_ORDER.index(mode1) + _MODE_ORDER.index(mode2) + 1
+
+
+def _case_bound(cid: int, beta: int) -> Optional[Fraction]:
+    two_b = Fraction(2) ** beta
+    if cid == 1:
+        return two_b / (4 + Fraction(2) ** (2 - beta))
+    if cid in (2, 4):
+        return two_b / (3 + Fraction(2) ** (1 - beta))
+    if cid in (3, 7):
+        return two_b / 2
+    if cid == 5:
+        return (two_b / 2) / (1 + Fraction(2) ** (-1 - beta))
+    return None
+
+
+def case_spec(mode1: RoundingMode, mode2: RoundingMode, beta: int = NATIVE_BETA) -> CaseSpec:
+    cid = case_id_of(mode1, mode2)
+    lo, hi = {1: (0, 1), 2: (0, 1), 3: (0, 1), 4: (0, 1), 5: (-1, 1), 6: (-1, 0), 7: (-1, 1), 8: (-1, 0),
+              9: (-1, 0)}[cid]
+    lost = {1: 3, 2: 2, 3: 1, 4: 2, 5: 2, 6: 0, 7: 1, 8: 0, 9: 0}[cid]
+    return CaseSpec(cid, mode1, mode2, lo, hi, _case_bound(cid, beta), lost)
+
+
+def case_spec_by_id(case_id: int, beta: int = NATIVE_BETA) -> CaseSpec:
+    if not 1 <= case_id <= 9:
+        raise ValueError("case_id must be 1..9")
+    return case_spec(_MODE_ORDER[(case_id - 1) // 3], _MODE_ORDER[(case_id - 1) % 3], beta)
+
+
+# ---------------------------------------------------------------------------
+# always-exact quotients (Alg. 4, PAPER.md:849-875)
+# ---------------------------------------------------------------------------
+# reciprocal mode paired with each multiplication mode so the result is never
+# below k (cases 4, 2, 3): one multiply-back decrement makes it exact
+_PAIRED_MODE1 = {UP: NEAREST, NEAREST: UP, DOWN: UP}
+
+
+@dataclass(frozen=True)
+class InversePack:
+    p: int
+    beta: int
+    backend: str
+    invp: dict = field(default_factory=dict)
+    bound: dict = field(default_factory=dict)  # mode2 -> first r that needs the multiply-back test
+
+
+def precompute_inverses(p: int, backend: str = "sim", beta: int = NATIVE_BETA) -> InversePack:
+    if not 1 <= p < (1 << beta):
+        raise ValueError("p out of range")
+    invp, bound = {}, {}
+    for mode2 in _MODE_ORDER:
+        mode1 = _PAIRED_MODE1[mode2]
+        if backend == "sim":
+            invp[mode2] = sim_reciprocal(p, mode1, beta)
+        elif backend == "native":
+            invp[mode2] = native_reciprocal(p, mode1)
+        else:
+            raise ValueError(f"unknown backend {backend!r}")
+        bound[mode2] = case_spec(mode1, mode2, beta).bound_threshold() + 1
+    return InversePack(p, beta, backend, invp, bound)
+
+
+def applied_fdiv(r: int, p: int, active_mode2: RoundingMode = NEAREST, inv: Optional[InversePack] = None,
+                 backend: str = "native", beta: int = NATIVE_BETA) -> int:
+    """Exactly floor(r/p): the reciprocal product plus the multiply-back test
+    (taken only once r reaches the pair's bound) -- the scalar twin of
+    qadic::fdiv_floor.  Defaults to the GPU's pair (RU reciprocal, nearest
+    product, native doubles); the reference's positional (r, p, mode2, inv)
+    calls and its "sim" backend work unchanged."""
+    if inv is None:
+        inv = precompute_inverses(p, backend=backend, beta=beta)
+    if not 0 <= r < (1 << inv.beta):
         raise ValueError("r out of range")
-    y = math.floor(r * native_reciprocal(p, UP))
-    if r >= case2_bound() and p * y > r:
+    f = inv.invp[active_mode2]
+    if inv.backend == "sim":
+        y = sim_mul_int(f, r, active_mode2).floor()
+    else:
+        if active_mode2 is not NEAREST:
+            raise ValueError("native multiplication only rounds to nearest")
+        y = math.floor(r * f)
+    if r >= inv.bound[active_mode2] and p * y > r:
         y -= 1
     return y

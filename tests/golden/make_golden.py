@@ -85,6 +85,21 @@ def main() -> None:
     sc["fdiv_bound_nearest"] = int(inv.bound[fdiv.NEAREST])
     sc["fdiv_invp3_up"] = float(fdiv.native_reciprocal(3, fdiv.UP)).hex()
     sc["fdiv_invp7_up"] = float(fdiv.native_reciprocal(7, fdiv.UP)).hex()
+    # the mode-pair case table and sampled fdiv / applied_fdiv results at small betas
+    modes = (fdiv.UP, fdiv.NEAREST, fdiv.DOWN)
+    sc["fdiv_cases"] = {str(cid): [fdiv.case_spec_by_id(cid, b).bound_threshold() for b in (8, 12, 53)]
+                        for cid in range(1, 10)}
+    fr = np.random.default_rng(17)
+    samples = []
+    for beta in (8, 11, 16, 53):
+        for _ in range(300):
+            p = int(fr.integers(1, min(1 << beta, 2000)))
+            r = int(fr.integers(0, 1 << min(beta, 62))) % (1 << beta)
+            row = [beta, r, p] + [fdiv.fdiv(r, p, m1, m2, beta) for m1 in modes for m2 in modes]
+            inv = fdiv.precompute_inverses(p, beta=beta)
+            row += [fdiv.applied_fdiv(r, p, m2, inv) for m2 in modes] + [inv.bound[m2] for m2 in modes]
+            samples.append(row)
+    sc["fdiv_samples"] = samples
 
     # ---- params --------------------------------------------------------------
     sc["params"] = {

@@ -90,6 +90,21 @@ class TestParams:
         for r in rng.integers(0, 1 << 53, 3000).tolist():
             assert fdiv.applied_fdiv(r, 7) == r // 7
 
+    def test_fdiv_case_table_and_sim_backend(self, golden_scalars):
+        """the nine mode pairs (bound thresholds at beta 8/12/53) and fdiv /
+        precompute_inverses / applied_fdiv on the reference's default "sim"
+        backend, against values produced by the reference (make_golden.py)."""
+        for cid, bounds in golden_scalars["fdiv_cases"].items():
+            assert [fdiv.case_spec_by_id(int(cid), b).bound_threshold() for b in (8, 12, 53)] == bounds
+        modes = (fdiv.UP, fdiv.NEAREST, fdiv.DOWN)
+        for row in golden_scalars["fdiv_samples"]:
+            beta, r, p = row[:3]
+            got = [fdiv.fdiv(r, p, m1, m2, beta) for m1 in modes for m2 in modes]
+            inv = fdiv.precompute_inverses(p, beta=beta)
+            got += [fdiv.applied_fdiv(r, p, m2, inv) for m2 in modes] + [inv.bound[m2] for m2 in modes]
+            assert got == row[3:], (beta, r, p)
+            assert got[9:12] == [r // p] * 3
+
 
 class TestFields:
     @pytest.mark.parametrize("name", ["gf9_64", "gf9_8192", "gf343_9", "gf9_auto", "gf25_20", "gf27_20",
