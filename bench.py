@@ -648,15 +648,16 @@ def run_primitive(args, kind):
     ms = e0.elapsed_time(e1) / steps
     launches = N.launch_count() - launches0
     peaks, peak_src = load_peaks()
-    if byts is None:  # tensor-bound: the byte-plane GEMMs issue 8 x 8 int8 MACs per uint64 MAC
-        ops = 2 * 64 * units
+    if byts is None:  # tensor-bound: nplanes GEMMs of nb-byte rows = nplanes * nb int8 MACs per uint64 MAC
+        nb = -(-PRIMS["mm64"]["bits"] // 8)
+        ops = 2 * min(2 * nb - 1, 8) * nb * units
         achieved_t = ops / (ms / 1e3) / 1e12
         roof = {"bound": "tensor", "kernel": kname, "achieved": round(achieved_t, 1), "peak": 4500.0,
                 "unit": "TOP/s", "frac": round(achieved_t / 4500.0, 4), "traffic": None,
                 "avg_launch_ms": round(ms, 4), "algorithmic_ops_per_launch": ops,
-                "avg_launch_source": "timed region / K (one call per step: 1 byte-plane kernel + 8 GEMMs)",
-                "peak_source": "fallback nominal dense int8 4.5 POP/s (B200_PROFILING.md); 36 of the 64 "
-                               "byte products per uint64 MAC are nonzero"}
+                "avg_launch_source": "timed region / K (one call per step: byte planes + one GEMM per plane)",
+                "peak_source": "fallback nominal dense int8 4.5 POP/s (B200_PROFILING.md); ops = the int8 "
+                               "MACs the trimmed byte-plane GEMMs issue"}
     else:
         achieved = byts / (ms / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],

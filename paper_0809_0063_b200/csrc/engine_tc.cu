@@ -1859,9 +1859,13 @@ static int run_kara(const FieldConst& f, const uint8_t* a, const uint8_t* b, int
 // needed mod 2^32 for s >= 4.  The epilogue adds D_s << 8s into C (uint64).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) u64_bplanes_kernel(const uint64_t* __restrict__ b, int64_t K, int64_t N,
-                                                           int64_t k0, int64_t kc, uint8_t* __restrict__ out,
-                                                           int64_t ld, int64_t plane_stride) {
+                                                           int64_t k0, int64_t kc, int nba, int nplanes,
+                                                           uint8_t* __restrict__ out, int64_t ld,
+                                                           int64_t plane_stride) {
+    // B^(s)[n][nba*(k-k0) + i] = byte i of bswap(B[k][n]) >> 8(7-s) = byte_{s-i}(B[k][n]), i < nba;
+    // a warp's 32 consecutive k of one row n form nba*32 contiguous bytes (staged, 16-byte stores)
     __shared__ uint64_t tile[32][33];
+    __shared__ __align__(16) uint8_t stage[8][8 * 32];
     const int64_t n0 = (int64_t)blockIdx.x * 32, kk0 = k0 + (int64_t)blockIdx.y * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps
 #pragma unroll
@@ -1870,17 +1874,52 @@ __global__ void __launch_bounds__(256) u64_bplanes_kernel(const uint64_t* __rest
         tile[r][tx] = (k < k0 + kc && n < N) ? b[k * N + n] : 0ull;
     }
     __syncthreads();
-#pragma unroll
-    for (int r = ty; r < 32; r += 8) {  // output row n = n0 + r, 32 k values (lane tx)
-        const int64_t n = n0 + r, k = kk0 + tx;
-        if (n >= N || k >= k0 + kc) continue;
+    const int64_t kvalid = (k0 + kc - kk0) < 32 ? (k0 + kc - kk0) : 32;  // k of this tile in the chunk
+    for (int r = ty; r < 32; r += 8) {  // output row n = n0 + r; lane tx = k offset
+        const int64_t n = n0 + r;
+        if (n >= N) continue;
         const uint64_t v = tile[tx][r];
         const uint64_t rv = ((uint64_t)__byte_perm((uint32_t)v, 0, 0x0123) << 32) |
                             __byte_perm((uint32_t)(v >> 32), 0, 0x0123);  // bswap64
-        uint64_t* dst = reinterpret_cast<uint64_t*>(out + n * ld) + (k - k0);
-#pragma unroll
-        for (int sp = 0; sp < 8; ++sp) dst[sp * plane_stride / 8] = rv >> (8 * (7 - sp));
+        uint8_t* rowp = out + n * ld + nba * (kk0 - k0);
+        const int nbytes = nba * (int)kvalid;
+        for (int sp = 0; sp < nplanes; ++sp) {
+            const uint64_t w = rv >> (8 * (7 - sp));
+            uint8_t* st = stage[ty];
+            for (int i = 0; i < nba; ++i) st[tx * nba + i] = (uint8_t)(w >> (8 * i));
+            __syncwarp();
+            uint8_t* dst = rowp + sp * plane_stride;
+            const bool vec = ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) && (nbytes % 16 == 0);
+            if (vec) {
+                for (int q = tx; q < nbytes / 16; q += 32)
+                    reinterpret_cast<uint4*>(dst)[q] = reinterpret_cast<const uint4*>(st)[q];
+            } else {
+                for (int q = tx; q < nbytes; q += 32) dst[q] = st[q];
+            }
+            __syncwarp();
+        }
     }
+}
+
+// A [M][K] uint64 -> its low nba bytes per element, rows of ld bytes
+__global__ void u64_compact_kernel(const uint64_t* __restrict__ a, int64_t M, int64_t K, int nba,
+                                   uint8_t* __restrict__ out, int64_t ld) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M * K) return;
+    const int64_t r = i / K, k = i % K;
+    const uint64_t v = a[i];
+    uint8_t* dst = out + r * ld + (int64_t)nba * k;
+    for (int q = 0; q < nba; ++q) dst[q] = (uint8_t)(v >> (8 * q));
+}
+
+// OR of every word (significant byte count of the operand)
+__global__ void u64_or_kernel(const uint64_t* __restrict__ x, int64_t n, unsigned long long* __restrict__ acc) {
+    uint64_t v = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        v |= x[i];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v |= __shfl_xor_sync(0xffffffffu, v, off);
+    if ((threadIdx.x & 31) == 0 && v) atomicOr(acc, (unsigned long long)v);
 }
 
 }  // namespace tc
@@ -1889,15 +1928,18 @@ bool tc_u64_ok(int64_t m, int64_t k, int64_t n, const void* a) {
     return m >= 128 && n >= 128 && k >= 16 && (k % 2 == 0) && ((reinterpret_cast<uintptr_t>(a) & 15) == 0);
 }
 
+static int sig_bytes(uint64_t v) {
+    int nb = 1;
+    while (nb < 8 && (v >> (8 * nb))) ++nb;
+    return nb;
+}
+
 int tc_matmul_u64(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_t m, int64_t k, int64_t n,
                   cudaStream_t s) {
     using namespace tc;
     constexpr int64_t KC = 16384;  // 4 * KC * 255^2 < 2^32
-    const int64_t kc_max = k < KC ? k : KC;
-    const int64_t ld = 8 * kc_max;  // bytes per B^(s) row (8 * kc_max is a multiple of 16)
-    const size_t plane = (size_t)n * ld;
-    uint8_t* bs = nullptr;
     static bool pool_kept = false;  // keep freed blocks in the stream-ordered pool across calls
+    static unsigned long long* host_or = nullptr;
     if (!pool_kept) {
         int dev = 0;
         cudaGetDevice(&dev);
@@ -1906,28 +1948,65 @@ int tc_matmul_u64(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_t m, 
             uint64_t keep = ~0ull;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
         }
+        cudaHostAlloc(reinterpret_cast<void**>(&host_or), 2 * sizeof(unsigned long long), cudaHostAllocDefault);
         cudaGetLastError();
         pool_kept = true;
     }
-    if (cudaMallocAsync(reinterpret_cast<void**>(&bs), 8 * plane, s) != cudaSuccess) {
+    // significant bytes of each operand: only byte planes that can be nonzero are multiplied
+    // (packed words of the reference's drivers have 5 -- 34 bits at cfg3 -- instead of 8)
+    // (one stream synchronisation; skipped -- all 8 bytes -- while the stream is being captured)
+    unsigned long long* dor = nullptr;
+    int nba = 8, nbb = 8;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cap);
+    if (host_or && cap == cudaStreamCaptureStatusNone &&
+        cudaMallocAsync(reinterpret_cast<void**>(&dor), 2 * sizeof(unsigned long long), s) == cudaSuccess) {
+        cudaMemsetAsync(dor, 0, 2 * sizeof(unsigned long long), s);
+        QADIC_TIMED("u64 or", s, u64_or_kernel<<<1024, 256, 0, s>>>(a, m * k, dor));
+        QADIC_TIMED("u64 or", s, u64_or_kernel<<<1024, 256, 0, s>>>(b, k * n, dor + 1));
+        cudaMemcpyAsync(host_or, dor, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+        cudaFreeAsync(dor, s);
+        if (cudaStreamSynchronize(s) == cudaSuccess) {
+            nba = sig_bytes(host_or[0]);
+            nbb = sig_bytes(host_or[1]);
+        }
         cudaGetLastError();
-        set_error(QADIC_ERR_CUDA, "matmul_exact_u64: cannot allocate %zu bytes of byte planes", 8 * plane);
+    }
+    const int nplanes = nba + nbb - 1 < 8 ? nba + nbb - 1 : 8;  // shifts 8s >= 64 vanish mod 2^64
+    const int64_t kc_max = k < KC ? k : KC;
+    const int64_t ld = (nba * kc_max + 15) / 16 * 16;  // bytes per B^(s) row
+    const size_t plane = (size_t)n * ld;
+    const int64_t lda = nba == 8 ? 8 * k : (nba * k + 15) / 16 * 16;
+    const size_t abytes = nba == 8 ? 0 : (size_t)m * lda;
+    uint8_t* bs = nullptr;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&bs), nplanes * plane + abytes, s) != cudaSuccess) {
+        cudaGetLastError();
+        set_error(QADIC_ERR_CUDA, "matmul_exact_u64: cannot allocate %zu bytes of byte planes",
+                  nplanes * plane + abytes);
         return QADIC_ERR_CUDA;
+    }
+    const uint8_t* a8 = reinterpret_cast<const uint8_t*>(a);
+    if (nba < 8) {  // A's low nba bytes per element
+        uint8_t* ac = bs + nplanes * plane;
+        QADIC_TIMED("u64 compact A", s,
+                    u64_compact_kernel<<<(unsigned)((m * k + 255) / 256), 256, 0, s>>>(a, m, k, nba, ac, lda));
+        a8 = ac;
     }
     const bool pair = pair_mode();
     constexpr int BN = Cfg<KIND_I8>::BN;
-    int rc = QADIC_OK;
+    int rc = check_launch("u64 prepare");
     for (int64_t k0 = 0; k0 < k && rc == QADIC_OK; k0 += KC) {
         const int64_t kc = (k - k0 < KC) ? k - k0 : KC;
         dim3 grid((unsigned)((n + 31) / 32), (unsigned)((kc + 31) / 32));
-        QADIC_TIMED("u64 byte planes", s, u64_bplanes_kernel<<<grid, 256, 0, s>>>(b, k, n, k0, kc, bs, ld, plane));
+        QADIC_TIMED("u64 byte planes", s,
+                    u64_bplanes_kernel<<<grid, 256, 0, s>>>(b, k, n, k0, kc, nba, nplanes, bs, ld, plane));
         rc = check_launch("u64 byte planes");
         if (rc) break;
         CUtensorMap ta, tb;
-        rc = make_tmap(&ta, reinterpret_cast<const uint8_t*>(a) + 8 * k0, 8 * kc, m, 8 * k, BM);
+        rc = make_tmap(&ta, a8 + nba * k0, nba * kc, m, lda, BM);
         if (rc) break;
-        for (int sp = 0; sp < 8 && rc == QADIC_OK; ++sp) {
-            rc = make_tmap(&tb, bs + sp * plane, 8 * kc, n, ld, pair ? BN / 2 : BN);
+        for (int sp = 0; sp < nplanes && rc == QADIC_OK; ++sp) {
+            rc = make_tmap(&tb, bs + sp * plane, nba * kc, n, ld, pair ? BN / 2 : BN);
             if (rc) break;
             Params prm = {};
             prm.M = m;
@@ -1937,7 +2016,7 @@ int tc_matmul_u64(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_t m, 
             prm.m_tiles = (int)((m + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM));
             prm.n_tiles = (int)((n + BN - 1) / BN);
             prm.n_full = (int)(n / BN);
-            prm.num_kb = (int)((8 * kc + BK - 1) / BK);
+            prm.num_kb = (int)((nba * kc + BK - 1) / BK);
             prm.planes = 1;
             prm.group_m = GROUP_M;
             prm.c64 = c;
