@@ -50,6 +50,10 @@ class TestLayerK:
         assert np.array_equal(_kernels.matmul_exact_u64(a, b), O.matmul_exact_u64(a, b))
         small = rng.integers(0, 1 << 20, (m, k), dtype=np.uint64)  # typical packed words
         assert np.array_equal(_kernels.matmul_exact_u64(small, b), O.matmul_exact_u64(small, b))
+        tiny = rng.integers(0, 1 << 12, (k, n), dtype=np.uint64)  # 3 x 2 significant bytes: 4 planes
+        assert np.array_equal(_kernels.matmul_exact_u64(small, tiny), O.matmul_exact_u64(small, tiny))
+        zero = np.zeros((k, n), np.uint64)
+        assert not _kernels.matmul_exact_u64(a, zero).any()
 
     def test_matmul_mod(self, golden):
         for chunk in (7, 64, 10**6):
