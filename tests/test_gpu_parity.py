@@ -257,6 +257,18 @@ class TestGFMatmul:
         for e in ENGINES:
             assert np.array_equal(f.matmul_coeffs(a, b, engine=e), ref)
 
+    def test_long_inner_dimension_switches_representatives(self):
+        """GF(7^3) with K = 120000: K * 12^2 >= 2^24, so the fp4 operand codes fall
+        back from the non-negative to the centred representatives (K * 3^2 < 2^24)."""
+        f = W.field_for(W.CONFIGS[5])
+        of = O.build_field(7, 3, irreducible=[5, 0, 0, 1], max_dot_length=9)
+        g = W.rng(120000)
+        a = g.integers(0, 7, (20, 120000, 3), dtype=np.uint8)
+        b = g.integers(0, 7, (120000, 24, 3), dtype=np.uint8)
+        ref = O.gf_matmul_planes(of, a, b)
+        for eng in ("auto", "fp4k", "i8"):
+            assert np.array_equal(f.matmul_coeffs(a, b, engine=eng), ref), eng
+
     @pytest.mark.parametrize("p,k", [(2, 2), (2, 3), (3, 4), (5, 3), (5, 4), (13, 2)])
     def test_more_fields_all_engines(self, p, k):
         """fields beyond the five configs: Toom-Cook (GF(4), GF(125)), Karatsuba
