@@ -343,6 +343,34 @@ class TestGFMatmul:
         assert np.array_equal(o_np, ref)
         assert np.array_equal(f.matmul_coeffs(a, b), ref)
 
+    def test_host_pipeline_pinned_staging(self):
+        """Pageable operands above STAGE_MIN_BYTES travel through the cached
+        pinned stages; back-to-back calls reuse them (the fence keeps a queued
+        call's inputs intact when the output is on the device)."""
+        import torch
+        from paper_0809_0063_b200 import _native as N
+
+        f = W.field_for(W.CONFIGS[5])
+        g = W.rng(91)
+        m, kd, n = 1200, 1500, 1100  # A 5.4 MB, B 4.95 MB, C 3.96 MB + next call's 4.5 MB
+        outs, refs, devs = [], [], []
+        for i in range(3):
+            a = g.integers(0, 7, (m, kd, 3), dtype=np.uint8)
+            b = g.integers(0, 7, (kd, n + 300 * (i == 2), 3), dtype=np.uint8)
+            assert a.nbytes >= N.STAGE_MIN_BYTES and b.nbytes >= N.STAGE_MIN_BYTES
+            refs.append(f.matmul_coeffs(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()).cpu().numpy())
+            o = torch.empty((m, b.shape[1], 3), dtype=torch.uint8, device="cuda")
+            devs.append(f.matmul_coeffs(a, b, out=o))  # device output: asynchronous
+            outs.append(f.matmul_coeffs(a, b))  # numpy in, numpy out (staged C)
+        for o, d, r in zip(outs, devs, refs):
+            assert np.array_equal(o, r)
+            assert np.array_equal(d.cpu().numpy(), r)
+        t = torch.from_numpy(g.integers(0, 7, (m, kd, 3), dtype=np.uint8))
+        o_cpu = torch.empty((m, n + 300, 3), dtype=torch.uint8)  # unpinned CPU tensor output
+        bb = g.integers(0, 7, (kd, n + 300, 3), dtype=np.uint8)
+        assert f.matmul_coeffs(t, bb, out=o_cpu) is o_cpu
+        assert np.array_equal(o_cpu.numpy(), f.matmul_coeffs(t.cuda(), torch.from_numpy(bb).cuda()).cpu().numpy())
+
     def test_guards(self, golden_scalars):
         f = _field(golden_scalars, "gf9_64")
         with pytest.raises(Q.ParamsViolation):
