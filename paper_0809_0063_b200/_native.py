@@ -219,57 +219,6 @@ def host_operand(x, np_dtype):
     return a, a.ctypes.data, a.shape
 
 
-_pinned = {}
-
-
-def pinned_stage(slot: str, nbytes: int):
-    """A cached page-locked host buffer (uint8, >= nbytes) for staging pageable
-    operands: DMA from/to pinned memory runs at the PCIe rate (cfg5 pinned
-    8.8 ms vs 48 ms straight from numpy), and torch's multi-threaded copy_ moves
-    the bytes between numpy and the stage at ~50 GB/s."""
-    t = torch()
-    ev = _stage_busy.pop(slot, None)
-    if ev is not None:
-        ev.synchronize()  # an earlier asynchronous call may still be reading / writing it
-    buf = _pinned.get(slot)
-    if buf is None or buf.numel() < nbytes:
-        _pinned[slot] = buf = t.empty(max(int(nbytes), 1), dtype=t.uint8).pin_memory()
-    return buf[:nbytes]
-
-
-_stage_busy = {}
-
-
-def stage_fence(*slots: str) -> None:
-    """Mark stages as in use by the work just queued on the current stream."""
-    t = torch()
-    for slot in slots:
-        ev = t.cuda.Event()
-        ev.record()
-        _stage_busy[slot] = ev
-
-
-STAGE_MIN_BYTES = 4 << 20  # below this the extra host copy does not pay
-
-
-def staged_host_operand(x, np_dtype, slot: str):
-    """host_operand(), but a large pageable operand is first copied into a
-    pinned stage (returns the same (keep, ptr, shape) triple)."""
-    h = host_operand(x, np_dtype)
-    if h is None:
-        return None
-    keep, ptr, shape = h
-    t = torch()
-    pinned = isinstance(keep, t.Tensor) and keep.is_pinned()
-    nbytes = int(np.prod(shape)) * np.dtype(np_dtype).itemsize
-    if pinned or nbytes < STAGE_MIN_BYTES:
-        return h
-    src = keep if isinstance(keep, t.Tensor) else t.from_numpy(keep)
-    st = pinned_stage(slot, nbytes).view(src.dtype).view(src.shape)
-    st.copy_(src)
-    return st, st.data_ptr(), shape
-
-
 def out_buffer(out, shape, np_dtype):
     """Device buffer the kernel writes: `out` itself when it is a matching
     CUDA tensor, else a fresh device tensor (copied into a host `out` by

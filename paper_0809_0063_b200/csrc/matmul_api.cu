@@ -1,10 +1,14 @@
 // Operation-level matmul entry points: bound checks (the reference's
 // a-priori conditions, src/params.py:99-141, src/gfext.py:320-325,
 // src/cmm.py:170-175) and engine selection.
+#include <algorithm>
+#include <cstdlib>
+#include <memory>
 #include <vector>
 
 #include "qadic_common.cuh"
 #include "qadic_internal.h"
+#include "host_stage.h"
 
 namespace qadic {
 int make_field_const(const qadic_field_desc* d, FieldConst* f);
@@ -130,11 +134,15 @@ int qadic_right_cmm_u8(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kd
 // travel in row panels on two copy streams so that H2D of panel i+1, the
 // compute of panel i and the D2H of panel i-1 overlap (PCIe is full duplex).
 // Device scratch: [engine workspace for one panel | B | 2 A panels | 2 C panels].
+// Pageable (unregistered) host operands go through pinned slots (host_stage.cu):
+// the host thread copies panel i in and panel i-3 out while the device works,
+// so such a call returns with the result in place (a pageable DMA would be
+// synchronous anyway).
 
 static int64_t host_panel_rows(int64_t m, int64_t panel_rows) {
-    // default ~16 panels of >= 256 rows (measured at cfg3/cfg5: 512-1024-row panels
-    // bring the call to within ~15% of the H2D time of A and B alone)
-    int64_t pr = panel_rows > 0 ? panel_rows : ((m + 15) / 16 + 127) / 128 * 128;
+    // default ~12 panels of >= 256 rows (measured at cfg5: 768-row panels 8.6 ms
+    // pinned / ~13-15 ms pageable, against 8.8 / ~15-19 ms with 512 rows)
+    int64_t pr = panel_rows > 0 ? panel_rows : ((m + 11) / 12 + 127) / 128 * 128;
     if (panel_rows <= 0 && pr < 256) pr = 256;
     if (pr < 1) pr = 1;
     return pr < m ? pr : m;
@@ -198,6 +206,19 @@ int qadic_gf_matmul_host_u8(const qadic_field_desc* fd, const uint8_t* a, const 
     cbuf[1] = cbuf[0] + align_up((size_t)(pr * n * k));
     CopyStreams& cs = copy_streams();
     const int64_t panels = (m + pr - 1) / pr;
+    static const bool no_stage = std::getenv("QADIC_NO_STAGE") != nullptr;
+    const bool a_st = !no_stage && !a_dev && kdim > 0 && is_pageable(a);
+    const bool b_st = !no_stage && !b_dev && kdim > 0 && is_pageable(b);
+    const bool c_st = !no_stage && !c_dev && is_pageable(c);
+    std::unique_ptr<StageLease> st;
+    if (a_st || b_st || c_st) {
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(s, &cap);
+        QADIC_REQUIRE(cap == cudaStreamCaptureStatusNone, QADIC_ERR_VALUE,
+                      "pageable host operands cannot be captured in a CUDA graph (use pinned or device buffers)");
+        st.reset(new StageLease(std::max((size_t)(pr * kdim * k), (size_t)(pr * n * k))));
+        QADIC_REQUIRE(st->ok(), QADIC_ERR_CUDA, "pinned staging buffer allocation failed");
+    }
     std::vector<cudaEvent_t> evs;
     auto event = [&]() {
         cudaEvent_t e;
@@ -215,7 +236,13 @@ int qadic_gf_matmul_host_u8(const qadic_field_desc* fd, const uint8_t* a, const 
     after(cs.h2d, s);
     after(cs.d2h, s);
     const uint8_t* bsrc = b;
-    if (!b_dev && kdim > 0) {
+    if (b_st) {  // B in slot-sized chunks through the input slots
+        const size_t tot = (size_t)(kdim * n * k), ch = (size_t)std::max(pr * kdim * k, pr * n * k);
+        for (size_t off = 0, j = 0; off < tot; off += ch, ++j)
+            st->h2d((int)(j % kStageIn), bbuf + off, b + off, std::min(ch, tot - off), cs.h2d);
+        bsrc = bbuf;
+        after(s, cs.h2d);
+    } else if (!b_dev && kdim > 0) {
         cudaMemcpyAsync(bbuf, b, (size_t)(kdim * n * k), cudaMemcpyHostToDevice, cs.h2d);
         bsrc = bbuf;
         after(s, cs.h2d);
@@ -224,16 +251,25 @@ int qadic_gf_matmul_host_u8(const qadic_field_desc* fd, const uint8_t* a, const 
     auto d2h = [&](int64_t i) {
         const int64_t r0 = i * pr, rows = (r0 + pr <= m ? pr : m - r0);
         cudaStreamWaitEvent(cs.d2h, done_c[i], 0);
-        cudaMemcpyAsync(c + r0 * n * k, cbuf[i & 1], (size_t)(rows * n * k), cudaMemcpyDeviceToHost, cs.d2h);
+        uint8_t* dst = c_st ? st->slot(kStageIn + (int)(i % kStageIn)) : c + r0 * n * k;
+        cudaMemcpyAsync(dst, cbuf[i & 1], (size_t)(rows * n * k), cudaMemcpyDeviceToHost, cs.d2h);
         done_d[i] = event();
         cudaEventRecord(done_d[i], cs.d2h);
+    };
+    auto unstage = [&](int64_t i) {  // pinned slot -> caller's pageable C (host waits for the D2H)
+        const int64_t r0 = i * pr, rows = (r0 + pr <= m ? pr : m - r0);
+        cudaEventSynchronize(done_d[i]);
+        parallel_copy(c + r0 * n * k, st->slot(kStageIn + (int)(i % kStageIn)), (size_t)(rows * n * k));
     };
     for (int64_t i = 0; i < panels && rc == QADIC_OK; ++i) {
         const int64_t r0 = i * pr, rows = (r0 + pr <= m ? pr : m - r0);
         const uint8_t* ap = a + r0 * kdim * k;
         if (!a_dev && kdim > 0) {
             if (i >= 2) cudaStreamWaitEvent(cs.h2d, done_c[i - 2], 0);  // panel i-2 no longer reads this buffer
-            cudaMemcpyAsync(abuf[i & 1], ap, (size_t)(rows * kdim * k), cudaMemcpyHostToDevice, cs.h2d);
+            if (a_st)
+                st->h2d((int)(i % kStageIn), abuf[i & 1], ap, (size_t)(rows * kdim * k), cs.h2d);
+            else
+                cudaMemcpyAsync(abuf[i & 1], ap, (size_t)(rows * kdim * k), cudaMemcpyHostToDevice, cs.h2d);
             ap = abuf[i & 1];
             after(s, cs.h2d);
         }
@@ -249,11 +285,15 @@ int qadic_gf_matmul_host_u8(const qadic_field_desc* fd, const uint8_t* a, const 
         cudaEventRecord(done_c[i], s);
         // D2H lags one panel so a pageable destination does not serialise the loop
         if (!c_dev && i >= 1) d2h(i - 1);
+        if (c_st && i >= kStageIn) unstage(i - kStageIn);  // frees the slot d2h(i) will use
     }
     if (rc == QADIC_OK && !c_dev) {
         d2h(panels - 1);
         after(s, cs.d2h);  // stream-ordered completion: s sees every copy
+        if (c_st)
+            for (int64_t j = std::max<int64_t>(0, panels - kStageIn); j < panels; ++j) unstage(j);
     }
+    st.reset();  // waits for the DMAs that read the input slots
     for (cudaEvent_t e : evs) cudaEventDestroy(e);
     if (rc) return rc;
     return check_launch("gf_matmul_host_u8");

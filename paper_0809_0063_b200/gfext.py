@@ -373,9 +373,10 @@ class GFqField:
     def _matmul_host(self, a, b, engine, fold_period, out, panel_rows: int = 0):
         """matmul_coeffs with a host A (B and `out` host or device): one call of
         qadic_gf_matmul_host_u8, which copies B once and streams A / C in row
-        panels so the PCIe transfers overlap the tensor-core work."""
-        ha = N.staged_host_operand(a, np.uint8, "gf_a")
-        hb = N.staged_host_operand(b, np.uint8, "gf_b")
+        panels so the PCIe transfers overlap the tensor-core work (pageable
+        numpy / CPU-tensor buffers through the library's pinned slots)."""
+        ha = N.host_operand(a, np.uint8)
+        hb = N.host_operand(b, np.uint8)
         db = None
         if hb is None:
             db = b.contiguous() if b.dtype == N.torch().uint8 else b.to(N.torch().uint8).contiguous()
@@ -393,28 +394,20 @@ class GFqField:
             fold = self.max_fold_period() if fold_period is None else int(fold_period)
             if fold < 4:
                 raise ParamsViolation("accumulation budget below one DMMA k-step")
-        T = N.torch()
-        dst = None  # pageable host destination, filled from a pinned stage after the call
         if out is None:
             res = np.empty((m, n, self.k), dtype=np.uint8)
-            cptr, keep, dst = res.ctypes.data, res, res
+            cptr, keep = res.ctypes.data, res
         else:
             if tuple(out.shape) != (m, n, self.k):
                 raise ValueError(f"out must have shape {(m, n, self.k)}")
             if N.is_tensor(out):
-                if not out.is_contiguous() or out.dtype != T.uint8:
+                if not out.is_contiguous() or out.dtype != N.torch().uint8:
                     raise ValueError("out must be a contiguous uint8 tensor")
                 cptr, keep = out.data_ptr(), out
-                if not out.is_cuda and not out.is_pinned():
-                    dst = out
             else:
                 if not (out.flags.c_contiguous and out.dtype == np.uint8):
                     raise ValueError("out must be a C-contiguous uint8 array")
-                cptr, keep, dst = out.ctypes.data, out, out
-        stage = None
-        if dst is not None and m * n * self.k >= N.STAGE_MIN_BYTES:
-            stage = N.pinned_stage("gf_c", m * n * self.k)
-            cptr = stage.data_ptr()
+                cptr, keep = out.ctypes.data, out
         desc = self.field_desc()
         L = N.lib()
         ws_bytes = L.qadic_gf_matmul_host_workspace(desc, m, kd, n, eng, panel_rows)
@@ -422,11 +415,7 @@ class GFqField:
         N.check(L.qadic_gf_matmul_host_u8(desc, aptr, bptr, m, kd, n, eng, fold, panel_rows, N.ptr(ws), ws_bytes,
                                           cptr, N.stream_ptr()), DimensionMismatch)
         if out is None or not (N.is_tensor(out) and out.is_cuda):
-            T.cuda.current_stream().synchronize()  # host result complete on return
-        else:
-            N.stage_fence("gf_a", "gf_b")  # device result: the call may still read staged inputs
-        if stage is not None:
-            (dst if N.is_tensor(dst) else T.from_numpy(dst)).view(-1).copy_(stage)
+            N.torch().cuda.current_stream().synchronize()  # host result complete on return
         del ha, hb, db, keep
         return res if out is None else out
 

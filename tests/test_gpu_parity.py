@@ -344,11 +344,10 @@ class TestGFMatmul:
         assert np.array_equal(f.matmul_coeffs(a, b), ref)
 
     def test_host_pipeline_pinned_staging(self):
-        """Pageable operands above STAGE_MIN_BYTES travel through the cached
-        pinned stages; back-to-back calls reuse them (the fence keeps a queued
-        call's inputs intact when the output is on the device)."""
+        """Pageable operands travel through the library's pinned slots (B in
+        slot-sized chunks, A / C per panel); back-to-back calls reuse the ring,
+        including calls whose output stays on the device (asynchronous)."""
         import torch
-        from paper_0809_0063_b200 import _native as N
 
         f = W.field_for(W.CONFIGS[5])
         g = W.rng(91)
@@ -357,7 +356,6 @@ class TestGFMatmul:
         for i in range(3):
             a = g.integers(0, 7, (m, kd, 3), dtype=np.uint8)
             b = g.integers(0, 7, (kd, n + 300 * (i == 2), 3), dtype=np.uint8)
-            assert a.nbytes >= N.STAGE_MIN_BYTES and b.nbytes >= N.STAGE_MIN_BYTES
             refs.append(f.matmul_coeffs(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()).cpu().numpy())
             o = torch.empty((m, b.shape[1], 3), dtype=torch.uint8, device="cuda")
             devs.append(f.matmul_coeffs(a, b, out=o))  # device output: asynchronous

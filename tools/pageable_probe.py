@@ -26,15 +26,17 @@ def t(fn, reps=3):
     return best * 1e3
 
 
-from paper_0809_0063_b200 import _native as N  # noqa: E402
+import os  # noqa: E402
 
-print("numpy in, numpy out (pinned stages): %.1f ms" % t(lambda: f._matmul_host(a, b, "auto", None, out)))
-lim, N.STAGE_MIN_BYTES = N.STAGE_MIN_BYTES, 1 << 62
-print("numpy in, numpy out (DMA from pageable): %.1f ms" % t(lambda: f._matmul_host(a, b, "auto", None, out)))
-N.STAGE_MIN_BYTES = lim
+print("numpy in, numpy out (%s): %.1f ms" % ("DMA from pageable" if os.environ.get("QADIC_NO_STAGE") else
+                                             "pinned slots", t(lambda: f._matmul_host(a, b, "auto", None, out))))
+for pr in [int(x) for x in os.environ.get("PROBE_PANELS", "256,1024").split(",")]:
+    print("  panel_rows %d: %.1f ms" % (pr, t(lambda: f._matmul_host(a, b, "auto", None, out, panel_rows=pr))))
 pa, pb = torch.from_numpy(a).pin_memory(), torch.from_numpy(b).pin_memory()
 po = torch.empty((8192, 8192, 3), dtype=torch.uint8).pin_memory()
 print("pinned in, pinned out: %.1f ms" % t(lambda: f._matmul_host(pa, pb, "auto", None, po)))
+for pr in [int(x) for x in os.environ.get("PROBE_PANELS", "256,1024").split(",")]:
+    print("  panel_rows %d: %.1f ms" % (pr, t(lambda: f._matmul_host(pa, pb, "auto", None, po, panel_rows=pr))))
 print("torch threads:", torch.get_num_threads())
 print("numpy -> pinned copy 201 MB: %.1f ms" % t(lambda: pa.copy_(torch.from_numpy(a))))
 print("pinned -> numpy copy 201 MB: %.1f ms" % t(lambda: torch.from_numpy(out).copy_(po)))
