@@ -386,7 +386,8 @@ class TestPackRows:
     """qadic_pack_rows_u8 / qadic_unpack_rows_u8 (cmm.py:72-85, 130-145): tiled
     16-byte kernels at ragged shapes and odd row offsets, both digit orders."""
 
-    @pytest.mark.parametrize("rows,cols", [(1, 1), (3, 7), (5, 1023), (17, 1537), (2, 4100), (64, 3000)])
+    @pytest.mark.parametrize("rows,cols", [(1, 1), (3, 7), (5, 1023), (17, 1537), (2, 4100), (64, 3000), (3, 16389),
+                                           (4, 24576)])
     @pytest.mark.parametrize("k,t", [(1, 8), (2, 17), (3, 17), (5, 12), (8, 8)])
     def test_pack_unpack(self, rows, cols, k, t):
         import torch
@@ -466,6 +467,59 @@ class TestRightCMM:
 # ---------------------------------------------------------------------------
 # C ABI error contract: status codes + qadic_last_error, no launch on bad input
 # ---------------------------------------------------------------------------
+class TestFdivScans:
+    """GPU exhaustive certification scans (csrc/fdiv_scan.cu) against the
+    reference's own reports (tests/golden/fdiv_scans.json) and the oracle."""
+
+    def test_against_reference_reports(self, golden_fdiv_scans):
+        from paper_0809_0063_b200 import fdiv
+
+        for key, want in golden_fdiv_scans["scans"].items():
+            beta, cid = map(int, key.split(":"))
+            rep = fdiv.exhaustive_check(beta, cid)
+            got = {"pairs_checked": rep.pairs_checked, "range_violations": rep.range_violations,
+                   "bound_violations": rep.bound_violations,
+                   "k_minus_1_witness": list(rep.k_minus_1_witness) if rep.k_minus_1_witness else None,
+                   "k_plus_1_witness": list(rep.k_plus_1_witness) if rep.k_plus_1_witness else None,
+                   "smallest_overflow_r": rep.smallest_overflow_r}
+            assert got == want, key
+            assert rep.ok
+        for beta, want in golden_fdiv_scans["applied_mismatches"].items():
+            assert fdiv.applied_fdiv_exhaustive(int(beta)) == want == 0
+
+    @pytest.mark.parametrize("beta", [5, 7, 9, 11])
+    def test_against_oracle(self, beta):
+        from paper_0809_0063_b200 import fdiv
+
+        for cid in (1, 2, 5, 6, 9):
+            rep = fdiv.exhaustive_check(beta, cid)
+            want = O.fdiv_exhaustive_check(beta, cid)
+            assert [rep.pairs_checked, rep.range_violations, rep.bound_violations] == \
+                [want["pairs_checked"], want["range_violations"], want["bound_violations"]]
+            assert (list(rep.k_minus_1_witness) if rep.k_minus_1_witness else None) == want["k_minus_1_witness"]
+            assert (list(rep.k_plus_1_witness) if rep.k_plus_1_witness else None) == want["k_plus_1_witness"]
+            assert rep.smallest_overflow_r == want["smallest_overflow_r"]
+
+    def test_extended_beta(self):
+        """beyond the reference's beta <= 16: Table 1 still holds at beta 18 / 20
+        (2^36 / 2^40 pairs per case) and Alg. 4 stays exact."""
+        from paper_0809_0063_b200 import fdiv
+
+        with pytest.raises(ValueError):
+            fdiv.exhaustive_check(17, 1)
+        with pytest.raises(ValueError):
+            fdiv.exhaustive_check(3, 1, extended=True)
+        with pytest.raises(ValueError):
+            fdiv.exhaustive_check(23, 1, extended=True)
+        for cid in range(1, 10):
+            rep = fdiv.exhaustive_check(18, cid, extended=True)
+            assert rep.ok and rep.pairs_checked == ((1 << 18) - 1) << 18
+            if cid == 5:  # both range endpoints attained (SPEC.md: case 5 at beta 8)
+                assert rep.k_minus_1_witness and rep.k_plus_1_witness
+        assert fdiv.applied_fdiv_exhaustive(18, extended=True) == 0
+        assert fdiv.exhaustive_check(20, 2, extended=True).ok
+
+
 class TestABIErrors:
     def test_status_codes(self):
         import ctypes
