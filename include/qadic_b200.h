@@ -179,6 +179,32 @@ QADIC_API int qadic_gather_u8(const int64_t *idx, int64_t n, const uint8_t *tabl
 QADIC_API int qadic_index_of_coeffs(const uint8_t *c, int64_t n, int32_t k, int32_t p,
                           const int64_t *index_of_code, int64_t *out, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * FDIV certification scans (fdiv.exhaustive_check / applied_fdiv_exhaustive,
+ * fdiv.py:405-461; Table 1, Alg. 4).
+ * Every (r, p) in [0, 2^beta) x [1, 2^beta) in beta-bit binary arithmetic:
+ * x = round2(r * round1(1/p)), diff = floor(x) - r // p.  Modes: 0 = up,
+ * 1 = nearest (ties to even), 2 = down (the reference's _MODE_ORDER).
+ * `out` / `mismatches` are HOST pointers; the call returns when they are
+ * filled (synchronous on `stream`).  beta in 4..22 (the reference: 4..16).
+ * ------------------------------------------------------------------------- */
+typedef struct qadic_fdiv_scan_report {
+    uint64_t pairs_checked;
+    uint64_t range_violations;     /* diff outside [range_lo, range_hi] */
+    uint64_t bound_violations;     /* diff > 0 with r <= bound_threshold */
+    int64_t k_minus_1_r, k_minus_1_p; /* first (p-major) pair with diff = -1 when range_lo = -1; else -1 */
+    int64_t k_plus_1_r, k_plus_1_p;   /* first (p-major) pair with diff = +1 when range_hi = 1; else -1 */
+    int64_t smallest_overflow_r;      /* least r with diff > 0 over all p, -1 if none */
+} qadic_fdiv_scan_report;
+
+/* one case (mode1, mode2): bound_threshold < 0 means the case has no bound */
+QADIC_API int qadic_fdiv_scan(int32_t beta, int32_t mode1, int32_t mode2, int32_t range_lo, int32_t range_hi,
+                              int64_t bound_threshold, qadic_fdiv_scan_report *out, void *stream);
+/* Alg. 4 for the three paired cases (mode2 = up / nearest / down with the
+ * reciprocal mode fdiv._PAIRED_MODE1 gives): y -= (r >= bound[mode2] && p*y > r),
+ * counts y != r // p over all (r, p, mode2). */
+QADIC_API int qadic_fdiv_applied_scan(int32_t beta, const int64_t bound[3], uint64_t *mismatches, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

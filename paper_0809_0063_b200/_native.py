@@ -43,6 +43,21 @@ class FieldDesc(ctypes.Structure):
     ]
 
 
+class FdivScanReport(ctypes.Structure):
+    """Mirror of `qadic_fdiv_scan_report`."""
+
+    _fields_ = [
+        ("pairs_checked", ctypes.c_uint64),
+        ("range_violations", ctypes.c_uint64),
+        ("bound_violations", ctypes.c_uint64),
+        ("k_minus_1_r", I64),
+        ("k_minus_1_p", I64),
+        ("k_plus_1_r", I64),
+        ("k_plus_1_p", I64),
+        ("smallest_overflow_r", I64),
+    ]
+
+
 _SIGNATURES = {
     "qadic_abi_version": ([], ctypes.c_int),
     "qadic_last_error": ([], ctypes.c_char_p),
@@ -67,6 +82,8 @@ _SIGNATURES = {
     "qadic_polymul_batch_u8": ([P, P, I64, I32, I64, I32, P, P], ctypes.c_int),
     "qadic_gather_u8": ([P, I64, P, I64, I32, P, P], ctypes.c_int),
     "qadic_index_of_coeffs": ([P, I64, I32, I32, P, P, P], ctypes.c_int),
+    "qadic_fdiv_scan": ([I32, I32, I32, I32, I32, I64, ctypes.POINTER(FdivScanReport), P], ctypes.c_int),
+    "qadic_fdiv_applied_scan": ([I32, ctypes.POINTER(I64 * 3), ctypes.POINTER(ctypes.c_uint64), P], ctypes.c_int),
 }
 
 EXPORTED = tuple(_SIGNATURES)

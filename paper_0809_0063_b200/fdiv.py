@@ -10,12 +10,14 @@ Reference: /root/reference/pkg/src/qadic/fdiv.py:166-180 (native_reciprocal),
 :183-210 (fdiv), :218-295 (the mode-pair case table), :298-363
 (precompute_inverses / applied_fdiv).  The "sim" backend here is a restatement
 of the beta-bit rounding (exact rationals, ties to even) so the reference's
-default-backend calls keep working; the exhaustive scans of the reference are
-certification tooling, out of scope.
+default-backend calls keep working.  The exhaustive certification scans
+(exhaustive_check / applied_fdiv_exhaustive, :405-461) run on the GPU
+(csrc/fdiv_scan.cu, one CTA per divisor).
 """
 
 from __future__ import annotations
 
+import ctypes
 import enum
 import math
 from dataclasses import dataclass, field
@@ -242,3 +244,75 @@ def applied_fdiv(r: int, p: int, active_mode2: RoundingMode = NEAREST, inv: Opti
     if r >= inv.bound[active_mode2] and p * y > r:
         y -= 1
     return y
+
+
+# ---------------------------------------------------------------------------
+# exhaustive certification scans (reference fdiv.py:371-461), on the GPU
+# ---------------------------------------------------------------------------
+SCAN_BETA_MIN, SCAN_BETA_MAX = 4, 16  # the reference's range
+GPU_SCAN_BETA_MAX = 22  # what the CUDA scan accepts with extended=True
+
+
+@dataclass
+class ScanReport:
+    """Findings of an exhaustive (r, p) scan of one case at one beta."""
+
+    beta: int
+    case_id: int
+    pairs_checked: int = 0
+    range_violations: int = 0
+    bound_violations: int = 0
+    k_minus_1_witness: Optional[tuple] = None  # (r, p) attaining floor = k-1 (first p, then first r)
+    k_plus_1_witness: Optional[tuple] = None  # (r, p) attaining floor = k+1
+    smallest_overflow_r: Optional[int] = None  # least r with floor > k anywhere
+
+    @property
+    def ok(self) -> bool:
+        return self.range_violations == 0 and self.bound_violations == 0
+
+
+def _scan_beta(beta: int, extended: bool) -> None:
+    hi = GPU_SCAN_BETA_MAX if extended else SCAN_BETA_MAX
+    if not SCAN_BETA_MIN <= beta <= hi:
+        raise ValueError(f"exhaustive scans support beta in {SCAN_BETA_MIN}..{hi}")
+
+
+def exhaustive_check(beta: int, case_id: int, extended: bool = False) -> ScanReport:
+    """Every (r, p) in [0, 2^beta) x [1, 2^beta) for one case: range
+    containment, floor(x) <= k below the case bound, and the first witnesses of
+    floor(x) = k -/+ 1 (reference fdiv.py:405-441).  One CUDA launch;
+    `extended` admits beta up to 22 (2^44 pairs)."""
+    from . import _native as N
+
+    _scan_beta(beta, extended)
+    spec = case_spec_by_id(case_id, beta)
+    N.require_cuda()
+    thr = spec.bound_threshold()
+    rep = N.FdivScanReport()
+    N.check(N.lib().qadic_fdiv_scan(beta, _MODE_ORDER.index(spec.mode1), _MODE_ORDER.index(spec.mode2),
+                                    spec.range_lo, spec.range_hi, -1 if thr is None else thr, ctypes.byref(rep),
+                                    N.stream_ptr()))
+
+    def wit(r, p):
+        return None if p < 0 else (int(r), int(p))
+
+    return ScanReport(beta=beta, case_id=case_id, pairs_checked=int(rep.pairs_checked),
+                      range_violations=int(rep.range_violations), bound_violations=int(rep.bound_violations),
+                      k_minus_1_witness=wit(rep.k_minus_1_r, rep.k_minus_1_p),
+                      k_plus_1_witness=wit(rep.k_plus_1_r, rep.k_plus_1_p),
+                      smallest_overflow_r=None if rep.smallest_overflow_r < 0 else int(rep.smallest_overflow_r))
+
+
+def applied_fdiv_exhaustive(beta: int, extended: bool = False) -> int:
+    """Mismatch count of applied_fdiv (Alg. 4: paired reciprocal mode plus one
+    multiply-back decrement at and above the case bound) against r // p over
+    all (r, p, mode2) (reference fdiv.py:444-461).  One CUDA launch."""
+    from . import _native as N
+
+    _scan_beta(beta, extended)
+    N.require_cuda()
+    bounds = (ctypes.c_int64 * 3)(*[case_spec(_PAIRED_MODE1[m2], m2, beta).bound_threshold() + 1
+                                    for m2 in _MODE_ORDER])
+    out = ctypes.c_uint64(0)
+    N.check(N.lib().qadic_fdiv_applied_scan(beta, ctypes.byref(bounds), ctypes.byref(out), N.stream_ptr()))
+    return int(out.value)

@@ -43,5 +43,12 @@ def golden_scalars():
         return json.load(fh)
 
 
+@pytest.fixture(scope="session")
+def golden_fdiv_scans():
+    """Reports of the reference's own exhaustive FDIV scans (make_fdiv_scans.py)."""
+    with open(os.path.join(GOLDEN, "fdiv_scans.json")) as fh:
+        return json.load(fh)
+
+
 def philox(seed):
     return np.random.Generator(np.random.Philox(seed))

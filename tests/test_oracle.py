@@ -78,6 +78,14 @@ class TestScalars:
             assert tup(O.cmm_params(3, int(n))) == v
         assert O.chunk_budget(7, 1 << 10, 3, 6, 6) == golden_scalars["cfg5_chunk"] == 9
 
+    @pytest.mark.parametrize("beta", [4, 6, 8, 10])
+    def test_fdiv_exhaustive_scans(self, golden_fdiv_scans, beta):
+        """the oracle's restatement of exhaustive_check / applied_fdiv_exhaustive
+        against the reports of the reference itself (all nine cases)."""
+        for cid in range(1, 10):
+            assert O.fdiv_exhaustive_check(beta, cid) == golden_fdiv_scans["scans"][f"{beta}:{cid}"], cid
+        assert O.applied_fdiv_exhaustive(beta) == golden_fdiv_scans["applied_mismatches"][str(beta)] == 0
+
     def test_fdiv_exact_below_bound(self):
         rng = np.random.default_rng(0)
         for p in (3, 5, 7, 23):
