@@ -12,7 +12,7 @@ NCU="ncu --clock-control none"
 B="python bench.py --no-cpu-baseline"
 ok=1
 for c in 1 2; do $B --config $c --warmup 5 > $O/bench_cfg$c.json 2>>$O/bench.err || ok=0; done
-for c in redq pack; do python bench.py --config $c > $O/bench_$c.json 2>>$O/bench.err || ok=0; done
+for c in redq pack mm64; do python bench.py --config $c > $O/bench_$c.json 2>>$O/bench.err || ok=0; done
 for c in 3 4 5; do
   for e in auto i8 fp4 fp4k; do $B --config $c --engine $e --steps 20 --warmup 3 > $O/bench_cfg${c}_$e.json 2>>$O/bench.err || ok=0; done
 done
@@ -39,5 +39,13 @@ full cfg2_gf_dot 2 auto gf_dot
 python bench.py --config redq --steps 3 > /dev/null 2>&1 && $NCU --set full -k regex:redq_vec -s 2 -c 1 -o $O/redq -f python bench.py --config redq --steps 3 > $O/redq.log 2>&1
 ncu -i $O/redq.ncu-rep --page raw --csv > $O/redq_raw.csv 2>/dev/null
 full cfg5_i8_gemm 5 i8 gemm_modp
+python bench.py --config pack --steps 3 > /dev/null 2>&1 && $NCU --set full -k regex:pack_rows -s 2 -c 1 -o $O/pack -f python bench.py --config pack --steps 3 > $O/pack.log 2>&1
+ncu -i $O/pack.ncu-rep --page raw --csv > $O/pack_raw.csv 2>/dev/null
+ncu -i $O/pack.ncu-rep --page details --csv > $O/pack_details.csv 2>/dev/null
+# measured ceilings and host-side paths on the same box
+REPS=200 python tools/fp4_library_peak.py 8192 residues > $O/fp4_library_ceiling.json 2>>$O/bench.err
+python tools/hbm_write_probe.py > $O/hbm_write_probe.json 2>>$O/bench.err
+python tools/e2e_probe.py > $O/e2e_probe.txt 2>>$O/bench.err
+python tools/pageable_probe.py > $O/pageable_probe.txt 2>>$O/bench.err
 echo "bench ok=$ok"
 ls -la $O | head -80
