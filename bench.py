@@ -377,7 +377,7 @@ def traffic_from_profiles(cfg, engine, kname):
     try:
         with open(path) as fh:
             t = json.load(fh)
-        return t.get(f"cfg{cfg}:{engine}:{kname}")
+        return t.get(f"cfg{cfg}:{engine}:{kname}" if engine is not None else f"{cfg}:{kname}")
     except (OSError, ValueError):
         return None
 
@@ -562,13 +562,15 @@ REF_BUDGET_S = float(os.environ.get("QADIC_REF_BUDGET_S", "90"))  # wall budget 
 
 
 # ---------------------------------------------------------------------------
-# Layer-K primitives at config scale (HBM-bound): --config redq | pack
+# Layer-K primitives at config scale: --config redq | pack | unpack (HBM-bound) | mm64 (tensor)
 # ---------------------------------------------------------------------------
 PRIMS = {
     # REDQ of cfg3's accumulators: 8192^2 words, p=3, q=2^17, d=2 -> digits uint64[n, 3]
     "redq": {"n": 1 << 26, "p": 3, "t": 17, "d": 2},
     # cfg4's row compression: uint8[16384, 16384] -> uint64[16384, 5462] (k=3, q=2^17)
     "pack": {"rows": 16384, "cols": 16384, "k": 3, "t": 17},
+    # its inverse (cmm.uncompress): uint64[16384, 5462] -> uint8[16384, 16384]
+    "unpack": {"rows": 16384, "cols": 16384, "k": 3, "t": 17},
     # the reference's GF(9) driver product: packed words uint64[8192, 8192] @ uint64[8192, 8192]
     # (Layer K matmul_exact_u64, exact mod 2^64; words of 2 digits at q=2^17)
     "mm64": {"n": 8192, "bits": 34},
@@ -616,6 +618,21 @@ def run_primitive(args, kind):
         byts, units, unit = None, n ** 3, "u64 MAC/s"
         workload = f"mm64:matmul_exact_u64 {n}^3 words < 2^{cfgp['bits']} (the reference GF(9) driver product)"
         kname = "u64 byte-plane gemm"
+    elif kind == "unpack":
+        rows, cols, k, t = cfgp["rows"], cfgp["cols"], cfgp["k"], cfgp["t"]
+        width = -(-cols // k)
+        words = sum(g.integers(0, 3, (rows, width), dtype=np.uint64) << np.uint64(j * t) for j in range(k))
+        sets = [torch.from_numpy(words.view(np.int64)).cuda(), torch.from_numpy(words.view(np.int64)).cuda()]
+        outs = [torch.empty((rows, cols), dtype=torch.uint8, device="cuda") for _ in sets]
+        L = N.lib()
+
+        def step(i):
+            N.check(L.qadic_unpack_rows_u8(N.ptr(sets[i % 2]), rows, cols, k, t, 0, N.ptr(outs[i % 2]),
+                                           N.stream_ptr()))
+
+        byts, units, unit = rows * cols + 8 * rows * width, rows * cols, "entries/s"
+        workload = f"unpack:uncompress uint64[{rows},{width}] -> uint8[{rows},{cols}] k={k} q=2^{t} (cfg4 layout)"
+        kname = "unpack_rows_u8"
     else:
         rows, cols, k, t = cfgp["rows"], cfgp["cols"], cfgp["k"], cfgp["t"]
         host = g.integers(0, 2, (rows, cols), dtype=np.uint8)
@@ -661,7 +678,8 @@ def run_primitive(args, kind):
     else:
         achieved = byts / (ms / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": kname, "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
-                "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
+                "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
+                "traffic": traffic_from_profiles(kind, None, kname),
                 "avg_launch_ms": round(ms, 5), "algorithmic_bytes_per_launch": byts,
                 "avg_launch_source": "timed region / K (one launch per step)",
                 "peak_source": f"{peak_src} hbm_gbs (copy)"}

@@ -394,6 +394,54 @@ __global__ void __launch_bounds__(PK_THREADS) unpack_rows_tile_kernel(const uint
         uint8_t* dst = out + r * cols + c0;
         const int lead = (int)(reinterpret_cast<uintptr_t>(dst) & 15);  // buf[lead + x] <-> dst[x]
         const uint64_t* roww = words + r * width + g0;
+        if (nw == PK_WORDS && nbytes == (int64_t)PK_WORDS * k && (reinterpret_cast<uintptr_t>(roww) & 15) == 0) {
+            // full tile (mirror of pack's fast path): 4 consecutive words per group,
+            // their 4k digit bytes assembled in k registers and written as aligned
+            // u32 at buf[4k*gi]; the copy-out funnel-shifts 5 aligned u32 per 16-byte
+            // chunk to the destination's alignment
+            uint32_t* b32 = reinterpret_cast<uint32_t*>(buf);
+#pragma unroll
+            for (int h = 0; h < PK_WPT / 4; ++h) {
+                const int gi = threadIdx.x + PK_THREADS * h;
+                const ulonglong2 w01 = __ldcs(reinterpret_cast<const ulonglong2*>(roww + 4 * gi));
+                const ulonglong2 w23 = __ldcs(reinterpret_cast<const ulonglong2*>(roww + 4 * gi + 2));
+                const uint64_t wd[4] = {w01.x, w01.y, w23.x, w23.y};
+                uint32_t x[k];
+#pragma unroll
+                for (int i = 0; i < k; ++i) x[i] = 0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < k; ++j) {
+                        const int q = i * k + j;  // byte of the group (compile-time)
+                        const uint32_t d = (uint32_t)((wd[i] >> ((reverse ? (k - 1 - j) : j) * t)) & mask) & 0xffu;
+                        x[q >> 2] |= d << (8 * (q & 3));
+                    }
+#pragma unroll
+                for (int i = 0; i < k; ++i) b32[k * gi + i] = x[i];
+            }
+            __syncthreads();
+            const int nchunks = (lead + PK_WORDS * k + 15) / 16;
+            uint8_t* base = dst - lead;
+            for (int i = threadIdx.x; i < nchunks; i += PK_THREADS) {
+                const int o = 16 * i - lead;  // buf offset of the chunk's first byte
+                if (o >= 0 && o + 16 <= PK_WORDS * k) {
+                    const uint32_t* src = b32 + (o >> 2);
+                    const int fs = 8 * (o & 3);
+                    uint32_t v[5];
+#pragma unroll
+                    for (int j = 0; j < 5; ++j) v[j] = src[j];
+                    __stcs(reinterpret_cast<uint4*>(base + 16 * i),
+                           make_uint4(__funnelshift_r(v[0], v[1], fs), __funnelshift_r(v[1], v[2], fs),
+                                      __funnelshift_r(v[2], v[3], fs), __funnelshift_r(v[3], v[4], fs)));
+                } else {
+                    for (int b = 0; b < 16; ++b)
+                        if (o + b >= 0 && o + b < PK_WORDS * k) base[16 * i + b] = buf[o + b];
+                }
+            }
+            __syncthreads();
+            continue;
+        }
         uint64_t wv[PK_WPT];
 #pragma unroll
         for (int h = 0; h < PK_WPT; h += 2) {  // lane-consecutive 16-byte pairs

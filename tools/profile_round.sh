@@ -12,7 +12,7 @@ NCU="ncu --clock-control none"
 B="python bench.py --no-cpu-baseline"
 ok=1
 for c in 1 2; do $B --config $c --warmup 5 > $O/bench_cfg$c.json 2>>$O/bench.err || ok=0; done
-for c in redq pack mm64; do python bench.py --config $c > $O/bench_$c.json 2>>$O/bench.err || ok=0; done
+for c in redq pack unpack mm64; do python bench.py --config $c > $O/bench_$c.json 2>>$O/bench.err || ok=0; done
 for c in 3 4 5; do
   for e in auto i8 fp4 fp4k; do $B --config $c --engine $e --steps 20 --warmup 3 > $O/bench_cfg${c}_$e.json 2>>$O/bench.err || ok=0; done
 done

@@ -32,7 +32,11 @@ TRAFFIC = {
     "cfg5_i8_gemm": ["cfg5:i8:i8 gemm"],
     "cfg1_polymul": ["cfg1:auto:polymul_k4"],
     "cfg2_gf_dot": ["cfg2:auto:gf_dot"],
+    "redq": ["redq:reduce_words"],
+    "pack": ["pack:pack_rows_u8"],
 }
+# measured ceilings / host-path probes written by profile_round.sh, copied verbatim
+PROBES = ["fp4_library_ceiling.json", "hbm_write_probe.json", "e2e_probe.txt", "pageable_probe.txt"]
 
 
 def to_bytes(v, unit):
@@ -102,6 +106,11 @@ def main():
             lines += ["| kernel | launches | total ns | share |", "|---|---|---|---|"]
             for nm, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
                 lines.append("| %s | %d | %.0f | %.3f |" % (nm, c, t, t / tot_all))
+    for name in PROBES:
+        f = os.path.join(src, name)
+        if os.path.exists(f) and os.path.getsize(f):
+            shutil.copy(f, dst)
+            lines += ["", "## %s" % name, "", "```", open(f).read().strip(), "```"]
     open(os.path.join(dst, "SUMMARY.md"), "w").write("\n".join(lines) + "\n")
     with open(os.path.join(ROOT, "profiles", "traffic.json"), "w") as fh:
         json.dump(traffic, fh, indent=1)
