@@ -205,6 +205,18 @@ QADIC_API int qadic_fdiv_scan(int32_t beta, int32_t mode1, int32_t mode2, int32_
  * counts y != r // p over all (r, p, mode2). */
 QADIC_API int qadic_fdiv_applied_scan(int32_t beta, const int64_t bound[3], uint64_t *mismatches, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * Diagnostics: measured pipe peaks (no reference
+ * counterpart).  Runs one on-chip probe (operands in shared memory / registers,
+ * no memory traffic) and returns the operations executed (*ops: 2 per MAC) and
+ * the event-timed duration (*ms); synchronous on `stream`.
+ *   kind 0: tcgen05.mma cta_group::2 kind::mxf4.block_scale (M256 N256 K64)
+ *   kind 1: tcgen05.mma cta_group::2 kind::i8 (M256 N256 K32)
+ *   kind 2: mma.sync m8n8k4 f64 (DMMA)
+ *   data 0: zero operands, 1: residue-like operands (what the engines feed), 2: random bits
+ * ------------------------------------------------------------------------- */
+QADIC_API int qadic_diag_pipe_peak(int32_t kind, int32_t data, int64_t iters, double *ops, float *ms, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -84,6 +84,8 @@ _SIGNATURES = {
     "qadic_index_of_coeffs": ([P, I64, I32, I32, P, P, P], ctypes.c_int),
     "qadic_fdiv_scan": ([I32, I32, I32, I32, I32, I64, ctypes.POINTER(FdivScanReport), P], ctypes.c_int),
     "qadic_fdiv_applied_scan": ([I32, ctypes.POINTER(I64 * 3), ctypes.POINTER(ctypes.c_uint64), P], ctypes.c_int),
+    "qadic_diag_pipe_peak": ([I32, I32, I64, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_float), P],
+                             ctypes.c_int),
 }
 
 EXPORTED = tuple(_SIGNATURES)
@@ -275,3 +277,16 @@ def workspace(nbytes: int):
     if buf is None or buf.numel() < nbytes:
         _workspace[dev] = buf = t.empty(max(int(nbytes), 1), dtype=t.uint8, device=device())
     return buf
+
+
+PIPE_KINDS = {"mxf4": 0, "i8": 1, "f64": 2}
+PIPE_DATA = {"zeros": 0, "residues": 1, "random": 2}
+
+
+def pipe_peak(kind: str, data: str = "residues", iters: int = 20000) -> Tuple[float, float]:
+    """One on-chip pipe-peak probe (qadic_diag_pipe_peak): (ops/s, ms)."""
+    require_cuda()
+    ops, ms = ctypes.c_double(0.0), ctypes.c_float(0.0)
+    check(lib().qadic_diag_pipe_peak(PIPE_KINDS[kind], PIPE_DATA[data], int(iters), ctypes.byref(ops),
+                                     ctypes.byref(ms), stream_ptr()))
+    return ops.value / (ms.value * 1e-3), ms.value

@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(PM_THREADS, 4) polymul_k4_kernel(const uint8_t
                                                                 PolyConst c, uint8_t* __restrict__ out) {
     pdl_wait();  // predecessor complete before any global access
     pdl_trigger();
-    const int64_t p0 = ((int64_t)blockIdx.x * PM_THREADS + threadIdx.x) * PM_PER;
+    const int64_t p0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * PM_PER;
     if (__all_sync(0xffffffffu, p0 >= n)) return;  // whole warp past the end (warps stay converged)
     uint32_t av[PM_PER], bv[PM_PER];
     const bool full = p0 + PM_PER <= n;
@@ -138,9 +138,18 @@ __global__ void __launch_bounds__(PM_THREADS, 4) polymul_k4_kernel(const uint8_t
 template <int T>
 static void launch_polymul_k4(const uint8_t* a, const uint8_t* b, int64_t n, const PolyConst& c, uint8_t* out,
                               cudaStream_t s) {
-    const unsigned blocks = (unsigned)((n + (int64_t)PM_THREADS * PM_PER - 1) / ((int64_t)PM_THREADS * PM_PER));
-    if (c.corr == 1 || c.p == 2) launch_pdl(polymul_k4_kernel<T, true>, dim3(blocks), dim3(PM_THREADS), 0, s, a, b, n, c, out);
-    else launch_pdl(polymul_k4_kernel<T, false>, dim3(blocks), dim3(PM_THREADS), 0, s, a, b, n, c, out);
+    // One wave, balanced: 4 blocks on every SM with the block width trimmed so
+    // that the pairs spread evenly (cfg1: 592 x 224 threads instead of 512 x 256,
+    // which left 68 SMs with a fourth block and the rest with three).  Larger
+    // batches run 256-thread blocks in several waves.
+    const int64_t per_wave = 4LL * num_sms_cached();
+    int64_t threads = (n + per_wave * PM_PER - 1) / (per_wave * PM_PER);
+    threads = (threads + 31) / 32 * 32;
+    if (threads > PM_THREADS) threads = PM_THREADS;
+    if (threads < 32) threads = 32;
+    const unsigned blocks = (unsigned)((n + threads * PM_PER - 1) / (threads * PM_PER));
+    if (c.corr == 1 || c.p == 2) launch_pdl(polymul_k4_kernel<T, true>, dim3(blocks), dim3((unsigned)threads), 0, s, a, b, n, c, out);
+    else launch_pdl(polymul_k4_kernel<T, false>, dim3(blocks), dim3((unsigned)threads), 0, s, a, b, n, c, out);
 }
 
 // ---- generic k (1..8): one pair per thread ---------------------------------------
@@ -168,12 +177,38 @@ __global__ void polymul_generic_kernel(const uint8_t* __restrict__ a, const uint
 
 // ---- cfg2: GF(p^k) dot products ----------------------------------------------------
 // G lanes per dot product (G = 4 on the vector path: a warp covers 8 dots, each
-// load instruction reads 64 contiguous bytes per dot).  Each element pair is
-// DQT-packed into 32-bit words and multiplied with one IMAD.WIDE into a 64-bit
-// accumulator (the delayed reduction: no modular work inside the sum); the
-// sum is < q^(2k-1) <= 2^53, so REDQ (FP64 reciprocal + correction) and the
-// L/H fold tables finish it exactly as in src/gfext.py:fgdp.
+// load instruction reads 64 contiguous bytes per dot).  The delayed reduction
+// (no modular work inside the sum) accumulates the dot's DQT word
+//     r = sum_e pack(x_e) * pack(y_e) = sum_j S_j q^j,
+//     S_j = sum_e sum_{i+i'=j} x_e[i] y_e[i']          (every S_j < q: the bound)
+// On the vector path (K | 4) the digit sums S_j are formed directly on the
+// coefficient bytes by 4-lane byte dot products (IDP4A) -- the packed product's
+// digits without materialising the packed words: K = 2 costs 3 IDP4A + 3 logic
+// ops per 2 elements instead of two packings and a wide multiply each.  r is
+// assembled once per dot (exact, < 2^53), then REDQ (FP64 reciprocal +
+// correction) and the L/H fold tables finish it exactly as in src/gfext.py:fgdp.
 constexpr int GD_THREADS = 256;
+
+// byte selectors: Y_j[i] = y[j - i] (0 outside 0..3), so dp4a(x, Y_j) = sum_i x_i y_{j-i}
+__host__ __device__ constexpr uint32_t conv_selector(int j) {
+    uint32_t sel = 0;
+    for (int i = 0; i < 4; ++i) sel |= (uint32_t)((j - i >= 0 && j - i < 4) ? (j - i) : 4) << (4 * i);
+    return sel;
+}
+
+template <int K>
+QADIC_D void digit_sums_word(uint32_t x, uint32_t y, uint32_t (&S)[2 * K - 1]) {
+    if constexpr (K == 1) {
+        S[0] = __dp4a(x, y, S[0]);
+    } else if constexpr (K == 2) {  // two elements (bytes 0,1 and 2,3); S[0] holds S_0 + S_2 until the end
+        S[0] = __dp4a(x, y, S[0]);
+        S[2] = __dp4a(x & 0xFF00FF00u, y, S[2]);
+        S[1] = __dp4a(x, __byte_perm(y, 0, 0x2301), S[1]);
+    } else {  // K == 4: one element per word
+#pragma unroll
+        for (int j = 0; j < 7; ++j) S[j] = __dp4a(x, __byte_perm(y, 0, conv_selector(j)), S[j]);
+    }
+}
 
 template <int K, int G, bool VEC>
 __global__ void __launch_bounds__(GD_THREADS) gf_dot_kernel(const uint8_t* __restrict__ v1,
@@ -182,19 +217,6 @@ __global__ void __launch_bounds__(GD_THREADS) gf_dot_kernel(const uint8_t* __res
                                                             uint8_t* __restrict__ out) {
     pdl_wait();  // predecessor complete before any global access
     pdl_trigger();
-    // the L/H correction tables (gfext.py:176-213) staged in shared memory when small
-    extern __shared__ uint32_t gd_tab[];
-    const uint32_t* ltab = f.l_table;
-    const uint32_t* htab = f.h_table;
-    if (tab_smem > 0) {
-        for (int i = threadIdx.x; i < tab_smem; i += GD_THREADS) {
-            gd_tab[i] = __ldg(f.l_table + i);
-            gd_tab[tab_smem + i] = __ldg(f.h_table + i);
-        }
-        __syncthreads();
-        ltab = gd_tab;
-        htab = gd_tab + tab_smem;
-    }
     const int lane = threadIdx.x % G;
     const int64_t dot = ((int64_t)blockIdx.x * GD_THREADS + threadIdx.x) / G;
     const bool live = dot < batch;
@@ -204,37 +226,42 @@ __global__ void __launch_bounds__(GD_THREADS) gf_dot_kernel(const uint8_t* __res
         const int64_t row_bytes = len * K;
         const uint8_t* r1 = v1 + dot * row_bytes;
         const uint8_t* r2 = v2 + dot * row_bytes;
-        if (VEC) {  // 16-byte chunks hold 16/K whole elements (K | 16); words fit 32 bits
+        if constexpr (VEC) {  // 16-byte chunks hold 16/K whole elements (K | 4)
             const int64_t nchunks = row_bytes / 16;
-            int64_t ch = lane;
+            const uint4* c1 = reinterpret_cast<const uint4*>(r1);
+            const uint4* c2 = reinterpret_cast<const uint4*>(r2);
+            uint32_t S[2 * K - 1];
+#pragma unroll
+            for (int j = 0; j < 2 * K - 1; ++j) S[j] = 0;
             auto body = [&](const uint4& x, const uint4& y) {
-                const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-#pragma unroll
-                    for (int e = 0; e < 4 / K; ++e) {
-                        uint32_t wx = 0, wy = 0;
-#pragma unroll
-                        for (int l = 0; l < K; ++l) {
-                            wx |= ((xs[q] >> (8 * (e * K + l))) & 0xFFu) << (l * t);
-                            wy |= ((ys[q] >> (8 * (e * K + l))) & 0xFFu) << (l * t);
-                        }
-                        acc += (uint64_t)wx * wy;  // IMAD.WIDE.U32
-                    }
-                }
+                digit_sums_word<K>(x.x, y.x, S);
+                digit_sums_word<K>(x.y, y.y, S);
+                digit_sums_word<K>(x.z, y.z, S);
+                digit_sums_word<K>(x.w, y.w, S);
             };
-            for (; ch + 3 * G < nchunks; ch += 4 * G) {  // 8 loads in flight per lane
+            // every load of a lane issued before the first use (cfg2: 2 chunks per operand)
+            int64_t ch = lane;
+            for (; ch + 3 * G < nchunks; ch += 4 * G) {
                 uint4 x[4], y[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    x[i] = __ldg(reinterpret_cast<const uint4*>(r1) + ch + i * G);
-                    y[i] = __ldg(reinterpret_cast<const uint4*>(r2) + ch + i * G);
+                    x[i] = __ldg(c1 + ch + i * G);
+                    y[i] = __ldg(c2 + ch + i * G);
                 }
 #pragma unroll
                 for (int i = 0; i < 4; ++i) body(x[i], y[i]);
             }
-            for (; ch < nchunks; ch += G)
-                body(__ldg(reinterpret_cast<const uint4*>(r1) + ch), __ldg(reinterpret_cast<const uint4*>(r2) + ch));
+            if (ch + G < nchunks) {
+                const uint4 x0 = __ldg(c1 + ch), y0 = __ldg(c2 + ch), x1 = __ldg(c1 + ch + G), y1 = __ldg(c2 + ch + G);
+                body(x0, y0);
+                body(x1, y1);
+                ch += 2 * G;
+            }
+            if (ch < nchunks) body(__ldg(c1 + ch), __ldg(c2 + ch));
+            if constexpr (K == 2) S[0] -= S[2];
+            // the packed word: every S_j < q (host-checked), so r < q^(2K-1) <= 2^53
+#pragma unroll
+            for (int j = 0; j < 2 * K - 1; ++j) acc += (uint64_t)S[j] << (j * t);
         } else {
             for (int64_t e = lane; e < len; e += G) {
                 uint64_t wx = 0, wy = 0;
@@ -249,6 +276,20 @@ __global__ void __launch_bounds__(GD_THREADS) gf_dot_kernel(const uint8_t* __res
     }
 #pragma unroll
     for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    // the L/H correction tables (gfext.py:176-213) staged in shared memory when
+    // small -- after the operand loads, so their latency overlaps the table's
+    extern __shared__ uint32_t gd_tab[];
+    const uint32_t* ltab = f.l_table;
+    const uint32_t* htab = f.h_table;
+    if (tab_smem > 0) {
+        for (int i = threadIdx.x; i < tab_smem; i += GD_THREADS) {
+            gd_tab[i] = __ldg(f.l_table + i);
+            gd_tab[tab_smem + i] = __ldg(f.h_table + i);
+        }
+        __syncthreads();
+        ltab = gd_tab;
+        htab = gd_tab + tab_smem;
+    }
     if (!live || lane != 0) return;
     constexpr int ND = 2 * K - 2;
     uint32_t u[ND + 1];
@@ -273,15 +314,16 @@ __global__ void __launch_bounds__(GD_THREADS) gf_dot_kernel(const uint8_t* __res
 template <int K>
 static void launch_gf_dot(const uint8_t* v1, const uint8_t* v2, int64_t batch, int64_t len, const FieldConst& f,
                           uint8_t* out, cudaStream_t s) {
-    const bool vec = (16 % K == 0) && ((len * K) % 16 == 0) && ((uintptr_t)v1 % 16 == 0) &&
-                     ((uintptr_t)v2 % 16 == 0) && K * f.t <= 32;
+    // digit sums in 32-bit lanes: every S_j < q = 2^t
+    const bool vec = (4 % K == 0) && ((len * K) % 16 == 0) && ((uintptr_t)v1 % 16 == 0) &&
+                     ((uintptr_t)v2 % 16 == 0) && f.t <= 32;
     const int entries = 1 << (f.bb * K);
     const int ntab = entries <= 2048 ? entries : 0;  // <= 16 KB of tables: shared memory
     const size_t smem = (size_t)ntab * 2 * sizeof(uint32_t);
     if (vec) {
         constexpr int G = 4;  // 4 lanes per dot: a warp reads 64 contiguous bytes per dot per load
         const unsigned blocks = (unsigned)((batch * G + GD_THREADS - 1) / GD_THREADS);
-        launch_pdl(gf_dot_kernel<K, G, (16 % K == 0)>, dim3(blocks), dim3(GD_THREADS), smem, s, v1, v2, batch, len,
+        launch_pdl(gf_dot_kernel<K, G, (4 % K == 0)>, dim3(blocks), dim3(GD_THREADS), smem, s, v1, v2, batch, len,
                    f, ntab, out);
     } else {
         constexpr int G = 8;

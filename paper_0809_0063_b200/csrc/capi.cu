@@ -81,6 +81,19 @@ int check_launch(const char* what, int launched) {
     return QADIC_OK;
 }
 
+int num_sms_cached() {
+    static int cache[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cache[dev]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        cache[dev] = n > 0 ? n : 148;
+    }
+    return cache[dev];
+}
+
 double host_reciprocal_up(int64_t p) {
     double base = 1.0 / (double)p;
     // residual base*p - 1 is exact under FMA (base has 53 bits, p < 2^26)

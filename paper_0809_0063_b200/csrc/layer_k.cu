@@ -487,12 +487,7 @@ __global__ void __launch_bounds__(PK_THREADS) unpack_rows_tile_kernel(const uint
 // one wave of resident blocks (grid-stride over the tiles)
 template <typename F>
 static int grid_for_tiles(F kern, int64_t tiles) {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int sms = num_sms_cached();
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PK_THREADS, 0);
     if (occ < 1) occ = 1;
@@ -605,12 +600,7 @@ static int redq_launch(const uint64_t* r, int64_t n, int64_t p, int32_t t, int32
     const bool aligned = ((uintptr_t)r % 16 == 0) && (!digits || (uintptr_t)digits % 16 == 0) &&
                          (!packed || (uintptr_t)packed % 16 == 0);
     if (aligned && d >= 1 && d <= 6) {
-        static int sms = 0;
-        if (!sms) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        }
+        const int sms = num_sms_cached();
         const int64_t pairs = (n + 1) / 2;
         const int grid = (int)std::min<int64_t>((pairs + RQ_THREADS - 1) / RQ_THREADS, (int64_t)sms * 8);
         const double inv = host_reciprocal_up(p), bnd = host_case2_bound();

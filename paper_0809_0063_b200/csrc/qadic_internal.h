@@ -15,6 +15,8 @@ double host_reciprocal_up(int64_t p);
 double host_case2_bound();
 
 void set_error(int code, const char* fmt, ...);
+// multiprocessor count of the current device (cached per device)
+int num_sms_cached();
 // `launched`: kernels this call site launched outside QADIC_TIMED (those count themselves)
 int check_launch(const char* what, int launched);
 void count_launch(int n = 1);

@@ -172,7 +172,12 @@ class TestGFDot:
         f = _field(golden_scalars, "gf25_20")
         assert np.array_equal(f.fgdp_batch(golden["gf25_v1"], golden["gf25_v2"]), golden["gf25_out"])
 
-    @pytest.mark.parametrize("p,k,n", [(3, 2, 64), (7, 3, 9), (2, 4, 20), (5, 1, 100), (3, 2, 5), (3, 3, 17)])
+    # vector (IDP4A digit-sum) path: k in {1, 2, 4} with n*k % 16 == 0, at 1, 3, 6, 7,
+    # 8, 9, 11, 32 and 256 chunks per operand row (every load-depth branch); the
+    # scalar path otherwise
+    @pytest.mark.parametrize("p,k,n", [(3, 2, 64), (7, 3, 9), (2, 4, 20), (5, 1, 100), (3, 2, 5), (3, 3, 17),
+                                       (3, 2, 8), (3, 2, 24), (3, 2, 72), (5, 1, 96), (3, 2, 256),
+                                       (2, 1, 4096), (7, 2, 32), (3, 4, 4), (2, 4, 28)])
     def test_vs_oracle(self, p, k, n):
         f = gfext.build_field(p, k, max_dot_length=n)
         of = O.build_field(p, k, max_dot_length=n)
@@ -563,3 +568,25 @@ class TestABIErrors:
         assert L.qadic_gf_matmul_u8(ctypes.byref(bad), N.ptr(a), N.ptr(a), 64, 64, 64, 0, 0, N.ptr(ws), need,
                                     N.ptr(c), s) == N.ERR_UNSUPPORTED
         torch.cuda.synchronize()
+
+
+# ---------------------------------------------------------------------------
+# Diagnostics: the measured pipe peaks the bench reports beside the nominal ones
+# ---------------------------------------------------------------------------
+class TestPipeProbe:
+    @pytest.mark.parametrize("kind,lo,hi", [("mxf4", 2e15, 1.0e16), ("i8", 1e15, 5.0e15), ("f64", 1e13, 4.5e13)])
+    def test_probe_rate_plausible(self, kind, lo, hi):
+        from paper_0809_0063_b200 import _native as N
+
+        rate, ms = N.pipe_peak(kind, "residues", 4000)
+        assert ms > 0 and lo < rate < hi, (kind, rate)
+
+    def test_probe_rejects_bad_arguments(self):
+        import ctypes
+
+        from paper_0809_0063_b200 import _native as N
+
+        ops, ms = ctypes.c_double(), ctypes.c_float()
+        L = N.lib()
+        assert L.qadic_diag_pipe_peak(3, 0, 10, ctypes.byref(ops), ctypes.byref(ms), N.stream_ptr()) == N.ERR_VALUE
+        assert L.qadic_diag_pipe_peak(0, 0, 0, ctypes.byref(ops), ctypes.byref(ms), N.stream_ptr()) == N.ERR_VALUE
