@@ -17,6 +17,7 @@ namespace qadic {
 
 struct PolyConst {
     uint32_t p, t, corr, magic;
+    uint32_t negp;  // -p mod 2^32: u = r + negp * s is one IMAD
     double invp_up, bound;
 };
 
@@ -31,6 +32,18 @@ constexpr int PM_PER = 8;  // pairs per thread (56 output bytes = 7 x 8-byte sto
 
 QADIC_D uint32_t pack4_bytes(uint32_t x, int t, uint32_t m) {
     return (x & m) | (((x >> 8) & m) << t) | (((x >> 16) & m) << (2 * t)) | (((x >> 24) & m) << (3 * t));
+}
+
+// byte selector for 4 consecutive stream bytes: starting at byte `first` of
+// the first operand, switching to byte 0 of the second after `take` bytes
+// (take = 0: all four from the 8-byte concatenation starting at `first`)
+__host__ __device__ constexpr uint32_t stream_sel(int first, int take) {
+    uint32_t sel = 0;
+    for (int i = 0; i < 4; ++i) {
+        const int b = take == 0 ? first + i : (i < take ? first + i : 4 + (i - take));
+        sel |= (uint32_t)b << (4 * i);
+    }
+    return sel;
 }
 
 // byte-lane v mod p for lanes < 2p
@@ -64,18 +77,15 @@ __global__ void __launch_bounds__(PM_THREADS, 4) polymul_k4_kernel(const uint8_t
             bv[j] = p0 + j < n ? *reinterpret_cast<const uint32_t*>(b + (p0 + j) * 4) : 0u;
         }
     }
-    constexpr uint32_t M = (1u << T) - 1;
+    constexpr uint32_t PK_LO = 1u | ((1u << T) << 8), PK_HI = (1u << 16) | ((1u << T) << 24);
     const double two52 = 4503599627370496.0;
-    uint32_t o[PM_PER * 7 / 4];
-#pragma unroll
-    for (int q = 0; q < PM_PER * 7 / 4; ++q) o[q] = 0;
+    uint32_t vlo[PM_PER], vhi[PM_PER];  // pair j's 7 result bytes: vlo = bytes 0..3, vhi = bytes 4..6
 #pragma unroll
     for (int j = 0; j < PM_PER; ++j) {
         const uint32_t x = av[j], y = bv[j];
-        const uint32_t wa = (x & M) | ((x >> (8 - T)) & (M << T)) | ((x >> (16 - 2 * T)) & (M << (2 * T))) |
-                            ((x >> (24 - 3 * T)) & (M << (3 * T)));
-        const uint32_t wb = (y & M) | ((y >> (8 - T)) & (M << T)) | ((y >> (16 - 2 * T)) & (M << (2 * T))) |
-                            ((y >> (24 - 3 * T)) & (M << (3 * T)));
+        // DQT pack by two byte dot products: (a0 + a1 q) + (a2 + a3 q) q^2 (digits < p <= q, q <= 2^7)
+        const uint32_t wa = __dp4a(x, PK_LO, 0u) + (__dp4a(x, PK_HI, 0u) << (2 * T));
+        const uint32_t wb = __dp4a(y, PK_LO, 0u) + (__dp4a(y, PK_HI, 0u) << (2 * T));
         // every digit of the product is < q (checked on the host), so r < q^7 <= 2^49
         const double rr = __dmul_rn(__hiloint2double(0x43300000, (int)wa) - two52,
                                     __hiloint2double(0x43300000, (int)wb) - two52);
@@ -85,27 +95,34 @@ __global__ void __launch_bounds__(PM_THREADS, 4) polymul_k4_kernel(const uint8_t
         // u_i only matters mod 2^8 (it is small): byte windows of r and s
         uint32_t u[7];
 #pragma unroll
-        for (int i = 0; i < 7; ++i) u[i] = (uint32_t)(ri >> (i * T)) - c.p * (uint32_t)(si >> (i * T));
-        uint64_t v;  // the 7 result bytes
+        for (int i = 0; i < 7; ++i) u[i] = (uint32_t)(ri >> (i * T)) + c.negp * (uint32_t)(si >> (i * T));
         if (CORR1) {  // mu_i = (u_i + u_{i+1}) mod p on byte lanes
+            // U0 = [u0 u1 u2 u3], U1 = [u1 u2 u3 u4], W0 = [u4 u5 u6 0], W1 = [u5 u6 0 0]
             const uint32_t U0 = __byte_perm(__byte_perm(u[0], u[1], 0x0040), __byte_perm(u[2], u[3], 0x0040), 0x5410);
-            const uint32_t U1 = __byte_perm(__byte_perm(u[1], u[2], 0x0040), __byte_perm(u[3], u[4], 0x0040), 0x5410);
-            const uint32_t W0 = __byte_perm(__byte_perm(u[4], u[5], 0x0040), u[6], 0x0410);
-            const uint32_t W1 = __byte_perm(u[5], u[6], 0x0040) & 0xFFFFu;
-            const uint32_t V0 = lanes_mod_2p(U0 + U1, c.p), V1 = lanes_mod_2p(W0 + W1, c.p) & 0xFFFFFFu;
-            v = (uint64_t)V0 | ((uint64_t)V1 << 32);
+            const uint32_t U1 = __byte_perm(U0, u[4], 0x4321);
+            const uint32_t W0 = __byte_perm(__byte_perm(u[4], u[5], 0x0040), u[6], 0x0410) & 0xFFFFFFu;
+            const uint32_t W1 = W0 >> 8;
+            // lane 2 of W0 + W1 is u6 < p (unchanged by the reduction), lane 3 is 0
+            const uint32_t V0 = lanes_mod_2p(U0 + U1, c.p), V1 = lanes_mod_2p(W0 + W1, c.p);
+            vlo[j] = V0;
+            vhi[j] = V1;
         } else {
-            v = 0;
+            uint64_t v = 0;
 #pragma unroll
             for (int i = 0; i < 6; ++i) v |= (uint64_t)mod_small(u[i] + c.corr * u[i + 1], c.p, c.magic) << (8 * i);
             v |= (uint64_t)(u[6] & 0xFF) << 48;
+            vlo[j] = (uint32_t)v;
+            vhi[j] = (uint32_t)(v >> 32);
         }
-        // bytes 7j .. 7j+6 of the thread's output stream
-        const int pos = j * 7, w = pos >> 2, sh = 8 * (pos & 3);
-        const uint64_t lo = v << sh;
-        o[w] |= (uint32_t)lo;
-        o[w + 1] |= (uint32_t)(lo >> 32);
-        if (sh > 8) o[w + 2] |= (uint32_t)(v >> (64 - sh));
+    }
+    // the thread's 56-byte output stream (pair j at bytes 7j..7j+6): every
+    // aligned word is one byte permute of two result words
+    uint32_t o[PM_PER * 7 / 4];
+#pragma unroll
+    for (int w = 0; w < PM_PER * 7 / 4; ++w) {
+        const int j = 4 * w / 7, k = 4 * w - 7 * j;  // the word starts at byte k of pair j
+        if (k + 4 <= 7) o[w] = __byte_perm(vlo[j], vhi[j], stream_sel(k, 0));
+        else o[w] = __byte_perm(vhi[j], vlo[j + 1], stream_sel(k - 4, 7 - k));
     }
     uint8_t* dst = out + p0 * 7;
     // a warp with all its pairs in range stages its 32 x 56 output bytes in shared
@@ -382,6 +399,7 @@ int qadic_polymul_batch_u8(const uint8_t* a, const uint8_t* b, int64_t n, int32_
     const uint64_t q = 1ull << t;
     c.corr = (q % c.p == 0) ? 0u : (uint32_t)((c.p - q % c.p) % c.p);
     c.magic = small_magic(c.p);
+    c.negp = 0u - c.p;
     c.invp_up = host_reciprocal_up(p);
     c.bound = host_case2_bound();
     cudaStream_t s = (cudaStream_t)stream;

@@ -151,9 +151,12 @@ template <int D>
 __device__ __forceinline__ void redq_word(uint64_t ri, uint64_t p, int t, double invp_up, double bound, uint64_t corr,
                                           int mode, const uint8_t* tab, uint64_t (&out)[D + 1], uint64_t& word) {
     const uint64_t s = div_p(ri, p, invp_up, bound);
+    // u_i = floor(r / 2^(it)) mod p lies in [0, p): 32-bit wrap-around arithmetic
+    // on the low words is exact (one funnel shift per operand + one IMAD with -p)
+    const uint32_t negp = 0u - (uint32_t)p;
     uint64_t u[D + 1];
 #pragma unroll
-    for (int i = 0; i <= D; ++i) u[i] = (ri >> (i * t)) - p * (s >> (i * t));
+    for (int i = 0; i <= D; ++i) u[i] = (uint32_t)(ri >> (i * t)) + negp * (uint32_t)(s >> (i * t));
     word = 0;
 #pragma unroll
     for (int i = 0; i <= D; ++i) {
@@ -599,7 +602,7 @@ static int redq_launch(const uint64_t* r, int64_t n, int64_t p, int32_t t, int32
     cudaStream_t s = (cudaStream_t)stream;
     const bool aligned = ((uintptr_t)r % 16 == 0) && (!digits || (uintptr_t)digits % 16 == 0) &&
                          (!packed || (uintptr_t)packed % 16 == 0);
-    if (aligned && d >= 1 && d <= 6) {
+    if (aligned && d >= 1 && d <= 6 && p < (1ll << 31)) {  // digits in [0, p) fit the 32-bit arithmetic
         const int sms = num_sms_cached();
         const int64_t pairs = (n + 1) / 2;
         const int grid = (int)std::min<int64_t>((pairs + RQ_THREADS - 1) / RQ_THREADS, (int64_t)sms * 8);

@@ -85,6 +85,16 @@ class TestLayerK:
         for p, t, d in ((3, 17, 2), (7, 10, 4), (5, 13, 3), (127, 20, 2)):
             assert np.array_equal(_kernels.redq_compress_u64(r, p, t, d), O.redq_compress_u64(r, p, t, d))
 
+    @pytest.mark.parametrize("p,t,d", [((1 << 31) - 1, 20, 2), ((1 << 31) + 11, 20, 2), ((1 << 40) + 15, 9, 6),
+                                       (2, 1, 6), (127, 9, 6), (65521, 16, 3)])
+    def test_redq_any_word_any_p(self, p, t, d):
+        """Full-range uint64 words, p on both sides of the 32-bit digit path's limit."""
+        rng = np.random.default_rng(p % 1000 + t)
+        r = rng.integers(0, 1 << 64, 4099, dtype=np.uint64)
+        assert np.array_equal(_kernels.redq_compress_u64(r, p, t, d), O.redq_compress_u64(r, p, t, d))
+        if p < 1 << 32:  # the correction's c * u stays inside 64 bits
+            assert np.array_equal(redq.reduce_words_digits(r, p, t, d), O.reduce_words_digits(r, p, t, d))
+
     def test_redq_rejects_wide_span(self):
         with pytest.raises(ValueError):
             _kernels.redq_compress_u64(np.zeros(3, np.uint64), 3, 16, 4)
