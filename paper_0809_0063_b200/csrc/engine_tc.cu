@@ -31,6 +31,7 @@
 // (4-11 when fused) epilogue (tcgen05.ld -> mod p -> residues) overlapping the
 // next tile through two TMEM accumulators.
 #include <cuda.h>
+#include <stdio.h>
 
 #include <utility>
 
@@ -75,12 +76,18 @@ struct Cfg<KIND_F4> {
 // FUSE_K > 0: the epilogue applies the plane combination C_l = sum_s W[l][s] D_s
 // itself, accumulating the S plane results of one output tile in registers
 // (8 epilogue warps, byte lanes).
-template <int KIND, bool PAIR, int FUSE_K = 0>
+// MC: two CTA pairs per cluster (4 CTAs) work on vertically adjacent tiles of
+// the same B columns; each pair TMA-loads half of the B tile and multicasts it
+// to both pairs, so L2 -> SM operand traffic drops by a quarter.  The B slot is
+// then 2 x 64 rows (slices land at 8-row swizzle-atom boundaries).
+template <int KIND, bool PAIR, int FUSE_K = 0, bool MC = false>
 struct Geo {
     static constexpr int BN = Cfg<KIND>::BN;
-    static constexpr int B_ROWS = PAIR ? BN / 2 : BN;  // B rows this CTA loads
+    static constexpr int B_ROWS = PAIR ? BN / 2 : BN;  // B rows this CTA's MMA half reads
+    static constexpr int B_BOX = MC ? 64 : B_ROWS;      // rows per B TMA box
+    static constexpr int B_SLOT = MC ? 2 * B_BOX : B_ROWS;
     static constexpr int A_BYTES = BM * BK;
-    static constexpr int B_BYTES = B_ROWS * BK;
+    static constexpr int B_BYTES = B_SLOT * BK;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int ACC_BYTES = 0;
     // as many stages as 227 KB of shared memory holds (deeper prefetch hides
@@ -127,6 +134,11 @@ struct Params {
     // exact uint64 GEMM through byte planes (KIND_I8): C64 = (acc64 ? C64 : 0) + (u32 D << shift)
     uint64_t* c64;
     int shift, acc64;
+    // column-tile range of this launch: tiles n_tile0 .. n_tile0 + n_tiles - 1
+    int n_tile0;
+    // launched as the programmatic dependent of a concurrent GEMM launch: wait for
+    // that grid to complete before exiting, so stream order still covers both
+    int pdl_tail;
 };
 
 // tile index -> (plane, m tile, n tile).  Unfused: planes outermost.  Fused:
@@ -177,12 +189,19 @@ __device__ __forceinline__ void decode_tile(int tile, const Params& prm, int& pl
     }
 }
 
-template <int KIND, bool PAIR, int FUSE_K = 0>
+template <int KIND, bool PAIR, int FUSE_K = 0, bool MC = false>
 __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
     gemm_modp_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ CUtensorMap tmap_b,
-                     const __grid_constant__ Params prm) {
+                     const __grid_constant__ Params prm_in) {
     using namespace sm100;
-    using G = Geo<KIND, PAIR, FUSE_K>;
+    using G = Geo<KIND, PAIR, FUSE_K, MC>;
+    static_assert(!MC || (PAIR && FUSE_K == 0), "multicast needs the CTA-pair, unfused kernel");
+    // MC: work units cover two m tiles (one per pair of the cluster)
+    Params prm = prm_in;
+    if (MC) {
+        prm.m_tiles = (prm_in.m_tiles + 1) / 2;
+        pdl_trigger();  // the concurrent tail launch may take the SMs no 4-CTA cluster fits on
+    }
     constexpr int BN = G::BN;
     constexpr int NST = G::STAGES_N;
     extern __shared__ uint8_t smem_raw[];
@@ -195,10 +214,14 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
-    const uint32_t rank = PAIR ? cluster_ctarank() : 0;
+    constexpr int CL = MC ? 4 : (PAIR ? 2 : 1);  // CTAs per cluster
+    const uint32_t crank = PAIR ? cluster_ctarank() : 0;
+    const uint32_t rank = crank & 1;                // rank within the CTA pair
+    const uint32_t pidx = MC ? (crank >> 1) : 0;    // pair within the cluster
+    const uint32_t pair_leader = crank & ~1u;       // cluster rank of this pair's leader
     const bool leader = rank == 0;
-    const int group_id = PAIR ? blockIdx.x / 2 : blockIdx.x;
-    const int num_groups = PAIR ? gridDim.x / 2 : gridDim.x;
+    const int group_id = blockIdx.x / CL;
+    const int num_groups = gridDim.x / CL;
     // work units: one tile of one plane; fused, one output tile with all its
     // planes processed back to back by the same CTA (group)
     const int plane_tiles = prm.m_tiles * prm.n_tiles;
@@ -210,7 +233,7 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
         tma_prefetch(&tmap_b);
         for (int s = 0; s < NST; ++s) {
             mbar_init(&full_bar[s], 1);
-            mbar_init(&empty_bar[s], 1);
+            mbar_init(&empty_bar[s], MC ? 2 : 1);  // MC: both pairs' MMAs free the stage
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tmem_full[a], 1);
@@ -246,15 +269,25 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                 const int tile = u * per_unit + sp;
                 int pl, mt, nt;
                 decode_tile<FUSE_K>(tile, prm, pl, mt, nt);
+                if (MC) mt = 2 * mt + (int)pidx;
+                nt += prm.n_tile0;
                 const int arow = (int)(pl * prm.M) + mt * G::TILE_M + (int)rank * BM;
                 // the pair splits the tile's (possibly narrowed, see tile_n) columns in halves
                 const int brow = (int)(pl * prm.N) + nt * BN + (int)rank * (tile_n<BN>(prm, nt) / 2);
+                // MC: CTA (pair i, rank r) loads slice i of half r and multicasts it to both pairs
+                const uint16_t mc_mask = (uint16_t)((1u << crank) | (1u << (crank ^ 2u)));
                 for (int kb = 0; kb < prm.num_kb; ++kb) {
                     mbar_wait(&empty_bar[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * G::STAGE_BYTES;
                     uint8_t* sb = sa + G::A_BYTES;
                     if (prm.diag_noload && (u != group_id || kb >= NST)) {  // wrong results: power probe
                         if (!PAIR || leader) mbar_arrive(&full_bar[stage]);
+                    } else if (MC) {
+                        const uint32_t lbar = map_to_rank(&full_bar[stage], pair_leader);
+                        if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * G::STAGE_BYTES);
+                        tma_load_2d_pair(sa, &tmap_a, lbar, kb * BK, arow);
+                        tma_load_2d_pair_mc(sb + pidx * G::B_BOX * BK, &tmap_b, lbar, kb * BK,
+                                            brow + (int)pidx * G::B_BOX, mc_mask);
                     } else if (PAIR) {
                         const uint32_t lbar = map_to_rank(&full_bar[stage], 0);
                         if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * G::STAGE_BYTES);
@@ -278,6 +311,7 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
         for (int sp = 0; sp < per_unit; ++sp, ++local) {
             int pl, mt, nt;
             decode_tile<FUSE_K>(u * per_unit + sp, prm, pl, mt, nt);
+            nt += prm.n_tile0;
             const uint32_t nn = (uint32_t)tile_n<BN>(prm, nt);
             const uint32_t idesc = KIND == KIND_I8 ? idesc_u8_s32(G::TILE_M, nn) : idesc_mxf4(G::TILE_M, nn);
             const int acc = local & 1;
@@ -305,8 +339,8 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                         }
                     }
                     if (PAIR) {
-                        umma_commit_pair(&empty_bar[stage], 0x3);
-                        if (kb == prm.num_kb - 1) umma_commit_pair(&tmem_full[acc], 0x3);
+                        umma_commit_pair(&empty_bar[stage], MC ? 0xF : 0x3);
+                        if (kb == prm.num_kb - 1) umma_commit_pair(&tmem_full[acc], (uint16_t)(0x3u << (2 * pidx)));
                     } else {
                         umma_commit(&empty_bar[stage]);
                         if (kb == prm.num_kb - 1) umma_commit(&tmem_full[acc]);
@@ -320,8 +354,8 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
         // ===== epilogue: TMEM -> registers -> mod p -> uint8 =====
         const int ew = warp - 4;   // TMEM lane quarter this warp may access (unfused: 4 warps)
         const int ew4 = warp & 3;  // fused (8 warps): warps 4+q and 8+q share lane quarter q
-        const uint32_t empty_addr0 = PAIR ? map_to_rank(&tmem_empty[0], 0) : 0;
-        const uint32_t empty_addr1 = PAIR ? map_to_rank(&tmem_empty[1], 0) : 0;
+        const uint32_t empty_addr0 = PAIR ? map_to_rank(&tmem_empty[0], pair_leader) : 0;
+        const uint32_t empty_addr1 = PAIR ? map_to_rank(&tmem_empty[1], pair_leader) : 0;
         int local = 0;
         // fused: this thread's byte-lane plane sums, 16 columns x FUSE_K bytes per chunk
         uint32_t facc[FUSE_K ? (BN / 16 + 1) / 2 : 1][FUSE_K ? 4 * FUSE_K : 1];
@@ -331,6 +365,8 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
             const int tile = u * per_unit + sp;
             int pl, mt, nt;
             decode_tile<FUSE_K>(tile, prm, pl, mt, nt);
+            if (MC) mt = 2 * mt + (int)pidx;
+            nt += prm.n_tile0;
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
             mbar_wait(&tmem_full[acc], acc_phase);
@@ -490,6 +526,7 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
         if (PAIR) tmem_dealloc_pair<512>(tmem_base);
         else tmem_dealloc<512>(tmem_base);
     }
+    if (prm.pdl_tail) pdl_wait();
 }
 
 // ---------------------------------------------------------------------------
@@ -731,6 +768,16 @@ static bool pair_mode() {
     return mode == 1;
 }
 
+// B-tile multicast across two CTA pairs for the unfused fp4k GEMM (QADIC_MCAST=1)
+static bool mcast_mode() {
+    static int mode = -1;
+    if (mode < 0) {
+        const char* e = getenv("QADIC_MCAST");
+        mode = (e && e[0] == '1') ? 1 : 0;
+    }
+    return mode == 1;
+}
+
 // E2M1 nibble codes of the centred residues 0..p-1 (p <= 7), packed 4 bits each
 // E2M1 codes of the residue representatives (4-bit code of residue r at nibble r).
 // Every operand value is a half-integer code under block scales 2^1 on both
@@ -804,35 +851,80 @@ static Layout plan(int kind, const uint8_t* a, int64_t m, int64_t kdim, int64_t 
     return L;
 }
 
-template <int KIND, bool PAIR, int FUSE_K = 0>
-static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, Params prm, cudaStream_t s,
-                       const char* label = nullptr) {
-    using G = Geo<KIND, PAIR, FUSE_K>;
-    auto kern = gemm_modp_kernel<KIND, PAIR, FUSE_K>;
+template <int KIND, bool PAIR, int FUSE_K = 0, bool MC = false>
+static cudaLaunchConfig_t gemm_config(cudaStream_t s) {
+    using G = Geo<KIND, PAIR, FUSE_K, MC>;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM);
+        cudaFuncSetAttribute(gemm_modp_kernel<KIND, PAIR, FUSE_K, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)G::SMEM);
         attr = true;
     }
-    const int tiles = prm.m_tiles * prm.n_tiles;
-    const int per = PAIR ? 2 : 1;
-    int grid = num_sms() / per;
-    if (tiles < grid) grid = tiles;
-    grid *= per;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(FUSE_K ? THREADS_FUSED : THREADS);
     cfg.dynamicSmemBytes = G::SMEM;
     cfg.stream = s;
-    cudaLaunchAttribute attrs[1];
+    return cfg;
+}
+
+// Co-resident clusters of the persistent GEMM (GPC shapes leave some SMs out
+// of 4-CTA clusters: 33 x 4 of 148 on B200; a second wave would double the time).
+template <int KIND, bool PAIR, int FUSE_K = 0, bool MC = false>
+static int gemm_max_clusters() {
+    static int max_clusters = 0;
+    if (!max_clusters) {
+        const int per = MC ? 4 : (PAIR ? 2 : 1);
+        cudaLaunchConfig_t cfg = gemm_config<KIND, PAIR, FUSE_K, MC>(nullptr);
+        cfg.gridDim = dim3((unsigned)(num_sms() / per * per));
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = per;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        if (cudaOccupancyMaxActiveClusters(&max_clusters, (void*)gemm_modp_kernel<KIND, PAIR, FUSE_K, MC>, &cfg) !=
+                cudaSuccess ||
+            max_clusters < 1)
+            max_clusters = num_sms() / per;
+        cudaGetLastError();
+        if (getenv_flag("QADIC_VERBOSE"))
+            fprintf(stderr, "[qadic] gemm<%d,%d,%d,%d>: %d co-resident clusters of %d CTAs (%d SMs)\n", KIND,
+                    (int)PAIR, FUSE_K, (int)MC, max_clusters, per, num_sms());
+    }
+    return max_clusters;
+}
+
+// One persistent GEMM launch.  max_clusters > 0 caps the grid (the tail launch
+// of a split runs on the SMs the 4-CTA clusters leave free); pdl_secondary
+// launches it as the programmatic dependent of the launch just before it.
+template <int KIND, bool PAIR, int FUSE_K = 0, bool MC = false>
+static cudaError_t launch_gemm_raw(const CUtensorMap& ta, const CUtensorMap& tb, const Params& prm, cudaStream_t s,
+                                   int max_clusters = 0, bool pdl_secondary = false) {
+    const int per = MC ? 4 : (PAIR ? 2 : 1);  // CTAs per cluster
+    const int tiles = (MC ? (prm.m_tiles + 1) / 2 : prm.m_tiles) * prm.n_tiles;  // cluster work units per plane
+    int grid = gemm_max_clusters<KIND, PAIR, FUSE_K, MC>();
+    if (max_clusters > 0 && max_clusters < grid) grid = max_clusters;
+    if (tiles < grid) grid = tiles;
+    cudaLaunchConfig_t cfg = gemm_config<KIND, PAIR, FUSE_K, MC>(s);
+    cfg.gridDim = dim3((unsigned)(grid * per));
+    cudaLaunchAttribute attrs[2];
     attrs[0].id = cudaLaunchAttributeClusterDimension;
     attrs[0].val.clusterDim.x = per;
     attrs[0].val.clusterDim.y = 1;
     attrs[0].val.clusterDim.z = 1;
+    attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attrs;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_secondary ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, gemm_modp_kernel<KIND, PAIR, FUSE_K, MC>, ta, tb, prm);
+}
+
+template <int KIND, bool PAIR, int FUSE_K = 0, bool MC = false>
+static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, Params prm, cudaStream_t s,
+                       const char* label = nullptr) {
     const char* name = label ? label : (KIND == KIND_I8 ? "i8 gemm" : "fp4 gemm");
-    QADIC_TIMED(name, s, cudaLaunchKernelEx(&cfg, kern, ta, tb, prm));
+    QADIC_TIMED(name, s, (launch_gemm_raw<KIND, PAIR, FUSE_K, MC>(ta, tb, prm, s)));
     return check_launch(name);
 }
 
@@ -1788,8 +1880,49 @@ static int run_kara(const FieldConst& f, const uint8_t* a, const uint8_t* b, int
         prm.c_plane = m * L.ldd;
         prm.nibble_out = 1;
     }
-    rc = pair ? launch_gemm<KIND_F4, true>(ta, tb, prm, s, "fp4k gemm")
-              : launch_gemm<KIND_F4, false>(ta, tb, prm, s, "fp4k gemm");
+    if (pair && mcast_mode() && prm.n_full >= 2) {
+        // B tiles multicast across two CTA pairs (4-CTA clusters, 64-row boxes) on
+        // the first column tiles; only C clusters of 4 fit (33 on B200), so the
+        // last column tiles run concurrently as a CTA-pair launch on the SMs left
+        // over, sized so both finish together (a multicast pair-tile costs
+        // 1/QADIC_MCAST_GAIN of a plain one).
+        CUtensorMap tbm;
+        rc = make_tmap(&tbm, bs, (kdim + 1) / 2, L.S * n, L.ldk, Geo<KIND_F4, true, 0, true>::B_BOX);
+        if (rc) return rc;
+        const int C = gemm_max_clusters<KIND_F4, true, 0, true>();
+        const int pairs_left = (num_sms() - 4 * C) / 2;
+        const double gain = getenv("QADIC_MCAST_GAIN") ? atof(getenv("QADIC_MCAST_GAIN")) : 1.06;
+        const double narrow = prm.n_tiles > prm.n_full ? (double)(n - (int64_t)prm.n_full * BN) / BN : 0.0;
+        const double share = pairs_left / (pairs_left + 2.0 * C * gain);  // of the tile work
+        int tail_full = (int)(share * (prm.n_full + narrow) - narrow + 0.5);
+        if (tail_full < 0) tail_full = 0;
+        if (tail_full > prm.n_full - 1) tail_full = prm.n_full - 1;
+        const bool split = pairs_left >= 1 && (tail_full > 0 || prm.n_tiles > prm.n_full);
+        Params pm = prm, pt = prm;
+        pm.n_tile0 = 0;
+        pm.n_full = pm.n_tiles = split ? prm.n_full - tail_full : prm.n_tiles;
+        if (!split) pm.n_full = prm.n_full;
+        pt.n_tile0 = pm.n_tiles;
+        pt.n_tiles = prm.n_tiles - pm.n_tiles;
+        pt.n_full = prm.n_full - pm.n_tiles;
+        pt.pdl_tail = 1;
+        const int pi = prof_begin(s, "fp4k gemm");
+        cudaError_t e = launch_gemm_raw<KIND_F4, true, 0, true>(ta, tbm, pm, s);
+        count_launch(1);
+        if (e == cudaSuccess && split) {
+            e = launch_gemm_raw<KIND_F4, true>(ta, tb, pt, s, pairs_left, true);
+            count_launch(1);
+        }
+        prof_end(pi, s);
+        if (e != cudaSuccess) {
+            set_error(QADIC_ERR_CUDA, "fp4k gemm (multicast): %s", cudaGetErrorString(e));
+            return QADIC_ERR_CUDA;
+        }
+        rc = check_launch("fp4k gemm", 0);
+    } else {
+        rc = pair ? launch_gemm<KIND_F4, true>(ta, tb, prm, s, "fp4k gemm")
+                  : launch_gemm<KIND_F4, false>(ta, tb, prm, s, "fp4k gemm");
+    }
     if (rc || k == 1) return rc;
     const uint32_t magic = small_magic(f.p);
     switch (k) {

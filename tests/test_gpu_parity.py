@@ -600,3 +600,41 @@ class TestPipeProbe:
         L = N.lib()
         assert L.qadic_diag_pipe_peak(3, 0, 10, ctypes.byref(ops), ctypes.byref(ms), N.stream_ptr()) == N.ERR_VALUE
         assert L.qadic_diag_pipe_peak(0, 0, 0, ctypes.byref(ops), ctypes.byref(ms), N.stream_ptr()) == N.ERR_VALUE
+
+
+# ---------------------------------------------------------------------------
+# Opt-in engine variant read once per process (QADIC_MCAST=1: B tiles multicast
+# across two CTA pairs + a concurrent CTA-pair tail launch), so it runs in a
+# child process.
+# ---------------------------------------------------------------------------
+_MCAST_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from oracle import qadic_oracle as O
+from paper_0809_0063_b200 import cmm, gfext, workloads as W
+from paper_0809_0063_b200.params import cmm_params
+g = W.rng(77)
+for (m, kk, n) in ((600, 300, 1000), (512, 256, 8192 // 4 + 7)):
+    f = gfext.build_field(7, 3, irreducible=[5, 0, 0, 1], max_dot_length=kk)
+    of = O.build_field(7, 3, irreducible=[5, 0, 0, 1], max_dot_length=kk)
+    a = g.integers(0, 7, (m, kk, 3), dtype=np.uint8)
+    b = g.integers(0, 7, (kk, n, 3), dtype=np.uint8)
+    assert np.array_equal(f.matmul_coeffs(a, b, engine="fp4k"), O.gf_matmul_planes(of, a, b)), (m, kk, n)
+u = np.triu(g.integers(0, 2, (1200, 1200)), 1)
+a = (u + u.T).astype(np.uint8)
+got = cmm.right_cmm(a, cmm.compress_rows(a, cmm_params(3, 1200, strict=True)), engine="fp4k")
+assert np.array_equal(got, O.modmatmul_planes(a, a, 3))
+print("mcast ok")
+"""
+
+
+def test_fp4k_multicast_variant():
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, QADIC_MCAST="1")
+    r = subprocess.run([sys.executable, "-c", _MCAST_CHILD, root], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "mcast ok" in r.stdout, r.stderr[-2000:]

@@ -11,6 +11,7 @@ mkdir -p $O
 NCU="ncu --clock-control none"
 B="python bench.py --no-cpu-baseline"
 ok=1
+python bench.py > $O/bench_default.json 2>>$O/bench.err || ok=0   # the driver's default command
 for c in 1 2; do $B --config $c --warmup 5 > $O/bench_cfg$c.json 2>>$O/bench.err || ok=0; done
 for c in redq pack unpack mm64; do python bench.py --config $c > $O/bench_$c.json 2>>$O/bench.err || ok=0; done
 for c in 3 4 5; do
@@ -43,6 +44,9 @@ python bench.py --config pack --steps 3 > /dev/null 2>&1 && $NCU --set full -k r
 ncu -i $O/pack.ncu-rep --page raw --csv > $O/pack_raw.csv 2>/dev/null
 ncu -i $O/pack.ncu-rep --page details --csv > $O/pack_details.csv 2>/dev/null
 # measured ceilings and host-side paths on the same box
+python tools/pipe_peak.py 1.0 > $O/pipe_peaks.json 2>>$O/bench.err
+python bench.py --config unpack --steps 3 > /dev/null 2>&1 && $NCU --set full -k regex:unpack_rows -s 2 -c 1 -o $O/unpack -f python bench.py --config unpack --steps 3 > $O/unpack.log 2>&1
+ncu -i $O/unpack.ncu-rep --page raw --csv > $O/unpack_raw.csv 2>/dev/null
 REPS=200 python tools/fp4_library_peak.py 8192 residues > $O/fp4_library_ceiling.json 2>>$O/bench.err
 python tools/hbm_write_probe.py > $O/hbm_write_probe.json 2>>$O/bench.err
 python tools/e2e_probe.py > $O/e2e_probe.txt 2>>$O/bench.err

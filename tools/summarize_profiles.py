@@ -34,9 +34,11 @@ TRAFFIC = {
     "cfg2_gf_dot": ["cfg2:auto:gf_dot"],
     "redq": ["redq:reduce_words"],
     "pack": ["pack:pack_rows_u8"],
+    "unpack": ["unpack:unpack_rows_u8"],
 }
 # measured ceilings / host-path probes written by profile_round.sh, copied verbatim
-PROBES = ["fp4_library_ceiling.json", "hbm_write_probe.json", "e2e_probe.txt", "pageable_probe.txt"]
+PROBES = ["pipe_peaks.json", "fp4_library_ceiling.json", "hbm_write_probe.json", "e2e_probe.txt",
+          "pageable_probe.txt"]
 
 
 def to_bytes(v, unit):
