@@ -614,9 +614,9 @@ from oracle import qadic_oracle as O
 from paper_0809_0063_b200 import cmm, gfext, workloads as W
 from paper_0809_0063_b200.params import cmm_params
 g = W.rng(77)
+f = W.field_for(W.CONFIGS[5])
+of = O.build_field(7, 3, irreducible=[5, 0, 0, 1], max_dot_length=9)
 for (m, kk, n) in ((600, 300, 1000), (512, 256, 8192 // 4 + 7)):
-    f = gfext.build_field(7, 3, irreducible=[5, 0, 0, 1], max_dot_length=kk)
-    of = O.build_field(7, 3, irreducible=[5, 0, 0, 1], max_dot_length=kk)
     a = g.integers(0, 7, (m, kk, 3), dtype=np.uint8)
     b = g.integers(0, 7, (kk, n, 3), dtype=np.uint8)
     assert np.array_equal(f.matmul_coeffs(a, b, engine="fp4k"), O.gf_matmul_planes(of, a, b)), (m, kk, n)
