@@ -707,16 +707,19 @@ def run_primitive(args, kind):
     ms = e0.elapsed_time(e1) / steps
     launches = N.launch_count() - launches0
     peaks, peak_src = load_peaks()
-    if byts is None:  # tensor-bound: nplanes GEMMs of nb-byte rows = nplanes * nb int8 MACs per uint64 MAC
+    if byts is None:  # tensor-bound: one byte-plane GEMM per shift s
+        # byte MACs the segmented byte-plane GEMMs issue per word MAC: plane s < 8
+        # multiplies A byte i by B byte s - i for every valid i (nb significant bytes each)
         nb = -(-PRIMS["mm64"]["bits"] // 8)
-        ops = 2 * min(2 * nb - 1, 8) * nb * units
+        per_word = sum(1 for sp in range(min(2 * nb - 1, 8)) for i in range(nb) if 0 <= sp - i < nb)
+        ops = 2 * per_word * units
         achieved_t = ops / (ms / 1e3) / 1e12
         roof = {"bound": "tensor", "kernel": kname, "achieved": round(achieved_t, 1), "peak": 4500.0,
                 "unit": "TOP/s", "frac": round(achieved_t / 4500.0, 4), "traffic": None,
                 "avg_launch_ms": round(ms, 4), "algorithmic_ops_per_launch": ops,
                 "avg_launch_source": "timed region / K (one call per step: byte planes + one GEMM per plane)",
                 "peak_source": "fallback nominal dense int8 4.5 POP/s (B200_PROFILING.md); ops = the int8 "
-                               "MACs the trimmed byte-plane GEMMs issue"}
+                               "MACs the segmented byte-plane GEMMs issue (24 per word MAC at 5 + 5 bytes)"}
         if not args.no_probe:
             timed_s = ms * steps / 1e3
             _attach_probe(roof, pipe_probe(N, "i8", timed_s), sustained=timed_s >= 0.1)

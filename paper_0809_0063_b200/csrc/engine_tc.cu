@@ -134,6 +134,10 @@ struct Params {
     // exact uint64 GEMM through byte planes (KIND_I8): C64 = (acc64 ? C64 : 0) + (u32 D << shift)
     uint64_t* c64;
     int shift, acc64;
+    // segmented K (uint64 byte planes): K'' block kb belongs to segment kb / seg_kpb,
+    // i = seg_i_lo + segment; A is read at byte offset i * seg_kp + (kb % seg_kpb) * BK
+    // of its row, B at row offset (seg_s - i) * N.  seg_kpb = 0: contiguous K.
+    int seg_kpb, seg_i_lo, seg_s, seg_kp;
     // column-tile range of this launch: tiles n_tile0 .. n_tile0 + n_tiles - 1
     int n_tile0;
     // launched as the programmatic dependent of a concurrent GEMM launch: wait for
@@ -280,23 +284,30 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                     mbar_wait(&empty_bar[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * G::STAGE_BYTES;
                     uint8_t* sb = sa + G::A_BYTES;
+                    int ak = kb * BK, bk = kb * BK, boff = 0;
+                    if (prm.seg_kpb) {  // byte-plane segments of the uint64 GEMM
+                        const int seg = kb / prm.seg_kpb, kin = kb - seg * prm.seg_kpb, i = prm.seg_i_lo + seg;
+                        ak = i * prm.seg_kp + kin * BK;
+                        bk = kin * BK;
+                        boff = (prm.seg_s - i) * (int)prm.N;
+                    }
                     if (prm.diag_noload && (u != group_id || kb >= NST)) {  // wrong results: power probe
                         if (!PAIR || leader) mbar_arrive(&full_bar[stage]);
                     } else if (MC) {
                         const uint32_t lbar = map_to_rank(&full_bar[stage], pair_leader);
                         if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * G::STAGE_BYTES);
-                        tma_load_2d_pair(sa, &tmap_a, lbar, kb * BK, arow);
-                        tma_load_2d_pair_mc(sb + pidx * G::B_BOX * BK, &tmap_b, lbar, kb * BK,
-                                            brow + (int)pidx * G::B_BOX, mc_mask);
+                        tma_load_2d_pair(sa, &tmap_a, lbar, ak, arow);
+                        tma_load_2d_pair_mc(sb + pidx * G::B_BOX * BK, &tmap_b, lbar, bk,
+                                            brow + boff + (int)pidx * G::B_BOX, mc_mask);
                     } else if (PAIR) {
                         const uint32_t lbar = map_to_rank(&full_bar[stage], 0);
                         if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * G::STAGE_BYTES);
-                        tma_load_2d_pair(sa, &tmap_a, lbar, kb * BK, arow);
-                        tma_load_2d_pair(sb, &tmap_b, lbar, kb * BK, brow);
+                        tma_load_2d_pair(sa, &tmap_a, lbar, ak, arow);
+                        tma_load_2d_pair(sb, &tmap_b, lbar, bk, brow + boff);
                     } else {
                         mbar_arrive_expect_tx(&full_bar[stage], G::STAGE_BYTES);
-                        tma_load_2d(sa, &tmap_a, &full_bar[stage], kb * BK, arow);
-                        tma_load_2d(sb, &tmap_b, &full_bar[stage], kb * BK, brow);
+                        tma_load_2d(sa, &tmap_a, &full_bar[stage], ak, arow);
+                        tma_load_2d(sb, &tmap_b, &full_bar[stage], bk, brow + boff);
                     }
                     if (++stage == NST) { stage = 0; phase ^= 1; }
                 }
@@ -1945,58 +1956,93 @@ static int run_kara(const FieldConst& f, const uint8_t* a, const uint8_t* b, int
 // (K chunks of <= 16384), and the accumulator's wrap-around is exactly the
 // needed mod 2^32 for s >= 4.  The epilogue adds D_s << 8s into C (uint64).
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) u64_bplanes_kernel(const uint64_t* __restrict__ b, int64_t K, int64_t N,
-                                                           int64_t k0, int64_t kc, int nba, int nplanes,
-                                                           uint8_t* __restrict__ out, int64_t ld,
-                                                           int64_t plane_stride) {
-    // B^(s)[n][nba*(k-k0) + i] = byte i of bswap(B[k][n]) >> 8(7-s) = byte_{s-i}(B[k][n]), i < nba;
-    // a warp's 32 consecutive k of one row n form nba*32 contiguous bytes (staged, 16-byte stores)
-    __shared__ uint64_t tile[32][33];
-    __shared__ __align__(16) uint8_t stage[8][8 * 32];
-    const int64_t n0 = (int64_t)blockIdx.x * 32, kk0 = k0 + (int64_t)blockIdx.y * 32;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 8 warps
+// 4 x 4 byte transpose: on return byte j of w[i] = old byte i of w[j]
+__device__ __forceinline__ void transpose4_bytes(uint32_t (&w)[4]) {
+    const uint32_t t0 = __byte_perm(w[0], w[1], 0x5140), t1 = __byte_perm(w[0], w[1], 0x7362);
+    const uint32_t t2 = __byte_perm(w[2], w[3], 0x5140), t3 = __byte_perm(w[2], w[3], 0x7362);
+    w[0] = __byte_perm(t0, t2, 0x5410);
+    w[1] = __byte_perm(t0, t2, 0x7632);
+    w[2] = __byte_perm(t1, t3, 0x5410);
+    w[3] = __byte_perm(t1, t3, 0x7632);
+}
+
+// 16 consecutive uint64 -> their byte planes: out[j] = 16 bytes (byte j of each word), j < 8
+__device__ __forceinline__ void u64x16_byte_planes(const uint64_t (&v)[16], uint4 (&out)[8]) {
 #pragma unroll
-    for (int r = ty; r < 32; r += 8) {
-        const int64_t k = kk0 + r, n = n0 + tx;
-        tile[r][tx] = (k < k0 + kc && n < N) ? b[k * N + n] : 0ull;
-    }
-    __syncthreads();
-    const int64_t kvalid = (k0 + kc - kk0) < 32 ? (k0 + kc - kk0) : 32;  // k of this tile in the chunk
-    for (int r = ty; r < 32; r += 8) {  // output row n = n0 + r; lane tx = k offset
-        const int64_t n = n0 + r;
-        if (n >= N) continue;
-        const uint64_t v = tile[tx][r];
-        const uint64_t rv = ((uint64_t)__byte_perm((uint32_t)v, 0, 0x0123) << 32) |
-                            __byte_perm((uint32_t)(v >> 32), 0, 0x0123);  // bswap64
-        uint8_t* rowp = out + n * ld + nba * (kk0 - k0);
-        const int nbytes = nba * (int)kvalid;
-        for (int sp = 0; sp < nplanes; ++sp) {
-            const uint64_t w = rv >> (8 * (7 - sp));
-            uint8_t* st = stage[ty];
-            for (int i = 0; i < nba; ++i) st[tx * nba + i] = (uint8_t)(w >> (8 * i));
-            __syncwarp();
-            uint8_t* dst = rowp + sp * plane_stride;
-            const bool vec = ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) && (nbytes % 16 == 0);
-            if (vec) {
-                for (int q = tx; q < nbytes / 16; q += 32)
-                    reinterpret_cast<uint4*>(dst)[q] = reinterpret_cast<const uint4*>(st)[q];
-            } else {
-                for (int q = tx; q < nbytes; q += 32) dst[q] = st[q];
-            }
-            __syncwarp();
+    for (int q = 0; q < 4; ++q) {  // words 4q .. 4q+3
+        uint32_t lo[4] = {(uint32_t)v[4 * q], (uint32_t)v[4 * q + 1], (uint32_t)v[4 * q + 2], (uint32_t)v[4 * q + 3]};
+        uint32_t hi[4] = {(uint32_t)(v[4 * q] >> 32), (uint32_t)(v[4 * q + 1] >> 32), (uint32_t)(v[4 * q + 2] >> 32),
+                          (uint32_t)(v[4 * q + 3] >> 32)};
+        transpose4_bytes(lo);
+        transpose4_bytes(hi);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            reinterpret_cast<uint32_t*>(&out[j])[q] = lo[j];
+            reinterpret_cast<uint32_t*>(&out[4 + j])[q] = hi[j];
         }
     }
 }
 
-// A [M][K] uint64 -> its low nba bytes per element, rows of ld bytes
-__global__ void u64_compact_kernel(const uint64_t* __restrict__ a, int64_t M, int64_t K, int nba,
-                                   uint8_t* __restrict__ out, int64_t ld) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= M * K) return;
-    const int64_t r = i / K, k = i % K;
-    const uint64_t v = a[i];
-    uint8_t* dst = out + r * ld + (int64_t)nba * k;
-    for (int q = 0; q < nba; ++q) dst[q] = (uint8_t)(v >> (8 * q));
+// A [M][K] uint64, columns k0 .. k0+kc -> byte-plane-major rows:
+//   out[m][i * kp + kk] = byte_i(A[m][k0 + kk]), i < nba, zero for kc <= kk < kp.
+// Thread: 16 consecutive kk of one row (one 16-byte store per plane).
+__global__ void __launch_bounds__(256) u64_aplanes_kernel(const uint64_t* __restrict__ a, int64_t M, int64_t K,
+                                                          int64_t k0, int64_t kc, int nba, int64_t kp,
+                                                          uint8_t* __restrict__ out) {
+    const int64_t per_row = kp / 16;
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= M * per_row) return;
+    const int64_t m = idx / per_row, kk0 = (idx % per_row) * 16;
+    const uint64_t* src = a + m * K + k0 + kk0;
+    uint64_t v[16];
+    if (kk0 + 16 <= kc && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const ulonglong2 x = __ldcs(reinterpret_cast<const ulonglong2*>(src) + q);
+            v[2 * q] = x.x;
+            v[2 * q + 1] = x.y;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = kk0 + q < kc ? src[q] : 0ull;
+    }
+    uint4 pl[8];
+    u64x16_byte_planes(v, pl);
+    uint8_t* dst = out + m * (nba * kp) + kk0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        if (i < nba) *reinterpret_cast<uint4*>(dst + i * kp) = pl[i];
+}
+
+// B [K][N] uint64, rows k0 .. k0+kc -> transposed byte planes:
+//   out[j][n][kk] = byte_j(B[k0 + kk][n]), j < nbb, zero for kc <= kk < kp.
+// Tile 128 kk x 32 n staged in shared memory (coalesced 256-byte row reads);
+// thread (n, g) emits 16 kk per plane as one 16-byte store, 8 threads per
+// 128-byte line of a plane row.
+__global__ void __launch_bounds__(256) u64_btplanes_kernel(const uint64_t* __restrict__ b, int64_t K, int64_t N,
+                                                           int64_t k0, int64_t kc, int nbb, int64_t kp,
+                                                           uint8_t* __restrict__ out) {
+    __shared__ uint64_t tile[128][33];
+    const int64_t n0 = (int64_t)blockIdx.x * 32, kk0 = (int64_t)blockIdx.y * 128;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+#pragma unroll 4
+    for (int r = ty; r < 128; r += 8) {
+        const int64_t kk = kk0 + r, n = n0 + tx;
+        tile[r][tx] = (kk < kc && n < N) ? __ldcs(b + (k0 + kk) * N + n) : 0ull;
+    }
+    __syncthreads();
+    const int nl = threadIdx.x & 31, g = threadIdx.x >> 5;  // column n0 + nl, kk 16g .. 16g+15
+    const int64_t n = n0 + nl;
+    if (n >= N) return;
+    uint64_t v[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = tile[16 * g + q][nl];
+    uint4 pl[8];
+    u64x16_byte_planes(v, pl);
+    uint8_t* dst = out + n * kp + kk0 + 16 * g;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if (j < nbb) *reinterpret_cast<uint4*>(dst + (int64_t)j * N * kp) = pl[j];
 }
 
 // OR of every word (significant byte count of the operand)
@@ -2059,42 +2105,42 @@ int tc_matmul_u64(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_t m, 
         }
         cudaGetLastError();
     }
+    // D_s = sum_{i+j=s} A_i B_j^T over the byte planes that can be nonzero (i < nba,
+    // j < nbb): plane s runs one GEMM whose K'' is the concatenation of its valid
+    // segments (A plane i against B plane s-i), so only the nonzero byte products
+    // are issued -- sum_s #{i} = 24 per word MAC at 5 + 5 bytes, not 8 x 5.
     const int nplanes = nba + nbb - 1 < 8 ? nba + nbb - 1 : 8;  // shifts 8s >= 64 vanish mod 2^64
     const int64_t kc_max = k < KC ? k : KC;
-    const int64_t ld = (nba * kc_max + 15) / 16 * 16;  // bytes per B^(s) row
-    const size_t plane = (size_t)n * ld;
-    const int64_t lda = nba == 8 ? 8 * k : (nba * k + 15) / 16 * 16;
-    const size_t abytes = nba == 8 ? 0 : (size_t)m * lda;
-    uint8_t* bs = nullptr;
-    if (cudaMallocAsync(reinterpret_cast<void**>(&bs), nplanes * plane + abytes, s) != cudaSuccess) {
+    const int64_t kp = (kc_max + BK - 1) / BK * BK;  // segment length (bytes), BK-aligned
+    const size_t abytes = (size_t)m * nba * kp, bbytes = (size_t)nbb * n * kp;
+    uint8_t* ws = nullptr;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&ws), abytes + bbytes, s) != cudaSuccess) {
         cudaGetLastError();
-        set_error(QADIC_ERR_CUDA, "matmul_exact_u64: cannot allocate %zu bytes of byte planes",
-                  nplanes * plane + abytes);
+        set_error(QADIC_ERR_CUDA, "matmul_exact_u64: cannot allocate %zu bytes of byte planes", abytes + bbytes);
         return QADIC_ERR_CUDA;
     }
-    const uint8_t* a8 = reinterpret_cast<const uint8_t*>(a);
-    if (nba < 8) {  // A's low nba bytes per element
-        uint8_t* ac = bs + nplanes * plane;
-        QADIC_TIMED("u64 compact A", s,
-                    u64_compact_kernel<<<(unsigned)((m * k + 255) / 256), 256, 0, s>>>(a, m, k, nba, ac, lda));
-        a8 = ac;
-    }
+    uint8_t* a8 = ws;
+    uint8_t* bt = ws + abytes;
     const bool pair = pair_mode();
     constexpr int BN = Cfg<KIND_I8>::BN;
     int rc = check_launch("u64 prepare");
     for (int64_t k0 = 0; k0 < k && rc == QADIC_OK; k0 += KC) {
         const int64_t kc = (k - k0 < KC) ? k - k0 : KC;
-        dim3 grid((unsigned)((n + 31) / 32), (unsigned)((kc + 31) / 32));
-        QADIC_TIMED("u64 byte planes", s,
-                    u64_bplanes_kernel<<<grid, 256, 0, s>>>(b, k, n, k0, kc, nba, nplanes, bs, ld, plane));
+        const int64_t ta = m * (kp / 16);
+        QADIC_TIMED("u64 byte planes A", s,
+                    u64_aplanes_kernel<<<(unsigned)((ta + 255) / 256), 256, 0, s>>>(a, m, k, k0, kc, nba, kp, a8));
+        dim3 grid((unsigned)((n + 31) / 32), (unsigned)(kp / 128));
+        QADIC_TIMED("u64 byte planes B", s, u64_btplanes_kernel<<<grid, 256, 0, s>>>(b, k, n, k0, kc, nbb, kp, bt));
         rc = check_launch("u64 byte planes");
         if (rc) break;
-        CUtensorMap ta, tb;
-        rc = make_tmap(&ta, a8 + nba * k0, nba * kc, m, lda, BM);
+        CUtensorMap ta_map, tb_map;
+        rc = make_tmap(&ta_map, a8, nba * kp, m, nba * kp, BM);
+        if (rc) break;
+        rc = make_tmap(&tb_map, bt, kp, (int64_t)nbb * n, kp, pair ? BN / 2 : BN);
         if (rc) break;
         for (int sp = 0; sp < nplanes && rc == QADIC_OK; ++sp) {
-            rc = make_tmap(&tb, bs + sp * plane, nba * kc, n, ld, pair ? BN / 2 : BN);
-            if (rc) break;
+            const int i_lo = sp - (nbb - 1) > 0 ? sp - (nbb - 1) : 0;
+            const int i_hi = sp < nba - 1 ? sp : nba - 1;
             Params prm = {};
             prm.M = m;
             prm.N = n;
@@ -2103,17 +2149,21 @@ int tc_matmul_u64(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_t m, 
             prm.m_tiles = (int)((m + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM));
             prm.n_tiles = (int)((n + BN - 1) / BN);
             prm.n_full = (int)(n / BN);
-            prm.num_kb = (int)((nba * kc + BK - 1) / BK);
+            prm.seg_kpb = (int)(kp / BK);
+            prm.seg_i_lo = i_lo;
+            prm.seg_s = sp;
+            prm.seg_kp = (int)kp;
+            prm.num_kb = (i_hi - i_lo + 1) * prm.seg_kpb;
             prm.planes = 1;
             prm.group_m = GROUP_M;
             prm.c64 = c;
             prm.shift = 8 * sp;
             prm.acc64 = (sp > 0 || k0 > 0) ? 1 : 0;
-            rc = pair ? launch_gemm<KIND_I8, true>(ta, tb, prm, s, "u64 byte-plane gemm")
-                      : launch_gemm<KIND_I8, false>(ta, tb, prm, s, "u64 byte-plane gemm");
+            rc = pair ? launch_gemm<KIND_I8, true>(ta_map, tb_map, prm, s, "u64 byte-plane gemm")
+                      : launch_gemm<KIND_I8, false>(ta_map, tb_map, prm, s, "u64 byte-plane gemm");
         }
     }
-    cudaFreeAsync(bs, s);
+    cudaFreeAsync(ws, s);
     return rc;
 }
 

@@ -52,6 +52,9 @@ class TestLayerK:
         assert np.array_equal(_kernels.matmul_exact_u64(small, b), O.matmul_exact_u64(small, b))
         tiny = rng.integers(0, 1 << 12, (k, n), dtype=np.uint64)  # 3 x 2 significant bytes: 4 planes
         assert np.array_equal(_kernels.matmul_exact_u64(small, tiny), O.matmul_exact_u64(small, tiny))
+        assert np.array_equal(_kernels.matmul_exact_u64(a, tiny), O.matmul_exact_u64(a, tiny))  # 8 x 2 bytes
+        one = rng.integers(0, 256, (m, k), dtype=np.uint64)  # 1 x 8 bytes
+        assert np.array_equal(_kernels.matmul_exact_u64(one, b), O.matmul_exact_u64(one, b))
         zero = np.zeros((k, n), np.uint64)
         assert not _kernels.matmul_exact_u64(a, zero).any()
 
