@@ -28,7 +28,11 @@ struct PolyConst {
 // 2^52 (the low mantissa bits are then the integer), 7 digits by the 32-bit
 // wrap trick, correction on 4 byte lanes at once.
 constexpr int PM_THREADS = 256;
-constexpr int PM_PER = 8;  // pairs per thread (56 output bytes = 7 x 8-byte stores)
+#ifndef QADIC_PM_PER
+#define QADIC_PM_PER 8
+#endif
+constexpr int PM_PER = QADIC_PM_PER;  // pairs per thread (8: 56 output bytes = 7 x 8-byte stores)
+constexpr int PM_MINB = PM_PER == 8 ? 4 : 8;  // resident blocks per SM the register cap allows
 
 QADIC_D uint32_t pack4_bytes(uint32_t x, int t, uint32_t m) {
     return (x & m) | (((x >> 8) & m) << t) | (((x >> 16) & m) << (2 * t)) | (((x >> 24) & m) << (3 * t));
@@ -53,7 +57,7 @@ QADIC_D uint32_t lanes_mod_2p(uint32_t v, uint32_t p) {
 }
 
 template <int T, bool CORR1>
-__global__ void __launch_bounds__(PM_THREADS, 4) polymul_k4_kernel(const uint8_t* __restrict__ a,
+__global__ void __launch_bounds__(PM_THREADS, PM_MINB) polymul_k4_kernel(const uint8_t* __restrict__ a,
                                                                 const uint8_t* __restrict__ b, int64_t n,
                                                                 PolyConst c, uint8_t* __restrict__ out) {
     pdl_wait();  // predecessor complete before any global access
@@ -133,8 +137,14 @@ __global__ void __launch_bounds__(PM_THREADS, 4) polymul_k4_kernel(const uint8_t
     if (__all_sync(0xffffffffu, full) && ((reinterpret_cast<uintptr_t>(wbase) & 15) == 0)) {
         uint32_t* st = pstage[threadIdx.x >> 5];
 #pragma unroll
-        for (int q = 0; q < PM_PER * 7 / 8; ++q)
-            *reinterpret_cast<uint2*>(st + lane * (PM_PER * 7 / 4) + 2 * q) = make_uint2(o[2 * q], o[2 * q + 1]);
+        if constexpr (PM_PER * 7 % 8 == 0) {
+#pragma unroll
+            for (int q = 0; q < PM_PER * 7 / 8; ++q)
+                *reinterpret_cast<uint2*>(st + lane * (PM_PER * 7 / 4) + 2 * q) = make_uint2(o[2 * q], o[2 * q + 1]);
+        } else {
+#pragma unroll
+            for (int q = 0; q < PM_PER * 7 / 4; ++q) st[lane * (PM_PER * 7 / 4) + q] = o[q];
+        }
         __syncwarp();
         constexpr int NV = 32 * PM_PER * 7 / 16;  // 16-byte vectors per warp
 #pragma unroll
@@ -142,7 +152,7 @@ __global__ void __launch_bounds__(PM_THREADS, 4) polymul_k4_kernel(const uint8_t
             reinterpret_cast<uint4*>(wbase)[v] = *reinterpret_cast<const uint4*>(st + 4 * v);
     } else if (p0 >= n) {
         return;
-    } else if (full && ((reinterpret_cast<uintptr_t>(dst) & 7) == 0)) {
+    } else if (full && PM_PER * 7 % 8 == 0 && ((reinterpret_cast<uintptr_t>(dst) & 7) == 0)) {
 #pragma unroll
         for (int q = 0; q < PM_PER * 7 / 8; ++q) reinterpret_cast<uint2*>(dst)[q] = make_uint2(o[2 * q], o[2 * q + 1]);
     } else {
@@ -159,7 +169,7 @@ static void launch_polymul_k4(const uint8_t* a, const uint8_t* b, int64_t n, con
     // that the pairs spread evenly (cfg1: 592 x 224 threads instead of 512 x 256,
     // which left 68 SMs with a fourth block and the rest with three).  Larger
     // batches run 256-thread blocks in several waves.
-    const int64_t per_wave = 4LL * num_sms_cached();
+    const int64_t per_wave = (int64_t)PM_MINB * num_sms_cached();
     int64_t threads = (n + per_wave * PM_PER - 1) / (per_wave * PM_PER);
     threads = (threads + 31) / 32 * 32;
     if (threads > PM_THREADS) threads = PM_THREADS;
@@ -227,15 +237,17 @@ QADIC_D void digit_sums_word(uint32_t x, uint32_t y, uint32_t (&S)[2 * K - 1]) {
     }
 }
 
-template <int K, int G, bool VEC>
-__global__ void __launch_bounds__(GD_THREADS) gf_dot_kernel(const uint8_t* __restrict__ v1,
+// NARROW: registers capped at 32 (8 resident blocks per SM) for short rows, where
+// the 4-deep load loop never runs (its spills stay cold) and a wave holds the batch.
+template <int K, int G, bool VEC, bool NARROW = false>
+__global__ void __launch_bounds__(GD_THREADS, NARROW ? 8 : 1) gf_dot_kernel(const uint8_t* __restrict__ v1,
                                                             const uint8_t* __restrict__ v2, int64_t batch,
                                                             int64_t len, FieldConst f, int tab_smem,
                                                             uint8_t* __restrict__ out) {
     pdl_wait();  // predecessor complete before any global access
     pdl_trigger();
     const int lane = threadIdx.x % G;
-    const int64_t dot = ((int64_t)blockIdx.x * GD_THREADS + threadIdx.x) / G;
+    const int64_t dot = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
     const bool live = dot < batch;
     const int t = (int)f.t;
     uint64_t acc = 0;
@@ -299,7 +311,7 @@ __global__ void __launch_bounds__(GD_THREADS) gf_dot_kernel(const uint8_t* __res
     const uint32_t* ltab = f.l_table;
     const uint32_t* htab = f.h_table;
     if (tab_smem > 0) {
-        for (int i = threadIdx.x; i < tab_smem; i += GD_THREADS) {
+        for (int i = threadIdx.x; i < tab_smem; i += blockDim.x) {
             gd_tab[i] = __ldg(f.l_table + i);
             gd_tab[tab_smem + i] = __ldg(f.h_table + i);
         }
@@ -338,10 +350,27 @@ static void launch_gf_dot(const uint8_t* v1, const uint8_t* v2, int64_t batch, i
     const int ntab = entries <= 2048 ? entries : 0;  // <= 16 KB of tables: shared memory
     const size_t smem = (size_t)ntab * 2 * sizeof(uint32_t);
     if (vec) {
-        constexpr int G = 4;  // 4 lanes per dot: a warp reads 64 contiguous bytes per dot per load
-        const unsigned blocks = (unsigned)((batch * G + GD_THREADS - 1) / GD_THREADS);
-        launch_pdl(gf_dot_kernel<K, G, (4 % K == 0)>, dim3(blocks), dim3(GD_THREADS), smem, s, v1, v2, batch, len,
-                   f, ntab, out);
+        // 4 lanes per dot.  Short rows (cfg2: 8 chunks, 2 per lane) use the narrow
+        // variant, whose 32 registers let 8 blocks reside per SM: the batch is one
+        // wave (the 48-register variant ran 1.4 waves: 5.14 vs 4.97 us).  The block
+        // width is trimmed to spread the batch evenly over the resident slots.
+        const int64_t nchunks = len * K / 16;
+        auto go = [&](auto kern, int G) {
+            static int occ = 0;
+            if (!occ) {
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, GD_THREADS, smem);
+                if (occ < 1) occ = 1;
+            }
+            const int64_t threads_total = batch * G, per_wave = (int64_t)occ * num_sms_cached();
+            int64_t width = (threads_total + per_wave - 1) / per_wave;
+            width = (width + 31) / 32 * 32;
+            if (width > GD_THREADS) width = GD_THREADS;
+            if (width < 64) width = 64;
+            const unsigned blocks = (unsigned)((threads_total + width - 1) / width);
+            launch_pdl(kern, dim3(blocks), dim3((unsigned)width), smem, s, v1, v2, batch, len, f, ntab, out);
+        };
+        if (nchunks <= 3 * 4) go(gf_dot_kernel<K, 4, (4 % K == 0), true>, 4);
+        else go(gf_dot_kernel<K, 4, (4 % K == 0), false>, 4);
     } else {
         constexpr int G = 8;
         const unsigned blocks = (unsigned)((batch * G + GD_THREADS - 1) / GD_THREADS);
