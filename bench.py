@@ -1,7 +1,7 @@
 """Benchmark of the qadic hot path on B200 (contract: see DESIGN.md section 6).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5|all|redq|pack|mm64]
-                    [--engine auto|i8|f64|fp4|fp4k] [--impl ours|reference]
+                    [--engine auto|i8|f64|fp4|fp4k|i8k] [--impl ours|reference]
 
 One "step" is one pass of the hot path over one batch of the config's
 synthetic seeded input (BASELINE.json configs).  Default workload: cfg5 --
@@ -341,8 +341,9 @@ def roofline(cfg, engine, kname, kstats, work, peaks, peak_src):
         return None
     count, total_ms = kstats
     avg_s = total_ms / count / 1e3
-    if kname == "i8 gemm":
-        ops = 2 * work["i8_macs"]
+    if kname in ("i8 gemm", "i8k gemm"):
+        # expanded form: M*(N k)*(K k) MACs; evaluation planes: S * M*N*K MACs
+        ops = 2 * (work["kara_macs"] if kname == "i8k gemm" else work["i8_macs"])
         achieved = ops / avg_s / 1e12
         # No int8 entry in MEASURED_PEAKS.json: the denominator is the
         # B200_PROFILING.md nominal dense rate (int8 = fp8 = 4.5 POP/s).  The
@@ -392,9 +393,11 @@ def dtype_label(cfg, engine, kname):
     if cfg == 1:
         return "f64 (DQT words, one DMUL per pair)"
     if cfg == 2:
-        return "u32 x u32 -> u64 DQT words, f64 REDQ"
+        return "u8 x u8 -> u32 digit sums (IDP4A) of the DQT word, f64 REDQ"
     if engine == "f64":
         return "f64 (DMMA on DQT words)"
+    if kname == "i8k gemm":
+        return "u8 x u8 -> s32 (tcgen05 kind::i8 on evaluation planes)"
     if kname and kname.startswith("fp4"):
         return "e2m1 x e2m1 -> f32 (tcgen05 kind::mxf4, exact integer sums)"
     return "u8 x u8 -> s32 (tcgen05 kind::i8)"
@@ -547,7 +550,8 @@ def run_ours(args):
     value = total_units / (ms / 1e3)
     unit = "pairs/s" if cfg == 1 else ("F_p mult-adds/s" if cfg == 4 else "GF mult-adds/s")
     kname = dominant_kernel(cfg, engine, prof)
-    pipe = {"fp4 gemm": "mxf4", "fp4k gemm": "mxf4", "i8 gemm": "i8", "f64 dmma gemm": "f64"}.get(kname)
+    pipe = {"fp4 gemm": "mxf4", "fp4k gemm": "mxf4", "i8 gemm": "i8", "i8k gemm": "i8",
+            "f64 dmma gemm": "f64"}.get(kname)
     timed_s = ms * args.steps / 1e3
     probe = pipe_probe(N, pipe, timed_s) if pipe and not args.no_probe else None
     if probe and pipe == "f64" and "burst" in probe:
@@ -804,7 +808,7 @@ def main():
                          "nvidia-smi clock samples fall inside it)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="5")
-    ap.add_argument("--engine", default="auto", choices=["auto", "i8", "f64", "fp4", "fp4k"])
+    ap.add_argument("--engine", default="auto", choices=["auto", "i8", "f64", "fp4", "fp4k", "i8k"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-probe", action="store_true", help="skip the measured pipe-peak probe after the timed region")

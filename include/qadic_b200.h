@@ -42,8 +42,10 @@ typedef enum qadic_engine {
     QADIC_ENGINE_I8_TC = 1,    /* tcgen05.mma kind::i8 on coefficient planes, int32 TMEM accumulators */
     QADIC_ENGINE_F64_DMMA = 2, /* the paper's formulation: DQT-packed FP64 words on DMMA tensor cores */
     QADIC_ENGINE_F4_TC = 3,    /* tcgen05.mma kind::mxf4 (E2M1, unit block scales) on centred residues, p <= 7 */
-    QADIC_ENGINE_F4K_TC = 4    /* F4 on evaluation planes (Toom-Cook over F_p: 2k-1 when 2k-1 <= p+1, else
+    QADIC_ENGINE_F4K_TC = 4,   /* F4 on evaluation planes (Toom-Cook over F_p: 2k-1 when 2k-1 <= p+1, else
                                   k(k+1)/2 Karatsuba) + mod-p combine: the fewest MACs */
+    QADIC_ENGINE_I8K_TC = 5    /* the same evaluation planes on tcgen05 kind::i8 (residues as int8, int32
+                                  TMEM accumulators), p <= 7 */
 } qadic_engine;
 
 QADIC_API int qadic_abi_version(void);

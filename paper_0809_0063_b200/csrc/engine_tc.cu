@@ -1344,6 +1344,11 @@ __global__ void __launch_bounds__(256) planes_kernel(const uint8_t* __restrict__
 //     4 rows x 128 contiguous bytes of each plane (whole lines, no partial sectors).
 // planes_b3_kernel feeds pass 1 by TMA; planes_b2_kernel (unaligned B) by lane loads.
 constexpr int P2_KK = 256, P2_J = 32;
+#ifndef QADIC_P2_NBUF
+#define QADIC_P2_NBUF 2
+#endif
+constexpr int P2_NBUF = QADIC_P2_NBUF;  // TMA input buffers of planes_b3_kernel (NBUF - 1 tiles in flight;
+                                        // 3 and 4 measured slower: fewer resident blocks)
 
 // pass 2 of the B-plane kernels: lane = (32-kk chunk, column) of the code tile
 template <int K>
@@ -1470,9 +1475,10 @@ __global__ void __launch_bounds__(256) planes_b3_kernel(const __grid_constant__ 
     constexpr int ROWB = P2_J * K;  // bytes per box row
     extern __shared__ __align__(128) uint8_t dsm3[];
     uint8_t* inb = dsm3;                                                     // 2 x [P2_KK][ROWB]
-    uint16_t (*codes)[P2_J] = reinterpret_cast<uint16_t (*)[P2_J]>(dsm3 + 2 * P2_KK * ROWB);
-    uint32_t* tab = reinterpret_cast<uint32_t*>(dsm3 + 2 * P2_KK * ROWB + P2_KK * P2_J * 2);
-    __shared__ __align__(8) uint64_t bar[2];
+    constexpr int NB = P2_NBUF;
+    uint16_t (*codes)[P2_J] = reinterpret_cast<uint16_t (*)[P2_J]>(dsm3 + NB * P2_KK * ROWB);
+    uint32_t* tab = reinterpret_cast<uint32_t*>(dsm3 + NB * P2_KK * ROWB + P2_KK * P2_J * 2);
+    __shared__ __align__(8) uint64_t bar[NB];
     build_plane_table(tab, p, K, S, ps, lut, gtab);
     const CodeCoef<K> cc = make_code_coef<K>(p);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1480,8 +1486,7 @@ __global__ void __launch_bounds__(256) planes_b3_kernel(const __grid_constant__ 
     const int64_t ntiles = (int64_t)tiles_kk * tiles_j;
     if (threadIdx.x == 0) {
         tma_prefetch(&tmap);
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+        for (int i = 0; i < NB; ++i) mbar_init(&bar[i], 1);
         fence_barrier_init();
     }
     __syncthreads();
@@ -1492,13 +1497,18 @@ __global__ void __launch_bounds__(256) planes_b3_kernel(const __grid_constant__ 
         mbar_arrive_expect_tx(&bar[buf], P2_KK * ROWB);
         tma_load_2d(inb + buf * P2_KK * ROWB, &tmap, &bar[buf], (int32_t)(j0 * K), (int32_t)kk0);
     };
-    if (threadIdx.x == 0 && (int64_t)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    if (threadIdx.x == 0)
+        for (int i = 0; i < NB - 1; ++i)
+            if ((int64_t)blockIdx.x + (int64_t)i * gridDim.x < ntiles) issue(blockIdx.x + (int64_t)i * gridDim.x, i);
     int it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
-        const int buf = it & 1;
+        const int buf = it % NB;
         // the other buffer was last read in the previous iteration's pass 1 (fenced by its barrier)
-        if (threadIdx.x == 0 && t + gridDim.x < ntiles) issue(t + gridDim.x, buf ^ 1);
-        mbar_wait(&bar[buf], (uint32_t)((it >> 1) & 1));
+        // NB - 1 tiles in flight; the buffer refilled here was last read in the previous
+        // iteration's pass 1 (fenced by its barriers)
+        const int64_t tn = t + (int64_t)(NB - 1) * gridDim.x;
+        if (threadIdx.x == 0 && tn < ntiles) issue(tn, (it + NB - 1) % NB);
+        mbar_wait(&bar[buf], (uint32_t)((it / NB) & 1));
         const int64_t kk0 = (t % tiles_kk) * P2_KK, j0 = (t / tiles_kk) * P2_J;
         const uint8_t* tb = inb + buf * P2_KK * ROWB;
 #pragma unroll
@@ -1520,7 +1530,7 @@ __global__ void __launch_bounds__(256) planes_b3_kernel(const __grid_constant__ 
 
 template <int K>
 constexpr size_t planes_b3_smem() {
-    return (size_t)2 * P2_KK * P2_J * K + (size_t)P2_KK * P2_J * 2 + PT_CODES * sizeof(uint32_t) + 128;
+    return (size_t)P2_NBUF * P2_KK * P2_J * K + (size_t)P2_KK * P2_J * 2 + PT_CODES * sizeof(uint32_t) + 128;
 }
 
 static int make_tmap_rows(CUtensorMap* map, const void* base, int64_t inner_bytes, int64_t rows, int64_t ld,
@@ -2055,6 +2065,253 @@ __global__ void u64_or_kernel(const uint64_t* __restrict__ x, int64_t n, unsigne
     if ((threadIdx.x & 31) == 0 && v) atomicOr(acc, (unsigned long long)v);
 }
 
+
+// ---------------------------------------------------------------------------
+// I8K: the evaluation-plane decomposition of the FP4K engine on kind::i8 --
+// residues 0..p-1 as int8 plane operands (exact in the int32 accumulator while
+// K (p-1)^2 < 2^31), the same D planes, combine and workspace order.
+// ---------------------------------------------------------------------------
+// plane table, one byte per plane: T[code] byte s = sum_i E[s][i] digit_i mod p
+__device__ __forceinline__ void build_plane_table8(uint2* tab, uint32_t p, int k, int S, const PlaneSpec& ps) {
+    int ncodes = 1;
+    for (int i = 0; i < k; ++i) ncodes *= (int)p;
+    for (int c = threadIdx.x; c < ncodes; c += blockDim.x) {
+        int r = c;
+        uint32_t dig[kMaxK] = {};
+        for (int i = 0; i < k; ++i) {
+            dig[i] = (uint32_t)(r % (int)p);
+            r /= (int)p;
+        }
+        uint32_t w[2] = {0, 0};
+        for (int s = 0; s < S; ++s) {
+            uint32_t v = 0;
+            for (int i = 0; i < k; ++i) v += ps.E[s][i] * dig[i];
+            w[s >> 2] |= (v % p) << (8 * (s & 3));
+        }
+        tab[c] = make_uint2(w[0], w[1]);
+    }
+}
+
+// 16 table entries (8 plane bytes each) -> 16 bytes per plane: out[s]
+__device__ __forceinline__ void entries16_to_planes(const uint2 (&e)[16], uint4 (&out)[8]) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        uint32_t lo[4] = {e[4 * q].x, e[4 * q + 1].x, e[4 * q + 2].x, e[4 * q + 3].x};
+        uint32_t hi[4] = {e[4 * q].y, e[4 * q + 1].y, e[4 * q + 2].y, e[4 * q + 3].y};
+        transpose4_bytes(lo);
+        transpose4_bytes(hi);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            reinterpret_cast<uint32_t*>(&out[j])[q] = lo[j];
+            reinterpret_cast<uint32_t*>(&out[4 + j])[q] = hi[j];
+        }
+    }
+}
+
+// Rows [R, Kd, K] of residues -> S byte planes [S][R][ld].  Thread: one row,
+// 16 consecutive kk (16 K bytes in, one 16-byte store per plane).
+template <int K>
+__global__ void __launch_bounds__(256) planes8_a_kernel(const uint8_t* __restrict__ src, int64_t R, int64_t Kd,
+                                                        uint32_t p, PlaneSpec ps, uint8_t* __restrict__ out,
+                                                        int64_t ld, int64_t plane_stride) {
+    __shared__ uint2 tab[PT_CODES];
+    build_plane_table8(tab, p, K, ps.S, ps);
+    __syncthreads();
+    const CodeCoef<K> cc = make_code_coef<K>(p);
+    const int64_t chunks = ld / 16;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < R * chunks;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = idx / chunks, kk0 = (idx % chunks) * 16;
+        const uint8_t* row = src + (r * Kd + kk0) * K;
+        uint32_t in[4 * K];
+        if (kk0 + 16 <= Kd && ((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
+#pragma unroll
+            for (int v = 0; v < K; ++v) {
+                const uint4 x = __ldg(reinterpret_cast<const uint4*>(row) + v);
+                in[4 * v] = x.x; in[4 * v + 1] = x.y; in[4 * v + 2] = x.z; in[4 * v + 3] = x.w;
+            }
+        } else {
+#pragma unroll
+            for (int v = 0; v < 4 * K; ++v) in[v] = 0;
+            for (int e = 0; e < 16 * K; ++e)
+                if (kk0 + e / K < Kd) in[e >> 2] |= (uint32_t)row[e] << (8 * (e & 3));
+        }
+        uint32_t code[16];
+        elem_codes<K, 4 * K>(in, cc, code);
+        uint2 e[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) e[i] = kk0 + i < Kd ? tab[code[i]] : make_uint2(0, 0);
+        uint4 pl[8];
+        entries16_to_planes(e, pl);
+        uint8_t* dst = out + r * ld + kk0;
+#pragma unroll
+        for (int sp = 0; sp < KMAX_S; ++sp)
+            if (sp < ps.S) *reinterpret_cast<uint4*>(dst + sp * plane_stride) = pl[sp];
+    }
+}
+
+// B [Kd, N, K] -> S transposed byte planes [S][N][ld].  Tile 128 kk x 32 j: the
+// element codes are staged j-major in shared memory (a lane reads 4 consecutive
+// elements = K words of a B row), then thread (j, g) looks up 16 kk of column j
+// and writes 16 bytes per plane (8 threads per 128-byte plane-row segment).
+template <int K>
+__global__ void __launch_bounds__(256, 4) planes8_b_kernel(const uint8_t* __restrict__ b, int64_t Kd, int64_t N,
+                                                        uint32_t p, PlaneSpec ps, uint8_t* __restrict__ out,
+                                                        int64_t ld, int64_t plane_stride, int tiles_kk, int tiles_j) {
+    __shared__ uint2 tab[PT_CODES];
+    __shared__ __align__(16) uint16_t codes[32][128 + 8];  // [j][kk]: pass 2 reads 16 kk as two 16-byte loads
+    build_plane_table8(tab, p, K, ps.S, ps);
+    const CodeCoef<K> cc = make_code_coef<K>(p);
+    const bool vec = ((N * K) % 4 == 0) && ((reinterpret_cast<uintptr_t>(b) & 3) == 0);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int r4 = lane >> 3, c8 = lane & 7;  // pass 1: row of the warp's 4, 4-element chunk
+    const int64_t ntiles = (int64_t)tiles_kk * tiles_j;
+    // pass-1 words of one tile (rows 32 q + 4 warp + r4, elements 4 c8 .. 4 c8 + 3):
+    // the next tile's are loaded into registers before this tile's pass 2, so the
+    // loads overlap the lookups and stores
+    uint32_t w[4][K];
+    auto load = [&](int64_t t) {
+        const int64_t kk0 = (t % tiles_kk) * 128, j0 = (t / tiles_kk) * 32;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int64_t gk = kk0 + 32 * q + 4 * warp + r4, gj = j0 + 4 * c8;
+            if (vec && gk < Kd && gj + 4 <= N) {
+                const uint32_t* src = reinterpret_cast<const uint32_t*>(b + (gk * N + gj) * K);
+#pragma unroll
+                for (int i = 0; i < K; ++i) w[q][i] = __ldg(src + i);
+            } else {
+#pragma unroll
+                for (int i = 0; i < K; ++i) w[q][i] = 0;
+                for (int e = 0; e < 4 * K; ++e)
+                    if (gk < Kd && gj + e / K < N) w[q][e >> 2] |= (uint32_t)b[(gk * N + gj) * K + e] << (8 * (e & 3));
+            }
+        }
+    };
+    if ((int64_t)blockIdx.x < ntiles) load(blockIdx.x);
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t kk0 = (t % tiles_kk) * 128, j0 = (t / tiles_kk) * 32;
+        __syncthreads();  // table built / previous tile's codes consumed
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            uint32_t cd[4];
+            elem_codes<K, K>(w[q], cc, cd);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) codes[4 * c8 + e][32 * q + 4 * warp + r4] = (uint16_t)cd[e];
+        }
+        __syncthreads();
+        if (t + gridDim.x < ntiles) load(t + gridDim.x);
+        // pass 2: column j0 + jl, kk 16 g .. 16 g + 15 of the tile; the 8 lanes of one
+        // column write 128 contiguous bytes of each plane row (a warp: 4 whole lines)
+        const int jl = 4 * warp + (lane >> 3), g = lane & 7;
+        const int64_t gj = j0 + jl, col = kk0 + 16 * g;
+        if (gj < N && col < ld) {
+            const uint4 c0 = *reinterpret_cast<const uint4*>(&codes[jl][16 * g]);
+            const uint4 c1 = *reinterpret_cast<const uint4*>(&codes[jl][16 * g + 8]);
+            const uint32_t cw[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+            uint2 e[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) e[i] = tab[(cw[i >> 1] >> (16 * (i & 1))) & 0xFFFFu];
+            uint4 pl[8];
+            entries16_to_planes(e, pl);
+            uint8_t* dst = out + gj * ld + col;
+#pragma unroll
+            for (int sp = 0; sp < KMAX_S; ++sp)
+                if (sp < ps.S) *reinterpret_cast<uint4*>(dst + sp * plane_stride) = pl[sp];
+        }
+    }
+}
+
+// C[m, n, k] = A B over GF(p^k) (or F_p, k = 1) through S int8 plane GEMMs.
+// Workspace: [B planes | A planes | D planes] (ldk = K bytes rounded to 16).
+static size_t kara8_workspace(int S, int64_t m, int64_t kdim, int64_t n) {
+    const int64_t ldk = round_up(kdim, 16), ldd = round_up((n + 1) / 2, 16);
+    return (size_t)round_up(S * n * ldk, 1024) + (size_t)round_up(S * m * ldk, 1024) +
+           (size_t)round_up(S * m * ldd, 1024);
+}
+
+static int run_kara8(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
+                     void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s, bool b_ready) {
+    const int k = (int)f.k;
+    PlaneSpec ps;
+    QADIC_REQUIRE(plan_planes(f, &ps), QADIC_ERR_UNSUPPORTED, "no plane decomposition with <= %d planes", KMAX_S);
+    const int S = ps.S;
+    const int64_t ldk = round_up(kdim, 16);
+    KaraLayout L = {};
+    L.S = S;
+    L.ldk = ldk;
+    L.ldd = round_up((n + 1) / 2, 16);
+    L.b_bytes = (size_t)round_up(S * n * ldk, 1024);
+    L.a_bytes = (size_t)round_up(S * m * ldk, 1024);
+    L.d_bytes = (size_t)round_up(S * m * L.ldd, 1024);
+    const size_t need = L.a_bytes + L.b_bytes + L.d_bytes;
+    QADIC_REQUIRE(ws != nullptr && ws_bytes >= need, QADIC_ERR_VALUE, "workspace too small (%zu < %zu)", ws_bytes,
+                  need);
+    uint8_t* bs = static_cast<uint8_t*>(ws);
+    uint8_t* as = bs + L.b_bytes;
+    uint8_t* dd = as + L.a_bytes;
+    auto planes = [&](auto kk) {
+        constexpr int K = decltype(kk)::value;
+        if (!b_ready) {
+            const int tk = (int)((ldk + 127) / 128), tj = (int)((n + 31) / 32);
+            const int64_t tiles = (int64_t)tk * tj;
+            const int grid = (int)(tiles < 4LL * num_sms() ? tiles : 4LL * num_sms());
+            QADIC_TIMED("i8k planes B", s,
+                        planes8_b_kernel<K><<<grid, 256, 0, s>>>(b, kdim, n, f.p, ps, bs, ldk, n * ldk, tk, tj));
+        }
+        const int64_t items = m * (ldk / 16);
+        const int grid = (int)((items + 255) / 256 < 8LL * num_sms() ? (items + 255) / 256 : 8LL * num_sms());
+        QADIC_TIMED("i8k planes A", s,
+                    planes8_a_kernel<K><<<grid, 256, 0, s>>>(a, m, kdim, f.p, ps, as, ldk, m * ldk));
+    };
+    switch (k) {
+        case 1: planes(std::integral_constant<int, 1>{}); break;
+        case 2: planes(std::integral_constant<int, 2>{}); break;
+        case 3: planes(std::integral_constant<int, 3>{}); break;
+        default: planes(std::integral_constant<int, 4>{}); break;
+    }
+    int rc = check_launch("i8k planes");
+    if (rc) return rc;
+    const bool pair = pair_mode();
+    constexpr int BN = Cfg<KIND_I8>::BN;
+    CUtensorMap ta, tb;
+    rc = make_tmap(&ta, as, kdim, S * m, ldk, BM);
+    if (rc) return rc;
+    rc = make_tmap(&tb, bs, kdim, S * n, ldk, pair ? BN / 2 : BN);
+    if (rc) return rc;
+    Params prm = {};
+    prm.group_m = GROUP_M;
+    prm.M = m;
+    prm.N = n;
+    prm.p = f.p;
+    prm.offset = 0;
+    prm.magic64 = wide_magic(f.p);
+    prm.m_tiles = (int)((m + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM));
+    prm.n_tiles = (int)((n + BN - 1) / BN);
+    prm.n_full = (int)(n / BN);
+    prm.num_kb = (int)((kdim + BK - 1) / BK);
+    prm.planes = S;
+    if (k == 1) {  // one plane: the GEMM writes C directly
+        prm.c = c;
+        prm.ldc = n;
+        prm.nibble_out = 0;
+    } else {
+        prm.c = dd;
+        prm.ldc = L.ldd;
+        prm.c_plane = m * L.ldd;
+        prm.nibble_out = 1;
+    }
+    rc = pair ? launch_gemm<KIND_I8, true>(ta, tb, prm, s, "i8k gemm")
+              : launch_gemm<KIND_I8, false>(ta, tb, prm, s, "i8k gemm");
+    if (rc || k == 1) return rc;
+    const uint32_t magic = small_magic(f.p);
+    switch (k) {
+        case 2: launch_combine<2>(dd, m, n, L, f.p, magic, ps, c, s); break;
+        case 3: launch_combine<3>(dd, m, n, L, f.p, magic, ps, c, s); break;
+        default: launch_combine<4>(dd, m, n, L, f.p, magic, ps, c, s); break;
+    }
+    return check_launch("i8k combine");
+}
+
 }  // namespace tc
 
 bool tc_u64_ok(int64_t m, int64_t k, int64_t n, const void* a) {
@@ -2198,6 +2455,37 @@ int tc_kara_right_cmm(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdi
     f.magic = small_magic(p);
     f.xpow[0][0] = 1;
     return tc_kara_gf_matmul(f, a, b, m, kdim, n, ws, ws_bytes, c, s, false);
+}
+
+// I8K engine: evaluation planes on int8 (p <= 7 for the nibble D planes and the
+// SWAR combine; K (p-1)^2 < 2^31 for the int32 accumulator)
+bool tc_kara8_ok(uint32_t p, int64_t kdim, int k) {
+    int ncodes = 1;
+    for (int i = 0; i < k; ++i) ncodes *= (int)p;
+    return p <= 7 && kara_planes(p, k) <= tc::KMAX_S && ncodes <= tc::PT_CODES &&
+           (__int128)kdim * (p - 1) * (p - 1) < ((__int128)1 << 31);
+}
+
+size_t tc_kara8_workspace(uint32_t p, int64_t m, int64_t kdim, int64_t n, int k) {
+    return tc::kara8_workspace(kara_planes(p, k), m, kdim, n);
+}
+
+int tc_kara8_gf_matmul(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
+                       void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s, bool b_ready) {
+    QADIC_REQUIRE(tc_kara8_ok(f.p, kdim, (int)f.k), QADIC_ERR_PARAMS,
+                  "i8k engine needs p <= 7, K*(p-1)^2 < 2^31 and at most %d planes", tc::KMAX_S);
+    return tc::run_kara8(f, a, b, m, kdim, n, ws, ws_bytes, c, s, b_ready);
+}
+
+int tc_kara8_right_cmm(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n, uint32_t p, void* ws,
+                       size_t ws_bytes, uint8_t* c, cudaStream_t s) {
+    FieldConst f = {};
+    f.p = p;
+    f.k = 1;
+    f.t = 8;
+    f.magic = small_magic(p);
+    f.xpow[0][0] = 1;
+    return tc_kara8_gf_matmul(f, a, b, m, kdim, n, ws, ws_bytes, c, s, false);
 }
 
 // ---- entry points used by matmul_api.cu ---------------------------------------

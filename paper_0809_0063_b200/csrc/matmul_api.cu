@@ -24,6 +24,12 @@ int tc_kara_gf_matmul(const FieldConst& f, const uint8_t* a, const uint8_t* b, i
                       void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s, bool b_ready);
 int tc_kara_right_cmm(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n, uint32_t p, void* ws,
                       size_t ws_bytes, uint8_t* c, cudaStream_t s);
+bool tc_kara8_ok(uint32_t p, int64_t kdim, int k);
+size_t tc_kara8_workspace(uint32_t p, int64_t m, int64_t kdim, int64_t n, int k);
+int tc_kara8_gf_matmul(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
+                       void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s, bool b_ready);
+int tc_kara8_right_cmm(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n, uint32_t p, void* ws,
+                       size_t ws_bytes, uint8_t* c, cudaStream_t s);
 size_t f64_gf_workspace(int64_t m, int64_t kdim, int64_t n, int k);
 size_t f64_cmm_workspace(int64_t m, int64_t kdim, int64_t n, int d);
 int f64_gf_matmul(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
@@ -52,6 +58,7 @@ static int gf_matmul_dev(const FieldConst& f, const uint8_t* a, const uint8_t* b
                          bool b_ready) {
     const int eng = resolve_engine(engine, f.p, kdim, (int)f.k);
     if (eng == QADIC_ENGINE_F4K_TC) return tc_kara_gf_matmul(f, a, b, m, kdim, n, ws, ws_bytes, c, s, b_ready);
+    if (eng == QADIC_ENGINE_I8K_TC) return tc_kara8_gf_matmul(f, a, b, m, kdim, n, ws, ws_bytes, c, s, b_ready);
     if (eng == QADIC_ENGINE_I8_TC || eng == QADIC_ENGINE_F4_TC)
         return tc_gf_matmul(tc_kind(eng), f, a, b, m, kdim, n, ws, ws_bytes, c, s);
     QADIC_REQUIRE(eng == QADIC_ENGINE_F64_DMMA, QADIC_ERR_VALUE, "unknown engine %d", engine);
@@ -79,6 +86,7 @@ size_t qadic_gf_matmul_workspace(const qadic_field_desc* f, int64_t m, int64_t k
     if (!f || m < 0 || kdim < 0 || n < 0) return 0;
     const int eng = resolve_engine(engine, (uint32_t)f->p, kdim, f->k);
     if (eng == QADIC_ENGINE_F4K_TC) return tc_kara_workspace((uint32_t)f->p, m, kdim, n, f->k);
+    if (eng == QADIC_ENGINE_I8K_TC) return tc_kara8_workspace((uint32_t)f->p, m, kdim, n, f->k);
     return eng == QADIC_ENGINE_F64_DMMA ? f64_gf_workspace(m, kdim, n, f->k)
                                         : tc_workspace(tc_kind(eng), m, kdim, n, f->k);
 }
@@ -103,6 +111,7 @@ size_t qadic_right_cmm_workspace(int64_t m, int64_t kdim, int64_t n, int64_t p, 
     if (m < 0 || kdim < 0 || n < 0 || d < 0) return 0;
     const int eng = resolve_engine(engine, (uint32_t)p, kdim, 1);
     if (eng == QADIC_ENGINE_F4K_TC) return tc_kara_workspace((uint32_t)p, m, kdim, n, 1);
+    if (eng == QADIC_ENGINE_I8K_TC) return tc_kara8_workspace((uint32_t)p, m, kdim, n, 1);
     return eng == QADIC_ENGINE_F64_DMMA ? f64_cmm_workspace(m, kdim, n, d) : tc_workspace(tc_kind(eng), m, kdim, n, 1);
 }
 
@@ -123,6 +132,7 @@ int qadic_right_cmm_u8(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kd
     }
     const int eng = resolve_engine(engine, (uint32_t)p, kdim, 1);
     if (eng == QADIC_ENGINE_F4K_TC) return tc_kara_right_cmm(a, b, m, kdim, n, (uint32_t)p, ws, ws_bytes, c, s);
+    if (eng == QADIC_ENGINE_I8K_TC) return tc_kara8_right_cmm(a, b, m, kdim, n, (uint32_t)p, ws, ws_bytes, c, s);
     if (eng == QADIC_ENGINE_I8_TC || eng == QADIC_ENGINE_F4_TC)
         return tc_right_cmm(tc_kind(eng), a, b, m, kdim, n, (uint32_t)p, ws, ws_bytes, c, s);
     QADIC_REQUIRE(eng == QADIC_ENGINE_F64_DMMA, QADIC_ERR_VALUE, "unknown engine %d", engine);

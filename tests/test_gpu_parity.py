@@ -208,7 +208,8 @@ class TestGFDot:
 # ---------------------------------------------------------------------------
 # cfg3 / cfg5: GF(p^k) matmul, both engines
 # ---------------------------------------------------------------------------
-ENGINES = ["i8", "f64", "fp4", "fp4k"]
+ENGINES = ["i8", "f64", "fp4", "fp4k", "i8k"]
+PLANE_ENGINES = ("fp4k", "i8k")  # evaluation planes: p <= 7 and a plane plan (<= 8 planes, p^k <= 1024 codes)
 
 
 def _fp4k_plan_fits(p, k):
@@ -225,7 +226,7 @@ class TestGFMatmul:
     def test_golden(self, golden, golden_scalars, engine, fname, pre):
         f = _field(golden_scalars, fname)
         sfx = "_idx" if pre.startswith("cfg") else ""
-        if engine in ("fp4", "fp4k") and f.p > 7:  # centred residues beyond E2M1's exact integers
+        if engine in ("fp4", "fp4k", "i8k") and f.p > 7:  # beyond E2M1's exact integers / the nibble D planes
             with pytest.raises(Q.ParamsViolation):
                 f.matmul(golden[f"{pre}_a{sfx}"], golden[f"{pre}_b{sfx}"], engine=engine)
             return
@@ -284,7 +285,7 @@ class TestGFMatmul:
         a = g.integers(0, 7, (20, 120000, 3), dtype=np.uint8)
         b = g.integers(0, 7, (120000, 24, 3), dtype=np.uint8)
         ref = O.gf_matmul_planes(of, a, b)
-        for eng in ("auto", "fp4k", "i8"):
+        for eng in ("auto", "fp4k", "i8", "i8k"):
             assert np.array_equal(f.matmul_coeffs(a, b, engine=eng), ref), eng
 
     @pytest.mark.parametrize("p,k", [(2, 2), (2, 3), (3, 4), (5, 3), (5, 4), (13, 2)])
@@ -301,12 +302,12 @@ class TestGFMatmul:
         a = g.integers(0, p, (m, kd, k), dtype=np.uint8)
         b = g.integers(0, p, (kd, n, k), dtype=np.uint8)
         ref = O.gf_matmul_planes(of, a, b)
-        for eng in ("auto", "i8", "fp4", "fp4k"):
-            if eng in ("fp4", "fp4k") and p > 7:
+        for eng in ("auto", "i8", "fp4", "fp4k", "i8k"):
+            if eng in ("fp4", "fp4k", "i8k") and p > 7:
                 with pytest.raises(Q.ParamsViolation):
                     f.matmul_coeffs(a, b, engine=eng)
                 continue
-            if eng == "fp4k" and not _fp4k_plan_fits(p, k):
+            if eng in PLANE_ENGINES and not _fp4k_plan_fits(p, k):
                 with pytest.raises(Q.ParamsViolation):
                     f.matmul_coeffs(a, b, engine=eng)
                 continue
