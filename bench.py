@@ -171,6 +171,7 @@ def build_step(cfg, engine, rank, ws, torch, dist, Q, W):
                                "parallelism": f"grid{R}x{C} (C blocks; B broadcast once at set-up)" if ws > 1
                                else "single"})
         meta["work"] = W.work_units(c, (rows, kd, cols))
+        meta["variant_step"] = lambda eng: (lambda i: f.matmul_coeffs(a, b, engine=eng, out=out))
         return step, e2e, units, e2e_bytes, meta
     if cfg == 4:
         (n,) = c.shape
@@ -219,6 +220,13 @@ def build_step(cfg, engine, rank, ws, torch, dist, Q, W):
         meta["work"]["i8_macs"] = rows * n * cols
         meta["work"]["kara_macs"] = rows * n * cols
         h2d = pin_full.numel() if pin_full is not None else pin_rows.numel() + pin_cols.numel()
+
+        def variant_step(eng):
+            def vstep(i):
+                Q.cmm.right_cmm(a_rows, Q.cmm.compress_rows(b_cols, prm), engine=eng, out=out)
+            return vstep
+
+        meta["variant_step"] = variant_step
         return step, e2e, units, (h2d, rows * cols), meta
     # batched configs: rotate buffer sets totalling > L2 so every step reads HBM
     if cfg == 1:
@@ -450,6 +458,65 @@ def _matmul_sample_inputs(c, rows):
     return {"a": x["a"][:max(rows, 64)], "b": x["b"]}
 
 
+def measure_variants(args, cfg, engine, meta, units, work, peaks, peak_src, torch, N, W):
+    """The north star's other exact GEMM engines on the same inputs (BASELINE.json:
+    the paper's FP64 DMMA formulation and INT8 coefficient planes are both reported):
+    a few CUDA-event-timed steps each after the headline measurement, with the
+    dominant kernel's roofline from a profiled pass."""
+    import ctypes
+
+    out = {}
+    lib = N.lib()
+    if "f64_probe_tflops" not in peaks:  # the DMMA pipe, measured live (roofline denominator of f64)
+        pr = pipe_probe(N, "f64", 0.1)
+        if "burst" in pr:
+            peaks = dict(peaks, f64_probe_tflops=pr["burst"])
+    for eng in ("i8k", "i8", "f64"):
+        if eng == engine or (eng == "i8k" and cfg == 4):  # k = 1: i8k only adds conversions
+            continue
+        step = meta["variant_step"](eng)
+        try:
+            step(0)
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            step(1)
+            torch.cuda.synchronize()
+            one = time.perf_counter() - t
+            k = max(2, min(20, int(0.5 / max(one, 1e-4))))  # ~0.5 s per engine
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for i in range(k):
+                step(i)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / k
+            lib.qadic_profile_enable(1)  # per-kernel events over the same k steps
+            for i in range(k):
+                step(i)
+            torch.cuda.synchronize()
+            lib.qadic_profile_enable(0)
+            buf = ctypes.create_string_buffer(1 << 16)
+            lib.qadic_profile_collect.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+            lib.qadic_profile_collect(buf, len(buf))
+            prof = parse_prof(buf.value.decode())
+            kname = dominant_kernel(cfg, eng, prof)
+            w = dict(work)
+            if eng == "f64" and cfg in (3, 5):
+                c_ = W.CONFIGS[cfg]
+                w["f64_fmas"] = w["madds"] * (c_.k if cfg == 5 else 1)
+            if eng == "f64" and cfg == 4:
+                n = W.CONFIGS[4].shape[0]
+                w["f64_fmas"] = n * n * (-(-n // 3))
+            roof = roofline(cfg, eng, kname, prof.get(kname), w, peaks, peak_src)
+            out[eng] = {"ms_per_step": round(ms, 4), "value": units / (ms / 1e3), "steps": k,
+                        "kernel": kname, "achieved": roof["achieved"] if roof else None,
+                        "unit": roof["unit"] if roof else None, "frac": roof["frac"] if roof else None,
+                        "kernels_ms_per_step": {kk: round(v[1] / k, 4) for kk, v in prof.items()}}
+        except Exception as exc:  # pragma: no cover - report, never fail the headline line
+            out[eng] = {"error": str(exc)[:200]}
+    return out
+
+
 def run_ours(args):
     import torch
 
@@ -595,6 +662,8 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "clocks": clocks,
     }
+    if ws == 1 and cfg in (3, 4, 5) and not args.no_variants and "variant_step" in meta:
+        line["variants"] = measure_variants(args, cfg, engine, meta, units, work, peaks, peak_src, torch, N, W)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_leg(cfg, args)
     if rank == 0:
@@ -812,6 +881,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-probe", action="store_true", help="skip the measured pipe-peak probe after the timed region")
+    ap.add_argument("--no-variants", action="store_true",
+                    help="skip the other exact GEMM engines (i8k, i8, f64) measured after the headline")
     ap.add_argument("--no-graph", action="store_true", help="eager launches for cfg1/cfg2")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup) if args.impl == "ours" else args.warmup
