@@ -61,3 +61,41 @@ def test_our_arm_line():
     assert d["gpu_launches"] == 200
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert d["e2e"]["h2d_bytes_per_step"] == 2 * (1 << 20) * 4
+
+
+def test_pipe_probe_attach_logic():
+    """roofline.pipe_probe: burst for short timed regions, sustained for long ones."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    roof = {"achieved": 7000.0}
+    probe = {"burst": 8900.0, "sustained": 7900.0}
+    bench._attach_probe(roof, dict(probe), sustained=False)
+    assert roof["pipe_probe"]["compare"] == "burst" and abs(roof["pipe_probe"]["frac"] - 7000 / 8900) < 1e-3
+    bench._attach_probe(roof, dict(probe), sustained=True)
+    assert roof["pipe_probe"]["compare"] == "sustained" and abs(roof["pipe_probe"]["frac"] - 7000 / 7900) < 1e-3
+    r2 = {"achieved": 1.0}
+    bench._attach_probe(r2, {"error": "no GPU"}, sustained=True)  # a failed probe leaves the roofline alone
+    assert "pipe_probe" not in r2
+    bench._attach_probe(None, dict(probe), sustained=True)
+
+
+def test_roofline_ops_per_engine():
+    """algorithmic ops of each GEMM kernel: expanded forms count k^2 MACs per GF
+    mult-add, evaluation planes S, the f64 engine its FMAs; the f64 denominator is
+    the live DMMA probe when present."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    work = {"i8_macs": 9 * 10 ** 12, "kara_macs": 5 * 10 ** 12, "f64_fmas": 10 ** 12, "io_bytes": 10 ** 9}
+    peaks = {"hbm_gbs": 6500.0, "bf16_tflops": 1650.0}
+    one_ms = (1, 1.0)  # one launch of 1 ms
+    assert bench.roofline(5, "i8", "i8 gemm", one_ms, work, peaks, "measured")["achieved"] == 18000.0
+    assert bench.roofline(5, "i8k", "i8k gemm", one_ms, work, peaks, "measured")["achieved"] == 10000.0
+    assert bench.roofline(5, "fp4k", "fp4k gemm", one_ms, work, peaks, "measured")["achieved"] == 10000.0
+    assert bench.roofline(5, "fp4", "fp4 gemm", one_ms, work, peaks, "measured")["achieved"] == 18000.0
+    r = bench.roofline(5, "f64", "f64 dmma gemm", one_ms, work, dict(peaks, f64_probe_tflops=37.1), "measured")
+    assert r["achieved"] == 2000.0 and r["peak"] == 37.1 and "probe" in r["peak_source"]
+    assert bench.roofline(5, "f64", "f64 dmma gemm", one_ms, work, peaks, "measured")["peak"] == 40.0
+    h = bench.roofline(1, "auto", "polymul_k4", one_ms, work, peaks, "measured")
+    assert h["bound"] == "hbm" and h["achieved"] == 1000.0 and h["peak"] == 6500.0
