@@ -78,7 +78,9 @@ __device__ __forceinline__ double fold_word(double r, const FieldConst& f) {
     return (double)w;
 }
 
-template <int K, Epi EPI, bool SMEM_TABLES>
+// FOLD: the launch folds the packed accumulators every prm.fold terms (the fold
+// code is compiled only into the kernels that need it)
+template <int K, Epi EPI, bool SMEM_TABLES, bool FOLD>
 __global__ void __launch_bounds__(THREADS, 1) dmma_gemm_kernel(Params prm, FieldConst f) {
     constexpr int ND = EPI == EPI_GF ? 2 * K - 2 : (EPI == EPI_GF1 ? K - 1 : 0);
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -133,8 +135,7 @@ __global__ void __launch_bounds__(THREADS, 1) dmma_gemm_kernel(Params prm, Field
         cp_async_commit();
         const double* a_s = sA + (kt % STAGES) * BM * SA + (wm * 32 + ar) * SA + ac;
         const double* b_s = sB + (kt % STAGES) * BK * SB + ac * SB + wn * 32 + ar;
-#pragma unroll
-        for (int k4 = 0; k4 < BK / 4; ++k4) {
+        auto k4_step = [&](int k4) {
             double af[4], bf[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) af[i] = a_s[i * 8 * SA + k4 * 4];
@@ -144,8 +145,22 @@ __global__ void __launch_bounds__(THREADS, 1) dmma_gemm_kernel(Params prm, Field
             for (int i = 0; i < 4; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-            if ((EPI == EPI_GF || EPI == EPI_GF1) && prm.fold) {
-                const int64_t kdone = (int64_t)kt * BK + (k4 + 1) * 4;
+        };
+        // delayed-reduction folds land on k4 boundaries; a stage holds one only
+        // every fold / BK stages, so the common stage runs the plain DMMA stream
+        // and only a fold stage checks per k4 step (the per-step modulo cost
+        // ~10% of the issue slots at cfg5)
+        const int64_t kbase = (int64_t)kt * BK;
+        const bool fold_here = FOLD && (EPI == EPI_GF || EPI == EPI_GF1) && prm.fold &&
+                               (kbase + BK) / prm.fold != kbase / prm.fold && kbase + BK <= prm.Kp;
+        if (!fold_here) {
+#pragma unroll
+            for (int k4 = 0; k4 < BK / 4; ++k4) k4_step(k4);
+        } else {
+#pragma unroll
+            for (int k4 = 0; k4 < BK / 4; ++k4) {
+                k4_step(k4);
+                const int64_t kdone = kbase + (k4 + 1) * 4;
                 if (kdone % prm.fold == 0 && kdone < prm.Kp) {
 #pragma unroll
                     for (int i = 0; i < 4; ++i)
@@ -299,7 +314,9 @@ static int launch(const Params& prm, const FieldConst& f, cudaStream_t s) {
     const size_t smem = PIPE_BYTES + (smem_tables ? 2 * TABLE_MAX * sizeof(uint32_t) : 0);
     dim3 grid((unsigned)(prm.Np / BN), (unsigned)((prm.M + BM - 1) / BM));
     QADIC_REQUIRE(grid.y <= 65535, QADIC_ERR_UNSUPPORTED, "m too large");
-    auto kern = smem_tables ? dmma_gemm_kernel<K, EPI, true> : dmma_gemm_kernel<K, EPI, false>;
+    const bool fold = (EPI == EPI_GF || EPI == EPI_GF1) && prm.fold;
+    auto kern = smem_tables ? (fold ? dmma_gemm_kernel<K, EPI, true, true> : dmma_gemm_kernel<K, EPI, true, false>)
+                            : (fold ? dmma_gemm_kernel<K, EPI, false, true> : dmma_gemm_kernel<K, EPI, false, false>);
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     QADIC_TIMED("f64 dmma gemm", s, kern<<<grid, THREADS, smem, s>>>(prm, f));
     return check_launch("f64 dmma gemm");
