@@ -9,13 +9,13 @@ R=${1:-r01}
 O=gpurun_out/$R
 mkdir -p $O
 NCU="ncu --clock-control none"
-B="python bench.py --no-cpu-baseline"
+B="python bench.py --no-cpu-baseline --no-variants"
 ok=1
 python bench.py > $O/bench_default.json 2>>$O/bench.err || ok=0   # the driver's default command
 for c in 1 2; do $B --config $c --warmup 5 > $O/bench_cfg$c.json 2>>$O/bench.err || ok=0; done
 for c in redq pack unpack mm64; do python bench.py --config $c > $O/bench_$c.json 2>>$O/bench.err || ok=0; done
 for c in 3 4 5; do
-  for e in auto i8 fp4 fp4k; do $B --config $c --engine $e --steps 20 --warmup 3 > $O/bench_cfg${c}_$e.json 2>>$O/bench.err || ok=0; done
+  for e in auto i8 i8k fp4 fp4k; do $B --config $c --engine $e --steps 20 --warmup 3 > $O/bench_cfg${c}_$e.json 2>>$O/bench.err || ok=0; done
 done
 $B --config 3 --engine f64 --steps 3 --warmup 3 > $O/bench_cfg3_f64.json 2>>$O/bench.err || ok=0
 $B --config 5 --engine f64 --steps 3 --warmup 3 > $O/bench_cfg5_f64.json 2>>$O/bench.err || ok=0
