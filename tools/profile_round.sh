@@ -51,5 +51,8 @@ REPS=200 python tools/fp4_library_peak.py 8192 residues > $O/fp4_library_ceiling
 python tools/hbm_write_probe.py > $O/hbm_write_probe.json 2>>$O/bench.err
 python tools/e2e_probe.py > $O/e2e_probe.txt 2>>$O/bench.err
 python tools/pageable_probe.py > $O/pageable_probe.txt 2>>$O/bench.err
+# gpurun copies back at most 64 MiB: keep the CSV exports, and of the reports only the headline GEMM's
+for f in $O/*.ncu-rep; do case "$f" in *cfg5_fp4k_gemm.ncu-rep) ;; *) rm -f "$f" ;; esac; done
+du -sh $O
 echo "bench ok=$ok"
 ls -la $O | head -80
