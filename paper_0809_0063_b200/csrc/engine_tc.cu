@@ -1281,18 +1281,15 @@ __global__ void __launch_bounds__(256) planes_kernel(const uint8_t* __restrict__
                                                      uint8_t* __restrict__ out, int64_t ld, int64_t plane_stride) {
 
     __shared__ uint32_t tab[PT_CODES];
-    int ncodes = 1;
-    for (int i = 0; i < K; ++i) ncodes *= (int)p;
-    for (int i = threadIdx.x; i < ncodes; i += blockDim.x) tab[i] = gtab[i];
-    __syncthreads();
     const int64_t chunks = ld / 16;
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= R * chunks) return;
-    const int64_t r = idx / chunks, q = idx % chunks;
+    const bool live = idx < R * chunks;
+    const int64_t r = live ? idx / chunks : 0, q = live ? idx % chunks : 0;
     const int64_t kk0 = q * 32;
     const uint8_t* row = src + (r * Kd + kk0) * K;
+    // the row's loads go out first; the plane table is staged while they are in flight
     uint32_t in[8 * K];
-    if (kk0 + 32 <= Kd && ((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
+    if (live && kk0 + 32 <= Kd && ((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
 #pragma unroll
         for (int v = 0; v < 2 * K; ++v) {
             const uint4 x = __ldg(reinterpret_cast<const uint4*>(row) + v);
@@ -1301,10 +1298,16 @@ __global__ void __launch_bounds__(256) planes_kernel(const uint8_t* __restrict__
     } else {
 #pragma unroll
         for (int v = 0; v < 8 * K; ++v) in[v] = 0;
+        if (live)
 #pragma unroll
-        for (int e = 0; e < 32 * K; ++e)
-            if (kk0 + e / K < Kd) in[e >> 2] |= (uint32_t)row[e] << (8 * (e & 3));
+            for (int e = 0; e < 32 * K; ++e)
+                if (kk0 + e / K < Kd) in[e >> 2] |= (uint32_t)row[e] << (8 * (e & 3));
     }
+    int ncodes = 1;
+    for (int i = 0; i < K; ++i) ncodes *= (int)p;
+    for (int i = threadIdx.x; i < ncodes; i += blockDim.x) tab[i] = gtab[i];
+    __syncthreads();
+    if (!live) return;
     if constexpr (K == 1) {  // one plane: 4 residues per PRMT lookup
         uint32_t lo, hi;
         byte_lut_from_table(tab, p, lo, hi);
