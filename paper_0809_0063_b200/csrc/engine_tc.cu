@@ -1482,27 +1482,28 @@ __global__ void __launch_bounds__(256) planes_b3_kernel(const __grid_constant__ 
     uint16_t (*codes)[P2_J] = reinterpret_cast<uint16_t (*)[P2_J]>(dsm3 + NB * P2_KK * ROWB);
     uint32_t* tab = reinterpret_cast<uint32_t*>(dsm3 + NB * P2_KK * ROWB + P2_KK * P2_J * 2);
     __shared__ __align__(8) uint64_t bar[NB];
-    build_plane_table(tab, p, K, S, ps, lut, gtab);
-    const CodeCoef<K> cc = make_code_coef<K>(p);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int r4 = lane >> 3, c8 = lane & 7;
     const int64_t ntiles = (int64_t)tiles_kk * tiles_j;
-    if (threadIdx.x == 0) {
-        tma_prefetch(&tmap);
-        for (int i = 0; i < NB; ++i) mbar_init(&bar[i], 1);
-        fence_barrier_init();
-    }
-    __syncthreads();
-    uint32_t lo = 0, hi = 0;
-    if (K == 1) byte_lut_from_table(tab, p, lo, hi);
     auto issue = [&](int64_t t, int buf) {
         const int64_t kk0 = (t % tiles_kk) * P2_KK, j0 = (t / tiles_kk) * P2_J;
         mbar_arrive_expect_tx(&bar[buf], P2_KK * ROWB);
         tma_load_2d(inb + buf * P2_KK * ROWB, &tmap, &bar[buf], (int32_t)(j0 * K), (int32_t)kk0);
     };
-    if (threadIdx.x == 0)
+    // the first tiles' loads go out before the plane table is built (the other
+    // threads wait on the barriers only after the __syncthreads below)
+    if (threadIdx.x == 0) {
+        tma_prefetch(&tmap);
+        for (int i = 0; i < NB; ++i) mbar_init(&bar[i], 1);
+        fence_barrier_init();
         for (int i = 0; i < NB - 1; ++i)
             if ((int64_t)blockIdx.x + (int64_t)i * gridDim.x < ntiles) issue(blockIdx.x + (int64_t)i * gridDim.x, i);
+    }
+    build_plane_table(tab, p, K, S, ps, lut, gtab);
+    const CodeCoef<K> cc = make_code_coef<K>(p);
+    __syncthreads();
+    uint32_t lo = 0, hi = 0;
+    if (K == 1) byte_lut_from_table(tab, p, lo, hi);
     int it = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
         const int buf = it % NB;
