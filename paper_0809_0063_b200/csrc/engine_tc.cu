@@ -138,6 +138,11 @@ struct Params {
     // i = seg_i_lo + segment; A is read at byte offset i * seg_kp + (kb % seg_kpb) * BK
     // of its row, B at row offset (seg_s - i) * N.  seg_kpb = 0: contiguous K.
     int seg_kpb, seg_i_lo, seg_s, seg_kp;
+    // plane_inner: all byte shifts of one output tile run back to back on one CTA
+    // (pair) in a single launch -- shift s = plane index, its segments
+    // seg_lo[s] .. seg_lo[s] + seg_cnt[s] - 1, C accumulated in program order
+    int plane_inner;
+    int seg_lo[8], seg_cnt[8];
     // column-tile range of this launch: tiles n_tile0 .. n_tile0 + n_tiles - 1
     int n_tile0;
     // launched as the programmatic dependent of a concurrent GEMM launch: wait for
@@ -172,7 +177,7 @@ __device__ __forceinline__ int tile_n(const Params& prm, int nt) {
 
 template <int FUSE_K>
 __device__ __forceinline__ void decode_tile(int tile, const Params& prm, int& pl, int& mt, int& nt) {
-    if (FUSE_K) {
+    if (FUSE_K || prm.plane_inner) {
         pl = tile % prm.planes;
         tile_coords(tile / prm.planes, prm.m_tiles, prm.n_tiles, mt, nt, prm.group_m);
     } else {
@@ -229,8 +234,9 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
     // work units: one tile of one plane; fused, one output tile with all its
     // planes processed back to back by the same CTA (group)
     const int plane_tiles = prm.m_tiles * prm.n_tiles;
-    const int per_unit = FUSE_K ? prm.planes : 1;
-    const int units = FUSE_K ? plane_tiles : plane_tiles * prm.planes;
+    const bool inner = FUSE_K || prm.plane_inner;
+    const int per_unit = inner ? prm.planes : 1;
+    const int units = inner ? plane_tiles : plane_tiles * prm.planes;
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmap_a);
@@ -275,21 +281,25 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                 decode_tile<FUSE_K>(tile, prm, pl, mt, nt);
                 if (MC) mt = 2 * mt + (int)pidx;
                 nt += prm.n_tile0;
-                const int arow = (int)(pl * prm.M) + mt * G::TILE_M + (int)rank * BM;
+                const int pstack = prm.plane_inner ? 0 : pl;  // planes stacked along the operand rows
+                const int arow = (int)(pstack * prm.M) + mt * G::TILE_M + (int)rank * BM;
                 // the pair splits the tile's (possibly narrowed, see tile_n) columns in halves
-                const int brow = (int)(pl * prm.N) + nt * BN + (int)rank * (tile_n<BN>(prm, nt) / 2);
+                const int brow = (int)(pstack * prm.N) + nt * BN + (int)rank * (tile_n<BN>(prm, nt) / 2);
+                const int nkb = prm.plane_inner ? prm.seg_cnt[pl] * prm.seg_kpb : prm.num_kb;
+                const int seg_lo = prm.plane_inner ? prm.seg_lo[pl] : prm.seg_i_lo;
+                const int seg_s = prm.plane_inner ? pl : prm.seg_s;
                 // MC: CTA (pair i, rank r) loads slice i of half r and multicasts it to both pairs
                 const uint16_t mc_mask = (uint16_t)((1u << crank) | (1u << (crank ^ 2u)));
-                for (int kb = 0; kb < prm.num_kb; ++kb) {
+                for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(&empty_bar[stage], phase ^ 1);
                     uint8_t* sa = smem + stage * G::STAGE_BYTES;
                     uint8_t* sb = sa + G::A_BYTES;
                     int ak = kb * BK, bk = kb * BK, boff = 0;
                     if (prm.seg_kpb) {  // byte-plane segments of the uint64 GEMM
-                        const int seg = kb / prm.seg_kpb, kin = kb - seg * prm.seg_kpb, i = prm.seg_i_lo + seg;
+                        const int seg = kb / prm.seg_kpb, kin = kb - seg * prm.seg_kpb, i = seg_lo + seg;
                         ak = i * prm.seg_kp + kin * BK;
                         bk = kin * BK;
-                        boff = (prm.seg_s - i) * (int)prm.N;
+                        boff = (seg_s - i) * (int)prm.N;
                     }
                     if (prm.diag_noload && (u != group_id || kb >= NST)) {  // wrong results: power probe
                         if (!PAIR || leader) mbar_arrive(&full_bar[stage]);
@@ -323,6 +333,7 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
             int pl, mt, nt;
             decode_tile<FUSE_K>(u * per_unit + sp, prm, pl, mt, nt);
             nt += prm.n_tile0;
+            const int nkb = prm.plane_inner ? prm.seg_cnt[pl] * prm.seg_kpb : prm.num_kb;
             const uint32_t nn = (uint32_t)tile_n<BN>(prm, nt);
             const uint32_t idesc = KIND == KIND_I8 ? idesc_u8_s32(G::TILE_M, nn) : idesc_mxf4(G::TILE_M, nn);
             const int acc = local & 1;
@@ -330,7 +341,7 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
             mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
             tc_fence_after();
             const uint32_t tmem_d = tmem_base + acc * BN;
-            for (int kb = 0; kb < prm.num_kb; ++kb) {
+            for (int kb = 0; kb < nkb; ++kb) {
                 mbar_wait(&full_bar[stage], phase);
                 tc_fence_after();
                 if (elect_one()) {
@@ -351,10 +362,10 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                     }
                     if (PAIR) {
                         umma_commit_pair(&empty_bar[stage], MC ? 0xF : 0x3);
-                        if (kb == prm.num_kb - 1) umma_commit_pair(&tmem_full[acc], (uint16_t)(0x3u << (2 * pidx)));
+                        if (kb == nkb - 1) umma_commit_pair(&tmem_full[acc], (uint16_t)(0x3u << (2 * pidx)));
                     } else {
                         umma_commit(&empty_bar[stage]);
-                        if (kb == prm.num_kb - 1) umma_commit(&tmem_full[acc]);
+                        if (kb == nkb - 1) umma_commit(&tmem_full[acc]);
                     }
                 }
                 __syncwarp();
@@ -464,13 +475,15 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                 const int64_t col0 = (int64_t)nt * BN + ch * 16;
                 if (!row_ok || col0 >= prm.N) continue;
                 if (KIND == KIND_I8 && prm.c64 != nullptr) {  // byte-plane uint64 GEMM (mod 2^64)
+                    const int shift = prm.plane_inner ? 8 * pl : prm.shift;
+                    const bool acc64 = prm.plane_inner ? (pl > 0 || prm.acc64) : prm.acc64 != 0;
                     uint64_t* crow64 = prm.c64 + row * prm.ldc + col0;
                     const int ncol = (int)(prm.N - col0 < 16 ? prm.N - col0 : 16);
                     if (ncol == 16 && ((reinterpret_cast<uintptr_t>(crow64) & 15) == 0)) {
 #pragma unroll
                         for (int e = 0; e < 16; e += 2) {
-                            ulonglong2 o = make_ulonglong2((uint64_t)v[e] << prm.shift, (uint64_t)v[e + 1] << prm.shift);
-                            if (prm.acc64) {
+                            ulonglong2 o = make_ulonglong2((uint64_t)v[e] << shift, (uint64_t)v[e + 1] << shift);
+                            if (acc64) {
                                 const ulonglong2 old = *reinterpret_cast<const ulonglong2*>(crow64 + e);
                                 o.x += old.x;
                                 o.y += old.y;
@@ -479,8 +492,8 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                         }
                     } else {
                         for (int e = 0; e < ncol; ++e) {
-                            const uint64_t o = (uint64_t)v[e] << prm.shift;
-                            crow64[e] = prm.acc64 ? crow64[e] + o : o;
+                            const uint64_t o = (uint64_t)v[e] << shift;
+                            crow64[e] = acc64 ? crow64[e] + o : o;
                         }
                     }
                     continue;
@@ -2399,25 +2412,47 @@ int tc_matmul_u64(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_t m, 
         if (rc) break;
         rc = make_tmap(&tb_map, bt, kp, (int64_t)nbb * n, kp, pair ? BN / 2 : BN);
         if (rc) break;
-        for (int sp = 0; sp < nplanes && rc == QADIC_OK; ++sp) {
+        Params base = {};
+        base.M = m;
+        base.N = n;
+        base.ldc = n;
+        base.p = 2;
+        base.m_tiles = (int)((m + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM));
+        base.n_tiles = (int)((n + BN - 1) / BN);
+        base.n_full = (int)(n / BN);
+        base.seg_kpb = (int)(kp / BK);
+        base.seg_kp = (int)kp;
+        base.group_m = GROUP_M;
+        base.c64 = c;
+        if (getenv_flag("QADIC_U64_INNER")) {
+            // one launch: every shift s of an output tile back to back on one CTA pair
+            // (no per-launch tails; C accumulated in program order by the same threads).
+            // Measured slower (8192^3: 11.0 vs 10.6 ms): a tile's segments of all shifts
+            // spread the operand working set, the shift-major launches reuse one B plane
+            // across every m tile in L2.  Opt-in.
+            Params prm = base;
+            prm.plane_inner = 1;
+            prm.planes = nplanes;
+            for (int sp = 0; sp < nplanes; ++sp) {
+                const int i_lo = sp - (nbb - 1) > 0 ? sp - (nbb - 1) : 0;
+                const int i_hi = sp < nba - 1 ? sp : nba - 1;
+                prm.seg_lo[sp] = i_lo;
+                prm.seg_cnt[sp] = i_hi - i_lo + 1;
+            }
+            prm.num_kb = prm.seg_cnt[0] * prm.seg_kpb;
+            prm.acc64 = k0 > 0 ? 1 : 0;
+            rc = pair ? launch_gemm<KIND_I8, true>(ta_map, tb_map, prm, s, "u64 byte-plane gemm")
+                      : launch_gemm<KIND_I8, false>(ta_map, tb_map, prm, s, "u64 byte-plane gemm");
+            continue;
+        }
+        for (int sp = 0; sp < nplanes && rc == QADIC_OK; ++sp) {  // one launch per shift (default)
             const int i_lo = sp - (nbb - 1) > 0 ? sp - (nbb - 1) : 0;
             const int i_hi = sp < nba - 1 ? sp : nba - 1;
-            Params prm = {};
-            prm.M = m;
-            prm.N = n;
-            prm.ldc = n;
-            prm.p = 2;
-            prm.m_tiles = (int)((m + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM));
-            prm.n_tiles = (int)((n + BN - 1) / BN);
-            prm.n_full = (int)(n / BN);
-            prm.seg_kpb = (int)(kp / BK);
+            Params prm = base;
             prm.seg_i_lo = i_lo;
             prm.seg_s = sp;
-            prm.seg_kp = (int)kp;
             prm.num_kb = (i_hi - i_lo + 1) * prm.seg_kpb;
             prm.planes = 1;
-            prm.group_m = GROUP_M;
-            prm.c64 = c;
             prm.shift = 8 * sp;
             prm.acc64 = (sp > 0 || k0 > 0) ? 1 : 0;
             rc = pair ? launch_gemm<KIND_I8, true>(ta_map, tb_map, prm, s, "u64 byte-plane gemm")

@@ -632,6 +632,32 @@ print("mcast ok")
 """
 
 
+_U64_INNER_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from oracle import qadic_oracle as O
+from paper_0809_0063_b200 import _kernels
+g = np.random.default_rng(3)
+for (m, k, n, ba, bb) in ((256, 96, 300, 34, 34), (300, 17000, 140, 64, 64), (513, 200, 1024, 20, 64)):
+    a = g.integers(0, 1 << ba, (m, k), dtype=np.uint64)
+    b = g.integers(0, 1 << bb, (k, n), dtype=np.uint64)
+    assert np.array_equal(_kernels.matmul_exact_u64(a, b), O.matmul_exact_u64(a, b)), (m, k, n)
+print("inner ok")
+"""
+
+
+def test_u64_plane_inner_variant():
+    """QADIC_U64_INNER=1: all byte shifts of a tile in one launch (opt-in variant)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _U64_INNER_CHILD, root], env=dict(os.environ, QADIC_U64_INNER="1"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "inner ok" in r.stdout, r.stderr[-2000:]
+
+
 def test_fp4k_multicast_variant():
     import os
     import subprocess
