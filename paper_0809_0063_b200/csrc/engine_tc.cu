@@ -1545,6 +1545,71 @@ __global__ void __launch_bounds__(256) planes_b3_kernel(const __grid_constant__ 
     }
 }
 
+// K = 1 (one plane, cfg4): B [Kd][N] residues -> E2M1 nibbles [N][ld], transposed.
+// Tile 128 kk x 128 j: a thread reads four 16-byte row vectors (the next tile's are
+// loaded during this tile's pass 2), scatters them j-major into shared memory
+// (16-byte chunks XOR-swizzled by j / 16, so a warp's byte stores hit 8 distinct
+// bank quads), then thread (j, g) turns 16 kk into 8 nibble bytes (one 16-byte
+// shared read, four PRMT lookups).  The 16-byte-per-row segments of pass 1 are
+// what the K = 1 tile of planes_b3 (32-byte rows) lacked.
+constexpr int B1_KK = 128, B1_J = 128;
+__global__ void __launch_bounds__(256) planes_b1_kernel(const uint8_t* __restrict__ b, int64_t Kd, int64_t N,
+                                                        uint32_t p, uint32_t* __restrict__ gtab, PlaneSpec ps,
+                                                        uint32_t lut, uint8_t* __restrict__ out, int64_t ld,
+                                                        int tiles_kk, int tiles_j) {
+    __shared__ uint32_t tab[PT_CODES];
+    __shared__ __align__(16) uint8_t res[B1_J][B1_KK];
+    const bool vec = (N % 16 == 0) && ((reinterpret_cast<uintptr_t>(b) & 15) == 0);
+    const int64_t ntiles = (int64_t)tiles_kk * tiles_j;
+    uint4 w[4];
+    auto load = [&](int64_t t) {
+        const int64_t kk0 = (t % tiles_kk) * B1_KK, j0 = (t / tiles_kk) * B1_J;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int c = threadIdx.x + 256 * q, row = c >> 3, cc = c & 7;
+            const int64_t gk = kk0 + row, gj = j0 + 16 * cc;
+            if (vec && gk < Kd && gj + 16 <= N) {
+                w[q] = __ldg(reinterpret_cast<const uint4*>(b + gk * N + gj));
+            } else {
+                uint32_t x[4] = {0, 0, 0, 0};
+                for (int e = 0; e < 16; ++e)
+                    if (gk < Kd && gj + e < N) x[e >> 2] |= (uint32_t)b[gk * N + gj + e] << (8 * (e & 3));
+                w[q] = make_uint4(x[0], x[1], x[2], x[3]);
+            }
+        }
+    };
+    if ((int64_t)blockIdx.x < ntiles) load(blockIdx.x);
+    build_plane_table(tab, p, 1, 1, ps, lut, gtab);
+    __syncthreads();
+    uint32_t lo, hi;
+    byte_lut_from_table(tab, p, lo, hi);
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int64_t kk0 = (t % tiles_kk) * B1_KK, j0 = (t / tiles_kk) * B1_J;
+        __syncthreads();  // previous tile's residues consumed
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int c = threadIdx.x + 256 * q, row = c >> 3, cc = c & 7;
+            const int col = ((((row >> 4) ^ cc) & 7) << 4) | (row & 15);  // swizzled kk position
+            const uint32_t x[4] = {w[q].x, w[q].y, w[q].z, w[q].w};
+#pragma unroll
+            for (int e = 0; e < 16; ++e) res[16 * cc + e][col] = (uint8_t)(x[e >> 2] >> (8 * (e & 3)));
+        }
+        __syncthreads();
+        if (t + gridDim.x < ntiles) load(t + gridDim.x);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int item = threadIdx.x + 256 * q, j = item >> 3, g = item & 7;
+            const int64_t gj = j0 + j, col = (kk0 + 16 * g) / 2;
+            if (gj < N && col < ld) {
+                const uint4 r = *reinterpret_cast<const uint4*>(&res[j][(g ^ ((j >> 4) & 7)) << 4]);
+                const uint32_t o0 = residues_to_e2m1(r.x, lo, hi) | (residues_to_e2m1(r.y, lo, hi) << 16);
+                const uint32_t o1 = residues_to_e2m1(r.z, lo, hi) | (residues_to_e2m1(r.w, lo, hi) << 16);
+                *reinterpret_cast<uint2*>(out + gj * ld + col) = make_uint2(o0, o1);
+            }
+        }
+    }
+}
+
 template <int K>
 constexpr size_t planes_b3_smem() {
     return (size_t)P2_NBUF * P2_KK * P2_J * K + (size_t)P2_KK * P2_J * 2 + PT_CODES * sizeof(uint32_t) + 128;
@@ -1777,7 +1842,18 @@ static void launch_planes(const uint8_t* a, const uint8_t* b, int64_t m, int64_t
         CUtensorMap tm;
         const bool use_tma = ((n * K) % 16 == 0) && ((reinterpret_cast<uintptr_t>(b) & 15) == 0) &&
                              make_tmap_rows(&tm, b, n * K, kdim, n * K, P2_J * K, P2_KK) == QADIC_OK;
-        if (use_tma) {  // TMA-fed; the grid is exactly one wave of resident blocks
+        if (K == 1 && !getenv_flag("QADIC_B1_TMA")) {  // one plane: 16-byte row segments, see planes_b1_kernel
+            const int t1k = (int)((L.ldk * 2 + B1_KK - 1) / B1_KK), t1j = (int)((n + B1_J - 1) / B1_J);
+            const int64_t t1 = (int64_t)t1k * t1j;
+            static int occ1 = 0;
+            if (!occ1) {
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ1, planes_b1_kernel, 256, 0);
+                if (occ1 < 1) occ1 = 1;
+            }
+            const int grid = (int)(t1 < (int64_t)occ1 * num_sms() ? t1 : (int64_t)occ1 * num_sms());
+            QADIC_TIMED("fp4k planes B", s,
+                        planes_b1_kernel<<<grid, 256, 0, s>>>(b, kdim, n, p, tab, ps, lut, bs, L.ldk, t1k, t1j));
+        } else if (use_tma) {  // TMA-fed; the grid is exactly one wave of resident blocks
             static int occ = 0;
             if (!occ) {
                 cudaFuncSetAttribute(planes_b3_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
