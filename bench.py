@@ -6,9 +6,12 @@
 One "step" is one pass of the hot path over one batch of the config's
 synthetic seeded input (BASELINE.json configs).  Default workload: cfg5 --
 the GF(7^3) matmul 8192^3 that BASELINE.json runs at 1/2/4/8 GPUs.
-Multi-GPU (torchrun, one rank per GPU): matmul configs shard A by row
-blocks and broadcast B once per step over NCCL (no reduction); batched
-configs shard the batch with no collective.  Prints ONE JSON line on rank 0.
+Multi-GPU (one rank per GPU; `--gpus N` without torchrun re-launches itself
+under torch.distributed.run): matmul configs shard A by row blocks and
+broadcast B over NCCL INSIDE every step, in column panels overlapped with the
+products (shard.RowBlockStep; no reduction collective); `--partition grid`
+keeps the 2-D block grid with B broadcast once at set-up.  Batched configs
+shard the batch with no collective.  Prints ONE JSON line on rank 0.
 """
 
 from __future__ import annotations
@@ -128,17 +131,130 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
-def build_step(cfg, engine, rank, ws, torch, dist, Q, W):
+def config_dict(cfg, engine, ws, partition="rows", panels=None):
+    """The `config` object of the JSON line: static workload facts only, so the
+    reference arm prints the same dict as ours."""
+    from paper_0809_0063_b200 import workloads as W
+
+    c = W.CONFIGS[cfg]
+    d = {"workload": c.label}
+    if cfg in (3, 5):
+        m, kd, n = c.shape
+        d.update({"M": m, "N": n, "K": kd, "k": c.k, "p": c.p, "fold_every": c.dot_bound, "engine": engine,
+                  "l2": "inputs 2x%d MiB > 126 MB L2" % ((kd * n * c.k) >> 20)})
+    elif cfg == 4:
+        (n,) = c.shape
+        d.update({"n": n, "p": 3, "t": W.params_for(c).t, "entries_per_word": W.params_for(c).k, "engine": engine,
+                  "density": 0.5, "l2": "A 256 MiB > 126 MB L2"})
+    else:
+        d.update({"shape": list(c.shape), "p": c.p, "k": c.k, "engine": "fused",
+                  "l2": "rotating 16 input sets > 126 MB L2"})
+    if ws == 1:
+        d["parallelism"] = "single"
+    elif cfg in (1, 2):
+        d["parallelism"] = f"batch{ws}"
+    elif partition == "rows":
+        d["parallelism"] = (f"rows{ws} (A row blocks; B broadcast over NCCL inside every step in {panels} "
+                            "column panels overlapped with the products)")
+    else:
+        from paper_0809_0063_b200 import shard
+
+        R, C = shard.grid2d(ws)
+        d["parallelism"] = f"grid{R}x{C} (C blocks; B broadcast once at set-up)"
+    return d
+
+
+def build_rowblock_step(cfg, engine, rank, ws, torch, Q, W, args, meta):
+    """Row-block partition (the north star's): rank r keeps A[rows_r]; rank 0
+    holds B in column-panel-major order and broadcasts it over NCCL inside every
+    step, panel by panel on a communication stream, each panel's product
+    starting as soon as it lands (shard.RowBlockStep).  No reduction."""
+    c = W.CONFIGS[cfg]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    P = args.panels
+    if cfg == 4:
+        (n,) = c.shape
+        m = kd = n
+        prm = W.params_for(c)
+        host_a = W.make_inputs(c)["a"]
+        host_b = host_a  # A^2: B = A
+        out_k = ()
+
+        def compute(a_rows, bp, cp, eng=engine):
+            Q.cmm.right_cmm(a_rows, Q.cmm.compress_rows(bp, prm), engine=eng, out=cp)
+    else:
+        f = W.field_for(c)
+        m, kd, n = c.shape
+        x = W.make_inputs(c)
+        host_a, host_b = x["a"], x["b"]
+        out_k = (c.k,)
+
+        def compute(a_rows, bp, cp, eng=engine):
+            f.matmul_coeffs(a_rows, bp, engine=eng, out=cp)
+    r0, r1 = Q.shard.row_block(m, ws, rank)
+    rows = r1 - r0
+    bounds = Q.shard.panel_bounds(n, P)
+    a = torch.from_numpy(np.ascontiguousarray(host_a[r0:r1])).to(dev)
+    if rank == 0:
+        b_panels = [p.to(dev) for p in Q.shard.split_panels(torch.from_numpy(host_b), P)]
+    else:
+        b_panels = [torch.empty((kd, j1 - j0) + out_k, dtype=torch.uint8, device=dev) for j0, j1 in bounds]
+    c_panels = [torch.empty((rows, j1 - j0) + out_k, dtype=torch.uint8, device=dev) for j0, j1 in bounds]
+    runner = Q.shard.RowBlockStep(a, b_panels, c_panels, compute)
+
+    def step(i):
+        runner()
+
+    # e2e: this rank's A rows from pinned host memory, B panels from rank 0's pinned
+    # host memory (copied in on the communication stream just before each panel's
+    # broadcast), C blocks back to pinned host memory
+    a_pin = torch.from_numpy(np.ascontiguousarray(host_a[r0:r1])).pin_memory()
+    b_pin = [p.pin_memory() for p in Q.shard.split_panels(torch.from_numpy(host_b), P)] if rank == 0 else None
+    c_pin = [torch.empty(cp.shape, dtype=torch.uint8).pin_memory() for cp in c_panels]
+    a_dev = torch.empty_like(a)
+    e_b = [torch.empty_like(bp) for bp in b_panels]
+    e_c = [torch.empty_like(cp) for cp in c_panels]
+
+    def stage(j):
+        e_b[j].copy_(b_pin[j], non_blocking=True)
+
+    e_runner = Q.shard.RowBlockStep(a_dev, e_b, e_c, compute, stage=stage if rank == 0 else None)
+
+    def e2e(i):
+        a_dev.copy_(a_pin, non_blocking=True)
+        e_runner()
+        for cp, hp in zip(e_c, c_pin):
+            hp.copy_(cp, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    units = rows * kd * n
+    # whole-job bytes: every rank's A rows + B once (rank 0) in, all of C out
+    h2d = host_a[:].nbytes + host_b.nbytes if cfg != 4 else 2 * host_a.nbytes
+    d2h = m * n * (c.k if cfg != 4 else 1)
+    if cfg == 4:
+        w = W.work_units(c)
+        meta["work"] = {k: v // ws for k, v in w.items() if isinstance(v, int)}
+        meta["work"]["i8_macs"] = meta["work"]["kara_macs"] = rows * n * kd
+    else:
+        meta["work"] = W.work_units(c, (rows, kd, n))
+    meta["broadcast_bytes_per_step"] = runner.bytes_broadcast()
+    meta["variant_step"] = None
+    return step, e2e, units, (h2d, d2h), meta
+
+
+def build_step(cfg, engine, rank, ws, torch, dist, Q, W, args):
     """Returns (step(i), e2e_step(i) or None, units/step/rank, meta)."""
     c = W.CONFIGS[cfg]
     dev = torch.device("cuda", torch.cuda.current_device())
-    meta = {"config": {"workload": c.label}}
+    meta = {"config": config_dict(cfg, engine, ws, args.partition, args.panels)}
+    if cfg in (3, 4, 5) and ws > 1 and args.partition == "rows":
+        return build_rowblock_step(cfg, engine, rank, ws, torch, Q, W, args, meta)
     if cfg in (3, 5):
         f = W.field_for(c)
         m, kd, n = c.shape
-        # rank's block of C on the grid2d(ws) grid; B reaches every rank by ONE NCCL
-        # broadcast here at set-up (outside the timed region), then each rank keeps
-        # its column block: no collective inside a step
+        # single GPU, or the 2-D grid option: rank's block of C on grid2d(ws); B
+        # reaches every rank by ONE NCCL broadcast here at set-up (outside the
+        # timed region), then each rank keeps its column block
         r0, r1, c0, c1 = Q.shard.block2d(m, n, ws, rank)
         rows, cols = r1 - r0, c1 - c0
         host = W.make_inputs(c)
@@ -166,10 +282,8 @@ def build_step(cfg, engine, rank, ws, torch, dist, Q, W):
         e2e_bytes = (a_h.nbytes + b_h.nbytes, rows * cols * c.k)
         units = rows * kd * cols
         R, C = Q.shard.grid2d(ws)
-        meta["config"].update({"M": m, "N": n, "K": kd, "k": c.k, "p": c.p, "fold_every": c.dot_bound,
-                               "engine": engine, "l2": "inputs 2x%d MiB > 126 MB L2" % (host["b"].nbytes >> 20),
-                               "parallelism": f"grid{R}x{C} (C blocks; B broadcast once at set-up)" if ws > 1
-                               else "single"})
+        meta["config"]["parallelism"] = f"grid{R}x{C} (C blocks; B broadcast once at set-up)" if ws > 1 \
+            else "single"
         meta["work"] = W.work_units(c, (rows, kd, cols))
         meta["variant_step"] = lambda eng: (lambda i: f.matmul_coeffs(a, b, engine=eng, out=out))
         return step, e2e, units, e2e_bytes, meta
@@ -211,10 +325,8 @@ def build_step(cfg, engine, rank, ws, torch, dist, Q, W):
 
         units = rows * n * cols
         R, C = Q.shard.grid2d(ws)
-        meta["config"].update({"n": n, "p": 3, "t": prm.t, "entries_per_word": prm.k, "engine": engine,
-                               "density": 0.5, "l2": "A 256 MiB > 126 MB L2",
-                               "parallelism": f"grid{R}x{C} (C blocks; A broadcast once at set-up)" if ws > 1
-                               else "single"})
+        meta["config"]["parallelism"] = f"grid{R}x{C} (C blocks; A broadcast once at set-up)" if ws > 1 \
+            else "single"
         w = W.work_units(c)
         meta["work"] = {k: v // ws for k, v in w.items() if isinstance(v, int)}
         meta["work"]["i8_macs"] = rows * n * cols
@@ -277,9 +389,7 @@ def build_step(cfg, engine, rank, ws, torch, dist, Q, W):
         units = shard[0] * shard[1]
         io = (host["v1"].nbytes * 2, o_pin.numel())
     per_set = sum(v.numel() for v in bufs[0].values())
-    meta["config"].update({"shape": list(c.shape), "p": c.p, "k": c.k, "engine": "fused",
-                           "l2": f"rotating {sets} input sets x {per_set >> 20} MiB > 126 MB L2",
-                           "parallelism": f"batch{ws}" if ws > 1 else "single"})
+    meta["config"]["l2"] = f"rotating {sets} input sets x {per_set >> 20} MiB > 126 MB L2"
     meta["work"] = W.work_units(c, shard)
     return step, e2e, units, io, meta
 
@@ -517,6 +627,68 @@ def measure_variants(args, cfg, engine, meta, units, work, peaks, peak_src, torc
     return out
 
 
+def sustained_and_burst(step, args, ms_main, torch, graphed, cfg):
+    """The headline pass is either a short burst or a long sustained run; time
+    the other one too (the board's power management lowers clocks over a long
+    run): 20-step burst and >= 200-step / >= 0.2 s sustained, both CUDA-event
+    timed on the same inputs."""
+    if graphed:
+        return None  # cfg1/cfg2: graph-replayed microsecond kernels, no clock drift to speak of
+    want = [("burst", 20), ("sustained", max(200, int(0.2 / max(ms_main / 1e3, 1e-6))))]
+    out = {"headline_steps": args.steps}
+    for name, k in want:
+        if (name == "burst" and args.steps <= 20) or (name == "sustained" and args.steps >= 200):
+            out[name] = {"steps": args.steps, "ms_per_step": round(ms_main, 5), "source": "headline pass"}
+            continue
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(k):
+            step(i)
+        e1.record()
+        torch.cuda.synchronize()
+        out[name] = {"steps": k, "ms_per_step": round(e0.elapsed_time(e1) / k, 5)}
+    return out
+
+
+def redq_line(args, torch, N):
+    """The standalone REDQ kernel (reduce_words_digits of cfg3's 2^26
+    accumulators, the `--config redq` line) measured in the same run, so the
+    default output carries a REDQ-vs-HBM roofline for work that really is REDQ."""
+    prm = PRIMS["redq"]
+    n, p, t, d = prm["n"], prm["p"], prm["t"], prm["d"]
+    g = np.random.default_rng(7)
+    host = sum(g.integers(0, 1 << t, n, dtype=np.uint64) << np.uint64(i * t) for i in range(d + 1))
+    sets = [torch.from_numpy(host.view(np.int64)).cuda() for _ in range(2)]
+    outs = [torch.empty((n, d + 1), dtype=torch.int64, device="cuda") for _ in sets]
+    L = N.lib()
+
+    def st(i):
+        N.check(L.qadic_reduce_words(N.ptr(sets[i % 2]), n, p, t, d, 0, N.ptr(outs[i % 2]), N.stream_ptr()))
+
+    for i in range(3):
+        st(i)
+    torch.cuda.synchronize()
+    k = 50
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(k):
+        st(i)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / k
+    byts = 8 * n + 8 * n * (d + 1)
+    peaks, src = load_peaks()
+    gbs = byts / (ms / 1e3) / 1e9
+    del sets, outs
+    return {"workload": f"reduce_words_digits n=2^26 p={p} q=2^{t} d={d} (cfg3 accumulators)",
+            "redq_coeffs_per_s": n * (d + 1) / (ms / 1e3), "words_per_s": n / (ms / 1e3), "ms": round(ms, 4),
+            "steps": k, "roofline": {"bound": "hbm", "kernel": "reduce_words", "achieved": round(gbs, 1),
+                                     "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                                     "frac": round(gbs / peaks["hbm_gbs"], 4),
+                                     "algorithmic_bytes_per_launch": byts}}
+
+
 def run_ours(args):
     import torch
 
@@ -535,7 +707,7 @@ def run_ours(args):
     N.load_library()
     cfg = args.config
     engine = args.engine
-    step, e2e, units, io, meta = build_step(cfg, engine, rank, ws, torch, dist, Q, W)
+    step, e2e, units, io, meta = build_step(cfg, engine, rank, ws, torch, dist, Q, W, args)
     peaks, peak_src = load_peaks()
     if cfg in (3, 4, 5) and engine == "i8":  # context for the i8 roofline only
         peaks["int8_tops"] = measure_int8_peak(torch)
@@ -655,14 +827,25 @@ def run_ours(args):
         "dtype": dtype_label(cfg, engine, kname),
         "data": "synthetic (seeded Philox, BASELINE.json config shapes)",
         "config": meta["config"],
-        "redq_coeffs_per_s": work["redq_coeffs"] * ws / (ms / 1e3),
         "roofline": roof,
         "e2e": {"value": total_units / e2e_s, "unit": unit, "h2d_bytes_per_step": int(io[0]),
                 "d2h_bytes_per_step": int(io[1]), "ms_per_step": e2e_s * 1e3},
         "gpu_launches": int(launches),
         "clocks": clocks,
     }
-    if ws == 1 and cfg in (3, 4, 5) and not args.no_variants and "variant_step" in meta:
+    # REDQ throughput only where the timed kernels run REDQ: the batched kernels
+    # (cfg1/cfg2) and the F64 engine's epilogue; the tensor-core engines reduce
+    # mod p directly.  The standalone REDQ kernel has its own line below.
+    if cfg in (1, 2) or engine == "f64":
+        line["redq_coeffs_per_s"] = work["redq_coeffs"] * ws / (ms / 1e3)
+    if meta.get("broadcast_bytes_per_step"):
+        line["broadcast"] = {"bytes_per_step": int(meta["broadcast_bytes_per_step"]), "panels": args.panels,
+                             "inside_timed_step": True, "collective": "ncclBroadcast (torch.distributed)"}
+    if ws == 1 and not args.no_sustained:
+        line["sustained_vs_burst"] = sustained_and_burst(step, args, ms, torch, graph is not None, cfg)
+    if ws == 1 and not args.no_redq_line and cfg in (3, 4, 5):
+        line["redq"] = redq_line(args, torch, N)
+    if ws == 1 and cfg in (3, 4, 5) and not args.no_variants and meta.get("variant_step"):
         line["variants"] = measure_variants(args, cfg, engine, meta, units, work, peaks, peak_src, torch, N, W)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_leg(cfg, args)
@@ -862,11 +1045,46 @@ def run_reference(args):
             "ms_per_step": tot_s / args.steps * 1e3, "higher_is_better": True,
             "scaling": "strong" if cfg in (3, 4, 5) else "weak", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (seeded Philox, BASELINE.json config shapes)",
-            "config": {"workload": c.label},
+            "config": config_dict(cfg, args.engine, ws, args.partition, args.panels),
             "cpu_baseline": {"value": value, "unit": unit, "cores": workers, "kind": kind, "sample": sample},
             "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
     print(json.dumps(line), flush=True)
+
+
+def ensure_world(args):
+    """`--gpus N` must run N ranks: under torchrun WORLD_SIZE has to equal N;
+    without it (N > 1) this process re-launches itself under
+    torch.distributed.run (one rank per GPU, rendezvous on 127.0.0.1).  Never
+    silently measures fewer GPUs than asked."""
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is not None:
+        if int(ws_env) != args.gpus and not (args.gpus == 1 and int(ws_env) > 1):
+            sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws_env}")
+        if args.gpus == 1 and int(ws_env) > 1:
+            args.gpus = int(ws_env)
+        return
+    if args.gpus <= 1:
+        return
+    if args.impl == "ours":
+        try:
+            import torch
+
+            have = torch.cuda.device_count()
+        except Exception:  # pragma: no cover
+            have = 0
+        if have < args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} requested but only {have} CUDA device(s) are visible")
+    import socket
+
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
 
 
 def main():
@@ -884,7 +1102,17 @@ def main():
     ap.add_argument("--no-variants", action="store_true",
                     help="skip the other exact GEMM engines (i8k, i8, f64) measured after the headline")
     ap.add_argument("--no-graph", action="store_true", help="eager launches for cfg1/cfg2")
+    ap.add_argument("--partition", default="rows", choices=["rows", "grid"],
+                    help="N > 1 matmul sharding: A row blocks with B broadcast inside every step (default), or "
+                         "the 2-D grid with B broadcast once at set-up")
+    ap.add_argument("--panels", type=int, default=None,
+                    help="B column panels per step for the row-block partition (default 4 when N > 1)")
+    ap.add_argument("--no-sustained", action="store_true", help="skip the burst / sustained companion timing")
+    ap.add_argument("--no-redq-line", action="store_true", help="skip the standalone REDQ kernel measurement")
     args = ap.parse_args()
+    ensure_world(args)
+    if args.panels is None:
+        args.panels = 4 if int(os.environ.get("WORLD_SIZE", "1")) > 1 else 1
     args.warmup = max(3, args.warmup) if args.impl == "ours" else args.warmup
     if args.config in PRIMS:
         if args.impl == "reference":

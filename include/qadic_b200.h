@@ -206,6 +206,12 @@ QADIC_API int qadic_fdiv_scan(int32_t beta, int32_t mode1, int32_t mode2, int32_
  * reciprocal mode fdiv._PAIRED_MODE1 gives): y -= (r >= bound[mode2] && p*y > r),
  * counts y != r // p over all (r, p, mode2). */
 QADIC_API int qadic_fdiv_applied_scan(int32_t beta, const int64_t bound[3], uint64_t *mismatches, void *stream);
+/* Native binary64 applied division on sampled pairs (fdiv.native_applied_random,
+ * reference src/fdiv.py:464-488): r[j*per_p + i] against divisor p[j] with
+ * invp[j] = RU(1/p[j]); y = floor(RN(r*invp)) - (r > threshold && p*y > r);
+ * counts y != r // p.  Device pointers; synchronous (returns the count). */
+QADIC_API int qadic_fdiv_native_check(const int64_t *r, int64_t per_p, const int64_t *p, const double *invp,
+                                      int64_t n_p, int64_t threshold, uint64_t *mismatches, void *stream);
 
 /* ---------------------------------------------------------------------------
  * Diagnostics: measured pipe peaks (no reference

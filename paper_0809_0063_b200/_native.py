@@ -85,6 +85,7 @@ _SIGNATURES = {
     "qadic_index_of_coeffs": ([P, I64, I32, I32, P, P, P], ctypes.c_int),
     "qadic_fdiv_scan": ([I32, I32, I32, I32, I32, I64, ctypes.POINTER(FdivScanReport), P], ctypes.c_int),
     "qadic_fdiv_applied_scan": ([I32, ctypes.POINTER(I64 * 3), ctypes.POINTER(ctypes.c_uint64), P], ctypes.c_int),
+    "qadic_fdiv_native_check": ([P, I64, P, P, I64, I64, ctypes.POINTER(ctypes.c_uint64), P], ctypes.c_int),
     "qadic_diag_pipe_peak": ([I32, I32, I64, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_float), P],
                              ctypes.c_int),
 }
@@ -241,25 +242,41 @@ def host_operand(x, np_dtype):
 
 def out_buffer(out, shape, np_dtype):
     """Device buffer the kernel writes: `out` itself when it is a matching
-    CUDA tensor, else a fresh device tensor (copied into a host `out` by
-    finish())."""
-    if out is not None and is_tensor(out) and out.is_cuda:
-        if tuple(out.shape) != tuple(int(s) for s in shape) or not out.is_contiguous():
-            raise ValueError(f"out must be a contiguous tensor of shape {tuple(shape)}")
-        return out
+    CUDA tensor, else a fresh device tensor that finish() copies into the
+    caller's host `out` (a CPU tensor or a numpy array)."""
+    shape = tuple(int(s) for s in shape)
+    if out is not None:
+        if is_tensor(out):
+            if tuple(out.shape) != shape or not out.is_contiguous():
+                raise ValueError(f"out must be a contiguous tensor of shape {shape}")
+            if out.is_cuda:
+                return out
+        elif isinstance(out, np.ndarray):
+            if out.shape != shape or not out.flags.c_contiguous or not out.flags.writeable:
+                raise ValueError(f"out must be a writeable C-contiguous array of shape {shape}")
+            if out.dtype != np.dtype(np_dtype):
+                raise ValueError(f"out must have dtype {np.dtype(np_dtype)}")
+        else:
+            raise TypeError("out must be a torch tensor or a numpy array")
     return empty(shape, np_dtype)
 
 
 def finish(dev, out, host: bool, np_dtype):
-    """Return convention of every array API: a host `out` tensor is filled
-    (non-blocking D2H from pinned memory when possible), host inputs give a
-    numpy result, device inputs a device tensor."""
-    if out is not None and is_tensor(out) and not out.is_cuda:
-        out.copy_(dev.view(out.dtype) if dev.dtype != out.dtype else dev, non_blocking=out.is_pinned())
+    """Return convention of every array API: a host `out` (CPU tensor or numpy
+    array) is filled and complete on return, host inputs give a numpy result,
+    device inputs a device tensor."""
+    if out is None:
+        return to_host(dev, np_dtype) if host else dev
+    if is_tensor(out) and out.is_cuda:
         return out
-    if out is not None:
+    if is_tensor(out):
+        src = dev.view(out.dtype) if dev.dtype != out.dtype else dev
+        out.copy_(src, non_blocking=out.is_pinned())
+        if out.is_pinned():  # the copy is queued on the current stream: complete it
+            torch().cuda.current_stream().synchronize()
         return out
-    return to_host(dev, np_dtype) if host else dev
+    np.copyto(out, to_host(dev, np_dtype))
+    return out
 
 
 def ptr(x) -> int:
@@ -270,13 +287,17 @@ _workspace = {}
 
 
 def workspace(nbytes: int):
-    """Device scratch buffer, grown on demand and reused across calls
-    (stream-ordered like every other launch of this package)."""
+    """Device scratch buffer, grown on demand and reused across calls on the
+    same (device, stream): every launch of this package is ordered on the
+    current stream, so two streams (or two threads on their own streams) never
+    share one.  A buffer that is replaced is released through the caching
+    allocator, which orders its reuse after the work queued on its stream."""
     t = require_cuda()
     dev = t.cuda.current_device()
-    buf = _workspace.get(dev)
+    key = (dev, t.cuda.current_stream().cuda_stream)
+    buf = _workspace.get(key)
     if buf is None or buf.numel() < nbytes:
-        _workspace[dev] = buf = t.empty(max(int(nbytes), 1), dtype=t.uint8, device=device())
+        _workspace[key] = buf = t.empty(max(int(nbytes), 1), dtype=t.uint8, device=device())
     return buf
 
 

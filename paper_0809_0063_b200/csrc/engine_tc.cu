@@ -33,6 +33,8 @@
 #include <cuda.h>
 #include <stdio.h>
 
+#include <algorithm>
+#include <atomic>
 #include <utility>
 
 #include "qadic_common.cuh"
@@ -2421,19 +2423,27 @@ int tc_matmul_u64(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_t m, 
                   cudaStream_t s) {
     using namespace tc;
     constexpr int64_t KC = 16384;  // 4 * KC * 255^2 < 2^32
-    static bool pool_kept = false;  // keep freed blocks in the stream-ordered pool across calls
-    static unsigned long long* host_or = nullptr;
-    if (!pool_kept) {
-        int dev = 0;
-        cudaGetDevice(&dev);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    // keep freed blocks in the stream-ordered pool across calls (once per device)
+    static std::atomic<bool> pool_kept[64];
+    if (!pool_kept[dev & 63].exchange(true)) {
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
             uint64_t keep = ~0ull;
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
         }
-        cudaHostAlloc(reinterpret_cast<void**>(&host_or), 2 * sizeof(unsigned long long), cudaHostAllocDefault);
         cudaGetLastError();
-        pool_kept = true;
+    }
+    // pinned landing slot for the operands' OR: one per host thread and device, so
+    // concurrent callers never read each other's significant-byte counts
+    thread_local unsigned long long* host_or_slot[64] = {};
+    unsigned long long*& host_or = host_or_slot[dev & 63];
+    if (!host_or) {
+        if (cudaHostAlloc(reinterpret_cast<void**>(&host_or), 2 * sizeof(unsigned long long), cudaHostAllocDefault) !=
+            cudaSuccess)
+            host_or = nullptr;
+        cudaGetLastError();
     }
     // significant bytes of each operand: only byte planes that can be nonzero are multiplied
     // (packed words of the reference's drivers have 5 -- 34 bits at cfg3 -- instead of 8)
@@ -2539,14 +2549,28 @@ int tc_matmul_u64(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_t m, 
     return rc;
 }
 
+// Largest |integer value| of the centred representative e2m1_lut() builds when the
+// non-negative set is out of range: v = r for 2r <= p-1, else r - p.  That is p/2
+// (not (p-1)/2): for p = 2 residue 1 is stored as -1.  The non-negative set is
+// bounded inside e2m1_lut itself (it falls back to this one when K*max^2 >= 2^24).
+static int64_t e2m1_max_abs(uint32_t p) {
+    int64_t h = 0;
+    for (uint32_t r = 0; r < p; ++r) {
+        const int64_t v = (2 * r <= p - 1) ? (int64_t)r : (int64_t)r - (int64_t)p;
+        h = std::max<int64_t>(h, v < 0 ? -v : v);
+    }
+    return h;
+}
+
 // planes of the decomposition plan_planes() picks (Toom-Cook when 2k-1 <= p+1)
 static int kara_planes(uint32_t p, int k) { return (2 * k - 1 <= (int)p + 1) ? 2 * k - 1 : k * (k + 1) / 2; }
 
 bool tc_kara_ok(uint32_t p, int64_t kdim, int k) {
     int ncodes = 1;
     for (int i = 0; i < k; ++i) ncodes *= (int)p;
+    const int64_t h = e2m1_max_abs(p);
     return p <= 7 && kara_planes(p, k) <= tc::KMAX_S && ncodes <= tc::PT_CODES &&
-           (__int128)kdim * ((p - 1) / 2) * ((p - 1) / 2) < ((__int128)1 << 24);
+           (__int128)kdim * h * h < ((__int128)1 << 24);
 }
 
 size_t tc_kara_workspace(uint32_t p, int64_t m, int64_t kdim, int64_t n, int k) {
@@ -2557,7 +2581,7 @@ size_t tc_kara_workspace(uint32_t p, int64_t m, int64_t kdim, int64_t n, int k) 
 int tc_kara_gf_matmul(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
                       void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s, bool b_ready) {
     QADIC_REQUIRE(tc_kara_ok(f.p, kdim, (int)f.k), QADIC_ERR_PARAMS,
-                  "fp4k engine needs p <= 7, K*((p-1)/2)^2 < 2^24 and at most %d planes", tc::KMAX_S);
+                  "fp4k engine needs p <= 7, K*h^2 < 2^24 (h = max |centred residue|) and at most %d planes", tc::KMAX_S);
     return tc::run_kara(f, a, b, m, kdim, n, ws, ws_bytes, c, s, b_ready);
 }
 
@@ -2611,10 +2635,10 @@ size_t tc_workspace(int kind, int64_t m, int64_t kdim, int64_t n, int k) {
     return (size_t)tc::round_up(n * k * ld, 1024) + (size_t)tc::round_up(m * ld, 1024);
 }
 
-// largest |centred residue| = (p-1)/2; F4 needs p <= 7 and an fp32-exact sum
+// F4 needs p <= 7 and an fp32-exact sum of K*k products of the centred representatives
 bool tc_f4_ok(uint32_t p, int64_t kdim, int k) {
     if (p > 7) return false;
-    const int64_t h = (p - 1) / 2;
+    const int64_t h = e2m1_max_abs(p);
     return (__int128)kdim * k * h * h < ((__int128)1 << 24);
 }
 
@@ -2625,7 +2649,7 @@ int tc_gf_matmul(int kind, const FieldConst& f, const uint8_t* a, const uint8_t*
                       "inner dimension %lld overflows the int32 plane accumulator", (long long)kdim);
     } else {
         QADIC_REQUIRE(tc_f4_ok(f.p, kdim, (int)f.k), QADIC_ERR_PARAMS,
-                      "fp4 engine needs p <= 7 and K*k*((p-1)/2)^2 < 2^24");
+                      "fp4 engine needs p <= 7 and K*k*h^2 < 2^24 (h = max |centred residue|)");
     }
     return tc::run(kind, f, a, b, m, kdim, n, ws, ws_bytes, c, s);
 }

@@ -22,6 +22,8 @@
 // where floor(x) is 0 (p >= 2) or exact (p = 1, even mantissa) either way.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "qadic_common.cuh"
 #include "qadic_internal.h"
 
@@ -163,6 +165,26 @@ __global__ void __launch_bounds__(SCAN_THREADS) fdiv_applied_kernel(int beta, lo
 
 constexpr int64_t MAX_CTAS_PER_LAUNCH = 1 << 22;
 
+// Native (IEEE binary64) applied division on sampled pairs (fdiv.native_applied_random,
+// reference fdiv.py:464-488): y = floor(RN(r * RU(1/p))), one multiply-back decrement
+// above the case-2 threshold, compared with the exact 64-bit r // p.  Block j of
+// the grid-stride loop owns divisor j / per_p's numerators r[j*per_p ...].
+__global__ void fdiv_native_kernel(const int64_t* __restrict__ r, int64_t per_p, const int64_t* __restrict__ p,
+                                   const double* __restrict__ invp, int64_t n_p, long long thr,
+                                   unsigned long long* mism) {
+    unsigned long long bad = 0;
+    const int64_t total = per_p * n_p;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = i / per_p;
+        const int64_t pj = p[j], ri = r[i];
+        int64_t y = (int64_t)floor(__dmul_rn((double)ri, invp[j]));
+        y -= (ri > thr) && (pj * y > ri);
+        bad += y != ri / pj;
+    }
+    const unsigned long long sum = warp_sum(bad);
+    if (threadIdx.x % 32 == 0 && sum) atomicAdd(mism, sum);
+}
+
 }  // namespace
 
 }  // namespace qadic
@@ -225,6 +247,31 @@ int qadic_fdiv_applied_scan(int32_t beta, const int64_t bound[3], uint64_t* mism
     int rc = check_launch("fdiv_applied_scan", (int)((np + MAX_CTAS_PER_LAUNCH - 1) / MAX_CTAS_PER_LAUNCH));
     if (rc) return rc;
     QADIC_REQUIRE(cudaStreamSynchronize(s) == cudaSuccess, QADIC_ERR_CUDA, "fdiv_applied_scan: %s",
+                  cudaGetErrorString(cudaGetLastError()));
+    *mismatches = res;
+    return QADIC_OK;
+}
+
+int qadic_fdiv_native_check(const int64_t* r, int64_t per_p, const int64_t* p, const double* invp, int64_t n_p,
+                            int64_t threshold, uint64_t* mismatches, void* stream) {
+    QADIC_REQUIRE(per_p >= 0 && n_p >= 0 && mismatches != nullptr, QADIC_ERR_VALUE, "bad arguments");
+    *mismatches = 0;
+    if (per_p == 0 || n_p == 0) return QADIC_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned long long* acc = nullptr;
+    unsigned long long res = 0;
+    QADIC_REQUIRE(cudaMallocAsync(reinterpret_cast<void**>(&acc), sizeof(*acc), s) == cudaSuccess, QADIC_ERR_CUDA,
+                  "scratch allocation failed");
+    cudaMemsetAsync(acc, 0, sizeof(*acc), s);
+    const int64_t total = per_p * n_p;
+    const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)num_sms_cached() * 8);
+    QADIC_TIMED("fdiv_native", s,
+                fdiv_native_kernel<<<(unsigned)blocks, 256, 0, s>>>(r, per_p, p, invp, n_p, (long long)threshold, acc));
+    cudaMemcpyAsync(&res, acc, sizeof(res), cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(acc, s);
+    int rc = check_launch("fdiv_native_check", 0);
+    if (rc) return rc;
+    QADIC_REQUIRE(cudaStreamSynchronize(s) == cudaSuccess, QADIC_ERR_CUDA, "fdiv_native_check: %s",
                   cudaGetErrorString(cudaGetLastError()));
     *mismatches = res;
     return QADIC_OK;

@@ -24,6 +24,8 @@ from dataclasses import dataclass, field
 from fractions import Fraction
 from typing import Optional
 
+import numpy as np
+
 NATIVE_BETA = 53
 
 
@@ -316,3 +318,43 @@ def applied_fdiv_exhaustive(beta: int, extended: bool = False) -> int:
     out = ctypes.c_uint64(0)
     N.check(N.lib().qadic_fdiv_applied_scan(beta, ctypes.byref(bounds), ctypes.byref(out), N.stream_ptr()))
     return int(out.value)
+
+
+# ---------------------------------------------------------------------------
+# sampled self-checks (reference fdiv.py:464-505)
+# ---------------------------------------------------------------------------
+def native_applied_random(n_samples: int, seed: int = 0) -> int:
+    """Mismatches of the native applied division (RU reciprocal, RN multiply,
+    one decrement above the case-2 threshold) against r // p on random 53-bit
+    pairs -- up to 10^4 random divisors with the numerators split evenly, drawn
+    from Philox(seed) in the reference's order.  The check runs as one CUDA
+    launch over all pairs (qadic_fdiv_native_check)."""
+    from . import _native as N
+
+    rng = np.random.Generator(np.random.Philox(seed))
+    n_p = max(1, min(10_000, n_samples // 1000))
+    per_p = -(-n_samples // n_p)
+    ps = rng.integers(1, 1 << 53, size=n_p, dtype=np.int64)
+    # the reference draws each divisor's numerators after that divisor, stopping
+    # once n_samples pairs are covered
+    used = min(n_p, -(-n_samples // per_p))
+    rs = np.concatenate([rng.integers(0, 1 << 53, size=per_p, dtype=np.int64) for _ in range(used)])
+    ps = ps[:used]
+    invp = np.array([native_reciprocal(int(p), UP) for p in ps], dtype=np.float64)
+    thr = case_spec(UP, NEAREST, NATIVE_BETA).bound_threshold()
+    torch = N.require_cuda()
+    dr, dp, di = (torch.from_numpy(x).to(N.device()) for x in (rs, ps, invp))
+    out = ctypes.c_uint64(0)
+    N.check(N.lib().qadic_fdiv_native_check(N.ptr(dr), per_p, N.ptr(dp), N.ptr(di), used, thr, ctypes.byref(out),
+                                            N.stream_ptr()))
+    return int(out.value)
+
+
+def sim_native_agreement(n_samples: int, seed: int = 0) -> int:
+    """Mismatches between the beta = 53 nearest-mode simulator (sim_div) and a
+    native double division on random pairs -- the simulator's self-check
+    (host control plane: exact rationals, no device work)."""
+    rng = np.random.Generator(np.random.Philox(seed))
+    rs = rng.integers(0, 1 << 53, size=n_samples, dtype=np.int64).tolist()
+    ps = rng.integers(1, 1 << 53, size=n_samples, dtype=np.int64).tolist()
+    return sum(1 for r, p in zip(rs, ps) if r / p != float(sim_div(r, p, NEAREST, NATIVE_BETA)))

@@ -207,3 +207,7 @@ def chunk_budget(params: PackingParams, ma: int, mb: int) -> int:
     """Products accumulable on one word whose carry digits are already < p,
     with operand digits bounded by ma and mb (reference polymul.py:159-167)."""
     return (params.q - 1 - (params.p - 1)) // (params.k * ma * mb)
+
+
+# analytic cost models (host bookkeeping; reference params.py:291-501)
+from .costs import CostReport, ConversionCost, cmm_cost, conversion_cost, polymul_cost  # noqa: E402,F401

@@ -1,21 +1,26 @@
 """Data-parallel sharding of the hot path across GPUs (one process per GPU).
 
-Only where the path shards naturally:
-* matmul (cfg3/4/5): C is split into an R x Cc grid of blocks (`grid2d`):
-  rank (i, j) computes C[rows_i, cols_j] = A[rows_i] B[:, cols_j] with no
-  collective in the step.  B reaches the ranks by ONE broadcast over NCCL
-  (NVLink/NVSwitch) at set-up, after which each rank keeps its column block.
-  The grid (rather than row blocks only) splits the per-call operand
-  conversion of B as well as A's: with row blocks every rank would re-convert
-  all of B (the evaluation planes), which caps 8-GPU efficiency near 60%;
-  a 2 x 4 grid leaves A/2 + B/4 per rank.  R = 1 gives plain row blocks of C^T
-  (column blocks), Cc = 1 plain row blocks.
+Only where the path shards naturally (the sharded operation is
+GFqField.matmul / right_cmm, reference src/gfext.py:311-345, src/cmm.py:244-276):
+
+* matmul (cfg3/4/5), the default partition (`RowBlockStep`): rank r owns the
+  row block A[rows_r] (resident) and computes C[rows_r] = A[rows_r] B.  B lives
+  on the source rank in column-panel-major order and is broadcast over NCCL
+  (NVLink / NVSwitch) INSIDE every step, one column panel at a time on a
+  communication stream; the product of panel j starts on the compute stream as
+  soon as panel j has landed, so the broadcast of panel j+1 overlaps the
+  product of panel j.  No reduction collective: each rank's C rows are final.
+  C is kept per panel ([rows, N_j, k] blocks).
+* the 2-D grid option (`grid2d` / `block2d`): rank (i, j) computes
+  C[rows_i, cols_j] with A[rows_i] and B[:, cols_j] resident after ONE
+  broadcast at set-up -- no collective in a step.  It splits the per-step
+  operand conversion of B as well as A's (with row blocks every rank converts
+  all of B), at the price of B never moving inside the step.
 * batched polymul / dots (cfg1/cfg2): the batch is split, no collective.
 
 The compute callable is the CUDA engine in production (bench.py) and may be
-any function of (a_rows, b) -- the multi-process CPU tests drive this module
-over gloo with the CPU oracle as the compute to check the partitioning and
-the broadcast.
+any function (a_rows, b_panel, out) -- the multi-process CPU tests drive the
+same step over gloo with the CPU oracle as the compute.
 """
 
 from __future__ import annotations
@@ -111,3 +116,95 @@ def gather_rows(c_rows, group=None):
     parts = [torch.empty_like(c_rows) for _ in range(dist.get_world_size(group))]
     dist.all_gather(parts, c_rows, group=group)
     return torch.cat(parts, dim=0)
+
+
+def panel_bounds(n: int, panels: int):
+    """[(j0, j1)] of `panels` near-equal column panels of an n-column operand."""
+    panels = max(1, min(panels, n)) if n else 1
+    return [row_block(n, panels, j) for j in range(panels)]
+
+
+def split_panels(b, panels: int):
+    """Column panels of B [K, N, ...] as contiguous copies (the source rank's
+    panel-major layout; works for numpy arrays and torch tensors)."""
+    bounds = panel_bounds(b.shape[1], panels)
+    if hasattr(b, "contiguous"):
+        return [b[:, j0:j1].contiguous() for j0, j1 in bounds]
+    import numpy as np
+
+    return [np.ascontiguousarray(b[:, j0:j1]) for j0, j1 in bounds]
+
+
+class RowBlockStep:
+    """One step of the row-block sharded product C[rows_r] = A[rows_r] @ B.
+
+    b_panels: B's column panels, allocated on every rank and filled on `src`
+    (the other ranks' contents are overwritten by the broadcast every step).
+    c_panels: this rank's output blocks, c_panels[j] = A[rows_r] @ b_panels[j].
+    compute(a_rows, b_panel, out): the local product (writes `out`).
+
+    On CUDA tensors the broadcasts run on a dedicated stream (NCCL async ops,
+    one event per panel) and the compute stream waits on each panel's event
+    only, so panel j+1 travels while panel j is multiplied.  On CPU tensors
+    (gloo) the same schedule runs synchronously.  `stage(j)` (optional) runs
+    on the source rank before panel j is sent -- the e2e step uses it to copy
+    the panel in from host memory."""
+
+    def __init__(self, a_rows, b_panels, c_panels, compute: Callable, src: int = 0, group=None,
+                 stage: Optional[Callable] = None):
+        if len(b_panels) != len(c_panels):
+            raise ValueError("one output block per B panel")
+        self.a_rows, self.b_panels, self.c_panels = a_rows, list(b_panels), list(c_panels)
+        self.compute, self.src, self.group, self.stage = compute, src, group, stage
+        dist = _dist()
+        self.world = dist.get_world_size(group) if dist is not None else 1
+        self.rank = dist.get_rank(group) if dist is not None else 0
+        self.cuda = getattr(a_rows, "is_cuda", False)
+        self.comm = None
+        if self.cuda:
+            import torch
+
+            self.comm = torch.cuda.Stream(device=a_rows.device)
+
+    def bytes_broadcast(self) -> int:
+        return sum(b.numel() * b.element_size() for b in self.b_panels) if self.world > 1 else 0
+
+    def __call__(self):
+        dist = _dist()
+        if not self.cuda:
+            for j, (bp, cp) in enumerate(zip(self.b_panels, self.c_panels)):
+                if self.stage is not None and self.rank == self.src:
+                    self.stage(j)
+                if dist is not None and self.world > 1:
+                    dist.broadcast(bp, src=self.src, group=self.group)
+                self.compute(self.a_rows, bp, cp)
+            return self.c_panels
+        import torch
+
+        cur = torch.cuda.current_stream()
+        self.comm.wait_stream(cur)  # the previous step's products no longer read the panel buffers
+        events = []
+        with torch.cuda.stream(self.comm):
+            for j, bp in enumerate(self.b_panels):
+                if self.stage is not None and self.rank == self.src:
+                    self.stage(j)
+                if dist is not None and self.world > 1:
+                    dist.broadcast(bp, src=self.src, group=self.group, async_op=True).wait()
+                ev = torch.cuda.Event()
+                ev.record(self.comm)
+                events.append(ev)
+        for ev, bp, cp in zip(events, self.b_panels, self.c_panels):
+            cur.wait_event(ev)
+            self.compute(self.a_rows, bp, cp)
+        return self.c_panels
+
+
+def assemble_panels(c_panels, axis: int = 1):
+    """Concatenate per-panel output blocks along the column axis."""
+    if hasattr(c_panels[0], "contiguous"):
+        import torch
+
+        return torch.cat(list(c_panels), dim=axis)
+    import numpy as np
+
+    return np.concatenate(list(c_panels), axis=axis)

@@ -11,6 +11,10 @@ if ROOT not in sys.path:
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 
+# tests/_ref_suite holds the reference's own test files (tools/ref_suite.py);
+# they run through tests/test_ref_suite.py in a child, never collected directly
+collect_ignore_glob = [] if os.environ.get("QADIC_REF_SUITE") == "1" else ["_ref_suite/*"]
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")

@@ -71,6 +71,47 @@ def _worker(rank, world, port, kind, result_q):
             blk = torch.from_numpy(O.right_cmm(a[r0:r1], np.ascontiguousarray(a[:, c0:c1]), 3, 17, 2))
             full = shard.gather_blocks(blk, n, n)
             ok = np.array_equal(full.numpy(), O.modmatmul_planes(a, a, 3))
+        elif kind == "rowpanel":  # the bench's default step: B panels broadcast inside the step
+            c = W.CONFIGS[5]
+            m, kd, n = 37, 50, 45
+            x = W.make_inputs(c, (m, kd, n))
+            f = O.build_field(7, 3, irreducible=[5, 0, 0, 1], max_dot_length=9)
+            r0, r1 = shard.row_block(m, world, rank)
+            bounds = shard.panel_bounds(n, 3)
+            if rank == 0:
+                b_panels = [torch.from_numpy(p) for p in shard.split_panels(x["b"], 3)]
+            else:
+                b_panels = [torch.zeros((kd, j1 - j0, 3), dtype=torch.uint8) for j0, j1 in bounds]
+            c_panels = [torch.zeros((r1 - r0, j1 - j0, 3), dtype=torch.uint8) for j0, j1 in bounds]
+
+            def compute(ar, bp, cp):
+                cp.copy_(torch.from_numpy(O.gf_matmul_folded(f, ar.numpy(), bp.numpy(), 9)))
+
+            stepper = shard.RowBlockStep(torch.from_numpy(x["a"][r0:r1]), b_panels, c_panels, compute)
+            ok = True
+            for _ in range(2):  # two steps: the second re-broadcasts into the same buffers
+                for bp in (b_panels if rank else []):
+                    bp.zero_()
+                stepper()
+                mine = shard.assemble_panels([cp.numpy() for cp in c_panels])
+                ok = ok and np.array_equal(mine, O.gf_matmul_planes(f, x["a"], x["b"])[r0:r1])
+            ok = ok and stepper.bytes_broadcast() == x["b"].nbytes
+        elif kind == "rowpanel_cmm":  # A^2 mod 3: rank 0 sends A's column panels as B
+            c = W.CONFIGS[4]
+            n = 40
+            a = W.make_inputs(c, (n,))["a"]
+            r0, r1 = shard.row_block(n, world, rank)
+            bounds = shard.panel_bounds(n, 4)
+            b_panels = [torch.from_numpy(p) for p in shard.split_panels(a, 4)] if rank == 0 else \
+                [torch.zeros((n, j1 - j0), dtype=torch.uint8) for j0, j1 in bounds]
+            c_panels = [torch.zeros((r1 - r0, j1 - j0), dtype=torch.uint8) for j0, j1 in bounds]
+
+            def compute(ar, bp, cp):
+                cp.copy_(torch.from_numpy(O.right_cmm(ar.numpy(), bp.numpy(), 3, 17, 2)))
+
+            shard.RowBlockStep(torch.from_numpy(a[r0:r1]), b_panels, c_panels, compute)()
+            rows = torch.from_numpy(shard.assemble_panels([cp.numpy() for cp in c_panels]))
+            ok = np.array_equal(rows.numpy(), O.modmatmul_planes(a, a, 3)[r0:r1])
         else:  # batch sharding, no collective
             c = W.CONFIGS[1]
             x = W.make_inputs(c, (1001,))
@@ -95,7 +136,7 @@ def _spawn(world, kind):
     return res
 
 
-@pytest.mark.parametrize("kind", ["gf", "cmm", "batch", "grid", "grid_cmm"])
+@pytest.mark.parametrize("kind", ["gf", "cmm", "batch", "grid", "grid_cmm", "rowpanel", "rowpanel_cmm"])
 def test_world2(kind):
     assert _spawn(2, kind) == {0: True, 1: True}
 
@@ -126,3 +167,33 @@ def test_row_block_partition():
             assert spans[0][0] == 0 and spans[-1][1] == n
             assert all(spans[i][1] == spans[i + 1][0] for i in range(w - 1))
             assert max(b - a for a, b in spans) - min(b - a for a, b in spans) <= 1
+
+
+@pytest.mark.parametrize("kind", ["rowpanel", "rowpanel_cmm"])
+def test_world4_rowpanel(kind):
+    """the bench's default multi-GPU step over four gloo ranks (ragged row blocks)."""
+    assert _spawn(4, kind) == {r: True for r in range(4)}
+
+
+def test_panel_bounds_and_split():
+    for n, p in ((8192, 4), (45, 3), (5, 8), (1, 4)):
+        b = shard.panel_bounds(n, p)
+        assert b[0][0] == 0 and b[-1][1] == n and len(b) == min(p, n)
+        arr = np.arange(7 * n).reshape(7, n)
+        assert np.array_equal(shard.assemble_panels(shard.split_panels(arr, p)), arr)
+
+
+def test_bench_gpus_flag_never_silently_single(tmp_path):
+    """`bench.py --gpus 2` on a box with fewer GPUs must fail loudly, not measure one."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode != 0 and "--gpus 2" in r.stderr
+    env["WORLD_SIZE"] = "4"
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "1"],
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode != 0 and "WORLD_SIZE=4" in r.stderr
