@@ -182,6 +182,73 @@ QADIC_API int qadic_index_of_coeffs(const uint8_t *c, int64_t n, int32_t k, int3
                           const int64_t *index_of_code, int64_t *out, void *stream);
 
 /* ---------------------------------------------------------------------------
+ * Long-polynomial products on packed words (csrc/polymul_long.cu):
+ * polymul.polymul_fqt / _wordconv_reduce / _kara_words (polymul.py:159-313) for a
+ * batch of pairs.  aw [batch][na], bw [batch][nb]: packed words (k = d+1 digits at
+ * radix 2^t, digits <= ma / mb); a REDQ fold every (2^t - 1 - (p-1)) / (k ma mb)
+ * inner terms, final REDQ, overlap-add mod p into out [batch][ncoef] (uint8 when
+ * out_u8, else int64).  algo 0 = classical, 1 = Karatsuba (breadth-first levels
+ * while n > threshold words).  stats (optional, host): the schedule's word
+ * products and reductions; flags bit 0 = a value beyond the top digit (validate),
+ * bit 1 = a nonzero coefficient at or beyond ncoef.  Synchronous.
+ * ------------------------------------------------------------------------- */
+typedef struct qadic_polymul_stats {
+    int64_t word_muls;
+    int64_t reductions;
+    int64_t leaves;
+    int32_t levels;
+    uint32_t flags;
+} qadic_polymul_stats;
+QADIC_API int qadic_polymul_words_batch(const uint64_t *aw, int64_t na, const uint64_t *bw, int64_t nb,
+                                        int64_t batch, int64_t p, int32_t t, int32_t d, int64_t ma, int64_t mb,
+                                        int32_t algo, int64_t threshold, int32_t validate, int32_t out_u8,
+                                        void *out, int64_t ncoef, qadic_polymul_stats *stats, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Any-field DQT word path (csrc/generic.cu): the reference's composition for the
+ * fields / primes outside the uint8 coefficient engines (p > 127, k > 4, wide
+ * L/H tables).  Handles are int64 (gfext.py:43-46), words uint64; the word
+ * product itself is qadic_matmul_exact_u64 (INT8 byte-plane tensor cores).
+ * ------------------------------------------------------------------------- */
+typedef struct qadic_gf_generic_desc {
+    int64_t p;                    /* prime < 2^26 */
+    int32_t k;                    /* extension degree, p^k <= 2^22 */
+    int32_t t;                    /* radix exponent: (2k-1) t <= 64 */
+    int32_t u_bits;               /* ceil(log2 p) bits per digit of the L/H index (gfext.py:178) */
+    int32_t reserved;
+    const int32_t *l_code;        /* device: code_of_index[l_table], 2^(u_bits k) entries */
+    const int32_t *h_code;        /* device: code_of_index[h_table] */
+    const int64_t *index_of_code; /* device: p^k entries */
+} qadic_gf_generic_desc;
+
+/* out[i] = table[idx[i]]  (pack_table gather, gfext.py:329-330) */
+QADIC_API int qadic_gather_u64(const int64_t *idx, int64_t n, const uint64_t *table, uint64_t *out, void *stream);
+/* acc[b] = sum_j pack[v1[b,j]] * pack[v2[b,j]] (uint64; GFqField.fgdp's word dot,
+ * gfext.py:287-290, batched over rows) */
+QADIC_API int qadic_gf_words_dot(const int64_t *v1, const int64_t *v2, int64_t rows, int64_t len,
+                                 const uint64_t *pack, uint64_t *acc, void *stream);
+/* handles[i] = L[u_0..u_{k-1}] + H[u_{k-1}..u_{2k-2}] with u = REDQ digits of acc[i]
+ * (gfext.py:291-296, 331-358: compress, L/H lookups, addition on codes) */
+QADIC_API int qadic_gf_words_finish(const uint64_t *acc, int64_t n, const qadic_gf_generic_desc *f,
+                                    int64_t *out, void *stream);
+/* int64 entries (any value < 2^t) <-> packed words; cmm.py:72-85 / 130-145 */
+QADIC_API int qadic_pack_rows_i64(const int64_t *m, int64_t rows, int64_t cols, int32_t k, int32_t t,
+                                  int32_t reverse, uint64_t *words, void *stream);
+QADIC_API int qadic_unpack_rows_i64(const uint64_t *words, int64_t rows, int64_t cols, int32_t k, int32_t t,
+                                    int32_t reverse, int64_t *out, void *stream);
+/* out[i] = ((acc[i] >> d t) & (2^t - 1)) mod p  (cmm_multiply's middle digit, cmm.py:200-204) */
+QADIC_API int qadic_extract_middle(const uint64_t *acc, int64_t n, int64_t p, int32_t t, int32_t d, int64_t *out,
+                                   void *stream);
+/* full_cmm's one REDQ per word over the (dq+1)(dth+1)-digit grid, corrected digits
+ * scattered to out[m, n] (cmm.py:349-359) */
+QADIC_API int qadic_full_cmm_reduce(const uint64_t *acc, int64_t mw, int64_t nw, int64_t p, int32_t t, int32_t dq,
+                                    int32_t dth, int64_t m, int64_t n, int64_t *out, void *stream);
+/* correct_digits_array (redq.py:308-315): mu_i = (u_i + c u_{i+1}) mod p (uint64 wrap),
+ * c = (p - q mod p) mod p, top digit kept; identity when q mod p == 0 */
+QADIC_API int qadic_correct_digits(const uint64_t *u, int64_t n, int32_t width, int64_t p, int64_t q_mod_p,
+                                   uint64_t *out, void *stream);
+
+/* ---------------------------------------------------------------------------
  * FDIV certification scans (fdiv.exhaustive_check / applied_fdiv_exhaustive,
  * fdiv.py:405-461; Table 1, Alg. 4).
  * Every (r, p) in [0, 2^beta) x [1, 2^beta) in beta-bit binary arithmetic:

@@ -44,6 +44,33 @@ class FieldDesc(ctypes.Structure):
     ]
 
 
+class GenericDesc(ctypes.Structure):
+    """Mirror of `qadic_gf_generic_desc`."""
+
+    _fields_ = [
+        ("p", I64),
+        ("k", I32),
+        ("t", I32),
+        ("u_bits", I32),
+        ("reserved", I32),
+        ("l_code", P),
+        ("h_code", P),
+        ("index_of_code", P),
+    ]
+
+
+class PolymulStats(ctypes.Structure):
+    """Mirror of `qadic_polymul_stats`."""
+
+    _fields_ = [
+        ("word_muls", I64),
+        ("reductions", I64),
+        ("leaves", I64),
+        ("levels", I32),
+        ("flags", ctypes.c_uint32),
+    ]
+
+
 class FdivScanReport(ctypes.Structure):
     """Mirror of `qadic_fdiv_scan_report`."""
 
@@ -85,6 +112,16 @@ _SIGNATURES = {
     "qadic_index_of_coeffs": ([P, I64, I32, I32, P, P, P], ctypes.c_int),
     "qadic_fdiv_scan": ([I32, I32, I32, I32, I32, I64, ctypes.POINTER(FdivScanReport), P], ctypes.c_int),
     "qadic_fdiv_applied_scan": ([I32, ctypes.POINTER(I64 * 3), ctypes.POINTER(ctypes.c_uint64), P], ctypes.c_int),
+    "qadic_polymul_words_batch": ([P, I64, P, I64, I64, I64, I32, I32, I64, I64, I32, I64, I32, I32, P, I64,
+                                   ctypes.POINTER(PolymulStats), P], ctypes.c_int),
+    "qadic_gather_u64": ([P, I64, P, P, P], ctypes.c_int),
+    "qadic_gf_words_dot": ([P, P, I64, I64, P, P, P], ctypes.c_int),
+    "qadic_gf_words_finish": ([P, I64, ctypes.POINTER(GenericDesc), P, P], ctypes.c_int),
+    "qadic_pack_rows_i64": ([P, I64, I64, I32, I32, I32, P, P], ctypes.c_int),
+    "qadic_unpack_rows_i64": ([P, I64, I64, I32, I32, I32, P, P], ctypes.c_int),
+    "qadic_extract_middle": ([P, I64, I64, I32, I32, P, P], ctypes.c_int),
+    "qadic_full_cmm_reduce": ([P, I64, I64, I64, I32, I32, I32, I64, I64, P, P], ctypes.c_int),
+    "qadic_correct_digits": ([P, I64, I32, I64, I64, P, P], ctypes.c_int),
     "qadic_fdiv_native_check": ([P, I64, P, P, I64, I64, ctypes.POINTER(ctypes.c_uint64), P], ctypes.c_int),
     "qadic_diag_pipe_peak": ([I32, I32, I64, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_float), P],
                              ctypes.c_int),

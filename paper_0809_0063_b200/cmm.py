@@ -88,18 +88,23 @@ def _entries(m, p: int):
     return m
 
 
-def _pack_dev(m_u8, k: int, t: int, reverse: bool):
-    rows, cols = m_u8.shape
+def _pack_dev(m, k: int, t: int, reverse: bool):
+    """Row packing on the device: uint8 entries (qadic_pack_rows_u8, the 16-byte
+    vector kernel) or int64 entries for p > 255 (qadic_pack_rows_i64)."""
+    rows, cols = m.shape
     out = N.empty((rows, -(-cols // k)), np.uint64)
-    N.check(N.lib().qadic_pack_rows_u8(N.ptr(m_u8), rows, cols, k, t, int(reverse), N.ptr(out), N.stream_ptr()))
+    fn = N.lib().qadic_pack_rows_u8 if m.dtype == N.torch().uint8 else N.lib().qadic_pack_rows_i64
+    N.check(fn(N.ptr(m), rows, cols, k, t, int(reverse), N.ptr(out), N.stream_ptr()))
     return out
 
 
-def _as_u8(m, p: int):
-    if p > 255:
-        raise NotImplementedError("uint8 entry path supports p <= 255")
-    d, _ = N.to_dev(m, np.uint8)
+def _as_dev_entries(m, p: int):
+    """Device entries: uint8 for p <= 255, int64 above."""
+    d, _ = N.to_dev(m, np.uint8 if p <= 255 else np.int64)
     return d
+
+
+_as_u8 = _as_dev_entries
 
 
 def compress_rows(a, params: PackingParams, digit_order: str = FORWARD) -> CompressedMatrix:
@@ -120,11 +125,21 @@ def compress_cols(b, params: PackingParams, digit_order: str = FORWARD) -> Compr
                             _host=not N.is_tensor(b))
 
 
-def _unpack_dev(words, rows: int, cols: int, k: int, t: int, reverse: bool):
+def _unpack_dev(words, rows: int, cols: int, k: int, t: int, reverse: bool, p: int = 2):
+    """Inverse of _pack_dev: uint8 entries for p <= 255, int64 above."""
     dw, _ = N.to_dev(words, np.uint64)
-    out = N.empty((rows, cols), np.uint8)
-    N.check(N.lib().qadic_unpack_rows_u8(N.ptr(dw), rows, cols, k, t, int(reverse), N.ptr(out), N.stream_ptr()))
+    if p <= 255:
+        out = N.empty((rows, cols), np.uint8)
+        fn = N.lib().qadic_unpack_rows_u8
+    else:
+        out = N.empty((rows, cols), np.int64)
+        fn = N.lib().qadic_unpack_rows_i64
+    N.check(fn(N.ptr(dw), rows, cols, k, t, int(reverse), N.ptr(out), N.stream_ptr()))
     return out
+
+
+def _host_int64(x):
+    return N.to_host(x, np.uint8 if x.dtype == N.torch().uint8 else np.int64).astype(np.int64)
 
 
 def uncompress(cm: CompressedMatrix):
@@ -133,11 +148,12 @@ def uncompress(cm: CompressedMatrix):
     host = not N.is_tensor(cm.words)
     lr, lc = cm.logical_shape
     if cm.orientation == ROWS:
-        out = _unpack_dev(cm.words, lr, lc, prm.k, prm.t, cm.digit_order == REVERSED)
+        out = _unpack_dev(cm.words, lr, lc, prm.k, prm.t, cm.digit_order == REVERSED, prm.p)
     else:
         dw, _ = N.to_dev(cm.words, np.uint64)
-        out = _unpack_dev(dw.t().contiguous(), lc, lr, prm.k, prm.t, cm.digit_order == REVERSED).t().contiguous()
-    return N.to_host(out, np.uint8).astype(np.int64) if host else out
+        out = _unpack_dev(dw.t().contiguous(), lc, lr, prm.k, prm.t, cm.digit_order == REVERSED,
+                          prm.p).t().contiguous()
+    return _host_int64(out) if host else out
 
 
 def modmatmul(a, b, p: int):
@@ -189,6 +205,8 @@ def right_cmm(a, cb: CompressedMatrix, params: Optional[PackingParams] = None, k
         raise DimensionMismatch("inner dimensions differ")
     _require_bounds(params, k_dim)
     host = not N.is_tensor(a)
+    if params.p > 127:  # beyond the coefficient engines: the reference's word composition
+        return _right_cmm_words(a, cb, params, keep_packed, host, out)
     da = _as_u8(a, params.p)
     db = cb._entries if cb._entries is not None else _unpack_dev(cb.words, k_dim, n, params.k, params.t, False)
     c = _right_cmm_raw(da, db, params.p, params.t, params.d, engine, out=out)
@@ -200,6 +218,23 @@ def right_cmm(a, cb: CompressedMatrix, params: Optional[PackingParams] = None, k
                                 orientation=ROWS, digit_order=FORWARD, logical_shape=(a.shape[0], n),
                                 _entries=c)
     return N.to_host(c, np.uint8).astype(np.int64) if host else c
+
+
+def _right_cmm_words(a, cb: CompressedMatrix, params: PackingParams, keep_packed: bool, host: bool, out):
+    """right_cmm as the reference composes it (cmm.py:266-276), on the GPU: the
+    exact uint64 product A x words on tensor cores, one REDQ + correction +
+    repack per word, then unpacking -- any p < 2^26."""
+    k_dim, n = cb.logical_shape
+    da, _ = N.to_dev(a, np.uint64)
+    acc = _kernels.matmul_exact_u64(da, N.to_dev(cb.words, np.uint64)[0])
+    red = redq.reduce_words_array(acc, params.p, params.t, params.d)
+    if keep_packed:
+        return CompressedMatrix(words=N.to_host(red, np.uint64) if host else red, params=params, orientation=ROWS,
+                                digit_order=FORWARD, logical_shape=(a.shape[0], n))
+    c = _unpack_dev(red, a.shape[0], n, params.k, params.t, False, params.p)
+    if out is not None:
+        return N.finish(c, out, host, np.uint8 if c.dtype == N.torch().uint8 else np.int64)
+    return _host_int64(c) if host else c
 
 
 def left_cmm(ca: CompressedMatrix, b, params: Optional[PackingParams] = None, keep_packed: bool = False):
@@ -242,8 +277,10 @@ def cmm_multiply(ca: CompressedMatrix, cb: CompressedMatrix, params: Optional[Pa
     _require_bounds(params, k_dim)
     host = not N.is_tensor(ca.words)
     acc = _kernels.matmul_exact_u64(N.to_dev(ca.words, np.uint64)[0], N.to_dev(cb.words, np.uint64)[0])
-    mid = ((acc >> (params.d * params.t)) & (params.q - 1)) % params.p
-    return N.to_host(mid, np.uint64).astype(np.int64) if host else mid
+    mid = N.empty(tuple(acc.shape), np.int64)
+    N.check(N.lib().qadic_extract_middle(N.ptr(acc), acc.numel(), params.p, params.t, params.d, N.ptr(mid),
+                                         N.stream_ptr()))
+    return N.to_host(mid, np.int64) if host else mid
 
 
 def extract_middle(word, params: PackingParams, mode: str = "inverse_mul") -> int:
@@ -275,14 +312,14 @@ def full_cmm(a, b, params2: FullCompressionParams):
     t, dq, dth = params2.t, params2.d_q, params2.d_theta
     if k_dim * (p - 1) ** 2 >= params2.q:
         raise ParamsViolation("inner dimension fills the digit capacity; use strict parameters")
-    ca = _pack_dev(_as_u8(np.ascontiguousarray(a.T), p), dq + 1, t, False).t().contiguous()
-    cb = _pack_dev(_as_u8(b, p), dth + 1, params2.theta_exp, False)
+    # A packed down its columns at radix Q, B along its rows at radix Theta = Q^(dq+1)
+    ca = _pack_dev(_as_dev_entries(np.ascontiguousarray(a.T), p), dq + 1, t, False).t().contiguous()
+    cb = _pack_dev(_as_dev_entries(b, p), dth + 1, params2.theta_exp, False)
     acc = _kernels.matmul_exact_u64(ca, cb)
-    ndig = (dq + 1) * (dth + 1)
-    digits = N.to_host(redq.reduce_words_digits(acc, p, t, ndig - 1), np.uint64)
-    tiles = digits.reshape(acc.shape[0], acc.shape[1], dth + 1, dq + 1)
-    out = tiles.transpose(0, 3, 1, 2).reshape(acc.shape[0] * (dq + 1), acc.shape[1] * (dth + 1))
-    return out[:m, :n].astype(np.int64)
+    out = N.empty((m, n), np.int64)
+    N.check(N.lib().qadic_full_cmm_reduce(N.ptr(acc), acc.shape[0], acc.shape[1], p, t, dq, dth, m, n, N.ptr(out),
+                                          N.stream_ptr()))
+    return N.to_host(out, np.int64)
 
 
 def write_matrix(f: TextIO, m, p: int) -> None:

@@ -171,32 +171,109 @@ class GFqField:
 
     # -- device-side view ---------------------------------------------------------
     def _device_state(self):
+        """Device tables of the coefficient I/O: handle <-> coefficient maps
+        (p <= 255) and, for the coefficient engines, the L/H byte tables and the
+        qadic_field_desc."""
         torch = N.require_cuda()
         dev = torch.cuda.current_device()
         st = self._dev.get(dev)
         if st is None:
+            if self.p > 255:
+                raise NotImplementedError("uint8 coefficient I/O needs p <= 255; use the handle API")
             d = N.device()
             st = {
-                "l": torch.from_numpy(self._l_bytes.view(np.int32)).to(d),
-                "h": torch.from_numpy(self._h_bytes.view(np.int32)).to(d),
                 "coeffs": torch.from_numpy(self.coeffs_of_code[self.code_of_index].astype(np.uint8)).to(d),
                 "ioc": torch.from_numpy(self.index_of_code).to(d),
             }
-            desc = N.FieldDesc()
-            desc.p, desc.k, desc.t, desc.u_bits = self.p, self.k, self.params.t, self.u_bits
-            for i in range(2 * self.k - 1):
-                for l in range(self.k):
-                    desc.xpow[i][l] = int(self.xpow[i, l])
-            desc.l_table = st["l"].data_ptr()
-            desc.h_table = st["h"].data_ptr()
-            st["desc"] = desc
+            if self.coeff_engines_ok:
+                st["l"] = torch.from_numpy(self._l_bytes.view(np.int32)).to(d)
+                st["h"] = torch.from_numpy(self._h_bytes.view(np.int32)).to(d)
+                desc = N.FieldDesc()
+                desc.p, desc.k, desc.t, desc.u_bits = self.p, self.k, self.params.t, self.u_bits
+                for i in range(2 * self.k - 1):
+                    for l in range(self.k):
+                        desc.xpow[i][l] = int(self.xpow[i, l])
+                desc.l_table = st["l"].data_ptr()
+                desc.h_table = st["h"].data_ptr()
+                st["desc"] = desc
             self._dev[dev] = st
         return st
+
+    # -- the any-field word path (csrc/generic.cu) ------------------------------------
+    @property
+    def coeff_engines_ok(self) -> bool:
+        """Whether the uint8 coefficient engines (batched dot, tensor-core / DMMA
+        matmul) cover this field: p <= 127, k <= 4, L/H index <= 24 bits and a
+        binary radix.  Other fields run the word path."""
+        return (self.p <= 127 and self.k <= 4 and self.u_bits * self.k <= 24 and self.params.t is not None)
+
+    def _generic_state(self):
+        torch = N.require_cuda()
+        dev = torch.cuda.current_device()
+        key = ("generic", dev)
+        st = self._dev.get(key)
+        if st is None:
+            if self.params.t is None:
+                raise ParamsViolation("the GPU path needs a binary radix")
+            d = N.device()
+            st = {
+                "pack": torch.from_numpy(self.pack_table.view(np.int64)).to(d),
+                "l_code": torch.from_numpy(self.code_of_index[self.l_table].astype(np.int32)).to(d),
+                "h_code": torch.from_numpy(self.code_of_index[self.h_table].astype(np.int32)).to(d),
+                "ioc": torch.from_numpy(self.index_of_code).to(d),
+            }
+            desc = N.GenericDesc()
+            desc.p, desc.k, desc.t, desc.u_bits = self.p, self.k, self.params.t, self.u_bits
+            desc.l_code, desc.h_code = st["l_code"].data_ptr(), st["h_code"].data_ptr()
+            desc.index_of_code = st["ioc"].data_ptr()
+            st["desc"] = desc
+            self._dev[key] = st
+        return st
+
+    def _words_of(self, handles):
+        """pack_table[handles] on the device (uint64 words in int64 storage)."""
+        st = self._generic_state()
+        out = N.empty(tuple(handles.shape), np.uint64)
+        N.check(N.lib().qadic_gather_u64(N.ptr(handles), handles.numel(), N.ptr(st["pack"]), N.ptr(out),
+                                         N.stream_ptr()))
+        return out
+
+    def _finish_words(self, acc):
+        """REDQ + L/H lookups + field addition of uint64 accumulators -> handles."""
+        st = self._generic_state()
+        out = N.empty(tuple(acc.shape), np.int64)
+        N.check(N.lib().qadic_gf_words_finish(N.ptr(acc), acc.numel(), st["desc"], N.ptr(out), N.stream_ptr()))
+        return out
+
+    def _fgdp_words(self, v1, v2):
+        d1, h1 = N.to_dev(v1, np.int64)
+        d2, h2 = N.to_dev(v2, np.int64)
+        if d1.dim() != 2 or tuple(d1.shape) != tuple(d2.shape):
+            raise DimensionMismatch("operands must both be [B, n]")
+        st = self._generic_state()
+        acc = N.empty((d1.shape[0],), np.uint64)
+        N.check(N.lib().qadic_gf_words_dot(N.ptr(d1), N.ptr(d2), d1.shape[0], d1.shape[1], N.ptr(st["pack"]),
+                                           N.ptr(acc), N.stream_ptr()), DimensionMismatch)
+        res = self._finish_words(acc)
+        return N.to_host(res, np.int64) if (h1 or h2) else res
+
+    def _matmul_words(self, a, b):
+        """GFqField.matmul as the reference composes it (gfext.py:329-345): word
+        gathers, the exact uint64 product on tensor cores, REDQ + L/H + addition."""
+        from . import _kernels
+
+        da, ha = N.to_dev(a, np.int64)
+        db, hb = N.to_dev(b, np.int64)
+        acc = _kernels.matmul_exact_u64(self._words_of(da), self._words_of(db))
+        res = self._finish_words(acc)
+        return N.to_host(res, np.int64) if (ha or hb) else res
 
     def field_desc(self) -> N.FieldDesc:
         """The qadic_field_desc of this field (device tables resident)."""
         if self.params.t is None:
             raise ParamsViolation("the GPU path needs a binary radix")
+        if not self.coeff_engines_ok:
+            raise NotImplementedError("the coefficient engines need p <= 127, k <= 4 (word path otherwise)")
         return self._device_state()["desc"]
 
     def to_coeffs(self, idx):
@@ -289,6 +366,9 @@ class GFqField:
         """Handles [B, n] x [B, n] -> handles [B]."""
         for m in (v1, v2):
             self._check_handles(m)
+        self._check_len((tuple(v1.shape) if N.is_tensor(v1) else np.shape(v1))[-1])
+        if not self.coeff_engines_ok:
+            return self._fgdp_words(v1, v2)
         c1 = self.to_coeffs(v1)
         c2 = self.to_coeffs(v2)
         return self.to_indices(self.fgdp_batch_coeffs(c1, c2))
@@ -301,6 +381,11 @@ class GFqField:
             raise DimensionMismatch(f"operands must both be [B, n, {self.k}]")
         b, n = d1.shape[0], d1.shape[1]
         self._check_len(n)
+        if not self.coeff_engines_ok:  # word path through handles (p <= 255)
+            res = self.to_coeffs(self._fgdp_words(self.to_indices(d1), self.to_indices(d2)))
+            if out is not None:
+                return N.finish(res, out, h1 or h2, np.uint8)
+            return N.to_host(res, np.uint8) if (h1 or h2) else res
         dev = N.out_buffer(out, (b, self.k), np.uint8)
         N.check(N.lib().qadic_gf_dot_batch_u8(self.field_desc(), N.ptr(d1), N.ptr(d2), b, n, N.ptr(dev),
                                               N.stream_ptr()), DimensionMismatch)
@@ -331,6 +416,8 @@ class GFqField:
         self._check_len(sa[1])
         for m in (a, b):
             self._check_handles(m)
+        if not self.coeff_engines_ok or (engine == "auto" and sa[1] * self.k * (self.p - 1) ** 2 >= (1 << 31)):
+            return self._matmul_words(a, b)
         c = self.matmul_coeffs(self.to_coeffs(a), self.to_coeffs(b), engine=engine)
         return self.to_indices(c)
 
@@ -347,6 +434,17 @@ class GFqField:
         in-register REDQ fold every `fold_period` inner terms (default: the
         largest multiple of 4 within the accumulation budget), i.e. the
         K-chunked GFqField.matmul of SURVEY.md 8(b)."""
+        if not self.coeff_engines_ok:  # word path through handles (p <= 255, K <= n_max)
+            da, ha = N.to_dev(a, np.uint8)
+            db, hb = N.to_dev(b, np.uint8)
+            if da.dim() != 3 or db.dim() != 3 or da.shape[1] != db.shape[0] or da.shape[2] != self.k \
+                    or db.shape[2] != self.k:
+                raise DimensionMismatch("incompatible shapes")
+            self._check_len(da.shape[1])
+            res = self.to_coeffs(self._matmul_words(self.to_indices(da), self.to_indices(db)))
+            if out is not None:
+                return N.finish(res, out, ha or hb, np.uint8)
+            return N.to_host(res, np.uint8) if (ha or hb) else res
         if not (N.is_tensor(a) and a.is_cuda):  # host A: panelled H2D / compute / D2H pipeline
             return self._matmul_host(a, b, engine, fold_period, out)
         da, ha = N.to_dev(a, np.uint8)

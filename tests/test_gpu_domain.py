@@ -1,0 +1,138 @@
+"""Drop-in domain: inputs the reference accepts beyond the five configs, against
+golden vectors produced by running the reference itself
+(tests/golden/make_golden_domain.py): primes above 127 / 255, extension degrees
+above 4, long polynomials over large primes, the batched engine fallback, the
+reference's wrap-around digit correction.  Reference domain: src/params.py:29
+(p < 2^26), src/gfext.py:38-39 (order <= 2^22), src/cmm.py:86-94."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import qadic_oracle as O
+from paper_0809_0063_b200 import cmm, gfext, polymul, redq
+from paper_0809_0063_b200.params import cmm_params, fqt_params, full_cmm_params
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.fixture(scope="module")
+def dom():
+    return np.load(os.path.join(HERE, "golden", "golden_domain.npz"))
+
+
+@pytest.fixture(scope="module")
+def dom_sc():
+    with open(os.path.join(HERE, "golden", "golden_domain.json")) as fh:
+        return json.load(fh)
+
+
+FIELDS = [(131, 1, 16), (2, 5, 4), (3, 5, 1), (2, 6, 2), (2, 7, 1), (131, 2, 2), (257, 1, 32), (65537, 1, 64)]
+
+
+@pytest.mark.parametrize("p,k,n", FIELDS)
+def test_field_matmul_and_dots(dom, dom_sc, p, k, n):
+    name = f"f{p}_{k}"
+    f = gfext.build_field(p, k, max_dot_length=n)
+    s = dom_sc[name]
+    assert list(f.irreducible) == s["irreducible"] and f.generator_code == s["generator_code"]
+    assert f.params.t == s["t"] and f.params.n_max == s["n_max"]
+    assert np.array_equal(f.code_of_index, dom[f"{name}_code_of_index"])
+    assert np.array_equal(f.matmul(dom[f"{name}_mm_a"], dom[f"{name}_mm_b"]), dom[f"{name}_mm_c"])
+    assert np.array_equal(f.fgdp_batch(dom[f"{name}_dot_v1"], dom[f"{name}_dot_v2"]), dom[f"{name}_dot_c"])
+    v1, v2 = dom[f"{name}_dot_v1"][0], dom[f"{name}_dot_v2"][0]
+    got = f.fgdp([f.elem(int(x)) for x in v1], [f.elem(int(y)) for y in v2])
+    assert got.index == int(dom[f"{name}_dot_c"][0])
+
+
+@pytest.mark.parametrize("p,k,n", [(131, 1, 16), (2, 5, 4), (131, 2, 2)])
+def test_field_coefficient_api_outside_engines(dom, p, k, n):
+    """matmul_coeffs / fgdp_batch_coeffs on fields the coefficient engines do not
+    cover run the word path through handles (p <= 255)."""
+    name = f"f{p}_{k}"
+    f = gfext.build_field(p, k, max_dot_length=n)
+    assert not f.coeff_engines_ok
+    ca, cb = f.to_coeffs(dom[f"{name}_mm_a"]), f.to_coeffs(dom[f"{name}_mm_b"])
+    assert np.array_equal(f.to_indices(f.matmul_coeffs(ca, cb)), dom[f"{name}_mm_c"])
+    d1, d2 = f.to_coeffs(dom[f"{name}_dot_v1"]), f.to_coeffs(dom[f"{name}_dot_v2"])
+    assert np.array_equal(f.to_indices(f.fgdp_batch_coeffs(d1, d2)), dom[f"{name}_dot_c"])
+
+
+def test_word_path_equals_engines_inside_their_domain():
+    """GF(9) and GF(7^3): the any-field word path (gathers, byte-plane tensor-core
+    uint64 GEMM, REDQ + L/H) agrees with the coefficient engines."""
+    g = np.random.default_rng(11)
+    for p, k, n in ((3, 2, 64), (7, 3, 9), (101, 1, 500)):
+        f = gfext.build_field(p, k, max_dot_length=n)
+        a = g.integers(0, f.order, (40, n), dtype=np.int64)
+        b = g.integers(0, f.order, (n, 33), dtype=np.int64)
+        assert np.array_equal(f._matmul_words(a, b), f.matmul(a, b))
+        assert np.array_equal(f._fgdp_words(a[:, :n], a[:, :n][::-1].copy()), f.fgdp_batch(a, a[::-1].copy()))
+
+
+@pytest.mark.parametrize("p", [131, 251, 257, 1021, 4099])
+def test_cmm_large_entries(dom, dom_sc, p):
+    tag = f"cmm{p}"
+    s = dom_sc[tag]
+    prm = cmm_params(p, s["k_dim"], strict=True)
+    a, b = dom[f"{tag}_a"], dom[f"{tag}_b"]
+    cb = cmm.compress_rows(b, prm, cmm.FORWARD)
+    assert np.array_equal(cb.words, dom[f"{tag}_words"])
+    assert np.array_equal(cmm.uncompress(cb), b)
+    assert np.array_equal(cmm.right_cmm(a, cb), dom[f"{tag}_right"])
+    assert np.array_equal(cmm.right_cmm(a, cb, keep_packed=True).words, dom[f"{tag}_right_packed"])
+    assert np.array_equal(cmm.left_cmm(cmm.compress_cols(a, prm, cmm.FORWARD), b), dom[f"{tag}_left"])
+    assert np.array_equal(cmm.cmm_multiply(cmm.compress_rows(a, prm, cmm.REVERSED), cmm.compress_cols(b, prm)),
+                          dom[f"{tag}_mid"])
+    assert np.array_equal(cmm.modmatmul(a, b, p), (a.astype(object) @ b.astype(object) % p).astype(np.int64))
+
+
+@pytest.mark.parametrize("p", [31, 89])
+def test_full_cmm_kernel(dom, dom_sc, p):
+    s = dom_sc[f"full{p}"]
+    fp = full_cmm_params(p, s["k_dim"], strict=True)
+    assert np.array_equal(cmm.full_cmm(dom[f"full{p}_a"], dom[f"full{p}_b"], fp), dom[f"full{p}_c"])
+
+
+@pytest.mark.parametrize("tag", ["poly131_1", "poly65537_0", "poly1009_0", "poly5_2", "poly3_3"])
+def test_long_polynomials(dom, dom_sc, tag):
+    s = dom_sc[tag]
+    p, d = s["p"], s["d"]
+    prm = fqt_params(p, d)
+    a, b = polymul.ModPoly(dom[f"{tag}_a"], p), polymul.ModPoly(dom[f"{tag}_b"], p)
+    st = polymul.PolymulStats()
+    got = polymul.polymul_fqt(a, b, prm, stats=st)
+    assert np.array_equal(got.coeffs, dom[f"{tag}_c"])
+    assert (st.word_muls, st.reductions) == (s["word_muls"], s["reductions"])
+    for thr in (2, 8, 64):
+        kara = polymul.polymul_fqt(a, b, prm, "karatsuba", threshold=thr, validate=True)
+        assert np.array_equal(kara.coeffs, dom[f"{tag}_kara"]), thr
+    assert np.array_equal(polymul.polymul_delayed(a, b).coeffs, dom[f"{tag}_delayed"])
+
+
+def test_batched_long_products():
+    """polymul_fqt_long_batch: every row equals the per-pair product (oracle)."""
+    g = np.random.default_rng(5)
+    for p, d, la, lb, bsz in ((3, 3, 777, 500, 5), (7, 2, 40, 41, 64), (2, 5, 3000, 3000, 2)):
+        prm = fqt_params(p, d)
+        a = g.integers(0, p, (bsz, la), dtype=np.int64)
+        b = g.integers(0, p, (bsz, lb), dtype=np.int64)
+        for algo in ("classical", "karatsuba"):
+            got = polymul.polymul_fqt_long_batch(a, b, prm, algo=algo, threshold=8)
+            for i in range(bsz):
+                want = O.polymul_fqt(a[i], b[i], p, prm.t, d)
+                assert np.array_equal(np.asarray(got[i], np.int64), want), (p, d, algo, i)
+
+
+def test_batched_one_word_beyond_fused_kernel(dom):
+    prm = fqt_params(131, 1)
+    got = polymul.polymul_fqt_batch(dom["pbatch131_a"], dom["pbatch131_b"], prm)
+    assert np.array_equal(np.asarray(got, np.int64), dom["pbatch131_c"])
+
+
+def test_correct_digits_wraparound(dom):
+    assert np.array_equal(redq.correct_digits_array(dom["corr_u"], 23, 1 << 13), dom["corr_mu_23_13"])
+    assert np.array_equal(redq.correct_digits_array(dom["corr_u"], 5, 100), dom["corr_mu_5_100"])
