@@ -150,7 +150,8 @@ def config_dict(cfg, engine, ws, partition="rows", panels=None):
         d.update({"shape": list(c.shape), "p": c.p, "k": c.k, "engine": "fused",
                   "l2": "rotating 16 input sets > 126 MB L2"})
     if ws == 1:
-        d["parallelism"] = "single"
+        d["parallelism"] = "single" if not panels or panels <= 1 or cfg in (1, 2) else \
+            f"single (B in {panels} column panels, the row-block step without a collective)"
     elif cfg in (1, 2):
         d["parallelism"] = f"batch{ws}"
     elif partition == "rows":
@@ -180,7 +181,7 @@ def build_rowblock_step(cfg, engine, rank, ws, torch, Q, W, args, meta):
         host_b = host_a  # A^2: B = A
         out_k = ()
 
-        def compute(a_rows, bp, cp, eng=engine):
+        def compute(a_rows, bp, cp, j=0, eng=engine):
             Q.cmm.right_cmm(a_rows, Q.cmm.compress_rows(bp, prm), engine=eng, out=cp)
     else:
         f = W.field_for(c)
@@ -189,8 +190,8 @@ def build_rowblock_step(cfg, engine, rank, ws, torch, Q, W, args, meta):
         host_a, host_b = x["a"], x["b"]
         out_k = (c.k,)
 
-        def compute(a_rows, bp, cp, eng=engine):
-            f.matmul_coeffs(a_rows, bp, engine=eng, out=cp)
+        def compute(a_rows, bp, cp, j=0, eng=engine):
+            f.matmul_coeffs(a_rows, bp, engine=eng, out=cp, col_panel=j)
     r0, r1 = Q.shard.row_block(m, ws, rank)
     rows = r1 - r0
     bounds = Q.shard.panel_bounds(n, P)
@@ -247,7 +248,7 @@ def build_step(cfg, engine, rank, ws, torch, dist, Q, W, args):
     c = W.CONFIGS[cfg]
     dev = torch.device("cuda", torch.cuda.current_device())
     meta = {"config": config_dict(cfg, engine, ws, args.partition, args.panels)}
-    if cfg in (3, 4, 5) and ws > 1 and args.partition == "rows":
+    if cfg in (3, 4, 5) and (ws > 1 or args.panels > 1) and args.partition == "rows":
         return build_rowblock_step(cfg, engine, rank, ws, torch, Q, W, args, meta)
     if cfg in (3, 5):
         f = W.field_for(c)
@@ -872,6 +873,13 @@ PRIMS = {
     # the reference's GF(9) driver product: packed words uint64[8192, 8192] @ uint64[8192, 8192]
     # (Layer K matmul_exact_u64, exact mod 2^64; words of 2 digits at q=2^17)
     "mm64": {"n": 8192, "bits": 34},
+    # batched long-polynomial products (polymul_fqt_long_batch, csrc/polymul_long.cu):
+    # 16 pairs of length-16384 polynomials over F_3, classical schedule, at
+    # fqt_params(3, 1) (t = 17, 2 coefficients per word, a REDQ fold every 16383 inner
+    # terms: FMA-bound) and at fqt_params(3, 3) (t = 7, 4 per word, a fold every 7
+    # terms: fold-bound)
+    "polylong": {"batch": 16, "len": 16384, "p": 3, "d": 1},
+    "polylong3": {"batch": 16, "len": 16384, "p": 3, "d": 3},
 }
 
 
@@ -916,6 +924,24 @@ def run_primitive(args, kind):
         byts, units, unit = None, n ** 3, "u64 MAC/s"
         workload = f"mm64:matmul_exact_u64 {n}^3 words < 2^{cfgp['bits']} (the reference GF(9) driver product)"
         kname = "u64 byte-plane gemm"
+    elif kind in ("polylong", "polylong3"):
+        from paper_0809_0063_b200 import polymul
+        from paper_0809_0063_b200.params import fqt_params
+
+        bsz, ln, p, d = cfgp["batch"], cfgp["len"], cfgp["p"], cfgp["d"]
+        prm = fqt_params(p, d)
+        sets = [torch.from_numpy(g.integers(0, p, (bsz, ln), dtype=np.uint8)).cuda() for _ in range(2)]
+        bset = [torch.from_numpy(g.integers(0, p, (bsz, ln), dtype=np.uint8)).cuda() for _ in range(2)]
+        outs = [torch.empty((bsz, 2 * ln - 1), dtype=torch.uint8, device="cuda") for _ in sets]
+
+        def step(i):
+            polymul.polymul_fqt_long_batch(sets[i % 2], bset[i % 2], prm, out=outs[i % 2])
+
+        nw = -(-ln // prm.k)
+        byts, units, unit = None, bsz * nw * nw, "word MAC/s"
+        workload = (f"polylong:polymul_fqt_long_batch {bsz} pairs x {ln} coeffs over F_{p}, q=2^{prm.t}, "
+                    f"k={prm.k} ({nw} words), fold every {(prm.q - 1 - (p - 1)) // (prm.k * (p - 1) ** 2)} terms")
+        kname = "polymul conv"
     elif kind == "unpack":
         rows, cols, k, t = cfgp["rows"], cfgp["cols"], cfgp["k"], cfgp["t"]
         width = -(-cols // k)
@@ -963,7 +989,19 @@ def run_primitive(args, kind):
     ms = e0.elapsed_time(e1) / steps
     launches = N.launch_count() - launches0
     peaks, peak_src = load_peaks()
-    if byts is None:  # tensor-bound: one byte-plane GEMM per shift s
+    if kind in ("polylong", "polylong3"):  # FP64 FMA + in-register folds (no tensor-core formulation)
+        fma_rate = units / (ms / 1e3)
+        peak_f = None
+        if not args.no_probe:
+            pr = pipe_probe(N, "f64", 0.1)
+            peak_f = pr.get("burst")
+        peak = (peak_f or 37.0) * 1e12 / 2  # FMA/s: DMMA probe flop/s / 2 (the FP64 pipe's measured rate)
+        roof = {"bound": "fp64", "kernel": kname, "achieved": round(fma_rate / 1e12, 3), "peak": round(peak / 1e12, 3),
+                "unit": "T word-FMA/s", "frac": round(fma_rate / peak, 4), "traffic": None,
+                "avg_launch_ms": round(ms, 4),
+                "peak_source": "measured DMMA pipe probe / 2 (FP64 FMA rate)" if peak_f else "nominal 37 TFLOP/s / 2",
+                "note": "the REDQ folds (every few terms at this radix) are integer ALU work on top of the FMAs"}
+    elif byts is None:  # tensor-bound: one byte-plane GEMM per shift s
         # byte MACs the segmented byte-plane GEMMs issue per word MAC: plane s < 8
         # multiplies A byte i by B byte s - i for every valid i (nb significant bytes each)
         nb = -(-PRIMS["mm64"]["bits"] // 8)

@@ -48,6 +48,14 @@ typedef enum qadic_engine {
                                   TMEM accumulators), p <= 7 */
 } qadic_engine;
 
+/* Flags OR-ed into the engine argument of qadic_gf_matmul_u8 for a caller that sweeps
+ * column panels of B against one A on one stream and workspace (the multi-GPU
+ * row-block step): COL_PANEL on the first panel, A_READY on the later ones -- the
+ * FP4K engine then keeps A's evaluation planes in the workspace instead of
+ * re-converting A per panel.  Other engines ignore them. */
+#define QADIC_ENGINE_FLAG_COL_PANEL 0x100
+#define QADIC_ENGINE_FLAG_A_READY 0x200
+
 QADIC_API int qadic_abi_version(void);
 QADIC_API const char *qadic_last_error(void);
 /* number of kernels this library launched since load (instrumentation) */

@@ -1879,6 +1879,7 @@ static void launch_planes(const uint8_t* a, const uint8_t* b, int64_t m, int64_t
                                                                   n * L.ldk, tk, tj));
         }
     }
+    if (a == nullptr) return;  // A planes already in the workspace (column-panel sweep)
     const int64_t ta = m * (L.ldk / 16);
     QADIC_TIMED("fp4k planes A", s,
                 planes_kernel<K><<<(unsigned)((ta + 255) / 256), 256, 0, s>>>(a, m, kdim, p, tab, L.S, as, L.ldk,
@@ -1909,9 +1910,14 @@ static void launch_combine(const uint8_t* d, int64_t m, int64_t n, const KaraLay
 // C[m, n, k] = A[m, K, k] B[K, n, k] over GF(p^k) through plane products.
 // Workspace: [plane table | B planes | A planes | D planes]; the table and the B
 // planes sit at offsets independent of m, so a row-panelled caller (the host
-// pipeline) prepares them once and passes b_ready for the later panels.
+// pipeline) prepares them once and passes REUSE_B_READY for the later panels.
+// REUSE_COL_PANEL swaps the layout to [table | A planes | B planes | D planes]
+// (A at an n-independent offset) for a caller that sweeps column panels of B
+// against one A (the multi-GPU row-block step); REUSE_A_READY then skips the A
+// conversion on every panel after the first.
 static int run_kara(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
-                    void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s, bool b_ready) {
+                    void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s, int reuse) {
+    const bool b_ready = reuse & REUSE_B_READY;
     const int k = (int)f.k;
     PlaneSpec ps;
     QADIC_REQUIRE(plan_planes(f, &ps), QADIC_ERR_UNSUPPORTED, "no plane decomposition with <= %d planes", KMAX_S);
@@ -1920,19 +1926,26 @@ static int run_kara(const FieldConst& f, const uint8_t* a, const uint8_t* b, int
     QADIC_REQUIRE(ws != nullptr && ws_bytes >= need, QADIC_ERR_VALUE, "workspace too small (%zu < %zu)", ws_bytes,
                   need);
     uint32_t* tab = static_cast<uint32_t*>(ws);
-    uint8_t* bs = static_cast<uint8_t*>(ws) + L.tab_bytes;
-    uint8_t* as = bs + L.b_bytes;
-    uint8_t* dd = as + L.a_bytes;
+    uint8_t *bs, *as;
+    if (reuse & REUSE_COL_PANEL) {
+        as = static_cast<uint8_t*>(ws) + L.tab_bytes;
+        bs = as + L.a_bytes;
+    } else {
+        bs = static_cast<uint8_t*>(ws) + L.tab_bytes;
+        as = bs + L.b_bytes;
+    }
+    uint8_t* dd = static_cast<uint8_t*>(ws) + L.tab_bytes + L.a_bytes + L.b_bytes;
     int ncodes = 1;
     for (int i = 0; i < k; ++i) ncodes *= (int)f.p;
     QADIC_REQUIRE(ncodes <= PT_CODES, QADIC_ERR_UNSUPPORTED, "plane table needs p^k <= %d", PT_CODES);
     const uint8_t* bsrc = b_ready ? nullptr : b;
+    const uint8_t* asrc = (reuse & REUSE_A_READY) ? nullptr : a;
     const uint32_t lut = e2m1_lut(f.p, kdim);
     switch (k) {
-        case 1: launch_planes<1>(a, bsrc, m, kdim, n, f.p, tab, ps, lut, L, as, bs, s); break;
-        case 2: launch_planes<2>(a, bsrc, m, kdim, n, f.p, tab, ps, lut, L, as, bs, s); break;
-        case 3: launch_planes<3>(a, bsrc, m, kdim, n, f.p, tab, ps, lut, L, as, bs, s); break;
-        default: launch_planes<4>(a, bsrc, m, kdim, n, f.p, tab, ps, lut, L, as, bs, s); break;
+        case 1: launch_planes<1>(asrc, bsrc, m, kdim, n, f.p, tab, ps, lut, L, as, bs, s); break;
+        case 2: launch_planes<2>(asrc, bsrc, m, kdim, n, f.p, tab, ps, lut, L, as, bs, s); break;
+        case 3: launch_planes<3>(asrc, bsrc, m, kdim, n, f.p, tab, ps, lut, L, as, bs, s); break;
+        default: launch_planes<4>(asrc, bsrc, m, kdim, n, f.p, tab, ps, lut, L, as, bs, s); break;
     }
     int rc = check_launch("fp4k planes");
     if (rc) return rc;
@@ -2579,10 +2592,10 @@ size_t tc_kara_workspace(uint32_t p, int64_t m, int64_t kdim, int64_t n, int k) 
 }
 
 int tc_kara_gf_matmul(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
-                      void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s, bool b_ready) {
+                      void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s, int reuse) {
     QADIC_REQUIRE(tc_kara_ok(f.p, kdim, (int)f.k), QADIC_ERR_PARAMS,
                   "fp4k engine needs p <= 7, K*h^2 < 2^24 (h = max |centred residue|) and at most %d planes", tc::KMAX_S);
-    return tc::run_kara(f, a, b, m, kdim, n, ws, ws_bytes, c, s, b_ready);
+    return tc::run_kara(f, a, b, m, kdim, n, ws, ws_bytes, c, s, reuse);
 }
 
 int tc_kara_right_cmm(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n, uint32_t p, void* ws,
@@ -2593,7 +2606,7 @@ int tc_kara_right_cmm(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdi
     f.t = 8;
     f.magic = small_magic(p);
     f.xpow[0][0] = 1;
-    return tc_kara_gf_matmul(f, a, b, m, kdim, n, ws, ws_bytes, c, s, false);
+    return tc_kara_gf_matmul(f, a, b, m, kdim, n, ws, ws_bytes, c, s, 0);
 }
 
 // I8K engine: evaluation planes on int8 (p <= 7 for the nibble D planes and the

@@ -21,7 +21,7 @@ int tc_right_cmm(int kind, const uint8_t* a, const uint8_t* b, int64_t m, int64_
 size_t tc_kara_workspace(uint32_t p, int64_t m, int64_t kdim, int64_t n, int k);
 bool tc_kara_ok(uint32_t p, int64_t kdim, int k);
 int tc_kara_gf_matmul(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
-                      void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s, bool b_ready);
+                      void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s, int reuse);
 int tc_kara_right_cmm(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n, uint32_t p, void* ws,
                       size_t ws_bytes, uint8_t* c, cudaStream_t s);
 bool tc_kara8_ok(uint32_t p, int64_t kdim, int k);
@@ -51,13 +51,15 @@ static int resolve_engine(int32_t engine, uint32_t p, int64_t kdim, int k) {
 }
 static int tc_kind(int eng) { return eng == QADIC_ENGINE_F4_TC ? 1 : 0; }
 
-// device-pointer GF(p^k) matmul on the resolved engine; b_ready: the fp4k
-// engine's B planes are already in `ws` (row panels of one host call)
+// device-pointer GF(p^k) matmul on the resolved engine; reuse (REUSE_* bits, fp4k
+// engine): B planes already in `ws` (row panels of one host call), or the
+// column-panel layout with A planes already in `ws`
 static int gf_matmul_dev(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
                          int32_t engine, int32_t fold_period, void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s,
-                         bool b_ready) {
+                         int reuse) {
+    const bool b_ready = reuse & REUSE_B_READY;
     const int eng = resolve_engine(engine, f.p, kdim, (int)f.k);
-    if (eng == QADIC_ENGINE_F4K_TC) return tc_kara_gf_matmul(f, a, b, m, kdim, n, ws, ws_bytes, c, s, b_ready);
+    if (eng == QADIC_ENGINE_F4K_TC) return tc_kara_gf_matmul(f, a, b, m, kdim, n, ws, ws_bytes, c, s, reuse);
     if (eng == QADIC_ENGINE_I8K_TC) return tc_kara8_gf_matmul(f, a, b, m, kdim, n, ws, ws_bytes, c, s, b_ready);
     if (eng == QADIC_ENGINE_I8_TC || eng == QADIC_ENGINE_F4_TC)
         return tc_gf_matmul(tc_kind(eng), f, a, b, m, kdim, n, ws, ws_bytes, c, s);
@@ -84,6 +86,7 @@ extern "C" {
 
 size_t qadic_gf_matmul_workspace(const qadic_field_desc* f, int64_t m, int64_t kdim, int64_t n, int32_t engine) {
     if (!f || m < 0 || kdim < 0 || n < 0) return 0;
+    engine &= 0xff;
     const int eng = resolve_engine(engine, (uint32_t)f->p, kdim, f->k);
     if (eng == QADIC_ENGINE_F4K_TC) return tc_kara_workspace((uint32_t)f->p, m, kdim, n, f->k);
     if (eng == QADIC_ENGINE_I8K_TC) return tc_kara8_workspace((uint32_t)f->p, m, kdim, n, f->k);
@@ -94,6 +97,11 @@ size_t qadic_gf_matmul_workspace(const qadic_field_desc* f, int64_t m, int64_t k
 int qadic_gf_matmul_u8(const qadic_field_desc* fd, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim,
                        int64_t n, int32_t engine, int32_t fold_period, void* ws, size_t ws_bytes, uint8_t* c,
                        void* stream) {
+    // column-panel sweep flags (QADIC_ENGINE_FLAG_*) ride on the engine argument
+    int reuse = 0;
+    if (engine & QADIC_ENGINE_FLAG_COL_PANEL) reuse |= REUSE_COL_PANEL;
+    if (engine & QADIC_ENGINE_FLAG_A_READY) reuse |= REUSE_COL_PANEL | REUSE_A_READY;
+    engine &= 0xff;
     FieldConst f;
     int rc = make_field_const(fd, &f);
     if (rc) return rc;
@@ -104,7 +112,7 @@ int qadic_gf_matmul_u8(const qadic_field_desc* fd, const uint8_t* a, const uint8
         cudaMemsetAsync(c, 0, (size_t)(m * n * f.k), s);
         return check_launch("gf_matmul (empty K)");
     }
-    return gf_matmul_dev(f, a, b, m, kdim, n, engine, fold_period, ws, ws_bytes, c, s, false);
+    return gf_matmul_dev(f, a, b, m, kdim, n, engine, fold_period, ws, ws_bytes, c, s, reuse);
 }
 
 size_t qadic_right_cmm_workspace(int64_t m, int64_t kdim, int64_t n, int64_t p, int32_t d, int32_t engine) {
@@ -289,7 +297,8 @@ int qadic_gf_matmul_host_u8(const qadic_field_desc* fd, const uint8_t* a, const 
             cudaMemsetAsync(cp, 0, (size_t)(rows * n * k), s);
             rc = check_launch("gf_matmul_host (empty K)");
         } else {
-            rc = gf_matmul_dev(f, ap, bsrc, rows, kdim, n, engine, fold_period, base, eng_ws, cp, s, i > 0);
+            rc = gf_matmul_dev(f, ap, bsrc, rows, kdim, n, engine, fold_period, base, eng_ws, cp, s,
+                               i > 0 ? REUSE_B_READY : 0);
         }
         done_c[i] = event();
         cudaEventRecord(done_c[i], s);

@@ -61,9 +61,12 @@ struct ConvArgs {
     uint64_t per0;       // k * ma * mb at depth 0
     uint32_t c;          // (-q) mod p
     double invp, bound, pd;
-    uint32_t* mu;        // [batch][nout][nd+1] digits mod p
+    uint32_t* mu;        // [segs][batch][nout][nd+1] digits mod p (one slab per inner segment)
     unsigned int* flag;  // validate: set when a value exceeds the top digit
     int validate;
+    int segs;            // inner-dimension segments (split-K): slab s holds the partial sums of segment s
+    uint32_t magic;      // small_magic(p) when small_p
+    int small_p;         // p^3 < 2^32: (u + c u') mod p by one 32-bit reciprocal multiply
 };
 
 QADIC_D uint64_t chunk_of(const ConvArgs& A, int64_t pair) {
@@ -91,7 +94,15 @@ QADIC_D void redq_digits(uint64_t r, const ConvArgs& A, F emit) {
     uint32_t u_next = 0;
     for (int i = A.nd; i >= 0; --i) {
         const uint32_t u = (uint32_t)(r >> (i * A.t)) - A.p * (uint32_t)(s >> (i * A.t));
-        const uint32_t mu = i == A.nd ? u : (uint32_t)mod_p53((uint64_t)u + (uint64_t)A.c * u_next, A);
+        uint32_t mu = u;
+        if (i != A.nd) {
+            if (A.small_p) {  // x < p^2 + p and p^3 < 2^32: the 32-bit reciprocal quotient is exact
+                const uint32_t x = u + A.c * u_next;
+                mu = x - A.p * __umulhi(x, A.magic);
+            } else {
+                mu = (uint32_t)mod_p53((uint64_t)u + (uint64_t)A.c * u_next, A);
+            }
+        }
         u_next = u;
         emit(i, mu);
     }
@@ -117,10 +128,10 @@ template <>
 QADIC_D void mac<uint64_t>(uint64_t& acc, uint64_t x, uint64_t y) { acc += x * y; }
 
 template <typename Acc>
-QADIC_D void store_digits(Acc v, int64_t pair, int64_t j, const ConvArgs& A) {
+QADIC_D void store_digits(Acc v, int64_t pair, int64_t j, const ConvArgs& A, int seg = 0) {
     const uint64_t r = as_u64(v);
     if (A.validate && (A.nd + 1) * A.t < 64 && (r >> ((A.nd + 1) * A.t))) atomicOr(A.flag, 1u);
-    uint32_t* dst = A.mu + (pair * A.nout + j) * (A.nd + 1);
+    uint32_t* dst = A.mu + (((int64_t)seg * A.batch + pair) * A.nout + j) * (A.nd + 1);
     redq_digits(r, A, [&](int i, uint32_t mu) { dst[i] = mu; });
 }
 
@@ -129,14 +140,21 @@ __global__ void __launch_bounds__(CT) conv_tile_kernel(ConvArgs A) {
     __shared__ Acc a_s[TI];
     __shared__ Acc b_s[BW_PAD];
     const int64_t tiles = (A.nout + TJ - 1) / TJ;
-    const int64_t pair = blockIdx.x / tiles;
-    const int64_t j0 = (blockIdx.x - pair * tiles) * TJ;
+    const int seg = (int)(blockIdx.x % A.segs);
+    const int64_t tile_id = blockIdx.x / A.segs;
+    const int64_t pair = tile_id / tiles;
+    const int64_t j0 = (tile_id - pair * tiles) * TJ;
     const uint64_t* ap = A.a + pair * A.na;
     const uint64_t* bp = A.b + pair * A.nb;
     const uint64_t chunk = chunk_of(A, pair);
-    // inner range touching this tile: i in [max(0, j0 - nb + 1), min(na, j0 + TJ))
-    const int64_t ilo = j0 - A.nb + 1 > 0 ? j0 - A.nb + 1 : 0;
-    const int64_t ihi = j0 + TJ < A.na ? j0 + TJ : A.na;
+    // inner range touching this tile: i in [max(0, j0 - nb + 1), min(na, j0 + TJ)), split
+    // into A.segs contiguous segments (whole staging rounds); this CTA sums segment `seg`
+    const int64_t tlo = j0 - A.nb + 1 > 0 ? j0 - A.nb + 1 : 0;
+    const int64_t thi = j0 + TJ < A.na ? j0 + TJ : A.na;
+    const int64_t rounds = (thi - tlo + TI - 1) / TI;
+    const int64_t per = (rounds + A.segs - 1) / A.segs;
+    const int64_t ilo = tlo + (int64_t)seg * per * TI;
+    const int64_t ihi = ilo + per * TI < thi ? ilo + per * TI : thi;
     Acc acc[CR];
 #pragma unroll
     for (int r = 0; r < CR; ++r) acc[r] = (Acc)0;
@@ -181,7 +199,7 @@ __global__ void __launch_bounds__(CT) conv_tile_kernel(ConvArgs A) {
 #pragma unroll
     for (int r = 0; r < CR; ++r) {
         const int64_t j = j0 + tj + r;
-        if (j < A.nout) store_digits(acc[r], pair, j, A);
+        if (j < A.nout) store_digits(acc[r], pair, j, A, seg);
     }
 }
 
@@ -211,9 +229,10 @@ __global__ void conv_direct_kernel(ConvArgs A) {
 // position at or beyond ncoef (up to (nout+1)k-1) is nonzero
 template <typename T>
 __global__ void overlap_kernel(const uint32_t* __restrict__ mu, int64_t batch, int64_t nout, int k, uint32_t p,
-                               int64_t ncoef, int64_t full, T* __restrict__ out, unsigned int* flag) {
+                               int64_t ncoef, int64_t full, T* __restrict__ out, unsigned int* flag, int segs) {
     const int nd = 2 * k - 2;
     const int64_t span = full > ncoef ? full : ncoef;
+    const int64_t slab = batch * nout * (nd + 1);
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < batch * span;
          g += (int64_t)gridDim.x * blockDim.x) {
         const int64_t pair = g / span, P = g - pair * span;
@@ -221,10 +240,12 @@ __global__ void overlap_kernel(const uint32_t* __restrict__ mu, int64_t batch, i
         if (P < full) {
             const int64_t j = P / k;
             const int r = (int)(P - j * k);
-            const uint32_t* m = mu + pair * nout * (nd + 1);
-            if (j < nout) v += m[j * (nd + 1) + r];
-            if (j >= 1 && r + k <= nd) v += m[(j - 1) * (nd + 1) + r + k];
-            if (v >= p) v -= p;
+            for (int sg = 0; sg < segs; ++sg) {  // partial sums of the inner segments, each < p
+                const uint32_t* m = mu + sg * slab + pair * nout * (nd + 1);
+                if (j < nout) v += m[j * (nd + 1) + r];
+                if (j >= 1 && r + k <= nd) v += m[(j - 1) * (nd + 1) + r + k];
+                v %= p;
+            }
         }
         if (P < ncoef) out[pair * ncoef + P] = (T)v;
         else if (v) atomicOr(flag, 2u);
@@ -404,7 +425,17 @@ int qadic_polymul_words_batch(const uint64_t* aw, int64_t na, const uint64_t* bw
     // ---- leaves: one batched convolution + REDQ ----
     const int64_t nout = n_a + n_b - 1;
     const int nd = 2 * d;
-    uint32_t* mu = static_cast<uint32_t*>(alloc((size_t)B * nout * (nd + 1) * 4));
+    const bool tiled = n_a >= 64;
+    // split-K: enough CTAs for ~8 per SM, each segment at least one staging round
+    int segs = 1;
+    if (tiled) {
+        const int64_t tiles = B * ((nout + TJ - 1) / TJ);
+        const int64_t want = (int64_t)num_sms_cached() * 8;
+        const int64_t max_rounds = std::min<int64_t>(n_a, TJ + n_b - 1) / TI + 1;
+        if (tiles < want) segs = (int)std::min<int64_t>({(want + tiles - 1) / tiles, max_rounds, 64});
+        if (segs < 1) segs = 1;
+    }
+    uint32_t* mu = static_cast<uint32_t*>(alloc((size_t)segs * B * nout * (nd + 1) * 4));
     if (!mu) {
         release();
         QADIC_REQUIRE(false, QADIC_ERR_CUDA, "polymul scratch allocation failed");
@@ -430,9 +461,11 @@ int qadic_polymul_words_batch(const uint64_t* aw, int64_t na, const uint64_t* bw
     A.mu = mu;
     A.flag = flag;
     A.validate = validate;
-    const bool tiled = n_a >= 64;
+    A.segs = segs;
+    A.small_p = (uint64_t)p * p * p < (1ull << 32);
+    A.magic = small_magic((uint32_t)p);
     if (tiled) {
-        const int64_t grid = B * ((nout + TJ - 1) / TJ);
+        const int64_t grid = B * ((nout + TJ - 1) / TJ) * segs;
         QADIC_REQUIRE(grid < (1ll << 31), QADIC_ERR_UNSUPPORTED, "batch too large for one launch");
         if (f64) QADIC_TIMED("polymul conv", s, conv_tile_kernel<double><<<(unsigned)grid, CT, 0, s>>>(A));
         else QADIC_TIMED("polymul conv", s, conv_tile_kernel<uint64_t><<<(unsigned)grid, CT, 0, s>>>(A));
@@ -465,17 +498,17 @@ int qadic_polymul_words_batch(const uint64_t* aw, int64_t na, const uint64_t* bw
         const int64_t full = coeff_len(nout, k);
         if (out_u8)
             QADIC_TIMED("polymul overlap", s, overlap_kernel<uint8_t><<<grid_for(B * std::max(full, ncoef)), 256, 0, s>>>(
-                mu, B, nout, k, (uint32_t)p, ncoef, full, static_cast<uint8_t*>(out), flag));
+                mu, B, nout, k, (uint32_t)p, ncoef, full, static_cast<uint8_t*>(out), flag, segs));
         else
             QADIC_TIMED("polymul overlap", s, overlap_kernel<int64_t><<<grid_for(B * std::max(full, ncoef)), 256, 0, s>>>(
-                mu, B, nout, k, (uint32_t)p, ncoef, full, static_cast<int64_t*>(out), flag));
+                mu, B, nout, k, (uint32_t)p, ncoef, full, static_cast<int64_t*>(out), flag, segs));
     } else {
         int64_t lc = coeff_len(nout, k);
         uint32_t* cur = static_cast<uint32_t*>(alloc((size_t)B * lc * 4));
         if (!cur) rc = QADIC_ERR_CUDA;
         if (rc == QADIC_OK)
             QADIC_TIMED("polymul overlap", s, overlap_kernel<uint32_t><<<grid_for(B * lc), 256, 0, s>>>(
-                mu, B, nout, k, (uint32_t)p, lc, lc, cur, flag));
+                mu, B, nout, k, (uint32_t)p, lc, lc, cur, flag, segs));
         for (int li = (int)levels.size() - 1; li >= 0 && rc == QADIC_OK; --li) {
             const Level& Lv = levels[li];
             const int64_t lp = coeff_len(2 * Lv.n - 1, k);

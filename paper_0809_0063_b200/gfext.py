@@ -426,14 +426,20 @@ class GFqField:
         (polymul.py:159-167) rounded down to the DMMA k-step of 4."""
         return (chunk_budget(self.params, self.p - 1, self.p - 1) // 4) * 4
 
-    def matmul_coeffs(self, a, b, engine: str = "auto", fold_period: Optional[int] = None, out=None):
+    def matmul_coeffs(self, a, b, engine: str = "auto", fold_period: Optional[int] = None, out=None,
+                      col_panel: Optional[int] = None):
         """Coefficient-plane product uint8 [M, K, k] x [K, N, k] -> [M, N, k].
 
         Exact for any K the chosen engine can hold: "i8" (default) while
         K*k*(p-1)^2 < 2^31; "f64" within the dot bound, or beyond it with an
         in-register REDQ fold every `fold_period` inner terms (default: the
         largest multiple of 4 within the accumulation budget), i.e. the
-        K-chunked GFqField.matmul of SURVEY.md 8(b)."""
+        K-chunked GFqField.matmul of SURVEY.md 8(b).
+
+        col_panel: index of this call in a sweep of B's column panels against
+        the same device A on the current stream (the multi-GPU row-block step):
+        the fp4k engine converts A to evaluation planes on panel 0 only and
+        keeps them in the stream's workspace for the later panels."""
         if not self.coeff_engines_ok:  # word path through handles (p <= 255, K <= n_max)
             da, ha = N.to_dev(a, np.uint8)
             db, hb = N.to_dev(b, np.uint8)
@@ -464,8 +470,9 @@ class GFqField:
         ws_bytes = N.lib().qadic_gf_matmul_workspace(desc, m, kd, n, eng)
         ws = N.workspace(ws_bytes)
         dev = N.out_buffer(out, (m, n, self.k), np.uint8)
-        N.check(N.lib().qadic_gf_matmul_u8(desc, N.ptr(da), N.ptr(db), m, kd, n, eng, fold, N.ptr(ws), ws_bytes,
-                                           N.ptr(dev), N.stream_ptr()), DimensionMismatch)
+        flags = 0 if col_panel is None else (N.ENGINE_FLAG_COL_PANEL if col_panel == 0 else N.ENGINE_FLAG_A_READY)
+        N.check(N.lib().qadic_gf_matmul_u8(desc, N.ptr(da), N.ptr(db), m, kd, n, eng | flags, fold, N.ptr(ws),
+                                           ws_bytes, N.ptr(dev), N.stream_ptr()), DimensionMismatch)
         return N.finish(dev, out, ha or hb, np.uint8)
 
     def _matmul_host(self, a, b, engine, fold_period, out, panel_rows: int = 0):

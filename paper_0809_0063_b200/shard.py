@@ -141,7 +141,8 @@ class RowBlockStep:
     b_panels: B's column panels, allocated on every rank and filled on `src`
     (the other ranks' contents are overwritten by the broadcast every step).
     c_panels: this rank's output blocks, c_panels[j] = A[rows_r] @ b_panels[j].
-    compute(a_rows, b_panel, out): the local product (writes `out`).
+    compute(a_rows, b_panel, out, j): the local product of panel j (writes
+    `out`; j lets the engine keep A's converted operand across the sweep).
 
     On CUDA tensors the broadcasts run on a dedicated stream (NCCL async ops,
     one event per panel) and the compute stream waits on each panel's event
@@ -177,7 +178,7 @@ class RowBlockStep:
                     self.stage(j)
                 if dist is not None and self.world > 1:
                     dist.broadcast(bp, src=self.src, group=self.group)
-                self.compute(self.a_rows, bp, cp)
+                self.compute(self.a_rows, bp, cp, j)
             return self.c_panels
         import torch
 
@@ -193,9 +194,9 @@ class RowBlockStep:
                 ev = torch.cuda.Event()
                 ev.record(self.comm)
                 events.append(ev)
-        for ev, bp, cp in zip(events, self.b_panels, self.c_panels):
+        for j, (ev, bp, cp) in enumerate(zip(events, self.b_panels, self.c_panels)):
             cur.wait_event(ev)
-            self.compute(self.a_rows, bp, cp)
+            self.compute(self.a_rows, bp, cp, j)
         return self.c_panels
 
 

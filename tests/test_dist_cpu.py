@@ -84,7 +84,7 @@ def _worker(rank, world, port, kind, result_q):
                 b_panels = [torch.zeros((kd, j1 - j0, 3), dtype=torch.uint8) for j0, j1 in bounds]
             c_panels = [torch.zeros((r1 - r0, j1 - j0, 3), dtype=torch.uint8) for j0, j1 in bounds]
 
-            def compute(ar, bp, cp):
+            def compute(ar, bp, cp, j=0):
                 cp.copy_(torch.from_numpy(O.gf_matmul_folded(f, ar.numpy(), bp.numpy(), 9)))
 
             stepper = shard.RowBlockStep(torch.from_numpy(x["a"][r0:r1]), b_panels, c_panels, compute)
@@ -106,7 +106,7 @@ def _worker(rank, world, port, kind, result_q):
                 [torch.zeros((n, j1 - j0), dtype=torch.uint8) for j0, j1 in bounds]
             c_panels = [torch.zeros((r1 - r0, j1 - j0), dtype=torch.uint8) for j0, j1 in bounds]
 
-            def compute(ar, bp, cp):
+            def compute(ar, bp, cp, j=0):
                 cp.copy_(torch.from_numpy(O.right_cmm(ar.numpy(), bp.numpy(), 3, 17, 2)))
 
             shard.RowBlockStep(torch.from_numpy(a[r0:r1]), b_panels, c_panels, compute)()
