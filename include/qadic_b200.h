@@ -198,7 +198,8 @@ QADIC_API int qadic_index_of_coeffs(const uint8_t *c, int64_t n, int32_t k, int3
  * out_u8, else int64).  algo 0 = classical, 1 = Karatsuba (breadth-first levels
  * while n > threshold words).  stats (optional, host): the schedule's word
  * products and reductions; flags bit 0 = a value beyond the top digit (validate),
- * bit 1 = a nonzero coefficient at or beyond ncoef.  Synchronous.
+ * bit 1 = a nonzero coefficient at or beyond ncoef.  Asynchronous on `stream`
+ * unless stats is given (the flags are read back: synchronous).
  * ------------------------------------------------------------------------- */
 typedef struct qadic_polymul_stats {
     int64_t word_muls;

@@ -81,6 +81,19 @@ int check_launch(const char* what, int launched) {
     return QADIC_OK;
 }
 
+void keep_mempool() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    static std::atomic<bool> kept[64];
+    if (kept[dev & 63].exchange(true)) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+}
+
 int num_sms_cached() {
     static int cache[64] = {0};
     int dev = 0;

@@ -2438,16 +2438,7 @@ int tc_matmul_u64(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_t m, 
     constexpr int64_t KC = 16384;  // 4 * KC * 255^2 < 2^32
     int dev = 0;
     cudaGetDevice(&dev);
-    // keep freed blocks in the stream-ordered pool across calls (once per device)
-    static std::atomic<bool> pool_kept[64];
-    if (!pool_kept[dev & 63].exchange(true)) {
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t keep = ~0ull;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-        }
-        cudaGetLastError();
-    }
+    keep_mempool();
     // pinned landing slot for the operands' OR: one per host thread and device, so
     // concurrent callers never read each other's significant-byte counts
     thread_local unsigned long long* host_or_slot[64] = {};

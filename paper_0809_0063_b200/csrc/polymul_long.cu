@@ -160,39 +160,58 @@ __global__ void __launch_bounds__(CT) conv_tile_kernel(ConvArgs A) {
     for (int r = 0; r < CR; ++r) acc[r] = (Acc)0;
     uint64_t since = 0;  // inner steps since the last fold (>= terms added to any accumulator)
     const int tj = threadIdx.x * CR;
+    // b_s[bpad(x + 1)] = b[bbase + x]; b_s[0] = 0 stands for the one index (-1) the
+    // last slide of thread 0 reads.  a_s is zero padded to TI: every round runs TI
+    // unconditional steps (zero terms only count towards the fold budget).
+    if (threadIdx.x == 0) b_s[0] = (Acc)0;
+    const bool block_fold = chunk >= CR;  // fold decisions once per CR steps
     for (int64_t i0 = ilo; i0 < ihi; i0 += TI) {
         const int cnt = (int)(ihi - i0 < TI ? ihi - i0 : TI);
         __syncthreads();
         for (int x = threadIdx.x; x < TI; x += CT) a_s[x] = x < cnt ? (Acc)ap[i0 + x] : (Acc)0;
-        // b window: b_s[x] = b[j0 - i0 - (TI - 1) + x]
         const int64_t bbase = j0 - i0 - (TI - 1);
         for (int x = threadIdx.x; x < BW; x += CT) {
             const int64_t bi = bbase + x;
-            b_s[bpad(x)] = (bi >= 0 && bi < A.nb) ? (Acc)bp[bi] : (Acc)0;
+            b_s[bpad(x + 1)] = (bi >= 0 && bi < A.nb) ? (Acc)bp[bi] : (Acc)0;
         }
         __syncthreads();
-        // thread's outputs j = j0 + tj + r; term (ii, r) uses b_s[tj + r + TI - 1 - ii]
+        // thread's outputs j = j0 + tj + r; term (ii, r) uses b[bbase + tj + r + TI - 1 - ii]:
+        // logical r lives in register slot (r - ii) mod CR, so a step loads one new value
         Acc w[CR];
 #pragma unroll
-        for (int r = 0; r < CR; ++r) w[r] = b_s[bpad(tj + r + TI - 1)];
-        for (int ii0 = 0; ii0 < cnt; ii0 += CR) {
+        for (int r = 0; r < CR; ++r) w[r] = b_s[bpad(tj + r + TI)];
+        if (block_fold) {
+#pragma unroll 1
+            for (int ii0 = 0; ii0 < TI; ii0 += CR) {
+                if (since + CR > chunk) {
 #pragma unroll
-            for (int u = 0; u < CR; ++u) {
-                const int ii = ii0 + u;
-                if (ii < cnt) {
-                    const Acc av = a_s[ii];
+                    for (int r = 0; r < CR; ++r) fold(acc[r], A);
+                    since = 0;
+                }
+#pragma unroll
+                for (int u = 0; u < CR; ++u) {
+                    const Acc av = a_s[ii0 + u];
 #pragma unroll
                     for (int r = 0; r < CR; ++r) mac<Acc>(acc[r], av, w[(r - u + CR) % CR]);
-                    if (++since == chunk && i0 + ii + 1 < ihi) {
+                    w[(CR - 1 - u + CR) % CR] = b_s[bpad(tj + TI - 1 - ii0 - u)];
+                }
+                since += CR;
+            }
+        } else {
+#pragma unroll 1
+            for (int ii0 = 0; ii0 < TI; ii0 += CR) {
+#pragma unroll
+                for (int u = 0; u < CR; ++u) {
+                    const Acc av = a_s[ii0 + u];
+#pragma unroll
+                    for (int r = 0; r < CR; ++r) mac<Acc>(acc[r], av, w[(r - u + CR) % CR]);
+                    if (++since == chunk) {
 #pragma unroll
                         for (int r = 0; r < CR; ++r) fold(acc[r], A);
                         since = 0;
                     }
+                    w[(CR - 1 - u + CR) % CR] = b_s[bpad(tj + TI - 1 - ii0 - u)];
                 }
-                // slide: the next step needs b_s[tj + r + TI - 2 - ii]; the register that
-                // held r = CR-1 takes the new r = 0 value
-                const int nx = tj + TI - 2 - ii;
-                w[(CR - 1 - u + CR) % CR] = nx >= 0 ? b_s[bpad(nx)] : (Acc)0;
             }
         }
     }
@@ -346,6 +365,7 @@ int qadic_polymul_words_batch(const uint64_t* aw, int64_t na, const uint64_t* bw
     if (stats) *stats = qadic_polymul_stats{0, 0, 0, 0, 0};
     if (batch == 0) return QADIC_OK;
 
+    keep_mempool();
     std::vector<void*> allocs;
     auto alloc = [&](size_t bytes) -> void* {
         void* ptr = nullptr;
@@ -430,9 +450,10 @@ int qadic_polymul_words_batch(const uint64_t* aw, int64_t na, const uint64_t* bw
     int segs = 1;
     if (tiled) {
         const int64_t tiles = B * ((nout + TJ - 1) / TJ);
+        // one full wave: 8 resident CTAs per SM (64 registers, 14 KB smem)
         const int64_t want = (int64_t)num_sms_cached() * 8;
         const int64_t max_rounds = std::min<int64_t>(n_a, TJ + n_b - 1) / TI + 1;
-        if (tiles < want) segs = (int)std::min<int64_t>({(want + tiles - 1) / tiles, max_rounds, 64});
+        if (tiles < want) segs = (int)std::min<int64_t>({want / tiles, max_rounds, 64});
         if (segs < 1) segs = 1;
     }
     uint32_t* mu = static_cast<uint32_t*>(alloc((size_t)segs * B * nout * (nd + 1) * 4));
@@ -531,19 +552,30 @@ int qadic_polymul_words_batch(const uint64_t* aw, int64_t na, const uint64_t* bw
                     cur, batch, lc, ncoef, static_cast<int64_t*>(out), flag));
         }
     }
-    unsigned int hflag = 0;
+    // the flags come back only when asked for (stats): without them the call stays
+    // asynchronous on the stream
+    unsigned int* hflag = nullptr;
     if (rc == QADIC_OK) {
         rc = check_launch("polymul_words_batch");
-        cudaMemcpyAsync(&hflag, flag, sizeof(hflag), cudaMemcpyDeviceToHost, s);
+        if (stats) {
+            static thread_local unsigned int* slot = nullptr;
+            if (!slot && cudaHostAlloc(reinterpret_cast<void**>(&slot), sizeof(unsigned int), cudaHostAllocDefault) !=
+                             cudaSuccess)
+                slot = nullptr;
+            hflag = slot;
+            if (hflag) cudaMemcpyAsync(hflag, flag, sizeof(unsigned int), cudaMemcpyDeviceToHost, s);
+        }
     }
     release();
     if (rc != QADIC_OK) {
         set_error(rc, "polymul_words_batch: %s", rc == QADIC_ERR_CUDA ? "allocation or launch failure" : "failed");
         return rc;
     }
-    QADIC_REQUIRE(cudaStreamSynchronize(s) == cudaSuccess, QADIC_ERR_CUDA, "polymul_words_batch: %s",
-                  cudaGetErrorString(cudaGetLastError()));
-    if (stats) stats->flags = hflag;
+    if (stats) {
+        QADIC_REQUIRE(hflag && cudaStreamSynchronize(s) == cudaSuccess, QADIC_ERR_CUDA, "polymul_words_batch: %s",
+                      cudaGetErrorString(cudaGetLastError()));
+        stats->flags = *hflag;
+    }
     return QADIC_OK;
 }
 

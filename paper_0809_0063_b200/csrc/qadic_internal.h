@@ -18,6 +18,9 @@ double host_reciprocal_up(int64_t p);
 double host_case2_bound();
 
 void set_error(int code, const char* fmt, ...);
+// keep the current device's stream-ordered pool from returning freed blocks to the
+// OS at every synchronisation (cudaMallocAsync scratch reused across calls)
+void keep_mempool();
 // multiprocessor count of the current device (cached per device)
 int num_sms_cached();
 // `launched`: kernels this call site launched outside QADIC_TIMED (those count themselves)

@@ -15,7 +15,7 @@ sys.path.insert(0, ROOT)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--config", default="5", help="1..5, or polylong / polylong3")
     ap.add_argument("--engine", default="auto")
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--scale", type=int, default=1, help="divide every dimension")
@@ -25,7 +25,21 @@ def main():
     import paper_0809_0063_b200 as Q
     from paper_0809_0063_b200 import workloads as W
 
-    c = W.CONFIGS[args.config]
+    if args.config.startswith("polylong"):
+        import numpy as np
+
+        from paper_0809_0063_b200.params import fqt_params
+
+        prm = fqt_params(3, 3 if args.config == "polylong3" else 1)
+        g = np.random.default_rng(7)
+        a = torch.from_numpy(g.integers(0, 3, (16, 16384 // args.scale), dtype=np.uint8)).cuda()
+        b = torch.from_numpy(g.integers(0, 3, (16, 16384 // args.scale), dtype=np.uint8)).cuda()
+        for _ in range(args.reps):
+            Q.polymul.polymul_fqt_long_batch(a, b, prm)
+        torch.cuda.synchronize()
+        print("ok")
+        return
+    c = W.CONFIGS[int(args.config)]
     shape = W.scaled_shape(c, args.scale)
     x = {k: torch.from_numpy(v).cuda() for k, v in W.make_inputs(c, shape).items()}
     for _ in range(args.reps):
