@@ -628,6 +628,52 @@ def measure_variants(args, cfg, engine, meta, units, work, peaks, peak_src, torc
     return out
 
 
+def copy_ceiling(cfg, ws, torch, N, K=2000, sets=16):
+    """The hand-written same-size copy kernel (qadic_diag_copy: out = a ^ b over
+    16-byte vectors, one balanced wave, programmatic dependent launch -- the
+    batched kernels' launch shape) in the same CUDA-graph harness as the
+    headline: the ceiling a ~16 MB single-wave call can reach on this box
+    (tools/small_copy_floor.py sweeps its shapes; 2 vectors per thread, 128-thread
+    blocks measured best for both)."""
+    from paper_0809_0063_b200 import workloads as W
+
+    c = W.CONFIGS[cfg]
+    w = W.work_units(c, (c.shape[0] // ws,) + tuple(c.shape[1:]))
+    if cfg == 1:
+        in_b, out_b = w["unit_count"] * c.k, w["unit_count"] * (2 * c.k - 1)
+    else:
+        in_b, out_b = w["io_bytes"] // 2 // 16 * 16, c.shape[0] // ws * c.k
+    in_b, out_b = in_b // 16 * 16, out_b // 16 * 16
+    L = N.lib()
+    ins = [(torch.randint(0, 255, (in_b,), dtype=torch.uint8, device="cuda"),
+            torch.randint(0, 255, (in_b,), dtype=torch.uint8, device="cuda")) for _ in range(sets)]
+    outs = [torch.empty(out_b, dtype=torch.uint8, device="cuda") for _ in range(sets)]
+
+    def st(i):
+        a, b = ins[i % sets]
+        N.check(L.qadic_diag_copy(a.data_ptr(), b.data_ptr(), in_b, outs[i % sets].data_ptr(), out_b, 2, 128,
+                                  N.stream_ptr()))
+
+    for i in range(3):
+        st(i)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(K):
+            st(i)
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    g.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / K
+    del ins, outs, g
+    return {"kernel": "qadic_diag_copy (out = a ^ b, 16-byte vectors, 2 per thread, 128-thread blocks, PDL)",
+            "bytes_per_call": 2 * in_b + out_b, "us": round(ms * 1e3, 3),
+            "gbs": round((2 * in_b + out_b) / (ms / 1e3) / 1e9, 1)}
+
+
 def sustained_and_burst(step, args, ms_main, torch, graphed, cfg):
     """The headline pass is either a short burst or a long sustained run; time
     the other one too (the board's power management lowers clocks over a long
@@ -842,6 +888,11 @@ def run_ours(args):
     if meta.get("broadcast_bytes_per_step"):
         line["broadcast"] = {"bytes_per_step": int(meta["broadcast_bytes_per_step"]), "panels": args.panels,
                              "inside_timed_step": True, "collective": "ncclBroadcast (torch.distributed)"}
+    if cfg in (1, 2) and roof is not None and not args.no_probe:
+        cc = copy_ceiling(cfg, ws, torch, N)
+        cc["frac_of_hbm"] = round(cc["gbs"] / roof["peak"], 4)
+        cc["kernel_frac_of_ceiling"] = round(roof["achieved"] / cc["gbs"], 4)
+        roof["copy_ceiling"] = cc
     if ws == 1 and not args.no_sustained:
         line["sustained_vs_burst"] = sustained_and_burst(step, args, ms, torch, graph is not None, cfg)
     if ws == 1 and not args.no_redq_line and cfg in (3, 4, 5):

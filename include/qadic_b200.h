@@ -300,6 +300,12 @@ QADIC_API int qadic_fdiv_native_check(const int64_t *r, int64_t per_p, const int
  *   data 0: zero operands, 1: residue-like operands (what the engines feed), 2: random bits
  * ------------------------------------------------------------------------- */
 QADIC_API int qadic_diag_pipe_peak(int32_t kind, int32_t data, int64_t iters, double *ops, float *ms, void *stream);
+/* Same-size copy ceiling of the single-wave batched kernels: out = a ^ b over
+ * 16-byte vectors (two input streams of in_bytes, one output stream of out_bytes
+ * <= 2 in_bytes), per_thread vectors of each input per thread (1, 2, 4, 8), one
+ * launch with programmatic dependent launch like the cfg1 / cfg2 kernels. */
+QADIC_API int qadic_diag_copy(const void *a, const void *b, int64_t in_bytes, void *out, int64_t out_bytes,
+                              int32_t per_thread, int32_t threads, void *stream);
 
 #ifdef __cplusplus
 }

@@ -10,6 +10,8 @@
 //
 // Both read uint8 coefficients with 128-bit loads and never touch the
 // packed words in HBM: DQT packing happens in registers.
+#include <cstdlib>
+
 #include "qadic_common.cuh"
 #include "qadic_internal.h"
 
@@ -268,7 +270,15 @@ __global__ void __launch_bounds__(GD_THREADS, NARROW ? 8 : 1) gf_dot_kernel(cons
                 digit_sums_word<K>(x.z, y.z, S);
                 digit_sums_word<K>(x.w, y.w, S);
             };
-            // every load of a lane issued before the first use (cfg2: 2 chunks per operand)
+            if constexpr (NARROW) {  // short rows: at most 2 chunks per lane (host-checked), no loop
+                const uint4 z = make_uint4(0, 0, 0, 0);
+                const uint4 x0 = lane < nchunks ? __ldg(c1 + lane) : z, y0 = lane < nchunks ? __ldg(c2 + lane) : z;
+                const uint4 x1 = lane + G < nchunks ? __ldg(c1 + lane + G) : z;
+                const uint4 y1 = lane + G < nchunks ? __ldg(c2 + lane + G) : z;
+                body(x0, y0);
+                body(x1, y1);
+            } else {
+            // every load of a lane issued before the first use
             int64_t ch = lane;
             for (; ch + 3 * G < nchunks; ch += 4 * G) {
                 uint4 x[4], y[4];
@@ -287,6 +297,7 @@ __global__ void __launch_bounds__(GD_THREADS, NARROW ? 8 : 1) gf_dot_kernel(cons
                 ch += 2 * G;
             }
             if (ch < nchunks) body(__ldg(c1 + ch), __ldg(c2 + ch));
+            }
             if constexpr (K == 2) S[0] -= S[2];
             // the packed word: every S_j < q (host-checked), so r < q^(2K-1) <= 2^53
 #pragma unroll
@@ -310,7 +321,7 @@ __global__ void __launch_bounds__(GD_THREADS, NARROW ? 8 : 1) gf_dot_kernel(cons
     extern __shared__ uint32_t gd_tab[];
     const uint32_t* ltab = f.l_table;
     const uint32_t* htab = f.h_table;
-    if (tab_smem > 0) {
+    if (tab_smem > 0) {  // (tab_smem == 0: tiny tables are read through L1 directly -- no barrier)
         for (int i = threadIdx.x; i < tab_smem; i += blockDim.x) {
             gd_tab[i] = __ldg(f.l_table + i);
             gd_tab[tab_smem + i] = __ldg(f.h_table + i);
@@ -319,8 +330,8 @@ __global__ void __launch_bounds__(GD_THREADS, NARROW ? 8 : 1) gf_dot_kernel(cons
         ltab = gd_tab;
         htab = gd_tab + tab_smem;
     }
-    if (!live || lane != 0) return;
     constexpr int ND = 2 * K - 2;
+    if (!live || lane != 0) return;
     uint32_t u[ND + 1];
     redq_compress_f64<ND>((double)acc, f.invp_up, (double)f.p, f.bound, f.p, t, u);
     uint32_t li = 0, hi = 0;
@@ -347,7 +358,10 @@ static void launch_gf_dot(const uint8_t* v1, const uint8_t* v2, int64_t batch, i
     const bool vec = (4 % K == 0) && ((len * K) % 16 == 0) && ((uintptr_t)v1 % 16 == 0) &&
                      ((uintptr_t)v2 % 16 == 0) && f.t <= 32;
     const int entries = 1 << (f.bb * K);
-    const int ntab = entries <= 2048 ? entries : 0;  // <= 16 KB of tables: shared memory
+    // 256 < entries <= 2048 (<= 16 KB of tables): staged in shared memory; tiny tables
+    // (cfg2: 16 entries) stay in L1 -- no staging loop, no block barrier in the tail
+    static const int tiny = getenv("QADIC_GD_TINY") ? atoi(getenv("QADIC_GD_TINY")) : 256;
+    const int ntab = (entries <= 2048 && entries > tiny) ? entries : 0;
     const size_t smem = (size_t)ntab * 2 * sizeof(uint32_t);
     if (vec) {
         // 4 lanes per dot.  Short rows (cfg2: 8 chunks, 2 per lane) use the narrow
@@ -355,6 +369,8 @@ static void launch_gf_dot(const uint8_t* v1, const uint8_t* v2, int64_t batch, i
         // wave (the 48-register variant ran 1.4 waves: 5.14 vs 4.97 us).  The block
         // width is trimmed to spread the batch evenly over the resident slots.
         const int64_t nchunks = len * K / 16;
+        static const int max_width = getenv("QADIC_GD_WIDTH") ? atoi(getenv("QADIC_GD_WIDTH")) : GD_THREADS;
+        static const int lanes = getenv("QADIC_GD_LANES") ? atoi(getenv("QADIC_GD_LANES")) : 4;
         auto go = [&](auto kern, int G) {
             static int occ = 0;
             if (!occ) {
@@ -364,12 +380,13 @@ static void launch_gf_dot(const uint8_t* v1, const uint8_t* v2, int64_t batch, i
             const int64_t threads_total = batch * G, per_wave = (int64_t)occ * num_sms_cached();
             int64_t width = (threads_total + per_wave - 1) / per_wave;
             width = (width + 31) / 32 * 32;
-            if (width > GD_THREADS) width = GD_THREADS;
+            if (width > max_width) width = max_width;
             if (width < 64) width = 64;
             const unsigned blocks = (unsigned)((threads_total + width - 1) / width);
             launch_pdl(kern, dim3(blocks), dim3((unsigned)width), smem, s, v1, v2, batch, len, f, ntab, out);
         };
-        if (nchunks <= 3 * 4) go(gf_dot_kernel<K, 4, (4 % K == 0), true>, 4);
+        if (lanes == 8 && nchunks <= 2 * 8) go(gf_dot_kernel<K, 8, (4 % K == 0), true>, 8);
+        else if (nchunks <= 2 * 4) go(gf_dot_kernel<K, 4, (4 % K == 0), true>, 4);
         else go(gf_dot_kernel<K, 4, (4 % K == 0), false>, 4);
     } else {
         constexpr int G = 8;

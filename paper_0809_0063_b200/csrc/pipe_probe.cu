@@ -201,3 +201,61 @@ extern "C" QADIC_API int qadic_diag_pipe_peak(int32_t kind, int32_t data, int64_
     *ms = t;
     return QADIC_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Same-size copy ceiling for the single-wave batched kernels (diagnostics): out
+// = a ^ b over 16-byte vectors -- the cfg1 / cfg2 traffic shape (two input
+// streams, one output stream, no arithmetic worth the name), launched like
+// those kernels (one balanced wave, programmatic dependent launch), so a CUDA
+// graph of back-to-back calls measures what a call of that size can reach.
+// ---------------------------------------------------------------------------
+namespace qadic {
+namespace probe {
+template <int V>
+__global__ void copy_like_kernel(const uint4* __restrict__ a, const uint4* __restrict__ b, int64_t n_in,
+                                 uint4* __restrict__ out, int64_t n_out) {
+    pdl_wait();
+    pdl_trigger();
+    const int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * V;
+    uint4 x[V], y[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        x[v] = j0 + v < n_in ? __ldg(a + j0 + v) : make_uint4(0, 0, 0, 0);
+        y[v] = j0 + v < n_in ? __ldg(b + j0 + v) : make_uint4(0, 0, 0, 0);
+    }
+    // the output stream is n_out / n_in of the input: thread j writes its share
+    const int64_t o0 = j0 * n_out / n_in, o1 = (j0 + V) * n_out / n_in;
+#pragma unroll
+    for (int v = 0; v < 2 * V; ++v) {
+        const uint4 p = x[v % V], q = y[(v + 1) % V];
+        if (o0 + v < o1 && o0 + v < n_out) out[o0 + v] = make_uint4(p.x ^ q.x, p.y ^ q.y, p.z ^ q.z, p.w ^ q.w);
+    }
+}
+}  // namespace probe
+}  // namespace qadic
+
+extern "C" QADIC_API int qadic_diag_copy(const void* a, const void* b, int64_t in_bytes, void* out, int64_t out_bytes,
+                                         int32_t per_thread, int32_t threads, void* stream) {
+    using namespace qadic;
+    using namespace qadic::probe;
+    if (in_bytes % 16 || out_bytes % 16 || out_bytes > 2 * in_bytes || threads < 32 || threads > 1024 ||
+        !(per_thread == 1 || per_thread == 2 || per_thread == 4 || per_thread == 8)) {
+        set_error(QADIC_ERR_VALUE, "diag_copy: bad geometry");
+        return QADIC_ERR_VALUE;
+    }
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int64_t n_in = in_bytes / 16, n_out = out_bytes / 16;
+    const unsigned blocks = (unsigned)((n_in + (int64_t)threads * per_thread - 1) / ((int64_t)threads * per_thread));
+    const uint4* pa = static_cast<const uint4*>(a);
+    const uint4* pb = static_cast<const uint4*>(b);
+    uint4* po = static_cast<uint4*>(out);
+    cudaError_t e;
+    switch (per_thread) {
+        case 1: e = launch_pdl(copy_like_kernel<1>, dim3(blocks), dim3(threads), 0, s, pa, pb, n_in, po, n_out); break;
+        case 2: e = launch_pdl(copy_like_kernel<2>, dim3(blocks), dim3(threads), 0, s, pa, pb, n_in, po, n_out); break;
+        case 4: e = launch_pdl(copy_like_kernel<4>, dim3(blocks), dim3(threads), 0, s, pa, pb, n_in, po, n_out); break;
+        default: e = launch_pdl(copy_like_kernel<8>, dim3(blocks), dim3(threads), 0, s, pa, pb, n_in, po, n_out); break;
+    }
+    (void)e;
+    return check_launch("diag_copy", 1);
+}
