@@ -252,6 +252,15 @@ QADIC_API int qadic_extract_middle(const uint64_t *acc, int64_t n, int64_t p, in
  * scattered to out[m, n] (cmm.py:349-359) */
 QADIC_API int qadic_full_cmm_reduce(const uint64_t *acc, int64_t mw, int64_t nw, int64_t p, int32_t t, int32_t dq,
                                     int32_t dth, int64_t m, int64_t n, int64_t *out, void *stream);
+/* Tabulated correction over a batch (build_correction_table / correct_tabulated,
+ * redq.py:194-300): digits of words[i] (REDQ-compressed at radix 2^t) -- or the
+ * given compressed digits[i, 0..d] -- corrected by overlapping width-j block
+ * lookups in `table` (entries packed ceil(log2 p) bits per residue; base_p != 0:
+ * index sum u_i p^i, else the bit-block index); out[n, d+1].  Give exactly one of
+ * words / digits. */
+QADIC_API int qadic_redq_tabulated(const uint64_t *words, const uint64_t *digits, int64_t n, int64_t p, int32_t t,
+                                   int32_t d, const uint64_t *table, int64_t table_entries, int32_t j,
+                                   int32_t base_p, uint64_t *out, void *stream);
 /* correct_digits_array (redq.py:308-315): mu_i = (u_i + c u_{i+1}) mod p (uint64 wrap),
  * c = (p - q mod p) mod p, top digit kept; identity when q mod p == 0 */
 QADIC_API int qadic_correct_digits(const uint64_t *u, int64_t n, int32_t width, int64_t p, int64_t q_mod_p,

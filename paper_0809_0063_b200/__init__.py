@@ -19,7 +19,7 @@ Additive batched APIs the benchmark configs use: polymul.polymul_fqt_batch
 cfg5), cmm.right_cmm (cfg4).
 """
 
-from . import _kernels, cmm, dqt, fdiv, gfext, params, polymul, redq, shard, workloads
+from . import _kernels, bench, cli, cmm, costs, dqt, fdiv, gfext, params, polymul, redq, shard, workloads
 from ._native import launch_count
 from .errors import (
     DimensionMismatch,

@@ -122,6 +122,7 @@ _SIGNATURES = {
     "qadic_unpack_rows_i64": ([P, I64, I64, I32, I32, I32, P, P], ctypes.c_int),
     "qadic_extract_middle": ([P, I64, I64, I32, I32, P, P], ctypes.c_int),
     "qadic_full_cmm_reduce": ([P, I64, I64, I64, I32, I32, I32, I64, I64, P, P], ctypes.c_int),
+    "qadic_redq_tabulated": ([P, P, I64, I64, I32, I32, P, I64, I32, I32, P, P], ctypes.c_int),
     "qadic_correct_digits": ([P, I64, I32, I64, I64, P, P], ctypes.c_int),
     "qadic_fdiv_native_check": ([P, I64, P, P, I64, I64, ctypes.POINTER(ctypes.c_uint64), P], ctypes.c_int),
     "qadic_diag_copy": ([P, P, I64, P, I64, I32, I32, P], ctypes.c_int),

@@ -169,6 +169,67 @@ __global__ void correct_digits_kernel(const uint64_t* __restrict__ u, int64_t n,
     }
 }
 
+// Tabulated correction (redq.py:194-300) over a batch: digits u_0..u_d of each
+// word (REDQ-compressed here from the word, or given), then overlapping width-j
+// block lookups (ceil(d/j) per word, the last block shifted down to end at digit
+// d-1) in a table of packed corrected residues -- staged in shared memory when it
+// fits, else read through L1/L2 -- and the top digit passes through (mod p).
+struct TabArgs {
+    const uint64_t* words;   // [n] words (compress first) or null
+    const uint64_t* digits;  // [n, d+1] compressed digits when words is null
+    int64_t n;
+    int64_t p;
+    int t, d, j, base_p, bb, smem_entries;
+    const uint64_t* table;
+    double invp_up, bound;
+    uint64_t* out;           // [n, d+1]
+};
+
+__global__ void tabulated_kernel(TabArgs A) {
+    extern __shared__ uint64_t tab_s[];
+    const uint64_t* tab = A.table;
+    if (A.smem_entries > 0) {
+        for (int i = threadIdx.x; i < A.smem_entries; i += blockDim.x) tab_s[i] = __ldg(A.table + i);
+        __syncthreads();
+        tab = tab_s;
+    }
+    const uint64_t p = (uint64_t)A.p;
+    const uint64_t mask = (1ull << A.bb) - 1;
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < A.n; w += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t u[64];
+        if (A.words) {
+            const uint64_t r = A.words[w];
+            const uint64_t s = floor_div(r, p, A.invp_up, A.bound);
+            for (int i = 0; i <= A.d; ++i) u[i] = (r >> (i * A.t)) - p * (s >> (i * A.t));
+        } else {
+            for (int i = 0; i <= A.d; ++i) u[i] = A.digits[w * (A.d + 1) + i];
+        }
+        uint64_t* o = A.out + w * (A.d + 1);
+        o[A.d] = u[A.d] % p;
+        if (A.d == 0) continue;
+        int nblocks = A.d - A.j + 1 > 0 ? (A.d - A.j) / A.j + 1 : 1;
+        for (int b = 0; b <= nblocks; ++b) {
+            int s0;
+            if (b < nblocks) s0 = b * A.j;
+            else if ((nblocks - 1) * A.j + A.j < A.d) s0 = A.d - A.j;  // trailing block, shifted down
+            else break;
+            uint64_t idx = 0, mul = 1;
+            for (int i = 0; i <= A.j; ++i) {
+                const uint64_t v = s0 + i <= A.d && s0 + i >= 0 ? u[s0 + i] : 0;  // zero padding past the top
+                if (A.base_p) {
+                    idx += v * mul;
+                    mul *= p;
+                } else {
+                    idx |= v << (A.bb * i);
+                }
+            }
+            const uint64_t e = tab[idx];
+            for (int i = 0; i < A.j; ++i)
+                if (s0 + i < A.d && s0 + i >= 0) o[s0 + i] = (e >> (A.bb * i)) & mask;
+        }
+    }
+}
+
 }  // namespace
 }  // namespace qadic
 
@@ -257,6 +318,38 @@ int qadic_full_cmm_reduce(const uint64_t* acc, int64_t mw, int64_t nw, int64_t p
                 full_cmm_reduce_kernel<<<grid_of(mw * nw), TPB, 0, s>>>(acc, mw, nw, p, t, dq, dth, m, n,
                                                                        host_reciprocal_up(p), host_case2_bound(), out));
     return check_launch("full_cmm_reduce");
+}
+
+int qadic_redq_tabulated(const uint64_t* words, const uint64_t* digits, int64_t n, int64_t p, int32_t t, int32_t d,
+                         const uint64_t* table, int64_t table_entries, int32_t j, int32_t base_p, uint64_t* out,
+                         void* stream) {
+    QADIC_REQUIRE(n >= 0 && p >= 2 && p < (1ll << 26) && d >= 0 && d < 64 && j >= 1 && table != nullptr,
+                  QADIC_ERR_VALUE, "bad tabulated-correction arguments");
+    QADIC_REQUIRE((words == nullptr) != (digits == nullptr), QADIC_ERR_VALUE, "give words or digits");
+    QADIC_REQUIRE(words == nullptr || (t >= 1 && (int64_t)(d + 1) * t <= 64), QADIC_ERR_VALUE,
+                  "digit span exceeds the 64-bit word");
+    if (n == 0) return QADIC_OK;
+    TabArgs A;
+    A.words = words;
+    A.digits = digits;
+    A.n = n;
+    A.p = p;
+    A.t = t;
+    A.d = d;
+    A.j = j;
+    A.base_p = base_p;
+    int bb = 1;
+    while ((1ll << bb) < p) ++bb;  // ceil(log2 p), at least 1 (redq.py:238)
+    A.bb = bb;
+    A.table = table;
+    A.invp_up = host_reciprocal_up(p);
+    A.bound = host_case2_bound();
+    A.out = out;
+    A.smem_entries = table_entries <= 6144 ? (int)table_entries : 0;  // <= 48 KB: shared memory
+    cudaStream_t s = (cudaStream_t)stream;
+    QADIC_TIMED("redq_tabulated", s,
+                tabulated_kernel<<<grid_of(n), TPB, (size_t)A.smem_entries * sizeof(uint64_t), s>>>(A));
+    return check_launch("redq_tabulated");
 }
 
 int qadic_correct_digits(const uint64_t* u, int64_t n, int32_t width, int64_t p, int64_t q_mod_p, uint64_t* out,

@@ -136,3 +136,29 @@ def test_batched_one_word_beyond_fused_kernel(dom):
 def test_correct_digits_wraparound(dom):
     assert np.array_equal(redq.correct_digits_array(dom["corr_u"], 23, 1 << 13), dom["corr_mu_23_13"])
     assert np.array_equal(redq.correct_digits_array(dom["corr_u"], 5, 100), dom["corr_mu_5_100"])
+
+
+@pytest.mark.parametrize("p,t,d,j,indexing", [(3, 17, 2, 1, "base-p"), (5, 12, 3, 2, "binary"), (7, 10, 4, 3, "base-p"),
+                                              (23, 13, 3, 2, "binary"), (131, 9, 4, 1, "base-p"),
+                                              (3, 5, 6, 4, "binary"), (2, 3, 10, 3, "base-p")])
+def test_tabulated_redq_batch(p, t, d, j, indexing):
+    """GPU tabulated correction (redq.py:194-300) on a batch: equal to the scalar
+    block-lookup path word by word and to the direct correction kernel."""
+    g = np.random.default_rng(p * 1000 + j)
+    q = 1 << t
+    table = redq.build_correction_table(p, q, j, indexing)
+    words = sum(g.integers(0, q, 3000, dtype=np.uint64) << np.uint64(i * t) for i in range(d + 1))
+    got = redq.reduce_words_tabulated(words, p, t, d, table)
+    assert np.array_equal(got, redq.reduce_words_digits(words, p, t, d))
+    u = redq_compress_rows(words, p, t, d)
+    via_digits = redq.correct_tabulated_array(u, table)
+    assert np.array_equal(via_digits, got)
+    for i in range(0, 3000, 211):
+        cd = redq.CompressedDigits(u=tuple(int(x) for x in u[i]))
+        assert list(via_digits[i]) == redq.correct_tabulated(cd, table)
+
+
+def redq_compress_rows(words, p, t, d):
+    from paper_0809_0063_b200 import _kernels
+
+    return _kernels.redq_compress_u64(words, p, t, d)

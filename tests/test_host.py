@@ -164,3 +164,53 @@ class TestScalarRedq:
                             for code in range(p ** (d + 1)):
                                 u = redq.CompressedDigits(tuple((code // p ** i) % p for i in range(d + 1)))
                                 assert redq.correct_tabulated(u, tab) == redq.redq_correct(u, p, q)
+
+
+class TestCLIHost:
+    """Host-only pieces of the command line and the matrix file format."""
+
+    def test_params_table_matches_reference(self):
+        import contextlib
+        import io
+        import json
+        import os
+
+        from paper_0809_0063_b200 import cli
+
+        with open(os.path.join(os.path.dirname(__file__), "golden", "golden_cli.json")) as fh:
+            gold = json.load(fh)
+        for key, want in gold.items():
+            p, fmt = key.split("_")
+            buf = io.StringIO()
+            with contextlib.redirect_stdout(buf):
+                assert cli.main(["params-table", "--p", p, "--format", fmt]) == 0
+            assert buf.getvalue() == want, key
+
+    def test_matrix_file_round_trip_bit_exact(self):
+        """cmm.write_matrix / read_matrix (reference cmm.py:367-385, pinned by its
+        tests/test_cmm.py:273-288): write -> read -> write is byte-identical."""
+        import io
+
+        from paper_0809_0063_b200 import cmm
+
+        g = np.random.default_rng(11)
+        for p, shape in ((7, (5, 9)), (65537, (3, 4)), (2, (1, 1)), (3, (0, 4))):
+            m = g.integers(0, p, shape, dtype=np.int64)
+            buf = io.StringIO()
+            cmm.write_matrix(buf, m, p)
+            text = buf.getvalue()
+            p2, m2 = cmm.read_matrix(io.StringIO(text))
+            assert p2 == p and m2.shape == m.shape and np.array_equal(m, m2)
+            buf2 = io.StringIO()
+            cmm.write_matrix(buf2, m2, p2)
+            assert buf2.getvalue() == text
+        with pytest.raises(ValueError):
+            cmm.read_matrix(io.StringIO("3 2\n1 2\n"))
+        with pytest.raises(ValueError):
+            cmm.write_matrix(io.StringIO(), np.array([[7]]), 5)
+
+    def test_cli_usage_errors(self):
+        from paper_0809_0063_b200 import cli
+
+        assert cli.main(["matmul", "--variant", "plain"]) == 2
+        assert cli.main(["verify"]) == 2
