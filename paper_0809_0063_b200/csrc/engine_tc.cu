@@ -1487,7 +1487,7 @@ template <int K>
 __global__ void __launch_bounds__(256) planes_b3_kernel(const __grid_constant__ CUtensorMap tmap, int64_t Kd,
                                                         int64_t N, uint32_t p, uint32_t* __restrict__ gtab, PlaneSpec ps, uint32_t lut,
                                                         int S, uint8_t* __restrict__ out, int64_t ld,
-                                                        int64_t plane_stride, int tiles_kk, int tiles_j) {
+                                                        int64_t plane_stride, int tiles_kk, int tiles_j, int jmajor) {
 
     using namespace sm100;
     constexpr int ROWB = P2_J * K;  // bytes per box row
@@ -1500,8 +1500,21 @@ __global__ void __launch_bounds__(256) planes_b3_kernel(const __grid_constant__ 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int r4 = lane >> 3, c8 = lane & 7;
     const int64_t ntiles = (int64_t)tiles_kk * tiles_j;
+    // tile t -> (kk0, j0): kk fastest (concurrent blocks write adjacent plane columns of
+    // the same rows) or, jmajor, j fastest (concurrent blocks read adjacent 96-byte
+    // segments of the same B rows)
+    auto tile_of = [&](int64_t t, int64_t& kk0, int64_t& j0) {
+        if (jmajor) {
+            kk0 = (t / tiles_j) * P2_KK;
+            j0 = (t % tiles_j) * P2_J;
+        } else {
+            kk0 = (t % tiles_kk) * P2_KK;
+            j0 = (t / tiles_kk) * P2_J;
+        }
+    };
     auto issue = [&](int64_t t, int buf) {
-        const int64_t kk0 = (t % tiles_kk) * P2_KK, j0 = (t / tiles_kk) * P2_J;
+        int64_t kk0, j0;
+        tile_of(t, kk0, j0);
         mbar_arrive_expect_tx(&bar[buf], P2_KK * ROWB);
         tma_load_2d(inb + buf * P2_KK * ROWB, &tmap, &bar[buf], (int32_t)(j0 * K), (int32_t)kk0);
     };
@@ -1528,7 +1541,8 @@ __global__ void __launch_bounds__(256) planes_b3_kernel(const __grid_constant__ 
         const int64_t tn = t + (int64_t)(NB - 1) * gridDim.x;
         if (threadIdx.x == 0 && tn < ntiles) issue(tn, (it + NB - 1) % NB);
         mbar_wait(&bar[buf], (uint32_t)((it / NB) & 1));
-        const int64_t kk0 = (t % tiles_kk) * P2_KK, j0 = (t / tiles_kk) * P2_J;
+        int64_t kk0, j0;
+        tile_of(t, kk0, j0);
         const uint8_t* tb = inb + buf * P2_KK * ROWB;
 #pragma unroll
         for (int r = 0; r < P2_KK / 32; ++r) {
@@ -1610,6 +1624,11 @@ __global__ void __launch_bounds__(256) planes_b1_kernel(const uint8_t* __restric
             }
         }
     }
+}
+
+static int b3_jmajor() {
+    static const int v = getenv("QADIC_B3_JMAJOR") ? atoi(getenv("QADIC_B3_JMAJOR")) : 1;  // measured 0.081 vs 0.083 ms (cfg5)
+    return v;
 }
 
 template <int K>
@@ -1866,7 +1885,8 @@ static void launch_planes(const uint8_t* a, const uint8_t* b, int64_t m, int64_t
             const int grid = (int)(tiles < (int64_t)occ * num_sms() ? tiles : (int64_t)occ * num_sms());
             QADIC_TIMED("fp4k planes B", s,
                         planes_b3_kernel<K><<<grid, 256, planes_b3_smem<K>(), s>>>(tm, kdim, n, p, tab, ps, lut, L.S,
-                                                                                  bs, L.ldk, n * L.ldk, tk, tj));
+                                                                                  bs, L.ldk, n * L.ldk, tk, tj,
+                                                                                  b3_jmajor()));
         } else {  // unaligned B: lane loads
             static int occ = 0;
             if (!occ) {
