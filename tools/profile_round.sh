@@ -5,7 +5,7 @@
 #   3. one `ncu --set full` capture per hot kernel of the headline (cfg5) and of cfg1-4.
 # Every ncu command runs only after the same program exited 0 without ncu.
 set -u
-R=${1:-r01}
+R=${1:-r02}
 O=gpurun_out/$R
 mkdir -p $O
 NCU="ncu --clock-control none"
@@ -13,7 +13,9 @@ B="python bench.py --no-cpu-baseline --no-variants"
 ok=1
 python bench.py > $O/bench_default.json 2>>$O/bench.err || ok=0   # the driver's default command
 for c in 1 2; do $B --config $c --warmup 5 > $O/bench_cfg$c.json 2>>$O/bench.err || ok=0; done
-for c in redq pack unpack mm64; do python bench.py --config $c > $O/bench_$c.json 2>>$O/bench.err || ok=0; done
+for c in redq pack unpack mm64 polylong polylong3; do python bench.py --config $c > $O/bench_$c.json 2>>$O/bench.err || ok=0; done
+python bench.py --panels 4 --no-variants --no-cpu-baseline --steps 100 > $O/bench_cfg5_panels4.json 2>>$O/bench.err || ok=0
+python tools/small_copy_floor.py > $O/copy_floor.jsonl 2>>$O/bench.err || ok=0
 for c in 3 4 5; do
   for e in auto i8 i8k fp4 fp4k; do $B --config $c --engine $e --steps 20 --warmup 3 > $O/bench_cfg${c}_$e.json 2>>$O/bench.err || ok=0; done
 done
@@ -37,6 +39,7 @@ full cfg3_fp4k_gemm 3 auto gemm_modp
 full cfg4_fp4k_gemm 4 auto gemm_modp
 full cfg1_polymul 1 auto polymul
 full cfg2_gf_dot 2 auto gf_dot
+full polylong polylong auto conv_tile
 python bench.py --config redq --steps 3 > /dev/null 2>&1 && $NCU --set full -k regex:redq_vec -s 2 -c 1 -o $O/redq -f python bench.py --config redq --steps 3 > $O/redq.log 2>&1
 ncu -i $O/redq.ncu-rep --page raw --csv > $O/redq_raw.csv 2>/dev/null
 full cfg5_i8_gemm 5 i8 gemm_modp

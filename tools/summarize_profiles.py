@@ -35,9 +35,10 @@ TRAFFIC = {
     "redq": ["redq:reduce_words"],
     "pack": ["pack:pack_rows_u8"],
     "unpack": ["unpack:unpack_rows_u8"],
+    "polylong": ["polylong:polymul conv"],
 }
 # measured ceilings / host-path probes written by profile_round.sh, copied verbatim
-PROBES = ["pipe_peaks.json", "fp4_library_ceiling.json", "hbm_write_probe.json", "e2e_probe.txt",
+PROBES = ["copy_floor.jsonl", "pipe_peaks.json", "fp4_library_ceiling.json", "hbm_write_probe.json", "e2e_probe.txt",
           "pageable_probe.txt"]
 
 
