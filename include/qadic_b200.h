@@ -137,6 +137,14 @@ typedef struct qadic_field_desc {
 QADIC_API int qadic_gf_dot_batch_u8(const qadic_field_desc *f, const uint8_t *v1, const uint8_t *v2,
                           int64_t batch, int64_t len, uint8_t *out, void *stream);
 
+/* The same dot products in the paper's accumulation form: every element packed
+ * into a DQT word held in a double, the packed products summed by DFMA (exact: every
+ * sum < 2^53), then REDQ + L/H.  Bit-identical to qadic_gf_dot_batch_u8 (which sums
+ * the packed product's digits on the coefficient bytes instead); k = 3 rows use the
+ * digit-sum form. */
+QADIC_API int qadic_gf_dot_batch_f64_u8(const qadic_field_desc *f, const uint8_t *v1, const uint8_t *v2,
+                                        int64_t batch, int64_t len, uint8_t *out, void *stream);
+
 /* cfg3 / cfg5 -- C[m,n,k] = A[m,kdim,k] @ B[kdim,n,k] over GF(p^k), coefficient
  * I/O.  GFqField.matmul, gfext.py:311-345.  fold_period (F64 engine only) is the
  * number of inner terms accumulated between in-register REDQ folds (0 = none,

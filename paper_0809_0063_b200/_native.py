@@ -100,6 +100,7 @@ _SIGNATURES = {
     "qadic_pack_rows_u8": ([P, I64, I64, I32, I32, I32, P, P], ctypes.c_int),
     "qadic_unpack_rows_u8": ([P, I64, I64, I32, I32, I32, P, P], ctypes.c_int),
     "qadic_gf_dot_batch_u8": ([ctypes.POINTER(FieldDesc), P, P, I64, I64, P, P], ctypes.c_int),
+    "qadic_gf_dot_batch_f64_u8": ([ctypes.POINTER(FieldDesc), P, P, I64, I64, P, P], ctypes.c_int),
     "qadic_gf_matmul_workspace": ([ctypes.POINTER(FieldDesc), I64, I64, I64, I32], SZ),
     "qadic_gf_matmul_u8": ([ctypes.POINTER(FieldDesc), P, P, I64, I64, I64, I32, I32, P, SZ, P, P],
                            ctypes.c_int),

@@ -5,8 +5,13 @@
 //    Reference: polymul.polymul_fqt for one-word operands
 //    (src/polymul.py:274-313 -> _wordconv_reduce :175-216 with na = nb = 1).
 //  * cfg2  gf_dot_batch  : GF(p^k) dot products with all products accumulated
-//    unreduced in FP64, then REDQ and the L/H correction+fold tables staged
-//    in shared memory.  Reference: GFqField.fgdp (src/gfext.py:268-309).
+//    unreduced (no modular work inside the sum), then REDQ and the L/H
+//    correction+fold tables.  Two accumulation forms, bit-identical:
+//    the default sums the packed product's DIGITS directly on the coefficient
+//    bytes (IDP4A; the packed words are never formed), the paper's form
+//    (qadic_gf_dot_batch_f64_u8) packs every element into a DQT word held in
+//    a double and accumulates the packed products with DFMA.
+//    Reference: GFqField.fgdp (src/gfext.py:268-309).
 //
 // Both read uint8 coefficients with 128-bit loads and never touch the
 // packed words in HBM: DQT packing happens in registers.
@@ -241,7 +246,20 @@ QADIC_D void digit_sums_word(uint32_t x, uint32_t y, uint32_t (&S)[2 * K - 1]) {
 
 // NARROW: registers capped at 32 (8 resident blocks per SM) for short rows, where
 // the 4-deep load loop never runs (its spills stay cold) and a wave holds the batch.
-template <int K, int G, bool VEC, bool NARROW = false>
+// the paper's accumulation (F64ACC): DQT words of the 4/K elements of one 32-bit chunk word
+// (digits < p <= q at shifts it; every word < 2^(K t) <= 2^53, so exact in a double)
+template <int K>
+QADIC_D void packed_words_f64(uint32_t x, int t, double (&w)[4 / K]) {
+#pragma unroll
+    for (int e = 0; e < 4 / K; ++e) {
+        uint64_t v = 0;
+#pragma unroll
+        for (int i = 0; i < K; ++i) v |= (uint64_t)((x >> (8 * (e * K + i))) & 0xFFu) << (i * t);
+        w[e] = (double)v;
+    }
+}
+
+template <int K, int G, bool VEC, bool NARROW = false, bool F64ACC = false>
 __global__ void __launch_bounds__(GD_THREADS, NARROW ? 8 : 1) gf_dot_kernel(const uint8_t* __restrict__ v1,
                                                             const uint8_t* __restrict__ v2, int64_t batch,
                                                             int64_t len, FieldConst f, int tab_smem,
@@ -264,11 +282,23 @@ __global__ void __launch_bounds__(GD_THREADS, NARROW ? 8 : 1) gf_dot_kernel(cons
             uint32_t S[2 * K - 1];
 #pragma unroll
             for (int j = 0; j < 2 * K - 1; ++j) S[j] = 0;
+            double accd = 0.0;  // F64ACC: the packed products summed in FP64 (every sum < 2^53)
+            auto word = [&](uint32_t xw, uint32_t yw) {
+                if constexpr (F64ACC) {
+                    double wx[4 / K], wy[4 / K];
+                    packed_words_f64<K>(xw, t, wx);
+                    packed_words_f64<K>(yw, t, wy);
+#pragma unroll
+                    for (int e = 0; e < 4 / K; ++e) accd = fma(wx[e], wy[e], accd);
+                } else {
+                    digit_sums_word<K>(xw, yw, S);
+                }
+            };
             auto body = [&](const uint4& x, const uint4& y) {
-                digit_sums_word<K>(x.x, y.x, S);
-                digit_sums_word<K>(x.y, y.y, S);
-                digit_sums_word<K>(x.z, y.z, S);
-                digit_sums_word<K>(x.w, y.w, S);
+                word(x.x, y.x);
+                word(x.y, y.y);
+                word(x.z, y.z);
+                word(x.w, y.w);
             };
             if constexpr (NARROW) {  // short rows: at most 2 chunks per lane (host-checked), no loop
                 const uint4 z = make_uint4(0, 0, 0, 0);
@@ -298,10 +328,14 @@ __global__ void __launch_bounds__(GD_THREADS, NARROW ? 8 : 1) gf_dot_kernel(cons
             }
             if (ch < nchunks) body(__ldg(c1 + ch), __ldg(c2 + ch));
             }
-            if constexpr (K == 2) S[0] -= S[2];
-            // the packed word: every S_j < q (host-checked), so r < q^(2K-1) <= 2^53
+            if constexpr (F64ACC) {
+                acc = (uint64_t)accd;
+            } else {
+                if constexpr (K == 2) S[0] -= S[2];
+                // the packed word: every S_j < q (host-checked), so r < q^(2K-1) <= 2^53
 #pragma unroll
-            for (int j = 0; j < 2 * K - 1; ++j) acc += (uint64_t)S[j] << (j * t);
+                for (int j = 0; j < 2 * K - 1; ++j) acc += (uint64_t)S[j] << (j * t);
+            }
         } else {
             for (int64_t e = lane; e < len; e += G) {
                 uint64_t wx = 0, wy = 0;
@@ -351,7 +385,7 @@ __global__ void __launch_bounds__(GD_THREADS, NARROW ? 8 : 1) gf_dot_kernel(cons
     }
 }
 
-template <int K>
+template <int K, bool F64ACC = false>
 static void launch_gf_dot(const uint8_t* v1, const uint8_t* v2, int64_t batch, int64_t len, const FieldConst& f,
                           uint8_t* out, cudaStream_t s) {
     // digit sums in 32-bit lanes: every S_j < q = 2^t
@@ -385,9 +419,9 @@ static void launch_gf_dot(const uint8_t* v1, const uint8_t* v2, int64_t batch, i
             const unsigned blocks = (unsigned)((threads_total + width - 1) / width);
             launch_pdl(kern, dim3(blocks), dim3((unsigned)width), smem, s, v1, v2, batch, len, f, ntab, out);
         };
-        if (lanes == 8 && nchunks <= 2 * 8) go(gf_dot_kernel<K, 8, (4 % K == 0), true>, 8);
-        else if (nchunks <= 2 * 4) go(gf_dot_kernel<K, 4, (4 % K == 0), true>, 4);
-        else go(gf_dot_kernel<K, 4, (4 % K == 0), false>, 4);
+        if (lanes == 8 && nchunks <= 2 * 8) go(gf_dot_kernel<K, 8, (4 % K == 0), true, F64ACC>, 8);
+        else if (nchunks <= 2 * 4) go(gf_dot_kernel<K, 4, (4 % K == 0), true, F64ACC>, 4);
+        else go(gf_dot_kernel<K, 4, (4 % K == 0), false, F64ACC>, 4);
     } else {
         constexpr int G = 8;
         const unsigned blocks = (unsigned)((batch * G + GD_THREADS - 1) / GD_THREADS);
@@ -470,8 +504,8 @@ int qadic_polymul_batch_u8(const uint8_t* a, const uint8_t* b, int64_t n, int32_
     return check_launch("polymul_batch_u8");
 }
 
-int qadic_gf_dot_batch_u8(const qadic_field_desc* fd, const uint8_t* v1, const uint8_t* v2, int64_t batch,
-                          int64_t len, uint8_t* out, void* stream) {
+static int gf_dot_batch(const qadic_field_desc* fd, const uint8_t* v1, const uint8_t* v2, int64_t batch, int64_t len,
+                        uint8_t* out, void* stream, bool f64acc) {
     FieldConst f;
     int rc = make_field_const(fd, &f);
     if (rc) return rc;
@@ -483,14 +517,33 @@ int qadic_gf_dot_batch_u8(const qadic_field_desc* fd, const uint8_t* v1, const u
     cudaStream_t s = (cudaStream_t)stream;
     const int pi = prof_begin(s, "gf_dot");
     count_launch(1);
-    switch (f.k) {
-        case 1: launch_gf_dot<1>(v1, v2, batch, len, f, out, s); break;
-        case 2: launch_gf_dot<2>(v1, v2, batch, len, f, out, s); break;
-        case 3: launch_gf_dot<3>(v1, v2, batch, len, f, out, s); break;
-        default: launch_gf_dot<4>(v1, v2, batch, len, f, out, s); break;
+    if (f64acc) {  // the FP64 form exists for the vector path (K | 4); K = 3 rows fall back to digit sums
+        switch (f.k) {
+            case 1: launch_gf_dot<1, true>(v1, v2, batch, len, f, out, s); break;
+            case 2: launch_gf_dot<2, true>(v1, v2, batch, len, f, out, s); break;
+            case 3: launch_gf_dot<3>(v1, v2, batch, len, f, out, s); break;
+            default: launch_gf_dot<4, true>(v1, v2, batch, len, f, out, s); break;
+        }
+    } else {
+        switch (f.k) {
+            case 1: launch_gf_dot<1>(v1, v2, batch, len, f, out, s); break;
+            case 2: launch_gf_dot<2>(v1, v2, batch, len, f, out, s); break;
+            case 3: launch_gf_dot<3>(v1, v2, batch, len, f, out, s); break;
+            default: launch_gf_dot<4>(v1, v2, batch, len, f, out, s); break;
+        }
     }
     prof_end(pi, s);
     return check_launch("gf_dot_batch_u8");
+}
+
+int qadic_gf_dot_batch_u8(const qadic_field_desc* fd, const uint8_t* v1, const uint8_t* v2, int64_t batch,
+                          int64_t len, uint8_t* out, void* stream) {
+    return gf_dot_batch(fd, v1, v2, batch, len, out, stream, false);
+}
+
+int qadic_gf_dot_batch_f64_u8(const qadic_field_desc* fd, const uint8_t* v1, const uint8_t* v2, int64_t batch,
+                              int64_t len, uint8_t* out, void* stream) {
+    return gf_dot_batch(fd, v1, v2, batch, len, out, stream, true);
 }
 
 }  // extern "C"

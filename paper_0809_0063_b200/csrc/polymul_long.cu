@@ -43,12 +43,17 @@ namespace qadic {
 namespace {
 
 constexpr int CT = 128;          // threads per conv CTA
-constexpr int CR = 8;            // output words per thread
+#ifndef QADIC_POLY_CR
+#define QADIC_POLY_CR 16
+#endif
+constexpr int CR = QADIC_POLY_CR;  // output words per thread (16: two shared loads per 16 FMAs)
+constexpr int CR_SHIFT = CR == 16 ? 4 : 3;
 constexpr int TJ = CT * CR;      // output words per CTA
 constexpr int TI = 256;          // inner terms staged per round
 constexpr int BW = TJ + TI - 1;  // b window length per round
-QADIC_D int bpad(int x) { return x + (x >> 3); }  // 1 pad double per 8: stride-8 thread reads spread over the banks
-constexpr int BW_PAD = BW + (BW >> 3) + 1;
+// one pad double per CR: the stride-CR thread reads of the b window spread over the banks
+QADIC_D int bpad(int x) { return x + (x >> CR_SHIFT); }
+constexpr int BW_PAD = BW + (BW >> CR_SHIFT) + 2;
 
 struct ConvArgs {
     const uint64_t* a;   // [batch][na] (the longer operand: the inner loop)
@@ -136,7 +141,7 @@ QADIC_D void store_digits(Acc v, int64_t pair, int64_t j, const ConvArgs& A, int
 }
 
 template <typename Acc>
-__global__ void __launch_bounds__(CT) conv_tile_kernel(ConvArgs A) {
+__global__ void __launch_bounds__(CT, 4) conv_tile_kernel(ConvArgs A) {
     __shared__ Acc a_s[TI];
     __shared__ Acc b_s[BW_PAD];
     const int64_t tiles = (A.nout + TJ - 1) / TJ;
@@ -197,20 +202,16 @@ __global__ void __launch_bounds__(CT) conv_tile_kernel(ConvArgs A) {
                 }
                 since += CR;
             }
-        } else {
+        } else {  // fold budget below CR (fold-bound radix): plain loads, a fold every `chunk` steps
 #pragma unroll 1
-            for (int ii0 = 0; ii0 < TI; ii0 += CR) {
+            for (int ii = 0; ii < TI; ++ii) {
+                const Acc av = a_s[ii];
 #pragma unroll
-                for (int u = 0; u < CR; ++u) {
-                    const Acc av = a_s[ii0 + u];
+                for (int r = 0; r < CR; ++r) mac<Acc>(acc[r], av, b_s[bpad(tj + r + TI - ii)]);
+                if (++since == chunk) {
 #pragma unroll
-                    for (int r = 0; r < CR; ++r) mac<Acc>(acc[r], av, w[(r - u + CR) % CR]);
-                    if (++since == chunk) {
-#pragma unroll
-                        for (int r = 0; r < CR; ++r) fold(acc[r], A);
-                        since = 0;
-                    }
-                    w[(CR - 1 - u + CR) % CR] = b_s[bpad(tj + TI - 1 - ii0 - u)];
+                    for (int r = 0; r < CR; ++r) fold(acc[r], A);
+                    since = 0;
                 }
             }
         }
@@ -450,8 +451,15 @@ int qadic_polymul_words_batch(const uint64_t* aw, int64_t na, const uint64_t* bw
     int segs = 1;
     if (tiled) {
         const int64_t tiles = B * ((nout + TJ - 1) / TJ);
-        // one full wave: 8 resident CTAs per SM (64 registers, 14 KB smem)
-        const int64_t want = (int64_t)num_sms_cached() * 8;
+        // one full wave of resident CTAs
+        static int occ = 0;
+        if (!occ) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f64 ? (const void*)conv_tile_kernel<double>
+                                                                    : (const void*)conv_tile_kernel<uint64_t>,
+                                                          CT, 0);
+            if (occ < 1) occ = 1;
+        }
+        const int64_t want = (int64_t)num_sms_cached() * occ;
         const int64_t max_rounds = std::min<int64_t>(n_a, TJ + n_b - 1) / TI + 1;
         if (tiles < want) segs = (int)std::min<int64_t>({want / tiles, max_rounds, 64});
         if (segs < 1) segs = 1;

@@ -373,8 +373,12 @@ class GFqField:
         c2 = self.to_coeffs(v2)
         return self.to_indices(self.fgdp_batch_coeffs(c1, c2))
 
-    def fgdp_batch_coeffs(self, v1, v2, out=None):
-        """cfg2 hot path: uint8 [B, n, k] x [B, n, k] -> uint8 [B, k]."""
+    def fgdp_batch_coeffs(self, v1, v2, out=None, engine: str = "auto"):
+        """cfg2 hot path: uint8 [B, n, k] x [B, n, k] -> uint8 [B, k].
+
+        engine "auto": the packed product's digits summed on the coefficient bytes
+        (IDP4A); "f64": the paper's form -- DQT words in doubles, products summed by
+        DFMA.  Bit-identical."""
         d1, h1 = N.to_dev(v1, np.uint8)
         d2, h2 = N.to_dev(v2, np.uint8)
         if d1.dim() != 3 or tuple(d1.shape) != tuple(d2.shape) or d1.shape[2] != self.k:
@@ -387,8 +391,10 @@ class GFqField:
                 return N.finish(res, out, h1 or h2, np.uint8)
             return N.to_host(res, np.uint8) if (h1 or h2) else res
         dev = N.out_buffer(out, (b, self.k), np.uint8)
-        N.check(N.lib().qadic_gf_dot_batch_u8(self.field_desc(), N.ptr(d1), N.ptr(d2), b, n, N.ptr(dev),
-                                              N.stream_ptr()), DimensionMismatch)
+        if engine not in ("auto", "f64"):
+            raise ValueError(f"unknown dot engine {engine!r}")
+        fn = N.lib().qadic_gf_dot_batch_f64_u8 if engine == "f64" else N.lib().qadic_gf_dot_batch_u8
+        N.check(fn(self.field_desc(), N.ptr(d1), N.ptr(d2), b, n, N.ptr(dev), N.stream_ptr()), DimensionMismatch)
         return N.finish(dev, out, h1 or h2, np.uint8)
 
     def _lh_lookup(self, u: Sequence[int], stats=None):

@@ -162,3 +162,17 @@ def redq_compress_rows(words, p, t, d):
     from paper_0809_0063_b200 import _kernels
 
     return _kernels.redq_compress_u64(words, p, t, d)
+
+
+@pytest.mark.parametrize("p,k,n", [(3, 2, 64), (3, 1, 500), (5, 4, 3), (2, 2, 200), (7, 2, 20), (3, 3, 8)])
+def test_dot_f64_accumulation_form(p, k, n):
+    """the paper's accumulation (DQT words in doubles, DFMA) is bit-identical to the
+    digit-sum form and to the oracle (cfg2 reports both)."""
+    f = gfext.build_field(p, k, max_dot_length=n)
+    of = O.build_field(p, k, irreducible=list(f.irreducible), max_dot_length=n)
+    g = np.random.default_rng(p * 100 + k)
+    v1 = g.integers(0, p, (3001, n, k), dtype=np.uint8)
+    v2 = g.integers(0, p, (3001, n, k), dtype=np.uint8)
+    want = O.gf_dot_batch(of, v1, v2)
+    assert np.array_equal(f.fgdp_batch_coeffs(v1, v2, engine="f64"), want)
+    assert np.array_equal(f.fgdp_batch_coeffs(v1, v2), want)
