@@ -463,11 +463,15 @@ def dominant_kernel(cfg, engine, prof):
     return max(prof, key=lambda k: prof[k][1])
 
 
-def roofline(cfg, engine, kname, kstats, work, peaks, peak_src):
+def roofline(cfg, engine, kname, kstats, work, peaks, peak_src, steps=None):
+    """`work` is per step; a step that launches the kernel several times (the
+    row-block column panels) splits it over the launches."""
     if kname is None:
         return None
     count, total_ms = kstats
     avg_s = total_ms / count / 1e3
+    per_launch = (steps / count) if steps else 1.0
+    work = {k: (v * per_launch if isinstance(v, (int, float)) else v) for k, v in work.items()}
     if kname in ("i8 gemm", "i8k gemm"):
         # expanded form: M*(N k)*(K k) MACs; evaluation planes: S * M*N*K MACs
         ops = 2 * (work["kara_macs"] if kname == "i8k gemm" else work["i8_macs"])
@@ -626,7 +630,7 @@ def measure_variants(args, cfg, engine, meta, units, work, peaks, peak_src, torc
             if eng == "f64" and cfg == 4:
                 n = W.CONFIGS[4].shape[0]
                 w["f64_fmas"] = n * n * (-(-n // 3))
-            roof = roofline(cfg, eng, kname, prof.get(kname), w, peaks, peak_src)
+            roof = roofline(cfg, eng, kname, prof.get(kname), w, peaks, peak_src, steps=k)
             out[eng] = {"ms_per_step": round(ms, 4), "value": units / (ms / 1e3), "steps": k,
                         "kernel": kname, "achieved": roof["achieved"] if roof else None,
                         "unit": roof["unit"] if roof else None, "frac": roof["frac"] if roof else None,
@@ -889,9 +893,10 @@ def run_ours(args):
     if engine == "f64" and cfg == 4:
         n = W.CONFIGS[4].shape[0]
         work["f64_fmas"] = (n // ws) * n * (-(-n // 3))
-    roof = roofline(cfg, engine, kname, prof.get(kname), work, peaks, peak_src)
+    roof = roofline(cfg, engine, kname, prof.get(kname), work, peaks, peak_src, steps=args.steps)
     if roof is not None:
         roof["traffic"] = traffic_from_profiles(cfg, engine, kname)
+        roof["launches_per_step"] = round(prof[kname][0] / args.steps, 3)
         total_ms = sum(v[1] for v in prof.values()) / args.steps
         roof["kernel_share_of_step"] = round((prof[kname][1] / args.steps) / ms, 4) if ms else None
         roof["kernels_ms_per_step"] = {k: round(v[1] / args.steps, 4) for k, v in prof.items()}
