@@ -34,6 +34,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "qadic_common.cuh"
@@ -44,9 +45,9 @@ namespace {
 
 constexpr int CT = 128;          // threads per conv CTA
 #ifndef QADIC_POLY_CR
-#define QADIC_POLY_CR 16
+#define QADIC_POLY_CR 8
 #endif
-constexpr int CR = QADIC_POLY_CR;  // output words per thread (16: two shared loads per 16 FMAs)
+constexpr int CR = QADIC_POLY_CR;  // output words per thread (8 measured faster than 16: 0.187 vs 0.211 ms, occupancy)
 constexpr int CR_SHIFT = CR == 16 ? 4 : 3;
 constexpr int TJ = CT * CR;      // output words per CTA
 constexpr int TI = 256;          // inner terms staged per round
@@ -141,7 +142,7 @@ QADIC_D void store_digits(Acc v, int64_t pair, int64_t j, const ConvArgs& A, int
 }
 
 template <typename Acc>
-__global__ void __launch_bounds__(CT, 4) conv_tile_kernel(ConvArgs A) {
+__global__ void __launch_bounds__(CT, 8) conv_tile_kernel(ConvArgs A) {
     __shared__ Acc a_s[TI];
     __shared__ Acc b_s[BW_PAD];
     const int64_t tiles = (A.nout + TJ - 1) / TJ;
@@ -459,7 +460,13 @@ int qadic_polymul_words_batch(const uint64_t* aw, int64_t na, const uint64_t* bw
                                                           CT, 0);
             if (occ < 1) occ = 1;
         }
-        const int64_t want = (int64_t)num_sms_cached() * occ;
+        // several waves of shorter segments: the tiles at both ends of a product have
+        // triangular (shorter) inner ranges, so one wave of equal-count CTAs leaves SMs idle
+        // (measured: one wave when the fold budget is >= CR -- FMA-bound, 0.192 vs 0.202 ms for
+        // two; three when it is below -- fold-bound, 0.645 vs 0.868 ms)
+        static const int waves_env = getenv("QADIC_POLY_WAVES") ? atoi(getenv("QADIC_POLY_WAVES")) : 0;
+        const int waves = waves_env > 0 ? waves_env : (budget / per0 >= (uint64_t)CR ? 1 : 3);
+        const int64_t want = (int64_t)num_sms_cached() * occ * waves;
         const int64_t max_rounds = std::min<int64_t>(n_a, TJ + n_b - 1) / TI + 1;
         if (tiles < want) segs = (int)std::min<int64_t>({want / tiles, max_rounds, 64});
         if (segs < 1) segs = 1;
