@@ -99,3 +99,38 @@ def test_roofline_ops_per_engine():
     assert bench.roofline(5, "f64", "f64 dmma gemm", one_ms, work, peaks, "measured")["peak"] == 40.0
     h = bench.roofline(1, "auto", "polymul_k4", one_ms, work, peaks, "measured")
     assert h["bound"] == "hbm" and h["achieved"] == 1000.0 and h["peak"] == 6500.0
+
+
+def test_roofline_splits_step_work_over_launches():
+    """a step that launches its dominant kernel P times (the row-block column panels)
+    quotes each launch against 1/P of the step's work."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    work = {"kara_macs": 4 * 10 ** 12, "io_bytes": 10 ** 9}
+    peaks = {"hbm_gbs": 6500.0, "bf16_tflops": 1650.0}
+    r1 = bench.roofline(5, "fp4k", "fp4k gemm", (10, 10.0), work, peaks, "measured", steps=10)
+    r4 = bench.roofline(5, "fp4k", "fp4k gemm", (40, 10.0), work, peaks, "measured", steps=10)
+    assert abs(r1["achieved"] - 8000.0) < 1e-6 and abs(r4["achieved"] - 8000.0) < 1e-6
+
+
+def test_reference_arm_prints_our_config():
+    """both arms describe the workload with the same config object."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    d = _run(["--impl", "reference", "--config", "2", "--steps", "2", "--warmup", "1"],
+             env={"QADIC_REF_BUDGET_S": "3"})
+    assert d["config"] == bench.config_dict(2, "auto", 1, "rows", 1)
+
+
+@pytest.mark.gpu
+def test_matmul_line_fields():
+    """cfg5 line at a reduced step count: no REDQ rate for the tensor-core engine (it
+    reduces mod p directly), the standalone REDQ line, burst + sustained timings."""
+    d = _run(["--config", "5", "--steps", "5", "--warmup", "3", "--no-cpu-baseline", "--no-variants"], timeout=900)
+    assert "redq_coeffs_per_s" not in d
+    assert d["redq"]["roofline"]["bound"] == "hbm" and 0 < d["redq"]["roofline"]["frac"] < 1
+    sb = d["sustained_vs_burst"]
+    assert sb["burst"]["steps"] == 5 and sb["sustained"]["steps"] >= 200
+    assert d["roofline"]["launches_per_step"] == 1
