@@ -244,6 +244,10 @@ QADIC_D void digit_sums_word(uint32_t x, uint32_t y, uint32_t (&S)[2 * K - 1]) {
     }
 }
 
+// QADIC_GD_SLOWTAIL=1: the generic REDQ tail everywhere (measurement switch)
+__constant__ int c_gd_slowtail = 0;
+QADIC_D bool tail_slow() { return c_gd_slowtail != 0; }
+
 // NARROW: registers capped at 32 (8 resident blocks per SM) for short rows, where
 // the 4-deep load loop never runs (its spills stay cold) and a wave holds the batch.
 // the paper's accumulation (F64ACC): DQT words of the 4/K elements of one 32-bit chunk word
@@ -367,7 +371,19 @@ __global__ void __launch_bounds__(GD_THREADS, NARROW ? 8 : 1) gf_dot_kernel(cons
     constexpr int ND = 2 * K - 2;
     if (!live || lane != 0) return;
     uint32_t u[ND + 1];
-    redq_compress_f64<ND>((double)acc, f.invp_up, (double)f.p, f.bound, f.p, t, u);
+    if ((ND + 1) * t <= 32 && !tail_slow()) {
+        // r < 2^32 (cfg2: 30 bits): the same FP64 REDQ without the conversion instructions --
+        // r enters as the low mantissa bits of 2^52 + r, s = floor(RN(r RU(1/p))) leaves as the
+        // low bits of the round-down sum with 2^52 (r < 2^32 < B: no correction branch)
+        const double two52 = 4503599627370496.0;
+        const uint32_t r32 = (uint32_t)acc;
+        const double rd = __hiloint2double(0x43300000, (int)r32) - two52;
+        const uint32_t s32 = (uint32_t)__double_as_longlong(__dadd_rd(__dmul_rn(rd, f.invp_up), two52));
+#pragma unroll
+        for (int i = 0; i <= ND; ++i) u[i] = (r32 >> (i * t)) - f.p * (s32 >> (i * t));
+    } else {
+        redq_compress_f64<ND>((double)acc, f.invp_up, (double)f.p, f.bound, f.p, t, u);
+    }
     uint32_t li = 0, hi = 0;
 #pragma unroll
     for (int i = 0; i < K; ++i) {
@@ -405,6 +421,12 @@ static void launch_gf_dot(const uint8_t* v1, const uint8_t* v2, int64_t batch, i
         const int64_t nchunks = len * K / 16;
         static const int max_width = getenv("QADIC_GD_WIDTH") ? atoi(getenv("QADIC_GD_WIDTH")) : GD_THREADS;
         static const int lanes = getenv("QADIC_GD_LANES") ? atoi(getenv("QADIC_GD_LANES")) : 4;
+        static bool slow_set = false;
+        if (!slow_set && getenv("QADIC_GD_SLOWTAIL")) {
+            const int v = atoi(getenv("QADIC_GD_SLOWTAIL"));
+            cudaMemcpyToSymbol(c_gd_slowtail, &v, sizeof(int));
+        }
+        slow_set = true;
         auto go = [&](auto kern, int G) {
             static int occ = 0;
             if (!occ) {
