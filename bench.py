@@ -594,8 +594,10 @@ def measure_variants(args, cfg, engine, meta, units, work, peaks, peak_src, torc
         pr = pipe_probe(N, "f64", 0.1)
         if "burst" in pr:
             peaks = dict(peaks, f64_probe_tflops=pr["burst"])
-    for eng in ("i8k", "i8", "f64"):
+    for eng in ("i8k", "i8", "f64", "f64-fold"):
         if eng == engine or (eng == "i8k" and cfg == 4):  # k = 1: i8k only adds conversions
+            continue
+        if eng == "f64-fold" and cfg != 5:  # the two-sided fold schedule is cfg5's own (fold every 9)
             continue
         step = meta["variant_step"](eng)
         try:
@@ -627,6 +629,8 @@ def measure_variants(args, cfg, engine, meta, units, work, peaks, peak_src, torc
             if eng == "f64" and cfg in (3, 5):
                 c_ = W.CONFIGS[cfg]
                 w["f64_fmas"] = w["madds"] * (c_.k if cfg == 5 else 1)
+            if eng == "f64-fold":  # two-sided: one FMA per GF mult-add (+ the folds, ALU work)
+                w["f64_fmas"] = w["madds"]
             if eng == "f64" and cfg == 4:
                 n = W.CONFIGS[4].shape[0]
                 w["f64_fmas"] = n * n * (-(-n // 3))

@@ -55,6 +55,10 @@ typedef enum qadic_engine {
  * re-converting A per panel.  Other engines ignore them. */
 #define QADIC_ENGINE_FLAG_COL_PANEL 0x100
 #define QADIC_ENGINE_FLAG_A_READY 0x200
+/* F64_DMMA engine: force the two-sided DQT form with in-register REDQ folds every
+ * fold_period terms (the paper's schedule; AUTO takes the one-sided form when the
+ * fold period is below 64, where the folds make the two-sided form ALU-bound). */
+#define QADIC_ENGINE_FLAG_F64_TWO_SIDED 0x400
 
 QADIC_API int qadic_abi_version(void);
 QADIC_API const char *qadic_last_error(void);

@@ -22,8 +22,11 @@ LIB_PATH = os.path.join(_HERE, "libqadic_b200.so")
 QADIC_OK, ERR_SHAPE, ERR_PARAMS, ERR_VALUE, ERR_CUDA, ERR_UNSUPPORTED = range(6)
 ENGINE_AUTO, ENGINE_I8_TC, ENGINE_F64_DMMA, ENGINE_F4_TC, ENGINE_F4K_TC, ENGINE_I8K_TC = 0, 1, 2, 3, 4, 5
 ENGINE_FLAG_COL_PANEL, ENGINE_FLAG_A_READY = 0x100, 0x200  # column-panel sweep (qadic_b200.h)
+ENGINE_FLAG_F64_TWO_SIDED = 0x400
 ENGINES = {"auto": ENGINE_AUTO, "i8": ENGINE_I8_TC, "f64": ENGINE_F64_DMMA, "fp4": ENGINE_F4_TC, "fp4k": ENGINE_F4K_TC,
-           "i8k": ENGINE_I8K_TC}
+           "i8k": ENGINE_I8K_TC,
+           # the paper's two-sided DQT schedule with in-register REDQ folds (cfg5: fold every 8 terms)
+           "f64-fold": ENGINE_F64_DMMA | ENGINE_FLAG_F64_TWO_SIDED}
 
 P = ctypes.c_void_p
 I64 = ctypes.c_int64

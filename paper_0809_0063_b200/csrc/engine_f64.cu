@@ -395,12 +395,16 @@ static int f64_gf_matmul_one_sided(const FieldConst& f, const uint8_t* a, const 
 }
 
 int f64_gf_matmul(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
-                  int fold, void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s) {
+                  int fold, void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s, bool two_sided) {
     using namespace f64;
     const int64_t Mp = rup(m, BM), Kp = rup(kdim, BK), Np = rup(n, BN);
     QADIC_REQUIRE(ws && ws_bytes >= f64_gf_workspace(m, kdim, n, (int)f.k), QADIC_ERR_VALUE, "workspace too small");
+    // the two-sided DQT form with in-register REDQ folds every `fold` terms is the paper's
+    // own schedule (cfg5: q = 2^10, fold every 8 <= 9 terms); below ONE_SIDED_BELOW it is
+    // ALU-bound, so AUTO picks the one-sided form unless asked (engine flag / env)
     const char* env = getenv("QADIC_F64_ONE_SIDED");
-    const bool one = env ? atoi(env) != 0 : (fold > 0 && fold < ONE_SIDED_BELOW && f.k > 1);
+    const bool one = two_sided ? false
+                               : (env ? atoi(env) != 0 : (fold > 0 && fold < ONE_SIDED_BELOW && f.k > 1));
     if (one) return f64_gf_matmul_one_sided(f, a, b, m, kdim, n, ws, c, s);
     double* aw = static_cast<double*>(ws);
     double* bw = aw + Mp * Kp;

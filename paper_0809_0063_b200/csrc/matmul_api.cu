@@ -33,7 +33,7 @@ int tc_kara8_right_cmm(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kd
 size_t f64_gf_workspace(int64_t m, int64_t kdim, int64_t n, int k);
 size_t f64_cmm_workspace(int64_t m, int64_t kdim, int64_t n, int d);
 int f64_gf_matmul(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n,
-                  int fold, void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s);
+                  int fold, void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s, bool two_sided);
 int f64_right_cmm(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, int64_t n, uint32_t p, int t, int d,
                   void* ws, size_t ws_bytes, uint8_t* c, cudaStream_t s);
 }  // namespace qadic
@@ -79,7 +79,7 @@ static int gf_matmul_dev(const FieldConst& f, const uint8_t* a, const uint8_t* b
                       "fold period %d exceeds the accumulation budget", fold_period);
         if (kdim <= fold_period) fold_period = 0;
     }
-    return f64_gf_matmul(f, a, b, m, kdim, n, fold_period, ws, ws_bytes, c, s);
+    return f64_gf_matmul(f, a, b, m, kdim, n, fold_period, ws, ws_bytes, c, s, (reuse & F64_TWO_SIDED) != 0);
 }
 
 extern "C" {
@@ -101,6 +101,7 @@ int qadic_gf_matmul_u8(const qadic_field_desc* fd, const uint8_t* a, const uint8
     int reuse = 0;
     if (engine & QADIC_ENGINE_FLAG_COL_PANEL) reuse |= REUSE_COL_PANEL;
     if (engine & QADIC_ENGINE_FLAG_A_READY) reuse |= REUSE_COL_PANEL | REUSE_A_READY;
+    if (engine & QADIC_ENGINE_FLAG_F64_TWO_SIDED) reuse |= F64_TWO_SIDED;
     engine &= 0xff;
     FieldConst f;
     int rc = make_field_const(fd, &f);
@@ -194,6 +195,7 @@ static CopyStreams& copy_streams() {
 size_t qadic_gf_matmul_host_workspace(const qadic_field_desc* f, int64_t m, int64_t kdim, int64_t n, int32_t engine,
                                       int64_t panel_rows) {
     if (!f || m < 0 || kdim < 0 || n < 0) return 0;
+    engine &= 0xff;
     const int64_t pr = host_panel_rows(m, panel_rows);
     const int64_t k = f->k;
     return align_up(qadic_gf_matmul_workspace(f, pr, kdim, n, engine)) + align_up((size_t)(kdim * n * k)) +
@@ -203,6 +205,8 @@ size_t qadic_gf_matmul_host_workspace(const qadic_field_desc* f, int64_t m, int6
 int qadic_gf_matmul_host_u8(const qadic_field_desc* fd, const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim,
                             int64_t n, int32_t engine, int32_t fold_period, int64_t panel_rows, void* ws,
                             size_t ws_bytes, uint8_t* c, void* stream) {
+    const int eflags = (engine & QADIC_ENGINE_FLAG_F64_TWO_SIDED) ? F64_TWO_SIDED : 0;
+    engine &= 0xff;
     FieldConst f;
     int rc = make_field_const(fd, &f);
     if (rc) return rc;
@@ -298,7 +302,7 @@ int qadic_gf_matmul_host_u8(const qadic_field_desc* fd, const uint8_t* a, const 
             rc = check_launch("gf_matmul_host (empty K)");
         } else {
             rc = gf_matmul_dev(f, ap, bsrc, rows, kdim, n, engine, fold_period, base, eng_ws, cp, s,
-                               i > 0 ? REUSE_B_READY : 0);
+                               (i > 0 ? REUSE_B_READY : 0) | eflags);
         }
         done_c[i] = event();
         cudaEventRecord(done_c[i], s);

@@ -9,7 +9,7 @@
 namespace qadic {
 
 // operand-plane reuse across successive GF matmul calls (fp4k engine; see run_kara)
-enum : int { REUSE_B_READY = 1, REUSE_COL_PANEL = 2, REUSE_A_READY = 4 };
+enum : int { REUSE_B_READY = 1, REUSE_COL_PANEL = 2, REUSE_A_READY = 4, F64_TWO_SIDED = 8 };  // + F64 engine form
 
 // RU(1/p): the smallest double >= 1/p (fdiv.py:166-180, mode UP).
 double host_reciprocal_up(int64_t p);

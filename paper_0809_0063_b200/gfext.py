@@ -467,7 +467,7 @@ class GFqField:
         m, kd, n = da.shape[0], da.shape[1], db.shape[1]
         eng = N.ENGINES[engine]
         fold = 0
-        if eng == N.ENGINE_F64_DMMA:
+        if (eng & 0xff) == N.ENGINE_F64_DMMA:
             if kd * self.k * (self.p - 1) ** 2 >= self.params.q:
                 fold = self.max_fold_period() if fold_period is None else int(fold_period)
                 if fold < 4:
@@ -501,7 +501,7 @@ class GFqField:
         m, kd, n = ashape[0], ashape[1], bshape[1]
         eng = N.ENGINES[engine]
         fold = 0
-        if eng == N.ENGINE_F64_DMMA and kd * self.k * (self.p - 1) ** 2 >= self.params.q:
+        if (eng & 0xff) == N.ENGINE_F64_DMMA and kd * self.k * (self.p - 1) ** 2 >= self.params.q:
             fold = self.max_fold_period() if fold_period is None else int(fold_period)
             if fold < 4:
                 raise ParamsViolation("accumulation budget below one DMMA k-step")

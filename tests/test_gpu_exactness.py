@@ -207,3 +207,19 @@ def test_cfg5_rows_vs_reference_composition():
     for r0 in (0, m // 2, m - 2):
         ref = cpu_ref.run_block(5, cpu_ref.sample_inputs(5, full, 2, start=r0, cols=2048), K)
         assert np.array_equal(got[r0:r0 + 2, :2048], ref), r0
+
+
+def test_f64_two_sided_engine_flag():
+    """engine "f64-fold" (QADIC_ENGINE_FLAG_F64_TWO_SIDED) runs cfg5's own schedule in
+    this process, device and host-buffer entry points alike."""
+    import torch
+
+    f = W.field_for(W.CONFIGS[5])
+    of = O.build_field(7, 3, irreducible=[5, 0, 0, 1], max_dot_length=9)
+    g = W.rng(66)
+    a = g.integers(0, 7, (70, 777, 3), dtype=np.uint8)
+    b = g.integers(0, 7, (777, 45, 3), dtype=np.uint8)
+    want = O.gf_matmul_planes(of, a, b)
+    assert np.array_equal(f.matmul_coeffs(a, b, engine="f64-fold"), want)  # host pipeline
+    da, db = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    assert np.array_equal(f.matmul_coeffs(da, db, engine="f64-fold").cpu().numpy(), want)
