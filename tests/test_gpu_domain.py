@@ -176,3 +176,74 @@ def test_dot_f64_accumulation_form(p, k, n):
     want = O.gf_dot_batch(of, v1, v2)
     assert np.array_equal(f.fgdp_batch_coeffs(v1, v2, engine="f64"), want)
     assert np.array_equal(f.fgdp_batch_coeffs(v1, v2), want)
+
+
+def _poly_ref(a, b, p):
+    """schoolbook product mod p in Python integers (independent of every kernel)."""
+    if len(a) == 0 or len(b) == 0:
+        return np.zeros(0, dtype=np.int64)
+    out = np.convolve(np.asarray(a, dtype=object), np.asarray(b, dtype=object)) % p
+    return np.asarray(out, dtype=np.int64)
+
+
+@pytest.mark.parametrize("p", [2, 3, 33554393])
+def test_delayed_product_extremes(p):
+    """polymul_delayed: one coefficient per word at radix 2^53, including the largest
+    primes the parameters admit (p ~ 2^25: a fold every few terms)."""
+    g = np.random.default_rng(p % 1000)
+    for la, lb in ((1, 1), (1, 700), (517, 3), (1000, 999)):
+        a = polymul.ModPoly(g.integers(0, p, la, dtype=np.int64), p)
+        b = polymul.ModPoly(g.integers(0, p, lb, dtype=np.int64), p)
+        assert np.array_equal(polymul.polymul_delayed(a, b).coeffs, _poly_ref(a.coeffs, b.coeffs, p)), (la, lb)
+
+
+@pytest.mark.parametrize("p,d", [(2, 1), (3, 2), (131, 1), (65537, 0)])
+def test_fqt_shapes_and_thresholds(p, d):
+    prm = fqt_params(p, d)
+    g = np.random.default_rng(p + d)
+    for la, lb in ((1, 1), (1, 300), (257, 1), (64, 64), (1025, 1023)):
+        a = polymul.ModPoly(g.integers(0, p, la, dtype=np.int64), p)
+        b = polymul.ModPoly(g.integers(0, p, lb, dtype=np.int64), p)
+        want = np.zeros(2 * max(la, lb) - 1, np.int64)
+        r = _poly_ref(a.coeffs, b.coeffs, p)
+        want[:r.size] = r
+        for algo, thr in (("classical", 16), ("karatsuba", 0), ("karatsuba", 1), ("karatsuba", 5)):
+            got = polymul.polymul_fqt(a, b, prm, algo, threshold=thr, validate=True)
+            assert np.array_equal(got.coeffs, want), (la, lb, algo, thr)
+
+
+def test_long_batch_uint8_and_device_io():
+    """batched long products: numpy in -> uint8 out (p <= 255), CUDA tensors stay on the
+    device, `out=` host and device buffers."""
+    import torch
+
+    prm = fqt_params(5, 2)
+    g = np.random.default_rng(9)
+    a = g.integers(0, 5, (7, 300), dtype=np.uint8)
+    b = g.integers(0, 5, (7, 200), dtype=np.uint8)
+    want = np.stack([_poly_ref(a[i].astype(np.int64), b[i].astype(np.int64), 5) for i in range(7)])
+    want = np.pad(want, ((0, 0), (0, 599 - want.shape[1])))
+    got = polymul.polymul_fqt_long_batch(a, b, prm)
+    assert got.dtype == np.uint8 and np.array_equal(got.astype(np.int64), want)
+    da, db = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    dev = polymul.polymul_fqt_long_batch(da, db, prm, algo="karatsuba", threshold=4)
+    assert dev.is_cuda and np.array_equal(dev.cpu().numpy().astype(np.int64), want)
+    host_out = np.zeros((7, 599), np.uint8)
+    polymul.polymul_fqt_long_batch(a, b, prm, out=host_out)
+    assert np.array_equal(host_out.astype(np.int64), want)
+
+
+@pytest.mark.parametrize("p,k,n,m,nn", [(257, 1, 32, 1000, 700), (131, 2, 2, 513, 900), (2, 7, 1, 300, 301)])
+def test_word_path_larger_shapes(p, k, n, m, nn):
+    """the any-field word path at shapes that tile the uint64 tensor-core GEMM, against
+    the field's own scalar arithmetic on sampled entries."""
+    f = gfext.build_field(p, k, max_dot_length=n)
+    g = np.random.default_rng(m + nn)
+    a = g.integers(0, f.order, (m, n), dtype=np.int64)
+    b = g.integers(0, f.order, (n, nn), dtype=np.int64)
+    c = f.matmul(a, b)
+    for (i, j) in ((0, 0), (m - 1, nn - 1), (m // 2, nn // 3), (7, nn - 2)):
+        acc = f.zero
+        for t in range(n):
+            acc = f.add(acc, f.mul(f.elem(int(a[i, t])), f.elem(int(b[t, j]))))
+        assert int(c[i, j]) == acc.index, (i, j)
