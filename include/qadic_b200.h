@@ -225,6 +225,16 @@ QADIC_API int qadic_polymul_words_batch(const uint64_t *aw, int64_t na, const ui
                                         int32_t algo, int64_t threshold, int32_t validate, int32_t out_u8,
                                         void *out, int64_t ncoef, qadic_polymul_stats *stats, void *stream);
 
+/* The same batched products on INT8 tensor cores (p <= 127, uint8 residues):
+ * out[s][y] = sum_x a[s][x] b[s][y-x] mod p as one batched Toeplitz GEMM (T_s[x][l] =
+ * a_s[x-l], 128 columns; b_s as 128-coefficient blocks; mod-p epilogue) plus an
+ * overlap-add.  out [batch][ncoef] uint8 (positions past na+nb-2 are zero);
+ * `workspace` (device) must hold qadic_polymul_tc_workspace() bytes.  Asynchronous. */
+QADIC_API size_t qadic_polymul_tc_workspace(int64_t batch, int64_t na, int64_t nb);
+QADIC_API int qadic_polymul_tc_u8(const uint8_t *a, int64_t na, const uint8_t *b, int64_t nb, int64_t batch,
+                                  int64_t p, uint8_t *out, int64_t ncoef, void *workspace, size_t ws_bytes,
+                                  void *stream);
+
 /* ---------------------------------------------------------------------------
  * Any-field DQT word path (csrc/generic.cu): the reference's composition for the
  * fields / primes outside the uint8 coefficient engines (p > 127, k > 4, wide

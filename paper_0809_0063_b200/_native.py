@@ -119,6 +119,8 @@ _SIGNATURES = {
     "qadic_fdiv_applied_scan": ([I32, ctypes.POINTER(I64 * 3), ctypes.POINTER(ctypes.c_uint64), P], ctypes.c_int),
     "qadic_polymul_words_batch": ([P, I64, P, I64, I64, I64, I32, I32, I64, I64, I32, I64, I32, I32, P, I64,
                                    ctypes.POINTER(PolymulStats), P], ctypes.c_int),
+    "qadic_polymul_tc_workspace": ([I64, I64, I64], SZ),
+    "qadic_polymul_tc_u8": ([P, I64, P, I64, I64, I64, P, I64, P, SZ, P], ctypes.c_int),
     "qadic_gather_u64": ([P, I64, P, P, P], ctypes.c_int),
     "qadic_gf_words_dot": ([P, P, I64, I64, P, P, P], ctypes.c_int),
     "qadic_gf_words_finish": ([P, I64, ctypes.POINTER(GenericDesc), P, P], ctypes.c_int),

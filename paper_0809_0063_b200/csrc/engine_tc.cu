@@ -150,6 +150,8 @@ struct Params {
     // launched as the programmatic dependent of a concurrent GEMM launch: wait for
     // that grid to complete before exiting, so stream order still covers both
     int pdl_tail;
+    // uint8 epilogue: store column n of row m at c[n * ldc + m + n * diag_shift] (0: row-major)
+    int64_t diag_shift;
 };
 
 // tile index -> (plane, m tile, n tile).  Unfused: planes outermost.  Fused:
@@ -524,6 +526,13 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                             dst[e / 2] = (uint8_t)(r[e] | (hi << 4));
                         }
                     }
+                } else if (prm.diag_shift) {
+                    // diagonal-shifted transpose (Toeplitz products): column v of row x lands at
+                    // c[v][x + v * diag_shift] -- a warp's 32 rows write 32 consecutive bytes per column
+                    uint8_t* cpl = prm.c + pl * prm.c_plane;
+#pragma unroll
+                    for (int e = 0; e < 16; ++e)
+                        if (col0 + e < prm.N) cpl[(col0 + e) * prm.ldc + row + (col0 + e) * prm.diag_shift] = (uint8_t)r[e];
                 } else {
                     uint32_t w[4];
 #pragma unroll
@@ -2440,7 +2449,281 @@ static int run_kara8(const FieldConst& f, const uint8_t* a, const uint8_t* b, in
     return check_launch("i8k combine");
 }
 
+// ---------------------------------------------------------------------------
+// Batched long-polynomial products on INT8 tensor cores (Toeplitz GEMM).
+//   out_s[y] = sum_x a_s[x] b_s[y - x] mod p   (s = 0 .. batch-1, residues < p <= 127)
+// Split b_s into V = ceil(nb / TL) blocks of TL coefficients: the product of a_s with
+// block v is column v of D_s = T_s Bv_s, where T_s [M = na + TL - 1][TL] is the
+// Toeplitz matrix T_s[x][l] = a_s[x - l] (K-major: row x is a reversed window of a_s)
+// and Bv_s [V][TL] is b_s itself, zero padded.  One batched GEMM (the batch as the
+// GEMM's planes, tcgen05 kind::i8, int32 TMEM sums of TL (p-1)^2 < 2^31, mod-p
+// epilogue to uint8) gives every D_s[x][v] = (a_s * b_{s,v})[x] mod p; the overlap-add
+// out_s[y] = sum_v D_s[y - v TL][v] mod p finishes.  The arithmetic is the convolution
+// itself (exact integers), so the result equals polymul_fqt's for any packing.
+// Traffic per pair: T (M TL bytes) + D (M V bytes), minimal near TL ~ sqrt(nb);
+// TL = 128 is one K block of the GEMM pipeline.
+constexpr int TL_DEFAULT = 256;  // Toeplitz width (GEMM K): measured 0.119 ms vs 0.121 (512), 0.162 (1024) at polylong
+
+// apad[s][k] = a_s[na - 1 - (k - TL)] for TL <= k < TL + na, else 0 (a_s reversed, zero
+// margins): the Toeplitz row x, chunk c is the 16 contiguous bytes at k = TL + na - 1 - x + 16c
+__global__ void reverse_pad_kernel(const uint8_t* __restrict__ a, int64_t batch, int64_t na, int64_t len,
+                                   uint8_t* __restrict__ apad, int TL) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < batch * len; g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t sidx = g / len, k = g - sidx * len, i = k - TL;
+        apad[g] = (i >= 0 && i < na) ? a[sidx * na + (na - 1 - i)] : (uint8_t)0;
+    }
+}
+
+__global__ void toeplitz_rows_kernel(const uint8_t* __restrict__ apad, int64_t batch, int64_t na, int64_t len,
+                                     int64_t M, uint8_t* __restrict__ T, int TL) {
+    // one thread per 16-byte chunk (s, x, c): T[s][x][16c + j] = a_s[x - 16c - j] = apad_s[o + j],
+    // o = TL + na - 1 - x + 16c: five aligned words, funnel-shifted into place
+    const int64_t chunks = TL / 16, total = batch * M * chunks;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t sx = g / chunks;
+        const int c = (int)(g - sx * chunks);
+        const int64_t sidx = sx / M, x = sx - sidx * M;
+        const int64_t o = TL + na - 1 - x + 16 * c;
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(apad + sidx * len) + (o >> 2);
+        const uint32_t sh = 8u * (uint32_t)(o & 3);
+        uint32_t v[5];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) v[k] = __ldg(w + k);
+        uint32_t r[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) r[k] = __funnelshift_r(v[k], v[k + 1], sh);
+        *reinterpret_cast<uint4*>(T + sx * TL + 16 * c) = make_uint4(r[0], r[1], r[2], r[3]);
+    }
+}
+
+__global__ void blocks_kernel(const uint8_t* __restrict__ b, int64_t batch, int64_t nb, int64_t V,
+                              uint8_t* __restrict__ Bv, int TL) {
+    // Bv[s][v][l] = b_s[v TL + l] (0 past nb), 16 bytes per thread
+    const int64_t chunks = V * TL / 16, total = batch * chunks;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t sidx = g / chunks, e0 = (g - sidx * chunks) * 16;
+        const uint8_t* bs = b + sidx * nb;
+        uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int64_t i = e0 + j;
+            const uint32_t v = i < nb ? (uint32_t)__ldg(bs + i) : 0u;
+            w[j >> 2] |= v << (8 * (j & 3));
+        }
+        *reinterpret_cast<uint4*>(Bv + sidx * V * TL + e0) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
+// out[s][y] = sum_v Dt[s][v][y - v TL] mod p over 0 <= y - v TL < M (Dt: the GEMM's
+// [V][ldc] residues, row v = the product with block v).  A thread owns 4 consecutive y:
+// TL is a multiple of 4, so every row segment it reads is one aligned word; the byte sums
+// ride in two 16-bit lanes per word (at most ceil(M / TL) + 1 terms of <= 126 each).
+__global__ void toeplitz_overlap_kernel(const uint8_t* __restrict__ Dt, int64_t batch, int64_t M, int64_t V,
+                                        int64_t ldc, uint32_t p, int64_t nfull, int64_t ncoef,
+                                        uint8_t* __restrict__ out, unsigned int* flag, int TL) {
+    const int64_t span = ((ncoef > nfull ? ncoef : nfull) + 3) / 4;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < batch * span;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t sidx = g / span, y0 = (g - sidx * span) * 4;
+        uint32_t ev = 0, od = 0;
+        if (y0 < nfull) {
+            const uint8_t* Ds = Dt + sidx * V * ldc;
+            const int64_t vlo = y0 + 3 >= M ? (y0 + 3 - M) / TL + 1 : 0;  // rows whose window can touch y0..y0+3
+            const int64_t vhi = (y0 + 3) / TL < V - 1 ? (y0 + 3) / TL : V - 1;
+            int terms = 0;
+            for (int64_t v = (vlo > 0 ? vlo - 1 : 0); v <= vhi; ++v) {
+                const int64_t x0 = y0 - v * TL;  // multiple of 4
+                if (x0 + 3 < 0 || x0 >= M) continue;
+                if (++terms == 500) {  // keep every 16-bit lane below 2^16 (500 x 126 + p)
+                    ev = ((ev & 0xFFFFu) % p) | (((ev >> 16) % p) << 16);
+                    od = ((od & 0xFFFFu) % p) | (((od >> 16) % p) << 16);
+                    terms = 1;
+                }
+                uint32_t w = *reinterpret_cast<const uint32_t*>(Ds + v * ldc + (x0 < 0 ? 0 : x0));
+                if (x0 < 0) w = 0;  // (x0 is a multiple of 4: a word is wholly inside or outside)
+                if (x0 + 3 >= M) w &= 0xFFFFFFFFu >> (8 * (x0 + 4 - M));  // bytes past the row end
+                ev += w & 0x00FF00FFu;
+                od += (w >> 8) & 0x00FF00FFu;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t y = y0 + j;
+            const uint32_t sum = ((j & 1) ? od : ev) >> (16 * (j >> 1)) & 0xFFFFu;
+            const uint32_t r = y < nfull ? sum % p : 0u;
+            if (y < ncoef) out[sidx * ncoef + y] = (uint8_t)r;
+            else if (r) atomicOr(flag, 2u);
+        }
+    }
+}
+
+// out[s][y] = sum_v E[s][v][y] mod p, E the GEMM's diagonal-shifted transpose
+// (E[v][x + v TL] = D[x][v]; entries outside [v TL, v TL + M) were never written and are
+// masked): a thread owns 16 consecutive y, one 16-byte load per row v, byte sums in
+// 16-bit lanes (V <= 500 terms of <= 126 between reductions)
+constexpr int OV_SPLIT = 8;  // threads per 16-output group (each sums every 8th row v)
+
+__global__ void toeplitz_overlap_diag_kernel(const uint8_t* __restrict__ E, int64_t batch, int64_t M, int64_t V,
+                                             int64_t lde, uint32_t p, int64_t nfull, int64_t ncoef,
+                                             uint8_t* __restrict__ out, unsigned int* flag, int TL) {
+    const int64_t span = ((ncoef > nfull ? ncoef : nfull) + 15) / 16;
+    const int part = threadIdx.x % OV_SPLIT;  // lanes of a group are consecutive: shuffle-combinable
+    const int64_t total = batch * span, stride = (int64_t)gridDim.x * blockDim.x / OV_SPLIT;
+    // warp-uniform trip count: every lane takes part in the group shuffles below
+    for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / OV_SPLIT; __any_sync(0xffffffffu, g < total);
+         g += stride) {
+        const bool act = g < total;
+        const int64_t gg = act ? g : 0;
+        const int64_t sidx = gg / span, y0 = (gg - sidx * span) * 16;
+        uint32_t acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // byte j of the 16 in lane (j & 1) of acc[j >> 1]
+        if (act && y0 < nfull) {
+            const uint8_t* Es = E + sidx * V * lde;
+            const int64_t vlo = y0 + 15 >= M ? (y0 + 15 - M) / TL : 0;
+            const int64_t vhi = y0 / TL < V - 1 ? y0 / TL : V - 1;
+            int terms = 0;
+            for (int64_t v = vlo + part; v <= vhi; v += OV_SPLIT) {
+                const int64_t lo = v * TL, hi = v * TL + M;  // written range of row v
+                if (y0 + 15 < lo || y0 >= hi) continue;
+                const uint4 w = __ldg(reinterpret_cast<const uint4*>(Es + v * lde + y0));
+                uint32_t x[4] = {w.x, w.y, w.z, w.w};
+                if (y0 < lo || y0 + 15 >= hi) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j)
+                        if (y0 + j < lo || y0 + j >= hi) x[j >> 2] &= ~(0xFFu << (8 * (j & 3)));
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    acc[2 * q] += x[q] & 0x00FF00FFu;
+                    acc[2 * q + 1] += (x[q] >> 8) & 0x00FF00FFu;
+                }
+                if (++terms == 60) {  // 8 partial sums of <= 60 x 126 + p are combined below
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) acc[i] = ((acc[i] & 0xFFFFu) % p) | (((acc[i] >> 16) % p) << 16);
+                    terms = 0;
+                }
+            }
+        }
+        // combine the group's partial sums (8 x < 7686 < 2^16 per lane)
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int o = OV_SPLIT / 2; o > 0; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+        if (part == 0 && act) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int64_t y = y0 + j;
+                const int q = j >> 2, b = j & 3;
+                const uint32_t sum = (acc[2 * q + (b & 1)] >> (16 * (b >> 1))) & 0xFFFFu;
+                const uint32_t r = y < nfull ? sum % p : 0u;
+                if (y < ncoef) out[sidx * ncoef + y] = (uint8_t)r;
+                else if (r) atomicOr(flag, 2u);
+            }
+        }
+    }
+}
+
+static bool tz_rows() {
+    static const int v = getenv("QADIC_TZ_ROWS") ? atoi(getenv("QADIC_TZ_ROWS")) : 1;
+    return v != 0;
+}
+
+static int tz_width() {
+    static const int w = getenv("QADIC_TZ_L") ? atoi(getenv("QADIC_TZ_L")) : TL_DEFAULT;
+    return (w >= 128 && w % 128 == 0) ? w : TL_DEFAULT;
+}
+static int64_t tz_pad_len(int64_t na, int TL) { return round_up(na + 2 * TL + 32, 16); }
+static int64_t tz_ldc(int64_t M) { return round_up(M, 16); }
+
+static size_t toeplitz_workspace(int64_t batch, int64_t na, int64_t nb) {
+    const int TL = tz_width();
+    const int64_t M = na + TL - 1, V = (nb + TL - 1) / TL;
+    return (size_t)round_up(batch * tz_pad_len(na, TL), 1024) + (size_t)round_up(batch * M * TL, 1024) +
+           (size_t)round_up(batch * V * TL, 1024) +
+           (size_t)round_up(batch * V * std::max(tz_ldc(M), round_up(M + (V - 1) * TL + 16, 16)), 1024) + 1024;
+}
+
+static int run_toeplitz(const uint8_t* a, int64_t na, const uint8_t* b, int64_t nb, int64_t batch, uint32_t p,
+                        uint8_t* out, int64_t ncoef, void* ws, size_t ws_bytes, cudaStream_t s) {
+    const int TL = tz_width();
+    const int64_t M = na + TL - 1, V = (nb + TL - 1) / TL, len = tz_pad_len(na, TL), ldc = tz_ldc(M);
+    QADIC_REQUIRE(ws && ws_bytes >= toeplitz_workspace(batch, na, nb), QADIC_ERR_VALUE, "workspace too small");
+    QADIC_REQUIRE(batch * M < (1ll << 31) && batch * V < (1ll << 31), QADIC_ERR_UNSUPPORTED,
+                  "batch x length beyond the TMA row range");
+    uint8_t* apad = static_cast<uint8_t*>(ws);
+    uint8_t* T = apad + round_up(batch * len, 1024);
+    uint8_t* Bv = T + round_up(batch * M * TL, 1024);
+    uint8_t* Dt = Bv + round_up(batch * V * TL, 1024);
+    unsigned int* flag = reinterpret_cast<unsigned int*>(
+        Dt + round_up(batch * V * std::max(ldc, round_up(M + (V - 1) * TL + 16, 16)), 1024));
+    const int sms = num_sms();
+    auto grid_of = [&](int64_t n) {
+        return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 16));
+    };
+    QADIC_TIMED("polymul toeplitz pad", s, reverse_pad_kernel<<<grid_of(batch * len), 256, 0, s>>>(a, batch, na, len, apad, TL));
+    QADIC_TIMED("polymul toeplitz A", s,
+                toeplitz_rows_kernel<<<grid_of(batch * M * (TL / 16)), 256, 0, s>>>(apad, batch, na, len, M, T, TL));
+    QADIC_TIMED("polymul toeplitz B", s, blocks_kernel<<<grid_of(batch * V * (TL / 16)), 256, 0, s>>>(b, batch, nb, V, Bv, TL));
+    int rc = check_launch("toeplitz operands");
+    if (rc) return rc;
+    // single-CTA tiles: the short-K, narrow-N tiles of this GEMM are latency-bound per tile, and
+    // 148 independent CTAs beat 74 pairs (measured 0.094 vs 0.103 ms per polylong batch)
+    static const bool pair = getenv("QADIC_TZ_PAIR") && atoi(getenv("QADIC_TZ_PAIR")) != 0;
+    constexpr int BN = Cfg<KIND_I8>::BN;
+    const bool rows = tz_rows();
+    // rows: GEMM rows = the M Toeplitz rows, columns = the V blocks of b (D[x][v]: every
+    // epilogue warp busy, V values per thread); else transposed, Dt[v][x]
+    // the diagonal-shifted layout: E[v][y] rows of lde >= M + (V - 1) TL + 16 bytes
+    const int64_t lde = round_up(M + (V - 1) * TL + 16, 16);
+    const int64_t gm = rows ? M : V, gn = rows ? V : M, ldd = rows ? lde : ldc;
+    CUtensorMap ta, tb;
+    rc = make_tmap(&ta, rows ? T : Bv, TL, batch * gm, TL, BM);
+    if (rc) return rc;
+    rc = make_tmap(&tb, rows ? Bv : T, TL, batch * gn, TL, pair ? BN / 2 : BN);
+    if (rc) return rc;
+    Params prm = {};
+    prm.sf = e2m1_scale_word();
+    prm.group_m = GROUP_M;
+    prm.M = gm;
+    prm.N = gn;
+    prm.ldc = ldd;
+    prm.p = p;
+    prm.offset = p * ((1u << 25) / p + 1);
+    prm.magic64 = wide_magic(p);
+    prm.m_tiles = (int)((gm + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM));
+    prm.n_tiles = (int)((gn + BN - 1) / BN);
+    prm.n_full = (int)(gn / BN);
+    prm.num_kb = (int)((TL + BK - 1) / BK);
+    prm.c = Dt;
+    prm.c_plane = rows ? V * lde : gm * ldd;
+    prm.diag_shift = rows ? TL : 0;
+    prm.planes = (int)batch;
+    prm.nibble_out = 0;
+    rc = pair ? launch_gemm<KIND_I8, true>(ta, tb, prm, s, "polymul toeplitz gemm")
+              : launch_gemm<KIND_I8, false>(ta, tb, prm, s, "polymul toeplitz gemm");
+    if (rc) return rc;
+    cudaMemsetAsync(flag, 0, sizeof(unsigned int), s);
+    const int64_t nfull = na + nb - 1;
+    if (rows)
+        QADIC_TIMED("polymul overlap", s,
+                    toeplitz_overlap_diag_kernel<<<grid_of(batch * ((std::max(nfull, ncoef) + 15) / 16) * OV_SPLIT), 256, 0, s>>>(
+                        Dt, batch, M, V, lde, p, nfull, ncoef, out, flag, TL));
+    else
+        QADIC_TIMED("polymul overlap", s,
+                    toeplitz_overlap_kernel<<<grid_of(batch * ((std::max(nfull, ncoef) + 3) / 4)), 256, 0, s>>>(
+                        Dt, batch, M, V, ldc, p, nfull, ncoef, out, flag, TL));
+    return check_launch("toeplitz overlap");
+}
+
 }  // namespace tc
+
+size_t tc_toeplitz_workspace(int64_t batch, int64_t na, int64_t nb) { return tc::toeplitz_workspace(batch, na, nb); }
+
+int tc_polymul_toeplitz(const uint8_t* a, int64_t na, const uint8_t* b, int64_t nb, int64_t batch, uint32_t p,
+                        uint8_t* out, int64_t ncoef, void* ws, size_t ws_bytes, cudaStream_t s) {
+    QADIC_REQUIRE(p >= 2 && p <= 127, QADIC_ERR_UNSUPPORTED, "the tensor-core product needs p <= 127");
+    QADIC_REQUIRE((int64_t)tc::tz_width() * (p - 1) * (p - 1) < (1ll << 31), QADIC_ERR_PARAMS, "int32 sum bound");
+    return tc::run_toeplitz(a, na, b, nb, batch, p, out, ncoef, ws, ws_bytes, s);
+}
 
 bool tc_u64_ok(int64_t m, int64_t k, int64_t n, const void* a) {
     return m >= 128 && n >= 128 && k >= 16 && (k % 2 == 0) && ((reinterpret_cast<uintptr_t>(a) & 15) == 0);

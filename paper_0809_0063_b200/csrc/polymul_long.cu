@@ -342,9 +342,27 @@ int64_t coeff_len(int64_t nw, int k) { return nw ? (nw + 1) * k - 1 : 0; }
 }  // namespace
 }  // namespace qadic
 
+namespace qadic {
+size_t tc_toeplitz_workspace(int64_t batch, int64_t na, int64_t nb);
+int tc_polymul_toeplitz(const uint8_t* a, int64_t na, const uint8_t* b, int64_t nb, int64_t batch, uint32_t p,
+                        uint8_t* out, int64_t ncoef, void* ws, size_t ws_bytes, cudaStream_t s);
+}  // namespace qadic
+
 using namespace qadic;
 
 extern "C" {
+
+size_t qadic_polymul_tc_workspace(int64_t batch, int64_t na, int64_t nb) {
+    if (batch < 0 || na < 1 || nb < 1) return 0;
+    return tc_toeplitz_workspace(batch, na, nb);
+}
+
+int qadic_polymul_tc_u8(const uint8_t* a, int64_t na, const uint8_t* b, int64_t nb, int64_t batch, int64_t p,
+                        uint8_t* out, int64_t ncoef, void* ws, size_t ws_bytes, void* stream) {
+    QADIC_REQUIRE(na >= 1 && nb >= 1 && batch >= 0 && ncoef >= 0, QADIC_ERR_SHAPE, "incompatible shapes");
+    if (batch == 0) return QADIC_OK;
+    return tc_polymul_toeplitz(a, na, b, nb, batch, (uint32_t)p, out, ncoef, ws, ws_bytes, (cudaStream_t)stream);
+}
 
 int qadic_polymul_words_batch(const uint64_t* aw, int64_t na, const uint64_t* bw, int64_t nb, int64_t batch,
                               int64_t p, int32_t t, int32_t d, int64_t ma, int64_t mb, int32_t algo,

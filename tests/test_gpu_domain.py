@@ -247,3 +247,36 @@ def test_word_path_larger_shapes(p, k, n, m, nn):
         for t in range(n):
             acc = f.add(acc, f.mul(f.elem(int(a[i, t])), f.elem(int(b[t, j]))))
         assert int(c[i, j]) == acc.index, (i, j)
+
+
+@pytest.mark.parametrize("p,la,lb,bsz", [(3, 16384, 16384, 3), (7, 300, 5000, 4), (127, 256, 257, 5), (2, 129, 131, 2),
+                                         (5, 1000, 1, 2), (3, 1, 1, 1)])
+def test_long_products_tensor_core_engine(p, la, lb, bsz):
+    """the Toeplitz GEMM engine (INT8 tensor cores) equals the packed-word engine and the
+    schoolbook product; edge lengths include one-coefficient operands and lengths that
+    are not multiples of the 128-coefficient blocks."""
+    prm = fqt_params(p, 1) if p <= 31 else fqt_params(p, 0)
+    g = np.random.default_rng(la + lb + p)
+    a = g.integers(0, p, (bsz, la), dtype=np.uint8)
+    b = g.integers(0, p, (bsz, lb), dtype=np.uint8)
+    tc = polymul.polymul_fqt_long_batch(a, b, prm, engine="tc")
+    words = polymul.polymul_fqt_long_batch(a, b, prm, engine="words")
+    assert np.array_equal(tc, words)
+    for i in (0, bsz - 1):
+        r = _poly_ref(a[i].astype(np.int64), b[i].astype(np.int64), p)
+        assert np.array_equal(np.asarray(tc[i][:r.size], np.int64), r) and not tc[i][r.size:].any()
+    with pytest.raises(ValueError):
+        polymul.polymul_fqt_long_batch(a, b, prm, engine="tc", validate=True)
+
+
+def test_long_products_tensor_core_long_rows():
+    """rows long enough that the overlap-add's 16-bit lane sums need intermediate reductions
+    (> 500 blocks of 128 per output) -- one pair of 70000 x 70000 coefficients over F_127."""
+    p = 127
+    prm = fqt_params(p, 0)
+    g = np.random.default_rng(70000)
+    a = g.integers(0, p, (1, 70000), dtype=np.uint8)
+    b = g.integers(0, p, (1, 70000), dtype=np.uint8)
+    tc = polymul.polymul_fqt_long_batch(a, b, prm, engine="tc")
+    words = polymul.polymul_fqt_long_batch(a, b, prm, engine="words")
+    assert np.array_equal(tc, words)
