@@ -2453,16 +2453,15 @@ static int run_kara8(const FieldConst& f, const uint8_t* a, const uint8_t* b, in
 // Batched long-polynomial products on INT8 tensor cores (Toeplitz GEMM).
 //   out_s[y] = sum_x a_s[x] b_s[y - x] mod p   (s = 0 .. batch-1, residues < p <= 127)
 // Split b_s into V = ceil(nb / TL) blocks of TL coefficients: the product of a_s with
-// block v is column v of D_s = T_s Bv_s, where T_s [M = na + TL - 1][TL] is the
+// block v is column v of D_s = T_s Bv_s^T, where T_s [M = na + TL - 1][TL] is the
 // Toeplitz matrix T_s[x][l] = a_s[x - l] (K-major: row x is a reversed window of a_s)
 // and Bv_s [V][TL] is b_s itself, zero padded.  One batched GEMM (the batch as the
-// GEMM's planes, tcgen05 kind::i8, int32 TMEM sums of TL (p-1)^2 < 2^31, mod-p
-// epilogue to uint8) gives every D_s[x][v] = (a_s * b_{s,v})[x] mod p; the overlap-add
-// out_s[y] = sum_v D_s[y - v TL][v] mod p finishes.  The arithmetic is the convolution
-// itself (exact integers), so the result equals polymul_fqt's for any packing.
-// Traffic per pair: T (M TL bytes) + D (M V bytes), minimal near TL ~ sqrt(nb);
-// TL = 128 is one K block of the GEMM pipeline.
-constexpr int TL_DEFAULT = 256;  // Toeplitz width (GEMM K): measured 0.119 ms vs 0.121 (512), 0.162 (1024) at polylong
+// GEMM's planes, tcgen05 kind::i8, int32 TMEM sums of TL (p-1)^2 < 2^31, mod-p epilogue)
+// stores D_s as its diagonal-shifted transpose E_s[v][x + v TL] = D_s[x][v] (uint8), so the
+// overlap-add out_s[y] = sum_v E_s[v][y] mod p reads whole aligned vectors.  The arithmetic
+// is the convolution itself (exact integers): the result equals polymul_fqt's for any
+// packing.  Traffic per pair: T (M TL bytes) + E (V (M + (V-1) TL) bytes).
+constexpr int TL_DEFAULT = 256;  // Toeplitz width (GEMM K): 0.103 ms vs 0.128 (128), 0.118 (512) at polylong
 
 // apad[s][k] = a_s[na - 1 - (k - TL)] for TL <= k < TL + na, else 0 (a_s reversed, zero
 // margins): the Toeplitz row x, chunk c is the 16 contiguous bytes at k = TL + na - 1 - x + 16c
@@ -2514,53 +2513,6 @@ __global__ void blocks_kernel(const uint8_t* __restrict__ b, int64_t batch, int6
     }
 }
 
-// out[s][y] = sum_v Dt[s][v][y - v TL] mod p over 0 <= y - v TL < M (Dt: the GEMM's
-// [V][ldc] residues, row v = the product with block v).  A thread owns 4 consecutive y:
-// TL is a multiple of 4, so every row segment it reads is one aligned word; the byte sums
-// ride in two 16-bit lanes per word (at most ceil(M / TL) + 1 terms of <= 126 each).
-__global__ void toeplitz_overlap_kernel(const uint8_t* __restrict__ Dt, int64_t batch, int64_t M, int64_t V,
-                                        int64_t ldc, uint32_t p, int64_t nfull, int64_t ncoef,
-                                        uint8_t* __restrict__ out, unsigned int* flag, int TL) {
-    const int64_t span = ((ncoef > nfull ? ncoef : nfull) + 3) / 4;
-    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < batch * span;
-         g += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t sidx = g / span, y0 = (g - sidx * span) * 4;
-        uint32_t ev = 0, od = 0;
-        if (y0 < nfull) {
-            const uint8_t* Ds = Dt + sidx * V * ldc;
-            const int64_t vlo = y0 + 3 >= M ? (y0 + 3 - M) / TL + 1 : 0;  // rows whose window can touch y0..y0+3
-            const int64_t vhi = (y0 + 3) / TL < V - 1 ? (y0 + 3) / TL : V - 1;
-            int terms = 0;
-            for (int64_t v = (vlo > 0 ? vlo - 1 : 0); v <= vhi; ++v) {
-                const int64_t x0 = y0 - v * TL;  // multiple of 4
-                if (x0 + 3 < 0 || x0 >= M) continue;
-                if (++terms == 500) {  // keep every 16-bit lane below 2^16 (500 x 126 + p)
-                    ev = ((ev & 0xFFFFu) % p) | (((ev >> 16) % p) << 16);
-                    od = ((od & 0xFFFFu) % p) | (((od >> 16) % p) << 16);
-                    terms = 1;
-                }
-                uint32_t w = *reinterpret_cast<const uint32_t*>(Ds + v * ldc + (x0 < 0 ? 0 : x0));
-                if (x0 < 0) w = 0;  // (x0 is a multiple of 4: a word is wholly inside or outside)
-                if (x0 + 3 >= M) w &= 0xFFFFFFFFu >> (8 * (x0 + 4 - M));  // bytes past the row end
-                ev += w & 0x00FF00FFu;
-                od += (w >> 8) & 0x00FF00FFu;
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int64_t y = y0 + j;
-            const uint32_t sum = ((j & 1) ? od : ev) >> (16 * (j >> 1)) & 0xFFFFu;
-            const uint32_t r = y < nfull ? sum % p : 0u;
-            if (y < ncoef) out[sidx * ncoef + y] = (uint8_t)r;
-            else if (r) atomicOr(flag, 2u);
-        }
-    }
-}
-
-// out[s][y] = sum_v E[s][v][y] mod p, E the GEMM's diagonal-shifted transpose
-// (E[v][x + v TL] = D[x][v]; entries outside [v TL, v TL + M) were never written and are
-// masked): a thread owns 16 consecutive y, one 16-byte load per row v, byte sums in
-// 16-bit lanes (V <= 500 terms of <= 126 between reductions)
 constexpr int OV_SPLIT = 8;  // threads per 16-output group (each sums every 8th row v)
 
 __global__ void toeplitz_overlap_diag_kernel(const uint8_t* __restrict__ E, int64_t batch, int64_t M, int64_t V,
@@ -2622,30 +2574,24 @@ __global__ void toeplitz_overlap_diag_kernel(const uint8_t* __restrict__ E, int6
     }
 }
 
-static bool tz_rows() {
-    static const int v = getenv("QADIC_TZ_ROWS") ? atoi(getenv("QADIC_TZ_ROWS")) : 1;
-    return v != 0;
-}
-
 static int tz_width() {
     static const int w = getenv("QADIC_TZ_L") ? atoi(getenv("QADIC_TZ_L")) : TL_DEFAULT;
     return (w >= 128 && w % 128 == 0) ? w : TL_DEFAULT;
 }
 static int64_t tz_pad_len(int64_t na, int TL) { return round_up(na + 2 * TL + 32, 16); }
-static int64_t tz_ldc(int64_t M) { return round_up(M, 16); }
 
 static size_t toeplitz_workspace(int64_t batch, int64_t na, int64_t nb) {
     const int TL = tz_width();
     const int64_t M = na + TL - 1, V = (nb + TL - 1) / TL;
     return (size_t)round_up(batch * tz_pad_len(na, TL), 1024) + (size_t)round_up(batch * M * TL, 1024) +
            (size_t)round_up(batch * V * TL, 1024) +
-           (size_t)round_up(batch * V * std::max(tz_ldc(M), round_up(M + (V - 1) * TL + 16, 16)), 1024) + 1024;
+           (size_t)round_up(batch * V * round_up(M + (V - 1) * TL + 16, 16), 1024) + 1024;
 }
 
 static int run_toeplitz(const uint8_t* a, int64_t na, const uint8_t* b, int64_t nb, int64_t batch, uint32_t p,
                         uint8_t* out, int64_t ncoef, void* ws, size_t ws_bytes, cudaStream_t s) {
     const int TL = tz_width();
-    const int64_t M = na + TL - 1, V = (nb + TL - 1) / TL, len = tz_pad_len(na, TL), ldc = tz_ldc(M);
+    const int64_t M = na + TL - 1, V = (nb + TL - 1) / TL, len = tz_pad_len(na, TL);
     QADIC_REQUIRE(ws && ws_bytes >= toeplitz_workspace(batch, na, nb), QADIC_ERR_VALUE, "workspace too small");
     QADIC_REQUIRE(batch * M < (1ll << 31) && batch * V < (1ll << 31), QADIC_ERR_UNSUPPORTED,
                   "batch x length beyond the TMA row range");
@@ -2653,8 +2599,8 @@ static int run_toeplitz(const uint8_t* a, int64_t na, const uint8_t* b, int64_t 
     uint8_t* T = apad + round_up(batch * len, 1024);
     uint8_t* Bv = T + round_up(batch * M * TL, 1024);
     uint8_t* Dt = Bv + round_up(batch * V * TL, 1024);
-    unsigned int* flag = reinterpret_cast<unsigned int*>(
-        Dt + round_up(batch * V * std::max(ldc, round_up(M + (V - 1) * TL + 16, 16)), 1024));
+    unsigned int* flag =
+        reinterpret_cast<unsigned int*>(Dt + round_up(batch * V * round_up(M + (V - 1) * TL + 16, 16), 1024));
     const int sms = num_sms();
     auto grid_of = [&](int64_t n) {
         return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 16));
@@ -2669,33 +2615,30 @@ static int run_toeplitz(const uint8_t* a, int64_t na, const uint8_t* b, int64_t 
     // 148 independent CTAs beat 74 pairs (measured 0.094 vs 0.103 ms per polylong batch)
     static const bool pair = getenv("QADIC_TZ_PAIR") && atoi(getenv("QADIC_TZ_PAIR")) != 0;
     constexpr int BN = Cfg<KIND_I8>::BN;
-    const bool rows = tz_rows();
-    // rows: GEMM rows = the M Toeplitz rows, columns = the V blocks of b (D[x][v]: every
-    // epilogue warp busy, V values per thread); else transposed, Dt[v][x]
-    // the diagonal-shifted layout: E[v][y] rows of lde >= M + (V - 1) TL + 16 bytes
+    // GEMM rows = the M Toeplitz rows, columns = the V blocks of b, stored as the
+    // diagonal-shifted transpose E[v][x + v TL] (rows of lde >= M + (V - 1) TL + 16 bytes)
     const int64_t lde = round_up(M + (V - 1) * TL + 16, 16);
-    const int64_t gm = rows ? M : V, gn = rows ? V : M, ldd = rows ? lde : ldc;
     CUtensorMap ta, tb;
-    rc = make_tmap(&ta, rows ? T : Bv, TL, batch * gm, TL, BM);
+    rc = make_tmap(&ta, T, TL, batch * M, TL, BM);
     if (rc) return rc;
-    rc = make_tmap(&tb, rows ? Bv : T, TL, batch * gn, TL, pair ? BN / 2 : BN);
+    rc = make_tmap(&tb, Bv, TL, batch * V, TL, pair ? BN / 2 : BN);
     if (rc) return rc;
     Params prm = {};
     prm.sf = e2m1_scale_word();
     prm.group_m = GROUP_M;
-    prm.M = gm;
-    prm.N = gn;
-    prm.ldc = ldd;
+    prm.M = M;
+    prm.N = V;
+    prm.ldc = lde;
     prm.p = p;
     prm.offset = p * ((1u << 25) / p + 1);
     prm.magic64 = wide_magic(p);
-    prm.m_tiles = (int)((gm + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM));
-    prm.n_tiles = (int)((gn + BN - 1) / BN);
-    prm.n_full = (int)(gn / BN);
+    prm.m_tiles = (int)((M + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM));
+    prm.n_tiles = (int)((V + BN - 1) / BN);
+    prm.n_full = (int)(V / BN);
     prm.num_kb = (int)((TL + BK - 1) / BK);
     prm.c = Dt;
-    prm.c_plane = rows ? V * lde : gm * ldd;
-    prm.diag_shift = rows ? TL : 0;
+    prm.c_plane = V * lde;
+    prm.diag_shift = TL;
     prm.planes = (int)batch;
     prm.nibble_out = 0;
     rc = pair ? launch_gemm<KIND_I8, true>(ta, tb, prm, s, "polymul toeplitz gemm")
@@ -2703,14 +2646,9 @@ static int run_toeplitz(const uint8_t* a, int64_t na, const uint8_t* b, int64_t 
     if (rc) return rc;
     cudaMemsetAsync(flag, 0, sizeof(unsigned int), s);
     const int64_t nfull = na + nb - 1;
-    if (rows)
-        QADIC_TIMED("polymul overlap", s,
-                    toeplitz_overlap_diag_kernel<<<grid_of(batch * ((std::max(nfull, ncoef) + 15) / 16) * OV_SPLIT), 256, 0, s>>>(
-                        Dt, batch, M, V, lde, p, nfull, ncoef, out, flag, TL));
-    else
-        QADIC_TIMED("polymul overlap", s,
-                    toeplitz_overlap_kernel<<<grid_of(batch * ((std::max(nfull, ncoef) + 3) / 4)), 256, 0, s>>>(
-                        Dt, batch, M, V, ldc, p, nfull, ncoef, out, flag, TL));
+    QADIC_TIMED("polymul overlap", s,
+                toeplitz_overlap_diag_kernel<<<grid_of(batch * ((std::max(nfull, ncoef) + 15) / 16) * OV_SPLIT), 256, 0, s>>>(
+                    Dt, batch, M, V, lde, p, nfull, ncoef, out, flag, TL));
     return check_launch("toeplitz overlap");
 }
 
