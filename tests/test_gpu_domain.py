@@ -280,3 +280,17 @@ def test_long_products_tensor_core_long_rows():
     tc = polymul.polymul_fqt_long_batch(a, b, prm, engine="tc")
     words = polymul.polymul_fqt_long_batch(a, b, prm, engine="words")
     assert np.array_equal(tc, words)
+
+
+def test_word_path_empty_and_tiny_shapes():
+    """the any-field word path on empty and 1 x 1 x 1 shapes (the reference returns
+    empty / exact results for these)."""
+    f = gfext.build_field(131, 1, max_dot_length=16)
+    assert f.matmul(np.zeros((0, 3), np.int64), np.zeros((3, 4), np.int64)).shape == (0, 4)
+    assert f.matmul(np.zeros((2, 3), np.int64), np.zeros((3, 0), np.int64)).shape == (2, 0)
+    assert f.fgdp_batch(np.zeros((0, 5), np.int64), np.zeros((0, 5), np.int64)).shape == (0,)
+    one = f.matmul(np.array([[5]]), np.array([[7]]))
+    assert int(one[0, 0]) == f.mul(f.elem(5), f.elem(7)).index
+    prm = cmm_params(257, 1, strict=True)
+    got = cmm.right_cmm(np.array([[200]]), cmm.compress_rows(np.array([[100]]), prm))
+    assert got.tolist() == [[200 * 100 % 257]]
