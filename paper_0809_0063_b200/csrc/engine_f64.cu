@@ -17,6 +17,8 @@
 // digit-reduced in registers (compress + correct + repack,
 // src/redq.py:318-332) -- the delayed-reduction fold of
 // src/polymul.py:198-208 without leaving the register file.
+#include <type_traits>
+
 #include "qadic_common.cuh"
 #include "qadic_internal.h"
 
@@ -63,6 +65,7 @@ struct Params {
     int64_t M, Nw, Kp, Np;   // logical rows, logical word columns, padded dims
     int64_t n_out;           // output entries per row (GF: N; CMM: N)
     int fold;                // 0 = none; else multiple of 4
+    int fold_mode;           // 0: fold_word; 1: fold_word_fast; 2: fast with lazy corrected digits
     int d;                   // CMM: digits per word - 1
     uint8_t* c;
 };
@@ -78,9 +81,39 @@ __device__ __forceinline__ double fold_word(double r, const FieldConst& f) {
     return (double)w;
 }
 
+// The same fold on the FP64 pipe where the generic one uses conversions (F2I /
+// I2F, quarter-rate, three per word -- they, not the DMMAs, bounded the fold
+// schedule): for an exact integer r < 2^51 (< the case-2 bound B, so no
+// correction step),
+//   bits(r + 2^52)                       = 0x433.. | r
+//   bits(RD(RN(r * RU(1/p)) + 2^52))     = 0x433.. | floor(RN(r * RU(1/p))) = s
+// then the REDQ digits u_i = lo32(r >> it) - p lo32(s >> it) (src/redq.py:58-85) and,
+// when the host cleared the budget for it (LAZY), the corrected digits are left
+// unreduced: mu_i = u_i + c u_{i+1} < p^2 is congruent to the reduced digit and the
+// next fold / the epilogue's REDQ sees it like any other digit sum.
+template <int ND, bool LAZY, int T>  // T > 0: the radix exponent f.t as a compile-time constant
+__device__ __forceinline__ double fold_word_fast(double r, const FieldConst& f) {
+    const int t = T > 0 ? T : (int)f.t;
+    constexpr double TWO52 = 4503599627370496.0;
+    constexpr uint64_t MANT = (1ull << 52) - 1;
+    const uint64_t rv = (uint64_t)__double_as_longlong(r + TWO52) & MANT;
+    const uint64_t sv = (uint64_t)__double_as_longlong(__dadd_rd(__dmul_rn(r, f.invp_up), TWO52)) & MANT;
+    uint32_t u[ND + 1];
+#pragma unroll
+    for (int i = 0; i <= ND; ++i) u[i] = (uint32_t)(rv >> (i * t)) - f.p * (uint32_t)(sv >> (i * t));
+    uint64_t w = u[ND];
+#pragma unroll
+    for (int i = ND - 1; i >= 0; --i) {
+        const uint32_t mu = u[i] + f.corr * u[i + 1];
+        w = (w << t) | (LAZY ? mu : mod_small(mu, f.p, f.magic));
+    }
+    return __longlong_as_double((long long)(w | 0x4330000000000000ull)) - TWO52;
+}
+
 // FOLD: the launch folds the packed accumulators every prm.fold terms (the fold
-// code is compiled only into the kernels that need it)
-template <int K, Epi EPI, bool SMEM_TABLES, bool FOLD>
+// code is compiled only into the kernels that need it): 0 none, else the
+// fold_mode_for() flavour + 1 (1 fold_word, 2 fold_word_fast, 3 fast and lazy)
+template <int K, Epi EPI, bool SMEM_TABLES, int FOLD>
 __global__ void __launch_bounds__(THREADS, 1) dmma_gemm_kernel(Params prm, FieldConst f) {
     constexpr int ND = EPI == EPI_GF ? 2 * K - 2 : (EPI == EPI_GF1 ? K - 1 : 0);
     extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -121,6 +154,25 @@ __global__ void __launch_bounds__(THREADS, 1) dmma_gemm_kernel(Params prm, Field
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
+    // the radix of this kernel's fold schedule as a compile-time constant (the
+    // generic runtime-t shifts of 64-bit words cost ~2x the integer instructions):
+    // two-sided DQT 2^(53/(2K-1)) (cfg5: 10), one-sided 2^min(53/K, 30)
+    constexpr int FOLD_T = EPI == EPI_GF ? 53 / (2 * K - 1) : (53 / K > 30 ? 30 : 53 / K);
+    auto fold_all = [&](auto tconst) {
+        constexpr int TT = decltype(tconst)::value;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    double& x = acc[i][j][h];
+                    if constexpr (FOLD == 3) x = fold_word_fast<ND, true, TT>(x, f);
+                    else if constexpr (FOLD == 2) x = fold_word_fast<ND, false, TT>(x, f);
+                    else x = fold_word<ND>(x, f);
+                }
+    };
+    (void)fold_all;
     const int nk = (int)(prm.Kp / BK);
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
@@ -157,18 +209,19 @@ __global__ void __launch_bounds__(THREADS, 1) dmma_gemm_kernel(Params prm, Field
 #pragma unroll
             for (int k4 = 0; k4 < BK / 4; ++k4) k4_step(k4);
         } else {
-#pragma unroll
+            // one copy of the DMMA step and of the fold code per radix case (the
+            // fully unrolled form held 4 x 32 inlined folds -- instruction cache)
+#pragma unroll 1
             for (int k4 = 0; k4 < BK / 4; ++k4) {
                 k4_step(k4);
                 const int64_t kdone = kbase + (k4 + 1) * 4;
                 if (kdone % prm.fold == 0 && kdone < prm.Kp) {
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            acc[i][j][0] = fold_word<ND>(acc[i][j][0], f);
-                            acc[i][j][1] = fold_word<ND>(acc[i][j][1], f);
-                        }
+                    if constexpr (FOLD >= 2) {
+                        if (f.t == (uint32_t)FOLD_T) fold_all(std::integral_constant<int, FOLD_T>{});
+                        else fold_all(std::integral_constant<int, 0>{});
+                    } else {
+                        fold_all(std::integral_constant<int, 0>{});
+                    }
                 }
             }
         }
@@ -308,15 +361,32 @@ static OneSided one_sided(uint32_t p, int k) {
 // two-sided fold periods below this make the in-register folds the bottleneck
 constexpr int ONE_SIDED_BELOW = 64;
 
+// fold flavour: fast when every folded word is below 2^51 (< the fdiv case-2 bound),
+// lazy when the unreduced corrected digits (< (p-1)(1+c)+1) still leave room for a
+// whole fold period of terms below q (per = per-term digit increment)
+static int fold_mode_for(const FieldConst& f, int nd, int fold, int64_t per) {
+    if (getenv("QADIC_F64_FOLD_MODE")) return atoi(getenv("QADIC_F64_FOLD_MODE"));
+    if ((int64_t)(nd + 1) * f.t > 51) return 0;
+    const int64_t q = 1ll << f.t;
+    return (int64_t)fold * per <= q - 1 - (int64_t)(f.p - 1) * (1 + f.corr) ? 2 : 1;
+}
+
 template <int K, Epi EPI>
 static int launch(const Params& prm, const FieldConst& f, cudaStream_t s) {
     const bool smem_tables = EPI == EPI_GF && (1 << (f.bb * K)) <= TABLE_MAX;
     const size_t smem = PIPE_BYTES + (smem_tables ? 2 * TABLE_MAX * sizeof(uint32_t) : 0);
     dim3 grid((unsigned)(prm.Np / BN), (unsigned)((prm.M + BM - 1) / BM));
     QADIC_REQUIRE(grid.y <= 65535, QADIC_ERR_UNSUPPORTED, "m too large");
-    const bool fold = (EPI == EPI_GF || EPI == EPI_GF1) && prm.fold;
-    auto kern = smem_tables ? (fold ? dmma_gemm_kernel<K, EPI, true, true> : dmma_gemm_kernel<K, EPI, true, false>)
-                            : (fold ? dmma_gemm_kernel<K, EPI, false, true> : dmma_gemm_kernel<K, EPI, false, false>);
+    const int fold = (EPI == EPI_GF || EPI == EPI_GF1) && prm.fold ? 1 + prm.fold_mode : 0;
+    auto pick = [&](auto tables) {
+        constexpr bool T = decltype(tables)::value;
+        if constexpr (EPI == EPI_CMM) return dmma_gemm_kernel<K, EPI, T, 0>;
+        else return fold == 3 ? dmma_gemm_kernel<K, EPI, T, 3>
+               : fold == 2 ? dmma_gemm_kernel<K, EPI, T, 2>
+               : fold == 1 ? dmma_gemm_kernel<K, EPI, T, 1>
+                           : dmma_gemm_kernel<K, EPI, T, 0>;
+    };
+    auto kern = smem_tables ? pick(std::true_type{}) : pick(std::false_type{});
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     QADIC_TIMED("f64 dmma gemm", s, kern<<<grid, THREADS, smem, s>>>(prm, f));
     return check_launch("f64 dmma gemm");
@@ -374,6 +444,7 @@ static int f64_gf_matmul_one_sided(const FieldConst& f, const uint8_t* a, const 
     prm.Np = Np1;
     prm.n_out = n * k * k;
     prm.fold = kdim > o.fold ? o.fold : 0;
+    prm.fold_mode = fold_mode_for(f1, k - 1, prm.fold, (int64_t)(f.p - 1) * (f.p - 1));
     prm.d = k - 1;
     prm.c = T;
     switch (k) {
@@ -423,6 +494,7 @@ int f64_gf_matmul(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64
     prm.Np = Np;
     prm.n_out = n;
     prm.fold = fold;
+    prm.fold_mode = fold_mode_for(f, 2 * (int)f.k - 2, fold, (int64_t)f.k * (f.p - 1) * (f.p - 1));
     prm.d = 0;
     prm.c = c;
     switch (f.k) {
@@ -466,6 +538,7 @@ int f64_right_cmm(const uint8_t* a, const uint8_t* b, int64_t m, int64_t kdim, i
     prm.Np = Np;
     prm.n_out = n;
     prm.fold = 0;
+    prm.fold_mode = 0;
     prm.d = d;
     prm.c = c;
     return launch<1, EPI_CMM>(prm, f, s);

@@ -140,6 +140,37 @@ def test_f64_two_sided_fold_path():
     _child(_F64_FOLD_CHILD, {"QADIC_F64_ONE_SIDED": "0"}, "fold ok")
 
 
+# every fold flavour (QADIC_F64_FOLD_MODE, read per call): 0 the conversion-based
+# REDQ fold, 1 the FP64-pipe fold, 2 the FP64-pipe fold with lazily corrected
+# digits (the default where the budget allows it) -- two-sided (cfg5's schedule,
+# all-maximal digits at every fold) and one-sided (fold every 3636 at q = 2^17)
+_F64_FOLD_MODES_CHILD = r"""
+import os, sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from oracle import qadic_oracle as O
+from paper_0809_0063_b200 import workloads as W
+f = W.field_for(W.CONFIGS[5])
+of = O.build_field(7, 3, irreducible=[5, 0, 0, 1], max_dot_length=9)
+g = W.rng(77)
+a = g.integers(0, 7, (40, 7800, 3), dtype=np.uint8)
+b = g.integers(0, 7, (7800, 24, 3), dtype=np.uint8)
+want = O.gf_matmul_planes(of, a, b)
+am = np.full((8, 4104, 3), 6, np.uint8)
+bm = np.full((4104, 8, 3), 6, np.uint8)
+want_m = O.gf_matmul_planes(of, am, bm)
+for mode in ("0", "1", "2"):
+    os.environ["QADIC_F64_FOLD_MODE"] = mode
+    for eng in ("f64-fold", "f64"):
+        assert np.array_equal(f.matmul_coeffs(a, b, engine=eng), want), (mode, eng)
+        assert np.array_equal(f.matmul_coeffs(am, bm, engine=eng), want_m), (mode, eng, "max")
+print("fold modes ok")
+"""
+
+
+def test_f64_fold_flavours():
+    _child(_F64_FOLD_MODES_CHILD, {}, "fold modes ok")
+
+
 # ---------------------------------------------------------------------------
 # k = 1 B planes: vector path on partial tiles, unaligned B, the TMA variant
 # ---------------------------------------------------------------------------
