@@ -2753,7 +2753,9 @@ int tc_matmul_u64(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_t m, 
         base.n_full = (int)(n / BN);
         base.seg_kpb = (int)(kp / BK);
         base.seg_kp = (int)kp;
-        base.group_m = GROUP_M;
+        // raster group of 8 m tiles (a squarer wave: fewer operand re-reads of the long
+        // segmented K from DRAM; 9.62-9.70 vs 9.74-9.76 ms at 8192^3 for 16)
+        base.group_m = getenv("QADIC_U64_GROUP_M") ? std::max(1, atoi(getenv("QADIC_U64_GROUP_M"))) : 8;
         base.c64 = c;
         if (getenv_flag("QADIC_U64_INNER")) {
             // one launch: every shift s of an output tile back to back on one CTA pair
