@@ -140,6 +140,10 @@ struct Params {
     // i = seg_i_lo + segment; A is read at byte offset i * seg_kp + (kb % seg_kpb) * BK
     // of its row, B at row offset (seg_s - i) * N.  seg_kpb = 0: contiguous K.
     int seg_kpb, seg_i_lo, seg_s, seg_kp;
+    // uint64 byte planes with the significant-byte counts resolved on the device:
+    // seg_dev[0] / [1] = bytes of A / B that can be nonzero; the launch derives its
+    // shift's segments (seg_i_lo, num_kb) from them and exits when it has none
+    const int* seg_dev;
     // plane_inner: all byte shifts of one output tile run back to back on one CTA
     // (pair) in a single launch -- shift s = plane index, its segments
     // seg_lo[s] .. seg_lo[s] + seg_cnt[s] - 1, C accumulated in program order
@@ -211,6 +215,13 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
     static_assert(!MC || (PAIR && FUSE_K == 0), "multicast needs the CTA-pair, unfused kernel");
     // MC: work units cover two m tiles (one per pair of the cluster)
     Params prm = prm_in;
+    if (KIND == KIND_I8 && prm.seg_dev != nullptr) {
+        const int nba = prm.seg_dev[0], nbb = prm.seg_dev[1], sp = prm.seg_s;
+        const int i_lo = sp - (nbb - 1) > 0 ? sp - (nbb - 1) : 0, i_hi = sp < nba - 1 ? sp : nba - 1;
+        if (i_hi < i_lo) return;  // every byte product of this shift is zero: C unchanged
+        prm.seg_i_lo = i_lo;
+        prm.num_kb = (i_hi - i_lo + 1) * prm.seg_kpb;
+    }
     if (MC) {
         prm.m_tiles = (prm_in.m_tiles + 1) / 2;
         pdl_trigger();  // the concurrent tail launch may take the SMs no 4-CTA cluster fits on
@@ -2135,7 +2146,9 @@ __device__ __forceinline__ void u64x16_byte_planes(const uint64_t (&v)[16], uint
 // Thread: 16 consecutive kk of one row (one 16-byte store per plane).
 __global__ void __launch_bounds__(256) u64_aplanes_kernel(const uint64_t* __restrict__ a, int64_t M, int64_t K,
                                                           int64_t k0, int64_t kc, int nba, int64_t kp,
-                                                          uint8_t* __restrict__ out) {
+                                                          uint8_t* __restrict__ out, const int* __restrict__ plan) {
+    // plan (device): planes past A's significant bytes are never read -- not written
+    const int nw = plan ? plan[0] : nba;
     const int64_t per_row = kp / 16;
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= M * per_row) return;
@@ -2158,7 +2171,7 @@ __global__ void __launch_bounds__(256) u64_aplanes_kernel(const uint64_t* __rest
     uint8_t* dst = out + m * (nba * kp) + kk0;
 #pragma unroll
     for (int i = 0; i < 8; ++i)
-        if (i < nba) *reinterpret_cast<uint4*>(dst + i * kp) = pl[i];
+        if (i < nba && i < nw) *reinterpret_cast<uint4*>(dst + i * kp) = pl[i];
 }
 
 // B [K][N] uint64, rows k0 .. k0+kc -> transposed byte planes:
@@ -2168,8 +2181,9 @@ __global__ void __launch_bounds__(256) u64_aplanes_kernel(const uint64_t* __rest
 // 128-byte line of a plane row.
 __global__ void __launch_bounds__(256) u64_btplanes_kernel(const uint64_t* __restrict__ b, int64_t K, int64_t N,
                                                            int64_t k0, int64_t kc, int nbb, int64_t kp,
-                                                           uint8_t* __restrict__ out) {
+                                                           uint8_t* __restrict__ out, const int* __restrict__ plan) {
     __shared__ uint64_t tile[128][33];
+    const int nw = plan ? plan[1] : nbb;
     const int64_t n0 = (int64_t)blockIdx.x * 32, kk0 = (int64_t)blockIdx.y * 128;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
 #pragma unroll 4
@@ -2189,7 +2203,7 @@ __global__ void __launch_bounds__(256) u64_btplanes_kernel(const uint64_t* __res
     uint8_t* dst = out + n * kp + kk0 + 16 * g;
 #pragma unroll
     for (int j = 0; j < 8; ++j)
-        if (j < nbb) *reinterpret_cast<uint4*>(dst + (int64_t)j * N * kp) = pl[j];
+        if (j < nbb && j < nw) *reinterpret_cast<uint4*>(dst + (int64_t)j * N * kp) = pl[j];
 }
 
 // OR of every word (significant byte count of the operand)
@@ -2200,6 +2214,14 @@ __global__ void u64_or_kernel(const uint64_t* __restrict__ x, int64_t n, unsigne
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) v |= __shfl_xor_sync(0xffffffffu, v, off);
     if ((threadIdx.x & 31) == 0 && v) atomicOr(acc, (unsigned long long)v);
+}
+
+// significant bytes of the two ORs (at least 1) -> plan[0], plan[1]
+__global__ void u64_plan_kernel(const unsigned long long* __restrict__ ors, int* __restrict__ plan) {
+    if (threadIdx.x < 2) {
+        const unsigned long long v = ors[threadIdx.x];
+        plan[threadIdx.x] = v ? (63 - __clzll((long long)v)) / 8 + 1 : 1;
+    }
 }
 
 
@@ -2667,65 +2689,43 @@ bool tc_u64_ok(int64_t m, int64_t k, int64_t n, const void* a) {
     return m >= 128 && n >= 128 && k >= 16 && (k % 2 == 0) && ((reinterpret_cast<uintptr_t>(a) & 15) == 0);
 }
 
-static int sig_bytes(uint64_t v) {
-    int nb = 1;
-    while (nb < 8 && (v >> (8 * nb))) ++nb;
-    return nb;
-}
-
 int tc_matmul_u64(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_t m, int64_t k, int64_t n,
                   cudaStream_t s) {
     using namespace tc;
     constexpr int64_t KC = 16384;  // 4 * KC * 255^2 < 2^32
-    int dev = 0;
-    cudaGetDevice(&dev);
     keep_mempool();
-    // pinned landing slot for the operands' OR: one per host thread and device, so
-    // concurrent callers never read each other's significant-byte counts
-    thread_local unsigned long long* host_or_slot[64] = {};
-    unsigned long long*& host_or = host_or_slot[dev & 63];
-    if (!host_or) {
-        if (cudaHostAlloc(reinterpret_cast<void**>(&host_or), 2 * sizeof(unsigned long long), cudaHostAllocDefault) !=
-            cudaSuccess)
-            host_or = nullptr;
-        cudaGetLastError();
-    }
-    // significant bytes of each operand: only byte planes that can be nonzero are multiplied
-    // (packed words of the reference's drivers have 5 -- 34 bits at cfg3 -- instead of 8)
-    // (one stream synchronisation; skipped -- all 8 bytes -- while the stream is being captured)
-    unsigned long long* dor = nullptr;
-    int nba = 8, nbb = 8;
-    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(s, &cap);
-    if (host_or && cap == cudaStreamCaptureStatusNone &&
-        cudaMallocAsync(reinterpret_cast<void**>(&dor), 2 * sizeof(unsigned long long), s) == cudaSuccess) {
-        cudaMemsetAsync(dor, 0, 2 * sizeof(unsigned long long), s);
-        QADIC_TIMED("u64 or", s, u64_or_kernel<<<1024, 256, 0, s>>>(a, m * k, dor));
-        QADIC_TIMED("u64 or", s, u64_or_kernel<<<1024, 256, 0, s>>>(b, k * n, dor + 1));
-        cudaMemcpyAsync(host_or, dor, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
-        cudaFreeAsync(dor, s);
-        if (cudaStreamSynchronize(s) == cudaSuccess) {
-            nba = sig_bytes(host_or[0]);
-            nbb = sig_bytes(host_or[1]);
-        }
-        cudaGetLastError();
-    }
     // D_s = sum_{i+j=s} A_i B_j^T over the byte planes that can be nonzero (i < nba,
     // j < nbb): plane s runs one GEMM whose K'' is the concatenation of its valid
     // segments (A plane i against B plane s-i), so only the nonzero byte products
-    // are issued -- sum_s #{i} = 24 per word MAC at 5 + 5 bytes, not 8 x 5.
-    const int nplanes = nba + nbb - 1 < 8 ? nba + nbb - 1 : 8;  // shifts 8s >= 64 vanish mod 2^64
+    // are issued -- sum_s #{i} = 24 per word MAC at 5 + 5 bytes, not 36.  nba / nbb
+    // (the operands' significant bytes: 5 for the reference drivers' packed words)
+    // are found on the device -- an OR reduction and a plan the GEMM launches read --
+    // so the call stays asynchronous on the caller's stream and capturable; the byte
+    // planes are laid out for all 8 bytes (the insignificant ones are zeros nobody reads).
+    // The opt-in single-launch form (QADIC_U64_INNER) keeps host-side segment tables
+    // and multiplies all 8 x 8 byte pairs.
+    const bool inner = getenv_flag("QADIC_U64_INNER");
+    const int nba = 8, nbb = 8;  // plane layout (and the inner form's segment tables)
+    const int nplanes = 8;       // shifts 8s >= 64 vanish mod 2^64
     const int64_t kc_max = k < KC ? k : KC;
     const int64_t kp = (kc_max + BK - 1) / BK * BK;  // segment length (bytes), BK-aligned
     const size_t abytes = (size_t)m * nba * kp, bbytes = (size_t)nbb * n * kp;
     uint8_t* ws = nullptr;
-    if (cudaMallocAsync(reinterpret_cast<void**>(&ws), abytes + bbytes, s) != cudaSuccess) {
+    if (cudaMallocAsync(reinterpret_cast<void**>(&ws), abytes + bbytes + 64, s) != cudaSuccess) {
         cudaGetLastError();
         set_error(QADIC_ERR_CUDA, "matmul_exact_u64: cannot allocate %zu bytes of byte planes", abytes + bbytes);
         return QADIC_ERR_CUDA;
     }
     uint8_t* a8 = ws;
     uint8_t* bt = ws + abytes;
+    unsigned long long* dor = reinterpret_cast<unsigned long long*>(ws + abytes + bbytes);
+    int* plan = reinterpret_cast<int*>(dor + 2);
+    if (!inner) {
+        cudaMemsetAsync(dor, 0, 2 * sizeof(unsigned long long), s);
+        QADIC_TIMED("u64 or", s, u64_or_kernel<<<1024, 256, 0, s>>>(a, m * k, dor));
+        QADIC_TIMED("u64 or", s, u64_or_kernel<<<1024, 256, 0, s>>>(b, k * n, dor + 1));
+        QADIC_TIMED("u64 or", s, u64_plan_kernel<<<1, 32, 0, s>>>(dor, plan));
+    }
     const bool pair = pair_mode();
     constexpr int BN = Cfg<KIND_I8>::BN;
     int rc = check_launch("u64 prepare");
@@ -2733,9 +2733,10 @@ int tc_matmul_u64(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_t m, 
         const int64_t kc = (k - k0 < KC) ? k - k0 : KC;
         const int64_t ta = m * (kp / 16);
         QADIC_TIMED("u64 byte planes A", s,
-                    u64_aplanes_kernel<<<(unsigned)((ta + 255) / 256), 256, 0, s>>>(a, m, k, k0, kc, nba, kp, a8));
+                    u64_aplanes_kernel<<<(unsigned)((ta + 255) / 256), 256, 0, s>>>(a, m, k, k0, kc, nba, kp, a8,
+                                                                                    inner ? nullptr : plan));
         dim3 grid((unsigned)((n + 31) / 32), (unsigned)(kp / 128));
-        QADIC_TIMED("u64 byte planes B", s, u64_btplanes_kernel<<<grid, 256, 0, s>>>(b, k, n, k0, kc, nbb, kp, bt));
+        QADIC_TIMED("u64 byte planes B", s, u64_btplanes_kernel<<<grid, 256, 0, s>>>(b, k, n, k0, kc, nbb, kp, bt, inner ? nullptr : plan));
         rc = check_launch("u64 byte planes");
         if (rc) break;
         CUtensorMap ta_map, tb_map;
@@ -2757,7 +2758,7 @@ int tc_matmul_u64(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_t m, 
         // segmented K from DRAM; 9.62-9.70 vs 9.74-9.76 ms at 8192^3 for 16)
         base.group_m = getenv("QADIC_U64_GROUP_M") ? std::max(1, atoi(getenv("QADIC_U64_GROUP_M"))) : 8;
         base.c64 = c;
-        if (getenv_flag("QADIC_U64_INNER")) {
+        if (inner) {
             // one launch: every shift s of an output tile back to back on one CTA pair
             // (no per-launch tails; C accumulated in program order by the same threads).
             // Measured slower (8192^3: 11.0 vs 10.6 ms): a tile's segments of all shifts
@@ -2779,12 +2780,11 @@ int tc_matmul_u64(const uint64_t* a, const uint64_t* b, uint64_t* c, int64_t m, 
             continue;
         }
         for (int sp = 0; sp < nplanes && rc == QADIC_OK; ++sp) {  // one launch per shift (default)
-            const int i_lo = sp - (nbb - 1) > 0 ? sp - (nbb - 1) : 0;
-            const int i_hi = sp < nba - 1 ? sp : nba - 1;
             Params prm = base;
-            prm.seg_i_lo = i_lo;
+            prm.seg_dev = plan;  // segments of shift sp from the device plan (shift 0 always has one)
             prm.seg_s = sp;
-            prm.num_kb = (i_hi - i_lo + 1) * prm.seg_kpb;
+            prm.seg_kpb = base.seg_kpb;
+            prm.num_kb = base.seg_kpb;  // placeholder; the kernel derives it
             prm.planes = 1;
             prm.shift = 8 * sp;
             prm.acc64 = (sp > 0 || k0 > 0) ? 1 : 0;

@@ -58,6 +58,44 @@ class TestLayerK:
         zero = np.zeros((k, n), np.uint64)
         assert not _kernels.matmul_exact_u64(a, zero).any()
 
+    def test_matmul_u64_async_and_capturable(self):
+        """the C-ABI call on device buffers neither synchronises the caller's stream
+        (the significant-byte plan is resolved on the device) nor breaks stream
+        capture: queued behind a ~0.3 s device sleep it returns at once, and a CUDA
+        graph of it replays to the same words."""
+        import time
+
+        import torch
+
+        from paper_0809_0063_b200 import _native as N
+
+        L = N.lib()
+        g = np.random.default_rng(11)
+        m, k, n = 256, 384, 320
+        ah = g.integers(0, 1 << 34, (m, k), dtype=np.uint64)
+        bh = g.integers(0, 1 << 20, (k, n), dtype=np.uint64)
+        want = O.matmul_exact_u64(ah, bh)
+        a = torch.from_numpy(ah.view(np.int64)).cuda()
+        b = torch.from_numpy(bh.view(np.int64)).cuda()
+        c = torch.empty((m, n), dtype=torch.int64, device="cuda")
+        side = torch.cuda.Stream()
+        with torch.cuda.stream(side):
+            N.check(L.qadic_matmul_exact_u64(N.ptr(a), N.ptr(b), N.ptr(c), m, k, n, N.stream_ptr()))  # warm
+            torch.cuda._sleep(600_000_000)  # ~0.3 s of device time queued ahead of the call
+            t0 = time.perf_counter()
+            N.check(L.qadic_matmul_exact_u64(N.ptr(a), N.ptr(b), N.ptr(c), m, k, n, N.stream_ptr()))
+            dt = time.perf_counter() - t0
+        side.synchronize()
+        assert dt < 0.1, f"the call blocked for {dt:.3f} s"
+        assert np.array_equal(c.cpu().numpy().view(np.uint64), want)
+        c.zero_()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=side):
+            N.check(L.qadic_matmul_exact_u64(N.ptr(a), N.ptr(b), N.ptr(c), m, k, n, N.stream_ptr()))
+        graph.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(c.cpu().numpy().view(np.uint64), want)
+
     def test_matmul_mod(self, golden):
         for chunk in (7, 64, 10**6):
             c = _kernels.matmul_mod_i64(golden["k_mm_mod_a"], golden["k_mm_mod_b"], 7, chunk)
