@@ -28,7 +28,10 @@ int make_field_const(const qadic_field_desc* d, FieldConst* f);
 
 namespace f64 {
 
-constexpr int BM = 128, BN = 128, BK = 16;
+#ifndef QADIC_F64_BK
+#define QADIC_F64_BK 32
+#endif
+constexpr int BM = 128, BN = 128, BK = QADIC_F64_BK;  // BK 32: half the block barriers of 16
 constexpr int SA = BK + 4;   // A smem row pitch (doubles): conflict-free fragment loads
 constexpr int SB = BN + 4;   // B smem row pitch (doubles)
 constexpr int STAGES = 3;
@@ -66,6 +69,7 @@ struct Params {
     int64_t n_out;           // output entries per row (GF: N; CMM: N)
     int fold;                // 0 = none; else multiple of 4
     int fold_mode;           // 0: fold_word; 1: fold_word_fast; 2: fast with lazy corrected digits
+    int group_m;             // row blocks per raster group
     int d;                   // CMM: digits per word - 1
     uint8_t* c;
 };
@@ -120,11 +124,22 @@ __global__ void __launch_bounds__(THREADS, 1) dmma_gemm_kernel(Params prm, Field
     double* sA = reinterpret_cast<double*>(smem_raw);
     double* sB = sA + STAGES * BM * SA;
     uint32_t* s_l = reinterpret_cast<uint32_t*>(sB + STAGES * BK * SB);
-    uint32_t* s_h = s_l + TABLE_MAX;
+    const int tsize = EPI == EPI_GF && SMEM_TABLES ? 1 << (f.bb * K) : 0;
+    uint32_t* s_h = s_l + tsize;
 
     const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
     const int wm = warp / 4, wn = warp % 4;
-    const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+    // grouped raster: consecutive blocks sweep prm.group_m row blocks of A per column
+    // block of B, so a B column panel (K x 128 words) is reused from L2 by group_m row
+    // blocks instead of streamed from DRAM once per row block
+    int64_t m0, n0;
+    {
+        const int nt = (int)gridDim.x, mt = (int)gridDim.y, gm = prm.group_m > 0 ? prm.group_m : 1;
+        const int id = (int)(blockIdx.y * gridDim.x + blockIdx.x);
+        const int per = gm * nt, grp = id / per, first = grp * gm, g = min(mt - first, gm), r = id % per;
+        m0 = (int64_t)(first + r % g) * BM;
+        n0 = (int64_t)(r / g) * BN;
+    }
 
     if (EPI == EPI_GF && SMEM_TABLES) {
         const int size = 1 << (f.bb * K);
@@ -139,7 +154,7 @@ __global__ void __launch_bounds__(THREADS, 1) dmma_gemm_kernel(Params prm, Field
         double* b_s = sB + slot * BK * SB;
         // A: 128 rows x 16 doubles = 1024 16-byte chunks; B: 16 rows x 128 doubles
 #pragma unroll
-        for (int it = 0; it < 2; ++it) {
+        for (int it = 0; it < BK / 8; ++it) {  // (BM x BK + BK x BN) doubles / 2 per chunk / THREADS
             const int c = tid + it * THREADS;
             const int r = c / (BK / 2), q = c % (BK / 2);
             cp_async16(a_s + r * SA + 2 * q, prm.a + (m0 + r) * prm.Kp + k0 + 2 * q);
@@ -372,9 +387,13 @@ static int fold_mode_for(const FieldConst& f, int nd, int fold, int64_t per) {
 }
 
 template <int K, Epi EPI>
-static int launch(const Params& prm, const FieldConst& f, cudaStream_t s) {
-    const bool smem_tables = EPI == EPI_GF && (1 << (f.bb * K)) <= TABLE_MAX;
-    const size_t smem = PIPE_BYTES + (smem_tables ? 2 * TABLE_MAX * sizeof(uint32_t) : 0);
+static int launch(const Params& prm_in, const FieldConst& f, cudaStream_t s) {
+    Params prm = prm_in;
+    prm.group_m = getenv("QADIC_F64_GROUP_M") ? atoi(getenv("QADIC_F64_GROUP_M")) : 8;
+    // L/H tables in shared memory when they fit next to the pipeline (cfg5: 2 x 512 entries)
+    const size_t tbytes = 2 * ((size_t)1 << (f.bb * K)) * sizeof(uint32_t);
+    const bool smem_tables = EPI == EPI_GF && (1 << (f.bb * K)) <= TABLE_MAX && PIPE_BYTES + tbytes <= 227 * 1024;
+    const size_t smem = PIPE_BYTES + (smem_tables ? tbytes : 0);
     dim3 grid((unsigned)(prm.Np / BN), (unsigned)((prm.M + BM - 1) / BM));
     QADIC_REQUIRE(grid.y <= 65535, QADIC_ERR_UNSUPPORTED, "m too large");
     const int fold = (EPI == EPI_GF || EPI == EPI_GF1) && prm.fold ? 1 + prm.fold_mode : 0;
