@@ -21,6 +21,7 @@ for c in 3 4 5; do
 done
 $B --config 3 --engine f64 --steps 3 --warmup 3 > $O/bench_cfg3_f64.json 2>>$O/bench.err || ok=0
 $B --config 5 --engine f64 --steps 3 --warmup 3 > $O/bench_cfg5_f64.json 2>>$O/bench.err || ok=0
+python bench.py --config 5 --steps 20 --no-cpu-baseline --no-sustained > $O/bench_cfg5_variants.json 2>>$O/bench.err || ok=0
 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $O/launch_cmd.json 2>>$O/bench.err && \
   $NCU --metrics gpu__time_duration.sum -c 400 --csv --log-file $O/launches_cfg5.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
@@ -39,7 +40,10 @@ full cfg3_fp4k_gemm 3 auto gemm_modp
 full cfg4_fp4k_gemm 4 auto gemm_modp
 full cfg1_polymul 1 auto polymul
 full cfg2_gf_dot 2 auto gf_dot
-full polylong polylong auto conv_tile
+full polylong polylong auto gemm_modp
+full cfg5_f64_dmma 5 f64 dmma_gemm
+full cfg5_f64fold_dmma 5 f64-fold dmma_gemm
+python tools/mm64_profile.py > /dev/null 2>&1 && $NCU --metrics gpu__time_duration.sum,sm__cycles_elapsed.avg.per_second,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed -k regex:gemm_modp -c 8 --csv --log-file $O/mm64_launches.csv python tools/mm64_profile.py > /dev/null 2>&1
 python bench.py --config redq --steps 3 > /dev/null 2>&1 && $NCU --set full -k regex:redq_vec -s 2 -c 1 -o $O/redq -f python bench.py --config redq --steps 3 > $O/redq.log 2>&1
 ncu -i $O/redq.ncu-rep --page raw --csv > $O/redq_raw.csv 2>/dev/null
 full cfg5_i8_gemm 5 i8 gemm_modp
