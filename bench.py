@@ -599,12 +599,20 @@ def measure_variants(args, cfg, engine, meta, units, work, peaks, peak_src, torc
         pr = pipe_probe(N, "f64", 0.1)
         if "burst" in pr:
             peaks = dict(peaks, f64_probe_tflops=pr["burst"])
-    for eng in ("i8k", "i8", "f64", "f64-fold"):
+    # the two-sided fold schedule (cfg5's own, fold every <= 9 terms) twice: with the
+    # default intermediate fold (the digit-wise pseudo-Mersenne fold, 2^6 = 1 mod 7) and
+    # with the paper's REDQ as the fold (QADIC_F64_FOLD_MODE=2: FP64-pipe REDQ, lazily
+    # corrected digits); the epilogue's final reduction is REDQ in both
+    fold_note = {"f64-fold": "intermediate folds: digit-wise pseudo-Mersenne (d mod 2^6 + d >> 6, 2^6 = 1 mod 7)",
+                 "f64-fold-redq": "intermediate folds: REDQ (FP64 reciprocal, lazily corrected digits)"}
+    for eng in ("i8k", "i8", "f64", "f64-fold", "f64-fold-redq"):
         if eng == engine or (eng == "i8k" and cfg == 4):  # k = 1: i8k only adds conversions
             continue
-        if eng == "f64-fold" and cfg != 5:  # the two-sided fold schedule is cfg5's own (fold every 9)
+        if eng.startswith("f64-fold") and cfg != 5:  # the two-sided fold schedule is cfg5's own (fold every 9)
             continue
-        step = meta["variant_step"](eng)
+        step = meta["variant_step"]("f64-fold" if eng.startswith("f64-fold") else eng)
+        if eng == "f64-fold-redq":
+            os.environ["QADIC_F64_FOLD_MODE"] = "2"
         try:
             step(0)
             torch.cuda.synchronize()
@@ -634,18 +642,23 @@ def measure_variants(args, cfg, engine, meta, units, work, peaks, peak_src, torc
             if eng == "f64" and cfg in (3, 5):
                 c_ = W.CONFIGS[cfg]
                 w["f64_fmas"] = w["madds"] * (c_.k if cfg == 5 else 1)
-            if eng == "f64-fold":  # two-sided: one FMA per GF mult-add (+ the folds, ALU work)
+            if eng.startswith("f64-fold"):  # two-sided: one FMA per GF mult-add (+ the folds, ALU work)
                 w["f64_fmas"] = w["madds"]
             if eng == "f64" and cfg == 4:
                 n = W.CONFIGS[4].shape[0]
                 w["f64_fmas"] = n * n * (-(-n // 3))
-            roof = roofline(cfg, eng, kname, prof.get(kname), w, peaks, peak_src, steps=k)
+            roof = roofline(cfg, "f64-fold" if eng.startswith("f64-fold") else eng, kname, prof.get(kname), w,
+                            peaks, peak_src, steps=k)
             out[eng] = {"ms_per_step": round(ms, 4), "value": units / (ms / 1e3), "steps": k,
                         "kernel": kname, "achieved": roof["achieved"] if roof else None,
                         "unit": roof["unit"] if roof else None, "frac": roof["frac"] if roof else None,
                         "kernels_ms_per_step": {kk: round(v[1] / k, 4) for kk, v in prof.items()}}
+            if eng in fold_note:
+                out[eng]["fold"] = fold_note[eng]
         except Exception as exc:  # pragma: no cover - report, never fail the headline line
             out[eng] = {"error": str(exc)[:200]}
+        finally:
+            os.environ.pop("QADIC_F64_FOLD_MODE", None)
     return out
 
 

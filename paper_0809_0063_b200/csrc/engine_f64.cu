@@ -35,7 +35,16 @@ constexpr int BM = 128, BN = 128, BK = QADIC_F64_BK;  // BK 32: half the block b
 constexpr int SA = BK + 4;   // A smem row pitch (doubles): conflict-free fragment loads
 constexpr int SB = BN + 4;   // B smem row pitch (doubles)
 constexpr int STAGES = 3;
-constexpr int THREADS = 512;  // 16 warps, 4 (M) x 4 (N), 32x32 per warp
+// warps along M (x 4 along N): WM = 2 -- 8 warps of 64 x 32 (32 DMMAs per 12 fragment
+// loads, 238 registers) for plain and pseudo-Mersenne-fold kernels; WM = 4 -- 16 warps of
+// 32 x 32 (128 registers) where the REDQ fold's temporaries would spill the 64-accumulator tile
+template <int WM>
+struct WarpTile {
+    static constexpr int THREADS = 32 * WM * 4;
+    static constexpr int MI = BM / (WM * 8);  // m8 fragments per warp
+};
+template <int FOLD>
+constexpr int wm_for_fold() { return FOLD >= 1 ? 4 : 2; }
 constexpr int TABLE_MAX = 4096;
 constexpr size_t PIPE_BYTES = (size_t)STAGES * (BM * SA + BK * SB) * sizeof(double);
 
@@ -70,6 +79,9 @@ struct Params {
     int fold;                // 0 = none; else multiple of 4
     int fold_mode;           // 0: fold_word; 1: fold_word_fast; 2: fast with lazy corrected digits
     int group_m;             // row blocks per raster group
+    uint64_t pm_lo, pm_hi;   // fold mode 3: lane masks (2^e - 1, 2^(t-e) - 1 at every digit)
+    int pm_e;
+    uint32_t pm_c;           // 2^e mod p
     int d;                   // CMM: digits per word - 1
     uint8_t* c;
 };
@@ -114,11 +126,30 @@ __device__ __forceinline__ double fold_word_fast(double r, const FieldConst& f) 
     return __longlong_as_double((long long)(w | 0x4330000000000000ull)) - TWO52;
 }
 
+// Digit-wise pseudo-Mersenne fold (fold mode 3): when 2^e = c (mod p) with c small
+// (cfg5: p = 7, 2^6 = 1), every digit d of the word (lanes of t bits, d < 2^t) maps
+// to (d mod 2^e) + c (d >> e) -- congruent mod p and at most (2^e - 1) + c ((2^t - 1) >> e)
+// (cfg5: 78) -- on the whole word at once: two masks, a shift, an add (no lane
+// carries: every new lane value is below 2^t), no quotient.  The intermediate folds
+// only have to keep the digits congruent and below the budget; the epilogue's REDQ
+// produces the reduced result.  For words below 2^52 (the 2^52 offset carries them).
+__device__ __forceinline__ double fold_word_pm(double r, uint64_t mlo, uint64_t mhi, int e, uint32_t c) {
+    constexpr double TWO52 = 4503599627370496.0;
+    const uint64_t w = (uint64_t)__double_as_longlong(r + TWO52);  // the exponent bits lie outside both masks
+    uint64_t hi = (w >> e) & mhi;
+    if (c != 1) hi *= c;
+    const uint64_t x = (w & mlo) + hi;
+    return __longlong_as_double((long long)(x | 0x4330000000000000ull)) - TWO52;
+}
+
 // FOLD: the launch folds the packed accumulators every prm.fold terms (the fold
 // code is compiled only into the kernels that need it): 0 none, else the
-// fold_mode_for() flavour + 1 (1 fold_word, 2 fold_word_fast, 3 fast and lazy)
+// fold_mode_for() flavour + 1 (1 fold_word, 2 fold_word_fast, 3 fast and lazy,
+// 4 the pseudo-Mersenne digit fold)
 template <int K, Epi EPI, bool SMEM_TABLES, int FOLD>
-__global__ void __launch_bounds__(THREADS, 1) dmma_gemm_kernel(Params prm, FieldConst f) {
+__global__ void __launch_bounds__(WarpTile<wm_for_fold<FOLD>()>::THREADS, 1) dmma_gemm_kernel(Params prm, FieldConst f) {
+    constexpr int THREADS = WarpTile<wm_for_fold<FOLD>()>::THREADS;
+    constexpr int MI = WarpTile<wm_for_fold<FOLD>()>::MI;
     constexpr int ND = EPI == EPI_GF ? 2 * K - 2 : (EPI == EPI_GF1 ? K - 1 : 0);
     extern __shared__ __align__(16) uint8_t smem_raw[];
     double* sA = reinterpret_cast<double*>(smem_raw);
@@ -154,7 +185,7 @@ __global__ void __launch_bounds__(THREADS, 1) dmma_gemm_kernel(Params prm, Field
         double* b_s = sB + slot * BK * SB;
         // A: 128 rows x 16 doubles = 1024 16-byte chunks; B: 16 rows x 128 doubles
 #pragma unroll
-        for (int it = 0; it < BK / 8; ++it) {  // (BM x BK + BK x BN) doubles / 2 per chunk / THREADS
+        for (int it = 0; it < BM * BK / 2 / THREADS; ++it) {  // BM x BK (= BK x BN) doubles, 2 per chunk
             const int c = tid + it * THREADS;
             const int r = c / (BK / 2), q = c % (BK / 2);
             cp_async16(a_s + r * SA + 2 * q, prm.a + (m0 + r) * prm.Kp + k0 + 2 * q);
@@ -163,9 +194,9 @@ __global__ void __launch_bounds__(THREADS, 1) dmma_gemm_kernel(Params prm, Field
         }
     };
 
-    double acc[4][4][2];
+    double acc[MI][4][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < MI; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
@@ -176,13 +207,14 @@ __global__ void __launch_bounds__(THREADS, 1) dmma_gemm_kernel(Params prm, Field
     auto fold_all = [&](auto tconst) {
         constexpr int TT = decltype(tconst)::value;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < MI; ++i)
 #pragma unroll
             for (int j = 0; j < 4; ++j)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     double& x = acc[i][j][h];
-                    if constexpr (FOLD == 3) x = fold_word_fast<ND, true, TT>(x, f);
+                    if constexpr (FOLD == 4) x = fold_word_pm(x, prm.pm_lo, prm.pm_hi, prm.pm_e, prm.pm_c);
+                    else if constexpr (FOLD == 3) x = fold_word_fast<ND, true, TT>(x, f);
                     else if constexpr (FOLD == 2) x = fold_word_fast<ND, false, TT>(x, f);
                     else x = fold_word<ND>(x, f);
                 }
@@ -200,16 +232,16 @@ __global__ void __launch_bounds__(THREADS, 1) dmma_gemm_kernel(Params prm, Field
         __syncthreads();
         if (kt + STAGES - 1 < nk) load_stage((kt + STAGES - 1) % STAGES, (int64_t)(kt + STAGES - 1) * BK);
         cp_async_commit();
-        const double* a_s = sA + (kt % STAGES) * BM * SA + (wm * 32 + ar) * SA + ac;
+        const double* a_s = sA + (kt % STAGES) * BM * SA + (wm * (MI * 8) + ar) * SA + ac;
         const double* b_s = sB + (kt % STAGES) * BK * SB + ac * SB + wn * 32 + ar;
         auto k4_step = [&](int k4) {
-            double af[4], bf[4];
+            double af[MI], bf[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) af[i] = a_s[i * 8 * SA + k4 * 4];
+            for (int i = 0; i < MI; ++i) af[i] = a_s[i * 8 * SA + k4 * 4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) bf[j] = b_s[k4 * 4 * SB + j * 8];
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < MI; ++i)
 #pragma unroll
                 for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
         };
@@ -223,6 +255,20 @@ __global__ void __launch_bounds__(THREADS, 1) dmma_gemm_kernel(Params prm, Field
         if (!fold_here) {
 #pragma unroll
             for (int k4 = 0; k4 < BK / 4; ++k4) k4_step(k4);
+        } else if (prm.fold == 8 && (kbase % 8) == 0 && kbase + BK < prm.Kp) {
+            // cfg5's schedule (fold every 8 terms, a stage boundary on a fold boundary, no
+            // fold at the very end): pairs of unrolled DMMA k-steps, one fold code copy
+#pragma unroll 1
+            for (int k8 = 0; k8 < BK / 8; ++k8) {
+                k4_step(2 * k8);
+                k4_step(2 * k8 + 1);
+                if constexpr (FOLD == 2 || FOLD == 3) {
+                    if (f.t == (uint32_t)FOLD_T) fold_all(std::integral_constant<int, FOLD_T>{});
+                    else fold_all(std::integral_constant<int, 0>{});
+                } else {
+                    fold_all(std::integral_constant<int, 0>{});
+                }
+            }
         } else {
             // one copy of the DMMA step and of the fold code per radix case (the
             // fully unrolled form held 4 x 32 inlined folds -- instruction cache)
@@ -231,7 +277,7 @@ __global__ void __launch_bounds__(THREADS, 1) dmma_gemm_kernel(Params prm, Field
                 k4_step(k4);
                 const int64_t kdone = kbase + (k4 + 1) * 4;
                 if (kdone % prm.fold == 0 && kdone < prm.Kp) {
-                    if constexpr (FOLD >= 2) {
+                    if constexpr (FOLD == 2 || FOLD == 3) {
                         if (f.t == (uint32_t)FOLD_T) fold_all(std::integral_constant<int, FOLD_T>{});
                         else fold_all(std::integral_constant<int, 0>{});
                     } else {
@@ -248,8 +294,8 @@ __global__ void __launch_bounds__(THREADS, 1) dmma_gemm_kernel(Params prm, Field
     const uint32_t* ltab = SMEM_TABLES ? s_l : f.l_table;
     const uint32_t* htab = SMEM_TABLES ? s_h : f.h_table;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int64_t row = m0 + wm * 32 + i * 8 + ar;
+    for (int i = 0; i < MI; ++i) {
+        const int64_t row = m0 + wm * (MI * 8) + i * 8 + ar;
         if (row >= prm.M) continue;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -379,10 +425,36 @@ constexpr int ONE_SIDED_BELOW = 64;
 // fold flavour: fast when every folded word is below 2^51 (< the fdiv case-2 bound),
 // lazy when the unreduced corrected digits (< (p-1)(1+c)+1) still leave room for a
 // whole fold period of terms below q (per = per-term digit increment)
-static int fold_mode_for(const FieldConst& f, int nd, int fold, int64_t per) {
-    if (getenv("QADIC_F64_FOLD_MODE")) return atoi(getenv("QADIC_F64_FOLD_MODE"));
-    if ((int64_t)(nd + 1) * f.t > 51) return 0;
+static int fold_mode_for(const FieldConst& f, int nd, int fold, int64_t per, Params* prm = nullptr) {
     const int64_t q = 1ll << f.t;
+    // pseudo-Mersenne digit fold: the split point e with the smallest post-fold digit bound
+    int best_e = 0;
+    int64_t best_b = q;
+    if ((int64_t)(nd + 1) * f.t <= 52 && fold > 0) {
+        for (int e = 1; e < (int)f.t; ++e) {
+            const int64_t c = (1ll << e) % f.p;
+            const int64_t b = ((1ll << e) - 1) + c * ((q - 1) >> e);
+            if (b < best_b && (int64_t)fold * per <= q - 1 - b) {
+                best_b = b;
+                best_e = e;
+            }
+        }
+    }
+    if (prm && best_e) {
+        prm->pm_e = best_e;
+        prm->pm_c = (uint32_t)((1ll << best_e) % f.p);
+        prm->pm_lo = prm->pm_hi = 0;
+        for (int i = 0; i <= nd; ++i) {
+            prm->pm_lo |= ((1ull << best_e) - 1) << (i * f.t);
+            prm->pm_hi |= ((1ull << (f.t - best_e)) - 1) << (i * f.t);
+        }
+    }
+    if (getenv("QADIC_F64_FOLD_MODE")) {
+        const int m = atoi(getenv("QADIC_F64_FOLD_MODE"));
+        return m == 3 && !best_e ? 2 : m;
+    }
+    if (best_e) return 3;
+    if ((int64_t)(nd + 1) * f.t > 51) return 0;
     return (int64_t)fold * per <= q - 1 - (int64_t)(f.p - 1) * (1 + f.corr) ? 2 : 1;
 }
 
@@ -400,14 +472,16 @@ static int launch(const Params& prm_in, const FieldConst& f, cudaStream_t s) {
     auto pick = [&](auto tables) {
         constexpr bool T = decltype(tables)::value;
         if constexpr (EPI == EPI_CMM) return dmma_gemm_kernel<K, EPI, T, 0>;
-        else return fold == 3 ? dmma_gemm_kernel<K, EPI, T, 3>
+        else return fold == 4 ? dmma_gemm_kernel<K, EPI, T, 4>
+               : fold == 3 ? dmma_gemm_kernel<K, EPI, T, 3>
                : fold == 2 ? dmma_gemm_kernel<K, EPI, T, 2>
                : fold == 1 ? dmma_gemm_kernel<K, EPI, T, 1>
                            : dmma_gemm_kernel<K, EPI, T, 0>;
     };
     auto kern = smem_tables ? pick(std::true_type{}) : pick(std::false_type{});
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    QADIC_TIMED("f64 dmma gemm", s, kern<<<grid, THREADS, smem, s>>>(prm, f));
+    const int threads = fold >= 1 ? WarpTile<4>::THREADS : WarpTile<2>::THREADS;  // wm_for_fold
+    QADIC_TIMED("f64 dmma gemm", s, kern<<<grid, threads, smem, s>>>(prm, f));
     return check_launch("f64 dmma gemm");
 }
 
@@ -463,7 +537,7 @@ static int f64_gf_matmul_one_sided(const FieldConst& f, const uint8_t* a, const 
     prm.Np = Np1;
     prm.n_out = n * k * k;
     prm.fold = kdim > o.fold ? o.fold : 0;
-    prm.fold_mode = fold_mode_for(f1, k - 1, prm.fold, (int64_t)(f.p - 1) * (f.p - 1));
+    prm.fold_mode = fold_mode_for(f1, k - 1, prm.fold, (int64_t)(f.p - 1) * (f.p - 1), &prm);
     prm.d = k - 1;
     prm.c = T;
     switch (k) {
@@ -513,7 +587,7 @@ int f64_gf_matmul(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64
     prm.Np = Np;
     prm.n_out = n;
     prm.fold = fold;
-    prm.fold_mode = fold_mode_for(f, 2 * (int)f.k - 2, fold, (int64_t)f.k * (f.p - 1) * (f.p - 1));
+    prm.fold_mode = fold_mode_for(f, 2 * (int)f.k - 2, fold, (int64_t)f.k * (f.p - 1) * (f.p - 1), &prm);
     prm.d = 0;
     prm.c = c;
     switch (f.k) {

@@ -142,7 +142,8 @@ def test_f64_two_sided_fold_path():
 
 # every fold flavour (QADIC_F64_FOLD_MODE, read per call): 0 the conversion-based
 # REDQ fold, 1 the FP64-pipe fold, 2 the FP64-pipe fold with lazily corrected
-# digits (the default where the budget allows it) -- two-sided (cfg5's schedule,
+# digits, 3 the digit-wise pseudo-Mersenne fold (the default where a split point
+# fits the budget: cfg5 two-sided; the one-sided form falls back to 2) -- two-sided (cfg5's schedule,
 # all-maximal digits at every fold) and one-sided (fold every 3636 at q = 2^17)
 _F64_FOLD_MODES_CHILD = r"""
 import os, sys, numpy as np
@@ -158,7 +159,7 @@ want = O.gf_matmul_planes(of, a, b)
 am = np.full((8, 4104, 3), 6, np.uint8)
 bm = np.full((4104, 8, 3), 6, np.uint8)
 want_m = O.gf_matmul_planes(of, am, bm)
-for mode in ("0", "1", "2"):
+for mode in ("0", "1", "2", "3"):
     os.environ["QADIC_F64_FOLD_MODE"] = mode
     for eng in ("f64-fold", "f64"):
         assert np.array_equal(f.matmul_coeffs(a, b, engine=eng), want), (mode, eng)
