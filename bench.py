@@ -599,20 +599,27 @@ def measure_variants(args, cfg, engine, meta, units, work, peaks, peak_src, torc
         pr = pipe_probe(N, "f64", 0.1)
         if "burst" in pr:
             peaks = dict(peaks, f64_probe_tflops=pr["burst"])
-    # the two-sided fold schedule (cfg5's own, fold every <= 9 terms) twice: with the
-    # default intermediate fold (the digit-wise pseudo-Mersenne fold, 2^6 = 1 mod 7) and
-    # with the paper's REDQ as the fold (QADIC_F64_FOLD_MODE=2: FP64-pipe REDQ, lazily
-    # corrected digits); the epilogue's final reduction is REDQ in both
-    fold_note = {"f64-fold": "intermediate folds: digit-wise pseudo-Mersenne (d mod 2^6 + d >> 6, 2^6 = 1 mod 7)",
-                 "f64-fold-redq": "intermediate folds: REDQ (FP64 reciprocal, lazily corrected digits)"}
-    for eng in ("i8k", "i8", "f64", "f64-fold", "f64-fold-redq"):
+    # cfg5's FP64 forms: "f64" is the engine's own choice (the paper's two-sided DQT
+    # schedule -- q = 2^10 words, a fold every 8 <= 9 terms -- with digit-wise
+    # pseudo-Mersenne intermediate folds, 2^6 = 1 mod 7); "f64-fold-redq" the same
+    # schedule with REDQ as the intermediate fold (QADIC_F64_FOLD_MODE=2: FP64-pipe REDQ,
+    # lazily corrected digits); "f64-one-sided" the one-sided DQT form (A packed, B's
+    # coefficient planes side by side, a fold every 3636 terms).  The final reduction
+    # is the epilogue's REDQ + L/H fold in every form.
+    fold_note = {"f64": "two-sided DQT q=2^10, fold every 8 terms; intermediate folds digit-wise "
+                        "pseudo-Mersenne (d mod 2^6 + d >> 6, 2^6 = 1 mod 7)",
+                 "f64-fold-redq": "two-sided DQT q=2^10, fold every 8 terms; intermediate folds REDQ "
+                                  "(FP64 reciprocal, lazily corrected digits)",
+                 "f64-one-sided": "one-sided DQT q=2^17 (B's coefficient planes side by side), fold every 3636 terms"}
+    env_for = {"f64-fold-redq": ("QADIC_F64_FOLD_MODE", "2"), "f64-one-sided": ("QADIC_F64_ONE_SIDED", "1")}
+    for eng in ("i8k", "i8", "f64", "f64-fold-redq", "f64-one-sided"):
         if eng == engine or (eng == "i8k" and cfg == 4):  # k = 1: i8k only adds conversions
             continue
-        if eng.startswith("f64-fold") and cfg != 5:  # the two-sided fold schedule is cfg5's own (fold every 9)
+        if eng in env_for and cfg != 5:  # the two-sided fold schedule is cfg5's own (fold every 9)
             continue
-        step = meta["variant_step"]("f64-fold" if eng.startswith("f64-fold") else eng)
-        if eng == "f64-fold-redq":
-            os.environ["QADIC_F64_FOLD_MODE"] = "2"
+        step = meta["variant_step"]("f64-fold" if eng == "f64-fold-redq" else ("f64" if eng.startswith("f64") else eng))
+        if eng in env_for:
+            os.environ[env_for[eng][0]] = env_for[eng][1]
         try:
             step(0)
             torch.cuda.synchronize()
@@ -639,15 +646,15 @@ def measure_variants(args, cfg, engine, meta, units, work, peaks, peak_src, torc
             prof = parse_prof(buf.value.decode())
             kname = dominant_kernel(cfg, eng, prof)
             w = dict(work)
-            if eng == "f64" and cfg in (3, 5):
+            if eng == "f64-one-sided" or (eng == "f64" and cfg == 3):  # one-sided: k FMAs per GF mult-add
                 c_ = W.CONFIGS[cfg]
                 w["f64_fmas"] = w["madds"] * (c_.k if cfg == 5 else 1)
-            if eng.startswith("f64-fold"):  # two-sided: one FMA per GF mult-add (+ the folds, ALU work)
+            if eng in ("f64", "f64-fold-redq") and cfg == 5:  # two-sided: one FMA per GF mult-add (+ the folds)
                 w["f64_fmas"] = w["madds"]
             if eng == "f64" and cfg == 4:
                 n = W.CONFIGS[4].shape[0]
                 w["f64_fmas"] = n * n * (-(-n // 3))
-            roof = roofline(cfg, "f64-fold" if eng.startswith("f64-fold") else eng, kname, prof.get(kname), w,
+            roof = roofline(cfg, "f64" if eng.startswith("f64") else eng, kname, prof.get(kname), w,
                             peaks, peak_src, steps=k)
             out[eng] = {"ms_per_step": round(ms, 4), "value": units / (ms / 1e3), "steps": k,
                         "kernel": kname, "achieved": roof["achieved"] if roof else None,
@@ -658,7 +665,8 @@ def measure_variants(args, cfg, engine, meta, units, work, peaks, peak_src, torc
         except Exception as exc:  # pragma: no cover - report, never fail the headline line
             out[eng] = {"error": str(exc)[:200]}
         finally:
-            os.environ.pop("QADIC_F64_FOLD_MODE", None)
+            if eng in env_for:
+                os.environ.pop(env_for[eng][0], None)
     return out
 
 
@@ -917,10 +925,11 @@ def run_ours(args):
         avg_src = "timed region / K (one launch per step)"
     work = meta["work"]
     if engine == "f64" and cfg in (3, 5):
-        # cfg5 runs the one-sided DQT form (two-sided would fold every 8 terms):
-        # k FP64 FMAs per GF mult-add; cfg3 the two-sided form, one FMA each
+        # the two-sided DQT form (cfg3; cfg5 with its pseudo-Mersenne folds every 8 terms):
+        # one FP64 FMA per GF mult-add; the one-sided form (QADIC_F64_ONE_SIDED=1) k of them
         c_ = W.CONFIGS[cfg]
-        work["f64_fmas"] = work["madds"] * (c_.k if cfg == 5 else 1)
+        one_sided = cfg == 5 and os.environ.get("QADIC_F64_ONE_SIDED", "0") not in ("", "0")
+        work["f64_fmas"] = work["madds"] * (c_.k if one_sided else 1)
     if engine == "f64" and cfg == 4:
         n = W.CONFIGS[4].shape[0]
         work["f64_fmas"] = (n // ws) * n * (-(-n // 3))

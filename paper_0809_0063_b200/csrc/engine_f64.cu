@@ -563,12 +563,14 @@ int f64_gf_matmul(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64
     using namespace f64;
     const int64_t Mp = rup(m, BM), Kp = rup(kdim, BK), Np = rup(n, BN);
     QADIC_REQUIRE(ws && ws_bytes >= f64_gf_workspace(m, kdim, n, (int)f.k), QADIC_ERR_VALUE, "workspace too small");
-    // the two-sided DQT form with in-register REDQ folds every `fold` terms is the paper's
-    // own schedule (cfg5: q = 2^10, fold every 8 <= 9 terms); below ONE_SIDED_BELOW it is
-    // ALU-bound, so AUTO picks the one-sided form unless asked (engine flag / env)
+    // the two-sided DQT form with in-register folds every `fold` terms is the paper's own
+    // schedule (cfg5: q = 2^10, fold every 8 <= 9 terms).  Below ONE_SIDED_BELOW its REDQ
+    // folds make it ALU-bound, so AUTO takes the one-sided form -- unless the cheap
+    // digit-wise pseudo-Mersenne fold applies (cfg5: 70 vs 111 ms) or asked (engine flag / env)
     const char* env = getenv("QADIC_F64_ONE_SIDED");
+    const bool pm = fold > 0 && fold_mode_for(f, 2 * (int)f.k - 2, fold, (int64_t)f.k * (f.p - 1) * (f.p - 1)) == 3;
     const bool one = two_sided ? false
-                               : (env ? atoi(env) != 0 : (fold > 0 && fold < ONE_SIDED_BELOW && f.k > 1));
+                               : (env ? atoi(env) != 0 : (fold > 0 && fold < ONE_SIDED_BELOW && f.k > 1 && !pm));
     if (one) return f64_gf_matmul_one_sided(f, a, b, m, kdim, n, ws, c, s);
     double* aw = static_cast<double*>(ws);
     double* bw = aw + Mp * Kp;
