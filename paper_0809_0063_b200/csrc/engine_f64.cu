@@ -107,12 +107,15 @@ __device__ __forceinline__ double fold_word(double r, const FieldConst& f) {
 // when the host cleared the budget for it (LAZY), the corrected digits are left
 // unreduced: mu_i = u_i + c u_{i+1} < p^2 is congruent to the reduced digit and the
 // next fold / the epilogue's REDQ sees it like any other digit sum.
+// `acc` is a BIASED accumulator (2^52 + r, see dmma_gemm_kernel): its bit pattern is
+// 0x433.. | r, so r needs no conversion and the folded word goes back as bits.
 template <int ND, bool LAZY, int T>  // T > 0: the radix exponent f.t as a compile-time constant
-__device__ __forceinline__ double fold_word_fast(double r, const FieldConst& f) {
+__device__ __forceinline__ double fold_word_fast(double acc, const FieldConst& f) {
     const int t = T > 0 ? T : (int)f.t;
     constexpr double TWO52 = 4503599627370496.0;
     constexpr uint64_t MANT = (1ull << 52) - 1;
-    const uint64_t rv = (uint64_t)__double_as_longlong(r + TWO52) & MANT;
+    const uint64_t rv = (uint64_t)__double_as_longlong(acc) & MANT;
+    const double r = acc - TWO52;
     const uint64_t sv = (uint64_t)__double_as_longlong(__dadd_rd(__dmul_rn(r, f.invp_up), TWO52)) & MANT;
     uint32_t u[ND + 1];
 #pragma unroll
@@ -123,7 +126,7 @@ __device__ __forceinline__ double fold_word_fast(double r, const FieldConst& f) 
         const uint32_t mu = u[i] + f.corr * u[i + 1];
         w = (w << t) | (LAZY ? mu : mod_small(mu, f.p, f.magic));
     }
-    return __longlong_as_double((long long)(w | 0x4330000000000000ull)) - TWO52;
+    return __longlong_as_double((long long)(w | 0x4330000000000000ull));
 }
 
 // Digit-wise pseudo-Mersenne fold (fold mode 3): when 2^e = c (mod p) with c small
@@ -133,13 +136,13 @@ __device__ __forceinline__ double fold_word_fast(double r, const FieldConst& f) 
 // carries: every new lane value is below 2^t), no quotient.  The intermediate folds
 // only have to keep the digits congruent and below the budget; the epilogue's REDQ
 // produces the reduced result.  For words below 2^52 (the 2^52 offset carries them).
-__device__ __forceinline__ double fold_word_pm(double r, uint64_t mlo, uint64_t mhi, int e, uint32_t c) {
-    constexpr double TWO52 = 4503599627370496.0;
-    const uint64_t w = (uint64_t)__double_as_longlong(r + TWO52);  // the exponent bits lie outside both masks
+// On the biased accumulator (bits 0x433.. | r): integer instructions only.
+__device__ __forceinline__ double fold_word_pm(double acc, uint64_t mlo, uint64_t mhi, int e, uint32_t c) {
+    const uint64_t w = (uint64_t)__double_as_longlong(acc);  // the exponent bits lie outside both masks
     uint64_t hi = (w >> e) & mhi;
     if (c != 1) hi *= c;
     const uint64_t x = (w & mlo) + hi;
-    return __longlong_as_double((long long)(x | 0x4330000000000000ull)) - TWO52;
+    return __longlong_as_double((long long)(x | 0x4330000000000000ull));
 }
 
 // FOLD: the launch folds the packed accumulators every prm.fold terms (the fold
@@ -194,11 +197,17 @@ __global__ void __launch_bounds__(WarpTile<wm_for_fold<FOLD>()>::THREADS, 1) dmm
         }
     };
 
+    // Fast-fold kernels accumulate on a 2^52 bias: the DMMA sums stay exact integers in
+    // [2^52, 2^53) (every word < 2^51), the bit pattern of 2^52 + r is 0x433.. | r, so the
+    // folds read and write words as bits (no conversion, no FP64 instruction in the
+    // pseudo-Mersenne fold); the epilogue removes the bias.
+    constexpr bool BIAS = FOLD >= 2;
+    constexpr double ACC0 = BIAS ? 4503599627370496.0 : 0.0;
     double acc[MI][4][2];
 #pragma unroll
     for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = ACC0;
 
     // the radix of this kernel's fold schedule as a compile-time constant (the
     // generic runtime-t shifts of 64-bit words cost ~2x the integer instructions):
@@ -303,7 +312,7 @@ __global__ void __launch_bounds__(WarpTile<wm_for_fold<FOLD>()>::THREADS, 1) dmm
             for (int h = 0; h < 2; ++h) {
                 const int64_t col = n0 + wn * 32 + j * 8 + ac * 2 + h;  // word column
                 if (col >= prm.Nw) continue;
-                const double r = acc[i][j][h];
+                const double r = BIAS ? acc[i][j][h] - ACC0 : acc[i][j][h];
                 if (EPI == EPI_GF) {
                     uint32_t u[ND + 1];
                     redq_compress_f64<ND>(r, f.invp_up, (double)f.p, f.bound, f.p, (int)f.t, u);
