@@ -79,9 +79,9 @@ struct Params {
     int fold;                // 0 = none; else multiple of 4
     int fold_mode;           // 0: fold_word; 1: fold_word_fast; 2: fast with lazy corrected digits
     int group_m;             // row blocks per raster group
-    uint64_t pm_lo, pm_hi;   // fold mode 3: lane masks (2^e - 1, 2^(t-e) - 1 at every digit)
+    uint64_t pm_hi;          // fold mode 3: lane mask 2^(t-e) - 1 at every digit
     int pm_e;
-    uint32_t pm_c;           // 2^e mod p
+    uint32_t pm_m;           // 2^e - (2^e mod p)
     int d;                   // CMM: digits per word - 1
     uint8_t* c;
 };
@@ -132,17 +132,19 @@ __device__ __forceinline__ double fold_word_fast(double acc, const FieldConst& f
 // Digit-wise pseudo-Mersenne fold (fold mode 3): when 2^e = c (mod p) with c small
 // (cfg5: p = 7, 2^6 = 1), every digit d of the word (lanes of t bits, d < 2^t) maps
 // to (d mod 2^e) + c (d >> e) -- congruent mod p and at most (2^e - 1) + c ((2^t - 1) >> e)
-// (cfg5: 78) -- on the whole word at once: two masks, a shift, an add (no lane
+// (cfg5: 78) -- on the whole word at once: a shift, a mask, a multiply-subtract (no lane
 // carries: every new lane value is below 2^t), no quotient.  The intermediate folds
 // only have to keep the digits congruent and below the budget; the epilogue's REDQ
 // produces the reduced result.  For words below 2^52 (the 2^52 offset carries them).
-// On the biased accumulator (bits 0x433.. | r): integer instructions only.
-__device__ __forceinline__ double fold_word_pm(double acc, uint64_t mlo, uint64_t mhi, int e, uint32_t c) {
-    const uint64_t w = (uint64_t)__double_as_longlong(acc);  // the exponent bits lie outside both masks
-    uint64_t hi = (w >> e) & mhi;
-    if (c != 1) hi *= c;
-    const uint64_t x = (w & mlo) + hi;
-    return __longlong_as_double((long long)(x | 0x4330000000000000ull));
+// On the biased accumulator (bits 0x433.. | r): integer instructions only.  With
+// hi = the digits' high parts d >> e, the folded word is w - (2^e - c) hi (each lane
+// d - 2^e (d >> e) + c (d >> e)): one mask and one multiply-subtract on the FMA pipe
+// instead of two masks and an add on the ALU pipe, and the exponent bits of w pass
+// through untouched (hi stays below bit 50, no lane goes negative).
+__device__ __forceinline__ double fold_word_pm(double acc, uint64_t mhi, int e, uint32_t m) {
+    const uint64_t w = (uint64_t)__double_as_longlong(acc);  // the exponent bits lie outside the mask
+    const uint64_t hi = (w >> e) & mhi;
+    return __longlong_as_double((long long)(w - (uint64_t)m * hi));
 }
 
 // FOLD: the launch folds the packed accumulators every prm.fold terms (the fold
@@ -222,13 +224,25 @@ __global__ void __launch_bounds__(WarpTile<wm_for_fold<FOLD>()>::THREADS, 1) dmm
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     double& x = acc[i][j][h];
-                    if constexpr (FOLD == 4) x = fold_word_pm(x, prm.pm_lo, prm.pm_hi, prm.pm_e, prm.pm_c);
+                    if constexpr (FOLD == 4) x = fold_word_pm(x, prm.pm_hi, prm.pm_e, prm.pm_m);
                     else if constexpr (FOLD == 3) x = fold_word_fast<ND, true, TT>(x, f);
                     else if constexpr (FOLD == 2) x = fold_word_fast<ND, false, TT>(x, f);
                     else x = fold_word<ND>(x, f);
                 }
     };
     (void)fold_all;
+    auto fold_now = [&]() {
+        if constexpr (FOLD == 2 || FOLD == 3) {
+            if (f.t == (uint32_t)FOLD_T) fold_all(std::integral_constant<int, FOLD_T>{});
+            else fold_all(std::integral_constant<int, 0>{});
+        } else {
+            fold_all(std::integral_constant<int, 0>{});
+        }
+    };
+    (void)fold_now;
+    // fold phase of this warp (see the fold-8 stage loop): every accumulator still folds
+    // at most every prm.fold terms, the odd warps' first fold comes after 4
+    const int fold_off = (FOLD && prm.fold == 8 && (warp & 1)) ? 4 : 0;
     const int nk = (int)(prm.Kp / BK);
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
@@ -266,17 +280,28 @@ __global__ void __launch_bounds__(WarpTile<wm_for_fold<FOLD>()>::THREADS, 1) dmm
             for (int k4 = 0; k4 < BK / 4; ++k4) k4_step(k4);
         } else if (prm.fold == 8 && (kbase % 8) == 0 && kbase + BK < prm.Kp) {
             // cfg5's schedule (fold every 8 terms, a stage boundary on a fold boundary, no
-            // fold at the very end): pairs of unrolled DMMA k-steps, one fold code copy
+            // fold at the very end): pairs of unrolled DMMA k-steps, one fold code copy.
+            // Odd warps fold half a period later (fold_off = 4), so at any time half the
+            // warps feed the DMMA pipe while the other half run the integer fold (with
+            // every warp folding at the same k-steps the block alternated between a
+            // DMMA-only and an ALU-only phase)
+            if (fold_off == 0) {
 #pragma unroll 1
-            for (int k8 = 0; k8 < BK / 8; ++k8) {
-                k4_step(2 * k8);
-                k4_step(2 * k8 + 1);
-                if constexpr (FOLD == 2 || FOLD == 3) {
-                    if (f.t == (uint32_t)FOLD_T) fold_all(std::integral_constant<int, FOLD_T>{});
-                    else fold_all(std::integral_constant<int, 0>{});
-                } else {
-                    fold_all(std::integral_constant<int, 0>{});
+                for (int k8 = 0; k8 < BK / 8; ++k8) {
+                    k4_step(2 * k8);
+                    k4_step(2 * k8 + 1);
+                    fold_now();
                 }
+            } else {
+                k4_step(0);
+                fold_now();
+#pragma unroll 1
+                for (int k8 = 0; k8 < BK / 8 - 1; ++k8) {
+                    k4_step(2 * k8 + 1);
+                    k4_step(2 * k8 + 2);
+                    fold_now();
+                }
+                k4_step(BK / 4 - 1);
             }
         } else {
             // one copy of the DMMA step and of the fold code per radix case (the
@@ -285,14 +310,7 @@ __global__ void __launch_bounds__(WarpTile<wm_for_fold<FOLD>()>::THREADS, 1) dmm
             for (int k4 = 0; k4 < BK / 4; ++k4) {
                 k4_step(k4);
                 const int64_t kdone = kbase + (k4 + 1) * 4;
-                if (kdone % prm.fold == 0 && kdone < prm.Kp) {
-                    if constexpr (FOLD == 2 || FOLD == 3) {
-                        if (f.t == (uint32_t)FOLD_T) fold_all(std::integral_constant<int, FOLD_T>{});
-                        else fold_all(std::integral_constant<int, 0>{});
-                    } else {
-                        fold_all(std::integral_constant<int, 0>{});
-                    }
-                }
+                if ((kdone - fold_off) % prm.fold == 0 && kdone < prm.Kp) fold_now();
             }
         }
     }
@@ -451,12 +469,9 @@ static int fold_mode_for(const FieldConst& f, int nd, int fold, int64_t per, Par
     }
     if (prm && best_e) {
         prm->pm_e = best_e;
-        prm->pm_c = (uint32_t)((1ll << best_e) % f.p);
-        prm->pm_lo = prm->pm_hi = 0;
-        for (int i = 0; i <= nd; ++i) {
-            prm->pm_lo |= ((1ull << best_e) - 1) << (i * f.t);
-            prm->pm_hi |= ((1ull << (f.t - best_e)) - 1) << (i * f.t);
-        }
+        prm->pm_m = (uint32_t)((1ll << best_e) - (1ll << best_e) % f.p);
+        prm->pm_hi = 0;
+        for (int i = 0; i <= nd; ++i) prm->pm_hi |= ((1ull << (f.t - best_e)) - 1) << (i * f.t);
     }
     if (getenv("QADIC_F64_FOLD_MODE")) {
         const int m = atoi(getenv("QADIC_F64_FOLD_MODE"));
