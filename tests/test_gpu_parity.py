@@ -706,3 +706,65 @@ def test_fp4k_multicast_variant():
     r = subprocess.run([sys.executable, "-c", _MCAST_CHILD, root], env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "mcast ok" in r.stdout, r.stderr[-2000:]
+
+
+# ---------------------------------------------------------------------------
+# Seeded random sweep: fields x shapes x engines x buffer kinds against the oracle
+# ---------------------------------------------------------------------------
+_SWEEP_FIELDS = [(2, 1), (2, 2), (2, 4), (3, 1), (3, 2), (3, 3), (5, 1), (5, 2), (5, 3), (7, 1), (7, 2),
+                 (7, 3), (11, 1), (11, 2), (13, 2), (31, 1), (127, 1)]
+
+
+@pytest.mark.parametrize("case", range(160))
+def test_random_sweep_matmul(case):
+    """Seeded draw per case: a field, ragged M/K/N (1..260; every 7th case a long inner
+    dimension up to 9000 with small M/N), an engine, host or device operands -- bit-exact
+    against the oracle's plane product; an engine that cannot hold the field or the inner
+    dimension must refuse with ParamsViolation."""
+    import torch
+
+    from paper_0809_0063_b200.gfext import build_field
+
+    g = np.random.default_rng(9000 + case)
+    p, k = _SWEEP_FIELDS[int(g.integers(len(_SWEEP_FIELDS)))]
+    m, kd, n = (int(x) for x in g.integers(1, 261, 3))
+    if case % 7 == 3:
+        m, n, kd = int(g.integers(1, 40)), int(g.integers(1, 40)), int(g.integers(4000, 9001))
+    eng = ("auto", "i8", "fp4", "fp4k", "i8k", "f64")[int(g.integers(6))]
+    f = build_field(p, k, max_dot_length=1)
+    of = O.build_field(p, k, irreducible=list(f.irreducible), max_dot_length=1)
+    a = g.integers(0, p, (m, kd, k), dtype=np.uint8)
+    b = g.integers(0, p, (kd, n, k), dtype=np.uint8)
+    if case % 5 == 4:  # all-maximal digits: the accumulation bounds' corner
+        a[:] = p - 1
+        b[:] = p - 1
+    ref = O.gf_matmul_planes(of, a, b)
+    dev = bool(g.integers(2))
+    xa, xb = (torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()) if dev else (a, b)
+    try:
+        got = f.matmul_coeffs(xa, xb, engine=eng)
+    except Q.ParamsViolation:
+        fits = _fp4k_plan_fits(p, k) if eng in PLANE_ENGINES else (p <= 7 if eng == "fp4" else False)
+        assert eng != "auto" and eng != "i8" and not (eng in ("fp4", "fp4k", "i8k") and fits and kd < 4096), \
+            (p, k, m, kd, n, eng)
+        return
+    got = got.cpu().numpy() if dev else got
+    assert np.array_equal(got, ref), (p, k, m, kd, n, eng, dev)
+
+
+@pytest.mark.parametrize("case", range(40))
+def test_random_sweep_right_cmm(case):
+    """Seeded right_cmm draws: p, ragged shapes, engines, against the oracle's modular product."""
+    g = np.random.default_rng(7000 + case)
+    p = (2, 3, 5, 7, 11, 31)[int(g.integers(6))]
+    m, kd, n = (int(x) for x in g.integers(1, 300, 3))
+    eng = ("auto", "i8", "fp4k", "f64")[int(g.integers(4))]
+    a = g.integers(0, p, (m, kd), dtype=np.uint8)
+    b = g.integers(0, p, (kd, n), dtype=np.uint8)
+    prm = cmm_params(p, kd, strict=True)
+    try:
+        got = cmm.right_cmm(a, cmm.compress_rows(b, prm), engine=eng)
+    except Q.ParamsViolation:
+        assert eng in ("fp4k",) and p > 7, (p, m, kd, n, eng)
+        return
+    assert np.array_equal(got, O.modmatmul_planes(a, b, p)), (p, m, kd, n, eng)
