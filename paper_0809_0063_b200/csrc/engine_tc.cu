@@ -156,6 +156,24 @@ struct Params {
     int pdl_tail;
     // uint8 epilogue: store column n of row m at c[n * ldc + m + n * diag_shift] (0: row-major)
     int64_t diag_shift;
+    // A operand as 16 phase-shifted copies read through one 4-D tensor map {K bytes,
+    // rows at a 16-byte stride, phase, plane} (the Toeplitz operand of the long-product
+    // GEMM without materialising it): a 128-row tile is one box of 16 phases x 8 rows,
+    // smem row 8 phi + r holding GEMM row 16 r + phi of the tile; the epilogue maps TMEM lanes
+    // back and stores GEMM row x at M - 1 - x (rows are the Toeplitz rows reversed)
+    int a_phase;
+    // Convolution mode (the batched long products, conv_tc): a work unit is the output
+    // block y = y0 + i + v TL (i < 128: TMEM lane, v: column) of one pair; its K loop runs
+    // over the Toeplitz row blocks w (rows y0 + w TL .. +127, A = the phase map at row
+    // (conv_x0 - y0 - w TL - 127) / 16) against the b blocks shifted by w (B = a 3-D map
+    // {TL, V, batch} at row v0 - w: out-of-range blocks load as zeros), so the overlap-add
+    // of the block products happens in the TMEM accumulator and the epilogue writes the
+    // final coefficients mod p.  m tile = y0 / 128, planes = pairs.
+    int conv, conv_tl, conv_x0, conv_kpw;  // kpw: K blocks per Toeplitz row block (TL / BK)
+    int conv_brows;                        // rows of the B box (the column tile, <= BN)
+    int conv_tn;                           // column tile width (<= BN, a multiple of 16)
+    int64_t conv_ncoef;
+    unsigned int* conv_flag;               // bit 1: a nonzero coefficient at or past ncoef
 };
 
 // tile index -> (plane, m tile, n tile).  Unfused: planes outermost.  Fused:
@@ -316,7 +334,25 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                         bk = kin * BK;
                         boff = (seg_s - i) * (int)prm.N;
                     }
-                    if (prm.diag_noload && (u != group_id || kb >= NST)) {  // wrong results: power probe
+                    if (PAIR && !MC && prm.conv) {  // convolution mode on a CTA pair: rows y0 = rank * 128
+                        const uint32_t lbar = map_to_rank(&full_bar[stage], 0);
+                        if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * (G::A_BYTES + prm.conv_brows * BK));
+                        const int w = kb / prm.conv_kpw, kin = (kb - w * prm.conv_kpw) * BK;
+                        const int r0 = (prm.conv_x0 - mt * G::TILE_M - (int)rank * BM - w * prm.conv_tl - 127) / 16;
+                        tma_load_4d_pair(sa, &tmap_a, lbar, kin, r0, 0, pl);  // 16 phases x 8 rows
+                        tma_load_3d_pair(sb, &tmap_b, lbar, kin, nt * prm.conv_tn + (int)rank * prm.conv_brows - w, pl);
+                    } else if (!PAIR && !MC && prm.conv) {  // convolution mode: Toeplitz block w, b blocks shifted by w
+                        mbar_arrive_expect_tx(&full_bar[stage], G::A_BYTES + prm.conv_brows * BK);
+                        const int w = kb / prm.conv_kpw, kin = (kb - w * prm.conv_kpw) * BK;
+                        const int r0 = (prm.conv_x0 - mt * G::TILE_M - w * prm.conv_tl - 127) / 16;
+                        tma_load_4d(sa, &tmap_a, &full_bar[stage], kin, r0, 0, pl);  // 16 phases x 8 rows
+                        tma_load_3d(sb, &tmap_b, &full_bar[stage], kin, nt * prm.conv_tn - w, pl);
+                    } else if (!PAIR && !MC && prm.a_phase) {  // Toeplitz operand: 16 phase boxes + B
+                        mbar_arrive_expect_tx(&full_bar[stage], G::STAGE_BYTES);
+                        const int r0 = (mt * G::TILE_M) / 16;
+                        tma_load_4d(sa, &tmap_a, &full_bar[stage], ak, r0, 0, pl);  // 16 phases x 8 rows
+                        tma_load_2d(sb, &tmap_b, &full_bar[stage], bk, brow + boff);
+                    } else if (prm.diag_noload && (u != group_id || kb >= NST)) {  // wrong results: power probe
                         if (!PAIR || leader) mbar_arrive(&full_bar[stage]);
                     } else if (MC) {
                         const uint32_t lbar = map_to_rank(&full_bar[stage], pair_leader);
@@ -349,7 +385,7 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
             decode_tile<FUSE_K>(u * per_unit + sp, prm, pl, mt, nt);
             nt += prm.n_tile0;
             const int nkb = prm.plane_inner ? prm.seg_cnt[pl] * prm.seg_kpb : prm.num_kb;
-            const uint32_t nn = (uint32_t)tile_n<BN>(prm, nt);
+            const uint32_t nn = prm.conv ? (uint32_t)prm.conv_tn : (uint32_t)tile_n<BN>(prm, nt);
             const uint32_t idesc = KIND == KIND_I8 ? idesc_u8_s32(G::TILE_M, nn) : idesc_mxf4(G::TILE_M, nn);
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
@@ -408,8 +444,14 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
             const uint32_t acc_phase = (local >> 1) & 1;
             mbar_wait(&tmem_full[acc], acc_phase);
             tc_fence_after();
-            const int64_t row = (int64_t)mt * G::TILE_M + (int)rank * BM + (FUSE_K ? ew4 : ew) * 32 + lane;
-            const bool row_ok = row < prm.M;
+            int64_t row = (int64_t)mt * G::TILE_M + (int)rank * BM + (FUSE_K ? ew4 : ew) * 32 + lane;
+            bool row_ok = row < prm.M;
+            if (!PAIR && prm.a_phase) {  // smem / TMEM row l = 8 phi + r holds GEMM row 16 r + phi
+                const int l = ew * 32 + lane;
+                const int64_t x = (int64_t)mt * G::TILE_M + 16 * (l % 8) + l / 8;
+                row_ok = x < prm.M;
+                row = prm.M - 1 - x;
+            }
             if constexpr (FUSE_K > 0) {
                 // plane pl of this tile: acc[(col, l)] += W[l][pl] * (D_pl[row, col] mod p)
                 // on byte lanes held in registers (S * (p-1)^2 < 256: no carries).
@@ -477,6 +519,36 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                                 if (e < nb) dst[e] = (uint8_t)(o[e >> 2] >> (8 * (e & 3)));
                         }
                     }
+                }
+                continue;
+            }
+            if (prm.conv) {
+                // TMEM lane l = smem row 8 phi + r = tile row i = 127 - 16 r - phi: coefficient
+                // y = y0 + i + v TL of pair pl, column c = block v (y0 = the CTA's 128 rows)
+                const int l = ew * 32 + lane;
+                const int64_t ybase = (int64_t)mt * G::TILE_M + (int)rank * BM + 127 - 16 * (l % 8) - l / 8;
+                uint8_t* orow = prm.c + (int64_t)pl * prm.ldc;
+                const int nch = prm.conv_tn / 16;
+#pragma unroll 1
+                for (int ch = 0; ch < nch; ++ch) {
+                    uint32_t v[16];
+                    tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN + ch * 16, v);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        const int64_t col = (int64_t)nt * prm.conv_tn + ch * 16 + e;
+                        if (col >= prm.N) continue;
+                        const int64_t y = ybase + col * prm.conv_tl;
+                        const uint32_t r = mod_u32(v[e], prm.p, prm.magic64);
+                        if (y < prm.conv_ncoef) orow[y] = (uint8_t)r;
+                        else if (r) atomicOr(prm.conv_flag, 2u);
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (PAIR) mbar_arrive_cluster(acc ? empty_addr1 : empty_addr0);
+                    else mbar_arrive(&tmem_empty[acc]);
                 }
                 continue;
             }
@@ -948,10 +1020,13 @@ template <int KIND, bool PAIR, int FUSE_K = 0, bool MC = false>
 static cudaError_t launch_gemm_raw(const CUtensorMap& ta, const CUtensorMap& tb, const Params& prm, cudaStream_t s,
                                    int max_clusters = 0, bool pdl_secondary = false) {
     const int per = MC ? 4 : (PAIR ? 2 : 1);  // CTAs per cluster
-    const int tiles = (MC ? (prm.m_tiles + 1) / 2 : prm.m_tiles) * prm.n_tiles;  // cluster work units per plane
+    // cluster work units of the launch: tiles of every plane (plane-inner / fused
+    // launches walk the planes of one tile inside a unit)
+    const int64_t per_plane = (int64_t)(MC ? (prm.m_tiles + 1) / 2 : prm.m_tiles) * prm.n_tiles;
+    const int64_t units = (FUSE_K || prm.plane_inner) ? per_plane : per_plane * (prm.planes > 0 ? prm.planes : 1);
     int grid = gemm_max_clusters<KIND, PAIR, FUSE_K, MC>();
     if (max_clusters > 0 && max_clusters < grid) grid = max_clusters;
-    if (tiles < grid) grid = tiles;
+    if (units < grid) grid = (int)units;
     cudaLaunchConfig_t cfg = gemm_config<KIND, PAIR, FUSE_K, MC>(s);
     cfg.gridDim = dim3((unsigned)(grid * per));
     cudaLaunchAttribute attrs[2];
@@ -2517,6 +2592,78 @@ __global__ void toeplitz_rows_kernel(const uint8_t* __restrict__ apad, int64_t b
     }
 }
 
+// The Toeplitz operand without materialising it: GEMM row x (Toeplitz row M-1-x) is
+// apad[1 + x .. 1 + x + TL), so with 16 copies P_phi[j] = apad[1 + phi + j] (16-byte
+// aligned) row 16 r + phi is P_phi[16 r ..] -- a tensor map with a 16-byte row stride
+// over overlapping rows reads any tile (GEMM producer, a_phase).  16 x (na + 2 TL)
+// bytes per pair instead of (na + TL) x TL.
+__global__ void toeplitz_phase_kernel(const uint8_t* __restrict__ apad, int64_t batch, int64_t len, int64_t Lc,
+                                      uint8_t* __restrict__ P) {
+    const int64_t chunks = Lc / 16, total = batch * 16 * chunks;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t sp = g / chunks, c = g - sp * chunks;
+        const int64_t sidx = sp / 16;
+        const int ph = (int)(sp - sidx * 16);
+        const int64_t o = 1 + ph + 16 * c;
+        const uint8_t* src = apad + sidx * len;
+        uint32_t r[4];
+        if (o + 20 <= len) {
+            const uint32_t* w = reinterpret_cast<const uint32_t*>(src) + (o >> 2);
+            const uint32_t sh = 8u * (uint32_t)(o & 3);
+            uint32_t v[5];
+#pragma unroll
+            for (int k = 0; k < 5; ++k) v[k] = __ldg(w + k);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) r[k] = __funnelshift_r(v[k], v[k + 1], sh);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) r[k] = 0;
+            for (int j = 0; j < 16; ++j)
+                if (o + j < len) r[j >> 2] |= (uint32_t)src[o + j] << (8 * (j & 3));
+        }
+        *reinterpret_cast<uint4*>(P + sp * Lc + 16 * c) = make_uint4(r[0], r[1], r[2], r[3]);
+    }
+}
+
+// Phase copies for the convolution mode: P[s][phi][j] = a_s[X0 - phi - j] (0 outside
+// [0, na)), so GEMM row x~ = 16 r + phi of the phase map, P_phi[16 r + k] = a[X0 - x~ - k],
+// is Toeplitz row X0 - x~ (T[x][k] = a[x - k]).
+__global__ void conv_phase_kernel(const uint8_t* __restrict__ a, int64_t batch, int64_t na, int64_t X0, int64_t Lc,
+                                  uint8_t* __restrict__ P) {
+    const int64_t chunks = Lc / 16, total = batch * 16 * chunks;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t sp = g / chunks, c = g - sp * chunks;
+        const int64_t sidx = sp / 16;
+        const int ph = (int)(sp - sidx * 16);
+        const uint8_t* as = a + sidx * na;
+        const int64_t top = X0 - ph - 16 * c;  // a index of byte 0 of this chunk (descending)
+        const int64_t lo = top - 15;           // the chunk is a[lo .. top] reversed
+        uint32_t r[4] = {0, 0, 0, 0};
+        if (lo >= 0 && top < na && (reinterpret_cast<uintptr_t>(as) & 3) == 0) {
+            // five aligned words cover a[lo .. top]; funnel-shift them into place, then reverse
+            const int64_t w0 = lo >> 2;
+            const uint32_t sh = 8u * (uint32_t)(lo & 3);
+            const uint32_t* aw = reinterpret_cast<const uint32_t*>(as) + w0;
+            const int64_t nw = (na + 3) >> 2;  // words that hold a byte of a
+            uint32_t v[5];
+#pragma unroll
+            for (int k = 0; k < 5; ++k) v[k] = (w0 + k < nw) ? __ldg(aw + k) : 0u;
+            uint32_t f[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) f[k] = __funnelshift_r(v[k], v[k + 1], sh);  // a[lo + 4k .. lo + 4k + 3]
+#pragma unroll
+            for (int k = 0; k < 4; ++k) r[k] = __byte_perm(f[3 - k], 0, 0x0123);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int64_t i = top - j;
+                if (i >= 0 && i < na) r[j >> 2] |= (uint32_t)__ldg(as + i) << (8 * (j & 3));
+            }
+        }
+        *reinterpret_cast<uint4*>(P + sp * Lc + 16 * c) = make_uint4(r[0], r[1], r[2], r[3]);
+    }
+}
+
 __global__ void blocks_kernel(const uint8_t* __restrict__ b, int64_t batch, int64_t nb, int64_t V,
                               uint8_t* __restrict__ Bv, int TL) {
     // Bv[s][v][l] = b_s[v TL + l] (0 past nb), 16 bytes per thread
@@ -2601,25 +2748,160 @@ static int tz_width() {
     return (w >= 128 && w % 128 == 0) ? w : TL_DEFAULT;
 }
 static int64_t tz_pad_len(int64_t na, int TL) { return round_up(na + 2 * TL + 32, 16); }
+static int64_t tz_phase_len(int64_t na, int TL) { return round_up(na + 2 * TL + 16, 16); }
+// the Toeplitz operand as 16 phase copies read through an overlapping-row tensor map
+// (default) or materialised row by row (QADIC_TZ_MATERIALIZE=1, the earlier form)
+static bool tz_materialize() {  // (the CTA-pair variant QADIC_TZ_PAIR=1 reads materialised rows)
+    static const bool m = (getenv("QADIC_TZ_MATERIALIZE") && atoi(getenv("QADIC_TZ_MATERIALIZE")) != 0) ||
+                          (getenv("QADIC_TZ_PAIR") && atoi(getenv("QADIC_TZ_PAIR")) != 0);
+    return m;
+}
 
 static size_t toeplitz_workspace(int64_t batch, int64_t na, int64_t nb) {
     const int TL = tz_width();
     const int64_t M = na + TL - 1, V = (nb + TL - 1) / TL;
-    return (size_t)round_up(batch * tz_pad_len(na, TL), 1024) + (size_t)round_up(batch * M * TL, 1024) +
+    const int64_t aop = tz_materialize() ? batch * M * TL : batch * 16 * tz_phase_len(na, TL);
+    return (size_t)round_up(batch * tz_pad_len(na, TL), 1024) + (size_t)round_up(aop, 1024) +
            (size_t)round_up(batch * V * TL, 1024) +
            (size_t)round_up(batch * V * round_up(M + (V - 1) * TL + 16, 16), 1024) + 1024;
 }
 
+// 4-D map over the phase copies: {TL bytes, rows (16-byte stride, overlapping), 16 phases, batch}
+static int make_tmap_phase(CUtensorMap* map, const void* base, int TL, int64_t rows, int64_t Lc, int64_t batch) {
+    EncodeTiledFn fn = encode_fn();
+    QADIC_REQUIRE(fn != nullptr, QADIC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[4] = {(cuuint64_t)TL, (cuuint64_t)rows, 16, (cuuint64_t)batch};
+    cuuint64_t strides[3] = {16, (cuuint64_t)Lc, (cuuint64_t)(16 * Lc)};
+    cuuint32_t box[4] = {(cuuint32_t)BK, 8, 16, 1};  // one box = a whole 128-row tile: [phase][8 rows][BK]
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    QADIC_REQUIRE(r == CUDA_SUCCESS, QADIC_ERR_CUDA, "cuTensorMapEncodeTiled (phase map) failed (%d)", (int)r);
+    return QADIC_OK;
+}
+
+// ---- convolution mode (default for the long products): overlap-add in TMEM ----------
+struct ConvPlan {
+    int TL;
+    int64_t X0, Lc, R, Vb, Vp, W;
+};
+static int conv_width() {  // K of one Toeplitz row block: 128 gives N = 256-column tiles at polylong
+    static const int w = getenv("QADIC_CONV_L") ? atoi(getenv("QADIC_CONV_L")) : 128;
+    return (w >= 128 && w % 128 == 0) ? w : 128;
+}
+static ConvPlan conv_plan(int64_t na, int64_t nb, int64_t ncoef) {
+    ConvPlan c;
+    c.TL = conv_width();
+    c.X0 = na + c.TL - 1;
+    c.X0 += (15 - c.X0 % 16 + 16) % 16;  // X0 = 15 (mod 16): every tile's first GEMM row on a phase row
+    c.Lc = round_up(c.X0 + c.TL + 16, 16);
+    c.R = (c.X0 + 16) / 16;
+    c.Vb = (nb + c.TL - 1) / c.TL;
+    const int64_t nfull = na + nb - 1, span = ncoef > nfull ? ncoef : nfull;
+    c.Vp = (span + c.TL - 1) / c.TL;
+    c.W = (na + c.TL - 2) / c.TL + 1;  // Toeplitz row blocks with a nonzero entry
+    return c;
+}
+static bool conv_default() {
+    static const bool old = (getenv("QADIC_TZ_OLD") && atoi(getenv("QADIC_TZ_OLD")) != 0) || tz_materialize();
+    return !old;
+}
+static size_t conv_workspace(int64_t batch, int64_t na, int64_t nb, int64_t ncoef) {
+    const ConvPlan c = conv_plan(na, nb, ncoef);
+    return (size_t)round_up(batch * 16 * c.Lc, 1024) + (size_t)round_up(batch * c.Vb * c.TL, 1024) + 1024;
+}
+
+static int run_conv(const uint8_t* a, int64_t na, const uint8_t* b, int64_t nb, int64_t batch, uint32_t p, uint8_t* out,
+                    int64_t ncoef, void* ws, size_t ws_bytes, cudaStream_t s) {
+    const ConvPlan c = conv_plan(na, nb, ncoef);
+    const int TL = c.TL;
+    QADIC_REQUIRE(ws && ws_bytes >= conv_workspace(batch, na, nb, ncoef), QADIC_ERR_VALUE, "workspace too small");
+    QADIC_REQUIRE((__int128)std::min(na, nb) * (p - 1) * (p - 1) < ((__int128)1 << 31), QADIC_ERR_PARAMS,
+                  "the int32 accumulator cannot hold min(len_a, len_b) * (p-1)^2");
+    QADIC_REQUIRE(c.R < (1ll << 31) && c.Vp < (1ll << 31) && c.W * (TL / BK) < (1ll << 30) && batch < (1ll << 31),
+                  QADIC_ERR_UNSUPPORTED, "long product beyond the tensor-map ranges");
+    uint8_t* P = static_cast<uint8_t*>(ws);
+    uint8_t* Bv = P + round_up(batch * 16 * c.Lc, 1024);
+    unsigned int* flag = reinterpret_cast<unsigned int*>(Bv + round_up(batch * c.Vb * TL, 1024));
+    const int sms = num_sms();
+    auto grid_of = [&](int64_t n) {
+        return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 16));
+    };
+    QADIC_TIMED("polymul conv A", s, conv_phase_kernel<<<grid_of(batch * c.Lc), 256, 0, s>>>(a, batch, na, c.X0, c.Lc, P));
+    QADIC_TIMED("polymul conv B", s, blocks_kernel<<<grid_of(batch * c.Vb * (TL / 16)), 256, 0, s>>>(b, batch, nb, c.Vb, Bv, TL));
+    int rc = check_launch("conv operands");
+    if (rc) return rc;
+    cudaMemsetAsync(flag, 0, sizeof(unsigned int), s);
+    constexpr int BN = Cfg<KIND_I8>::BN;
+    CUtensorMap ta, tb;
+    rc = make_tmap_phase(&ta, P, TL, c.R, c.Lc, batch);
+    if (rc) return rc;
+    // CTA pairs (cta_group::2): the two 128-row halves (y0 = 0, 128) of a 256-coefficient
+    // block share the b blocks, each CTA loading half of the column tile; the B box holds
+    // that half only (a single tile of Vp <= BN columns loads Vp / 2 rows, not BN / 2)
+    const bool pair = TL % 256 == 0 && !(getenv("QADIC_CONV_PAIR") && atoi(getenv("QADIC_CONV_PAIR")) == 0);
+    // every column tile has the same width (the box is fixed): one tile of Vp rounded to 16,
+    // or full BN tiles over Vp rounded up to BN (the extra columns address coefficients past
+    // the output and come out zero)
+    // column tile: as wide as the MMA allows (N = 256: an N = 128 tile runs the int8 pipe at
+    // about half rate), narrowed while the launch would leave SMs idle (small batches)
+    int tile_cols = (int)std::min<int64_t>(BN, round_up(c.Vp, 16));
+    const int per_pair_rows = TL / (pair ? 2 * BM : BM);
+    while (tile_cols > 32 && batch * per_pair_rows * ((c.Vp + tile_cols - 1) / tile_cols) < num_sms())
+        tile_cols = (int)round_up(tile_cols / 2, 16);
+    const int64_t Np = round_up(c.Vp, tile_cols);
+    const int brows = pair ? tile_cols / 2 : tile_cols;
+    {
+        EncodeTiledFn fn = encode_fn();
+        QADIC_REQUIRE(fn != nullptr, QADIC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        cuuint64_t dims[3] = {(cuuint64_t)TL, (cuuint64_t)c.Vb, (cuuint64_t)batch};
+        cuuint64_t strides[2] = {(cuuint64_t)TL, (cuuint64_t)(c.Vb * TL)};
+        cuuint32_t box[3] = {(cuuint32_t)BK, (cuuint32_t)brows, 1};
+        cuuint32_t estr[3] = {1, 1, 1};
+        CUresult r = fn(&tb, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, Bv, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        QADIC_REQUIRE(r == CUDA_SUCCESS, QADIC_ERR_CUDA, "cuTensorMapEncodeTiled (conv B) failed (%d)", (int)r);
+    }
+    Params prm = {};
+    prm.sf = e2m1_scale_word();
+    prm.group_m = GROUP_M;
+    prm.M = TL;
+    prm.N = Np;
+    prm.p = p;
+    prm.magic64 = wide_magic(p);
+    prm.m_tiles = TL / (pair ? 2 * BM : BM);
+    prm.n_tiles = (int)(Np / tile_cols);
+    prm.n_full = prm.n_tiles;
+    prm.num_kb = (int)(c.W * (TL / BK));
+    prm.planes = (int)batch;
+    prm.c = out;
+    prm.ldc = ncoef;
+    prm.conv = 1;
+    prm.conv_tl = TL;
+    prm.conv_x0 = (int)c.X0;
+    prm.conv_kpw = TL / BK;
+    prm.conv_ncoef = ncoef;
+    prm.conv_flag = flag;
+    prm.conv_brows = brows;
+    prm.conv_tn = tile_cols;
+    return pair ? launch_gemm<KIND_I8, true>(ta, tb, prm, s, "polymul conv gemm")
+                : launch_gemm<KIND_I8, false>(ta, tb, prm, s, "polymul conv gemm");
+}
+
 static int run_toeplitz(const uint8_t* a, int64_t na, const uint8_t* b, int64_t nb, int64_t batch, uint32_t p,
                         uint8_t* out, int64_t ncoef, void* ws, size_t ws_bytes, cudaStream_t s) {
+    if (conv_default()) return run_conv(a, na, b, nb, batch, p, out, ncoef, ws, ws_bytes, s);
     const int TL = tz_width();
     const int64_t M = na + TL - 1, V = (nb + TL - 1) / TL, len = tz_pad_len(na, TL);
     QADIC_REQUIRE(ws && ws_bytes >= toeplitz_workspace(batch, na, nb), QADIC_ERR_VALUE, "workspace too small");
     QADIC_REQUIRE(batch * M < (1ll << 31) && batch * V < (1ll << 31), QADIC_ERR_UNSUPPORTED,
                   "batch x length beyond the TMA row range");
+    const bool mat = tz_materialize();
+    const int64_t Lc = tz_phase_len(na, TL);
     uint8_t* apad = static_cast<uint8_t*>(ws);
-    uint8_t* T = apad + round_up(batch * len, 1024);
-    uint8_t* Bv = T + round_up(batch * M * TL, 1024);
+    uint8_t* T = apad + round_up(batch * len, 1024);  // materialised rows or the 16 phase copies
+    uint8_t* Bv = T + round_up(mat ? batch * M * TL : batch * 16 * Lc, 1024);
     uint8_t* Dt = Bv + round_up(batch * V * TL, 1024);
     unsigned int* flag =
         reinterpret_cast<unsigned int*>(Dt + round_up(batch * V * round_up(M + (V - 1) * TL + 16, 16), 1024));
@@ -2628,8 +2910,12 @@ static int run_toeplitz(const uint8_t* a, int64_t na, const uint8_t* b, int64_t 
         return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 16));
     };
     QADIC_TIMED("polymul toeplitz pad", s, reverse_pad_kernel<<<grid_of(batch * len), 256, 0, s>>>(a, batch, na, len, apad, TL));
-    QADIC_TIMED("polymul toeplitz A", s,
-                toeplitz_rows_kernel<<<grid_of(batch * M * (TL / 16)), 256, 0, s>>>(apad, batch, na, len, M, T, TL));
+    if (mat)
+        QADIC_TIMED("polymul toeplitz A", s,
+                    toeplitz_rows_kernel<<<grid_of(batch * M * (TL / 16)), 256, 0, s>>>(apad, batch, na, len, M, T, TL));
+    else
+        QADIC_TIMED("polymul toeplitz A", s,
+                    toeplitz_phase_kernel<<<grid_of(batch * Lc), 256, 0, s>>>(apad, batch, len, Lc, T));
     QADIC_TIMED("polymul toeplitz B", s, blocks_kernel<<<grid_of(batch * V * (TL / 16)), 256, 0, s>>>(b, batch, nb, V, Bv, TL));
     int rc = check_launch("toeplitz operands");
     if (rc) return rc;
@@ -2641,7 +2927,8 @@ static int run_toeplitz(const uint8_t* a, int64_t na, const uint8_t* b, int64_t 
     // diagonal-shifted transpose E[v][x + v TL] (rows of lde >= M + (V - 1) TL + 16 bytes)
     const int64_t lde = round_up(M + (V - 1) * TL + 16, 16);
     CUtensorMap ta, tb;
-    rc = make_tmap(&ta, T, TL, batch * M, TL, BM);
+    const bool phase = !mat && !pair;
+    rc = phase ? make_tmap_phase(&ta, T, TL, (M + 15) / 16, Lc, batch) : make_tmap(&ta, T, TL, batch * M, TL, BM);
     if (rc) return rc;
     rc = make_tmap(&tb, Bv, TL, batch * V, TL, pair ? BN / 2 : BN);
     if (rc) return rc;
@@ -2663,6 +2950,7 @@ static int run_toeplitz(const uint8_t* a, int64_t na, const uint8_t* b, int64_t 
     prm.diag_shift = TL;
     prm.planes = (int)batch;
     prm.nibble_out = 0;
+    prm.a_phase = phase ? 1 : 0;
     rc = pair ? launch_gemm<KIND_I8, true>(ta, tb, prm, s, "polymul toeplitz gemm")
               : launch_gemm<KIND_I8, false>(ta, tb, prm, s, "polymul toeplitz gemm");
     if (rc) return rc;
@@ -2676,7 +2964,9 @@ static int run_toeplitz(const uint8_t* a, int64_t na, const uint8_t* b, int64_t 
 
 }  // namespace tc
 
-size_t tc_toeplitz_workspace(int64_t batch, int64_t na, int64_t nb) { return tc::toeplitz_workspace(batch, na, nb); }
+size_t tc_toeplitz_workspace(int64_t batch, int64_t na, int64_t nb) {
+    return tc::conv_default() ? tc::conv_workspace(batch, na, nb, 0) : tc::toeplitz_workspace(batch, na, nb);
+}
 
 int tc_polymul_toeplitz(const uint8_t* a, int64_t na, const uint8_t* b, int64_t nb, int64_t batch, uint32_t p,
                         uint8_t* out, int64_t ncoef, void* ws, size_t ws_bytes, cudaStream_t s) {

@@ -294,3 +294,32 @@ def test_word_path_empty_and_tiny_shapes():
     prm = cmm_params(257, 1, strict=True)
     got = cmm.right_cmm(np.array([[200]]), cmm.compress_rows(np.array([[100]]), prm))
     assert got.tolist() == [[200 * 100 % 257]]
+
+
+_TZ_MAT_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_0809_0063_b200 import polymul
+from paper_0809_0063_b200.params import fqt_params
+for (p, la, lb, bsz) in ((3, 4000, 3000, 3), (7, 300, 5000, 2), (2, 129, 131, 2)):
+    prm = fqt_params(p, 1)
+    g = np.random.default_rng(la + lb)
+    a = g.integers(0, p, (bsz, la), dtype=np.uint8)
+    b = g.integers(0, p, (bsz, lb), dtype=np.uint8)
+    assert np.array_equal(polymul.polymul_fqt_long_batch(a, b, prm, engine="tc"),
+                          polymul.polymul_fqt_long_batch(a, b, prm, engine="words")), (p, la, lb)
+print("tz materialized ok")
+"""
+
+
+def test_long_products_materialized_toeplitz_variant():
+    """the earlier Toeplitz operand form (rows materialised in HBM, QADIC_TZ_MATERIALIZE=1,
+    read once per process) still equals the word engine."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _TZ_MAT_CHILD, root], env=dict(os.environ, QADIC_TZ_MATERIALIZE="1"),
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "tz materialized ok" in r.stdout, (r.stdout[-2000:], r.stderr[-3000:])
