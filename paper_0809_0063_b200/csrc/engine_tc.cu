@@ -172,6 +172,13 @@ struct Params {
     int conv, conv_tl, conv_x0, conv_kpw;  // kpw: K blocks per Toeplitz row block (TL / BK)
     int conv_brows;                        // rows of the B box (the column tile, <= BN)
     int conv_tn;                           // column tile width (<= BN, a multiple of 16)
+    // split-K over the Toeplitz row blocks (small batches): m tile = split * conv_rows + y0
+    // tile; split j runs row blocks [j conv_wc, min(conv_w, (j+1) conv_wc)) and, when
+    // conv_part is set, writes raw int32 sums to conv_part[j][plane][y] (y < conv_ytot)
+    // for conv_reduce_kernel
+    int conv_rows, conv_wc, conv_w;
+    int32_t* conv_part;
+    int64_t conv_ytot;
     int64_t conv_ncoef;
     unsigned int* conv_flag;               // bit 1: a nonzero coefficient at or past ncoef
 };
@@ -222,6 +229,15 @@ __device__ __forceinline__ void decode_tile(int tile, const Params& prm, int& pl
             nt = prm.n_tiles - 1;
         }
     }
+}
+
+// convolution mode: a unit's y0 tile, first Toeplitz row block and K blocks
+__device__ __forceinline__ void conv_unit(const Params& prm, int mt, int& my, int& w_lo, int& nkb) {
+    const int split = mt / prm.conv_rows;
+    my = mt - split * prm.conv_rows;
+    w_lo = split * prm.conv_wc;
+    const int w_hi = min(prm.conv_w, w_lo + prm.conv_wc);
+    nkb = (w_hi - w_lo) * prm.conv_kpw;
 }
 
 template <int KIND, bool PAIR, int FUSE_K = 0, bool MC = false>
@@ -318,7 +334,9 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                 const int arow = (int)(pstack * prm.M) + mt * G::TILE_M + (int)rank * BM;
                 // the pair splits the tile's (possibly narrowed, see tile_n) columns in halves
                 const int brow = (int)(pstack * prm.N) + nt * BN + (int)rank * (tile_n<BN>(prm, nt) / 2);
-                const int nkb = prm.plane_inner ? prm.seg_cnt[pl] * prm.seg_kpb : prm.num_kb;
+                int nkb = prm.plane_inner ? prm.seg_cnt[pl] * prm.seg_kpb : prm.num_kb;
+                int cmy = 0, cwlo = 0;
+                if (prm.conv) conv_unit(prm, mt, cmy, cwlo, nkb);
                 const int seg_lo = prm.plane_inner ? prm.seg_lo[pl] : prm.seg_i_lo;
                 const int seg_s = prm.plane_inner ? pl : prm.seg_s;
                 // MC: CTA (pair i, rank r) loads slice i of half r and multicasts it to both pairs
@@ -337,14 +355,14 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                     if (PAIR && !MC && prm.conv) {  // convolution mode on a CTA pair: rows y0 = rank * 128
                         const uint32_t lbar = map_to_rank(&full_bar[stage], 0);
                         if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * (G::A_BYTES + prm.conv_brows * BK));
-                        const int w = kb / prm.conv_kpw, kin = (kb - w * prm.conv_kpw) * BK;
-                        const int r0 = (prm.conv_x0 - mt * G::TILE_M - (int)rank * BM - w * prm.conv_tl - 127) / 16;
+                        const int wk = kb / prm.conv_kpw, kin = (kb - wk * prm.conv_kpw) * BK, w = cwlo + wk;
+                        const int r0 = (prm.conv_x0 - cmy * G::TILE_M - (int)rank * BM - w * prm.conv_tl - 127) / 16;
                         tma_load_4d_pair(sa, &tmap_a, lbar, kin, r0, 0, pl);  // 16 phases x 8 rows
                         tma_load_3d_pair(sb, &tmap_b, lbar, kin, nt * prm.conv_tn + (int)rank * prm.conv_brows - w, pl);
                     } else if (!PAIR && !MC && prm.conv) {  // convolution mode: Toeplitz block w, b blocks shifted by w
                         mbar_arrive_expect_tx(&full_bar[stage], G::A_BYTES + prm.conv_brows * BK);
-                        const int w = kb / prm.conv_kpw, kin = (kb - w * prm.conv_kpw) * BK;
-                        const int r0 = (prm.conv_x0 - mt * G::TILE_M - w * prm.conv_tl - 127) / 16;
+                        const int wk = kb / prm.conv_kpw, kin = (kb - wk * prm.conv_kpw) * BK, w = cwlo + wk;
+                        const int r0 = (prm.conv_x0 - cmy * G::TILE_M - w * prm.conv_tl - 127) / 16;
                         tma_load_4d(sa, &tmap_a, &full_bar[stage], kin, r0, 0, pl);  // 16 phases x 8 rows
                         tma_load_3d(sb, &tmap_b, &full_bar[stage], kin, nt * prm.conv_tn - w, pl);
                     } else if (!PAIR && !MC && prm.a_phase) {  // Toeplitz operand: 16 phase boxes + B
@@ -384,7 +402,11 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
             int pl, mt, nt;
             decode_tile<FUSE_K>(u * per_unit + sp, prm, pl, mt, nt);
             nt += prm.n_tile0;
-            const int nkb = prm.plane_inner ? prm.seg_cnt[pl] * prm.seg_kpb : prm.num_kb;
+            int nkb = prm.plane_inner ? prm.seg_cnt[pl] * prm.seg_kpb : prm.num_kb;
+            if (prm.conv) {
+                int cmy, cwlo;
+                conv_unit(prm, mt, cmy, cwlo, nkb);
+            }
             const uint32_t nn = prm.conv ? (uint32_t)prm.conv_tn : (uint32_t)tile_n<BN>(prm, nt);
             const uint32_t idesc = KIND == KIND_I8 ? idesc_u8_s32(G::TILE_M, nn) : idesc_mxf4(G::TILE_M, nn);
             const int acc = local & 1;
@@ -526,8 +548,12 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                 // TMEM lane l = smem row 8 phi + r = tile row i = 127 - 16 r - phi: coefficient
                 // y = y0 + i + v TL of pair pl, column c = block v (y0 = the CTA's 128 rows)
                 const int l = ew * 32 + lane;
-                const int64_t ybase = (int64_t)mt * G::TILE_M + (int)rank * BM + 127 - 16 * (l % 8) - l / 8;
+                int cmy, cwlo, cnkb;
+                conv_unit(prm, mt, cmy, cwlo, cnkb);
+                const int64_t ybase = (int64_t)cmy * G::TILE_M + (int)rank * BM + 127 - 16 * (l % 8) - l / 8;
                 uint8_t* orow = prm.c + (int64_t)pl * prm.ldc;
+                int32_t* prow = prm.conv_part ? prm.conv_part + ((int64_t)(mt / prm.conv_rows) * prm.planes + pl) * prm.conv_ytot
+                                              : nullptr;
                 const int nch = prm.conv_tn / 16;
 #pragma unroll 1
                 for (int ch = 0; ch < nch; ++ch) {
@@ -539,6 +565,10 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                         const int64_t col = (int64_t)nt * prm.conv_tn + ch * 16 + e;
                         if (col >= prm.N) continue;
                         const int64_t y = ybase + col * prm.conv_tl;
+                        if (prow) {  // split-K partial: raw int32 sum
+                            if (y < prm.conv_ytot) prow[y] = (int32_t)v[e];
+                            continue;
+                        }
                         const uint32_t r = mod_u32(v[e], prm.p, prm.magic64);
                         if (y < prm.conv_ncoef) orow[y] = (uint8_t)r;
                         else if (r) atomicOr(prm.conv_flag, 2u);
@@ -2664,6 +2694,33 @@ __global__ void conv_phase_kernel(const uint8_t* __restrict__ a, int64_t batch, 
     }
 }
 
+// split-K partials of the convolution mode -> coefficients mod p (4 per thread)
+__global__ void conv_reduce_kernel(const int32_t* __restrict__ part, int S, int64_t batch, int64_t ytot, int64_t ncoef,
+                                   uint32_t p, uint64_t magic64, uint8_t* __restrict__ out, unsigned int* flag) {
+    const int64_t q4 = (ytot + 3) / 4, total = batch * q4;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total; g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t sidx = g / q4, y0 = (g - sidx * q4) * 4;
+        uint32_t acc[4] = {0, 0, 0, 0};
+        for (int j = 0; j < S; ++j) {
+            const int32_t* src = part + ((int64_t)j * batch + sidx) * ytot + y0;
+            if (y0 + 4 <= ytot && (ytot & 3) == 0) {
+                const int4 v = __ldcs(reinterpret_cast<const int4*>(src));
+                acc[0] += (uint32_t)v.x; acc[1] += (uint32_t)v.y; acc[2] += (uint32_t)v.z; acc[3] += (uint32_t)v.w;
+            } else {
+                for (int e = 0; e < 4; ++e)
+                    if (y0 + e < ytot) acc[e] += (uint32_t)src[e];
+            }
+        }
+        for (int e = 0; e < 4; ++e) {
+            const int64_t y = y0 + e;
+            if (y >= ytot) break;
+            const uint32_t r = mod_u32(acc[e], p, magic64);
+            if (y < ncoef) out[sidx * ncoef + y] = (uint8_t)r;
+            else if (r) atomicOr(flag, 2u);
+        }
+    }
+}
+
 __global__ void blocks_kernel(const uint8_t* __restrict__ b, int64_t batch, int64_t nb, int64_t V,
                               uint8_t* __restrict__ Bv, int TL) {
     // Bv[s][v][l] = b_s[v TL + l] (0 past nb), 16 bytes per thread
@@ -2807,9 +2864,26 @@ static bool conv_default() {
     static const bool old = (getenv("QADIC_TZ_OLD") && atoi(getenv("QADIC_TZ_OLD")) != 0) || tz_materialize();
     return !old;
 }
+constexpr int CONV_MAX_SPLIT = 16;
+// split-K factor: enough units to fill the SMs, at least 4 Toeplitz row blocks per split
+static int conv_splits(int64_t units, int64_t W) {
+    int S = 1;
+    while (S < CONV_MAX_SPLIT && units * S < num_sms_cached() && W / (2 * S) >= 4) S *= 2;
+    return S;
+}
+static int64_t conv_cols(const ConvPlan& c) {  // N per column tile (256 = the full-rate int8 MMA)
+    return std::min<int64_t>(256, round_up(c.Vp, 16));
+}
+static size_t conv_part_bytes(int64_t batch, const ConvPlan& c) {
+    const int64_t tc = conv_cols(c), Np = round_up(c.Vp, tc);
+    const int64_t units = batch * (c.TL / 128) * (Np / tc);  // upper bound (no pairs)
+    const int S = conv_splits(units, c.W);
+    return S > 1 ? (size_t)S * batch * Np * c.TL * sizeof(int32_t) : 0;
+}
 static size_t conv_workspace(int64_t batch, int64_t na, int64_t nb, int64_t ncoef) {
     const ConvPlan c = conv_plan(na, nb, ncoef);
-    return (size_t)round_up(batch * 16 * c.Lc, 1024) + (size_t)round_up(batch * c.Vb * c.TL, 1024) + 1024;
+    return (size_t)round_up(batch * 16 * c.Lc, 1024) + (size_t)round_up(batch * c.Vb * c.TL, 1024) +
+           (size_t)round_up((int64_t)conv_part_bytes(batch, c), 1024) + 1024;
 }
 
 static int run_conv(const uint8_t* a, int64_t na, const uint8_t* b, int64_t nb, int64_t batch, uint32_t p, uint8_t* out,
@@ -2823,7 +2897,10 @@ static int run_conv(const uint8_t* a, int64_t na, const uint8_t* b, int64_t nb, 
                   QADIC_ERR_UNSUPPORTED, "long product beyond the tensor-map ranges");
     uint8_t* P = static_cast<uint8_t*>(ws);
     uint8_t* Bv = P + round_up(batch * 16 * c.Lc, 1024);
-    unsigned int* flag = reinterpret_cast<unsigned int*>(Bv + round_up(batch * c.Vb * TL, 1024));
+    int32_t* part = reinterpret_cast<int32_t*>(Bv + round_up(batch * c.Vb * TL, 1024));
+    const size_t part_room = ws_bytes - (size_t)(reinterpret_cast<uint8_t*>(part) - P) - 1024;
+    unsigned int* flag = reinterpret_cast<unsigned int*>(reinterpret_cast<uint8_t*>(part) +
+                                                         round_up((int64_t)conv_part_bytes(batch, c), 1024));
     const int sms = num_sms();
     auto grid_of = [&](int64_t n) {
         return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 16));
@@ -2846,12 +2923,16 @@ static int run_conv(const uint8_t* a, int64_t na, const uint8_t* b, int64_t nb, 
     // the output and come out zero)
     // column tile: as wide as the MMA allows (N = 256: an N = 128 tile runs the int8 pipe at
     // about half rate), narrowed while the launch would leave SMs idle (small batches)
-    int tile_cols = (int)std::min<int64_t>(BN, round_up(c.Vp, 16));
+    const int tile_cols = (int)conv_cols(c);
     const int per_pair_rows = TL / (pair ? 2 * BM : BM);
-    while (tile_cols > 32 && batch * per_pair_rows * ((c.Vp + tile_cols - 1) / tile_cols) < num_sms())
-        tile_cols = (int)round_up(tile_cols / 2, 16);
     const int64_t Np = round_up(c.Vp, tile_cols);
     const int brows = pair ? tile_cols / 2 : tile_cols;
+    // small batches: split the row blocks across CTAs (int32 partials + conv_reduce_kernel)
+    int S = conv_splits(batch * per_pair_rows * (Np / tile_cols), c.W);
+    const int64_t ytot = Np * TL;
+    if (S > 1 && (size_t)S * batch * ytot * sizeof(int32_t) > part_room) S = 1;
+    const int wc = (int)((c.W + S - 1) / S);
+    S = (int)((c.W + wc - 1) / wc);  // every split non-empty
     {
         EncodeTiledFn fn = encode_fn();
         QADIC_REQUIRE(fn != nullptr, QADIC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
@@ -2870,7 +2951,7 @@ static int run_conv(const uint8_t* a, int64_t na, const uint8_t* b, int64_t nb, 
     prm.N = Np;
     prm.p = p;
     prm.magic64 = wide_magic(p);
-    prm.m_tiles = TL / (pair ? 2 * BM : BM);
+    prm.m_tiles = per_pair_rows * S;
     prm.n_tiles = (int)(Np / tile_cols);
     prm.n_full = prm.n_tiles;
     prm.num_kb = (int)(c.W * (TL / BK));
@@ -2885,8 +2966,18 @@ static int run_conv(const uint8_t* a, int64_t na, const uint8_t* b, int64_t nb, 
     prm.conv_flag = flag;
     prm.conv_brows = brows;
     prm.conv_tn = tile_cols;
-    return pair ? launch_gemm<KIND_I8, true>(ta, tb, prm, s, "polymul conv gemm")
-                : launch_gemm<KIND_I8, false>(ta, tb, prm, s, "polymul conv gemm");
+    prm.conv_rows = per_pair_rows;
+    prm.conv_wc = wc;
+    prm.conv_w = (int)c.W;
+    prm.conv_part = S > 1 ? part : nullptr;
+    prm.conv_ytot = ytot;
+    rc = pair ? launch_gemm<KIND_I8, true>(ta, tb, prm, s, "polymul conv gemm")
+              : launch_gemm<KIND_I8, false>(ta, tb, prm, s, "polymul conv gemm");
+    if (rc || S == 1) return rc;
+    QADIC_TIMED("polymul conv reduce", s,
+                conv_reduce_kernel<<<grid_of(batch * ((ytot + 3) / 4)), 256, 0, s>>>(part, S, batch, ytot, ncoef, p,
+                                                                                   wide_magic(p), out, flag));
+    return check_launch("conv reduce");
 }
 
 static int run_toeplitz(const uint8_t* a, int64_t na, const uint8_t* b, int64_t nb, int64_t batch, uint32_t p,
