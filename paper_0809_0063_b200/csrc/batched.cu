@@ -73,7 +73,25 @@ __global__ void __launch_bounds__(PM_THREADS, PM_MINB) polymul_k4_kernel(const u
     if (__all_sync(0xffffffffu, p0 >= n)) return;  // whole warp past the end (warps stay converged)
     uint32_t av[PM_PER], bv[PM_PER];
     const bool full = p0 + PM_PER <= n;
-    if (full) {
+    // Coalesced warp path (every pair of the warp in range, 16-byte aligned operands): the
+    // warp's 32 * PM_PER pairs are read as lane-consecutive 16-byte vectors (vector v of
+    // lane l = pairs wp0 + 128 v + 4 l .. +3), so every load instruction covers 512
+    // contiguous bytes -- the per-thread-contiguous mapping put lanes 32 bytes apart and
+    // fetched every sector twice.
+    const int lane = threadIdx.x & 31;
+    const int64_t wp0 = p0 - (int64_t)lane * PM_PER;  // the warp's first pair
+    const bool wfast = PM_PER == 8 && wp0 + 32 * PM_PER <= n &&
+                       ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) |
+                         reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+    if (wfast) {
+#pragma unroll
+        for (int v = 0; v < PM_PER / 4; ++v) {
+            const uint4 x = __ldg(reinterpret_cast<const uint4*>(a + wp0 * 4) + 32 * v + lane);
+            const uint4 y = __ldg(reinterpret_cast<const uint4*>(b + wp0 * 4) + 32 * v + lane);
+            av[4 * v] = x.x; av[4 * v + 1] = x.y; av[4 * v + 2] = x.z; av[4 * v + 3] = x.w;
+            bv[4 * v] = y.x; bv[4 * v + 1] = y.y; bv[4 * v + 2] = y.z; bv[4 * v + 3] = y.w;
+        }
+    } else if (full) {
 #pragma unroll
         for (int v = 0; v < PM_PER / 4; ++v) {
             const uint4 x = __ldg(reinterpret_cast<const uint4*>(a + p0 * 4) + v);
@@ -97,12 +115,14 @@ __global__ void __launch_bounds__(PM_THREADS, PM_MINB) polymul_k4_kernel(const u
         // DQT pack by two byte dot products: (a0 + a1 q) + (a2 + a3 q) q^2 (digits < p <= q, q <= 2^7)
         const uint32_t wa = __dp4a(x, PK_LO, 0u) + (__dp4a(x, PK_HI, 0u) << (2 * T));
         const uint32_t wb = __dp4a(y, PK_LO, 0u) + (__dp4a(y, PK_HI, 0u) << (2 * T));
-        // every digit of the product is < q (checked on the host), so r < q^7 <= 2^49
-        const double rr = __dmul_rn(__hiloint2double(0x43300000, (int)wa) - two52,
-                                    __hiloint2double(0x43300000, (int)wb) - two52);
+        // every digit of the product is < q (checked on the host), so r < q^7 <= 2^49: the packed
+        // product is one 32 x 32 -> 64-bit integer multiply (exact), and enters the FP64
+        // reciprocal as the low mantissa bits of 2^52 + r (one DADD; the FP64 product of the
+        // two packed words needed two of those plus a DMUL and a DADD back to r's bits)
+        const uint64_t ri = (uint64_t)wa * wb;
+        const double rr = __longlong_as_double((long long)(0x4330000000000000ull | ri)) - two52;
         // r < 2^49 < fdiv bound B: floor(RN(r * RU(1/p))) = r // p with no correction branch
         const uint64_t si = (uint64_t)__double_as_longlong(__dadd_rd(__dmul_rn(rr, c.invp_up), two52));
-        const uint64_t ri = (uint64_t)__double_as_longlong(__dadd_rn(rr, two52));
         // u_i only matters mod 2^8 (it is small): byte windows of r and s
         uint32_t u[7];
 #pragma unroll
@@ -139,9 +159,20 @@ __global__ void __launch_bounds__(PM_THREADS, PM_MINB) polymul_k4_kernel(const u
     // a warp with all its pairs in range stages its 32 x 56 output bytes in shared
     // memory and stores them as lane-consecutive 16-byte vectors
     __shared__ __align__(16) uint32_t pstage[PM_THREADS / 32][32 * PM_PER * 7 / 4];
-    const int lane = threadIdx.x & 31;
     uint8_t* wbase = dst - (int64_t)lane * PM_PER * 7;  // the warp's first output byte
-    if (__all_sync(0xffffffffu, full) && ((reinterpret_cast<uintptr_t>(wbase) & 15) == 0)) {
+    if (wfast) {  // o[0..6]: pairs wp0 + 4 l .. +3 (28 bytes), o[7..13]: pairs wp0 + 128 + 4 l ..
+        uint32_t* st = pstage[threadIdx.x >> 5];
+#pragma unroll
+        for (int q = 0; q < 7; ++q) {
+            st[7 * lane + q] = o[q];  // word stride 7: conflict-free
+            st[224 + 7 * lane + q] = o[7 + q];
+        }
+        __syncwarp();
+        constexpr int NV = 32 * PM_PER * 7 / 16;  // 16-byte vectors per warp
+#pragma unroll
+        for (int v = lane; v < NV; v += 32)
+            reinterpret_cast<uint4*>(wbase)[v] = *reinterpret_cast<const uint4*>(st + 4 * v);
+    } else if (__all_sync(0xffffffffu, full) && ((reinterpret_cast<uintptr_t>(wbase) & 15) == 0)) {
         uint32_t* st = pstage[threadIdx.x >> 5];
 #pragma unroll
         if constexpr (PM_PER * 7 % 8 == 0) {

@@ -223,12 +223,16 @@ __global__ void copy_like_kernel(const uint4* __restrict__ a, const uint4* __res
         x[v] = j0 + v < n_in ? __ldg(a + j0 + v) : make_uint4(0, 0, 0, 0);
         y[v] = j0 + v < n_in ? __ldg(b + j0 + v) : make_uint4(0, 0, 0, 0);
     }
-    // the output stream is n_out / n_in of the input: thread j writes its share
-    const int64_t o0 = j0 * n_out / n_in, o1 = (j0 + V) * n_out / n_in;
+    // the output stream (n_out <= 2 n_in vectors) in two coalesced halves: vector i of
+    // the inputs writes out[i] and out[n_in + i] (an earlier form wrote each thread's
+    // n_out / n_in share contiguously -- lanes 1.75 vectors apart at cfg1's shape, a
+    // partial-sector store pattern that made this ceiling slow)
 #pragma unroll
-    for (int v = 0; v < 2 * V; ++v) {
-        const uint4 p = x[v % V], q = y[(v + 1) % V];
-        if (o0 + v < o1 && o0 + v < n_out) out[o0 + v] = make_uint4(p.x ^ q.x, p.y ^ q.y, p.z ^ q.z, p.w ^ q.w);
+    for (int v = 0; v < V; ++v) {
+        const int64_t i = j0 + v;
+        const uint4 p = x[v], q = y[v];
+        if (i < n_out) out[i] = make_uint4(p.x ^ q.x, p.y ^ q.y, p.z ^ q.z, p.w ^ q.w);
+        if (n_in + i < n_out) out[n_in + i] = make_uint4(p.x + q.x, p.y + q.y, p.z + q.z, p.w + q.w);
     }
 }
 }  // namespace probe
