@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(PM_THREADS, PM_MINB) polymul_k4_kernel(const u
     // fetched every sector twice.
     const int lane = threadIdx.x & 31;
     const int64_t wp0 = p0 - (int64_t)lane * PM_PER;  // the warp's first pair
-    const bool wfast = PM_PER == 8 && wp0 + 32 * PM_PER <= n &&
+    const bool wfast = PM_PER % 4 == 0 && wp0 + 32 * PM_PER <= n &&
                        ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) |
                          reinterpret_cast<uintptr_t>(out)) & 15) == 0;
     if (wfast) {
@@ -160,13 +160,12 @@ __global__ void __launch_bounds__(PM_THREADS, PM_MINB) polymul_k4_kernel(const u
     // memory and stores them as lane-consecutive 16-byte vectors
     __shared__ __align__(16) uint32_t pstage[PM_THREADS / 32][32 * PM_PER * 7 / 4];
     uint8_t* wbase = dst - (int64_t)lane * PM_PER * 7;  // the warp's first output byte
-    if (wfast) {  // o[0..6]: pairs wp0 + 4 l .. +3 (28 bytes), o[7..13]: pairs wp0 + 128 + 4 l ..
+    if (wfast) {  // o[7v .. 7v+6]: pairs wp0 + 128 v + 4 l .. +3 (28 bytes each)
         uint32_t* st = pstage[threadIdx.x >> 5];
 #pragma unroll
-        for (int q = 0; q < 7; ++q) {
-            st[7 * lane + q] = o[q];  // word stride 7: conflict-free
-            st[224 + 7 * lane + q] = o[7 + q];
-        }
+        for (int v = 0; v < PM_PER / 4; ++v)
+#pragma unroll
+            for (int q = 0; q < 7; ++q) st[224 * v + 7 * lane + q] = o[7 * v + q];  // word stride 7: conflict-free
         __syncwarp();
         constexpr int NV = 32 * PM_PER * 7 / 16;  // 16-byte vectors per warp
 #pragma unroll
