@@ -614,6 +614,8 @@ int f64_gf_matmul(const FieldConst& f, const uint8_t* a, const uint8_t* b, int64
     prm.n_out = n;
     prm.fold = fold;
     prm.fold_mode = fold_mode_for(f, 2 * (int)f.k - 2, fold, (int64_t)f.k * (f.p - 1) * (f.p - 1), &prm);
+    // diagnostics only (wrong results): the pseudo-Mersenne fold's multiply-subtract by 0
+    if (getenv("QADIC_DIAG_F64_NOFOLDMATH")) prm.pm_m = 0, prm.pm_hi = 0;
     prm.d = 0;
     prm.c = c;
     switch (f.k) {
