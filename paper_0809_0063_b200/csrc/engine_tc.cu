@@ -1075,7 +1075,9 @@ template <int KIND, bool PAIR, int FUSE_K = 0, bool MC = false>
 static int launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, Params prm, cudaStream_t s,
                        const char* label = nullptr) {
     const char* name = label ? label : (KIND == KIND_I8 ? "i8 gemm" : "fp4 gemm");
-    QADIC_TIMED(name, s, (launch_gemm_raw<KIND, PAIR, FUSE_K, MC>(ta, tb, prm, s)));
+    // diagnostics: QADIC_DIAG_GEMM_CLUSTERS caps the persistent grid (SM-count scaling probe)
+    static const int cap = getenv("QADIC_DIAG_GEMM_CLUSTERS") ? atoi(getenv("QADIC_DIAG_GEMM_CLUSTERS")) : 0;
+    QADIC_TIMED(name, s, (launch_gemm_raw<KIND, PAIR, FUSE_K, MC>(ta, tb, prm, s, cap)));
     return check_launch(name);
 }
 
