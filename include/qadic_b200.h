@@ -75,9 +75,9 @@ QADIC_API int qadic_profile_collect(char *buf, size_t len);
  * ------------------------------------------------------------------------- */
 
 /* C[m,n] = A[m,k] @ B[k,n] over uint64 mod 2^64.  _speed.pyx:15-30, 58-66.
- * Large shapes run on INT8 tensor cores through byte planes; this call reads the
- * operands' significant byte counts back to the host (one stream synchronisation,
- * skipped under stream capture). */
+ * Large shapes run on INT8 tensor cores through byte planes; the operands'
+ * significant byte counts are found on the device (no host synchronisation), so the
+ * call is asynchronous on `stream` and may be captured in a CUDA graph. */
 QADIC_API int qadic_matmul_exact_u64(const uint64_t *a, const uint64_t *b, uint64_t *c,
                            int64_t m, int64_t k, int64_t n, void *stream);
 
