@@ -312,14 +312,18 @@ print("tz materialized ok")
 """
 
 
-def test_long_products_materialized_toeplitz_variant():
-    """the earlier Toeplitz operand form (rows materialised in HBM, QADIC_TZ_MATERIALIZE=1,
-    read once per process) still equals the word engine."""
+@pytest.mark.parametrize("env", [{"QADIC_TZ_MATERIALIZE": "1"}, {"QADIC_TZ_OLD": "1"}, {"QADIC_CONV_PAIR": "0"},
+                                 {"QADIC_CONV_L": "256"}])
+def test_long_products_toeplitz_variants(env):
+    """the earlier Toeplitz GEMM forms (rows materialised in HBM; 16 phase copies through the
+    overlapping-row map with the D intermediate + overlap-add pass) and the convolution mode's
+    own options (TL = 256 on CTA pairs, or on single CTAs) -- read once per process -- all
+    equal the word engine."""
     import os
     import subprocess
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    r = subprocess.run([sys.executable, "-c", _TZ_MAT_CHILD, root], env=dict(os.environ, QADIC_TZ_MATERIALIZE="1"),
+    r = subprocess.run([sys.executable, "-c", _TZ_MAT_CHILD, root], env=dict(os.environ, **env),
                        capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0 and "tz materialized ok" in r.stdout, (r.stdout[-2000:], r.stderr[-3000:])
+    assert r.returncode == 0 and "tz materialized ok" in r.stdout, (env, r.stdout[-2000:], r.stderr[-3000:])
