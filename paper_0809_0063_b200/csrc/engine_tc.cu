@@ -2882,27 +2882,30 @@ static size_t conv_part_bytes(int64_t batch, const ConvPlan& c) {
     const int S = conv_splits(units, c.W);
     return S > 1 ? (size_t)S * batch * Np * c.TL * sizeof(int32_t) : 0;
 }
+// workspace: [phase copies | b blocks | flag (1 KB) | split-K partials (optional: used
+// when the room after the flag holds them, sized here for ncoef <= na + nb - 1)]
+static size_t conv_fixed_bytes(int64_t batch, const ConvPlan& c) {
+    return (size_t)round_up(batch * 16 * c.Lc, 1024) + (size_t)round_up(batch * c.Vb * c.TL, 1024) + 1024;
+}
 static size_t conv_workspace(int64_t batch, int64_t na, int64_t nb, int64_t ncoef) {
     const ConvPlan c = conv_plan(na, nb, ncoef);
-    return (size_t)round_up(batch * 16 * c.Lc, 1024) + (size_t)round_up(batch * c.Vb * c.TL, 1024) +
-           (size_t)round_up((int64_t)conv_part_bytes(batch, c), 1024) + 1024;
+    return conv_fixed_bytes(batch, c) + conv_part_bytes(batch, c);
 }
 
 static int run_conv(const uint8_t* a, int64_t na, const uint8_t* b, int64_t nb, int64_t batch, uint32_t p, uint8_t* out,
                     int64_t ncoef, void* ws, size_t ws_bytes, cudaStream_t s) {
     const ConvPlan c = conv_plan(na, nb, ncoef);
     const int TL = c.TL;
-    QADIC_REQUIRE(ws && ws_bytes >= conv_workspace(batch, na, nb, ncoef), QADIC_ERR_VALUE, "workspace too small");
+    QADIC_REQUIRE(ws && ws_bytes >= conv_fixed_bytes(batch, c), QADIC_ERR_VALUE, "workspace too small");
     QADIC_REQUIRE((__int128)std::min(na, nb) * (p - 1) * (p - 1) < ((__int128)1 << 31), QADIC_ERR_PARAMS,
                   "the int32 accumulator cannot hold min(len_a, len_b) * (p-1)^2");
     QADIC_REQUIRE(c.R < (1ll << 31) && c.Vp < (1ll << 31) && c.W * (TL / BK) < (1ll << 30) && batch < (1ll << 31),
                   QADIC_ERR_UNSUPPORTED, "long product beyond the tensor-map ranges");
     uint8_t* P = static_cast<uint8_t*>(ws);
     uint8_t* Bv = P + round_up(batch * 16 * c.Lc, 1024);
-    int32_t* part = reinterpret_cast<int32_t*>(Bv + round_up(batch * c.Vb * TL, 1024));
-    const size_t part_room = ws_bytes - (size_t)(reinterpret_cast<uint8_t*>(part) - P) - 1024;
-    unsigned int* flag = reinterpret_cast<unsigned int*>(reinterpret_cast<uint8_t*>(part) +
-                                                         round_up((int64_t)conv_part_bytes(batch, c), 1024));
+    unsigned int* flag = reinterpret_cast<unsigned int*>(Bv + round_up(batch * c.Vb * TL, 1024));
+    int32_t* part = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(flag) + 1024);
+    const size_t part_room = ws_bytes - conv_fixed_bytes(batch, c);
     const int sms = num_sms();
     auto grid_of = [&](int64_t n) {
         return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 16));
@@ -3058,7 +3061,9 @@ static int run_toeplitz(const uint8_t* a, int64_t na, const uint8_t* b, int64_t 
 }  // namespace tc
 
 size_t tc_toeplitz_workspace(int64_t batch, int64_t na, int64_t nb) {
-    return tc::conv_default() ? tc::conv_workspace(batch, na, nb, 0) : tc::toeplitz_workspace(batch, na, nb);
+    // (split-K partials sized for the batched API's output length, 2 max(na, nb) - 1)
+    return tc::conv_default() ? tc::conv_workspace(batch, na, nb, 2 * std::max(na, nb) - 1)
+                              : tc::toeplitz_workspace(batch, na, nb);
 }
 
 int tc_polymul_toeplitz(const uint8_t* a, int64_t na, const uint8_t* b, int64_t nb, int64_t batch, uint32_t p,

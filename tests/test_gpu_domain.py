@@ -250,7 +250,7 @@ def test_word_path_larger_shapes(p, k, n, m, nn):
 
 
 @pytest.mark.parametrize("p,la,lb,bsz", [(3, 16384, 16384, 3), (7, 300, 5000, 4), (127, 256, 257, 5), (2, 129, 131, 2),
-                                         (5, 1000, 1, 2), (3, 1, 1, 1)])
+                                         (5, 1000, 1, 2), (3, 1, 1, 1), (3, 16384, 9000, 2), (5, 7000, 20000, 3)])
 def test_long_products_tensor_core_engine(p, la, lb, bsz):
     """the Toeplitz GEMM engine (INT8 tensor cores) equals the packed-word engine and the
     schoolbook product; edge lengths include one-coefficient operands and lengths that
