@@ -66,8 +66,13 @@ QADIC_D uint32_t lanes_mod_2p(uint32_t v, uint32_t p) {
 template <int T, bool CORR1>
 __global__ void __launch_bounds__(PM_THREADS, PM_MINB) polymul_k4_kernel(const uint8_t* __restrict__ a,
                                                                 const uint8_t* __restrict__ b, int64_t n,
-                                                                PolyConst c, uint8_t* __restrict__ out) {
-    pdl_wait();  // predecessor complete before any global access
+                                                                PolyConst c, uint8_t* __restrict__ out, int pf) {
+    if (pf && threadIdx.x == 0) {  // the block's operand bytes towards L2 while the predecessor drains
+        const int64_t off = (int64_t)blockIdx.x * blockDim.x * PM_PER * 4, len = (int64_t)blockDim.x * PM_PER * 4;
+        l2_prefetch_span(a, off, len, n * 4);
+        l2_prefetch_span(b, off, len, n * 4);
+    }
+    pdl_wait();  // predecessor complete before any global load or store
     pdl_trigger();
     const int64_t p0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * PM_PER;
     if (__all_sync(0xffffffffu, p0 >= n)) return;  // whole warp past the end (warps stay converged)
@@ -211,9 +216,12 @@ static void launch_polymul_k4(const uint8_t* a, const uint8_t* b, int64_t n, con
     threads = (threads + 31) / 32 * 32;
     if (threads > PM_THREADS) threads = PM_THREADS;
     if (threads < 32) threads = 32;
+    static const int width_env = getenv("QADIC_PM_WIDTH") ? atoi(getenv("QADIC_PM_WIDTH")) : 0;  // A/B knob
+    if (width_env >= 32 && width_env <= PM_THREADS) threads = width_env / 32 * 32;
     const unsigned blocks = (unsigned)((n + threads * PM_PER - 1) / (threads * PM_PER));
-    if (c.corr == 1 || c.p == 2) launch_pdl(polymul_k4_kernel<T, true>, dim3(blocks), dim3((unsigned)threads), 0, s, a, b, n, c, out);
-    else launch_pdl(polymul_k4_kernel<T, false>, dim3(blocks), dim3((unsigned)threads), 0, s, a, b, n, c, out);
+    const int pf = pdl_prefetch_enabled();
+    if (c.corr == 1 || c.p == 2) launch_pdl(polymul_k4_kernel<T, true>, dim3(blocks), dim3((unsigned)threads), 0, s, a, b, n, c, out, pf);
+    else launch_pdl(polymul_k4_kernel<T, false>, dim3(blocks), dim3((unsigned)threads), 0, s, a, b, n, c, out, pf);
 }
 
 // ---- generic k (1..8): one pair per thread ---------------------------------------
@@ -297,8 +305,13 @@ template <int K, int G, bool VEC, bool NARROW = false, bool F64ACC = false>
 __global__ void __launch_bounds__(GD_THREADS, NARROW ? 8 : 1) gf_dot_kernel(const uint8_t* __restrict__ v1,
                                                             const uint8_t* __restrict__ v2, int64_t batch,
                                                             int64_t len, FieldConst f, int tab_smem,
-                                                            uint8_t* __restrict__ out) {
-    pdl_wait();  // predecessor complete before any global access
+                                                            uint8_t* __restrict__ out, int pf) {
+    if (pf && threadIdx.x == 0) {  // the block's rows towards L2 while the predecessor drains
+        const int64_t rb = len * K, off = (int64_t)blockIdx.x * (blockDim.x / G) * rb;
+        l2_prefetch_span(v1, off, (int64_t)(blockDim.x / G) * rb, batch * rb);
+        l2_prefetch_span(v2, off, (int64_t)(blockDim.x / G) * rb, batch * rb);
+    }
+    pdl_wait();  // predecessor complete before any global load or store
     pdl_trigger();
     const int lane = threadIdx.x % G;
     const int64_t dot = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
@@ -469,7 +482,8 @@ static void launch_gf_dot(const uint8_t* v1, const uint8_t* v2, int64_t batch, i
             if (width > max_width) width = max_width;
             if (width < 64) width = 64;
             const unsigned blocks = (unsigned)((threads_total + width - 1) / width);
-            launch_pdl(kern, dim3(blocks), dim3((unsigned)width), smem, s, v1, v2, batch, len, f, ntab, out);
+            launch_pdl(kern, dim3(blocks), dim3((unsigned)width), smem, s, v1, v2, batch, len, f, ntab, out,
+                       pdl_prefetch_enabled());
         };
         if (lanes == 8 && nchunks <= 2 * 8) go(gf_dot_kernel<K, 8, (4 % K == 0), true, F64ACC>, 8);
         else if (nchunks <= 2 * 4) go(gf_dot_kernel<K, 4, (4 % K == 0), true, F64ACC>, 4);
@@ -478,7 +492,7 @@ static void launch_gf_dot(const uint8_t* v1, const uint8_t* v2, int64_t batch, i
         constexpr int G = 8;
         const unsigned blocks = (unsigned)((batch * G + GD_THREADS - 1) / GD_THREADS);
         launch_pdl(gf_dot_kernel<K, G, false>, dim3(blocks), dim3(GD_THREADS), smem, s, v1, v2, batch, len, f, ntab,
-                   out);
+                   out, 0);
     }
 }
 

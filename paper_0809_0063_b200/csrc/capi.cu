@@ -69,6 +69,12 @@ bool pdl_enabled() {
     return on;
 }
 
+int pdl_prefetch_enabled() {
+    // QADIC_PDL_PREFETCH=0 switches the pre-wait L2 prefetch of the batched kernels off (A/B)
+    static const int on = pdl_enabled() && !(getenv("QADIC_PDL_PREFETCH") && atoi(getenv("QADIC_PDL_PREFETCH")) == 0);
+    return on;
+}
+
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 int check_launch(const char* what, int launched) {

@@ -213,7 +213,12 @@ namespace qadic {
 namespace probe {
 template <int V>
 __global__ void copy_like_kernel(const uint4* __restrict__ a, const uint4* __restrict__ b, int64_t n_in,
-                                 uint4* __restrict__ out, int64_t n_out) {
+                                 uint4* __restrict__ out, int64_t n_out, int pf) {
+    if (pf && threadIdx.x == 0) {  // as in the batched kernels: the block's inputs towards L2 before the wait
+        const int64_t off = (int64_t)blockIdx.x * blockDim.x * V * 16, len = (int64_t)blockDim.x * V * 16;
+        l2_prefetch_span(a, off, len, n_in * 16);
+        l2_prefetch_span(b, off, len, n_in * 16);
+    }
     pdl_wait();
     pdl_trigger();
     const int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * V;
@@ -254,11 +259,12 @@ extern "C" QADIC_API int qadic_diag_copy(const void* a, const void* b, int64_t i
     const uint4* pb = static_cast<const uint4*>(b);
     uint4* po = static_cast<uint4*>(out);
     cudaError_t e;
+    const int pf = pdl_prefetch_enabled();
     switch (per_thread) {
-        case 1: e = launch_pdl(copy_like_kernel<1>, dim3(blocks), dim3(threads), 0, s, pa, pb, n_in, po, n_out); break;
-        case 2: e = launch_pdl(copy_like_kernel<2>, dim3(blocks), dim3(threads), 0, s, pa, pb, n_in, po, n_out); break;
-        case 4: e = launch_pdl(copy_like_kernel<4>, dim3(blocks), dim3(threads), 0, s, pa, pb, n_in, po, n_out); break;
-        default: e = launch_pdl(copy_like_kernel<8>, dim3(blocks), dim3(threads), 0, s, pa, pb, n_in, po, n_out); break;
+        case 1: e = launch_pdl(copy_like_kernel<1>, dim3(blocks), dim3(threads), 0, s, pa, pb, n_in, po, n_out, pf); break;
+        case 2: e = launch_pdl(copy_like_kernel<2>, dim3(blocks), dim3(threads), 0, s, pa, pb, n_in, po, n_out, pf); break;
+        case 4: e = launch_pdl(copy_like_kernel<4>, dim3(blocks), dim3(threads), 0, s, pa, pb, n_in, po, n_out, pf); break;
+        default: e = launch_pdl(copy_like_kernel<8>, dim3(blocks), dim3(threads), 0, s, pa, pb, n_in, po, n_out, pf); break;
     }
     (void)e;
     return check_launch("diag_copy", 1);

@@ -33,6 +33,24 @@ namespace qadic {
 QADIC_D void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 QADIC_D void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// L2 prefetch hint for the byte range [off, off + bytes) of a read-only operand of
+// `total` bytes (clipped to the operand, 16-byte granules), issued by ONE thread
+// BEFORE pdl_wait(): a block that became resident while the stream predecessor
+// drains uses the wait to pull its inputs from HBM into L2.  A prefetch returns no
+// data to the SM and L2 is the GPU's point of coherence, so a predecessor that is
+// still writing the range is seen correctly by the loads after the wait.
+QADIC_D void l2_prefetch_span(const void* base, int64_t off, int64_t bytes, int64_t total) {
+    uintptr_t lo = reinterpret_cast<uintptr_t>(base) + (uintptr_t)(off < 0 ? 0 : off);
+    int64_t end = off + bytes > total ? total : off + bytes;
+    uintptr_t hi = reinterpret_cast<uintptr_t>(base) + (uintptr_t)(end < 0 ? 0 : end);
+    lo = (lo + 15) & ~(uintptr_t)15;
+    hi &= ~(uintptr_t)15;
+    if (hi > lo) {
+        const uint32_t sz = (uint32_t)(hi - lo);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"(sz) : "memory");
+    }
+}
+
 constexpr int kMaxK = 4;             // extension degree supported by the GF kernels
 constexpr int kMaxDigits = 2 * kMaxK - 1;
 

@@ -31,6 +31,8 @@ void prof_end(int idx, cudaStream_t s);
 
 // PDL launches are on unless QADIC_NO_PDL=1
 bool pdl_enabled();
+// the batched kernels' L2 prefetch ahead of pdl_wait() (qadic_common.cuh), on with PDL
+int pdl_prefetch_enabled();
 
 // Launch with programmatic stream serialisation (see pdl_wait in qadic_common.cuh).
 template <typename... KArgs, typename... Args>
