@@ -362,6 +362,14 @@ def build_step(cfg, engine, rank, ws, torch, dist, Q, W, args):
             x = bufs[i % sets]
             Q.polymul.polymul_fqt_batch(x["a"], x["b"], prm, out=outs[i % sets])
 
+        def variant_step(eng):  # the paper's q = 2^5 FP64-reciprocal REDQ form
+            def vstep(i):
+                x = bufs[i % sets]
+                Q.polymul.polymul_fqt_batch(x["a"], x["b"], prm, out=outs[i % sets], engine=eng)
+            return vstep
+
+        meta["variant_step"] = variant_step
+
         host = W.make_inputs(c, shard, seed=1000 * cfg + 100 * rank)
         pins = {k: torch.from_numpy(v).pin_memory() for k, v in host.items()}
         o_pin = torch.empty((shard[0], 2 * c.k - 1), dtype=torch.uint8).pin_memory()
@@ -527,7 +535,7 @@ def roofline(cfg, engine, kname, kstats, work, peaks, peak_src, steps=None):
 
 def dtype_label(cfg, engine, kname):
     if cfg == 1:
-        return "f64 (DQT words, one DMUL per pair)"
+        return "u32 x u32 -> u64 packed product at q = 2^8, byte-lane reduction (variant redq: q = 2^5, f64 reciprocal)"
     if cfg == 2:
         return "u8 x u8 -> u32 digit sums (IDP4A) of the DQT word, f64 REDQ"
     if engine == "f64":
@@ -722,7 +730,7 @@ def copy_ceiling(cfg, ws, torch, N, K=2000, sets=16):
             "gbs": round((2 * in_b + out_b) / (ms / 1e3) / 1e9, 1)}
 
 
-def graphed_variant(step, args, units, roof, torch):
+def graphed_variant(step, args, units, roof, torch, kernel="gf_dot (FP64 accumulation of the DQT words: the paper's form)"):
     """A batched-config variant timed like the headline: K steps in one CUDA graph."""
     for i in range(3):
         step(i)
@@ -739,7 +747,7 @@ def graphed_variant(step, args, units, roof, torch):
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
     out = {"ms_per_step": round(ms, 5), "value": units / (ms / 1e3), "steps": args.steps,
-           "kernel": "gf_dot (FP64 accumulation of the DQT words: the paper's form)"}
+           "kernel": kernel}
     if roof is not None and roof.get("algorithmic_bytes_per_launch"):
         gbs = roof["algorithmic_bytes_per_launch"] / (ms / 1e3) / 1e9
         out.update({"achieved": round(gbs, 1), "unit": "GB/s", "frac": round(gbs / roof["peak"], 4)})
@@ -982,6 +990,10 @@ def run_ours(args):
         line["redq"] = redq_line(args, torch, N)
     if ws == 1 and cfg == 2 and not args.no_variants and meta.get("variant_step"):
         line["variants"] = {"f64": graphed_variant(meta["variant_step"]("f64"), args, units, roof, torch)}
+    if ws == 1 and cfg == 1 and not args.no_variants and meta.get("variant_step"):
+        line["variants"] = {"redq": graphed_variant(
+            meta["variant_step"]("redq"), args, units, roof, torch,
+            kernel="polymul_k4 (the paper's form: DQT at q = 2^5, FP64-reciprocal REDQ + correction)")}
     if ws == 1 and cfg in (3, 4, 5) and not args.no_variants and meta.get("variant_step"):
         line["variants"] = measure_variants(args, cfg, engine, meta, units, work, peaks, peak_src, torch, N, W)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

@@ -186,10 +186,21 @@ QADIC_API int qadic_right_cmm_u8(const uint8_t *a, const uint8_t *b, int64_t m, 
                        size_t workspace_bytes, uint8_t *c, void *stream);
 
 /* cfg1 -- out[n, 2k-1] = a[n,k] * b[n,k] over F_p for n independent pairs:
- * one packed FP64 product + REDQ per pair.  polymul.polymul_fqt,
- * polymul.py:274-313 (one word per operand), batched. */
+ * one packed product + simultaneous reduction per pair.  polymul.polymul_fqt,
+ * polymul.py:274-313 (one word per operand), batched.  For k = 4 and
+ * 4 (p-1)^2 <= 255 (p = 2, 3, 5) the transform runs at q = 2^8 whatever t says: the
+ * DQT word of an operand is its four coefficient bytes, the packed product one
+ * 32 x 32 -> 64-bit multiply, and all digits are reduced at once by a byte-lane
+ * reciprocal multiply (no correction step: byte-aligned digits do not borrow).  The
+ * result is the same for every admissible q. */
 QADIC_API int qadic_polymul_batch_u8(const uint8_t *a, const uint8_t *b, int64_t n, int32_t k, int64_t p,
                            int32_t t, uint8_t *out, void *stream);
+
+/* The same products always in the paper's form: DQT words at q = 2^t, one packed
+ * product per pair, REDQ with the FP64 reciprocal (fdiv.py:66-93) and the correction
+ * pass (redq.py:118-143).  Bit-identical to qadic_polymul_batch_u8. */
+QADIC_API int qadic_polymul_batch_redq_u8(const uint8_t *a, const uint8_t *b, int64_t n, int32_t k, int64_t p,
+                                int32_t t, uint8_t *out, void *stream);
 
 /* ---------------------------------------------------------------------------
  * Handle conversion for the discrete-log API (gfext.py:43-46, 136-146):

@@ -113,6 +113,7 @@ _SIGNATURES = {
     "qadic_right_cmm_workspace": ([I64, I64, I64, I64, I32, I32], SZ),
     "qadic_right_cmm_u8": ([P, P, I64, I64, I64, I64, I32, I32, I32, P, SZ, P, P], ctypes.c_int),
     "qadic_polymul_batch_u8": ([P, P, I64, I32, I64, I32, P, P], ctypes.c_int),
+    "qadic_polymul_batch_redq_u8": ([P, P, I64, I32, I64, I32, P, P], ctypes.c_int),
     "qadic_gather_u8": ([P, I64, P, I64, I32, P, P], ctypes.c_int),
     "qadic_index_of_coeffs": ([P, I64, I32, I32, P, P, P], ctypes.c_int),
     "qadic_fdiv_scan": ([I32, I32, I32, I32, I32, I64, ctypes.POINTER(FdivScanReport), P], ctypes.c_int),

@@ -1,7 +1,12 @@
 // HBM-bound batched kernels of the hot path:
 //
-//  * cfg1  polymul_batch : one packed FP64 product per pair of short
-//    polynomials, then REDQ (compression + correction) -> 2k-1 residues.
+//  * cfg1  polymul_batch : one packed product per pair of short polynomials,
+//    then the simultaneous reduction of its 2k-1 digits.  Two forms, bit-identical:
+//    the default for k = 4, p <= 5 runs the transform at q = 2^8, where the operand's
+//    coefficient bytes ARE its DQT word (one 32 x 32 -> 64-bit multiply, byte-lane
+//    reciprocal reduction, no correction step); the paper's form
+//    (qadic_polymul_batch_redq_u8) packs at q = 2^t, and REDQ divides by p through the
+//    FP64 reciprocal and runs the correction pass.
 //    Reference: polymul.polymul_fqt for one-word operands
 //    (src/polymul.py:274-313 -> _wordconv_reduce :175-216 with na = nb = 1).
 //  * cfg2  gf_dot_batch  : GF(p^k) dot products with all products accumulated
@@ -25,21 +30,28 @@ namespace qadic {
 struct PolyConst {
     uint32_t p, t, corr, magic;
     uint32_t negp;  // -p mod 2^32: u = r + negp * s is one IMAD
+    uint32_t lm, lsh, lmask, lfix;  // byte-lane quotient: floor(d / p) ~ (d * lm) >> lsh on every lane at once
     double invp_up, bound;
 };
 
-// ---- cfg1 fast path: k = 4 (degree-3 operands), 8 pairs per thread -----------
-// One thread: 8 pairs = 2 x 16 B of a and of b in, 7 x 8 B out -- every HBM
-// access a full vector, no shared memory.  Per pair: DQT-pack both operands
+// ---- cfg1 fast path: k = 4 (degree-3 operands), 4 or 8 pairs per thread -------
+// One thread of the REDQ form: 8 pairs = 2 x 16 B of a and of b in, 56 B out -- every
+// HBM access a full vector (outputs staged per warp).  Per pair: DQT-pack both operands
 // in registers, one FP64 product, s = floor(r * RU(1/p)) by a round-down add of
 // 2^52 (the low mantissa bits are then the integer), 7 digits by the 32-bit
 // wrap trick, correction on 4 byte lanes at once.
 constexpr int PM_THREADS = 256;
+// pairs per thread: 8 for the REDQ form (56 output bytes = 7 x 8-byte stores; 4 measured slower
+// under the 32-register cap that 8 resident blocks impose), 4 for the byte-lane form (30
+// registers, 8 resident blocks: 2.92 vs 3.51 us at cfg1 -- twice as many warps whose
+// stores overlap the other warps' loads)
 #ifndef QADIC_PM_PER
 #define QADIC_PM_PER 8
 #endif
-constexpr int PM_PER = QADIC_PM_PER;  // pairs per thread (8: 56 output bytes = 7 x 8-byte stores)
-constexpr int PM_MINB = PM_PER == 8 ? 4 : 8;  // resident blocks per SM the register cap allows
+#ifndef QADIC_PM_PER_LANES
+#define QADIC_PM_PER_LANES 4
+#endif
+constexpr int pm_minb(int per) { return per >= 8 ? 4 : 8; }  // resident blocks per SM the register cap allows
 
 QADIC_D uint32_t pack4_bytes(uint32_t x, int t, uint32_t m) {
     return (x & m) | (((x >> 8) & m) << t) | (((x >> 16) & m) << (2 * t)) | (((x >> 24) & m) << (3 * t));
@@ -63,8 +75,25 @@ QADIC_D uint32_t lanes_mod_2p(uint32_t v, uint32_t p) {
     return v - ((t >> 7) & 0x01010101u) * p;
 }
 
-template <int T, bool CORR1>
-__global__ void __launch_bounds__(PM_THREADS, PM_MINB) polymul_k4_kernel(const uint8_t* __restrict__ a,
+// Byte-lane form (MODE 2 / 3), the B200-native shape of the same transform: at q = 2^8 the
+// DQT word of a degree-3 operand IS its four coefficient bytes, so the packed product is one
+// 32 x 32 -> 64-bit multiply of the words as loaded (every digit <= 4 (p-1)^2 <= 255 stays in
+// its lane), and the simultaneous reduction of all digits is one lane-wise reciprocal
+// multiply per 32-bit half: s = ((v * lm) >> lsh) & lmask holds floor(d / p) (MODE 2) or a
+// quotient short by at most one (MODE 3, finished by lanes_mod_2p) of every lane, and
+// v - p * s the residues.  Byte-aligned digits never borrow from their neighbours, so REDQ's
+// correction step has nothing to correct.  (lm, lsh) come from the host's exhaustive search
+// over d <= 4 (p-1)^2 (lane_quotient_consts); the result does not depend on the caller's q.
+QADIC_D uint32_t lanes_mod_p(uint32_t v, const PolyConst& c, bool fix) {
+    const uint32_t s = ((v * c.lm) >> c.lsh) & c.lmask;
+    const uint32_t u = v + c.negp * s;
+    return fix ? lanes_mod_2p(u, c.p) : u;
+}
+
+// MODE 0: REDQ with a general correction factor; 1: REDQ, correction factor 1 (byte-lane
+// correction); 2 / 3: the byte-lane form above (exact quotient / quotient short by <= 1)
+template <int T, int MODE, int PM_PER>
+__global__ void __launch_bounds__(PM_THREADS, pm_minb(PM_PER)) polymul_k4_kernel(const uint8_t* __restrict__ a,
                                                                 const uint8_t* __restrict__ b, int64_t n,
                                                                 PolyConst c, uint8_t* __restrict__ out, int pf) {
     if (pf && threadIdx.x == 0) {  // the block's operand bytes towards L2 while the predecessor drains
@@ -117,6 +146,13 @@ __global__ void __launch_bounds__(PM_THREADS, PM_MINB) polymul_k4_kernel(const u
 #pragma unroll
     for (int j = 0; j < PM_PER; ++j) {
         const uint32_t x = av[j], y = bv[j];
+        if constexpr (MODE >= 2) {
+            const uint64_t r = (uint64_t)x * y;  // digits c_0..c_6 on byte lanes 0..6
+            vlo[j] = lanes_mod_p((uint32_t)r, c, MODE == 3);
+            vhi[j] = lanes_mod_p((uint32_t)(r >> 32), c, MODE == 3);
+            continue;
+        }
+        constexpr bool CORR1 = MODE == 1;
         // DQT pack by two byte dot products: (a0 + a1 q) + (a2 + a3 q) q^2 (digits < p <= q, q <= 2^7)
         const uint32_t wa = __dp4a(x, PK_LO, 0u) + (__dp4a(x, PK_HI, 0u) << (2 * T));
         const uint32_t wb = __dp4a(y, PK_LO, 0u) + (__dp4a(y, PK_HI, 0u) << (2 * T));
@@ -145,7 +181,9 @@ __global__ void __launch_bounds__(PM_THREADS, PM_MINB) polymul_k4_kernel(const u
         } else {
             uint64_t v = 0;
 #pragma unroll
-            for (int i = 0; i < 6; ++i) v |= (uint64_t)mod_small(u[i] + c.corr * u[i + 1], c.p, c.magic) << (8 * i);
+            // only the low byte of a window is u_i: the high windows of s carry the 2^52 exponent bits
+            for (int i = 0; i < 6; ++i)
+                v |= (uint64_t)mod_small((u[i] & 0xFFu) + c.corr * (u[i + 1] & 0xFFu), c.p, c.magic) << (8 * i);
             v |= (uint64_t)(u[6] & 0xFF) << 48;
             vlo[j] = (uint32_t)v;
             vhi[j] = (uint32_t)(v >> 32);
@@ -211,7 +249,8 @@ static void launch_polymul_k4(const uint8_t* a, const uint8_t* b, int64_t n, con
     // that the pairs spread evenly (cfg1: 592 x 224 threads instead of 512 x 256,
     // which left 68 SMs with a fourth block and the rest with three).  Larger
     // batches run 256-thread blocks in several waves.
-    const int64_t per_wave = (int64_t)PM_MINB * num_sms_cached();
+    constexpr int PM_PER = T == 0 ? QADIC_PM_PER_LANES : QADIC_PM_PER;
+    const int64_t per_wave = (int64_t)pm_minb(PM_PER) * num_sms_cached();
     int64_t threads = (n + per_wave * PM_PER - 1) / (per_wave * PM_PER);
     threads = (threads + 31) / 32 * 32;
     if (threads > PM_THREADS) threads = PM_THREADS;
@@ -220,8 +259,35 @@ static void launch_polymul_k4(const uint8_t* a, const uint8_t* b, int64_t n, con
     if (width_env >= 32 && width_env <= PM_THREADS) threads = width_env / 32 * 32;
     const unsigned blocks = (unsigned)((n + threads * PM_PER - 1) / (threads * PM_PER));
     const int pf = pdl_prefetch_enabled();
-    if (c.corr == 1 || c.p == 2) launch_pdl(polymul_k4_kernel<T, true>, dim3(blocks), dim3((unsigned)threads), 0, s, a, b, n, c, out, pf);
-    else launch_pdl(polymul_k4_kernel<T, false>, dim3(blocks), dim3((unsigned)threads), 0, s, a, b, n, c, out, pf);
+    if constexpr (T == 0) {  // byte-lane form
+        if (c.lfix) launch_pdl(polymul_k4_kernel<0, 3, PM_PER>, dim3(blocks), dim3((unsigned)threads), 0, s, a, b, n, c, out, pf);
+        else launch_pdl(polymul_k4_kernel<0, 2, PM_PER>, dim3(blocks), dim3((unsigned)threads), 0, s, a, b, n, c, out, pf);
+    } else if (c.corr == 1) {  // (p = 2: q is even, the correction factor is 0 -> the general form)
+        launch_pdl(polymul_k4_kernel<T, 1, PM_PER>, dim3(blocks), dim3((unsigned)threads), 0, s, a, b, n, c, out, pf);
+    } else {
+        launch_pdl(polymul_k4_kernel<T, 0, PM_PER>, dim3(blocks), dim3((unsigned)threads), 0, s, a, b, n, c, out, pf);
+    }
+}
+
+// (lm, lsh) with d - p * ((d * lm) >> lsh) in [0, p) (exact) or [0, 2p) for every digit
+// d <= dmax, and dmax * lm <= 255 so that no lane of v * lm carries into the next; checked
+// exhaustively.  Returns 0 if no pair exists, 1 for an exact quotient, 2 for one short by <= 1.
+static int lane_quotient_consts(uint32_t p, uint32_t dmax, uint32_t* lm, uint32_t* lsh) {
+    for (int want = 1; want <= 2; ++want)
+        for (uint32_t sh = 0; sh < 8; ++sh)
+            for (uint32_t m = 1; m * dmax <= 255; ++m) {
+                bool ok = true;
+                for (uint32_t d = 0; d <= dmax && ok; ++d) {
+                    const uint32_t qh = (d * m) >> sh;
+                    ok = qh * p <= d && d - qh * p < (uint32_t)want * p;
+                }
+                if (ok) {
+                    *lm = m;
+                    *lsh = sh;
+                    return want;
+                }
+            }
+    return 0;
 }
 
 // ---- generic k (1..8): one pair per thread ---------------------------------------
@@ -530,8 +596,8 @@ int make_field_const(const qadic_field_desc* d, FieldConst* f) {
 
 extern "C" {
 
-int qadic_polymul_batch_u8(const uint8_t* a, const uint8_t* b, int64_t n, int32_t k, int64_t p, int32_t t,
-                           uint8_t* out, void* stream) {
+static int polymul_batch(const uint8_t* a, const uint8_t* b, int64_t n, int32_t k, int64_t p, int32_t t,
+                         uint8_t* out, void* stream, bool redq_form) {
     QADIC_REQUIRE(n >= 0, QADIC_ERR_SHAPE, "negative batch");
     QADIC_REQUIRE(k >= 1 && k <= 8, QADIC_ERR_UNSUPPORTED, "packing width k must be 1..8");
     QADIC_REQUIRE(p >= 2 && p <= 127, QADIC_ERR_UNSUPPORTED, "GPU path supports 2 <= p <= 127");
@@ -546,11 +612,24 @@ int qadic_polymul_batch_u8(const uint8_t* a, const uint8_t* b, int64_t n, int32_
     c.corr = (q % c.p == 0) ? 0u : (uint32_t)((c.p - q % c.p) % c.p);
     c.magic = small_magic(c.p);
     c.negp = 0u - c.p;
+    c.lm = c.lsh = c.lmask = c.lfix = 0;
     c.invp_up = host_reciprocal_up(p);
     c.bound = host_case2_bound();
     cudaStream_t s = (cudaStream_t)stream;
     const bool aligned = ((uintptr_t)a % 16 == 0) && ((uintptr_t)b % 16 == 0) && ((uintptr_t)out % 16 == 0);
-    if (k == 4 && aligned && t <= 7) {  // words < 2^28, products < 2^49 (exact, below the fdiv bound)
+    // QADIC_PM_LANES=0: the paper's q = 2^t FP64-reciprocal REDQ form everywhere (measurement switch)
+    static const bool lanes_env = !(getenv("QADIC_PM_LANES") && atoi(getenv("QADIC_PM_LANES")) == 0);
+    const uint32_t dmax = 4u * (c.p - 1) * (c.p - 1);
+    int lanes = 0;
+    if (k == 4 && aligned && lanes_env && !redq_form && dmax <= 255) lanes = lane_quotient_consts(c.p, dmax, &c.lm, &c.lsh);
+    if (lanes) {
+        c.lmask = (0xFFu >> c.lsh) * 0x01010101u;
+        c.lfix = lanes == 2;
+        const int pi = prof_begin(s, "polymul_k4");
+        count_launch(1);
+        launch_polymul_k4<0>(a, b, n, c, out, s);
+        prof_end(pi, s);
+    } else if (k == 4 && aligned && t <= 7) {  // words < 2^28, products < 2^49 (exact, below the fdiv bound)
         const int pi = prof_begin(s, "polymul_k4");
         count_launch(1);
         switch (t) {
@@ -568,6 +647,16 @@ int qadic_polymul_batch_u8(const uint8_t* a, const uint8_t* b, int64_t n, int32_
                     polymul_generic_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(a, b, n, k, c, out));
     }
     return check_launch("polymul_batch_u8");
+}
+
+int qadic_polymul_batch_u8(const uint8_t* a, const uint8_t* b, int64_t n, int32_t k, int64_t p, int32_t t,
+                           uint8_t* out, void* stream) {
+    return polymul_batch(a, b, n, k, p, t, out, stream, false);
+}
+
+int qadic_polymul_batch_redq_u8(const uint8_t* a, const uint8_t* b, int64_t n, int32_t k, int64_t p, int32_t t,
+                                uint8_t* out, void* stream) {
+    return polymul_batch(a, b, n, k, p, t, out, stream, true);
 }
 
 static int gf_dot_batch(const qadic_field_desc* fd, const uint8_t* v1, const uint8_t* v2, int64_t batch, int64_t len,

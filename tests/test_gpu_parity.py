@@ -162,6 +162,60 @@ class TestPolymul:
         c = polymul.polymul_fqt_batch(golden["cfg1_a"], golden["cfg1_b"], prm)
         assert np.array_equal(c, golden["cfg1_c"])
 
+    @pytest.mark.parametrize("engine", ["auto", "redq"])
+    @pytest.mark.parametrize("p", [2, 3, 5])
+    def test_k4_every_operand_pair(self, p, engine):
+        """Every pair of degree-3 operands over F_p (p^8 pairs), through the byte-lane
+        form (auto: q = 2^8, lane-wise reciprocal) and the paper's REDQ form (redq:
+        q = 2^t, FP64 reciprocal + correction), against the oracle."""
+        prm = dqt_params(p, n=1, k=4)
+        idx = np.arange(p ** 8, dtype=np.int64)
+        digits = np.stack([(idx // p ** i) % p for i in range(8)], axis=1).astype(np.uint8)
+        a, b = np.ascontiguousarray(digits[:, :4]), np.ascontiguousarray(digits[:, 4:])
+        c = polymul.polymul_fqt_batch(a, b, prm, engine=engine)
+        assert np.array_equal(c, O.polymul_batch(a, b, p, prm.t))
+
+    @pytest.mark.parametrize("engine", ["auto", "redq"])
+    @pytest.mark.parametrize("n", [1, 5, 255, 256, 257, 7169, 100003])
+    def test_k4_engines_ragged(self, n, engine):
+        g = W.rng(n + 17)
+        a = g.integers(0, 3, (n, 4), dtype=np.uint8)
+        b = g.integers(0, 3, (n, 4), dtype=np.uint8)
+        c = polymul.polymul_fqt_batch(a, b, dqt_params(3, n=1, k=4), engine=engine)
+        assert np.array_equal(c, O.polymul_batch(a, b, 3, 5))
+
+    @pytest.mark.parametrize("p,t", [(2, 3), (2, 4), (2, 7), (3, 5), (3, 6), (3, 7), (5, 7)])
+    def test_k4_redq_form_any_radix(self, p, t):
+        """The paper's form at every admissible radix 2^t (the correction factor -q mod p
+        takes the values 0, 1 and 2 here), on all-maximal rows and random ones."""
+        from paper_0809_0063_b200.params import PackingParams
+
+        prm = PackingParams(p=p, q=1 << t, d=3, beta=53, n_max=1)
+        g = W.rng(31 * p + t)
+        a = g.integers(0, p, (20000, 4), dtype=np.uint8)
+        b = g.integers(0, p, (20000, 4), dtype=np.uint8)
+        a[:64] = p - 1
+        b[:64] = p - 1
+        ref = O.polymul_batch(a, b, p, t)
+        for engine in ("redq", "auto"):
+            assert np.array_equal(polymul.polymul_fqt_batch(a, b, prm, engine=engine), ref), engine
+
+    def test_k4_unaligned_views(self):
+        """Operands at a 4-byte offset (not 16-byte aligned) take the generic kernel."""
+        import torch
+
+        g = W.rng(99)
+        a = g.integers(0, 3, (1001, 4), dtype=np.uint8)
+        b = g.integers(0, 3, (1001, 4), dtype=np.uint8)
+        da, db = torch.from_numpy(a).cuda()[1:], torch.from_numpy(b).cuda()[1:]
+        c = polymul.polymul_fqt_batch(da, db, dqt_params(3, n=1, k=4))
+        assert np.array_equal(c.cpu().numpy(), O.polymul_batch(a[1:], b[1:], 3, 5))
+
+    def test_unknown_engine(self):
+        z = np.zeros((4, 4), np.uint8)
+        with pytest.raises(ValueError):
+            polymul.polymul_fqt_batch(z, z, dqt_params(3, n=1, k=4), engine="nope")
+
     @pytest.mark.parametrize("n", [1, 3, 1023, 1024, 1025, 5000])
     def test_cfg1_ragged(self, n):
         g = W.rng(n)
