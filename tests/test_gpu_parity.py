@@ -822,3 +822,79 @@ def test_random_sweep_right_cmm(case):
         assert eng in ("fp4k",) and p > 7, (p, m, kd, n, eng)
         return
     assert np.array_equal(got, O.modmatmul_planes(a, b, p)), (p, m, kd, n, eng)
+
+
+_PRIMES_127 = [2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37, 41, 43, 47, 53, 59, 61, 67, 71, 73, 79, 83, 89, 97,
+               101, 103, 107, 109, 113, 127]
+
+
+@pytest.mark.parametrize("case", range(80))
+def test_random_sweep_polymul_batch(case):
+    """Seeded draws over the whole domain of the fused batched product: a prime <= 127, an
+    operand length k <= 8, EVERY admissible radix from the smallest q > k (p-1)^2 up to the
+    word budget (2k-1) t <= 53, a ragged batch, both forms, host or device operands; every
+    fourth case all-maximal rows."""
+    import torch
+
+    from paper_0809_0063_b200.params import PackingParams
+
+    g = np.random.default_rng(31000 + case)
+    while True:
+        p = _PRIMES_127[int(g.integers(len(_PRIMES_127)))]
+        k = 4 if case % 3 == 0 else int(g.integers(1, 9))
+        tmin = (k * (p - 1) ** 2).bit_length()
+        tmax = 53 // (2 * k - 1)
+        if tmin <= tmax:
+            break
+    t = int(g.integers(tmin, tmax + 1))
+    n = int(g.integers(1, 40000))
+    a = g.integers(0, p, (n, k), dtype=np.uint8)
+    b = g.integers(0, p, (n, k), dtype=np.uint8)
+    if case % 4 == 1:
+        a[:] = p - 1
+        b[:] = p - 1
+    prm = PackingParams(p=p, q=1 << t, d=k - 1, beta=53, n_max=1)
+    ref = O.polymul_batch(a, b, p, t)
+    dev = bool(g.integers(2))
+    xa, xb = (torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()) if dev else (a, b)
+    for engine in ("auto", "redq"):
+        got = polymul.polymul_fqt_batch(xa, xb, prm, engine=engine)
+        got = got.cpu().numpy() if dev else got
+        assert np.array_equal(got, ref), (p, k, t, n, engine, dev)
+
+
+@pytest.mark.parametrize("case", range(60))
+def test_random_sweep_gf_dot(case):
+    """Seeded draws over fields (orders up to 4096), dot lengths up to the field's digit
+    capacity, ragged batches, both accumulation forms; every fourth case all-maximal."""
+    g = np.random.default_rng(41000 + case)
+    fields = [(2, 1), (2, 2), (2, 3), (2, 4), (3, 1), (3, 2), (3, 3), (3, 4), (5, 1), (5, 2), (5, 3), (5, 4),
+              (7, 1), (7, 2), (7, 3), (11, 1), (11, 2), (11, 3), (13, 2), (31, 1), (31, 2), (127, 1)]
+    p, k = fields[int(g.integers(len(fields)))]
+    n = int(g.integers(1, 400)) if case % 5 else int(g.integers(400, 5000))
+    n = max(1, min(n, ((1 << (53 // (2 * k - 1))) - 1) // (k * (p - 1) ** 2)))  # the longest dot the word holds
+    f = gfext.build_field(p, k, max_dot_length=n)
+    of = O.build_field(p, k, irreducible=list(f.irreducible), max_dot_length=n)
+    batch = int(g.integers(1, 3000)) if n < 400 else int(g.integers(1, 200))
+    v1 = g.integers(0, p, (batch, n, k), dtype=np.uint8)
+    v2 = g.integers(0, p, (batch, n, k), dtype=np.uint8)
+    if case % 4 == 1:
+        v1[:] = p - 1
+        v2[:] = p - 1
+    ref = O.gf_dot_batch(of, v1, v2)
+    for engine in ("auto", "f64"):
+        assert np.array_equal(f.fgdp_batch_coeffs(v1, v2, engine=engine), ref), (p, k, n, batch, engine)
+
+
+@pytest.mark.parametrize("case", range(40))
+def test_random_sweep_redq(case):
+    """Seeded draws of (p, t, digit count) with (d+1) t <= 64 over full-range and
+    bound-respecting words, against the oracle's REDQ."""
+    g = np.random.default_rng(51000 + case)
+    p = int((2, 3, 5, 7, 11, 127, 251, 257, 65521, (1 << 25) - 39, (1 << 31) - 1)[int(g.integers(11))])
+    d = int(g.integers(0, 8))
+    t = int(g.integers(1, 64 // (d + 1) + 1))
+    n = int(g.integers(1, 70000))
+    hi = 64 if case % 2 else min(64, (d + 1) * t)
+    r = g.integers(0, 1 << hi, n, dtype=np.uint64) if hi < 64 else g.integers(0, 1 << 63, n, dtype=np.uint64) * 2 + 1
+    assert np.array_equal(_kernels.redq_compress_u64(r, p, t, d), O.redq_compress_u64(r, p, t, d)), (p, t, d, n)
