@@ -264,6 +264,9 @@ __global__ void unpack_rows_kernel(const uint64_t* __restrict__ words, int64_t r
 // (aligned to the global address, so any row offset works); each thread packs
 // or unpacks PK_WPT consecutive words and writes / reads them as 16-byte vectors.
 constexpr int PK_THREADS = 256, PK_WPT = 8, PK_WORDS = PK_WPT * PK_THREADS;
+#ifndef QADIC_PK_ST256
+#define QADIC_PK_ST256 1  // 0: the byte-wise generic path only (measurement / fallback build)
+#endif
 
 template <int k>
 __global__ void __launch_bounds__(PK_THREADS) pack_rows_tile_kernel(const uint8_t* __restrict__ m, int64_t rows,
@@ -315,15 +318,25 @@ __global__ void __launch_bounds__(PK_THREADS) pack_rows_tile_kernel(const uint8_
         __syncthreads();
         const Geo g = geo(tile);
         uint64_t* rowp = words + g.r * width + g.g0;
-        if (g.nw == PK_WORDS && g.nbytes == (int64_t)PK_WORDS * k && (reinterpret_cast<uintptr_t>(rowp) & 15) == 0) {
-            // full tile: each thread packs 2 groups of 4 consecutive words from 4k
-            // staged bytes read as k+1 aligned u32 (stride 3k/4 words across lanes:
-            // conflict-free for odd k) and funnel-shifted into place -- ~5 integer
-            // ops per digit instead of a byte load with bounds tests
+        if (QADIC_PK_ST256) {
+            // Each thread packs up to 2 groups of 4 consecutive words from 4k staged bytes read
+            // as k+1 aligned u32 (stride 3k/4 words across lanes: conflict-free for odd k) and
+            // funnel-shifted into place -- ~5 integer ops per digit instead of a byte load with
+            // bounds tests -- and writes each group with ONE 32-byte store (st.global.v4.b64,
+            // sm_100: a full sector per lane, 1 KB contiguous per warp instruction; two 16-byte
+            // stores per lane wrote half sectors).  Groups start at the first 32-byte-aligned
+            // word of the row segment, so any row offset works; every whole group of a partial
+            // tile (a row's last tile: a third of cfg4's) takes this path too, and only the
+            // words before the first / after the last whole group (at most 7) are packed byte
+            // by byte.
+            const int whole_words = (int)(g.nbytes / k) < g.nw ? (int)(g.nbytes / k) : g.nw;
+            const int woff = (int)((32 - (reinterpret_cast<uintptr_t>(rowp) & 31)) & 31) >> 3;
+            const int ngroups = whole_words > woff ? (whole_words - woff) / 4 : 0;
 #pragma unroll
             for (int h = 0; h < PK_WPT / 4; ++h) {
                 const int gi = threadIdx.x + PK_THREADS * h;
-                const int b0 = g.lead + gi * 4 * k;  // first byte of the group in buf
+                if (gi >= ngroups) continue;
+                const int b0 = g.lead + (woff + gi * 4) * k;  // first byte of the group in buf
                 const uint32_t* src = reinterpret_cast<const uint32_t*>(buf[bi] + (b0 & ~3));
                 const int fs = 8 * (b0 & 3);
                 uint32_t v[k + 1], x[k];
@@ -343,8 +356,21 @@ __global__ void __launch_bounds__(PK_THREADS) pack_rows_tile_kernel(const uint8_
                     }
                     out4[i] = wd;
                 }
-                __stcs(reinterpret_cast<ulonglong2*>(rowp + 4 * gi), make_ulonglong2(out4[0], out4[1]));
-                __stcs(reinterpret_cast<ulonglong2*>(rowp + 4 * gi + 2), make_ulonglong2(out4[2], out4[3]));
+                asm volatile("st.global.cs.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(rowp + woff + 4 * gi), "l"(out4[0]),
+                             "l"(out4[1]), "l"(out4[2]), "l"(out4[3])
+                             : "memory");
+            }
+            // ragged ends: words [0, woff) and [woff + 4 ngroups, nw)
+            const int nhead = woff < g.nw ? woff : g.nw;
+            const int ntail = g.nw - (ngroups ? woff + 4 * ngroups : nhead);
+            if ((int)threadIdx.x < nhead + ntail) {
+                const int w = (int)threadIdx.x < nhead ? (int)threadIdx.x : g.nw - ntail + ((int)threadIdx.x - nhead);
+                uint64_t wd = 0;
+                for (int j = 0; j < k; ++j) {
+                    const int64_t off = (int64_t)w * k + j;
+                    if (off < g.nbytes) wd += (uint64_t)buf[bi][g.lead + off] << ((reverse ? (k - 1 - j) : j) * t);
+                }
+                rowp[w] = wd;
             }
             __syncthreads();  // this buffer is refilled two tiles later
             continue;
