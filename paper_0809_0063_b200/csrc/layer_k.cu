@@ -189,13 +189,21 @@ __global__ void __launch_bounds__(RQ_THREADS) redq_vec_kernel(const uint64_t* __
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t pairs = n / 2;
     const int64_t stride = (int64_t)gridDim.x * RQ_THREADS;
+    // the next iteration's pair of words is loaded before this one is reduced (two loads in
+    // flight per thread: the kernel's stalls were the load latency, ncu long scoreboard)
+    ulonglong2 xn = make_ulonglong2(0, 0);
+    {
+        const int64_t qf = (int64_t)blockIdx.x * RQ_THREADS + threadIdx.x;
+        if (qf < pairs) xn = __ldcs(reinterpret_cast<const ulonglong2*>(r) + qf);
+    }
     for (int64_t q0 = (int64_t)blockIdx.x * RQ_THREADS; q0 < pairs; q0 += stride) {
         const int64_t q = q0 + threadIdx.x;
         const int64_t qw = q0 + 32 * wid;  // first pair of this warp
         const bool live = q < pairs;
         uint64_t o0[D + 1], o1[D + 1], w0 = 0, w1 = 0;
+        const ulonglong2 x = xn;
+        if (q + stride < pairs) xn = __ldcs(reinterpret_cast<const ulonglong2*>(r) + q + stride);
         if (live) {
-            const ulonglong2 x = __ldcs(reinterpret_cast<const ulonglong2*>(r) + q);
             redq_word<D>(x.x, p, t, invp_up, bound, corr, mode, tab, o0, w0);
             redq_word<D>(x.y, p, t, invp_up, bound, corr, mode, tab, o1, w1);
         }
@@ -519,6 +527,8 @@ static int grid_for_tiles(F kern, int64_t tiles) {
     const int sms = num_sms_cached();
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, PK_THREADS, 0);
+    static const int blocks_env = getenv("QADIC_PK_BLOCKS") ? atoi(getenv("QADIC_PK_BLOCKS")) : 0;  // measurement switch
+    if (blocks_env > 0 && blocks_env < occ) occ = blocks_env;
     if (occ < 1) occ = 1;
     return (int)std::min<int64_t>(tiles, (int64_t)sms * occ);
 }
@@ -631,14 +641,26 @@ static int redq_launch(const uint64_t* r, int64_t n, int64_t p, int32_t t, int32
     if (aligned && d >= 1 && d <= 6 && p < (1ll << 31)) {  // digits in [0, p) fit the 32-bit arithmetic
         const int sms = num_sms_cached();
         const int64_t pairs = (n + 1) / 2;
-        const int grid = (int)std::min<int64_t>((pairs + RQ_THREADS - 1) / RQ_THREADS, (int64_t)sms * 8);
         const double inv = host_reciprocal_up(p), bnd = host_case2_bound();
         const uint64_t pp = (uint64_t)p;
+        // one wave of 4 blocks per SM (grid-stride loop).  Measured at 2^26 words, d = 2 (cfg3's
+        // accumulators), blocks per SM -> ms: 1 0.700, 2 0.443, 3 0.384, 4 0.364, 5 0.400,
+        // 6 0.439, 8 (a partial second round) 0.378: beyond 4 the extra concurrent write
+        // streams cost more DRAM efficiency than their latency hiding returns.
+        // QADIC_RQ_BLOCKS=n: n blocks per SM (measurement switch)
+        static const int blocks_env = getenv("QADIC_RQ_BLOCKS") ? atoi(getenv("QADIC_RQ_BLOCKS")) : 0;
         switch (d) {
-#define QADIC_RQ(DD)                                                                                       \
-    case DD:                                                                                               \
-        redq_vec_kernel<DD><<<grid, RQ_THREADS, 0, s>>>(r, n, pp, t, inv, bnd, corr, mode, digits, packed); \
-        break;
+#define QADIC_RQ(DD)                                                                                           \
+    case DD: {                                                                                                 \
+        int occ = 0;                                                                                           \
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, redq_vec_kernel<DD>, RQ_THREADS, 0);               \
+        if (occ > 4) occ = 4;                                                                                  \
+        if (blocks_env > 0) occ = blocks_env;                                                                  \
+        if (occ < 1) occ = 1;                                                                                  \
+        const int grid = (int)std::min<int64_t>((pairs + RQ_THREADS - 1) / RQ_THREADS, (int64_t)sms * occ);    \
+        redq_vec_kernel<DD><<<grid, RQ_THREADS, 0, s>>>(r, n, pp, t, inv, bnd, corr, mode, digits, packed);     \
+        break;                                                                                                 \
+    }
             QADIC_RQ(1) QADIC_RQ(2) QADIC_RQ(3) QADIC_RQ(4) QADIC_RQ(5) QADIC_RQ(6)
 #undef QADIC_RQ
         }
