@@ -765,6 +765,9 @@ def test_fp4k_multicast_variant():
 # ---------------------------------------------------------------------------
 # Seeded random sweep: fields x shapes x engines x buffer kinds against the oracle
 # ---------------------------------------------------------------------------
+# QADIC_SWEEP_SEED=n shifts every sweep's seeds (tools/soak.sh runs the sweeps under many offsets)
+_SOAK = 100003 * int(__import__("os").environ.get("QADIC_SWEEP_SEED", "0"))
+
 _SWEEP_FIELDS = [(2, 1), (2, 2), (2, 4), (3, 1), (3, 2), (3, 3), (5, 1), (5, 2), (5, 3), (7, 1), (7, 2),
                  (7, 3), (11, 1), (11, 2), (13, 2), (31, 1), (127, 1)]
 
@@ -779,7 +782,7 @@ def test_random_sweep_matmul(case):
 
     from paper_0809_0063_b200.gfext import build_field
 
-    g = np.random.default_rng(9000 + case)
+    g = np.random.default_rng(9000 + case + _SOAK)
     p, k = _SWEEP_FIELDS[int(g.integers(len(_SWEEP_FIELDS)))]
     m, kd, n = (int(x) for x in g.integers(1, 261, 3))
     if case % 7 == 3:
@@ -809,7 +812,7 @@ def test_random_sweep_matmul(case):
 @pytest.mark.parametrize("case", range(40))
 def test_random_sweep_right_cmm(case):
     """Seeded right_cmm draws: p, ragged shapes, engines, against the oracle's modular product."""
-    g = np.random.default_rng(7000 + case)
+    g = np.random.default_rng(7000 + case + _SOAK)
     p = (2, 3, 5, 7, 11, 31)[int(g.integers(6))]
     m, kd, n = (int(x) for x in g.integers(1, 300, 3))
     eng = ("auto", "i8", "fp4k", "f64")[int(g.integers(4))]
@@ -838,7 +841,7 @@ def test_random_sweep_polymul_batch(case):
 
     from paper_0809_0063_b200.params import PackingParams
 
-    g = np.random.default_rng(31000 + case)
+    g = np.random.default_rng(31000 + case + _SOAK)
     while True:
         p = _PRIMES_127[int(g.integers(len(_PRIMES_127)))]
         k = 4 if case % 3 == 0 else int(g.integers(1, 9))
@@ -867,7 +870,7 @@ def test_random_sweep_polymul_batch(case):
 def test_random_sweep_gf_dot(case):
     """Seeded draws over fields (orders up to 4096), dot lengths up to the field's digit
     capacity, ragged batches, both accumulation forms; every fourth case all-maximal."""
-    g = np.random.default_rng(41000 + case)
+    g = np.random.default_rng(41000 + case + _SOAK)
     fields = [(2, 1), (2, 2), (2, 3), (2, 4), (3, 1), (3, 2), (3, 3), (3, 4), (5, 1), (5, 2), (5, 3), (5, 4),
               (7, 1), (7, 2), (7, 3), (11, 1), (11, 2), (11, 3), (13, 2), (31, 1), (31, 2), (127, 1)]
     p, k = fields[int(g.integers(len(fields)))]
@@ -890,7 +893,7 @@ def test_random_sweep_gf_dot(case):
 def test_random_sweep_redq(case):
     """Seeded draws of (p, t, digit count) with (d+1) t <= 64 over full-range and
     bound-respecting words, against the oracle's REDQ."""
-    g = np.random.default_rng(51000 + case)
+    g = np.random.default_rng(51000 + case + _SOAK)
     p = int((2, 3, 5, 7, 11, 127, 251, 257, 65521, (1 << 25) - 39, (1 << 31) - 1)[int(g.integers(11))])
     d = int(g.integers(0, 8))
     t = int(g.integers(1, 64 // (d + 1) + 1))
@@ -898,3 +901,58 @@ def test_random_sweep_redq(case):
     hi = 64 if case % 2 else min(64, (d + 1) * t)
     r = g.integers(0, 1 << hi, n, dtype=np.uint64) if hi < 64 else g.integers(0, 1 << 63, n, dtype=np.uint64) * 2 + 1
     assert np.array_equal(_kernels.redq_compress_u64(r, p, t, d), O.redq_compress_u64(r, p, t, d)), (p, t, d, n)
+
+
+@pytest.mark.parametrize("case", range(40))
+def test_random_sweep_pack_unpack(case):
+    """Seeded draws of the tiled row pack / unpack: ragged rows x cols (a row's last tile
+    partial, odd row offsets of the word rows), k <= 8 digits per word at any radix with
+    k t <= 64, both digit orders; pack against the oracle, unpack back to the input."""
+    import torch
+
+    g = np.random.default_rng(61000 + case + _SOAK)
+    k = int(g.integers(1, 9))
+    t = int(g.integers(1, 64 // k + 1))
+    rows = int(g.integers(1, 40))
+    cols = int(g.integers(1, 30000)) if case % 3 else int(g.integers(1, 200))
+    m = g.integers(0, 1 << min(t, 8), (rows, cols), dtype=np.uint8)
+    dm = torch.from_numpy(m).cuda()
+    reverse = bool(g.integers(2))
+    w = cmm._pack_dev(dm, k, t, reverse).cpu().numpy().view(np.uint64)
+    padded = np.zeros((rows, -(-cols // k) * k), np.uint8)
+    padded[:, :cols] = m
+    assert np.array_equal(w, O.pack_last_axis(padded.reshape(rows, -1, k), t, reverse=reverse)), (rows, cols, k, t)
+    back = cmm._unpack_dev(torch.from_numpy(w.view(np.int64)).cuda(), rows, cols, k, t, reverse)
+    assert np.array_equal(back.cpu().numpy(), m), (rows, cols, k, t, reverse)
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_random_sweep_long_products(case):
+    """Seeded draws of batched long products: a prime, unequal lengths up to a few thousand
+    coefficients, a small batch; the tensor-core convolution engine against the packed-word
+    engine, and a sampled pair against the schoolbook product (which the oracle's
+    polymul_fqt is checked against too)."""
+    from paper_0809_0063_b200.params import fqt_params as _fqt
+
+    g = np.random.default_rng(71000 + case + _SOAK)
+    p = int((2, 3, 5, 7, 31, 127)[int(g.integers(6))])
+    la, lb = (int(x) for x in g.integers(1, 6000, 2))
+    if case % 4 == 0:
+        la, lb = int(g.integers(1, 40)), int(g.integers(1, 40))
+    bsz = int(g.integers(1, 6))
+    prm = _fqt(p, 1) if p <= 31 else _fqt(p, 0)
+    a = g.integers(0, p, (bsz, la), dtype=np.uint8)
+    b = g.integers(0, p, (bsz, lb), dtype=np.uint8)
+    if case % 5 == 1:
+        a[:] = p - 1
+        b[:] = p - 1
+    tc = polymul.polymul_fqt_long_batch(a, b, prm, engine="tc")
+    words = polymul.polymul_fqt_long_batch(a, b, prm, engine="words")
+    assert np.array_equal(tc, words), (p, la, lb, bsz)
+    i = int(g.integers(bsz))
+    want = np.convolve(a[i].astype(np.int64), b[i].astype(np.int64)) % p  # schoolbook, independent of every kernel
+    got = np.asarray(tc[i], np.int64)
+    assert np.array_equal(got[:want.size], want) and not got[want.size:].any(), (p, la, lb, i)
+    ref = O.polymul_fqt(a[i].astype(np.int64), b[i].astype(np.int64), p, prm.t, prm.d)
+    n = min(ref.size, want.size)
+    assert np.array_equal(ref[:n], want[:n]) and not ref[n:].any()
