@@ -1870,7 +1870,7 @@ __device__ __forceinline__ void place_coeffs(const uint32_t* T, uint32_t* out) {
 template <int K, int S>
 __global__ void __launch_bounds__(256, 4) combine_swar_kernel(const uint8_t* __restrict__ d, int64_t M, int64_t N,
                                                            int64_t ldd, int64_t plane_stride, uint32_t p,
-                                                           LaneDiv ld, PlaneSpec ps, uint8_t* __restrict__ c) {
+                                                           LaneDiv ld, PlaneSpec ps, uint8_t* __restrict__ c, int st256) {
 
     const int64_t chunks = (N + 31) / 32;
     int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1923,9 +1923,20 @@ __global__ void __launch_bounds__(256, 4) combine_swar_kernel(const uint8_t* __r
                 make_uint4(o[4 * v], o[4 * v + 1], o[4 * v + 2], o[4 * v + 3]);
         __syncwarp();
         uint4* wdst = reinterpret_cast<uint4*>(dst - (int64_t)lane * 32 * K);  // the warp's first chunk
+        if (st256 && (reinterpret_cast<uintptr_t>(wdst) & 31) == 0) {  // 32-byte stores: 1 KB per warp instruction
 #pragma unroll
-        for (int v = 0; v < 2 * K; ++v)
-            __stcs(wdst + v * 32 + lane, *reinterpret_cast<const uint4*>(st + (v * 32 + lane) * 4));
+            for (int v = 0; v < K; ++v) {
+                const uint4 x0 = *reinterpret_cast<const uint4*>(st + (v * 32 + lane) * 8);
+                const uint4 x1 = *reinterpret_cast<const uint4*>(st + (v * 32 + lane) * 8 + 4);
+                asm volatile("st.global.cs.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(wdst + 2 * (v * 32 + lane)),
+                             "r"(x0.x), "r"(x0.y), "r"(x0.z), "r"(x0.w), "r"(x1.x), "r"(x1.y), "r"(x1.z), "r"(x1.w)
+                             : "memory");
+            }
+        } else {
+#pragma unroll
+            for (int v = 0; v < 2 * K; ++v)
+                __stcs(wdst + v * 32 + lane, *reinterpret_cast<const uint4*>(st + (v * 32 + lane) * 4));
+        }
     } else if (!live) {
         return;
     } else if (j0 + 32 <= N && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
@@ -2042,7 +2053,8 @@ static void launch_combine(const uint8_t* d, int64_t m, int64_t n, const KaraLay
         !getenv_flag("QADIC_COMBINE_SCALAR")) {
         const unsigned blocks = (unsigned)((tot + 255) / 256);
         auto go = [&](auto kern) {
-            QADIC_TIMED("fp4k combine", s, kern<<<blocks, 256, 0, s>>>(d, m, n, L.ldd, m * L.ldd, p, ld, ps, c));
+            static const int st256 = getenv("QADIC_COMBINE_ST256") ? atoi(getenv("QADIC_COMBINE_ST256")) : 0;
+            QADIC_TIMED("fp4k combine", s, kern<<<blocks, 256, 0, s>>>(d, m, n, L.ldd, m * L.ldd, p, ld, ps, c, st256));
         };
         // the plane counts plan_planes() produces: Toom 2K-1, Karatsuba K(K+1)/2
         constexpr int S_TOOM = 2 * K - 1, S_KARA = K * (K + 1) / 2 <= KMAX_S ? K * (K + 1) / 2 : 2 * K - 1;

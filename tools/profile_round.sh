@@ -13,6 +13,7 @@ B="python bench.py --no-cpu-baseline --no-variants"
 ok=1
 python bench.py > $O/bench_default.json 2>>$O/bench.err || ok=0   # the driver's default command
 for c in 1 2; do $B --config $c --warmup 5 > $O/bench_cfg$c.json 2>>$O/bench.err || ok=0; done
+for c in 1 2; do python bench.py --config $c --no-cpu-baseline --warmup 5 > $O/bench_cfg${c}_variants.json 2>>$O/bench.err || ok=0; done  # + the paper's forms
 for c in redq pack unpack mm64 polylong polylong3 polylong1024; do python bench.py --config $c > $O/bench_$c.json 2>>$O/bench.err || ok=0; done
 python bench.py --panels 4 --no-variants --no-cpu-baseline --steps 100 > $O/bench_cfg5_panels4.json 2>>$O/bench.err || ok=0
 python tools/small_copy_floor.py > $O/copy_floor.jsonl 2>>$O/bench.err || ok=0
