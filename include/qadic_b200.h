@@ -342,6 +342,11 @@ QADIC_API int qadic_fdiv_native_check(const int64_t *r, int64_t per_p, const int
  *   data 0: zero operands, 1: residue-like operands (what the engines feed), 2: random bits
  * ------------------------------------------------------------------------- */
 QADIC_API int qadic_diag_pipe_peak(int32_t kind, int32_t data, int64_t iters, double *ops, float *ms, void *stream);
+/* Host-only: the byte-lane quotient constants qadic_polymul_batch_u8 uses for prime p
+ * and digits <= dmax (s = ((v * m) >> sh) on every byte lane): returns 1 when
+ * d - p * ((d * m) >> sh) lies in [0, p) for every d <= dmax, 2 when in [0, 2p), 0 when no
+ * pair with dmax * m <= 255 exists.  No device work (CPU-testable). */
+QADIC_API int qadic_diag_lane_quotient(uint32_t p, uint32_t dmax, uint32_t *m, uint32_t *sh);
 /* Same-size copy ceiling of the single-wave batched kernels: out = a ^ b over
  * 16-byte vectors (two input streams of in_bytes, one output stream of out_bytes
  * <= 2 in_bytes), per_thread vectors of each input per thread (1, 2, 4, 8), one

@@ -132,6 +132,8 @@ _SIGNATURES = {
     "qadic_redq_tabulated": ([P, P, I64, I64, I32, I32, P, I64, I32, I32, P, P], ctypes.c_int),
     "qadic_correct_digits": ([P, I64, I32, I64, I64, P, P], ctypes.c_int),
     "qadic_fdiv_native_check": ([P, I64, P, P, I64, I64, ctypes.POINTER(ctypes.c_uint64), P], ctypes.c_int),
+    "qadic_diag_lane_quotient": ([ctypes.c_uint32, ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint32),
+                                  ctypes.POINTER(ctypes.c_uint32)], ctypes.c_int),
     "qadic_diag_copy": ([P, P, I64, P, I64, I32, I32, P], ctypes.c_int),
     "qadic_diag_pipe_peak": ([I32, I32, I64, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_float), P],
                              ctypes.c_int),

@@ -649,6 +649,14 @@ static int polymul_batch(const uint8_t* a, const uint8_t* b, int64_t n, int32_t 
     return check_launch("polymul_batch_u8");
 }
 
+int qadic_diag_lane_quotient(uint32_t p, uint32_t dmax, uint32_t* m, uint32_t* sh) {
+    uint32_t mm = 0, ss = 0;
+    const int r = (p >= 2 && dmax <= 255) ? lane_quotient_consts(p, dmax, &mm, &ss) : 0;
+    if (m) *m = mm;
+    if (sh) *sh = ss;
+    return r;
+}
+
 int qadic_polymul_batch_u8(const uint8_t* a, const uint8_t* b, int64_t n, int32_t k, int64_t p, int32_t t,
                            uint8_t* out, void* stream) {
     return polymul_batch(a, b, n, k, p, t, out, stream, false);

@@ -53,6 +53,40 @@ class TestABI:
             Q._kernels.matmul_exact_u64(np.zeros((2, 2), np.uint64), np.zeros((2, 2), np.uint64))
 
 
+class TestLaneQuotient:
+    """The byte-lane reduction constants of the cfg1 kernel (host-side search in the
+    library, no device work): simulate the kernel's lane arithmetic on a packed word."""
+
+    @pytest.mark.parametrize("p", [2, 3, 5])
+    def test_constants_reduce_every_digit(self, p):
+        import ctypes
+
+        dmax = 4 * (p - 1) ** 2  # a digit of the product of two degree-3 operands
+        m, sh = ctypes.c_uint32(), ctypes.c_uint32()
+        kind = N.lib().qadic_diag_lane_quotient(p, dmax, ctypes.byref(m), ctypes.byref(sh))
+        assert kind in (1, 2)
+        m, sh = m.value, sh.value
+        assert dmax * m <= 255  # no lane of v * m carries into its neighbour
+        mask = (0xFF >> sh) * 0x01010101
+        for d0 in range(dmax + 1):  # four lanes at once, as the kernel holds them
+            lanes = [d0, dmax - d0, (7 * d0) % (dmax + 1), dmax]
+            v = sum(x << (8 * i) for i, x in enumerate(lanes))
+            s_ = (((v * m) & 0xFFFFFFFF) >> sh) & mask
+            u = (v - p * s_) & 0xFFFFFFFF
+            got = [(u >> (8 * i)) & 0xFF for i in range(4)]
+            if kind == 2:  # quotient short by at most one: the kernel's conditional subtract
+                assert all(x < 2 * p for x in got)
+                got = [x - p if x >= p else x for x in got]
+            assert got == [x % p for x in lanes], (p, lanes)
+
+    def test_no_constants_beyond_a_byte_lane(self):
+        import ctypes
+
+        m, sh = ctypes.c_uint32(), ctypes.c_uint32()
+        assert N.lib().qadic_diag_lane_quotient(7, 255, ctypes.byref(m), ctypes.byref(sh)) == 0
+        assert N.lib().qadic_diag_lane_quotient(7, 4 * 36, ctypes.byref(m), ctypes.byref(sh)) == 0
+
+
 class TestParams:
     def test_config_params(self, golden_scalars):
         P = golden_scalars["params"]
