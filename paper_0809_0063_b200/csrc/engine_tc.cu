@@ -1618,8 +1618,11 @@ __global__ void __launch_bounds__(256) planes_b2_kernel(const uint8_t* __restric
 // of the next tile streams into shared memory (cp.async.bulk.tensor, zero fill
 // outside B) while the current tile is converted, so the strided B rows are
 // fetched by the copy engine in whole sectors instead of 4-byte lane loads.
+#ifndef QADIC_P2_MINB
+#define QADIC_P2_MINB 1
+#endif
 template <int K>
-__global__ void __launch_bounds__(256) planes_b3_kernel(const __grid_constant__ CUtensorMap tmap, int64_t Kd,
+__global__ void __launch_bounds__(256, QADIC_P2_MINB) planes_b3_kernel(const __grid_constant__ CUtensorMap tmap, int64_t Kd,
                                                         int64_t N, uint32_t p, uint32_t* __restrict__ gtab, PlaneSpec ps, uint32_t lut,
                                                         int S, uint8_t* __restrict__ out, int64_t ld,
                                                         int64_t plane_stride, int tiles_kk, int tiles_j, int jmajor) {
@@ -1659,7 +1662,7 @@ __global__ void __launch_bounds__(256) planes_b3_kernel(const __grid_constant__ 
         tma_prefetch(&tmap);
         for (int i = 0; i < NB; ++i) mbar_init(&bar[i], 1);
         fence_barrier_init();
-        for (int i = 0; i < NB - 1; ++i)
+        for (int i = 0; i < (NB > 1 ? NB - 1 : 1); ++i)
             if ((int64_t)blockIdx.x + (int64_t)i * gridDim.x < ntiles) issue(blockIdx.x + (int64_t)i * gridDim.x, i);
     }
     build_plane_table(tab, p, K, S, ps, lut, gtab);
@@ -1673,8 +1676,8 @@ __global__ void __launch_bounds__(256) planes_b3_kernel(const __grid_constant__ 
         // the other buffer was last read in the previous iteration's pass 1 (fenced by its barrier)
         // NB - 1 tiles in flight; the buffer refilled here was last read in the previous
         // iteration's pass 1 (fenced by its barriers)
-        const int64_t tn = t + (int64_t)(NB - 1) * gridDim.x;
-        if (threadIdx.x == 0 && tn < ntiles) issue(tn, (it + NB - 1) % NB);
+        const int64_t tn = t + (int64_t)(NB > 1 ? NB - 1 : 1) * gridDim.x;
+        if (NB > 1 && threadIdx.x == 0 && tn < ntiles) issue(tn, (it + NB - 1) % NB);
         mbar_wait(&bar[buf], (uint32_t)((it / NB) & 1));
         int64_t kk0, j0;
         tile_of(t, kk0, j0);
@@ -1691,6 +1694,8 @@ __global__ void __launch_bounds__(256) planes_b3_kernel(const __grid_constant__ 
                 make_uint2(__byte_perm(cd[0], cd[1], 0x5410), __byte_perm(cd[2], cd[3], 0x5410));
         }
         __syncthreads();
+        // one input buffer: pass 1 has consumed it, the next tile streams in during pass 2
+        if (NB == 1 && threadIdx.x == 0 && tn < ntiles) issue(tn, 0);
         planes_b_pass2<K>(codes, tab, lo, hi, j0, kk0, N, ld, plane_stride, S, out);
         __syncthreads();  // code tile rewritten next iteration
     }
