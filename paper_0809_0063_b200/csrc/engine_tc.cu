@@ -1425,8 +1425,14 @@ constexpr int PT_CODES = 1024;
 // Thread: one row, 32 consecutive kk.  Per element one shared-memory table
 // lookup yields all S plane nibbles; an 8x8 nibble transpose turns 8
 // elements' lookups into the 8 plane words.
+// resident blocks per SM asked of the compiler: 6 (40 registers, 16 B of spills) measured 0.0457 vs
+// 0.0494 ms at cfg3 and 0.067 vs 0.068 at cfg5 against the unconstrained 48 registers / 5 blocks; 7-8
+// (32 registers, 148 B of spills) 0.098 ms
+#ifndef QADIC_PA_MINB
+#define QADIC_PA_MINB 6
+#endif
 template <int K>
-__global__ void __launch_bounds__(256) planes_kernel(const uint8_t* __restrict__ src, int64_t R, int64_t Kd, uint32_t p,
+__global__ void __launch_bounds__(256, (K <= 3 ? QADIC_PA_MINB : 5)) planes_kernel(const uint8_t* __restrict__ src, int64_t R, int64_t Kd, uint32_t p,
                                                      const uint32_t* __restrict__ gtab, int S,
                                                      uint8_t* __restrict__ out, int64_t ld, int64_t plane_stride) {
 
@@ -1880,8 +1886,13 @@ __device__ __forceinline__ void place_coeffs(const uint32_t* T, uint32_t* out) {
     }
 }
 
+// 5 resident blocks per SM (48 registers, no spills): 0.064 vs 0.070 ms at cfg5 for 4 blocks (63
+// registers); 6 (40 registers) 0.067, 8 (32 registers, spills) 0.084 ms
+#ifndef QADIC_COMBINE_MINB
+#define QADIC_COMBINE_MINB 5
+#endif
 template <int K, int S>
-__global__ void __launch_bounds__(256, 4) combine_swar_kernel(const uint8_t* __restrict__ d, int64_t M, int64_t N,
+__global__ void __launch_bounds__(256, (K <= 3 ? QADIC_COMBINE_MINB : 4)) combine_swar_kernel(const uint8_t* __restrict__ d, int64_t M, int64_t N,
                                                            int64_t ldd, int64_t plane_stride, uint32_t p,
                                                            LaneDiv ld, PlaneSpec ps, uint8_t* __restrict__ c, int st256) {
 
@@ -2052,9 +2063,12 @@ static void launch_planes(const uint8_t* a, const uint8_t* b, int64_t m, int64_t
     }
     if (a == nullptr) return;  // A planes already in the workspace (column-panel sweep)
     const int64_t ta = m * (L.ldk / 16);
+    // QADIC_PA_PAD=bytes: unused dynamic shared memory, caps the resident blocks per SM (measurement switch)
+    static const int pa_pad = getenv("QADIC_PA_PAD") ? atoi(getenv("QADIC_PA_PAD")) : 0;
+    if (pa_pad > 0) cudaFuncSetAttribute(planes_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, pa_pad);
     QADIC_TIMED("fp4k planes A", s,
-                planes_kernel<K><<<(unsigned)((ta + 255) / 256), 256, 0, s>>>(a, m, kdim, p, tab, L.S, as, L.ldk,
-                                                                                m * L.ldk));
+                planes_kernel<K><<<(unsigned)((ta + 255) / 256), 256, pa_pad, s>>>(a, m, kdim, p, tab, L.S, as, L.ldk,
+                                                                                     m * L.ldk));
 }
 
 template <int K>
@@ -2067,7 +2081,9 @@ static void launch_combine(const uint8_t* d, int64_t m, int64_t n, const KaraLay
         const unsigned blocks = (unsigned)((tot + 255) / 256);
         auto go = [&](auto kern) {
             static const int st256 = getenv("QADIC_COMBINE_ST256") ? atoi(getenv("QADIC_COMBINE_ST256")) : 0;
-            QADIC_TIMED("fp4k combine", s, kern<<<blocks, 256, 0, s>>>(d, m, n, L.ldd, m * L.ldd, p, ld, ps, c, st256));
+            static const int pad = getenv("QADIC_COMBINE_PAD") ? atoi(getenv("QADIC_COMBINE_PAD")) : 0;  // as QADIC_PA_PAD
+            if (pad > 0) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, pad);
+            QADIC_TIMED("fp4k combine", s, kern<<<blocks, 256, pad, s>>>(d, m, n, L.ldd, m * L.ldd, p, ld, ps, c, st256));
         };
         // the plane counts plan_planes() produces: Toom 2K-1, Karatsuba K(K+1)/2
         constexpr int S_TOOM = 2 * K - 1, S_KARA = K * (K + 1) / 2 <= KMAX_S ? K * (K + 1) / 2 : 2 * K - 1;
