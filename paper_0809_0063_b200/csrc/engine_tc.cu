@@ -123,6 +123,7 @@ struct Params {
     uint32_t p;
     uint32_t offset;     // multiple of p added before the unsigned mod (centred kinds)
     uint64_t magic64;
+    uint32_t magic32;    // nonzero: accumulator + offset < 2^32 / p, so x mod p = x - p * umulhi(x, magic32) (2 instructions)
     int m_tiles, n_tiles, num_kb;
     int n_full;          // column tiles of full width BN (n_tiles - 1 when N % BN != 0)
     int planes;          // independent plane products, stacked along the A / B rows
@@ -510,7 +511,8 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
 #pragma unroll
                         for (int c = 0; c < 16; ++c) {
                             const uint32_t x = (uint32_t)(__float2int_rn(__uint_as_float(v[c])) + (int)prm.offset);
-                            const uint32_t r = mod_u32(x, prm.p, prm.magic64);
+                            const uint32_t r = prm.magic32 ? x - prm.p * __umulhi(x, prm.magic32)
+                                                           : mod_u32(x, prm.p, prm.magic64);
 #pragma unroll
                             for (int l = 0; l < FUSE_K; ++l) {
                                 const int pos = c * FUSE_K + l;
@@ -628,7 +630,8 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                     uint32_t x;
                     if (KIND == KIND_I8) x = v[e];
                     else x = (uint32_t)(__float2int_rn(__uint_as_float(v[e])) + (int)prm.offset);
-                    r[e] = mod_u32(x, prm.p, prm.magic64);
+                    r[e] = (KIND != KIND_I8 && prm.magic32) ? x - prm.p * __umulhi(x, prm.magic32)
+                                                            : mod_u32(x, prm.p, prm.magic64);
                 }
                 if (prm.nibble_out) {  // residues < 16: two per byte, 8 bytes per 16 columns
                     uint32_t w0 = 0, w1 = 0;
@@ -2160,6 +2163,10 @@ static int run_kara(const FieldConst& f, const uint8_t* a, const uint8_t* b, int
     prm.p = f.p;
     prm.offset = f.p * ((1u << 25) / f.p + 1);
     prm.magic64 = wide_magic(f.p);
+    // FP4 sums are exact integers |v| < 2^24 (the engine's guard), so x = v + offset < 2^26 and the
+    // 32-bit reciprocal is exact while x * p < 2^32 (every plane-engine prime): the epilogue's mod p
+    // drops from a 64-bit multiply-high to IMAD.HI + IMAD.  QADIC_EPI_MOD64=1: the 64-bit form
+    prm.magic32 = ((uint64_t)f.p << 26 < (1ull << 32) && !getenv_flag("QADIC_EPI_MOD64")) ? small_magic(f.p) : 0;
     prm.m_tiles = (int)((m + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM));
     prm.n_tiles = (int)((n + BN - 1) / BN);
     prm.n_full = (int)(n / BN);
