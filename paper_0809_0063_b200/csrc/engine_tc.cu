@@ -123,6 +123,7 @@ struct Params {
     uint32_t p;
     uint32_t offset;     // multiple of p added before the unsigned mod (centred kinds)
     uint64_t magic64;
+    int epi_mod64;       // QADIC_EPI_MOD64=1: the unfused epilogue keeps the 64-bit form (measurement switch)
     uint32_t magic32;    // nonzero: accumulator + offset < 2^32 / p, so x mod p = x - p * umulhi(x, magic32) (2 instructions)
     int m_tiles, n_tiles, num_kb;
     int n_full;          // column tiles of full width BN (n_tiles - 1 when N % BN != 0)
@@ -511,8 +512,8 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
 #pragma unroll
                         for (int c = 0; c < 16; ++c) {
                             const uint32_t x = (uint32_t)(__float2int_rn(__uint_as_float(v[c])) + (int)prm.offset);
-                            const uint32_t r = prm.magic32 ? x - prm.p * __umulhi(x, prm.magic32)
-                                                           : mod_u32(x, prm.p, prm.magic64);
+                            // (run_kara always sets magic32 for the fused kernel's fields: p <= 7)
+                            const uint32_t r = __umulhi(x, prm.magic32) * (0u - prm.p) + x;
 #pragma unroll
                             for (int l = 0; l < FUSE_K; ++l) {
                                 const int pos = c * FUSE_K + l;
@@ -625,20 +626,37 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                     continue;
                 }
                 uint32_t r[16];
+                if (KIND != KIND_I8 && prm.magic32 && !prm.epi_mod64) {  // (a real branch: both forms predicated per element cost issue slots)
+                    const uint32_t m32 = prm.magic32, np = 0u - prm.p;  // x - p q as one IMAD with -p
+                    const int off = (int)prm.offset;
+                    if (off == 0) {  // non-negative representatives: F2I, IMAD.HI, IMAD per element
 #pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                    uint32_t x;
-                    if (KIND == KIND_I8) x = v[e];
-                    else x = (uint32_t)(__float2int_rn(__uint_as_float(v[e])) + (int)prm.offset);
-                    r[e] = (KIND != KIND_I8 && prm.magic32) ? x - prm.p * __umulhi(x, prm.magic32)
-                                                            : mod_u32(x, prm.p, prm.magic64);
+                        for (int e = 0; e < 16; ++e) {
+                            const uint32_t x = (uint32_t)__float2int_rn(__uint_as_float(v[e]));
+                            r[e] = __umulhi(x, m32) * np + x;
+                        }
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) {
+                            const uint32_t x = (uint32_t)(__float2int_rn(__uint_as_float(v[e])) + off);
+                            r[e] = __umulhi(x, m32) * np + x;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        uint32_t x;
+                        if (KIND == KIND_I8) x = v[e];
+                        else x = (uint32_t)(__float2int_rn(__uint_as_float(v[e])) + (int)prm.offset);
+                        r[e] = mod_u32(x, prm.p, prm.magic64);
+                    }
                 }
                 if (prm.nibble_out) {  // residues < 16: two per byte, 8 bytes per 16 columns
-                    uint32_t w0 = 0, w1 = 0;
+                    uint32_t w0 = r[7], w1 = r[15];  // Horner: one multiply-add per nibble
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        w0 |= r[e] << (4 * e);
-                        w1 |= r[8 + e] << (4 * e);
+                    for (int e = 6; e >= 0; --e) {
+                        w0 = w0 * 16u + r[e];
+                        w1 = w1 * 16u + r[8 + e];
                     }
                     uint8_t* dst = crow + col0 / 2;
                     if (col0 + 16 <= prm.N && ((reinterpret_cast<uintptr_t>(dst) & 7) == 0)) {
@@ -2162,11 +2180,17 @@ static int run_kara(const FieldConst& f, const uint8_t* a, const uint8_t* b, int
     prm.N = n;
     prm.p = f.p;
     prm.offset = f.p * ((1u << 25) / f.p + 1);
+    {  // non-negative representatives (no sign bit in any code): the sums are >= 0, no offset to add
+        bool nonneg = true;
+        for (uint32_t r = 0; r < f.p; ++r) nonneg = nonneg && !((lut >> (4 * r)) & 8u);
+        if (nonneg) prm.offset = 0;
+    }
     prm.magic64 = wide_magic(f.p);
     // FP4 sums are exact integers |v| < 2^24 (the engine's guard), so x = v + offset < 2^26 and the
     // 32-bit reciprocal is exact while x * p < 2^32 (every plane-engine prime): the epilogue's mod p
     // drops from a 64-bit multiply-high to IMAD.HI + IMAD.  QADIC_EPI_MOD64=1: the 64-bit form
-    prm.magic32 = ((uint64_t)f.p << 26 < (1ull << 32) && !getenv_flag("QADIC_EPI_MOD64")) ? small_magic(f.p) : 0;
+    prm.magic32 = small_magic(f.p);  // (p <= 7 here: x * p < 2^29)
+    prm.epi_mod64 = getenv_flag("QADIC_EPI_MOD64");
     prm.m_tiles = (int)((m + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM));
     prm.n_tiles = (int)((n + BN - 1) / BN);
     prm.n_full = (int)(n / BN);
