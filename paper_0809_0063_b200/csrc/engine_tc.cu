@@ -594,6 +594,48 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
             }
             uint8_t* crow = prm.c + pl * prm.c_plane + row * prm.ldc;
             const int nch = tile_n<BN>(prm, nt) / 16;  // accumulator columns the MMA wrote
+            // Whole tile in range, nibble planes, 32-bit reciprocal: the plane GEMM's common case without
+            // the per-chunk range / alignment tests (the epilogue runs under the MMA, but every
+            // instruction it issues is power the capped tensor clock does not get)
+            if (KIND != KIND_I8 && prm.nibble_out && prm.magic32 && !prm.epi_mod64 && !prm.diag_shift &&
+                __all_sync(0xffffffffu, row_ok) && (int64_t)nt * BN + nch * 16 <= prm.N &&
+                ((reinterpret_cast<uintptr_t>(crow + ((int64_t)nt * BN) / 2)) & 7) == 0) {
+                uint2* dst = reinterpret_cast<uint2*>(crow + ((int64_t)nt * BN) / 2);
+                const uint32_t m32 = prm.magic32, np = 0u - prm.p, off = prm.offset;
+                const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
+                const bool stream = prm.stream_out != 0;
+                auto chunks = [&](auto has_off) {  // per element: F2I (+ offset), IMAD.HI, IMAD, IMAD (Horner pack)
+#pragma unroll 1
+                    for (int ch = 0; ch < nch; ++ch) {
+                        uint32_t v[16];
+                        tmem_ld_32x32b_x16(tbase + ch * 16, v);
+                        tmem_ld_wait();
+                        uint32_t w[2];
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            uint32_t acc_w = 0;
+#pragma unroll
+                            for (int e = 7; e >= 0; --e) {
+                                uint32_t x = (uint32_t)__float2int_rn(__uint_as_float(v[8 * h + e]));
+                                if (decltype(has_off)::value) x += off;
+                                acc_w = acc_w * 16u + (__umulhi(x, m32) * np + x);
+                            }
+                            w[h] = acc_w;
+                        }
+                        if (stream) __stcs(dst + ch, make_uint2(w[0], w[1]));
+                        else dst[ch] = make_uint2(w[0], w[1]);
+                    }
+                };
+                if (off) chunks(std::true_type{});
+                else chunks(std::false_type{});
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (PAIR) mbar_arrive_cluster(acc ? empty_addr1 : empty_addr0);
+                    else mbar_arrive(&tmem_empty[acc]);
+                }
+                continue;
+            }
 #pragma unroll 1
             for (int ch = 0; ch < nch; ++ch) {
                 uint32_t v[16];
