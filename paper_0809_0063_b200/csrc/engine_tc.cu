@@ -597,7 +597,7 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
             // Whole tile in range, nibble planes, 32-bit reciprocal: the plane GEMM's common case without
             // the per-chunk range / alignment tests (the epilogue runs under the MMA, but every
             // instruction it issues is power the capped tensor clock does not get)
-            if (KIND != KIND_I8 && prm.nibble_out && prm.magic32 && !prm.epi_mod64 && !prm.diag_shift &&
+            if (prm.nibble_out && prm.magic32 && !prm.epi_mod64 && !prm.diag_shift &&
                 __all_sync(0xffffffffu, row_ok) && (int64_t)nt * BN + nch * 16 <= prm.N &&
                 ((reinterpret_cast<uintptr_t>(crow + ((int64_t)nt * BN) / 2)) & 7) == 0) {
                 uint2* dst = reinterpret_cast<uint2*>(crow + ((int64_t)nt * BN) / 2);
@@ -616,7 +616,8 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                             uint32_t acc_w = 0;
 #pragma unroll
                             for (int e = 7; e >= 0; --e) {
-                                uint32_t x = (uint32_t)__float2int_rn(__uint_as_float(v[8 * h + e]));
+                                uint32_t x = KIND == KIND_I8 ? v[8 * h + e]
+                                                             : (uint32_t)__float2int_rn(__uint_as_float(v[8 * h + e]));
                                 if (decltype(has_off)::value) x += off;
                                 acc_w = acc_w * 16u + (__umulhi(x, m32) * np + x);
                             }
@@ -2671,6 +2672,9 @@ static int run_kara8(const FieldConst& f, const uint8_t* a, const uint8_t* b, in
     prm.p = f.p;
     prm.offset = 0;
     prm.magic64 = wide_magic(f.p);
+    // plane sums <= kdim (p-1)^2: the epilogue's 32-bit reciprocal is exact while sum * p < 2^32
+    if ((__int128)kdim * (f.p - 1) * (f.p - 1) * f.p < ((__int128)1 << 32)) prm.magic32 = small_magic(f.p);
+    prm.epi_mod64 = getenv_flag("QADIC_EPI_MOD64");
     prm.m_tiles = (int)((m + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM));
     prm.n_tiles = (int)((n + BN - 1) / BN);
     prm.n_full = (int)(n / BN);
