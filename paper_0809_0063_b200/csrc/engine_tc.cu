@@ -135,8 +135,6 @@ struct Params {
     uint32_t lane_m, lane_sh, lane_qmask;  // FUSE_K: per-16-bit-lane division by p (LaneDiv)
     int group_m;                           // FUSE_K: m tiles per raster group
     int diag_noload;     // diagnostics only (QADIC_DIAG_NOLOAD): stages after the first pass skip the TMA
-    int l2_hint_a, l2_hint_b;  // QADIC_L2_HINT=ab: L2 eviction policy of the pair GEMM's A / B loads (l2_policy kinds)
-    int stream_out;      // QADIC_STREAM_OUT=1: nibble-plane stores marked streaming (st.global.cs)
     // exact uint64 GEMM through byte planes (KIND_I8): C64 = (acc64 ? C64 : 0) + (u32 D << shift)
     uint64_t* c64;
     int shift, acc64;
@@ -327,9 +325,6 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            const uint64_t pol_a = l2_policy(prm.l2_hint_a), pol_b = l2_policy(prm.l2_hint_b);
-            (void)pol_a;
-            (void)pol_b;
             for (int u = group_id; u < units; u += num_groups)
             for (int sp = 0; sp < per_unit; ++sp) {
                 const int tile = u * per_unit + sp;
@@ -388,10 +383,8 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                     } else if (PAIR) {
                         const uint32_t lbar = map_to_rank(&full_bar[stage], 0);
                         if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * G::STAGE_BYTES);
-                        if (prm.l2_hint_a) tma_load_2d_pair_hint(sa, &tmap_a, lbar, ak, arow, pol_a);
-                        else tma_load_2d_pair(sa, &tmap_a, lbar, ak, arow);
-                        if (prm.l2_hint_b) tma_load_2d_pair_hint(sb, &tmap_b, lbar, bk, brow + boff, pol_b);
-                        else tma_load_2d_pair(sb, &tmap_b, lbar, bk, brow + boff);
+                        tma_load_2d_pair(sa, &tmap_a, lbar, ak, arow);
+                        tma_load_2d_pair(sb, &tmap_b, lbar, bk, brow + boff);
                     } else {
                         mbar_arrive_expect_tx(&full_bar[stage], G::STAGE_BYTES);
                         tma_load_2d(sa, &tmap_a, &full_bar[stage], ak, arow);
@@ -603,7 +596,6 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                 uint2* dst = reinterpret_cast<uint2*>(crow + ((int64_t)nt * BN) / 2);
                 const uint32_t m32 = prm.magic32, np = 0u - prm.p, off = prm.offset;
                 const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * BN;
-                const bool stream = prm.stream_out != 0;
                 auto chunks = [&](auto has_off) {  // per element: F2I (+ offset), IMAD.HI, IMAD, IMAD (Horner pack)
 #pragma unroll 1
                     for (int ch = 0; ch < nch; ++ch) {
@@ -623,8 +615,7 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                             }
                             w[h] = acc_w;
                         }
-                        if (stream) __stcs(dst + ch, make_uint2(w[0], w[1]));
-                        else dst[ch] = make_uint2(w[0], w[1]);
+                        dst[ch] = make_uint2(w[0], w[1]);
                     }
                 };
                 if (off) chunks(std::true_type{});
@@ -703,8 +694,7 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                     }
                     uint8_t* dst = crow + col0 / 2;
                     if (col0 + 16 <= prm.N && ((reinterpret_cast<uintptr_t>(dst) & 7) == 0)) {
-                        if (prm.stream_out) __stcs(reinterpret_cast<uint2*>(dst), make_uint2(w0, w1));
-                        else *reinterpret_cast<uint2*>(dst) = make_uint2(w0, w1);
+                        *reinterpret_cast<uint2*>(dst) = make_uint2(w0, w1);
                     } else {
                         for (int e = 0; e < 16 && col0 + e < prm.N; e += 2) {
                             const uint32_t hi = (col0 + e + 1 < prm.N) ? r[e + 1] : 0;
@@ -2213,12 +2203,6 @@ static int run_kara(const FieldConst& f, const uint8_t* a, const uint8_t* b, int
     prm.group_m = getenv("QADIC_GROUP_M") ? atoi(getenv("QADIC_GROUP_M")) : GROUP_M;
     if (prm.group_m < 1) prm.group_m = 1;
     prm.diag_noload = getenv_flag("QADIC_DIAG_NOLOAD");
-    {
-        static const int hint = getenv("QADIC_L2_HINT") ? atoi(getenv("QADIC_L2_HINT")) : 0;  // two digits: A, B
-        prm.l2_hint_a = (hint / 10) % 10;
-        prm.l2_hint_b = hint % 10;
-        prm.stream_out = getenv_flag("QADIC_STREAM_OUT");
-    }
     prm.M = m;
     prm.N = n;
     prm.p = f.p;

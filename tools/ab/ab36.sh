@@ -1,4 +1,4 @@
-# fp4k GEMM: L2 eviction hints on the operand TMA loads (QADIC_L2_HINT=ab: 1 evict_first, 2 evict_last,
+# (historical: the switches were removed again, see DESIGN 9) fp4k GEMM: L2 eviction hints on the operand TMA loads (QADIC_L2_HINT=ab: 1 evict_first, 2 evict_last,
 # 3 evict_normal) and streaming plane stores (QADIC_STREAM_OUT=1): step time and the GEMM's DRAM bytes
 run() { # env...
   env "$@" python bench.py --config 5 --steps 50 --no-cpu-baseline --no-variants --no-sustained --no-redq-line 2>gpurun_out/ab36.err | python -c "
