@@ -495,26 +495,33 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                         for (int q = 0; q < W4; ++q) facc[i][q] = 0;
                 }
                 const int nch = tile_n<BN>(prm, nt) / 16;
+                // (run_kara always sets magic32 for the fused kernel's fields: p <= 7; the offset add is
+                // compiled out for non-negative representatives, cfg3's case)
+                const uint32_t fm32 = prm.magic32, fnp = 0u - prm.p, foff = prm.offset;
+                auto fchunks = [&](auto has_off) {
 #pragma unroll
-                for (int i = 0; i < MYCH; ++i) {
-                    const int ch = 2 * i + h;
-                    if (ch < NCH && ch < nch) {
-                        uint32_t v[16];
-                        tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(ew4 * 32) << 16) + acc * BN + ch * 16, v);
-                        tmem_ld_wait();
+                    for (int i = 0; i < MYCH; ++i) {
+                        const int ch = 2 * i + h;
+                        if (ch < NCH && ch < nch) {
+                            uint32_t v[16];
+                            tmem_ld_32x32b_x16(tmem_base + ((uint32_t)(ew4 * 32) << 16) + acc * BN + ch * 16, v);
+                            tmem_ld_wait();
 #pragma unroll
-                        for (int c = 0; c < 16; ++c) {
-                            const uint32_t x = (uint32_t)(__float2int_rn(__uint_as_float(v[c])) + (int)prm.offset);
-                            // (run_kara always sets magic32 for the fused kernel's fields: p <= 7)
-                            const uint32_t r = __umulhi(x, prm.magic32) * (0u - prm.p) + x;
+                            for (int c = 0; c < 16; ++c) {
+                                uint32_t x = (uint32_t)__float2int_rn(__uint_as_float(v[c]));
+                                if (decltype(has_off)::value) x += foff;
+                                const uint32_t r = __umulhi(x, fm32) * fnp + x;
 #pragma unroll
-                            for (int l = 0; l < FUSE_K; ++l) {
-                                const int pos = c * FUSE_K + l;
-                                facc[i][pos >> 2] += r * mult[l][pos & 3];
+                                for (int l = 0; l < FUSE_K; ++l) {
+                                    const int pos = c * FUSE_K + l;
+                                    facc[i][pos >> 2] += r * mult[l][pos & 3];
+                                }
                             }
                         }
                     }
-                }
+                };
+                if (foff) fchunks(std::true_type{});
+                else fchunks(std::false_type{});
                 // TMEM fully read: hand the accumulator back to the MMA warp first
                 tc_fence_before();
                 __syncwarp();
