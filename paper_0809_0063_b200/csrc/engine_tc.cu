@@ -667,10 +667,13 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                     continue;
                 }
                 uint32_t r[16];
-                if (KIND != KIND_I8 && prm.magic32 && !prm.epi_mod64) {  // (a real branch: both forms predicated per element cost issue slots)
+                if (prm.magic32 && !prm.epi_mod64) {  // (a real branch: both forms predicated per element cost issue slots)
                     const uint32_t m32 = prm.magic32, np = 0u - prm.p;  // x - p q as one IMAD with -p
                     const int off = (int)prm.offset;
-                    if (off == 0) {  // non-negative representatives: F2I, IMAD.HI, IMAD per element
+                    if (KIND == KIND_I8) {  // non-negative int32 sums (the host sets magic32 only then)
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) r[e] = __umulhi(v[e], m32) * np + v[e];
+                    } else if (off == 0) {  // non-negative representatives: F2I, IMAD.HI, IMAD per element
 #pragma unroll
                         for (int e = 0; e < 16; ++e) {
                             const uint32_t x = (uint32_t)__float2int_rn(__uint_as_float(v[e]));
@@ -1227,6 +1230,12 @@ static int run(int kind, const FieldConst& f, const uint8_t* a, const uint8_t* b
     prm.p = f.p;
     prm.offset = f.p * ((1u << 25) / f.p + 1);  // > |centred sum| (< 2^24), multiple of p
     prm.magic64 = wide_magic(f.p);
+    // the light epilogue (32-bit reciprocal) where x * p < 2^32: F4 sums + offset < 2^26 (p <= 7), I8 sums
+    // of non-negative residue bytes <= K k (p-1)^2
+    if (kind == KIND_F4 ? ((uint64_t)f.p << 26) < (1ull << 32)
+                        : (__int128)kdim * k * (f.p - 1) * (f.p - 1) * f.p < ((__int128)1 << 32))
+        prm.magic32 = small_magic(f.p);
+    prm.epi_mod64 = getenv_flag("QADIC_EPI_MOD64");
     prm.m_tiles = (int)((m + (pair ? 2 * BM : BM) - 1) / (pair ? 2 * BM : BM));
     prm.n_tiles = (int)((prm.N + BN - 1) / BN);
     prm.n_full = (int)(prm.N / BN);
