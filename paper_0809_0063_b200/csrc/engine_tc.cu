@@ -249,6 +249,9 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
     using namespace sm100;
     using G = Geo<KIND, PAIR, FUSE_K, MC>;
     static_assert(!MC || (PAIR && FUSE_K == 0), "multicast needs the CTA-pair, unfused kernel");
+    // the convolution / Toeplitz long-product modes run on the int8 kind only: compiled out of the
+    // FP4 instantiations (the headline kernel), whose code then holds only what it executes
+    constexpr bool CONVK = KIND == KIND_I8 && FUSE_K == 0;
     // MC: work units cover two m tiles (one per pair of the cluster)
     Params prm = prm_in;
     if (KIND == KIND_I8 && prm.seg_dev != nullptr) {
@@ -338,7 +341,7 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                 const int brow = (int)(pstack * prm.N) + nt * BN + (int)rank * (tile_n<BN>(prm, nt) / 2);
                 int nkb = prm.plane_inner ? prm.seg_cnt[pl] * prm.seg_kpb : prm.num_kb;
                 int cmy = 0, cwlo = 0;
-                if (prm.conv) conv_unit(prm, mt, cmy, cwlo, nkb);
+                if (CONVK && prm.conv) conv_unit(prm, mt, cmy, cwlo, nkb);
                 const int seg_lo = prm.plane_inner ? prm.seg_lo[pl] : prm.seg_i_lo;
                 const int seg_s = prm.plane_inner ? pl : prm.seg_s;
                 // MC: CTA (pair i, rank r) loads slice i of half r and multicasts it to both pairs
@@ -354,20 +357,20 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                         bk = kin * BK;
                         boff = (seg_s - i) * (int)prm.N;
                     }
-                    if (PAIR && !MC && prm.conv) {  // convolution mode on a CTA pair: rows y0 = rank * 128
+                    if (CONVK && PAIR && !MC && prm.conv) {  // convolution mode on a CTA pair: rows y0 = rank * 128
                         const uint32_t lbar = map_to_rank(&full_bar[stage], 0);
                         if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * (G::A_BYTES + prm.conv_brows * BK));
                         const int wk = kb / prm.conv_kpw, kin = (kb - wk * prm.conv_kpw) * BK, w = cwlo + wk;
                         const int r0 = (prm.conv_x0 - cmy * G::TILE_M - (int)rank * BM - w * prm.conv_tl - 127) / 16;
                         tma_load_4d_pair(sa, &tmap_a, lbar, kin, r0, 0, pl);  // 16 phases x 8 rows
                         tma_load_3d_pair(sb, &tmap_b, lbar, kin, nt * prm.conv_tn + (int)rank * prm.conv_brows - w, pl);
-                    } else if (!PAIR && !MC && prm.conv) {  // convolution mode: Toeplitz block w, b blocks shifted by w
+                    } else if (CONVK && !PAIR && !MC && prm.conv) {  // convolution mode: Toeplitz block w, b blocks shifted by w
                         mbar_arrive_expect_tx(&full_bar[stage], G::A_BYTES + prm.conv_brows * BK);
                         const int wk = kb / prm.conv_kpw, kin = (kb - wk * prm.conv_kpw) * BK, w = cwlo + wk;
                         const int r0 = (prm.conv_x0 - cmy * G::TILE_M - w * prm.conv_tl - 127) / 16;
                         tma_load_4d(sa, &tmap_a, &full_bar[stage], kin, r0, 0, pl);  // 16 phases x 8 rows
                         tma_load_3d(sb, &tmap_b, &full_bar[stage], kin, nt * prm.conv_tn - w, pl);
-                    } else if (!PAIR && !MC && prm.a_phase) {  // Toeplitz operand: 16 phase boxes + B
+                    } else if (CONVK && !PAIR && !MC && prm.a_phase) {  // Toeplitz operand: 16 phase boxes + B
                         mbar_arrive_expect_tx(&full_bar[stage], G::STAGE_BYTES);
                         const int r0 = (mt * G::TILE_M) / 16;
                         tma_load_4d(sa, &tmap_a, &full_bar[stage], ak, r0, 0, pl);  // 16 phases x 8 rows
@@ -405,11 +408,11 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
             decode_tile<FUSE_K>(u * per_unit + sp, prm, pl, mt, nt);
             nt += prm.n_tile0;
             int nkb = prm.plane_inner ? prm.seg_cnt[pl] * prm.seg_kpb : prm.num_kb;
-            if (prm.conv) {
+            if (CONVK && prm.conv) {
                 int cmy, cwlo;
                 conv_unit(prm, mt, cmy, cwlo, nkb);
             }
-            const uint32_t nn = prm.conv ? (uint32_t)prm.conv_tn : (uint32_t)tile_n<BN>(prm, nt);
+            const uint32_t nn = (CONVK && prm.conv) ? (uint32_t)prm.conv_tn : (uint32_t)tile_n<BN>(prm, nt);
             const uint32_t idesc = KIND == KIND_I8 ? idesc_u8_s32(G::TILE_M, nn) : idesc_mxf4(G::TILE_M, nn);
             const int acc = local & 1;
             const uint32_t acc_phase = (local >> 1) & 1;
@@ -470,7 +473,7 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
             tc_fence_after();
             int64_t row = (int64_t)mt * G::TILE_M + (int)rank * BM + (FUSE_K ? ew4 : ew) * 32 + lane;
             bool row_ok = row < prm.M;
-            if (!PAIR && prm.a_phase) {  // smem / TMEM row l = 8 phi + r holds GEMM row 16 r + phi
+            if (CONVK && !PAIR && prm.a_phase) {  // smem / TMEM row l = 8 phi + r holds GEMM row 16 r + phi
                 const int l = ew * 32 + lane;
                 const int64_t x = (int64_t)mt * G::TILE_M + 16 * (l % 8) + l / 8;
                 row_ok = x < prm.M;
@@ -554,7 +557,7 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                 }
                 continue;
             }
-            if (prm.conv) {
+            if (CONVK && prm.conv) {
                 // TMEM lane l = smem row 8 phi + r = tile row i = 127 - 16 r - phi: coefficient
                 // y = y0 + i + v TL of pair pl, column c = block v (y0 = the CTA's 128 rows)
                 const int l = ew * 32 + lane;
@@ -711,7 +714,7 @@ __global__ void __launch_bounds__(FUSE_K ? THREADS_FUSED : THREADS, 1)
                             dst[e / 2] = (uint8_t)(r[e] | (hi << 4));
                         }
                     }
-                } else if (prm.diag_shift) {
+                } else if (CONVK && prm.diag_shift) {
                     // diagonal-shifted transpose (Toeplitz products): column v of row x lands at
                     // c[v][x + v * diag_shift] -- a warp's 32 rows write 32 consecutive bytes per column
                     uint8_t* cpl = prm.c + pl * prm.c_plane;
